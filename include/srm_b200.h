@@ -1,0 +1,203 @@
+/*
+ * srm_b200.h -- C ABI of the B200-native SRM EM engine (libsrm_b200.so).
+ *
+ * This is the drop-in boundary for the reference's SRM fit path
+ * (/root/reference/pkg/src/factorfit/srm.py).  The reference has no FFI of
+ * its own (it is numpy/scipy); each entry point below names the reference
+ * function or call site whose work it replaces.  Signatures use plain
+ * pointers and sizes only: device pointers, host arrays of dimensions, and an
+ * opaque cudaStream_t passed as void*.  No torch types cross this boundary.
+ *
+ * Error convention (mirrors factorfit/errors.py):
+ *   every function returns an srm_status code; SRM_OK == 0.  Device-side
+ *   failures (non-finite input, rank deficiency, Cholesky breakdown) are
+ *   recorded asynchronously in a device status word -- {code, arg, iteration,
+ *   0} -- and surface through srm_read_status().  `arg` is the failing
+ *   Cholesky pivot (0-based, DefinitenessError.pivot) or the global subject
+ *   index (RankError / InvalidInputError).  srm_last_error() returns a
+ *   thread-local message for the last host-side failure.
+ *
+ * Threading: one plan per GPU process; plans are not shared between threads
+ * (reference SPEC.md:177-178: communicators and workers are not shareable).
+ */
+#ifndef SRM_B200_H_
+#define SRM_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRM_B200_ABI_VERSION 1
+
+/* storage dtype of the demeaned data X-hat (all arithmetic is fp64) */
+enum srm_dtype { SRM_F64 = 0, SRM_F32 = 1 };
+
+/* status codes <-> factorfit.errors exception classes */
+enum srm_status {
+  SRM_OK = 0,
+  SRM_ERR_CONFIG = 1,        /* ConfigError            */
+  SRM_ERR_SHAPE = 2,         /* ShapeError             */
+  SRM_ERR_INVALID_INPUT = 3, /* InvalidInputError      */
+  SRM_ERR_DEFINITENESS = 4,  /* DefinitenessError(pivot) */
+  SRM_ERR_RANK = 5,          /* RankError              */
+  SRM_ERR_CUDA = 6,          /* CUDA runtime failure   */
+  SRM_ERR_UNSUPPORTED = 7    /* outside this build's limits (e.g. k > 112) */
+};
+
+/* plan flags */
+enum srm_flags {
+  SRM_FLAG_ORDERED = 1,   /* E-step terms summed in ascending global subject order
+                             from a gathered per-subject table (srm.py:193-213);
+                             otherwise per-rank sums are all-reduced */
+  SRM_FLAG_TOLERANCE = 2, /* compute |S - S_prev| / |S_prev| every iteration (srm.py:275-287) */
+  SRM_FLAG_GRAM = 4       /* per-iteration contractions through the T x T data Gram
+                             (one-time X^T X); exact algebra, fewer flops when
+                             4*K*iterations > T */
+};
+
+/* workspace regions (srm_plan_region) */
+enum srm_region {
+  SRM_R_XHAT = 0,     /* [rows_total x ldx] X-hat, dtype                              */
+  SRM_R_AMAT = 1,     /* [rows_total x kp] f64: A_i = X_i S^T / 2 (init: N(0,1) draw)  */
+  SRM_R_WOUT = 2,     /* [rows_total x k] f64: final W_i (srm.py:315-327 model.W)     */
+  SRM_R_MU = 3,       /* [rows_total] f64: voxel means (model.mu)                      */
+  SRM_R_TERMS = 4,    /* [n_slots x term_stride] f64: per-subject E-step records       */
+  SRM_R_RED = 5,      /* [red_stride] f64: reduced K x ldx sum + scalars               */
+  SRM_R_REDLOCAL = 6, /* [red_stride] f64: this rank's partial (unordered mode)        */
+  SRM_R_S = 7,        /* [kp x ldx] f64: shared response S (model.S)                   */
+  SRM_R_SIGMA = 8,    /* [kp x kp] f64: Sigma_s (model.sigma_s)                        */
+  SRM_R_HIST = 9,     /* [iterations x hist_stride] f64: per-iteration scalars         */
+  SRM_R_STATUS = 10,  /* int32[4] device status word                                   */
+  SRM_R_MMAT = 11,    /* [n_local x kp x kp] f64: polar transforms M_i                 */
+  SRM_R_SCAL = 12,    /* [n_local x 8] f64: per-subject scalars                        */
+  SRM_R_GRAM = 13,    /* [n_local x ldx x ldx] f64/f32: X_i^T X_i (SRM_FLAG_GRAM only) */
+  SRM_R_VAR = 14,     /* [kp x kp] f64: posterior covariance var_s                     */
+  SRM_R_COUNT = 15
+};
+
+/* plan dimensions (srm_plan_dim) */
+enum srm_dim {
+  SRM_D_LDX = 0,          /* padded T (row stride of X-hat, S, terms)   */
+  SRM_D_KP = 1,           /* padded K                                   */
+  SRM_D_ROWS = 2,         /* sum of local voxel counts                  */
+  SRM_D_TERM_STRIDE = 3,  /* doubles per subject record in SRM_R_TERMS  */
+  SRM_D_RED_STRIDE = 4,   /* doubles in SRM_R_RED                       */
+  SRM_D_HIST_STRIDE = 5,  /* doubles per iteration in SRM_R_HIST        */
+  SRM_D_N_SLOTS = 6,      /* subject records in SRM_R_TERMS             */
+  SRM_D_SLOT_OFFSET = 7,  /* first record slot owned by this rank       */
+  SRM_D_ITEMS_E = 8,      /* work items of the V-contraction kernel     */
+  SRM_D_ITEMS_A = 9,      /* work items of the T-contraction kernel     */
+  SRM_D_CHUNK_ROWS = 10   /* rows per V chunk                           */
+};
+
+/* per-iteration history columns (SRM_R_HIST, hist_stride doubles per row) */
+enum srm_hist {
+  SRM_H_LL = 0,       /* log-likelihood of the parameters entering the iteration */
+  SRM_H_TRACE = 1,    /* tr(Sigma_s_new)                                         */
+  SRM_H_RHO0 = 2,     /* sum_i 1/rho_i^2 used by the E-step                      */
+  SRM_H_SDIFF = 3,    /* |S - S_prev|_F                                          */
+  SRM_H_SPREV = 4,    /* |S_prev|_F                                              */
+  SRM_H_RHO2 = 8      /* first of n_local post-M-step rho_i^2                    */
+};
+
+typedef struct srm_plan srm_plan;
+
+/* ---- version / errors ---------------------------------------------------- */
+int srm_abi_version(void);
+const char* srm_last_error(void);
+
+/* ---- plan ------------------------------------------------------------------
+ * srm_plan_create replaces the bookkeeping of factorfit.srm.fit
+ * (srm.py:216-246: validation, rank_offsets, per-subject state).
+ *   n_local subjects with voxel counts n_voxels[n_local] (host array), T TRs,
+ *   k factors; world_size ranks with counts_per_rank[world_size] subjects
+ *   each (contiguous shards, cli.py:82-85); this rank is `rank`.
+ */
+int srm_plan_create(srm_plan** out, int dtype, int n_local, const int64_t* n_voxels,
+                    int64_t n_trs, int64_t k, int iterations, int world_size, int rank,
+                    const int32_t* counts_per_rank, int flags);
+int srm_plan_destroy(srm_plan* plan);
+int64_t srm_plan_workspace_bytes(const srm_plan* plan);
+int64_t srm_plan_dim(const srm_plan* plan, int which);
+/* bind a device workspace of srm_plan_workspace_bytes() bytes (256-B aligned) */
+int srm_plan_bind(srm_plan* plan, void* workspace, int64_t bytes);
+int srm_plan_region(const srm_plan* plan, int region, int64_t* offset, int64_t* bytes);
+
+/* ---- one-time work ----------------------------------------------------------
+ * srm_load_subject: srm.py:94-98 `demean` + kernels.py:45 finite check +
+ *   the loop-invariant kernels.py:152-155 `trace_ata` (hoisted out of the EM
+ *   loop, srm.py:152).  x is a device array [V_i x ld] of x_dtype; it is not
+ *   modified (srm.py:98 returns a copy).
+ * srm_init_mapping: srm.py:101-113 `init_subject` after the host RNG draw
+ *   (the N(0,1) matrix, PCG64-seeded as the reference, is written to
+ *   SRM_R_AMAT first): polar factor via Gram + Jacobi eigensolver, and the
+ *   first E-step term W_i^T X_i (srm.py:116-118) with rho_i^2 = 1.
+ */
+int srm_load_subject(srm_plan* plan, int local_index, const void* x, int x_dtype,
+                     int64_t ld, void* stream);
+int srm_finish_load(srm_plan* plan, void* stream);
+int srm_init_mapping(srm_plan* plan, void* stream);
+
+/* ---- per-iteration work (srm.py:254-287) -----------------------------------
+ * The iteration index lives in a device counter (set to 0 by
+ * srm_init_mapping, advanced by srm_m_step) so one captured CUDA graph of
+ * {e_step, m_step} serves every iteration.  History rows wrap modulo
+ * `iterations`.
+ * srm_set_iteration: overwrite the device counter (asynchronous).
+ * srm_reduce_local: unordered mode only -- this rank's sum of its E-step
+ *   terms into SRM_R_REDLOCAL, to be all-reduced into SRM_R_RED.
+ * srm_e_step: srm.py:193-213 ordered accumulation (ordered mode), then
+ *   srm.py:121-129 `e_step_global` and srm.py:132-142 `update_sigma_s`:
+ *   K x K Cholesky inverses, S, Sigma_s, tr(Sigma_s), the Woodbury
+ *   log-likelihood and the tolerance statistic.
+ * srm_m_step: srm.py:145-155 `m_step_subject` for every local subject:
+ *   A_i = X_i S^T / 2, the polar factor W_i = A_i (A_i^T A_i)^{-1/2}, the
+ *   cross term and rho_i^2, and the next E-step term W_i^T X_i / rho_i^2
+ *   (srm.py:151 and :118 share one product).
+ * srm_finalize: materialise W_i = A_i M_i (model.W).
+ */
+int srm_set_iteration(srm_plan* plan, int iteration, void* stream);
+int srm_reduce_local(srm_plan* plan, void* stream);
+int srm_e_step(srm_plan* plan, void* stream);
+int srm_m_step(srm_plan* plan, void* stream);
+int srm_finalize(srm_plan* plan, void* stream);
+
+/* synchronous copy of the device status word {code, arg, iteration, 0} */
+int srm_read_status(srm_plan* plan, int32_t* out4);
+/* clear the device status word (asynchronous) */
+int srm_clear_status(srm_plan* plan, void* stream);
+
+/* ---- stateless kernels (step-function API, srm.py:116-155, kernels.py) ---- */
+/* out[k x t] = alpha * W^T X over all V rows; W [V x ldw] f64, X [V x ldx]
+ * dtype; replaces srm.py:118 (e_step_local) and srm.py:151 (W_new^T Xhat). */
+int srm_gemm_tn(const double* w, int64_t ldw, const void* x, int x_dtype, int64_t ldx,
+                int64_t v, int64_t k, int64_t t, double alpha, double* out, int64_t ldo,
+                void* workspace, int64_t ws_bytes, void* stream);
+/* out[v x k] = alpha * X S^T; replaces srm.py:147 (A = Xhat S^T / 2). */
+int srm_gemm_nt(const void* x, int x_dtype, int64_t ldx, const double* s, int64_t lds,
+                int64_t v, int64_t t, int64_t k, double alpha, double* out, int64_t ldo,
+                void* workspace, int64_t ws_bytes, void* stream);
+/* in-place SPD inverse of a [n x n] f64 matrix (kernels.py:168-187).  Status
+ * (DefinitenessError pivot) goes to status4 (device int32[4]). */
+int srm_spd_inverse(double* a, int64_t n, int32_t* status4, void* stream);
+/* srm.py:121-142 e_step_global + update_sigma_s for one reduced K x T sum:
+ * S (k x t), var_s (k x k), Sigma_new (k x k) and tr(Sigma_new) (one double),
+ * all device pointers; DefinitenessError pivots go to status4.  Synchronous. */
+int srm_tail_step(const double* reduced, int64_t ldr, const double* sigma, int64_t ldsig,
+                  int64_t k, int64_t t, double rho0, double* s_out, int64_t lds_out,
+                  double* var_out, double* sigma_out, double* trace_out, int32_t* status4,
+                  void* workspace, int64_t ws_bytes, void* stream);
+/* orthogonal polar factor W = A (A^T A)^{-1/2} of a [v x k] f64 matrix
+ * (kernels.py:190-212); rank failures go to status4. */
+int srm_polar(const double* a, int64_t lda, int64_t v, int64_t k, double* w, int64_t ldw,
+              int32_t* status4, void* workspace, int64_t ws_bytes, void* stream);
+/* workspace bytes needed by srm_gemm_tn / srm_gemm_nt / srm_polar / srm_tail_step */
+int64_t srm_stateless_workspace_bytes(int64_t v, int64_t k, int64_t t);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SRM_B200_H_ */

@@ -1,0 +1,505 @@
+// C ABI of libsrm_b200.so (declared in include/srm_b200.h).
+//
+// A plan is the device-side state of one worker's share of an SRM fit
+// (srm.py:216-327): the concatenated X-hat of its subjects, the per-subject
+// E-step term table, the K x K state and the static work decomposition of the
+// streaming kernels.  The caller (the Python host layer) allocates one device
+// workspace; the plan carves it into regions, uploads its work tables once in
+// srm_plan_bind, and every phase function below only enqueues kernels on the
+// given stream -- no host synchronisation, so a whole iteration can be
+// captured into a CUDA graph.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/srm_b200.h"
+#include "kernels.h"
+#include "plan.h"
+
+using namespace srm;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SRM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+enum Internal {
+  I_ROWSQ = SRM_R_COUNT,
+  I_CMAT,
+  I_TAILSCR,
+  I_SSPART,
+  I_TAILPART,
+  I_PART,
+  I_BRED,
+  I_QMAT,
+  I_QSCR,
+  I_CROSSP,
+  I_SUBJ,
+  I_ORDER,
+  I_ORDER_LOCAL,
+  I_ITEMS_EX,
+  I_ITEMS_EA,
+  I_ITEMS_A,
+  I_COUNT
+};
+
+}  // namespace
+
+struct srm_plan {
+  int dtype = SRM_F64;
+  int n_local = 0;
+  std::vector<int64_t> V;
+  int64_t T = 0, K = 0, ldx = 0, kp = 0, ldo = 0;
+  int iterations = 0;
+  int world = 1, rank = 0;
+  std::vector<int32_t> counts;
+  int flags = 0;
+  int n_total = 0, max_local = 0, global0 = 0;
+  int n_slots = 0, slot0 = 0;
+  int64_t rows_total = 0;
+  std::vector<int64_t> row_off;
+  int64_t chunk_rows = 0;
+  std::vector<int64_t> chunk0, nchunk;
+  int64_t chunks_total = 0;
+  std::vector<ItemE> items_ex, items_ea;
+  std::vector<ItemA> items_a;
+  std::vector<int64_t> subj;
+  std::vector<int32_t> order, order_local;
+  int64_t off[I_COUNT] = {0};
+  int64_t size[I_COUNT] = {0};
+  int64_t total_bytes = 0;
+  char* ws = nullptr;
+  DevPlan dp{};
+};
+
+namespace {
+
+int64_t esize(int dtype) { return dtype == SRM_F64 ? 8 : 4; }
+
+void layout(srm_plan* p) {
+  const int64_t kp2 = p->kp * p->kp;
+  const int ntile_tail = (int)((p->ldx + 31) / 32);
+  const int ntile_apply = (int)((p->ldx + 63) / 64);
+  const int64_t term_stride = p->kp * p->ldx + kRecScalars;
+  const int64_t red_stride = p->kp * p->ldx + kRedScalars;
+  const int64_t hist_stride = SRM_H_RHO2 + std::max(p->n_local, 1);
+  int64_t sz[I_COUNT] = {0};
+  sz[SRM_R_XHAT] = p->rows_total * p->ldx * esize(p->dtype);
+  sz[SRM_R_AMAT] = p->rows_total * p->kp * 8;
+  sz[SRM_R_WOUT] = p->rows_total * p->K * 8;
+  sz[SRM_R_MU] = p->rows_total * 8;
+  sz[SRM_R_TERMS] = (int64_t)p->n_slots * term_stride * 8;
+  sz[SRM_R_RED] = red_stride * 8;
+  sz[SRM_R_REDLOCAL] = red_stride * 8;
+  sz[SRM_R_S] = p->kp * p->ldx * 8;
+  sz[SRM_R_SIGMA] = kp2 * 8;
+  sz[SRM_R_HIST] = (int64_t)std::max(p->iterations, 1) * hist_stride * 8;
+  sz[SRM_R_STATUS] = 32;  // status word + iteration counter
+  sz[SRM_R_MMAT] = (int64_t)p->n_local * kp2 * 8;
+  sz[SRM_R_SCAL] = (int64_t)p->n_local * 8 * 8;
+  sz[SRM_R_GRAM] = 0;
+  sz[SRM_R_VAR] = kp2 * 8;
+  sz[I_ROWSQ] = p->rows_total * 8;
+  sz[I_CMAT] = kp2 * 8;
+  sz[I_TAILSCR] = kTailScalars * 8;
+  sz[I_SSPART] = (int64_t)ntile_tail * kp2 * 8;
+  sz[I_TAILPART] = (int64_t)ntile_tail * 4 * 8;
+  sz[I_PART] = p->chunks_total * p->kp * p->ldo * 8;
+  sz[I_BRED] = (int64_t)p->n_local * p->kp * p->ldo * 8;
+  sz[I_QMAT] = (int64_t)p->n_local * kp2 * 8;
+  sz[I_QSCR] = (int64_t)p->n_local * kp2 * 8;
+  sz[I_CROSSP] = (int64_t)p->n_local * ntile_apply * 8;
+  sz[I_SUBJ] = (int64_t)p->subj.size() * 8;
+  sz[I_ORDER] = (int64_t)p->order.size() * 4;
+  sz[I_ORDER_LOCAL] = (int64_t)p->order_local.size() * 4;
+  sz[I_ITEMS_EX] = (int64_t)p->items_ex.size() * sizeof(ItemE);
+  sz[I_ITEMS_EA] = (int64_t)p->items_ea.size() * sizeof(ItemE);
+  sz[I_ITEMS_A] = (int64_t)p->items_a.size() * sizeof(ItemA);
+  int64_t cur = 0;
+  for (int r = 0; r < I_COUNT; ++r) {
+    p->off[r] = cur;
+    p->size[r] = sz[r];
+    cur += round_up(sz[r], 256);
+  }
+  p->total_bytes = std::max<int64_t>(cur, 256);
+  DevPlan& d = p->dp;
+  d.n_local = p->n_local;
+  d.n_total = p->n_total;
+  d.n_order = (int)p->order.size();
+  d.flags = p->flags;
+  d.T = p->T;
+  d.K = p->K;
+  d.ldx = p->ldx;
+  d.kp = p->kp;
+  d.ldo = p->ldo;
+  d.ntile_apply = ntile_apply;
+  d.ntile_tail = ntile_tail;
+  d.term_stride = term_stride;
+  d.red_stride = red_stride;
+  d.hist_stride = hist_stride;
+}
+
+template <typename T>
+T* region(srm_plan* p, int r) {
+  return reinterpret_cast<T*>(p->ws + p->off[r]);
+}
+
+void build_work(srm_plan* p) {
+  // V-chunking of the split-V contraction: about 8 waves of 2 CTAs per SM
+  const int64_t ntiles = (p->ldx + 127) / 128;
+  const int64_t target_items = 148 * 2 * 8;
+  int64_t cr = round_up(std::max<int64_t>(1, p->rows_total * ntiles / target_items), 16);
+  cr = std::max<int64_t>(cr, 256);
+  p->chunk_rows = cr;
+  p->chunk0.assign(p->n_local, 0);
+  p->nchunk.assign(p->n_local, 0);
+  int64_t c = 0;
+  for (int i = 0; i < p->n_local; ++i) {
+    p->chunk0[i] = c;
+    p->nchunk[i] = std::max<int64_t>(1, (p->V[i] + cr - 1) / cr);
+    c += p->nchunk[i];
+  }
+  p->chunks_total = c;
+  p->items_ex.clear();
+  p->items_ea.clear();
+  p->items_a.clear();
+  for (int i = 0; i < p->n_local; ++i) {
+    for (int64_t ch = 0; ch < p->nchunk[i]; ++ch) {
+      const int64_t r0 = p->row_off[i] + ch * cr;
+      const int64_t rows = std::max<int64_t>(0, std::min<int64_t>(cr, p->V[i] - ch * cr));
+      const int64_t obase = (p->chunk0[i] + ch) * p->kp * p->ldo;
+      for (int64_t n0 = 0; n0 < p->ldx; n0 += 128) {
+        ItemE it;
+        it.l_off = r0 * p->kp;
+        it.r_off = r0 * p->ldx + n0;
+        it.o_off = obase + n0;
+        it.rows = (int32_t)rows;
+        it.ncols = (int32_t)std::min<int64_t>(128, p->ldx - n0);
+        p->items_ex.push_back(it);
+      }
+      ItemE ia;
+      ia.l_off = r0 * p->kp;
+      ia.r_off = r0 * p->kp;
+      ia.o_off = obase + p->ldx;
+      ia.rows = (int32_t)rows;
+      ia.ncols = (int32_t)p->kp;
+      p->items_ea.push_back(ia);
+    }
+    for (int64_t r = 0; r < p->V[i]; r += 128) {
+      ItemA it;
+      it.x_off = (p->row_off[i] + r) * p->ldx;
+      it.o_off = (p->row_off[i] + r) * p->kp;
+      it.rows = (int32_t)std::min<int64_t>(128, p->V[i] - r);
+      it.pad = i;
+      p->items_a.push_back(it);
+    }
+  }
+  // subject table
+  p->subj.assign((size_t)p->n_local * kSubjCols, 0);
+  for (int i = 0; i < p->n_local; ++i) {
+    int64_t* s = &p->subj[(size_t)i * kSubjCols];
+    s[SC_ROW_OFF] = p->row_off[i];
+    s[SC_V] = p->V[i];
+    s[SC_CHUNK0] = p->chunk0[i];
+    s[SC_NCHUNK] = p->nchunk[i];
+    s[SC_GLOBAL] = p->global0 + i;
+    s[SC_SLOT] = p->slot0 + i;
+  }
+  // record order: ascending global subject index
+  p->order.clear();
+  p->order_local.clear();
+  for (int i = 0; i < p->n_local; ++i) p->order_local.push_back(p->slot0 + i);
+  if (p->flags & SRM_FLAG_ORDERED) {
+    for (int r = 0; r < p->world; ++r)
+      for (int j = 0; j < p->counts[r]; ++j) p->order.push_back(r * p->max_local + j);
+  } else {
+    p->order = p->order_local;
+  }
+}
+
+void set_pointers(srm_plan* p) {
+  DevPlan& d = p->dp;
+  d.xhat = p->ws + p->off[SRM_R_XHAT];
+  d.amat = region<double>(p, SRM_R_AMAT);
+  d.wout = region<double>(p, SRM_R_WOUT);
+  d.mu = region<double>(p, SRM_R_MU);
+  d.rowsq = region<double>(p, I_ROWSQ);
+  d.terms = region<double>(p, SRM_R_TERMS);
+  d.red = region<double>(p, SRM_R_RED);
+  d.redlocal = region<double>(p, SRM_R_REDLOCAL);
+  d.S = region<double>(p, SRM_R_S);
+  d.sigma = region<double>(p, SRM_R_SIGMA);
+  d.var = region<double>(p, SRM_R_VAR);
+  d.cmat = region<double>(p, I_CMAT);
+  d.tailscr = region<double>(p, I_TAILSCR);
+  d.sspart = region<double>(p, I_SSPART);
+  d.tailpart = region<double>(p, I_TAILPART);
+  d.part = region<double>(p, I_PART);
+  d.bred = region<double>(p, I_BRED);
+  d.mmat = region<double>(p, SRM_R_MMAT);
+  d.qmat = region<double>(p, I_QMAT);
+  d.qscr = region<double>(p, I_QSCR);
+  d.crossp = region<double>(p, I_CROSSP);
+  d.hist = region<double>(p, SRM_R_HIST);
+  d.status = region<int32_t>(p, SRM_R_STATUS);
+  d.iter = d.status + 4;
+  d.n_hist = std::max(p->iterations, 1);
+  d.subj = region<int64_t>(p, I_SUBJ);
+  d.order = region<int32_t>(p, I_ORDER);
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int check(cudaError_t e, const char* where) { return e == cudaSuccess ? SRM_OK : cuda_fail(e, where); }
+
+int run_contractions(srm_plan* p, cudaStream_t st) {
+  const DevPlan& d = p->dp;
+  cudaError_t e = launch_contract_e((int)p->kp, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo,
+                                    1.0, region<ItemE>(p, I_ITEMS_EX), (int)p->items_ex.size(), st);
+  if (e != cudaSuccess) return cuda_fail(e, "contract_e(xhat)");
+  e = launch_contract_e((int)p->kp, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0,
+                        region<ItemE>(p, I_ITEMS_EA), (int)p->items_ea.size(), st);
+  if (e != cudaSuccess) return cuda_fail(e, "contract_e(amat)");
+  e = launch_reduce_chunks(d, st);
+  return check(e, "reduce_chunks");
+}
+
+}  // namespace
+
+extern "C" {
+
+int srm_abi_version(void) { return SRM_B200_ABI_VERSION; }
+
+const char* srm_last_error(void) { return g_last_error.c_str(); }
+
+int srm_plan_create(srm_plan** out, int dtype, int n_local, const int64_t* n_voxels, int64_t n_trs,
+                    int64_t k, int iterations, int world_size, int rank,
+                    const int32_t* counts_per_rank, int flags) {
+  if (!out) return fail(SRM_ERR_CONFIG, "null plan pointer");
+  *out = nullptr;
+  if (dtype != SRM_F64 && dtype != SRM_F32) return fail(SRM_ERR_CONFIG, "dtype must be SRM_F64 or SRM_F32");
+  if (k < 1) return fail(SRM_ERR_CONFIG, "k must be at least 1");
+  if (iterations < 1) return fail(SRM_ERR_CONFIG, "iterations must be at least 1");
+  if (n_local < 1) return fail(SRM_ERR_CONFIG, "each worker needs at least one subject");
+  if (n_trs < 1) return fail(SRM_ERR_SHAPE, "need at least 1 TR");
+  if (k > max_supported_k())
+    return fail(SRM_ERR_UNSUPPORTED, "k > " + std::to_string(max_supported_k()) + " is not supported by this build");
+  if (world_size < 1 || rank < 0 || rank >= world_size) return fail(SRM_ERR_CONFIG, "invalid rank/size");
+  if (!counts_per_rank) return fail(SRM_ERR_CONFIG, "counts_per_rank is required");
+  if (counts_per_rank[rank] != n_local) return fail(SRM_ERR_CONFIG, "counts_per_rank[rank] != n_local");
+  srm_plan* p = new srm_plan();
+  p->dtype = dtype;
+  p->n_local = n_local;
+  p->V.assign(n_voxels, n_voxels + n_local);
+  for (int i = 0; i < n_local; ++i) {
+    if (p->V[i] < k) {
+      delete p;
+      return fail(SRM_ERR_SHAPE, "subject has " + std::to_string(n_voxels[i]) + " voxels, fewer than k=" +
+                                     std::to_string(k) + " factors");
+    }
+  }
+  p->T = n_trs;
+  p->K = k;
+  p->kp = round_up(k, 8);
+  p->ldx = round_up(n_trs, 32);
+  p->ldo = p->ldx + p->kp;
+  p->iterations = iterations;
+  p->world = world_size;
+  p->rank = rank;
+  p->counts.assign(counts_per_rank, counts_per_rank + world_size);
+  p->flags = flags;
+  if (world_size == 1) p->flags |= SRM_FLAG_ORDERED;
+  p->n_total = 0;
+  p->max_local = 0;
+  p->global0 = 0;
+  for (int r = 0; r < world_size; ++r) {
+    if (r < rank) p->global0 += p->counts[r];
+    p->n_total += p->counts[r];
+    p->max_local = std::max(p->max_local, p->counts[r]);
+  }
+  if (p->flags & SRM_FLAG_ORDERED) {
+    p->n_slots = world_size * p->max_local;
+    p->slot0 = rank * p->max_local;
+  } else {
+    p->n_slots = n_local;
+    p->slot0 = 0;
+  }
+  p->row_off.assign(n_local, 0);
+  int64_t r = 0;
+  for (int i = 0; i < n_local; ++i) {
+    p->row_off[i] = r;
+    r += p->V[i];
+  }
+  p->rows_total = r;
+  build_work(p);
+  layout(p);
+  *out = p;
+  return SRM_OK;
+}
+
+int srm_plan_destroy(srm_plan* plan) {
+  delete plan;
+  return SRM_OK;
+}
+
+int64_t srm_plan_workspace_bytes(const srm_plan* plan) { return plan ? plan->total_bytes : -1; }
+
+int64_t srm_plan_dim(const srm_plan* p, int which) {
+  if (!p) return -1;
+  switch (which) {
+    case SRM_D_LDX: return p->ldx;
+    case SRM_D_KP: return p->kp;
+    case SRM_D_ROWS: return p->rows_total;
+    case SRM_D_TERM_STRIDE: return p->dp.term_stride;
+    case SRM_D_RED_STRIDE: return p->dp.red_stride;
+    case SRM_D_HIST_STRIDE: return p->dp.hist_stride;
+    case SRM_D_N_SLOTS: return p->n_slots;
+    case SRM_D_SLOT_OFFSET: return p->slot0;
+    case SRM_D_ITEMS_E: return (int64_t)(p->items_ex.size() + p->items_ea.size());
+    case SRM_D_ITEMS_A: return (int64_t)p->items_a.size();
+    case SRM_D_CHUNK_ROWS: return p->chunk_rows;
+    default: return -1;
+  }
+}
+
+int srm_plan_region(const srm_plan* p, int region_id, int64_t* offset, int64_t* bytes) {
+  if (!p || region_id < 0 || region_id >= SRM_R_COUNT) return fail(SRM_ERR_CONFIG, "bad region");
+  if (offset) *offset = p->off[region_id];
+  if (bytes) *bytes = p->size[region_id];
+  return SRM_OK;
+}
+
+int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
+  if (!p || !workspace) return fail(SRM_ERR_CONFIG, "null plan/workspace");
+  if (bytes < p->total_bytes) return fail(SRM_ERR_CONFIG, "workspace too small");
+  if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0) return fail(SRM_ERR_CONFIG, "workspace must be 256-byte aligned");
+  p->ws = static_cast<char*>(workspace);
+  set_pointers(p);
+  cudaError_t e = cudaMemset(p->ws, 0, p->total_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "bind memset");
+  struct Up {
+    int r;
+    const void* src;
+  } ups[] = {{I_SUBJ, p->subj.data()},         {I_ORDER, p->order.data()},
+             {I_ORDER_LOCAL, p->order_local.data()}, {I_ITEMS_EX, p->items_ex.data()},
+             {I_ITEMS_EA, p->items_ea.data()},  {I_ITEMS_A, p->items_a.data()}};
+  for (const Up& u : ups) {
+    if (p->size[u.r] == 0) continue;
+    e = cudaMemcpy(p->ws + p->off[u.r], u.src, p->size[u.r], cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "bind upload");
+  }
+  // Sigma_s = I (srm.py:248); S starts at zero
+  std::vector<double> eye((size_t)p->kp * p->kp, 0.0);
+  for (int64_t j = 0; j < p->K; ++j) eye[(size_t)j * p->kp + j] = 1.0;
+  e = cudaMemcpy(region<double>(p, SRM_R_SIGMA), eye.data(), eye.size() * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "bind sigma");
+  // warm up kernel attributes outside any graph capture
+  const DevPlan& d = p->dp;
+  e = launch_contract_e((int)p->kp, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0, nullptr, 0, 0);
+  if (e == cudaSuccess)
+    e = launch_contract_e((int)p->kp, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0, nullptr, 0, 0);
+  if (e == cudaSuccess)
+    e = launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp, 0.5, nullptr, 0, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
+  return SRM_OK;
+}
+
+int srm_load_subject(srm_plan* p, int local, const void* x, int x_dtype, int64_t ld, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  if (local < 0 || local >= p->n_local) return fail(SRM_ERR_CONFIG, "subject index out of range");
+  if (x_dtype != SRM_F64 && x_dtype != SRM_F32) return fail(SRM_ERR_CONFIG, "x dtype must be f64 or f32");
+  if (ld < p->T) return fail(SRM_ERR_SHAPE, "leading dimension smaller than T");
+  return check(launch_prep(p->dp, local, p->V[local], x, x_dtype, ld, p->dtype, as_stream(stream)), "prep");
+}
+
+int srm_finish_load(srm_plan* p, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  return check(launch_subject_sqnorm(p->dp, as_stream(stream)), "sqnorm");
+}
+
+int srm_init_mapping(srm_plan* p, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  cudaStream_t st = as_stream(stream);
+  int rc = run_contractions(p, st);
+  if (rc) return rc;
+  cudaError_t e = launch_eig_polar(p->dp, 1, st);
+  if (e == cudaSuccess) e = launch_apply_m(p->dp, 0, st);
+  if (e == cudaSuccess) e = launch_finalize_rho(p->dp, 1, st);
+  if (e == cudaSuccess) e = launch_set_iteration(p->dp, 0, 0, st);
+  return check(e, "init_mapping");
+}
+
+int srm_reduce_local(srm_plan* p, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  return check(launch_reduce_terms(p->dp, p->dp.redlocal, region<int32_t>(p, I_ORDER_LOCAL), p->n_local,
+                                   as_stream(stream)),
+               "reduce_local");
+}
+
+int srm_set_iteration(srm_plan* p, int iteration, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  if (iteration < 0) return fail(SRM_ERR_CONFIG, "iteration must be >= 0");
+  return check(launch_set_iteration(p->dp, iteration, 0, as_stream(stream)), "set_iteration");
+}
+
+int srm_e_step(srm_plan* p, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaSuccess;
+  if (p->flags & SRM_FLAG_ORDERED)
+    e = launch_reduce_terms(p->dp, p->dp.red, p->dp.order, (int)p->order.size(), st);
+  if (e == cudaSuccess) e = launch_tail(p->dp, st);
+  return check(e, "e_step");
+}
+
+int srm_m_step(srm_plan* p, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  cudaStream_t st = as_stream(stream);
+  const DevPlan& d = p->dp;
+  cudaError_t e = launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
+                                    0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
+  if (e != cudaSuccess) return cuda_fail(e, "contract_a");
+  int rc = run_contractions(p, st);
+  if (rc) return rc;
+  e = launch_eig_polar(d, 0, st);
+  if (e == cudaSuccess) e = launch_apply_m(d, 1, st);
+  if (e == cudaSuccess) e = launch_finalize_rho(d, 0, st);
+  if (e == cudaSuccess) e = launch_set_iteration(d, 0, 1, st);
+  return check(e, "m_step");
+}
+
+int srm_finalize(srm_plan* p, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  return check(launch_apply_w(p->dp, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), as_stream(stream)),
+               "finalize");
+}
+
+int srm_read_status(srm_plan* p, int32_t* out4) {
+  if (!p || !p->ws || !out4) return fail(SRM_ERR_CONFIG, "plan not bound");
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "synchronize");
+  e = cudaMemcpy(out4, p->dp.status, 16, cudaMemcpyDeviceToHost);
+  out4[3] = 0;
+  return check(e, "read_status");
+}
+
+int srm_clear_status(srm_plan* p, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  return check(cudaMemsetAsync(p->dp.status, 0, 16, as_stream(stream)), "clear_status");
+}
+
+}  // extern "C"

@@ -1,0 +1,41 @@
+// Internal launcher interface between the C-ABI layer (capi.cu) and the
+// kernel translation units.  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace srm {
+
+// One CTA of the V-contraction kernel: out[m][n0+j] += sum_{c<rows} L[c][m] R[c][n0+j]
+// for m < KP, j < ncols (<= 128).  Offsets are in elements of each base.
+struct ItemE {
+  int64_t l_off;  // L(row 0, col 0) of this chunk
+  int64_t r_off;  // R(row 0, col n0)
+  int64_t o_off;  // out(0, n0)
+  int32_t rows;   // contraction rows in this chunk
+  int32_t ncols;  // valid output columns (<= 128)
+};
+
+// One CTA of the T-contraction kernel: out[r][f] = alpha sum_t X[r][t] S[f][t]
+// for r < rows (<= 128), f < KP, t < ldx.
+struct ItemA {
+  int64_t x_off;  // X(row r0, 0)
+  int64_t o_off;  // out(row r0, 0)
+  int32_t rows;   // valid rows (<= 128)
+  int32_t pad;
+};
+
+// V-contraction: dtype of R (X-hat or f64); L is always f64.
+cudaError_t launch_contract_e(int kp, int r_dtype, const double* L, int64_t ldl, const void* R,
+                              int64_t ldr, double* out, int64_t ldo, double alpha,
+                              const ItemE* items, int n_items, cudaStream_t stream);
+
+// T-contraction over `ncontract` columns (multiple of 16).
+cudaError_t launch_contract_a(int kp, int x_dtype, const void* X, int64_t ldx, const double* S,
+                              int64_t lds, int64_t ncontract, double* out, int64_t ldo,
+                              double alpha, const ItemA* items, int n_items, cudaStream_t stream);
+
+bool contract_kp_supported(int kp);
+
+}  // namespace srm

@@ -1,0 +1,89 @@
+// Device-side view of an SRM plan (passed by value to every kernel) and the
+// kernel launchers of smallmat.cu.  Internal; not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace srm {
+
+// per local subject record in DevPlan::subj (int64 x kSubjCols)
+enum SubjCol {
+  SC_ROW_OFF = 0,   // first row in the concatenated X-hat / A / W arrays
+  SC_V = 1,         // voxel count
+  SC_CHUNK0 = 2,    // first V-chunk index (partials)
+  SC_NCHUNK = 3,    // number of V-chunks
+  SC_GLOBAL = 4,    // global subject index (srm.py:237 rank_offsets)
+  SC_SLOT = 5,      // record slot in the E-step term table
+  kSubjCols = 8
+};
+
+// scalar fields at the end of each E-step term record (after kp * ldx doubles)
+enum RecCol { RC_RHO2 = 0, RC_V = 1, RC_SQNORM = 2, kRecScalars = 8 };
+
+// scalar fields after the kp * ldx reduced sum in RED / REDLOCAL
+enum RedCol { RD_RHO0 = 0, RD_VLOGRHO = 1, RD_SQRHO = 2, RD_VSUM = 3, kRedScalars = 8 };
+
+// tail scratch scalars
+enum TailCol { TS_LOGDET_SIGMA = 0, TS_LOGDET_PREC = 1, TS_TRACE = 2, kTailScalars = 8 };
+
+struct DevPlan {
+  int n_local, n_total, n_order;
+  int flags;
+  int64_t T, K, ldx, kp, ldo;
+  int ntile_apply;  // 64-column tiles of ldx
+  int ntile_tail;   // 32-column tiles of ldx
+  int64_t term_stride, red_stride, hist_stride;
+  // regions
+  void* xhat;
+  double* amat;
+  double* wout;
+  double* mu;
+  double* rowsq;
+  double* terms;
+  double* red;
+  double* redlocal;
+  double* S;
+  double* sigma;
+  double* var;
+  double* cmat;
+  double* tailscr;
+  double* sspart;    // [ntile_tail][kp][kp]
+  double* tailpart;  // [ntile_tail][4]
+  double* part;      // [chunks][kp][ldo]
+  double* bred;      // [n_local][kp][ldo]
+  double* mmat;      // [n_local][kp][kp]
+  double* qmat;      // [n_local][kp][kp]
+  double* qscr;      // [n_local][kp][kp]
+  double* crossp;    // [n_local][ntile_apply]
+  double* hist;      // [iterations][hist_stride]
+  int32_t* status;
+  int32_t* iter;          // device iteration counter (one graph serves every iteration)
+  int n_hist;             // history rows
+  const int64_t* subj;   // [n_local][kSubjCols]
+  const int32_t* order;  // [n_order] record slots, ascending global subject index
+};
+
+cudaError_t launch_prep(const DevPlan& p, int local, int64_t V, const void* x, int x_dtype,
+                        int64_t ld, int xhat_dtype, cudaStream_t s);
+cudaError_t launch_subject_sqnorm(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_reduce_chunks(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_eig_polar(const DevPlan& p, int init, cudaStream_t s);
+cudaError_t launch_apply_m(const DevPlan& p, int with_cross, cudaStream_t s);
+cudaError_t launch_finalize_rho(const DevPlan& p, int init, cudaStream_t s);
+cudaError_t launch_set_iteration(const DevPlan& p, int iteration, int advance, cudaStream_t s);
+cudaError_t launch_reduce_terms(const DevPlan& p, double* dst, const int32_t* order, int count,
+                                cudaStream_t s);
+cudaError_t launch_tail(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_apply_w(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);
+
+// stateless helpers
+cudaError_t launch_spd_inverse(double* a, int n, int32_t* status, cudaStream_t s);
+cudaError_t launch_polar_small(const double* gram, int64_t ldg, int n, double* m, int64_t ldm,
+                               int32_t* status, cudaStream_t s);
+cudaError_t launch_apply_right(const double* a, int64_t lda, int64_t v, int k, const double* m,
+                               int64_t ldm, double* w, int64_t ldw, cudaStream_t s);
+
+int max_supported_k();
+
+}  // namespace srm

@@ -1,0 +1,222 @@
+// Stateless step kernels behind the reference's per-step API
+// (srm.py:116-155 e_step_local / m_step_subject pieces, kernels.py:168-212).
+// They stage their operands into zero-padded workspace copies (so any caller
+// layout is accepted) and reuse the same DMMA contraction kernels as the fit.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/srm_b200.h"
+#include "kernels.h"
+#include "plan.h"
+
+using namespace srm;
+
+namespace {
+
+inline int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+constexpr int64_t kChunk = 2048;
+
+struct Carve {
+  char* base;
+  int64_t used = 0;
+  int64_t cap;
+  template <typename T>
+  T* take(int64_t n) {
+    T* p = reinterpret_cast<T*>(base + used);
+    used += rup(n * (int64_t)sizeof(T), 256);
+    return used <= cap ? p : nullptr;
+  }
+};
+
+__global__ void k_sum_chunks(const double* __restrict__ part, int64_t stride, int nch, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= stride) return;
+  double acc = part[e];
+  for (int c = 1; c < nch; ++c) acc += part[(int64_t)c * stride + e];
+  out[e] = acc;
+}
+
+int ret(cudaError_t e) { return e == cudaSuccess ? SRM_OK : SRM_ERR_CUDA; }
+
+// out (kp x ncols_pad) = L^T R over v rows, L [v x kp] f64, R [v x ldr] dtype
+cudaError_t split_v(const double* L, int64_t kp, const void* R, int r_dtype, int64_t ldr, int64_t ncols,
+                    int64_t v, double alpha, double* part, double* out, ItemE* items_dev, cudaStream_t st) {
+  const int nch = (int)std::max<int64_t>(1, (v + kChunk - 1) / kChunk);
+  std::vector<ItemE> items;
+  for (int c = 0; c < nch; ++c) {
+    const int64_t r0 = (int64_t)c * kChunk;
+    for (int64_t n0 = 0; n0 < ncols; n0 += 128) {
+      ItemE it;
+      it.l_off = r0 * kp;
+      it.r_off = r0 * ldr + n0;
+      it.o_off = (int64_t)c * kp * ncols + n0;
+      it.rows = (int32_t)std::max<int64_t>(0, std::min<int64_t>(kChunk, v - r0));
+      it.ncols = (int32_t)std::min<int64_t>(128, ncols - n0);
+      items.push_back(it);
+    }
+  }
+  cudaError_t e = cudaMemcpyAsync(items_dev, items.data(), items.size() * sizeof(ItemE), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  e = launch_contract_e((int)kp, r_dtype, L, kp, R, ldr, part, ncols, alpha, items_dev, (int)items.size(), st);
+  if (e != cudaSuccess) return e;
+  const int64_t n = kp * ncols;
+  k_sum_chunks<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, n, nch, out);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t srm_stateless_workspace_bytes(int64_t v, int64_t k, int64_t t) {
+  const int64_t kp = rup(k, 8), ldxp = rup(t, 32);
+  const int64_t nch = std::max<int64_t>(1, (v + kChunk - 1) / kChunk);
+  const int64_t ntile = (std::max(ldxp, kp) + 127) / 128;
+  int64_t b = 0;
+  b += rup(v * kp * 8, 256);                         // L / A copy
+  b += rup(v * ldxp * 8, 256);                       // X copy
+  b += rup(nch * kp * std::max(ldxp, kp) * 8, 256);  // partials
+  b += rup(kp * std::max(ldxp, kp) * 8, 256);        // reduced
+  b += rup(v * kp * 8, 256);                         // T-contraction output
+  b += rup(kp * kp * 8 * 2, 256);                    // M / scratch
+  b += rup(nch * ntile * (int64_t)sizeof(ItemE) + ((v + 127) / 128) * (int64_t)sizeof(ItemA), 256);
+  // tail step: red, S (kp x ldx), sigma/var/cmat, per-tile partials
+  const int64_t ntail = ldxp / 32;
+  b += rup((2 * kp * ldxp + 16) * 8, 256) + rup((3 + ntail) * kp * kp * 8, 256) + rup((ntail * 4 + 64) * 8, 256);
+  return b + 4096;
+}
+
+int srm_gemm_tn(const double* w, int64_t ldw, const void* x, int x_dtype, int64_t ldx, int64_t v, int64_t k,
+                int64_t t, double alpha, double* out, int64_t ldo, void* workspace, int64_t ws_bytes,
+                void* stream) {
+  if (v < 1 || k < 1 || t < 1 || !contract_kp_supported((int)rup(k, 8))) return SRM_ERR_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t kp = rup(k, 8), ldxp = rup(t, 32);
+  const int64_t es = x_dtype == SRM_F64 ? 8 : 4;
+  const int64_t nch = std::max<int64_t>(1, (v + kChunk - 1) / kChunk);
+  Carve c{static_cast<char*>(workspace), 0, ws_bytes};
+  double* Lp = c.take<double>(v * kp);
+  char* Xp = c.take<char>(v * ldxp * es);
+  double* part = c.take<double>(nch * kp * ldxp);
+  double* red = c.take<double>(kp * ldxp);
+  ItemE* items = c.take<ItemE>(nch * ((ldxp + 127) / 128));
+  if (!items) return SRM_ERR_CONFIG;
+  cudaError_t e = cudaMemsetAsync(Lp, 0, v * kp * 8, st);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(Lp, kp * 8, w, ldw * 8, k * 8, v, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(Xp, 0, v * ldxp * es, st);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(Xp, ldxp * es, x, ldx * es, t * es, v, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = split_v(Lp, kp, Xp, x_dtype, ldxp, ldxp, v, alpha, part, red, items, st);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(out, ldo * 8, red, ldxp * 8, t * 8, k, cudaMemcpyDeviceToDevice, st);
+  return ret(e);
+}
+
+int srm_gemm_nt(const void* x, int x_dtype, int64_t ldx, const double* s, int64_t lds, int64_t v, int64_t t,
+                int64_t k, double alpha, double* out, int64_t ldo, void* workspace, int64_t ws_bytes,
+                void* stream) {
+  if (v < 1 || k < 1 || t < 1 || !contract_kp_supported((int)rup(k, 8))) return SRM_ERR_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t kp = rup(k, 8), ldxp = rup(t, 32);
+  const int64_t es = x_dtype == SRM_F64 ? 8 : 4;
+  Carve c{static_cast<char*>(workspace), 0, ws_bytes};
+  char* Xp = c.take<char>(v * ldxp * es);
+  double* Sp = c.take<double>(kp * ldxp);
+  double* Op = c.take<double>(v * kp);
+  ItemA* items = c.take<ItemA>((v + 127) / 128);
+  if (!items) return SRM_ERR_CONFIG;
+  std::vector<ItemA> host;
+  for (int64_t r = 0; r < v; r += 128) {
+    ItemA it;
+    it.x_off = r * ldxp;
+    it.o_off = r * kp;
+    it.rows = (int32_t)std::min<int64_t>(128, v - r);
+    it.pad = 0;
+    host.push_back(it);
+  }
+  cudaError_t e = cudaMemsetAsync(Xp, 0, v * ldxp * es, st);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(Xp, ldxp * es, x, ldx * es, t * es, v, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(Sp, 0, kp * ldxp * 8, st);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(Sp, ldxp * 8, s, lds * 8, t * 8, k, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(items, host.data(), host.size() * sizeof(ItemA), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = launch_contract_a((int)kp, x_dtype, Xp, ldxp, Sp, ldxp, ldxp, Op, kp, alpha, items, (int)host.size(), st);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(out, ldo * 8, Op, kp * 8, k * 8, v, cudaMemcpyDeviceToDevice, st);
+  return ret(e);
+}
+
+int srm_tail_step(const double* reduced, int64_t ldr, const double* sigma, int64_t ldsig, int64_t k, int64_t t,
+                  double rho0, double* s_out, int64_t lds_out, double* var_out, double* sigma_out,
+                  double* trace_out, int32_t* status4, void* workspace, int64_t ws_bytes, void* stream) {
+  if (k < 1 || t < 1) return SRM_ERR_SHAPE;
+  if (k > max_supported_k()) return SRM_ERR_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t kp = rup(k, 8), ldx = rup(t, 32);
+  const int ntail = (int)(ldx / 32);
+  Carve c{static_cast<char*>(workspace), 0, ws_bytes};
+  DevPlan d{};
+  d.T = t;
+  d.K = k;
+  d.ldx = ldx;
+  d.kp = kp;
+  d.ldo = ldx + kp;
+  d.ntile_tail = ntail;
+  d.ntile_apply = (int)((ldx + 63) / 64);
+  d.red_stride = kp * ldx + kRedScalars;
+  d.hist_stride = 8;
+  d.n_hist = 1;
+  d.red = c.take<double>(d.red_stride);
+  d.S = c.take<double>(kp * ldx);
+  d.sigma = c.take<double>(kp * kp);
+  d.var = c.take<double>(kp * kp);
+  d.cmat = c.take<double>(kp * kp);
+  d.sspart = c.take<double>(ntail * kp * kp);
+  d.tailpart = c.take<double>(ntail * 4);
+  d.tailscr = c.take<double>(kTailScalars);
+  d.hist = c.take<double>(8);
+  d.iter = c.take<int32_t>(4);
+  d.status = status4;
+  if (!d.iter) return SRM_ERR_CONFIG;
+  cudaError_t e = cudaMemsetAsync(workspace, 0, c.used, st);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(d.red, ldx * 8, reduced, ldr * 8, t * 8, k, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d.red + kp * ldx + RD_RHO0, &rho0, 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(d.sigma, kp * 8, sigma, ldsig * 8, k * 8, k, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = launch_tail(d, st);
+  if (e == cudaSuccess && s_out) e = cudaMemcpy2DAsync(s_out, lds_out * 8, d.S, ldx * 8, t * 8, k, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && var_out) e = cudaMemcpy2DAsync(var_out, k * 8, d.var, kp * 8, k * 8, k, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && sigma_out) e = cudaMemcpy2DAsync(sigma_out, k * 8, d.sigma, kp * 8, k * 8, k, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && trace_out) e = cudaMemcpyAsync(trace_out, d.tailscr + TS_TRACE, 8, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // rho0 staged from the caller's stack
+  return ret(e);
+}
+
+int srm_spd_inverse(double* a, int64_t n, int32_t* status4, void* stream) {
+  if (n < 1 || n > max_supported_k()) return n < 1 ? SRM_ERR_SHAPE : SRM_ERR_UNSUPPORTED;
+  return ret(launch_spd_inverse(a, (int)n, status4, static_cast<cudaStream_t>(stream)));
+}
+
+int srm_polar(const double* a, int64_t lda, int64_t v, int64_t k, double* w, int64_t ldw, int32_t* status4,
+              void* workspace, int64_t ws_bytes, void* stream) {
+  if (v < k) return SRM_ERR_SHAPE;
+  if (k < 1) return SRM_ERR_SHAPE;
+  if (k > max_supported_k()) return SRM_ERR_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t kp = rup(k, 8);
+  const int64_t nch = std::max<int64_t>(1, (v + kChunk - 1) / kChunk);
+  Carve c{static_cast<char*>(workspace), 0, ws_bytes};
+  double* Ap = c.take<double>(v * kp);
+  double* part = c.take<double>(nch * kp * kp);
+  double* G = c.take<double>(kp * kp);
+  double* M = c.take<double>(kp * kp);
+  ItemE* items = c.take<ItemE>(nch);
+  if (!items) return SRM_ERR_CONFIG;
+  cudaError_t e = cudaMemsetAsync(Ap, 0, v * kp * 8, st);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(Ap, kp * 8, a, lda * 8, k * 8, v, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = split_v(Ap, kp, Ap, SRM_F64, kp, kp, v, 1.0, part, G, items, st);
+  if (e == cudaSuccess) e = launch_polar_small(G, kp, (int)k, M, kp, status4, st);
+  if (e == cudaSuccess) e = launch_apply_right(Ap, kp, v, (int)k, M, kp, w, ldw, st);
+  return ret(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,316 @@
+"""Device-resident SRM EM engine: one plan of libsrm_b200.so per GPU process.
+
+``SrmEngine`` owns the plan's single HBM workspace (a torch uint8 tensor),
+uploads and demeans the subjects, draws the reference initialisation,
+enqueues the per-iteration phases and exposes region views as torch
+tensors.  The EM loop itself is ``fit`` in :mod:`paper_1608_04647_b200.srm`;
+this class is the plumbing between it and the C ABI.
+
+Per iteration (srm.py:254-287) the device work is
+``[exchange] -> srm_e_step -> srm_m_step``; with a single rank the two phase
+calls are captured once into a CUDA graph and replayed (the iteration index
+lives in a device counter).
+"""
+
+import ctypes
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, DeviceError, from_status
+
+_MASK64 = 0xFFFFFFFFFFFFFFFF
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def reference_gaussian(n_voxels, k, seed, subject_index):
+    """The N(0,1) draw of srm.py:111 (numpy PCG64 seeded (seed, index))."""
+    gen = np.random.default_rng((int(seed) & _MASK64, int(subject_index)))
+    return gen.standard_normal((int(n_voxels), int(k)))
+
+
+class SrmEngine:
+    """Device state of one worker's subjects for an SRM fit."""
+
+    def __init__(self, n_voxels, n_trs, k, iterations, *, storage="f64", world_size=1,
+                 rank=0, counts=None, ordered=True, tolerance=False, device=None):
+        torch = _torch()
+        self.lib = _lib.load()
+        if not torch.cuda.is_available():
+            raise DeviceError("the SRM engine needs a CUDA device (B200); no CPU fallback")
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        if self.device.type != "cuda":
+            raise DeviceError("device must be a CUDA device")
+        self.n_voxels = [int(v) for v in n_voxels]
+        self.n_local = len(self.n_voxels)
+        self.T = int(n_trs)
+        self.K = int(k)
+        self.iterations = int(iterations)
+        self.world_size = int(world_size)
+        self.rank = int(rank)
+        self.counts = list(counts) if counts is not None else [self.n_local]
+        self.storage = storage
+        dt = _lib.SRM_F64 if storage == "f64" else _lib.SRM_F32
+        flags = 0
+        if ordered:
+            flags |= _lib.FLAG_ORDERED
+        if tolerance:
+            flags |= _lib.FLAG_TOLERANCE
+        self.ordered = bool(ordered) or self.world_size == 1
+        plan = ctypes.c_void_p()
+        varr = (ctypes.c_int64 * self.n_local)(*self.n_voxels)
+        carr = (ctypes.c_int32 * self.world_size)(*self.counts)
+        _lib.check(self.lib.srm_plan_create(ctypes.byref(plan), dt, self.n_local, varr, self.T,
+                                            self.K, self.iterations, self.world_size, self.rank,
+                                            carr, flags), "plan_create")
+        self.plan = plan
+        nbytes = int(self.lib.srm_plan_workspace_bytes(plan))
+        with torch.cuda.device(self.device):
+            self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        _lib.check(self.lib.srm_plan_bind(plan, ctypes.c_void_p(self.ws.data_ptr()), nbytes), "plan_bind")
+        d = lambda w: int(self.lib.srm_plan_dim(plan, w))  # noqa: E731
+        self.ldx = d(_lib.D_LDX)
+        self.kp = d(_lib.D_KP)
+        self.rows = d(_lib.D_ROWS)
+        self.term_stride = d(_lib.D_TERM_STRIDE)
+        self.red_stride = d(_lib.D_RED_STRIDE)
+        self.hist_stride = d(_lib.D_HIST_STRIDE)
+        self.n_slots = d(_lib.D_N_SLOTS)
+        self.slot0 = d(_lib.D_SLOT_OFFSET)
+        self.row_off = np.concatenate([[0], np.cumsum(self.n_voxels)[:-1]]).astype(np.int64)
+        self._graph = None
+        self._staging = {}
+
+    # ------------------------------------------------------------------ views
+    def region(self, rid, dtype=None):
+        torch = _torch()
+        off = ctypes.c_int64()
+        nb = ctypes.c_int64()
+        _lib.check(self.lib.srm_plan_region(self.plan, rid, ctypes.byref(off), ctypes.byref(nb)))
+        view = self.ws[off.value: off.value + nb.value]
+        return view.view(dtype or torch.float64)
+
+    @property
+    def xhat(self):
+        torch = _torch()
+        dt = torch.float64 if self.storage == "f64" else torch.float32
+        return self.region(_lib.R_XHAT, dt).view(self.rows, self.ldx)
+
+    @property
+    def amat(self):
+        return self.region(_lib.R_AMAT).view(self.rows, self.kp)
+
+    @property
+    def wout(self):
+        return self.region(_lib.R_WOUT).view(self.rows, self.K)
+
+    @property
+    def mu(self):
+        return self.region(_lib.R_MU)
+
+    @property
+    def terms(self):
+        return self.region(_lib.R_TERMS).view(self.n_slots, self.term_stride)
+
+    @property
+    def red(self):
+        return self.region(_lib.R_RED)
+
+    @property
+    def redlocal(self):
+        return self.region(_lib.R_REDLOCAL)
+
+    @property
+    def S(self):
+        return self.region(_lib.R_S).view(self.kp, self.ldx)[: self.K, : self.T]
+
+    @property
+    def sigma(self):
+        return self.region(_lib.R_SIGMA).view(self.kp, self.kp)[: self.K, : self.K]
+
+    @property
+    def hist(self):
+        return self.region(_lib.R_HIST).view(max(self.iterations, 1), self.hist_stride)
+
+    def stream(self):
+        return _torch().cuda.current_stream(self.device).cuda_stream
+
+    # --------------------------------------------------------------- loading
+    def _staging_buf(self, slot, dtype, numel):
+        torch = _torch()
+        key = (slot, dtype)
+        buf = self._staging.get(key)
+        if buf is None or buf.numel() < numel:
+            buf = torch.empty(numel, dtype=dtype, device=self.device)
+            self._staging[key] = buf
+        return buf[:numel]
+
+    def load(self, xs):
+        """Upload (if needed) and demean every local subject (srm.py:238-240)."""
+        torch = _torch()
+        if len(xs) != self.n_local:
+            raise ConfigError("subject count does not match the plan")
+        main = torch.cuda.current_stream(self.device)
+        copier = torch.cuda.Stream(device=self.device)
+        done = [None, None]
+        for j, x in enumerate(xs):
+            v = self.n_voxels[j]
+            if isinstance(x, torch.Tensor) and x.device == self.device and x.dim() == 2 \
+                    and x.dtype in (torch.float64, torch.float32) and x.stride(1) == 1:
+                src = x
+                ld = x.stride(0)
+            else:
+                if isinstance(x, torch.Tensor):
+                    host = x.detach()
+                    if host.dtype not in (torch.float64, torch.float32):
+                        host = host.to(torch.float64)
+                    host = host.contiguous()
+                else:
+                    arr = np.asarray(x)
+                    if arr.dtype not in (np.float64, np.float32):
+                        arr = arr.astype(np.float64)
+                    host = torch.from_numpy(np.ascontiguousarray(arr))
+                b = j % 2
+                buf = self._staging_buf(b, host.dtype, v * self.T).view(v, self.T)
+                with torch.cuda.stream(copier):
+                    if done[b] is not None:
+                        copier.wait_event(done[b])
+                    buf.copy_(host, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copier)
+                main.wait_event(ev)
+                src = buf
+                ld = self.T
+            if tuple(src.shape) != (v, self.T):
+                raise ConfigError("subject shape does not match the plan")
+            dt = _lib.SRM_F64 if src.dtype == torch.float64 else _lib.SRM_F32
+            _lib.check(self.lib.srm_load_subject(self.plan, j, ctypes.c_void_p(src.data_ptr()), dt, ld,
+                                                 ctypes.c_void_p(main.cuda_stream)), "load_subject")
+            ev2 = torch.cuda.Event()
+            ev2.record(main)
+            done[j % 2] = ev2
+        _lib.check(self.lib.srm_finish_load(self.plan, ctypes.c_void_p(main.cuda_stream)), "finish_load")
+        main.synchronize()
+        self._staging.clear()
+        self.raise_status()
+
+    def init_mapping(self, seed, global_offset, gaussians=None, threads=8):
+        """init_subject (srm.py:101-113): host PCG64 draws, device polar + first E-step."""
+        torch = _torch()
+        amat = self.amat
+        if gaussians is None:
+            def draw(j):
+                return reference_gaussian(self.n_voxels[j], self.K, seed, global_offset + j)
+
+            with ThreadPoolExecutor(max(1, min(threads, self.n_local))) as pool:
+                futures = [pool.submit(draw, j) for j in range(self.n_local)]
+                for j, fut in enumerate(futures):
+                    g = fut.result()
+                    r0 = int(self.row_off[j])
+                    amat[r0: r0 + self.n_voxels[j], : self.K].copy_(torch.from_numpy(g))
+                    futures[j] = None
+        else:
+            for j, g in enumerate(gaussians):
+                r0 = int(self.row_off[j])
+                src = g if isinstance(g, torch.Tensor) else torch.from_numpy(np.asarray(g, np.float64))
+                amat[r0: r0 + self.n_voxels[j], : self.K].copy_(src)
+        _lib.check(self.lib.srm_init_mapping(self.plan, ctypes.c_void_p(self.stream())), "init_mapping")
+
+    # ------------------------------------------------------------- iteration
+    def exchange(self, comm):
+        """Make every subject's E-step term visible to this rank (srm.py:259-269)."""
+        torch = _torch()
+        if self.world_size == 1:
+            return
+        if hasattr(comm, "all_gather_into"):
+            if self.ordered:
+                m = self.n_slots // self.world_size
+                mine = self.terms[self.rank * m: (self.rank + 1) * m]
+                comm.all_gather_into(self.terms, mine)
+            else:
+                _lib.check(self.lib.srm_reduce_local(self.plan, ctypes.c_void_p(self.stream())))
+                self.red.copy_(self.redlocal)
+                comm.all_reduce_sum(self.red)
+            return
+        # reference protocol (gather + broadcast of host bytes)
+        if not self.ordered:
+            raise ConfigError("reference-protocol communicators need ordered exchange")
+        m = self.n_slots // self.world_size
+        mine = self.terms[self.rank * m: (self.rank + 1) * m].cpu().numpy()
+        blobs = comm.gather(mine.tobytes())
+        table = None
+        if comm.rank == 0:
+            table = np.concatenate([np.frombuffer(b, dtype=np.float64) for b in blobs]).reshape(
+                self.n_slots, self.term_stride)
+        table = comm.broadcast(table)
+        self.terms.copy_(torch.from_numpy(np.ascontiguousarray(table)).to(self.device))
+
+    def step(self, comm=None):
+        """One EM iteration: [exchange] -> E-step tail -> M-step."""
+        if comm is not None and self.world_size > 1:
+            self.exchange(comm)
+        st = ctypes.c_void_p(self.stream())
+        _lib.check(self.lib.srm_e_step(self.plan, st), "e_step")
+        _lib.check(self.lib.srm_m_step(self.plan, st), "m_step")
+
+    def capture(self):
+        """Capture {e_step, m_step} into a CUDA graph (single rank only)."""
+        torch = _torch()
+        if self.world_size != 1:
+            raise ConfigError("graph capture is for single-rank plans")
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=self.device)
+        # snapshot the iteration counter: capture enqueues nothing that runs
+        with torch.cuda.graph(g, stream=side):
+            st = ctypes.c_void_p(side.cuda_stream)
+            _lib.check(self.lib.srm_e_step(self.plan, st), "e_step(capture)")
+            _lib.check(self.lib.srm_m_step(self.plan, st), "m_step(capture)")
+        self._graph = g
+        return g
+
+    def replay(self):
+        self._graph.replay()
+
+    def set_iteration(self, it):
+        _lib.check(self.lib.srm_set_iteration(self.plan, int(it), ctypes.c_void_p(self.stream())))
+
+    def finalize(self):
+        _lib.check(self.lib.srm_finalize(self.plan, ctypes.c_void_p(self.stream())), "finalize")
+
+    # --------------------------------------------------------------- results
+    def status(self):
+        out = (ctypes.c_int32 * 4)()
+        _lib.check(self.lib.srm_read_status(self.plan, out), "read_status")
+        return list(out)
+
+    def raise_status(self):
+        code, arg, it, _ = self.status()
+        if code:
+            raise from_status(code, arg=arg)
+
+    def local_rho2(self):
+        col = self.kp * self.ldx + _lib.REC_RHO2
+        return self.terms[self.slot0: self.slot0 + self.n_local, col]
+
+    def subject_rows(self, j):
+        r0 = int(self.row_off[j])
+        return slice(r0, r0 + self.n_voxels[j])
+
+    def close(self):
+        if getattr(self, "plan", None) is not None and self.lib is not None:
+            self.lib.srm_plan_destroy(self.plan)
+            self.plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

@@ -1,0 +1,491 @@
+"""Shared response model fit on B200: the reference ``factorfit.srm`` API.
+
+Drop-in for ``/root/reference/pkg/src/factorfit/srm.py``: the same names
+(``__all__``), argument meanings, return types and exceptions.  Every piece
+of arithmetic runs in hand-written sm_100a CUDA (libsrm_b200.so, fp64 on
+the FP64 tensor cores); Python only orchestrates, as the reference's
+``fit`` does.  There is no CPU fallback -- without the library or a GPU the
+calls raise.
+
+The EM iteration (srm.py:254-287) on the device:
+
+* E-step term ``W_i^T Xhat_i / rho_i^2`` is never formed from ``W_i``:
+  with ``A_i = Xhat_i S^T / 2`` and ``M_i = (A_i^T A_i)^{-1/2}`` the polar
+  factor is ``W_i = A_i M_i`` (kernels.py:190-212, unique for full rank), so
+  ``W_i^T Xhat_i = M_i^T (A_i^T Xhat_i)``.  One product serves both the
+  M-step cross term (srm.py:151) and the next E-step (srm.py:118); ``W_i``
+  is materialised once at the end.
+* the reduction sums the per-subject terms in ascending global subject
+  order (srm.py:193-213) from an all-gathered table, so ``S`` is identical
+  on every rank and for every shard layout.
+* the K x K algebra (two Cholesky inverses, S, Sigma_s, trace) runs
+  redundantly on every rank: no broadcast (srm.py:266-269) is needed.
+"""
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .collectives import SerialCommunicator, TorchCommunicator, rank_counts
+from .data import SubjectData
+from .engine import SrmEngine, reference_gaussian
+from .errors import ConfigError, DeviceError, ShapeError, from_status
+
+__all__ = [
+    "SrmConfig",
+    "SrmModel",
+    "SubjectData",
+    "demean",
+    "init_subject",
+    "e_step_local",
+    "e_step_global",
+    "update_sigma_s",
+    "m_step_subject",
+    "fit",
+    "project",
+    "map_between",
+    "project_batch",
+]
+
+RHO_FLOOR = 1e-12
+
+
+@dataclass
+class SrmConfig:
+    """srm.py:54-67."""
+
+    k: int
+    iterations: int = 10
+    seed: int = 0
+    tolerance: Optional[float] = None
+
+    def validate(self):
+        if self.k < 1:
+            raise ConfigError("k must be at least 1")
+        if self.iterations < 1:
+            raise ConfigError("iterations must be at least 1")
+        if self.tolerance is not None and self.tolerance <= 0:
+            raise ConfigError("tolerance must be positive when given")
+
+
+@dataclass
+class SrmModel:
+    """Fitted model state held by one worker (srm.py:70-91).
+
+    Extra fields beyond the reference: ``log_likelihood`` (per iteration,
+    the marginal log-likelihood of the parameters that entered that
+    iteration's E-step) and ``device_state`` (the engine, when the caller
+    asked to keep results on the GPU).
+    """
+
+    subject_ids: list
+    subject_indices: list
+    W: list
+    rho2: list
+    mu: list
+    S: np.ndarray
+    rho0: float
+    n_subjects: int
+    sigma_s: Optional[np.ndarray] = None
+    rho2_all: Optional[np.ndarray] = None
+    objective_trace: list = field(default_factory=list)
+    log_likelihood: list = field(default_factory=list)
+    device_state: object = None
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("a CUDA device is required (no CPU fallback)")
+    return torch
+
+
+def _dev(a, dtype=None):
+    """Host/device array -> contiguous float64 (or float32) CUDA tensor."""
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        t = a.detach()
+        if dtype is None:
+            dtype = t.dtype if t.dtype in (torch.float64, torch.float32) else torch.float64
+        return t.to(device="cuda", dtype=dtype).contiguous()
+    arr = np.asarray(a)
+    if dtype is None:
+        dtype = torch.float32 if arr.dtype == np.float32 else torch.float64
+    np_dt = np.float32 if dtype == torch.float32 else np.float64
+    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np_dt)).to("cuda")
+
+
+def _as_matrix(a, name="matrix"):
+    arr = a if hasattr(a, "shape") else np.asarray(a)
+    if len(arr.shape) != 2:
+        raise ShapeError(f"{name} must be 2-D, got ndim={len(arr.shape)}")
+    if arr.shape[0] < 1 or arr.shape[1] < 1:
+        raise ShapeError(f"{name} must have at least one row and column")
+    return arr
+
+
+def _status_tensor():
+    torch = _torch()
+    return torch.zeros(4, dtype=torch.int32, device="cuda")
+
+
+def _raise_status(status):
+    code, arg = (int(x) for x in status[:2].tolist())
+    if code:
+        raise from_status(code, arg=arg)
+
+
+def _workspace(v, k, t):
+    torch = _torch()
+    lib = _lib.load()
+    nb = int(lib.srm_stateless_workspace_bytes(int(v), int(k), int(t)))
+    return torch.empty(nb, dtype=torch.uint8, device="cuda"), nb
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _finite(t, name):
+    torch = _torch()
+    if not bool(torch.isfinite(t).all()):
+        from .errors import InvalidInputError
+
+        raise InvalidInputError(f"{name} contains non-finite entries")
+
+
+# ---------------------------------------------------------------------------
+# step functions (srm.py:94-155)
+# ---------------------------------------------------------------------------
+
+def demean(X):
+    """Remove each voxel's temporal mean; returns (Xhat, mu)  (srm.py:94-98)."""
+    torch = _torch()
+    x = _as_matrix(X, "X")
+    v, t = int(x.shape[0]), int(x.shape[1])
+    eng = SrmEngine([v], t, 1, 1, storage="f64")
+    try:
+        eng.load([x])
+    except Exception:
+        eng.close()
+        raise
+    xhat = eng.xhat[:, :t].clone()
+    mu = eng.mu[:v].clone()
+    eng.close()
+    torch.cuda.synchronize()
+    return xhat.cpu().numpy(), mu.cpu().numpy()
+
+
+def _polar(a_dev, k):
+    torch = _torch()
+    lib = _lib.load()
+    v = a_dev.shape[0]
+    if v < k:
+        raise ShapeError(f"polar_orthogonal needs rows >= cols, got {tuple(a_dev.shape)}")
+    ws, nb = _workspace(v, k, 32)
+    w = torch.empty((v, k), dtype=torch.float64, device="cuda")
+    st = _status_tensor()
+    _lib.check(lib.srm_polar(_ptr(a_dev), a_dev.stride(0), v, k, _ptr(w), k, _ptr(st), _ptr(ws), nb,
+                             _stream()), "polar")
+    _raise_status(st)
+    return w
+
+
+def init_subject(n_voxels, config, subject_index):
+    """Seeded random orthogonal mapping and unit noise variance (srm.py:101-113)."""
+    if n_voxels < config.k:
+        raise ShapeError(f"subject has {n_voxels} voxels, fewer than k={config.k} factors")
+    g = reference_gaussian(n_voxels, config.k, config.seed, subject_index)
+    return _polar(_dev(g), config.k).cpu().numpy(), 1.0
+
+
+def _gemm_tn(w_dev, x_dev, alpha=1.0):
+    torch = _torch()
+    lib = _lib.load()
+    v, k = w_dev.shape
+    t = x_dev.shape[1]
+    out = torch.empty((k, t), dtype=torch.float64, device="cuda")
+    ws, nb = _workspace(v, k, t)
+    dt = _lib.SRM_F64 if x_dev.dtype == torch.float64 else _lib.SRM_F32
+    _lib.check(lib.srm_gemm_tn(_ptr(w_dev), w_dev.stride(0), _ptr(x_dev), dt, x_dev.stride(0), v, k, t,
+                               float(alpha), _ptr(out), t, _ptr(ws), nb, _stream()), "gemm_tn")
+    return out
+
+
+def _gemm_nt(x_dev, s_dev, alpha=1.0):
+    torch = _torch()
+    lib = _lib.load()
+    v, t = x_dev.shape
+    k = s_dev.shape[0]
+    out = torch.empty((v, k), dtype=torch.float64, device="cuda")
+    ws, nb = _workspace(v, k, t)
+    dt = _lib.SRM_F64 if x_dev.dtype == torch.float64 else _lib.SRM_F32
+    _lib.check(lib.srm_gemm_nt(_ptr(x_dev), dt, x_dev.stride(0), _ptr(s_dev), s_dev.stride(0), v, t, k,
+                               float(alpha), _ptr(out), k, _ptr(ws), nb, _stream()), "gemm_nt")
+    return out
+
+
+def e_step_local(W_i, rho2_i, Xhat_i):
+    """This subject's term of the reduction: rho_i^{-2} W_i^T Xhat_i (srm.py:116-118)."""
+    w = _dev(_as_matrix(W_i, "W"), _torch().float64)
+    x = _dev(_as_matrix(Xhat_i, "Xhat"))
+    return (_gemm_tn(w, x) / rho2_i).cpu().numpy()
+
+
+def _tail(reduced, sigma_s, rho0):
+    torch = _torch()
+    lib = _lib.load()
+    red = _dev(_as_matrix(reduced, "reduced"), torch.float64)
+    sig = _dev(_as_matrix(sigma_s, "sigma_s"), torch.float64)
+    k, t = red.shape
+    if sig.shape != (k, k):
+        raise ShapeError(f"sigma_s must be {k} x {k}")
+    _finite(sig, "A")
+    s = torch.empty((k, t), dtype=torch.float64, device="cuda")
+    var = torch.empty((k, k), dtype=torch.float64, device="cuda")
+    sig_new = torch.empty((k, k), dtype=torch.float64, device="cuda")
+    trace = torch.empty(1, dtype=torch.float64, device="cuda")
+    ws, nb = _workspace(1, k, t)
+    st = _status_tensor()
+    _lib.check(lib.srm_tail_step(_ptr(red), t, _ptr(sig), k, k, t, float(rho0), _ptr(s), t, _ptr(var),
+                                 _ptr(sig_new), _ptr(trace), _ptr(st), _ptr(ws), nb, _stream()), "tail")
+    _raise_status(st)
+    return s, var, sig_new, trace
+
+
+def e_step_global(reduced, sigma_s, rho0):
+    """Posterior mean S and covariance from the reduction (srm.py:121-129)."""
+    s, var, _, _ = _tail(reduced, sigma_s, rho0)
+    return s.cpu().numpy(), var.cpu().numpy()
+
+
+def update_sigma_s(sigma_s, rho0, S):
+    """Shared-covariance update; returns (Sigma_new, trace) (srm.py:132-142).
+
+    ``update_sigma_s`` needs only ``var_s`` (from ``sigma_s`` and ``rho0``)
+    and ``S``; the device tail computes it from a zero reduction whose S
+    output is discarded.
+    """
+    torch = _torch()
+    s_dev = _dev(_as_matrix(S, "S"), torch.float64)
+    k, t = s_dev.shape
+    _, var, _, _ = _tail(torch.zeros((k, t), dtype=torch.float64, device="cuda"), sigma_s, rho0)
+    ss = _gemm_tn(s_dev.t().contiguous(), s_dev.t().contiguous())  # S S^T via the V-contraction
+    new = var + ss / t
+    new = 0.5 * (new + new.t())
+    return new.cpu().numpy(), float(torch.diagonal(new).sum().item())
+
+
+def m_step_subject(Xhat_i, S, trace_sigma_s_new):
+    """Per-subject mapping and noise update (srm.py:145-155)."""
+    torch = _torch()
+    x = _dev(_as_matrix(Xhat_i, "Xhat"))
+    s = _dev(_as_matrix(S, "S"), torch.float64)
+    _finite(x, "A")
+    a = _gemm_nt(x, s, 0.5)
+    w = _polar(a, s.shape[0])
+    n_trs = s.shape[1]
+    n_voxels = x.shape[0]
+    cross = float((_gemm_tn(w, x) * s).sum().item())
+    xd = x.to(torch.float64)
+    sq = float((xd * xd).sum().item())
+    rho2 = (sq + n_trs * trace_sigma_s_new - 2.0 * cross) / (n_trs * n_voxels)
+    return w.cpu().numpy(), max(rho2, RHO_FLOOR)
+
+
+# ---------------------------------------------------------------------------
+# the fit (srm.py:216-327)
+# ---------------------------------------------------------------------------
+
+def _storage_for(subjects, storage):
+    if storage in ("f64", "f32"):
+        return storage
+    if storage not in (None, "auto"):
+        raise ConfigError("storage must be 'auto', 'f64' or 'f32'")
+    try:
+        import torch
+
+        tensor_t = torch.Tensor
+    except ImportError:  # pragma: no cover
+        tensor_t = ()
+    f32 = []
+    for s in subjects:
+        x = s.X
+        if isinstance(x, tensor_t):
+            f32.append(str(x.dtype) == "torch.float32")
+        else:
+            f32.append(np.asarray(x).dtype == np.float32)
+    return "f32" if all(f32) else "f64"
+
+
+def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=True,
+        keep_on_device=False, device=None, engine_out=None):
+    """Run the distributed EM; ``subjects`` are this worker's share (srm.py:216).
+
+    Every worker calls this with the same config and its own communicator
+    (``SerialCommunicator``, ``TorchCommunicator`` or any object with the
+    reference protocol).  Subject data may be numpy arrays or torch tensors
+    (CPU -- pinned for asynchronous upload -- or already on the GPU).
+
+    ``storage`` picks the HBM dtype of X-hat: ``"auto"`` keeps fp32 inputs
+    fp32 (half the bytes; arithmetic stays fp64), else fp64.
+    ``ordered`` (default: when the gathered E-step table is <= 64 MiB) sums
+    subject terms in ascending global order on every rank -- bit-identical
+    results for any shard layout; otherwise per-rank sums are all-reduced.
+    """
+    config.validate()
+    if not subjects:
+        raise ConfigError("each worker needs at least one subject")
+    comm = comm if comm is not None else SerialCommunicator()
+    n_trs = int(subjects[0].X.shape[1])
+    for s in subjects:
+        if int(s.X.shape[1]) != n_trs:
+            raise ShapeError(f"subject {s.subject_id} has {s.X.shape[1]} TRs, expected {n_trs}")
+    if n_trs < 2:
+        raise ShapeError("need at least 2 TRs")
+    k = config.k
+    for s in subjects:
+        if int(s.X.shape[0]) < k:
+            raise ShapeError(f"subject has {s.X.shape[0]} voxels, fewer than k={k} factors")
+
+    counts = rank_counts(comm, len(subjects))
+    offset = int(sum(counts[: comm.rank]))
+    n_subjects = int(sum(counts))
+    if ordered is None:
+        kp = -(-k // 8) * 8
+        ldx = -(-n_trs // 32) * 32
+        table = comm.size * max(counts) * (kp * ldx + 8) * 8
+        ordered = comm.size == 1 or table <= (64 << 20) or not hasattr(comm, "all_reduce_sum")
+
+    eng = SrmEngine([int(s.X.shape[0]) for s in subjects], n_trs, k, config.iterations,
+                    storage=_storage_for(subjects, storage), world_size=comm.size, rank=comm.rank,
+                    counts=counts, ordered=ordered, tolerance=config.tolerance is not None,
+                    device=device)
+    if engine_out is not None:
+        engine_out.append(eng)
+    eng.load([s.X for s in subjects])
+    eng.init_mapping(config.seed, offset)
+
+    use_graph = graphs and comm.size == 1
+    n_done = 0
+    for it in range(config.iterations):
+        if use_graph and it == 1:
+            eng.capture()
+        if use_graph and it >= 1:
+            eng.replay()
+        else:
+            eng.step(comm)
+        n_done = it + 1
+        if config.tolerance is not None:
+            eng.raise_status()
+            row = eng.hist[it]
+            if it >= 1:
+                sdiff = float(row[_lib.H_SDIFF].item())
+                sprev = float(row[_lib.H_SPREV].item())
+                if sdiff / max(sprev, 1e-300) < config.tolerance:
+                    break
+    eng.finalize()
+    eng.raise_status()
+    return _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device)
+
+
+def _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device):
+    torch = _torch()
+    rho2_local = eng.local_rho2().clone()
+    # final rho^2 gather + rho0 refresh (srm.py:289-313)
+    if comm.size > 1:
+        m = max(eng.counts)
+        mine = torch.zeros(m, dtype=torch.float64, device=eng.device)
+        mine[: eng.n_local] = rho2_local
+        if hasattr(comm, "all_gather_into"):
+            allr = torch.empty(comm.size * m, dtype=torch.float64, device=eng.device)
+            comm.all_gather_into(allr, mine)
+            parts = [allr[r * m: r * m + eng.counts[r]] for r in range(comm.size)]
+            rho2_all = torch.cat(parts).cpu().numpy()
+        else:
+            blobs = comm.gather(rho2_local.cpu().numpy().tobytes())
+            tab = None
+            if comm.rank == 0:
+                tab = np.concatenate([np.frombuffer(b, np.float64) for b in blobs])[None, :]
+            rho2_all = comm.broadcast(tab)[0]
+    else:
+        rho2_all = rho2_local.cpu().numpy()
+    rho0 = float(np.add.reduce(1.0 / rho2_all))
+    hist = eng.hist[:n_done].cpu().numpy()
+    rho2_hist = hist[:, _lib.H_RHO2: _lib.H_RHO2 + eng.n_local]
+    objective = [float(np.mean(r)) for r in rho2_hist]
+    lls = [float(x) for x in hist[:, _lib.H_LL]]
+    if keep_on_device:
+        W = [eng.wout[eng.subject_rows(j)] for j in range(eng.n_local)]
+        mu = [eng.mu[eng.subject_rows(j)] for j in range(eng.n_local)]
+        S = eng.S.clone()
+        sigma = eng.sigma.clone()
+    else:
+        wout = eng.wout.cpu().numpy()
+        muh = eng.mu.cpu().numpy()
+        W = [np.ascontiguousarray(wout[eng.subject_rows(j)]) for j in range(eng.n_local)]
+        mu = [muh[eng.subject_rows(j)].copy() for j in range(eng.n_local)]
+        S = np.ascontiguousarray(eng.S.cpu().numpy())
+        sigma = np.ascontiguousarray(eng.sigma.cpu().numpy())
+    model = SrmModel(
+        subject_ids=[s.subject_id for s in subjects],
+        subject_indices=list(range(offset, offset + len(subjects))),
+        W=W,
+        rho2=[float(r) for r in rho2_local.cpu().numpy()],
+        mu=mu,
+        S=S,
+        rho0=rho0,
+        n_subjects=n_subjects,
+        sigma_s=sigma if comm.rank == 0 else None,
+        rho2_all=np.asarray(rho2_all) if comm.rank == 0 else None,
+        objective_trace=objective,
+        log_likelihood=lls,
+        device_state=eng if keep_on_device else None,
+    )
+    if not keep_on_device:
+        eng.close()
+    return model
+
+
+# ---------------------------------------------------------------------------
+# transforms (srm.py:330-338)
+# ---------------------------------------------------------------------------
+
+def project_batch(model, i, X):
+    """Map V_i x T' volumes of held subject ``i`` into the shared space: W_i^T (X - mu_i)."""
+    torch = _torch()
+    w = _dev(model.W[i], torch.float64)
+    mu = _dev(model.mu[i], torch.float64).reshape(-1, 1)
+    x = _dev(X, torch.float64)
+    if x.dim() == 1:
+        x = x.reshape(-1, 1)
+    return _gemm_tn(w, (x - mu).contiguous())
+
+
+def project(model, i, x):
+    """Map one volume of held subject ``i`` into the shared space (srm.py:330-333)."""
+    torch = _torch()
+    xv = _dev(np.asarray(x, dtype=np.float64).ravel() if not isinstance(x, torch.Tensor) else x.reshape(-1),
+              torch.float64)
+    return project_batch(model, i, xv.reshape(-1, 1)).reshape(-1).cpu().numpy()
+
+
+def map_between(model, i, j, x):
+    """Map a volume of subject ``i`` into subject ``j``'s voxel space (srm.py:336-338)."""
+    torch = _torch()
+    z = project_batch(model, i, _dev(np.asarray(x, dtype=np.float64).ravel()).reshape(-1, 1))
+    wj = _dev(model.W[j], torch.float64)
+    out = _gemm_nt(wj, z.t().contiguous())  # W_j z (V_j x 1)
+    return (out.reshape(-1) + _dev(model.mu[j], torch.float64)).cpu().numpy()

@@ -1,0 +1,172 @@
+"""CUDA path vs the reference (golden fixtures) and the CPU oracle.
+
+Tolerance (BASELINE.json north_star): per EM iteration, normwise relative
+1e-9 for fp64 and 1e-4 for fp32 inputs, on S, every W_i, rho^2, Sigma_s and
+the log-likelihood.  Per-iteration states come from fits of 1..N iterations
+(the reference's own test_srm.py:231-245 pattern).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_subjects, load_golden, nrel
+from oracle import srm_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-9
+TOL32 = 1e-4
+
+
+@pytest.fixture(scope="module")
+def srm():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a CUDA device")
+    from paper_1608_04647_b200 import srm as mod
+
+    return mod
+
+
+def _subjects(srm, xs):
+    return [srm.SubjectData(f"s{i}", x) for i, x in enumerate(xs)]
+
+
+def _check_model(model, ref_S, ref_sigma, ref_rho2, ref_W, tol, what=""):
+    assert nrel(model.S, ref_S) <= tol, (what, "S", nrel(model.S, ref_S))
+    assert nrel(model.sigma_s, ref_sigma) <= tol, (what, "sigma", nrel(model.sigma_s, ref_sigma))
+    assert nrel(model.rho2, ref_rho2) <= tol, (what, "rho2", nrel(model.rho2, ref_rho2))
+    for i, w in enumerate(ref_W):
+        assert nrel(model.W[i], w) <= tol, (what, "W", i, nrel(model.W[i], w))
+
+
+@pytest.mark.parametrize("name", ["em_small", "em_ragged", "em_recipe_f32", "em_smooth_f32"])
+def test_fit_every_iteration_matches_reference(srm, name):
+    g = load_golden(name)
+    xs = golden_subjects(g)
+    k, iters, seed = int(g["k"]), int(g["iterations"]), int(g["seed"])
+    tol = TOL64 if xs[0].dtype == np.float64 else TOL32
+    for n in range(1, iters + 1):
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=k, iterations=n, seed=seed))
+        it = n - 1
+        _check_model(m, g[f"it{it}_S"], g[f"it{it}_sigma_s"], g[f"it{it}_rho2"],
+                     [g[f"it{it}_W{i}"] for i in range(len(xs))], tol, f"{name} it{it}")
+        # LL of the parameters entering each iteration vs the reference naive LL
+        for j in range(n):
+            ref = float(g[f"it{j}_ll_naive"])
+            if np.isfinite(ref):
+                assert abs(m.log_likelihood[j] - ref) <= TOL64 * abs(ref), (name, j)
+        # orthogonality after every M-step (acceptance criterion 4)
+        for w in m.W:
+            assert np.max(np.abs(w.T @ w - np.eye(k))) <= 1e-8
+    assert nrel(m.objective_trace, g["fit_objective"]) <= tol
+    assert abs(m.rho0 - float(g["fit_rho0"])) <= tol * abs(float(g["fit_rho0"]))
+    for i in range(len(xs)):
+        assert nrel(m.mu[i], g[f"fit_mu{i}"]) <= tol or np.max(np.abs(m.mu[i] - g[f"fit_mu{i}"])) <= 1e-12
+
+
+def test_tolerance_stop(srm):
+    g = load_golden("tolerance")
+    m = srm.fit(_subjects(srm, [g["X0"], g["X1"]]), srm.SrmConfig(k=2, iterations=50, seed=1, tolerance=1e-8))
+    assert len(m.objective_trace) == int(g["n_iter"])
+    assert nrel(m.S, g["S"]) <= TOL64
+
+
+def test_recipe_vs_oracle_moderate(srm):
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(5, 2500, 160, 20, seed=11)
+    ref = orc.run_em(xs, 20, 6, seed=0)
+    for n in (1, 3, 6):
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=20, iterations=n, seed=0))
+        r = ref["iters"][n - 1]
+        _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, f"recipe it{n-1}")
+        for j in range(n):
+            assert abs(m.log_likelihood[j] - ref["iters"][j]["ll"]) <= TOL64 * abs(ref["iters"][j]["ll"])
+
+
+def test_cfg1_full_size_vs_oracle(srm):
+    """BASELINE cfg 1 (10 x 5000 x 500, K=50, fp64, 10 iterations) at parity."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(10, 5000, 500, 50, seed=1)
+    ref = orc.run_em(xs, 50, 10, seed=0)
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=50, iterations=10, seed=0))
+    r = ref["iters"][-1]
+    _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, "cfg1")
+    lls = np.array(m.log_likelihood)
+    ref_ll = np.array([x["ll"] for x in ref["iters"]])
+    assert np.max(np.abs(lls - ref_ll) / np.abs(ref_ll)) <= TOL64
+    assert np.all(np.diff(lls) >= -1e-9 * np.abs(lls[1:]))
+
+
+# --------------------------------------------------------------------------
+# step-function API (srm.py:94-155) vs golden
+# --------------------------------------------------------------------------
+
+def test_steps_match_reference(srm):
+    g = load_golden("steps")
+    ws = [g[f"W{i}"] for i in range(3)]
+    xs = [g[f"Xhat{i}"] for i in range(3)]
+    for i in range(3):
+        assert nrel(srm.e_step_local(ws[i], float(g["rho2"][i]), xs[i]), g[f"local{i}"]) <= 1e-13
+    S, var = srm.e_step_global(g["reduced"], g["sigma_s"], float(g["rho0"]))
+    assert nrel(S, g["S"]) <= TOL64 and nrel(var, g["var_s"]) <= TOL64
+    sig, tr = srm.update_sigma_s(g["sigma_s"], float(g["rho0"]), g["S"])
+    assert nrel(sig, g["sigma_new"]) <= TOL64 and abs(tr - float(g["trace"])) <= TOL64 * abs(float(g["trace"]))
+    for i in range(3):
+        w, r = srm.m_step_subject(xs[i], g["S"], float(g["trace"]))
+        assert nrel(w, g[f"mW{i}"]) <= TOL64
+        assert abs(r - float(g[f"mrho2_{i}"])) <= TOL64 * abs(float(g[f"mrho2_{i}"]))
+
+
+def test_demean_and_init_match_reference(srm):
+    g = load_golden("kernels")
+    xh, mu = srm.demean(g["demean_in"])
+    assert np.array_equal(xh, g["demean_xhat"]) and np.array_equal(mu, g["demean_mu"])
+    xh, mu = srm.demean(g["demean_in2"])
+    assert np.max(np.abs(xh - g["demean_xhat2"])) <= 1e-12 and np.max(np.abs(mu - g["demean_mu2"])) <= 1e-12
+    for j in range(4):
+        v, k, seed, idx = (int(x) for x in g[f"init_args{j}"])
+        w, rho2 = srm.init_subject(v, srm.SrmConfig(k=k, seed=seed), idx)
+        assert rho2 == 1.0
+        assert nrel(w, g[f"init_W{j}"]) <= 1e-12, (j, nrel(w, g[f"init_W{j}"]))
+
+
+def test_errors(srm):
+    from paper_1608_04647_b200.errors import (DefinitenessError, InvalidInputError, RankError,
+                                              ShapeError, ConfigError)
+
+    rng = np.random.default_rng(8)
+    with pytest.raises(RankError):
+        srm.m_step_subject(rng.standard_normal((6, 4)), np.zeros((2, 4)), 1.0)
+    with pytest.raises(DefinitenessError) as ei:
+        srm.e_step_global(np.zeros((3, 4)), np.zeros((3, 3)), 1.0)
+    assert ei.value.pivot == 0
+    x = rng.standard_normal((20, 8))
+    x[3, 2] = np.nan
+    with pytest.raises(InvalidInputError):
+        srm.fit([srm.SubjectData("a", x)], srm.SrmConfig(k=2, iterations=2))
+    with pytest.raises(ShapeError):
+        srm.fit([srm.SubjectData("a", np.zeros((5, 4))), srm.SubjectData("b", np.zeros((5, 6)))],
+                srm.SrmConfig(k=2))
+    with pytest.raises(ShapeError):
+        srm.init_subject(2, srm.SrmConfig(k=3), 0)
+    with pytest.raises(ConfigError):
+        srm.fit([], srm.SrmConfig(k=2))
+
+
+def test_projection(srm):
+    g = load_golden("em_small")
+    xs = golden_subjects(g)
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=4, iterations=5, seed=0))
+    assert np.max(np.abs(srm.project(m, 0, m.mu[0]))) == 0.0
+    x = xs[1][:, 3]
+    z = srm.project(m, 1, x)
+    assert nrel(z, m.W[1].T @ (x - m.mu[1])) <= 1e-13
+    once = srm.map_between(m, 0, 0, xs[0][:, 0])
+    twice = srm.map_between(m, 0, 0, once)
+    assert np.max(np.abs(twice - once)) <= 1e-10
+    with pytest.raises(IndexError):
+        srm.project(m, 7, np.zeros(60))
