@@ -89,7 +89,8 @@ enum srm_dim {
   SRM_D_SLOT_OFFSET = 7,  /* first record slot owned by this rank       */
   SRM_D_ITEMS_E = 8,      /* work items of the V-contraction kernel     */
   SRM_D_ITEMS_A = 9,      /* work items of the T-contraction kernel     */
-  SRM_D_CHUNK_ROWS = 10   /* rows per V chunk                           */
+  SRM_D_CHUNK_ROWS = 10,  /* rows per V chunk                           */
+  SRM_D_LAUNCHES = 11     /* kernel launches per EM iteration (e+m step) */
 };
 
 /* per-iteration history columns (SRM_R_HIST, hist_stride doubles per row) */
@@ -163,6 +164,13 @@ int srm_reduce_local(srm_plan* plan, void* stream);
 int srm_e_step(srm_plan* plan, void* stream);
 int srm_m_step(srm_plan* plan, void* stream);
 int srm_finalize(srm_plan* plan, void* stream);
+
+/* measurement: run one e_step + m_step eagerly with a CUDA event between every
+ * kernel, synchronise, and write each kernel's duration (ms) to ms_out; *n_out
+ * receives the number of kernels.  srm_profile_name(i) names kernel i of the
+ * last profiled iteration. */
+int srm_profile_iteration(srm_plan* plan, float* ms_out, int capacity, int* n_out, void* stream);
+const char* srm_profile_name(int index);
 
 /* synchronous copy of the device status word {code, arg, iteration, 0} */
 int srm_read_status(srm_plan* plan, int32_t* out4);

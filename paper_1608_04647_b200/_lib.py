@@ -39,6 +39,8 @@ SIGNATURES = [
     ("srm_e_step", c_int, [c_vp, c_vp]),
     ("srm_m_step", c_int, [c_vp, c_vp]),
     ("srm_finalize", c_int, [c_vp, c_vp]),
+    ("srm_profile_iteration", c_int, [c_vp, ctypes.POINTER(ctypes.c_float), c_int, c_i32p, c_vp]),
+    ("srm_profile_name", ctypes.c_char_p, [c_int]),
     ("srm_read_status", c_int, [c_vp, c_i32p]),
     ("srm_clear_status", c_int, [c_vp, c_vp]),
     ("srm_gemm_tn", c_int, [c_vp, c_i64, c_vp, c_int, c_i64, c_i64, c_i64, c_i64, c_dbl, c_vp,
@@ -58,7 +60,7 @@ FLAG_ORDERED, FLAG_TOLERANCE, FLAG_GRAM = 1, 2, 4
 (R_XHAT, R_AMAT, R_WOUT, R_MU, R_TERMS, R_RED, R_REDLOCAL, R_S, R_SIGMA, R_HIST, R_STATUS,
  R_MMAT, R_SCAL, R_GRAM, R_VAR) = range(15)
 (D_LDX, D_KP, D_ROWS, D_TERM_STRIDE, D_RED_STRIDE, D_HIST_STRIDE, D_N_SLOTS, D_SLOT_OFFSET,
- D_ITEMS_E, D_ITEMS_A, D_CHUNK_ROWS) = range(11)
+ D_ITEMS_E, D_ITEMS_A, D_CHUNK_ROWS, D_LAUNCHES) = range(12)
 H_LL, H_TRACE, H_RHO0, H_SDIFF, H_SPREV, H_RHO2 = 0, 1, 2, 3, 4, 8
 REC_RHO2, REC_V, REC_SQNORM, REC_SCALARS = 0, 1, 2, 8
 RED_RHO0, RED_VLOGRHO, RED_SQRHO, RED_VSUM = 0, 1, 2, 3

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -58,6 +59,10 @@ enum Internal {
 };
 
 }  // namespace
+
+void srm::set_last_error(const char* where, cudaError_t e) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+}
 
 struct srm_plan {
   int dtype = SRM_F64;
@@ -266,17 +271,67 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 int check(cudaError_t e, const char* where) { return e == cudaSuccess ? SRM_OK : cuda_fail(e, where); }
 
-int run_contractions(srm_plan* p, cudaStream_t st) {
+struct Stage {
+  const char* name;
+  std::function<cudaError_t(cudaStream_t)> fn;
+};
+
+void contraction_stages(srm_plan* p, std::vector<Stage>& out) {
   const DevPlan& d = p->dp;
-  cudaError_t e = launch_contract_e((int)p->kp, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo,
-                                    1.0, region<ItemE>(p, I_ITEMS_EX), (int)p->items_ex.size(), st);
-  if (e != cudaSuccess) return cuda_fail(e, "contract_e(xhat)");
-  e = launch_contract_e((int)p->kp, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0,
-                        region<ItemE>(p, I_ITEMS_EA), (int)p->items_ea.size(), st);
-  if (e != cudaSuccess) return cuda_fail(e, "contract_e(amat)");
-  e = launch_reduce_chunks(d, st);
-  return check(e, "reduce_chunks");
+  out.push_back({"contract_e_xhat", [p, d](cudaStream_t st) {
+                   return launch_contract_e((int)p->kp, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
+                                            region<ItemE>(p, I_ITEMS_EX), (int)p->items_ex.size(), st);
+                 }});
+  out.push_back({"contract_e_gram", [p, d](cudaStream_t st) {
+                   return launch_contract_e((int)p->kp, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0,
+                                            region<ItemE>(p, I_ITEMS_EA), (int)p->items_ea.size(), st);
+                 }});
+  out.push_back({"reduce_chunks", [d](cudaStream_t st) { return launch_reduce_chunks(d, st); }});
 }
+
+std::vector<Stage> e_stages(srm_plan* p) {
+  const DevPlan& d = p->dp;
+  std::vector<Stage> v;
+  if (p->flags & SRM_FLAG_ORDERED) {
+    const int n = (int)p->order.size();
+    v.push_back({"reduce_terms", [d, n](cudaStream_t st) { return launch_reduce_terms(d, d.red, d.order, n, st); }});
+  }
+  v.push_back({"tail_kk", [d](cudaStream_t st) { return launch_tail_kk(d, st); }});
+  v.push_back({"tail_s", [d](cudaStream_t st) { return launch_tail_s(d, st); }});
+  v.push_back({"tail_sigma", [d](cudaStream_t st) { return launch_tail_sigma(d, st); }});
+  return v;
+}
+
+std::vector<Stage> m_stages(srm_plan* p) {
+  const DevPlan& d = p->dp;
+  std::vector<Stage> v;
+  v.push_back({"contract_a", [p, d](cudaStream_t st) {
+                 return launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
+                                          0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
+               }});
+  contraction_stages(p, v);
+  v.push_back({"eig_polar", [d](cudaStream_t st) { return launch_eig_polar(d, 0, st); }});
+  v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 1, st); }});
+  v.push_back({"finalize_rho", [d](cudaStream_t st) { return launch_finalize_rho(d, 0, st); }});
+  v.push_back({"advance_iteration", [d](cudaStream_t st) { return launch_set_iteration(d, 0, 1, st); }});
+  return v;
+}
+
+int run_stages(const std::vector<Stage>& stages, cudaStream_t st) {
+  for (const Stage& s : stages) {
+    cudaError_t e = s.fn(st);
+    if (e != cudaSuccess) return cuda_fail(e, s.name);
+  }
+  return SRM_OK;
+}
+
+int run_contractions(srm_plan* p, cudaStream_t st) {
+  std::vector<Stage> v;
+  contraction_stages(p, v);
+  return run_stages(v, st);
+}
+
+std::vector<std::string> g_profile_names;
 
 }  // namespace
 
@@ -372,6 +427,7 @@ int64_t srm_plan_dim(const srm_plan* p, int which) {
     case SRM_D_ITEMS_E: return (int64_t)(p->items_ex.size() + p->items_ea.size());
     case SRM_D_ITEMS_A: return (int64_t)p->items_a.size();
     case SRM_D_CHUNK_ROWS: return p->chunk_rows;
+    case SRM_D_LAUNCHES: return (int64_t)(e_stages(const_cast<srm_plan*>(p)).size() + m_stages(const_cast<srm_plan*>(p)).size());
     default: return -1;
   }
 }
@@ -458,28 +514,47 @@ int srm_set_iteration(srm_plan* p, int iteration, void* stream) {
 
 int srm_e_step(srm_plan* p, void* stream) {
   if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
-  cudaStream_t st = as_stream(stream);
-  cudaError_t e = cudaSuccess;
-  if (p->flags & SRM_FLAG_ORDERED)
-    e = launch_reduce_terms(p->dp, p->dp.red, p->dp.order, (int)p->order.size(), st);
-  if (e == cudaSuccess) e = launch_tail(p->dp, st);
-  return check(e, "e_step");
+  return run_stages(e_stages(p), as_stream(stream));
 }
 
 int srm_m_step(srm_plan* p, void* stream) {
   if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  return run_stages(m_stages(p), as_stream(stream));
+}
+
+int srm_profile_iteration(srm_plan* p, float* ms_out, int capacity, int* n_out, void* stream) {
+  if (!p || !p->ws || !ms_out || !n_out) return fail(SRM_ERR_CONFIG, "plan not bound");
   cudaStream_t st = as_stream(stream);
-  const DevPlan& d = p->dp;
-  cudaError_t e = launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
-                                    0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
-  if (e != cudaSuccess) return cuda_fail(e, "contract_a");
-  int rc = run_contractions(p, st);
-  if (rc) return rc;
-  e = launch_eig_polar(d, 0, st);
-  if (e == cudaSuccess) e = launch_apply_m(d, 1, st);
-  if (e == cudaSuccess) e = launch_finalize_rho(d, 0, st);
-  if (e == cudaSuccess) e = launch_set_iteration(d, 0, 1, st);
-  return check(e, "m_step");
+  std::vector<Stage> stages = e_stages(p);
+  std::vector<Stage> m = m_stages(p);
+  stages.insert(stages.end(), m.begin(), m.end());
+  const int n = (int)stages.size();
+  std::vector<cudaEvent_t> ev(n + 1);
+  for (auto& e : ev) cudaEventCreate(&e);
+  cudaEventRecord(ev[0], st);
+  int rc = SRM_OK;
+  for (int i = 0; i < n && rc == SRM_OK; ++i) {
+    cudaError_t e = stages[i].fn(st);
+    if (e != cudaSuccess) rc = cuda_fail(e, stages[i].name);
+    cudaEventRecord(ev[i + 1], st);
+  }
+  cudaError_t e = cudaEventSynchronize(ev[n]);
+  if (rc == SRM_OK && e != cudaSuccess) rc = cuda_fail(e, "profile sync");
+  g_profile_names.clear();
+  for (int i = 0; i < n; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+    if (i < capacity) ms_out[i] = ms;
+    g_profile_names.push_back(stages[i].name);
+  }
+  for (auto& x : ev) cudaEventDestroy(x);
+  *n_out = n;
+  return rc;
+}
+
+const char* srm_profile_name(int index) {
+  if (index < 0 || index >= (int)g_profile_names.size()) return "";
+  return g_profile_names[index].c_str();
 }
 
 int srm_finalize(srm_plan* p, void* stream) {

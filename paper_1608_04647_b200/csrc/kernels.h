@@ -38,4 +38,7 @@ cudaError_t launch_contract_a(int kp, int x_dtype, const void* X, int64_t ldx, c
 
 bool contract_kp_supported(int kp);
 
+// thread-local message returned by srm_last_error() (defined in capi.cu)
+void set_last_error(const char* where, cudaError_t e);
+
 }  // namespace srm

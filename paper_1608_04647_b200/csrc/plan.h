@@ -75,6 +75,9 @@ cudaError_t launch_set_iteration(const DevPlan& p, int iteration, int advance, c
 cudaError_t launch_reduce_terms(const DevPlan& p, double* dst, const int32_t* order, int count,
                                 cudaStream_t s);
 cudaError_t launch_tail(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_tail_sigma(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_apply_w(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);
 
 // stateless helpers

@@ -802,21 +802,36 @@ cudaError_t launch_reduce_terms(const DevPlan& p, double* dst, const int32_t* or
   return cudaGetLastError();
 }
 
-cudaError_t launch_tail(const DevPlan& p, cudaStream_t s) {
+cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s) {
   const int K = (int)p.K;
-  size_t b1 = (size_t)2 * K * (K + 1) * sizeof(double);
+  const size_t b1 = (size_t)2 * K * (K + 1) * sizeof(double);
   cudaError_t e = set_smem((const void*)k_tail_kk, b1);
   if (e != cudaSuccess) return e;
   k_tail_kk<<<1, kSmallThreads, b1, s>>>(p);
-  size_t b2 = (size_t)2 * K * 32 * sizeof(double);
-  e = set_smem((const void*)k_tail_s, b2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s) {
+  const size_t b2 = (size_t)2 * p.K * 32 * sizeof(double);
+  cudaError_t e = set_smem((const void*)k_tail_s, b2);
   if (e != cudaSuccess) return e;
   k_tail_s<<<p.ntile_tail, kSmallThreads, b2, s>>>(p);
-  size_t b3 = (size_t)K * K * sizeof(double);
-  e = set_smem((const void*)k_tail_sigma, b3);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tail_sigma(const DevPlan& p, cudaStream_t s) {
+  const size_t b3 = (size_t)p.K * p.K * sizeof(double);
+  cudaError_t e = set_smem((const void*)k_tail_sigma, b3);
   if (e != cudaSuccess) return e;
   k_tail_sigma<<<1, kSmallThreads, b3, s>>>(p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_tail(const DevPlan& p, cudaStream_t s) {
+  cudaError_t e = launch_tail_kk(p, s);
+  if (e == cudaSuccess) e = launch_tail_s(p, s);
+  if (e == cudaSuccess) e = launch_tail_sigma(p, s);
+  return e;
 }
 
 cudaError_t launch_apply_w(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s) {

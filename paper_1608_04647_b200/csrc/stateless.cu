@@ -39,7 +39,11 @@ __global__ void k_sum_chunks(const double* __restrict__ part, int64_t stride, in
   out[e] = acc;
 }
 
-int ret(cudaError_t e) { return e == cudaSuccess ? SRM_OK : SRM_ERR_CUDA; }
+int ret(cudaError_t e, const char* where = "stateless") {
+  if (e == cudaSuccess) return SRM_OK;
+  set_last_error(where, e);
+  return SRM_ERR_CUDA;
+}
 
 // out (kp x ncols_pad) = L^T R over v rows, L [v x kp] f64, R [v x ldr] dtype
 cudaError_t split_v(const double* L, int64_t kp, const void* R, int r_dtype, int64_t ldr, int64_t ncols,
@@ -135,15 +139,18 @@ int srm_gemm_nt(const void* x, int x_dtype, int64_t ldx, const double* s, int64_
     it.pad = 0;
     host.push_back(it);
   }
+  const char* where = "gemm_nt: stage X";
   cudaError_t e = cudaMemsetAsync(Xp, 0, v * ldxp * es, st);
   if (e == cudaSuccess) e = cudaMemcpy2DAsync(Xp, ldxp * es, x, ldx * es, t * es, v, cudaMemcpyDeviceToDevice, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(Sp, 0, kp * ldxp * 8, st);
+  if (e == cudaSuccess) { where = "gemm_nt: stage S"; e = cudaMemsetAsync(Sp, 0, kp * ldxp * 8, st); }
   if (e == cudaSuccess) e = cudaMemcpy2DAsync(Sp, ldxp * 8, s, lds * 8, t * 8, k, cudaMemcpyDeviceToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(items, host.data(), host.size() * sizeof(ItemA), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess)
+  if (e == cudaSuccess) { where = "gemm_nt: items"; e = cudaMemcpyAsync(items, host.data(), host.size() * sizeof(ItemA), cudaMemcpyHostToDevice, st); }
+  if (e == cudaSuccess) {
+    where = "gemm_nt: contract_a";
     e = launch_contract_a((int)kp, x_dtype, Xp, ldxp, Sp, ldxp, ldxp, Op, kp, alpha, items, (int)host.size(), st);
-  if (e == cudaSuccess) e = cudaMemcpy2DAsync(out, ldo * 8, Op, kp * 8, k * 8, v, cudaMemcpyDeviceToDevice, st);
-  return ret(e);
+  }
+  if (e == cudaSuccess) { where = "gemm_nt: copy out"; e = cudaMemcpy2DAsync(out, ldo * 8, Op, kp * 8, k * 8, v, cudaMemcpyDeviceToDevice, st); }
+  return ret(e, where);
 }
 
 int srm_tail_step(const double* reduced, int64_t ldr, const double* sigma, int64_t ldsig, int64_t k, int64_t t,

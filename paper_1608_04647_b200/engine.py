@@ -282,6 +282,19 @@ class SrmEngine:
     def set_iteration(self, it):
         _lib.check(self.lib.srm_set_iteration(self.plan, int(it), ctypes.c_void_p(self.stream())))
 
+    def profile_iteration(self):
+        """One eager iteration with an event between kernels -> [(name, ms)]."""
+        cap = 64
+        ms = (ctypes.c_float * cap)()
+        n = ctypes.c_int32()
+        _lib.check(self.lib.srm_profile_iteration(self.plan, ms, cap, ctypes.byref(n),
+                                                  ctypes.c_void_p(self.stream())), "profile")
+        return [(self.lib.srm_profile_name(i).decode(), float(ms[i])) for i in range(n.value)]
+
+    @property
+    def launches_per_iteration(self):
+        return int(self.lib.srm_plan_dim(self.plan, _lib.D_LAUNCHES))
+
     def finalize(self):
         _lib.check(self.lib.srm_finalize(self.plan, ctypes.c_void_p(self.stream())), "finalize")
 

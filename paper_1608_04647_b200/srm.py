@@ -154,6 +154,11 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _ld(t):
+    """Row pitch in elements of a row-major 2-D tensor (size-1 rows may carry any stride)."""
+    return int(t.stride(0)) if t.shape[0] > 1 else int(t.shape[1])
+
+
 def _stream():
     return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
 
@@ -197,7 +202,7 @@ def _polar(a_dev, k):
     ws, nb = _workspace(v, k, 32)
     w = torch.empty((v, k), dtype=torch.float64, device="cuda")
     st = _status_tensor()
-    _lib.check(lib.srm_polar(_ptr(a_dev), a_dev.stride(0), v, k, _ptr(w), k, _ptr(st), _ptr(ws), nb,
+    _lib.check(lib.srm_polar(_ptr(a_dev), _ld(a_dev), v, k, _ptr(w), k, _ptr(st), _ptr(ws), nb,
                              _stream()), "polar")
     _raise_status(st)
     return w
@@ -219,7 +224,7 @@ def _gemm_tn(w_dev, x_dev, alpha=1.0):
     out = torch.empty((k, t), dtype=torch.float64, device="cuda")
     ws, nb = _workspace(v, k, t)
     dt = _lib.SRM_F64 if x_dev.dtype == torch.float64 else _lib.SRM_F32
-    _lib.check(lib.srm_gemm_tn(_ptr(w_dev), w_dev.stride(0), _ptr(x_dev), dt, x_dev.stride(0), v, k, t,
+    _lib.check(lib.srm_gemm_tn(_ptr(w_dev), _ld(w_dev), _ptr(x_dev), dt, _ld(x_dev), v, k, t,
                                float(alpha), _ptr(out), t, _ptr(ws), nb, _stream()), "gemm_tn")
     return out
 
@@ -232,7 +237,7 @@ def _gemm_nt(x_dev, s_dev, alpha=1.0):
     out = torch.empty((v, k), dtype=torch.float64, device="cuda")
     ws, nb = _workspace(v, k, t)
     dt = _lib.SRM_F64 if x_dev.dtype == torch.float64 else _lib.SRM_F32
-    _lib.check(lib.srm_gemm_nt(_ptr(x_dev), dt, x_dev.stride(0), _ptr(s_dev), s_dev.stride(0), v, t, k,
+    _lib.check(lib.srm_gemm_nt(_ptr(x_dev), dt, _ld(x_dev), _ptr(s_dev), _ld(s_dev), v, t, k,
                                float(alpha), _ptr(out), k, _ptr(ws), nb, _stream()), "gemm_nt")
     return out
 
