@@ -165,6 +165,13 @@ int srm_e_step(srm_plan* plan, void* stream);
 int srm_m_step(srm_plan* plan, void* stream);
 int srm_finalize(srm_plan* plan, void* stream);
 
+/* one EM iteration as a CUDA graph: srm_graph_capture records
+ * {srm_e_step, srm_m_step} once (single-rank plans; call after one eager
+ * iteration so every kernel is configured); srm_graph_launch replays it on
+ * `stream` (the device iteration counter advances inside the graph). */
+int srm_graph_capture(srm_plan* plan);
+int srm_graph_launch(srm_plan* plan, void* stream);
+
 /* measurement: run one e_step + m_step eagerly with a CUDA event between every
  * kernel, synchronise, and write each kernel's duration (ms) to ms_out; *n_out
  * receives the number of kernels.  srm_profile_name(i) names kernel i of the

@@ -55,6 +55,7 @@ enum Internal {
   I_ITEMS_EX,
   I_ITEMS_EA,
   I_ITEMS_A,
+  I_ITEMS_G,
   I_COUNT
 };
 
@@ -81,7 +82,7 @@ struct srm_plan {
   std::vector<int64_t> chunk0, nchunk;
   int64_t chunks_total = 0;
   std::vector<ItemE> items_ex, items_ea;
-  std::vector<ItemA> items_a;
+  std::vector<ItemA> items_a, items_g;
   std::vector<int64_t> subj;
   std::vector<int32_t> order, order_local;
   int64_t off[I_COUNT] = {0};
@@ -89,6 +90,9 @@ struct srm_plan {
   int64_t total_bytes = 0;
   char* ws = nullptr;
   DevPlan dp{};
+  cudaStream_t cap_stream = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
 };
 
 namespace {
@@ -134,6 +138,7 @@ void layout(srm_plan* p) {
   sz[I_ITEMS_EX] = (int64_t)p->items_ex.size() * sizeof(ItemE);
   sz[I_ITEMS_EA] = (int64_t)p->items_ea.size() * sizeof(ItemE);
   sz[I_ITEMS_A] = (int64_t)p->items_a.size() * sizeof(ItemA);
+  sz[I_ITEMS_G] = (int64_t)p->items_g.size() * sizeof(ItemA);
   int64_t cur = 0;
   for (int r = 0; r < I_COUNT; ++r) {
     p->off[r] = cur;
@@ -182,6 +187,16 @@ void build_work(srm_plan* p) {
   p->items_ex.clear();
   p->items_ea.clear();
   p->items_a.clear();
+  p->items_g.clear();
+  for (int i = 0; i < p->n_local; ++i) {
+    // A_i^T A_i = (A_i^T Xhat_i) S^T / 2 = B_i S^T / 2 over the reduced B_i
+    ItemA g;
+    g.x_off = (int64_t)i * p->kp * p->ldo;
+    g.o_off = (int64_t)i * p->kp * p->ldo + p->ldx;
+    g.rows = (int32_t)p->K;
+    g.pad = i;
+    p->items_g.push_back(g);
+  }
   for (int i = 0; i < p->n_local; ++i) {
     for (int64_t ch = 0; ch < p->nchunk[i]; ++ch) {
       const int64_t r0 = p->row_off[i] + ch * cr;
@@ -259,6 +274,7 @@ void set_pointers(srm_plan* p) {
   d.qmat = region<double>(p, I_QMAT);
   d.qscr = region<double>(p, I_QSCR);
   d.crossp = region<double>(p, I_CROSSP);
+  d.scal = region<double>(p, SRM_R_SCAL);
   d.hist = region<double>(p, SRM_R_HIST);
   d.status = region<int32_t>(p, SRM_R_STATUS);
   d.iter = d.status + 4;
@@ -309,7 +325,15 @@ std::vector<Stage> m_stages(srm_plan* p) {
                  return launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
                                           0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
                }});
-  contraction_stages(p, v);
+  v.push_back({"contract_e_xhat", [p, d](cudaStream_t st) {
+                 return launch_contract_e((int)p->kp, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
+                                          region<ItemE>(p, I_ITEMS_EX), (int)p->items_ex.size(), st);
+               }});
+  v.push_back({"reduce_chunks", [d](cudaStream_t st) { return launch_reduce_chunks(d, st); }});
+  v.push_back({"gram_from_b", [p, d](cudaStream_t st) {
+                 return launch_contract_a((int)p->kp, SRM_F64, d.bred, p->ldo, d.S, p->ldx, p->ldx, d.bred, p->ldo,
+                                          0.5, region<ItemA>(p, I_ITEMS_G), (int)p->items_g.size(), st);
+               }});
   v.push_back({"eig_polar", [d](cudaStream_t st) { return launch_eig_polar(d, 0, st); }});
   v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 1, st); }});
   v.push_back({"finalize_rho", [d](cudaStream_t st) { return launch_finalize_rho(d, 0, st); }});
@@ -407,6 +431,11 @@ int srm_plan_create(srm_plan** out, int dtype, int n_local, const int64_t* n_vox
 }
 
 int srm_plan_destroy(srm_plan* plan) {
+  if (plan) {
+    if (plan->graph_exec) cudaGraphExecDestroy(plan->graph_exec);
+    if (plan->graph) cudaGraphDestroy(plan->graph);
+    if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
+  }
   delete plan;
   return SRM_OK;
 }
@@ -452,7 +481,8 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     const void* src;
   } ups[] = {{I_SUBJ, p->subj.data()},         {I_ORDER, p->order.data()},
              {I_ORDER_LOCAL, p->order_local.data()}, {I_ITEMS_EX, p->items_ex.data()},
-             {I_ITEMS_EA, p->items_ea.data()},  {I_ITEMS_A, p->items_a.data()}};
+             {I_ITEMS_EA, p->items_ea.data()},  {I_ITEMS_A, p->items_a.data()},
+             {I_ITEMS_G, p->items_g.data()}};
   for (const Up& u : ups) {
     if (p->size[u.r] == 0) continue;
     e = cudaMemcpy(p->ws + p->off[u.r], u.src, p->size[u.r], cudaMemcpyHostToDevice);
@@ -470,6 +500,8 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     e = launch_contract_e((int)p->kp, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0, nullptr, 0, 0);
   if (e == cudaSuccess)
     e = launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp, 0.5, nullptr, 0, 0);
+  if (e == cudaSuccess)
+    e = launch_contract_a((int)p->kp, SRM_F64, d.bred, p->ldo, d.S, p->ldx, p->ldx, d.bred, p->ldo, 0.5, nullptr, 0, 0);
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
   return SRM_OK;
 }
@@ -520,6 +552,37 @@ int srm_e_step(srm_plan* p, void* stream) {
 int srm_m_step(srm_plan* p, void* stream) {
   if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
   return run_stages(m_stages(p), as_stream(stream));
+}
+
+int srm_graph_capture(srm_plan* p) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  if (p->graph_exec) return SRM_OK;
+  cudaError_t e = cudaSuccess;
+  if (!p->cap_stream) e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e, "capture stream");
+  e = cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return cuda_fail(e, "begin capture");
+  int rc = run_stages(e_stages(p), p->cap_stream);
+  if (rc == SRM_OK) rc = run_stages(m_stages(p), p->cap_stream);
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(p->cap_stream, &g);
+  if (rc != SRM_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "end capture");
+  e = cudaGraphInstantiate(&p->graph_exec, g, 0);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return cuda_fail(e, "instantiate");
+  }
+  p->graph = g;
+  return SRM_OK;
+}
+
+int srm_graph_launch(srm_plan* p, void* stream) {
+  if (!p || !p->graph_exec) return fail(SRM_ERR_CONFIG, "no captured graph");
+  return check(cudaGraphLaunch(p->graph_exec, as_stream(stream)), "graph launch");
 }
 
 int srm_profile_iteration(srm_plan* p, float* ms_out, int capacity, int* n_out, void* stream) {

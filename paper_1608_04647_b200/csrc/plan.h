@@ -56,6 +56,7 @@ struct DevPlan {
   double* qmat;      // [n_local][kp][kp]
   double* qscr;      // [n_local][kp][kp]
   double* crossp;    // [n_local][ntile_apply]
+  double* scal;      // [n_local][8]: {jacobi sweeps, ...}
   double* hist;      // [iterations][hist_stride]
   int32_t* status;
   int32_t* iter;          // device iteration counter (one graph serves every iteration)

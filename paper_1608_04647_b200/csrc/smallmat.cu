@@ -128,14 +128,29 @@ struct JacobiScratch {
 
 __device__ int rr_slot(int i, int r, int np2) { return i == 0 ? 0 : 1 + ((i - 1 + r) % (np2 - 1)); }
 
-__device__ void jacobi_eig(double* C, double* Q, int n, int ld, JacobiScratch js, int max_sweeps) {
+// Returns the number of sweeps run.  Convergence: the off-diagonal Frobenius
+// norm is at most 1e-15 of the matrix norm at the start of a sweep (eigen-
+// value errors ~1e-15 |C|).  A purely relative per-entry test can stall on
+// roundoff-level entries next to small eigenvalues; rotations on entries
+// below 1e-18 |C| are skipped as noise.
+__device__ int jacobi_eig(double* C, double* Q, int n, int ld, JacobiScratch js, int max_sweeps) {
+  __shared__ double red_scratch[32];
   const int tid = threadIdx.x;
   const int np2 = (n + 1) & ~1;
   const int npairs = np2 / 2;
-  const double tol = 1e-15;
-  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) *js.rot = 0;
-    __syncthreads();
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int a = e / n, b = e - a * n;
+      const double v = C[a * ld + b];
+      tot += v * v;
+      if (a != b) off += v * v;
+    }
+    off = block_sum<kSmallThreads>(off, red_scratch);
+    tot = block_sum<kSmallThreads>(tot, red_scratch);
+    if (!(off > 1e-30 * tot)) break;  // also stops on NaN
+    const double noise = 1e-18 * sqrt(tot);
     for (int r = 0; r < np2 - 1; ++r) {
       for (int j = tid; j < npairs; j += blockDim.x) {
         const int a = rr_slot(j, r, np2), b = rr_slot(np2 - 1 - j, r, np2);
@@ -145,7 +160,7 @@ __device__ void jacobi_eig(double* C, double* Q, int n, int ld, JacobiScratch js
           const double apq = C[pi * ld + qi];
           const double app = C[pi * ld + pi];
           const double aqq = C[qi * ld + qi];
-          if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app * aqq))) {
+          if (fabs(apq) > noise && fabs(apq) > 1e-17 * sqrt(fabs(app * aqq))) {
             const double tau = (aqq - app) / (2.0 * apq);
             double t;
             if (fabs(tau) > 1e150) {
@@ -155,7 +170,6 @@ __device__ void jacobi_eig(double* C, double* Q, int n, int ld, JacobiScratch js
             }
             c = 1.0 / sqrt(1.0 + t * t);
             s = t * c;
-            atomicAdd(js.rot, 1);
           }
         }
         js.pp[j] = pi;
@@ -192,10 +206,8 @@ __device__ void jacobi_eig(double* C, double* Q, int n, int ld, JacobiScratch js
       }
       __syncthreads();
     }
-    const int rotated = *js.rot;
-    __syncthreads();
-    if (rotated == 0) break;
   }
+  return sweep;
 }
 
 // Shared tail of the polar factor: rank check on the Gram eigenvalues and
@@ -291,7 +303,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_eig_polar(DevPlan p, int init
     __syncthreads();
   }
   JacobiScratch js{cs, sn, pp, qq, &rot};
-  jacobi_eig(C, Q, n, ld, js, 60);
+  const int sweeps = jacobi_eig(C, Q, n, ld, js, 40);
+  if (tid == 0) p.scal[(int64_t)i * 8 + 0] = (double)sweeps;
   const bool bad = polar_from_eig(C, Q, n, ld, wsh, p.mmat + (int64_t)i * kp * kp, kp, kp);
   for (int e = tid; e < kp * kp; e += blockDim.x) {
     const int a = e / kp, b = e - a * kp;
@@ -685,7 +698,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar_small(const double* g, 
   }
   __syncthreads();
   JacobiScratch js{cs, sn, pp, qq, &rot};
-  jacobi_eig(C, Q, n, ld, js, 60);
+  jacobi_eig(C, Q, n, ld, js, 40);
   const bool bad = polar_from_eig(C, Q, n, ld, wsh, m, ldm, n);
   if (bad && threadIdx.x == 0) raise_status(status, SRM_ERR_RANK, 0, -1);
 }

@@ -17,7 +17,7 @@ from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
-from . import _lib
+from . import _lib, hostio
 from .errors import ConfigError, DeviceError, from_status
 
 _MASK64 = 0xFFFFFFFFFFFFFFFF
@@ -179,12 +179,17 @@ class SrmEngine:
                     host = torch.from_numpy(np.ascontiguousarray(arr))
                 b = j % 2
                 buf = self._staging_buf(b, host.dtype, v * self.T).view(v, self.T)
-                with torch.cuda.stream(copier):
-                    if done[b] is not None:
-                        copier.wait_event(done[b])
-                    buf.copy_(host, non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(copier)
+                if done[b] is not None:
+                    copier.wait_event(done[b])
+                if host.is_pinned():
+                    with torch.cuda.stream(copier):
+                        buf.copy_(host, non_blocking=True)
+                else:
+                    # pageable memory: staged pinned chunks + threaded memcpy
+                    done[b].synchronize() if done[b] is not None else None
+                    hostio.to_device(host.numpy(), self.device, out=buf)
+                ev = torch.cuda.Event()
+                ev.record(copier)
                 main.wait_event(ev)
                 src = buf
                 ld = self.T
@@ -218,9 +223,12 @@ class SrmEngine:
                     futures[j] = None
         else:
             for j, g in enumerate(gaussians):
+                if hasattr(g, "result"):
+                    g = g.result()
                 r0 = int(self.row_off[j])
                 src = g if isinstance(g, torch.Tensor) else torch.from_numpy(np.asarray(g, np.float64))
                 amat[r0: r0 + self.n_voxels[j], : self.K].copy_(src)
+                gaussians[j] = None
         _lib.check(self.lib.srm_init_mapping(self.plan, ctypes.c_void_p(self.stream())), "init_mapping")
 
     # ------------------------------------------------------------- iteration
@@ -261,23 +269,14 @@ class SrmEngine:
         _lib.check(self.lib.srm_m_step(self.plan, st), "m_step")
 
     def capture(self):
-        """Capture {e_step, m_step} into a CUDA graph (single rank only)."""
-        torch = _torch()
+        """Record {e_step, m_step} as a native CUDA graph (single rank only)."""
         if self.world_size != 1:
             raise ConfigError("graph capture is for single-rank plans")
-        torch.cuda.synchronize(self.device)
-        g = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream(device=self.device)
-        # snapshot the iteration counter: capture enqueues nothing that runs
-        with torch.cuda.graph(g, stream=side):
-            st = ctypes.c_void_p(side.cuda_stream)
-            _lib.check(self.lib.srm_e_step(self.plan, st), "e_step(capture)")
-            _lib.check(self.lib.srm_m_step(self.plan, st), "m_step(capture)")
-        self._graph = g
-        return g
+        _lib.check(self.lib.srm_graph_capture(self.plan), "graph_capture")
+        self._graph = True
 
     def replay(self):
-        self._graph.replay()
+        _lib.check(self.lib.srm_graph_launch(self.plan, ctypes.c_void_p(self.stream())), "graph_launch")
 
     def set_iteration(self, it):
         _lib.check(self.lib.srm_set_iteration(self.plan, int(it), ctypes.c_void_p(self.stream())))

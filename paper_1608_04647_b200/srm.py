@@ -23,12 +23,15 @@ The EM iteration (srm.py:254-287) on the device:
 """
 
 import ctypes
+import os
+import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import Optional
 
 import numpy as np
 
-from . import _lib
+from . import _lib, hostio
 from .collectives import SerialCommunicator, TorchCommunicator, rank_counts
 from .data import SubjectData
 from .engine import SrmEngine, reference_gaussian
@@ -336,7 +339,7 @@ def _storage_for(subjects, storage):
 
 
 def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=True,
-        keep_on_device=False, device=None, engine_out=None):
+        keep_on_device=False, device=None, engine_out=None, timings=None):
     """Run the distributed EM; ``subjects`` are this worker's share (srm.py:216).
 
     Every worker calls this with the same config and its own communicator
@@ -349,7 +352,9 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     ``ordered`` (default: when the gathered E-step table is <= 64 MiB) sums
     subject terms in ascending global order on every rank -- bit-identical
     results for any shard layout; otherwise per-rank sums are all-reduced.
+    ``timings`` (a dict) receives per-phase wall seconds (synchronising).
     """
+    clock = _PhaseClock(timings)
     config.validate()
     if not subjects:
         raise ConfigError("each worker needs at least one subject")
@@ -380,8 +385,16 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
                     device=device)
     if engine_out is not None:
         engine_out.append(eng)
+    # the init draws depend only on (seed, global index, V, k): overlap them with the upload
+    pool = ThreadPoolExecutor(max(1, min(os.cpu_count() or 1, len(subjects))))
+    draws = [pool.submit(reference_gaussian, int(s.X.shape[0]), k, config.seed, offset + j)
+             for j, s in enumerate(subjects)]
+    clock.tick("setup")
     eng.load([s.X for s in subjects])
-    eng.init_mapping(config.seed, offset)
+    clock.tick("load")
+    eng.init_mapping(config.seed, offset, gaussians=draws)
+    pool.shutdown(wait=False)
+    clock.tick("init")
 
     use_graph = graphs and comm.size == 1
     n_done = 0
@@ -401,9 +414,27 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
                 sprev = float(row[_lib.H_SPREV].item())
                 if sdiff / max(sprev, 1e-300) < config.tolerance:
                     break
+    clock.tick("em")
     eng.finalize()
     eng.raise_status()
-    return _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device)
+    clock.tick("finalize")
+    model = _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device)
+    clock.tick("collect")
+    return model
+
+
+class _PhaseClock:
+    def __init__(self, out):
+        self.out = out
+        self.t = time.perf_counter()
+
+    def tick(self, name):
+        if self.out is None:
+            return
+        _torch().cuda.synchronize()
+        now = time.perf_counter()
+        self.out[name] = self.out.get(name, 0.0) + now - self.t
+        self.t = now
 
 
 def _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device):
@@ -438,8 +469,8 @@ def _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device):
         S = eng.S.clone()
         sigma = eng.sigma.clone()
     else:
-        wout = eng.wout.cpu().numpy()
-        muh = eng.mu.cpu().numpy()
+        wout = hostio.to_host(eng.wout)
+        muh = hostio.to_host(eng.mu)
         W = [np.ascontiguousarray(wout[eng.subject_rows(j)]) for j in range(eng.n_local)]
         mu = [muh[eng.subject_rows(j)].copy() for j in range(eng.n_local)]
         S = np.ascontiguousarray(eng.S.cpu().numpy())
