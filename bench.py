@@ -7,7 +7,9 @@
 A *step* is one EM iteration over every subject of the workload (srm.py:254-287:
 E-step reduction, K x K tail, M-step over all subjects).  ``value`` is the
 whole-job subject*voxel*TR/s per iteration with X already resident in HBM,
-timed with CUDA events over exactly K steps (max over ranks); ``e2e`` is the
+timed with CUDA events over a K-step fit (max over ranks): the one-time Gram
+precompute (when that path is chosen) and the final W are inside the timed
+region, demean and the reference initialisation are not; ``e2e`` is the
 same metric through the public API ``srm.fit`` on pinned host arrays, host to
 device copies, the reference initialisation and the read-back of the model
 included.  The default workload is BASELINE config 2 (40 subjects x 30,000
@@ -42,7 +44,7 @@ FALLBACK_HBM_GBS = 6650.0
 def parse_args():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
@@ -51,6 +53,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--algorithm", default="auto", choices=["auto", "stream", "gram"])
     return ap.parse_args()
 
 
@@ -261,32 +264,51 @@ def run_ours(args):
                             dtype=cfg["dtype"], first_subject=start, count=n_local, device=dev)
     torch.cuda.synchronize()
 
-    # ---------------- value: X resident in HBM, K timed EM iterations ---------
-    total_iters = args.warmup + args.steps + 8
+    # ---------------- value: X resident in HBM, a K-iteration fit timed --------
+    # The timed region is everything a fit does after demean + init (the
+    # reference's per-iteration accounting also excludes those): the Gram
+    # precompute when the Gram path is chosen, K EM iterations, and the final
+    # W_i = A_i M_i.  One-time work is therefore charged to the K steps.
+    algo = args.algorithm
+    if algo == "auto":
+        algo = srm.choose_algorithm([V] * cfg["n_subjects"], T, K, args.steps,
+                                    torch.cuda.mem_get_info(dev)[0] * world)
+    total_iters = max(args.warmup, args.steps) + 8
     eng = SrmEngine([V] * n_local, T, K, total_iters, storage=cfg["dtype"], world_size=world, rank=rank,
-                    counts=counts, ordered=True, device=dev)
+                    counts=counts, ordered=True, gram=(algo == "gram"), device=dev)
     eng.load(xs)
-    eng.init_mapping(args.seed, start)
     use_graph = world == 1
-    eng.step(comm)  # iteration 0 eagerly (configures kernels), then graph replays
-    if use_graph:
-        eng.capture()
-    for _ in range(max(0, args.warmup - 1)):
-        eng.replay() if use_graph else eng.step(comm)
+
+    def schedule(n_iter, timed_events=None):
+        if timed_events:
+            timed_events[0].record(torch.cuda.current_stream())
+        eng.prepare_gram()
+        for it in range(n_iter):
+            if use_graph and eng._graph is not None:
+                eng.replay()
+            else:
+                eng.step(comm)
+                if use_graph and it == 0:
+                    eng.capture()
+        eng.finalize()
+        if timed_events:
+            timed_events[1].record(torch.cuda.current_stream())
+
+    eng.init_mapping(args.seed, start)
+    schedule(max(1, args.warmup))          # warm-up fit: configures kernels, captures the graph
+    eng.raise_status()
+    eng.reset()
+    eng.init_mapping(args.seed, start)     # fresh EM start (untimed, like the reference's init)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.2)
-    stream = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(args.steps):
-        eng.replay() if use_graph else eng.step(comm)
-    e1.record(stream)
+    schedule(args.steps, (e0, e1))
     torch.cuda.synchronize()
     clocks = sampler.stop()
     if world > 1:
@@ -299,45 +321,77 @@ def run_ours(args):
     eng.raise_status()
     units = cfg["n_subjects"] * V * T
     value = units / (ms / 1e3)
-    launches = eng.launches_per_iteration * args.steps
+    n_gram_launches = 2 if algo == "gram" else 0
+    n_final = 2 if algo == "gram" else 1
+    launches = eng.launches_per_iteration * args.steps + n_gram_launches + n_final
 
-    # per-kernel durations (CUDA events on the launch stream, eager iterations)
-    prof = {}
+    # per-kernel durations (CUDA events on the launch stream, untimed pass)
+    st = torch.cuda.current_stream()
+    prof_iter = {}
     for _ in range(5):
         for name, t_ms in eng.profile_iteration():
-            prof.setdefault(name, []).append(t_ms)
-    prof = {k_: float(np.mean(v_)) for k_, v_ in prof.items()}
+            prof_iter.setdefault(name, []).append(t_ms)
+    prof_iter = {k_: float(np.mean(v_)) for k_, v_ in prof_iter.items()}
+    once = {}
+    for name, fn in (("gram_xtx", eng.prepare_gram), ("finalize", eng.finalize)):
+        if name == "gram_xtx" and algo != "gram":
+            continue
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(st)
+        fn()
+        a1.record(st)
+        torch.cuda.synchronize()
+        once[name] = a0.elapsed_time(a1)
     eng.raise_status()
     del eng
     torch.cuda.empty_cache()
 
+    # time share of each kernel inside the timed region (K iterations + one-time work)
+    region_ms = {k_: v_ * args.steps for k_, v_ in prof_iter.items()}
+    region_ms.update(once)
+    tot = sum(region_ms.values())
+    step_share = {k_: v_ / tot for k_, v_ in region_ms.items()}
+    dom = max(region_ms, key=region_ms.get)
     hbm_peak, peak_src = peaks()
-    stream_kernels = {k_: v_ for k_, v_ in prof.items() if k_ in ("contract_a", "contract_e_xhat")}
-    dom = max(stream_kernels, key=stream_kernels.get)
     local_units = n_local * V * T
-    alg_bytes = local_units * b          # one pass over X-hat (b bytes per unit per pass)
-    alg_flops = 2.0 * local_units * K    # 2K flops per unit per pass
-    achieved = alg_bytes / (prof[dom] / 1e3) / 1e9
+    ldx = -(-T // 32) * 32
+    if dom == "gram_xtx":
+        launch_ms = once["gram_xtx"]
+        alg_flops = float(n_local) * V * T * (T + 1)          # symmetric X^T X: T(T+1)/2 dots of length V
+        alg_bytes = float(local_units * b)                      # X-hat read once
+    elif dom == "finalize":
+        launch_ms = once["finalize"]
+        alg_flops = 2.0 * local_units * K
+        alg_bytes = float(local_units * b)
+    else:
+        launch_ms = prof_iter[dom]
+        if dom in ("contract_a", "contract_e_xhat"):
+            alg_flops = 2.0 * local_units * K                   # one pass: 2K flops per unit
+            alg_bytes = float(local_units * b)                  # b bytes per unit per pass
+        else:
+            alg_flops = 2.0 * n_local * K * T * T
+            alg_bytes = float(n_local * T * T * 8)
+    achieved_tf = alg_flops / (launch_ms / 1e3) / 1e12
+    achieved_gbs = alg_bytes / (launch_ms / 1e3) / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get(args.config, {}).get(dom)
+            traffic = json.loads(tfile.read_text()).get(f"{args.config}:{algo}", {}).get(dom)
         except Exception:  # noqa: BLE001
             traffic = None
     roofline = {
-        "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-        "traffic": traffic, "kernel": dom, "launch_ms": prof[dom],
-        "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
-        "note": "fp64 X-hat: the kernel is bound by the FP64 tensor pipe (see compute_roofline)",
+        "bound": "tensor", "achieved": achieved_tf, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+        "frac": achieved_tf / DMMA_PEAK_TFLOPS, "traffic": traffic, "kernel": dom, "launch_ms": launch_ms,
+        "algorithmic_flops_per_launch": alg_flops, "algorithmic_bytes_per_launch": alg_bytes,
+        "peak_source": ("FP64 tensor pipe (mma.sync.m8n8k4.f64 = SASS DMMA) measured on this pool by "
+                        "tools/fp64_peak.cu (37.1 TF/s); the path computes in fp64 like the reference, "
+                        "so the bf16 figure of MEASURED_PEAKS.json does not apply"),
     }
-    compute_roofline = {
-        "bound": "fp64 tensor (DMMA)", "achieved": alg_flops / (prof[dom] / 1e3) / 1e12,
-        "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-        "frac": alg_flops / (prof[dom] / 1e3) / 1e12 / DMMA_PEAK_TFLOPS,
-        "peak_source": "tools/fp64_peak.cu: mma.sync.m8n8k4.f64 loop, 148 CTAs x 256 threads, measured on this pool",
-    }
-    step_share = {k_: v_ / sum(prof.values()) for k_, v_ in prof.items()}
+    hbm_roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved_gbs / hbm_peak, "kernel": dom, "peak_source": peak_src}
+    prof = {"per_iteration_ms": prof_iter, "one_time_ms": once}
 
     # ---------------- e2e: public API, pinned host inputs ---------------------
     e2e = None
@@ -347,14 +401,14 @@ def run_ours(args):
         torch.cuda.empty_cache()
         subjects = [SubjectData(f"sub-{start + j:04d}", host[j]) for j in range(n_local)]
         conf = srm.SrmConfig(k=K, iterations=cfg["iterations"], seed=args.seed)
-        srm.fit(subjects, conf, comm)  # warm-up (allocator, kernels)
+        srm.fit(subjects, conf, comm, algorithm=args.algorithm)  # warm-up (allocator, kernels)
         times = []
         for _ in range(max(1, args.e2e_fits)):
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            model = srm.fit(subjects, conf, comm)
+            model = srm.fit(subjects, conf, comm, algorithm=args.algorithm)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             if world > 1:
@@ -382,7 +436,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic: BASELINE generative recipe (seeded, device Philox stream); reference init",
             "config": config_json(cfg, args.config, world),
-            "roofline": roofline, "compute_roofline": compute_roofline,
+            "roofline": roofline, "hbm_roofline": hbm_roofline, "algorithm": algo,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "kernel_ms": prof, "kernel_share": step_share, "impl": "ours",
         }

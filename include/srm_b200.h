@@ -140,6 +140,14 @@ int srm_load_subject(srm_plan* plan, int local_index, const void* x, int x_dtype
                      int64_t ld, void* stream);
 int srm_finish_load(srm_plan* plan, void* stream);
 int srm_init_mapping(srm_plan* plan, void* stream);
+/* SRM_FLAG_GRAM plans: G_i = Xhat_i^T Xhat_i (T x T, fp64) for every local
+ * subject, after srm_load_subject.  The per-iteration M-step then needs
+ * B_i = A_i^T Xhat_i = S G_i / 2 and A_i^T A_i = B_i S^T / 2 only; A_i itself is
+ * formed once in srm_finalize.  No-op for streaming plans. */
+int srm_prepare_gram(srm_plan* plan, void* stream);
+/* restart the EM state (Sigma_s = I, status cleared, iteration 0); the next
+ * srm_init_mapping draws a fresh start (used to time repeated fits) */
+int srm_reset(srm_plan* plan, void* stream);
 
 /* ---- per-iteration work (srm.py:254-287) -----------------------------------
  * The iteration index lives in a device counter (set to 0 by

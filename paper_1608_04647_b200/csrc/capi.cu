@@ -56,6 +56,9 @@ enum Internal {
   I_ITEMS_EA,
   I_ITEMS_A,
   I_ITEMS_G,
+  I_ST,
+  I_ITEMS_GRAM,
+  I_ITEMS_BG,
   I_COUNT
 };
 
@@ -81,7 +84,7 @@ struct srm_plan {
   int64_t chunk_rows = 0;
   std::vector<int64_t> chunk0, nchunk;
   int64_t chunks_total = 0;
-  std::vector<ItemE> items_ex, items_ea;
+  std::vector<ItemE> items_ex, items_ea, items_gram, items_bg;
   std::vector<ItemA> items_a, items_g;
   std::vector<int64_t> subj;
   std::vector<int32_t> order, order_local;
@@ -120,7 +123,7 @@ void layout(srm_plan* p) {
   sz[SRM_R_STATUS] = 32;  // status word + iteration counter
   sz[SRM_R_MMAT] = (int64_t)p->n_local * kp2 * 8;
   sz[SRM_R_SCAL] = (int64_t)p->n_local * 8 * 8;
-  sz[SRM_R_GRAM] = 0;
+  sz[SRM_R_GRAM] = (p->flags & SRM_FLAG_GRAM) ? (int64_t)p->n_local * p->ldx * p->ldx * 8 : 0;
   sz[SRM_R_VAR] = kp2 * 8;
   sz[I_ROWSQ] = p->rows_total * 8;
   sz[I_CMAT] = kp2 * 8;
@@ -139,6 +142,9 @@ void layout(srm_plan* p) {
   sz[I_ITEMS_EA] = (int64_t)p->items_ea.size() * sizeof(ItemE);
   sz[I_ITEMS_A] = (int64_t)p->items_a.size() * sizeof(ItemA);
   sz[I_ITEMS_G] = (int64_t)p->items_g.size() * sizeof(ItemA);
+  sz[I_ST] = p->ldx * p->kp * 8;
+  sz[I_ITEMS_GRAM] = (int64_t)p->items_gram.size() * sizeof(ItemE);
+  sz[I_ITEMS_BG] = (int64_t)p->items_bg.size() * sizeof(ItemE);
   int64_t cur = 0;
   for (int r = 0; r < I_COUNT; ++r) {
     p->off[r] = cur;
@@ -209,6 +215,8 @@ void build_work(srm_plan* p) {
         it.o_off = obase + n0;
         it.rows = (int32_t)rows;
         it.ncols = (int32_t)std::min<int64_t>(128, p->ldx - n0);
+        it.mrows = (int32_t)p->kp;
+        it.pad = 0;
         p->items_ex.push_back(it);
       }
       ItemE ia;
@@ -217,6 +225,8 @@ void build_work(srm_plan* p) {
       ia.o_off = obase + p->ldx;
       ia.rows = (int32_t)rows;
       ia.ncols = (int32_t)p->kp;
+      ia.mrows = (int32_t)p->kp;
+      ia.pad = 0;
       p->items_ea.push_back(ia);
     }
     for (int64_t r = 0; r < p->V[i]; r += 128) {
@@ -226,6 +236,37 @@ void build_work(srm_plan* p) {
       it.rows = (int32_t)std::min<int64_t>(128, p->V[i] - r);
       it.pad = i;
       p->items_a.push_back(it);
+    }
+  }
+  // Gram path: one-time X_i^T X_i (upper 128 x 128 tiles) and per-iteration B_i = S G_i / 2
+  p->items_gram.clear();
+  p->items_bg.clear();
+  if (p->flags & SRM_FLAG_GRAM) {
+    for (int i = 0; i < p->n_local; ++i) {
+      for (int64_t m0 = 0; m0 < p->ldx; m0 += 128) {
+        for (int64_t n0 = m0; n0 < p->ldx; n0 += 128) {
+          ItemE it;
+          it.l_off = p->row_off[i] * p->ldx + m0;
+          it.r_off = p->row_off[i] * p->ldx + n0;
+          it.o_off = (int64_t)i * p->ldx * p->ldx + m0 * p->ldx + n0;
+          it.rows = (int32_t)p->V[i];
+          it.ncols = (int32_t)std::min<int64_t>(128, p->ldx - n0);
+          it.mrows = (int32_t)std::min<int64_t>(128, p->ldx - m0);
+          it.pad = 0;
+          p->items_gram.push_back(it);
+        }
+      }
+      for (int64_t n0 = 0; n0 < p->ldx; n0 += 128) {
+        ItemE it;
+        it.l_off = 0;
+        it.r_off = (int64_t)i * p->ldx * p->ldx + n0;
+        it.o_off = (int64_t)i * p->kp * p->ldo + n0;
+        it.rows = (int32_t)p->ldx;
+        it.ncols = (int32_t)std::min<int64_t>(128, p->ldx - n0);
+        it.mrows = (int32_t)p->kp;
+        it.pad = 0;
+        p->items_bg.push_back(it);
+      }
     }
   }
   // subject table
@@ -275,6 +316,8 @@ void set_pointers(srm_plan* p) {
   d.qscr = region<double>(p, I_QSCR);
   d.crossp = region<double>(p, I_CROSSP);
   d.scal = region<double>(p, SRM_R_SCAL);
+  d.st = region<double>(p, I_ST);
+  d.gram = p->size[SRM_R_GRAM] ? region<double>(p, SRM_R_GRAM) : nullptr;
   d.hist = region<double>(p, SRM_R_HIST);
   d.status = region<int32_t>(p, SRM_R_STATUS);
   d.iter = d.status + 4;
@@ -295,11 +338,11 @@ struct Stage {
 void contraction_stages(srm_plan* p, std::vector<Stage>& out) {
   const DevPlan& d = p->dp;
   out.push_back({"contract_e_xhat", [p, d](cudaStream_t st) {
-                   return launch_contract_e((int)p->kp, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
+                   return launch_contract_e((int)p->kp, SRM_F64, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
                                             region<ItemE>(p, I_ITEMS_EX), (int)p->items_ex.size(), st);
                  }});
   out.push_back({"contract_e_gram", [p, d](cudaStream_t st) {
-                   return launch_contract_e((int)p->kp, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0,
+                   return launch_contract_e((int)p->kp, SRM_F64, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0,
                                             region<ItemE>(p, I_ITEMS_EA), (int)p->items_ea.size(), st);
                  }});
   out.push_back({"reduce_chunks", [d](cudaStream_t st) { return launch_reduce_chunks(d, st); }});
@@ -321,12 +364,28 @@ std::vector<Stage> e_stages(srm_plan* p) {
 std::vector<Stage> m_stages(srm_plan* p) {
   const DevPlan& d = p->dp;
   std::vector<Stage> v;
+  if (p->flags & SRM_FLAG_GRAM) {
+    // B_i = S G_i / 2 straight into the reduced slot (G_i = X_i^T X_i, one-time)
+    v.push_back({"gram_b", [p, d](cudaStream_t st) {
+                   return launch_contract_e((int)p->kp, SRM_F64, SRM_F64, d.st, p->kp, d.gram, p->ldx, d.bred, p->ldo,
+                                            0.5, region<ItemE>(p, I_ITEMS_BG), (int)p->items_bg.size(), st);
+                 }});
+    v.push_back({"gram_from_b", [p, d](cudaStream_t st) {
+                   return launch_contract_a((int)p->kp, SRM_F64, d.bred, p->ldo, d.S, p->ldx, p->ldx, d.bred, p->ldo,
+                                            0.5, region<ItemA>(p, I_ITEMS_G), (int)p->items_g.size(), st);
+                 }});
+    v.push_back({"eig_polar", [d](cudaStream_t st) { return launch_eig_polar(d, 0, st); }});
+    v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 1, st); }});
+    v.push_back({"finalize_rho", [d](cudaStream_t st) { return launch_finalize_rho(d, 0, st); }});
+    v.push_back({"advance_iteration", [d](cudaStream_t st) { return launch_set_iteration(d, 0, 1, st); }});
+    return v;
+  }
   v.push_back({"contract_a", [p, d](cudaStream_t st) {
                  return launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
                                           0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
                }});
   v.push_back({"contract_e_xhat", [p, d](cudaStream_t st) {
-                 return launch_contract_e((int)p->kp, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
+                 return launch_contract_e((int)p->kp, SRM_F64, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
                                           region<ItemE>(p, I_ITEMS_EX), (int)p->items_ex.size(), st);
                }});
   v.push_back({"reduce_chunks", [d](cudaStream_t st) { return launch_reduce_chunks(d, st); }});
@@ -482,7 +541,8 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
   } ups[] = {{I_SUBJ, p->subj.data()},         {I_ORDER, p->order.data()},
              {I_ORDER_LOCAL, p->order_local.data()}, {I_ITEMS_EX, p->items_ex.data()},
              {I_ITEMS_EA, p->items_ea.data()},  {I_ITEMS_A, p->items_a.data()},
-             {I_ITEMS_G, p->items_g.data()}};
+             {I_ITEMS_G, p->items_g.data()},     {I_ITEMS_GRAM, p->items_gram.data()},
+             {I_ITEMS_BG, p->items_bg.data()}};
   for (const Up& u : ups) {
     if (p->size[u.r] == 0) continue;
     e = cudaMemcpy(p->ws + p->off[u.r], u.src, p->size[u.r], cudaMemcpyHostToDevice);
@@ -495,13 +555,15 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
   if (e != cudaSuccess) return cuda_fail(e, "bind sigma");
   // warm up kernel attributes outside any graph capture
   const DevPlan& d = p->dp;
-  e = launch_contract_e((int)p->kp, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0, nullptr, 0, 0);
+  e = launch_contract_e((int)p->kp, SRM_F64, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0, nullptr, 0, 0);
   if (e == cudaSuccess)
-    e = launch_contract_e((int)p->kp, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0, nullptr, 0, 0);
+    e = launch_contract_e((int)p->kp, SRM_F64, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0, nullptr, 0, 0);
   if (e == cudaSuccess)
     e = launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp, 0.5, nullptr, 0, 0);
   if (e == cudaSuccess)
     e = launch_contract_a((int)p->kp, SRM_F64, d.bred, p->ldo, d.S, p->ldx, p->ldx, d.bred, p->ldo, 0.5, nullptr, 0, 0);
+  if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM))
+    e = launch_contract_e(128, p->dtype, p->dtype, d.xhat, p->ldx, d.xhat, p->ldx, d.gram, p->ldx, 1.0, nullptr, 0, 0);
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
   return SRM_OK;
 }
@@ -622,8 +684,30 @@ const char* srm_profile_name(int index) {
 
 int srm_finalize(srm_plan* p, void* stream) {
   if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
-  return check(launch_apply_w(p->dp, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), as_stream(stream)),
-               "finalize");
+  cudaStream_t st = as_stream(stream);
+  const DevPlan& d = p->dp;
+  if (p->flags & SRM_FLAG_GRAM) {  // A_i = Xhat_i S^T / 2 is not kept per iteration on the Gram path
+    cudaError_t e = launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
+                                      0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
+    if (e != cudaSuccess) return cuda_fail(e, "finalize contract_a");
+  }
+  return check(launch_apply_w(d, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st), "finalize");
+}
+
+int srm_prepare_gram(srm_plan* p, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  if (!(p->flags & SRM_FLAG_GRAM)) return SRM_OK;
+  cudaStream_t st = as_stream(stream);
+  const DevPlan& d = p->dp;
+  cudaError_t e = launch_contract_e(128, p->dtype, p->dtype, d.xhat, p->ldx, d.xhat, p->ldx, d.gram, p->ldx, 1.0,
+                                    region<ItemE>(p, I_ITEMS_GRAM), (int)p->items_gram.size(), st);
+  if (e == cudaSuccess) e = launch_mirror_gram(d, st);
+  return check(e, "prepare_gram");
+}
+
+int srm_reset(srm_plan* p, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  return check(launch_reset(p->dp, as_stream(stream)), "reset");
 }
 
 int srm_read_status(srm_plan* p, int32_t* out4) {

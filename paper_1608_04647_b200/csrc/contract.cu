@@ -32,15 +32,21 @@ __host__ __device__ constexpr int pad4mod16(int n) { return n + ((4 - n) % 16 + 
 template <typename T>
 __host__ __device__ constexpr int e_r_stride() { return sizeof(T) == 8 ? kTileN + 4 : kTileN + 8; }
 
-template <int KP, typename TR>
-constexpr int e_stage_bytes() {
-  return kBC * (pad4mod16(KP) * 8 + e_r_stride<TR>() * (int)sizeof(TR));
+// L-tile row stride: doubles == 4 mod 16, floats == 8 mod 32 (conflict-free fragments)
+template <int KP, typename TL>
+__host__ __device__ constexpr int e_l_stride() {
+  return sizeof(TL) == 8 ? pad4mod16(KP) : KP + ((8 - KP) % 32 + 32) % 32;
 }
 
-template <int KP, typename TR>
+template <int KP, typename TL, typename TR>
+constexpr int e_stage_bytes() {
+  return kBC * (e_l_stride<KP, TL>() * (int)sizeof(TL) + e_r_stride<TR>() * (int)sizeof(TR));
+}
+
+template <int KP, typename TL, typename TR>
 constexpr int e_stages() {
-  return (kSmemBudget / e_stage_bytes<KP, TR>()) >= 4 ? 4
-         : (kSmemBudget / e_stage_bytes<KP, TR>()) >= 3 ? 3 : 2;
+  return (kSmemBudget / e_stage_bytes<KP, TL, TR>()) >= 4 ? 4
+         : (kSmemBudget / e_stage_bytes<KP, TL, TR>()) >= 3 ? 3 : 2;
 }
 
 constexpr int kAStride = 20;  // == 4 mod 16 doubles; conflict-free for floats too
@@ -63,25 +69,26 @@ __device__ __forceinline__ void store2(double* p, double a, double b) {
 // ---------------------------------------------------------------------------
 // V-contraction
 // ---------------------------------------------------------------------------
-template <int KP, typename TR, int STAGES>
-__global__ void __launch_bounds__(kThreads) k_contract_e(const double* __restrict__ L, int64_t ldl,
+template <int KP, typename TL, typename TR, int STAGES>
+__global__ void __launch_bounds__(kThreads) k_contract_e(const TL* __restrict__ L, int64_t ldl,
                                                          const TR* __restrict__ R, int64_t ldr,
                                                          double* __restrict__ out, int64_t ldo,
                                                          double alpha,
                                                          const ItemE* __restrict__ items) {
-  constexpr int SL = pad4mod16(KP);
+  constexpr int SL = e_l_stride<KP, TL>();
   constexpr int SR = e_r_stride<TR>();
   constexpr int MT = KP / 8;
   constexpr int EPC = 16 / (int)sizeof(TR);  // elements per 16-byte chunk
-  constexpr int LCH = KP / 2;                // 16-byte chunks per L row
+  constexpr int LEPC = 16 / (int)sizeof(TL);
+  constexpr int LCH = KP / LEPC;             // 16-byte chunks per L row
   constexpr int RCH = kTileN / EPC;          // 16-byte chunks per R row
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* Ls = reinterpret_cast<double*>(smem_raw);
-  TR* Rs = reinterpret_cast<TR*>(smem_raw + STAGES * kBC * SL * 8);
+  TL* Ls = reinterpret_cast<TL*>(smem_raw);
+  TR* Rs = reinterpret_cast<TR*>(smem_raw + STAGES * kBC * SL * (int)sizeof(TL));
 
   const ItemE it = items[blockIdx.x];
-  const double* Lb = L + it.l_off;
+  const TL* Lb = L + it.l_off;
   const TR* Rb = R + it.r_off;
   const int rows = it.rows;
   const int ncols = it.ncols;
@@ -92,9 +99,9 @@ __global__ void __launch_bounds__(kThreads) k_contract_e(const double* __restric
 
   auto load_stage = [&](int s, int buf) {
     const int r0 = s * kBC;
-    double* ld = Ls + buf * kBC * SL;
+    TL* ld = Ls + buf * kBC * SL;
     for (int i = tid; i < kBC * LCH; i += kThreads) {
-      const int r = i / LCH, c = (i - r * LCH) * 2;
+      const int r = i / LCH, c = (i - r * LCH) * LEPC;
       const bool ok = (r0 + r) < rows;
       cp_async16(ld + r * SL + c, Lb + (int64_t)(ok ? r0 + r : 0) * ldl + c, ok);
     }
@@ -129,7 +136,7 @@ __global__ void __launch_bounds__(kThreads) k_contract_e(const double* __restric
       cp_async_commit();
     }
     const int buf = s % STAGES;
-    const double* Lt = Ls + buf * kBC * SL;
+    const TL* Lt = Ls + buf * kBC * SL;
     const TR* Rt = Rs + buf * kBC * SR;
 #pragma unroll
     for (int kk = 0; kk < kBC; kk += 4) {
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(kThreads) k_contract_e(const double* __restric
       const double b1 = to_f64(Rt[cr * SR + ncol + 8]);
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
-        const double a = Lt[cr * SL + m * 8 + (lane >> 2)];
+        const double a = to_f64(Lt[cr * SL + m * 8 + (lane >> 2)]);
         dmma(acc[m][0][0], acc[m][0][1], a, b0);
         dmma(acc[m][1][0], acc[m][1][1], a, b1);
       }
@@ -147,13 +154,14 @@ __global__ void __launch_bounds__(kThreads) k_contract_e(const double* __restric
   cp_async_wait<0>();
 
   double* ob = out + it.o_off;
+  const int mrows = it.mrows;
 #pragma unroll
   for (int m = 0; m < MT; ++m) {
     const int row = m * 8 + (lane >> 2);
 #pragma unroll
     for (int n = 0; n < 2; ++n) {
       const int col = warp * 16 + n * 8 + 2 * (lane & 3);
-      if (col < ncols) store2(ob + (int64_t)row * ldo + col, alpha * acc[m][n][0], alpha * acc[m][n][1]);
+      if (col < ncols && row < mrows) store2(ob + (int64_t)row * ldo + col, alpha * acc[m][n][0], alpha * acc[m][n][1]);
     }
   }
 }
@@ -254,12 +262,12 @@ __global__ void __launch_bounds__(kThreads) k_contract_a(const TX* __restrict__ 
   }
 }
 
-template <int KP, typename TR>
-cudaError_t run_e(const double* L, int64_t ldl, const TR* R, int64_t ldr, double* out, int64_t ldo,
+template <int KP, typename TL, typename TR>
+cudaError_t run_e(const TL* L, int64_t ldl, const TR* R, int64_t ldr, double* out, int64_t ldo,
                   double alpha, const ItemE* items, int n_items, cudaStream_t stream) {
-  constexpr int ST = e_stages<KP, TR>();
-  constexpr int bytes = ST * e_stage_bytes<KP, TR>();
-  auto kern = k_contract_e<KP, TR, ST>;
+  constexpr int ST = e_stages<KP, TL, TR>();
+  constexpr int bytes = ST * e_stage_bytes<KP, TL, TR>();
+  auto kern = k_contract_e<KP, TL, TR, ST>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -296,16 +304,22 @@ bool contract_kp_supported(int kp) { return kp >= 8 && kp <= 128 && kp % 8 == 0;
 #define SRM_KP_CASES(F) \
   F(8) F(16) F(24) F(32) F(40) F(48) F(56) F(64) F(72) F(80) F(88) F(96) F(104) F(112) F(120) F(128)
 
-cudaError_t launch_contract_e(int kp, int r_dtype, const double* L, int64_t ldl, const void* R,
+cudaError_t launch_contract_e(int kp, int l_dtype, int r_dtype, const void* L, int64_t ldl, const void* R,
                               int64_t ldr, double* out, int64_t ldo, double alpha,
                               const ItemE* items, int n_items, cudaStream_t stream) {
-#define CASE_E(K)                                                                              \
-  case K:                                                                                      \
-    return r_dtype == SRM_F64                                                                  \
-               ? run_e<K, double>(L, ldl, static_cast<const double*>(R), ldr, out, ldo, alpha, \
-                                  items, n_items, stream)                                      \
-               : run_e<K, float>(L, ldl, static_cast<const float*>(R), ldr, out, ldo, alpha,   \
-                                 items, n_items, stream);
+  if (l_dtype == SRM_F32 && r_dtype == SRM_F64) return cudaErrorInvalidValue;
+#define CASE_E(K)                                                                                  \
+  case K:                                                                                          \
+    if (l_dtype == SRM_F64 && r_dtype == SRM_F64)                                                  \
+      return run_e<K, double, double>(static_cast<const double*>(L), ldl,                          \
+                                      static_cast<const double*>(R), ldr, out, ldo, alpha, items,  \
+                                      n_items, stream);                                            \
+    if (l_dtype == SRM_F64)                                                                        \
+      return run_e<K, double, float>(static_cast<const double*>(L), ldl,                           \
+                                     static_cast<const float*>(R), ldr, out, ldo, alpha, items,    \
+                                     n_items, stream);                                             \
+    return run_e<K, float, float>(static_cast<const float*>(L), ldl, static_cast<const float*>(R), \
+                                  ldr, out, ldo, alpha, items, n_items, stream);
   switch (kp) {
     SRM_KP_CASES(CASE_E)
     default:

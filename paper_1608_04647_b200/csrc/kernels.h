@@ -15,6 +15,8 @@ struct ItemE {
   int64_t o_off;  // out(0, n0)
   int32_t rows;   // contraction rows in this chunk
   int32_t ncols;  // valid output columns (<= 128)
+  int32_t mrows;  // valid output rows (<= KP)
+  int32_t pad;
 };
 
 // One CTA of the T-contraction kernel: out[r][f] = alpha sum_t X[r][t] S[f][t]
@@ -26,8 +28,8 @@ struct ItemA {
   int32_t pad;
 };
 
-// V-contraction: dtype of R (X-hat or f64); L is always f64.
-cudaError_t launch_contract_e(int kp, int r_dtype, const double* L, int64_t ldl, const void* R,
+// V-contraction; L and R are f64 or f32 (X-hat), (f32, f64) is not instantiated.
+cudaError_t launch_contract_e(int kp, int l_dtype, int r_dtype, const void* L, int64_t ldl, const void* R,
                               int64_t ldr, double* out, int64_t ldo, double alpha,
                               const ItemE* items, int n_items, cudaStream_t stream);
 

@@ -57,6 +57,8 @@ struct DevPlan {
   double* qscr;      // [n_local][kp][kp]
   double* crossp;    // [n_local][ntile_apply]
   double* scal;      // [n_local][8]: {jacobi sweeps, ...}
+  double* st;        // [ldx][kp]: S^T (Gram path operand)
+  double* gram;      // [n_local][ldx][ldx]: X_i^T X_i (Gram path)
   double* hist;      // [iterations][hist_stride]
   int32_t* status;
   int32_t* iter;          // device iteration counter (one graph serves every iteration)
@@ -79,6 +81,8 @@ cudaError_t launch_tail(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_sigma(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_mirror_gram(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_reset(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_apply_w(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);
 
 // stateless helpers

@@ -564,6 +564,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_s(DevPlan p) {
     }
     quad += Rt[f * 32 + col] * y;
     St[f * 32 + col] = s;
+    if (tin && p.st) p.st[t * kp + f] = s;
     if (tin) {
       double* sp = p.S + (int64_t)f * p.ldx + t;
       const double old = *sp;
@@ -632,6 +633,30 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_sigma(DevPlan p) {
     h[SRM_H_SDIFF] = sqrt(dsq);
     h[SRM_H_SPREV] = sqrt(osq);
     p.tailscr[TS_TRACE] = trace;
+  }
+}
+
+// mirror the upper 128-tiles of every X_i^T X_i into the lower ones
+__global__ void k_mirror_gram(DevPlan p) {
+  const int64_t n = p.ldx * p.ldx;
+  double* g = p.gram + (int64_t)blockIdx.y * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = e / p.ldx, b = e - a * p.ldx;
+    if ((a >> 7) > (b >> 7)) g[e] = g[b * p.ldx + a];
+  }
+}
+
+// restart the EM state: Sigma_s = I (srm.py:248), clear the status word and
+// the iteration counter
+__global__ void k_reset(DevPlan p) {
+  const int kp = (int)p.kp;
+  for (int e = threadIdx.x; e < kp * kp; e += blockDim.x) {
+    const int a = e / kp, b = e - a * kp;
+    p.sigma[e] = (a == b && a < p.K) ? 1.0 : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    p.status[0] = p.status[1] = p.status[2] = 0;
+    *p.iter = 0;
   }
 }
 
@@ -845,6 +870,17 @@ cudaError_t launch_tail(const DevPlan& p, cudaStream_t s) {
   if (e == cudaSuccess) e = launch_tail_s(p, s);
   if (e == cudaSuccess) e = launch_tail_sigma(p, s);
   return e;
+}
+
+cudaError_t launch_mirror_gram(const DevPlan& p, cudaStream_t s) {
+  const dim3 grid(256, (unsigned)p.n_local);
+  k_mirror_gram<<<grid, kSmallThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reset(const DevPlan& p, cudaStream_t s) {
+  k_reset<<<1, kSmallThreads, 0, s>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_apply_w(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s) {

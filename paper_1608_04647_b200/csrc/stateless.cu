@@ -59,12 +59,14 @@ cudaError_t split_v(const double* L, int64_t kp, const void* R, int r_dtype, int
       it.o_off = (int64_t)c * kp * ncols + n0;
       it.rows = (int32_t)std::max<int64_t>(0, std::min<int64_t>(kChunk, v - r0));
       it.ncols = (int32_t)std::min<int64_t>(128, ncols - n0);
+      it.mrows = (int32_t)kp;
+      it.pad = 0;
       items.push_back(it);
     }
   }
   cudaError_t e = cudaMemcpyAsync(items_dev, items.data(), items.size() * sizeof(ItemE), cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
-  e = launch_contract_e((int)kp, r_dtype, L, kp, R, ldr, part, ncols, alpha, items_dev, (int)items.size(), st);
+  e = launch_contract_e((int)kp, SRM_F64, r_dtype, L, kp, R, ldr, part, ncols, alpha, items_dev, (int)items.size(), st);
   if (e != cudaSuccess) return e;
   const int64_t n = kp * ncols;
   k_sum_chunks<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, n, nch, out);

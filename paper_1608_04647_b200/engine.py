@@ -39,7 +39,7 @@ class SrmEngine:
     """Device state of one worker's subjects for an SRM fit."""
 
     def __init__(self, n_voxels, n_trs, k, iterations, *, storage="f64", world_size=1,
-                 rank=0, counts=None, ordered=True, tolerance=False, device=None):
+                 rank=0, counts=None, ordered=True, tolerance=False, gram=False, device=None):
         torch = _torch()
         self.lib = _lib.load()
         if not torch.cuda.is_available():
@@ -63,6 +63,9 @@ class SrmEngine:
             flags |= _lib.FLAG_ORDERED
         if tolerance:
             flags |= _lib.FLAG_TOLERANCE
+        if gram:
+            flags |= _lib.FLAG_GRAM
+        self.gram = bool(gram)
         self.ordered = bool(ordered) or self.world_size == 1
         plan = ctypes.c_void_p()
         varr = (ctypes.c_int64 * self.n_local)(*self.n_voxels)
@@ -277,6 +280,13 @@ class SrmEngine:
 
     def replay(self):
         _lib.check(self.lib.srm_graph_launch(self.plan, ctypes.c_void_p(self.stream())), "graph_launch")
+
+    def prepare_gram(self):
+        """One-time X_i^T X_i for the Gram path (no-op on streaming plans)."""
+        _lib.check(self.lib.srm_prepare_gram(self.plan, ctypes.c_void_p(self.stream())), "prepare_gram")
+
+    def reset(self):
+        _lib.check(self.lib.srm_reset(self.plan, ctypes.c_void_p(self.stream())), "reset")
 
     def set_iteration(self, it):
         _lib.check(self.lib.srm_set_iteration(self.plan, int(it), ctypes.c_void_p(self.stream())))

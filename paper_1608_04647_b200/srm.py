@@ -338,8 +338,30 @@ def _storage_for(subjects, storage):
     return "f32" if all(f32) else "f64"
 
 
+def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None):
+    """'gram' or 'stream' from the fp64 tensor-core flop count of each path.
+
+    stream: per iteration two passes over X-hat (A = X S^T / 2, B = A^T X),
+            4 V T K flops per subject.
+    gram:   one-time X^T X (upper 128-tiles, V T^2 flops), then 2 K T^2 per
+            subject-iteration for B = S G / 2, plus one final A pass.
+    """
+    kp = -(-k // 8) * 8
+    ldx = -(-n_trs // 32) * 32
+    nt = -(-ldx // 128)
+    stream = 0.0
+    gram = 0.0
+    for v in n_voxels:
+        stream += iterations * 2 * (2.0 * v * ldx * kp)
+        gram += nt * (nt + 1) / 2 * 128 * 128 * 2.0 * v + iterations * 2.0 * kp * ldx * ldx + 2.0 * v * ldx * kp
+    need = len(n_voxels) * ldx * ldx * 8
+    if free_bytes is not None and need > 0.25 * free_bytes:
+        return "stream"
+    return "gram" if gram < 0.8 * stream else "stream"
+
+
 def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=True,
-        keep_on_device=False, device=None, engine_out=None, timings=None):
+        keep_on_device=False, device=None, engine_out=None, timings=None, algorithm="auto"):
     """Run the distributed EM; ``subjects`` are this worker's share (srm.py:216).
 
     Every worker calls this with the same config and its own communicator
@@ -353,6 +375,10 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     subject terms in ascending global order on every rank -- bit-identical
     results for any shard layout; otherwise per-rank sums are all-reduced.
     ``timings`` (a dict) receives per-phase wall seconds (synchronising).
+    ``algorithm``: ``"stream"`` (two passes over X-hat per iteration),
+    ``"gram"`` (one-time X^T X, then T x T algebra per iteration) or
+    ``"auto"`` (:func:`choose_algorithm`).  Both compute the reference's
+    iteration exactly; they differ only in rounding.
     """
     clock = _PhaseClock(timings)
     config.validate()
@@ -379,10 +405,17 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
         table = comm.size * max(counts) * (kp * ldx + 8) * 8
         ordered = comm.size == 1 or table <= (64 << 20) or not hasattr(comm, "all_reduce_sum")
 
-    eng = SrmEngine([int(s.X.shape[0]) for s in subjects], n_trs, k, config.iterations,
+    n_vox = [int(s.X.shape[0]) for s in subjects]
+    if algorithm == "auto":
+        torch = _torch()
+        free, _ = torch.cuda.mem_get_info(device)
+        algorithm = choose_algorithm(n_vox, n_trs, k, config.iterations, free)
+    if algorithm not in ("stream", "gram"):
+        raise ConfigError("algorithm must be 'auto', 'stream' or 'gram'")
+    eng = SrmEngine(n_vox, n_trs, k, config.iterations,
                     storage=_storage_for(subjects, storage), world_size=comm.size, rank=comm.rank,
                     counts=counts, ordered=ordered, tolerance=config.tolerance is not None,
-                    device=device)
+                    gram=algorithm == "gram", device=device)
     if engine_out is not None:
         engine_out.append(eng)
     # the init draws depend only on (seed, global index, V, k): overlap them with the upload
@@ -395,6 +428,8 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     eng.init_mapping(config.seed, offset, gaussians=draws)
     pool.shutdown(wait=False)
     clock.tick("init")
+    eng.prepare_gram()
+    clock.tick("gram")
 
     use_graph = graphs and comm.size == 1
     n_done = 0

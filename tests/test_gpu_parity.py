@@ -170,3 +170,29 @@ def test_projection(srm):
     assert np.max(np.abs(twice - once)) <= 1e-10
     with pytest.raises(IndexError):
         srm.project(m, 7, np.zeros(60))
+
+
+@pytest.mark.parametrize("name", ["em_small", "em_ragged", "em_recipe_f32"])
+@pytest.mark.parametrize("algorithm", ["stream", "gram"])
+def test_algorithms_agree_with_reference(srm, name, algorithm):
+    g = load_golden(name)
+    xs = golden_subjects(g)
+    k, iters, seed = int(g["k"]), int(g["iterations"]), int(g["seed"])
+    tol = TOL64 if xs[0].dtype == np.float64 else TOL32
+    for n in (1, 2, iters):
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=k, iterations=n, seed=seed), algorithm=algorithm)
+        it = n - 1
+        _check_model(m, g[f"it{it}_S"], g[f"it{it}_sigma_s"], g[f"it{it}_rho2"],
+                     [g[f"it{it}_W{i}"] for i in range(len(xs))], tol, f"{name} {algorithm} it{it}")
+
+
+def test_gram_cfg1_full_size_vs_oracle(srm):
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(10, 5000, 500, 50, seed=1)
+    ref = orc.run_em(xs, 50, 10, seed=0)
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=50, iterations=10, seed=0), algorithm="gram")
+    r = ref["iters"][-1]
+    _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, "cfg1 gram")
+    ref_ll = np.array([x["ll"] for x in ref["iters"]])
+    assert np.max(np.abs(np.array(m.log_likelihood) - ref_ll) / np.abs(ref_ll)) <= TOL64
