@@ -93,5 +93,7 @@ cudaError_t launch_apply_right(const double* a, int64_t lda, int64_t v, int k, c
                                int64_t ldm, double* w, int64_t ldw, cudaStream_t s);
 
 int max_supported_k();
+bool ns_polar_supported(int kp);
+cudaError_t launch_ns_polar(const DevPlan& p, int init, cudaStream_t s);
 
 }  // namespace srm

@@ -1,0 +1,192 @@
+// Polar transform M_i = (A_i^T A_i)^{-1/2} by the coupled Newton-Schulz
+// iteration on the FP64 tensor cores (one CTA per subject, K <= 80).
+//
+// kernels.py:190-212 forms the polar factor W = U V^T from an SVD of A.  For
+// full-rank A it equals A (A^T A)^{-1/2}; with C = A^T A scaled by c >= lambda_max
+// (Gershgorin bound), the iteration
+//     Y_0 = C / c,  Z_0 = I,  T_k = (3 I - Z_k Y_k) / 2,
+//     Y_{k+1} = T_k Y_k,  Z_{k+1} = T_k Z_k
+// converges quadratically to Y -> (C/c)^{1/2}, Z -> (C/c)^{-1/2} (all iterates
+// are polynomials in C, so they commute and stay symmetric).  Each step is three
+// K x K products done with mma.sync.m8n8k4.f64 from shared memory -- a
+// tensor-core replacement for the latency-bound Jacobi rotations.  A direction
+// with lambda ~ 0 never converges: that is reported as RankError
+// (kernels.py:202-206).
+#include "common.cuh"
+#include "plan.h"
+
+namespace srm {
+
+namespace {
+
+constexpr int kNsThreads = 256;
+
+__host__ __device__ constexpr int ns_ld(int kp) { return kp + ((4 - kp) % 16 + 16) % 16; }
+
+// D = A * B for KP x KP matrices in smem (row stride LD); warp w computes the
+// 8-row strips w, w+8, ...; `epi(row, col, v0, v1)` consumes D[row][col..col+1].
+template <int KP, typename Epi>
+__device__ __forceinline__ void mm(const double* __restrict__ A, const double* __restrict__ B, Epi epi) {
+  constexpr int LD = ns_ld(KP);
+  constexpr int NT = KP / 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int mt = warp; mt < NT; mt += kNsThreads / 32) {
+    double acc[NT][2];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
+    const double* arow = A + (mt * 8 + (lane >> 2)) * LD + (lane & 3);
+#pragma unroll 2
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      const double a = arow[k0];
+      const double* brow = B + (k0 + (lane & 3)) * LD + (lane >> 2);
+#pragma unroll
+      for (int n = 0; n < NT; ++n) dmma(acc[n][0], acc[n][1], a, brow[n * 8]);
+    }
+    const int row = mt * 8 + (lane >> 2);
+#pragma unroll
+    for (int n = 0; n < NT; ++n) epi(row, n * 8 + 2 * (lane & 3), acc[n][0], acc[n][1]);
+  }
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kNsThreads) k_ns_polar(DevPlan p, int init) {
+  constexpr int LD = ns_ld(KP);
+  constexpr int MAT = KP * LD;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[32];
+  __shared__ double s_scale;
+  const int i = blockIdx.x;
+  const int n = (int)p.K;
+  const int tid = threadIdx.x;
+  double* buf[4] = {sm, sm + MAT, sm + 2 * MAT, sm + 3 * MAT};
+  const double* Cg = p.bred + (int64_t)i * p.kp * p.ldo + p.ldx;  // A^T A block, row stride ldo
+
+  // Y0 = sym(C) / c (c: Gershgorin bound on lambda_max), Z0 = I; pads are zero
+  double rowmax = 0.0;
+  for (int a = tid; a < KP; a += blockDim.x) {
+    double rs = 0.0;
+    for (int b = 0; b < n && a < n; ++b)
+      rs += fabs(0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a]));
+    rowmax = fmax(rowmax, rs);
+  }
+  rowmax = warp_max(rowmax);
+  if ((tid & 31) == 0) red[tid >> 5] = rowmax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < kNsThreads / 32; ++w) m = fmax(m, red[w]);
+    s_scale = m;
+  }
+  __syncthreads();
+  const double c = s_scale;
+  const bool degenerate = !(c > 0.0) || !isfinite(c);
+  const double inv_c = degenerate ? 0.0 : 1.0 / c;
+  for (int e = tid; e < KP * LD; e += blockDim.x) {
+    const int a = e / LD, b = e - a * LD;
+    double y = 0.0;
+    if (a < n && b < n) y = 0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a]) * inv_c;
+    buf[0][e] = y;
+    buf[1][e] = (a == b && a < n) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+
+  int y = 0, z = 1;  // buffer indices of Y and Z
+  bool converged = false;
+  int extra = -1;
+  double prev_err = 1e300;
+  const int max_iter = 90;
+  int it = 0;
+  for (; it < max_iter && !degenerate; ++it) {
+    // free buffers: the two not holding Y or Z
+    int f0 = -1, f1 = -1;
+    for (int q = 0; q < 4; ++q)
+      if (q != y && q != z) (f0 < 0 ? f0 : f1) = q;
+    double* Tm = buf[f0];
+    double* Yn = buf[f1];
+    // P = Z Y -> T = (3I - P)/2 in place, and |I - P|_F^2
+    double err = 0.0;
+    mm<KP>(buf[z], buf[y], [&](int r, int col, double v0, double v1) {
+      const double d0 = (r == col ? 1.0 : 0.0) - v0, d1 = (r == col + 1 ? 1.0 : 0.0) - v1;
+      if (r < n && col < n) err += d0 * d0;
+      if (r < n && col + 1 < n) err += d1 * d1;
+      Tm[r * LD + col] = 0.5 * (r == col ? 3.0 - v0 : -v0);
+      Tm[r * LD + col + 1] = 0.5 * (r == col + 1 ? 3.0 - v1 : -v1);
+    });
+    err = block_sum<kNsThreads>(err, red);  // includes a barrier: T is complete
+    if (extra == 0) {
+      converged = true;
+      break;
+    }
+    if (!(err == err)) break;  // NaN
+    // |I - P|_F <= 1e-13, or quadratic convergence has hit the roundoff floor
+    // (|I - P| no longer shrinking while below 1e-9): one more step, then stop
+    if (extra < 0 && (err <= 1e-26 || (err < 1e-18 && err > 0.25 * prev_err))) extra = 1;
+    prev_err = err;
+    // Y_new = T Y  (-> Yn),  Z_new = T Z (-> old Y buffer once Y is consumed)
+    mm<KP>(Tm, buf[y], [&](int r, int col, double v0, double v1) {
+      Yn[r * LD + col] = v0;
+      Yn[r * LD + col + 1] = v1;
+    });
+    __syncthreads();
+    double* Zn = buf[y];
+    mm<KP>(Tm, buf[z], [&](int r, int col, double v0, double v1) {
+      Zn[r * LD + col] = v0;
+      Zn[r * LD + col + 1] = v1;
+    });
+    __syncthreads();
+    z = y;   // Z now lives in the old Y buffer
+    y = f1;  // Y in Yn
+    if (extra > 0) --extra;
+  }
+  // M = sym(Z) / sqrt(c)
+  const int kp = (int)p.kp;
+  double* Mg = p.mmat + (int64_t)i * kp * kp;
+  const double* Z = buf[z];
+  const double s = degenerate ? 0.0 : 1.0 / sqrt(c);
+  for (int e = tid; e < kp * kp; e += blockDim.x) {
+    const int a = e / kp, b = e - a * kp;
+    Mg[e] = (a < n && b < n) ? 0.5 * (Z[a * LD + b] + Z[b * LD + a]) * s : 0.0;
+  }
+  if (tid == 0) {
+    p.scal[(int64_t)i * 8 + 0] = (double)it;
+    if (degenerate || !converged) {
+      const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
+      raise_status(p.status, SRM_ERR_RANK, (int)sj[SC_GLOBAL], init ? -1 : *p.iter);
+    }
+  }
+}
+
+template <int KP>
+cudaError_t run_ns(const DevPlan& p, int init, cudaStream_t s) {
+  constexpr int bytes = 4 * KP * ns_ld(KP) * (int)sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_ns_polar<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_ns_polar<KP><<<p.n_local, kNsThreads, bytes, s>>>(p, init);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool ns_polar_supported(int kp) { return kp >= 8 && kp <= 80 && kp % 8 == 0; }
+
+cudaError_t launch_ns_polar(const DevPlan& p, int init, cudaStream_t s) {
+  switch ((int)p.kp) {
+    case 8: return run_ns<8>(p, init, s);
+    case 16: return run_ns<16>(p, init, s);
+    case 24: return run_ns<24>(p, init, s);
+    case 32: return run_ns<32>(p, init, s);
+    case 40: return run_ns<40>(p, init, s);
+    case 48: return run_ns<48>(p, init, s);
+    case 56: return run_ns<56>(p, init, s);
+    case 64: return run_ns<64>(p, init, s);
+    case 72: return run_ns<72>(p, init, s);
+    case 80: return run_ns<80>(p, init, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace srm

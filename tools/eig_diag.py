@@ -15,4 +15,4 @@ eng.init_mapping(0, 0)
 scal = eng.region(_lib.R_SCAL).view(n, 8)
 for it in range(12):
     prof = dict(eng.profile_iteration())
-    print(it, "sweeps", scal[:, 0].tolist()[:6], "eig ms %.3f tail_kk %.3f" % (prof["eig_polar"], prof["tail_kk"]))
+    print(it, "iters", scal[:, 0].tolist()[:6], {k: round(v, 3) for k, v in prof.items()})
