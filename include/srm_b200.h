@@ -145,6 +145,9 @@ int srm_init_mapping(srm_plan* plan, void* stream);
  * B_i = A_i^T Xhat_i = S G_i / 2 and A_i^T A_i = B_i S^T / 2 only; A_i itself is
  * formed once in srm_finalize.  No-op for streaming plans. */
 int srm_prepare_gram(srm_plan* plan, void* stream);
+/* the same for local subjects [first, first + count) -- lets the loader
+ * overlap each subject's Gram with the next subject's host-to-device copy */
+int srm_prepare_gram_range(srm_plan* plan, int first, int count, void* stream);
 /* restart the EM state (Sigma_s = I, status cleared, iteration 0); the next
  * srm_init_mapping draws a fresh start (used to time repeated fits) */
 int srm_reset(srm_plan* plan, void* stream);

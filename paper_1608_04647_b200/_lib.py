@@ -35,6 +35,7 @@ SIGNATURES = [
     ("srm_finish_load", c_int, [c_vp, c_vp]),
     ("srm_init_mapping", c_int, [c_vp, c_vp]),
     ("srm_prepare_gram", c_int, [c_vp, c_vp]),
+    ("srm_prepare_gram_range", c_int, [c_vp, c_int, c_int, c_vp]),
     ("srm_reset", c_int, [c_vp, c_vp]),
     ("srm_set_iteration", c_int, [c_vp, c_int, c_vp]),
     ("srm_reduce_local", c_int, [c_vp, c_vp]),

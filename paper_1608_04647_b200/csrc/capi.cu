@@ -694,15 +694,23 @@ int srm_finalize(srm_plan* p, void* stream) {
   return check(launch_apply_w(d, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st), "finalize");
 }
 
-int srm_prepare_gram(srm_plan* p, void* stream) {
+int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
   if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
   if (!(p->flags & SRM_FLAG_GRAM)) return SRM_OK;
+  if (first < 0 || count < 0 || first + count > p->n_local) return fail(SRM_ERR_CONFIG, "subject range out of bounds");
+  if (count == 0) return SRM_OK;
   cudaStream_t st = as_stream(stream);
   const DevPlan& d = p->dp;
+  const int per = (int)(p->items_gram.size() / p->n_local);  // upper tiles per subject (subject-major)
   cudaError_t e = launch_contract_e(128, p->dtype, p->dtype, d.xhat, p->ldx, d.xhat, p->ldx, d.gram, p->ldx, 1.0,
-                                    region<ItemE>(p, I_ITEMS_GRAM), (int)p->items_gram.size(), st);
-  if (e == cudaSuccess) e = launch_mirror_gram(d, st);
+                                    region<ItemE>(p, I_ITEMS_GRAM) + (int64_t)first * per, count * per, st);
+  if (e == cudaSuccess) e = launch_mirror_gram(d, first, count, st);
   return check(e, "prepare_gram");
+}
+
+int srm_prepare_gram(srm_plan* p, void* stream) {
+  if (!p) return fail(SRM_ERR_CONFIG, "null plan");
+  return srm_prepare_gram_range(p, 0, p->n_local, stream);
 }
 
 int srm_reset(srm_plan* p, void* stream) {

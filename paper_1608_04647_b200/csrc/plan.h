@@ -81,7 +81,7 @@ cudaError_t launch_tail(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_sigma(const DevPlan& p, cudaStream_t s);
-cudaError_t launch_mirror_gram(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_mirror_gram(const DevPlan& p, int first, int count, cudaStream_t s);
 cudaError_t launch_reset(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_apply_w(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);
 

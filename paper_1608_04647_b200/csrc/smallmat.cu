@@ -637,9 +637,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_sigma(DevPlan p) {
 }
 
 // mirror the upper 128-tiles of every X_i^T X_i into the lower ones
-__global__ void k_mirror_gram(DevPlan p) {
+__global__ void k_mirror_gram(DevPlan p, int first) {
   const int64_t n = p.ldx * p.ldx;
-  double* g = p.gram + (int64_t)blockIdx.y * n;
+  double* g = p.gram + (int64_t)(first + blockIdx.y) * n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = e / p.ldx, b = e - a * p.ldx;
     if ((a >> 7) > (b >> 7)) g[e] = g[b * p.ldx + a];
@@ -873,9 +873,9 @@ cudaError_t launch_tail(const DevPlan& p, cudaStream_t s) {
   return e;
 }
 
-cudaError_t launch_mirror_gram(const DevPlan& p, cudaStream_t s) {
-  const dim3 grid(256, (unsigned)p.n_local);
-  k_mirror_gram<<<grid, kSmallThreads, 0, s>>>(p);
+cudaError_t launch_mirror_gram(const DevPlan& p, int first, int count, cudaStream_t s) {
+  const dim3 grid(256, (unsigned)count);
+  k_mirror_gram<<<grid, kSmallThreads, 0, s>>>(p, first);
   return cudaGetLastError();
 }
 

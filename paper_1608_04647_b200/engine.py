@@ -155,14 +155,22 @@ class SrmEngine:
             self._staging[key] = buf
         return buf[:numel]
 
-    def load(self, xs):
-        """Upload (if needed) and demean every local subject (srm.py:238-240)."""
+    def load(self, xs, gaussians=None, gram=False):
+        """Upload (if needed) and demean every local subject (srm.py:238-240).
+
+        Pipelined per subject: the host-to-device copy of subject j+1 (copy
+        stream) overlaps the demean -- and, with ``gram``, the one-time
+        X_j^T X_j -- of subject j (compute stream).  ``gaussians`` (arrays or
+        futures of the init draws) are uploaded into the A region on the way.
+        """
         torch = _torch()
         if len(xs) != self.n_local:
             raise ConfigError("subject count does not match the plan")
         main = torch.cuda.current_stream(self.device)
         copier = torch.cuda.Stream(device=self.device)
+        gram_stream = torch.cuda.Stream(device=self.device)
         done = [None, None]
+        next_g = 0
         for j, x in enumerate(xs):
             v = self.n_voxels[j]
             if isinstance(x, torch.Tensor) and x.device == self.device and x.dim() == 2 \
@@ -204,10 +212,72 @@ class SrmEngine:
             ev2 = torch.cuda.Event()
             ev2.record(main)
             done[j % 2] = ev2
+            if gram and self.gram:
+                # batch subjects so each Gram launch fills the 148 SMs (1 CTA/SM per 128x128
+                # tile); it runs on its own stream so staging-buffer reuse only waits on demean
+                nt = -(-self.ldx // 128)
+                batch = max(1, -(-148 // (nt * (nt + 1) // 2)))
+                if (j + 1) % batch == 0 or j + 1 == self.n_local:
+                    first = (j // batch) * batch
+                    gram_stream.wait_event(ev2)
+                    _lib.check(self.lib.srm_prepare_gram_range(self.plan, first, j + 1 - first,
+                                                               ctypes.c_void_p(gram_stream.cuda_stream)),
+                               "prepare_gram")
+            if gaussians is not None:
+                # upload the init draws that are ready without stalling the copy stream
+                while next_g < self.n_local and (next_g <= j or not hasattr(gaussians[next_g], "done")
+                                                 or gaussians[next_g].done()):
+                    if hasattr(gaussians[next_g], "done") and not gaussians[next_g].done() and next_g > j - 2:
+                        break
+                    with torch.cuda.stream(copier):
+                        self._upload_gaussian(next_g, gaussians[next_g], stream=copier)
+                    gaussians[next_g] = None
+                    next_g += 1
+        while gaussians is not None and next_g < self.n_local:
+            with torch.cuda.stream(copier):
+                self._upload_gaussian(next_g, gaussians[next_g], stream=copier)
+            gaussians[next_g] = None
+            next_g += 1
         _lib.check(self.lib.srm_finish_load(self.plan, ctypes.c_void_p(main.cuda_stream)), "finish_load")
+        main.wait_stream(gram_stream)
+        main.wait_stream(copier)
         main.synchronize()
         self._staging.clear()
         self.raise_status()
+
+    def _upload_gaussian(self, j, g, stream=None):
+        """Copy subject j's init draw into its A-region rows (pad columns stay 0).
+
+        ``g`` is an array, a tensor, a future of either, or a (ring, slot) pair
+        of a PinnedRing slot filled by a worker (asynchronous copy).
+        """
+        torch = _torch()
+        if hasattr(g, "result"):
+            g = g.result()
+        r0 = int(self.row_off[j])
+        rows = self.amat[r0: r0 + self.n_voxels[j]]
+        if isinstance(g, tuple):
+            ring, slot = g
+            nbytes = self.n_voxels[j] * self.K * 8
+            src = ring.tensor(slot, nbytes).view(torch.float64).view(self.n_voxels[j], self.K)
+            st = stream or torch.cuda.current_stream(self.device)
+            with torch.cuda.stream(st):
+                tmp = torch.empty((self.n_voxels[j], self.K), dtype=torch.float64, device=self.device)
+                tmp.copy_(src, non_blocking=True)
+                rows[:, : self.K].copy_(tmp)
+                ev = torch.cuda.Event()
+                ev.record(st)
+            ring.mark_used(slot, ev)
+            return
+        if isinstance(g, torch.Tensor):
+            rows[:, : self.K].copy_(g)
+            return
+        tmp = hostio.to_device(np.ascontiguousarray(g, dtype=np.float64), self.device)
+        rows[:, : self.K].copy_(tmp)
+
+    def init_kernels(self):
+        """The device part of init_subject once the draws are in the A region."""
+        _lib.check(self.lib.srm_init_mapping(self.plan, ctypes.c_void_p(self.stream())), "init_mapping")
 
     def init_mapping(self, seed, global_offset, gaussians=None, threads=8):
         """init_subject (srm.py:101-113): host PCG64 draws, device polar + first E-step."""

@@ -115,3 +115,53 @@ def to_device(arr, device, out=None):
                 ev.synchronize()
     torch.cuda.current_stream(device).wait_stream(stream)
     return out
+
+
+class PinnedRing:
+    """A few reusable pinned host slots (cached per device and slot size).
+
+    Producers fill a slot on a worker thread after the slot's previous device
+    copy has completed; the consumer issues an asynchronous copy from it and
+    records an event that guards the slot's next reuse.
+    """
+
+    _cache = {}
+
+    def __init__(self, slot_bytes, nslots):
+        torch = _torch()
+        self.slots = [torch.empty(slot_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(nslots)]
+        self.events = [None] * nslots
+        self.slot_bytes = slot_bytes
+
+    @classmethod
+    def get(cls, device, slot_bytes, nslots=4, n_items=0):
+        key = (str(device), nslots)
+        with _lock:
+            ring = cls._cache.get(key)
+            if ring is None or ring.slot_bytes < slot_bytes:
+                ring = cls(slot_bytes, nslots)
+                cls._cache[key] = ring
+        ring.events = [None] * nslots
+        ring.issued = [threading.Event() for _ in range(n_items)]
+        return ring
+
+    def view(self, i, shape, dtype=np.float64):
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        return self.slots[i % len(self.slots)][:n].numpy().view(dtype).reshape(shape)
+
+    def tensor(self, i, nbytes):
+        return self.slots[i % len(self.slots)][:nbytes]
+
+    def wait_free(self, i):
+        """Block until item i's slot is no longer read by item i - nslots's copy."""
+        prev = i - len(self.slots)
+        if prev >= 0:
+            self.issued[prev].wait()
+            ev = self.events[prev % len(self.slots)]
+            if ev is not None:
+                ev.synchronize()
+
+    def mark_used(self, i, event):
+        self.events[i % len(self.slots)] = event
+        if i < len(self.issued):
+            self.issued[i].set()

@@ -420,16 +420,23 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
         engine_out.append(eng)
     # the init draws depend only on (seed, global index, V, k): overlap them with the upload
     pool = ThreadPoolExecutor(max(1, min(os.cpu_count() or 1, len(subjects))))
-    draws = [pool.submit(reference_gaussian, int(s.X.shape[0]), k, config.seed, offset + j)
-             for j, s in enumerate(subjects)]
+    ring = hostio.PinnedRing.get(eng.device, max(n_vox) * k * 8, nslots=min(16, len(subjects)),
+                                 n_items=len(subjects))
+
+    def draw(j):  # the srm.py:111 PCG64 stream, written straight into a pinned slot
+        ring.wait_free(j)
+        gen = np.random.default_rng((config.seed & 0xFFFFFFFFFFFFFFFF, offset + j))
+        gen.standard_normal(out=ring.view(j, (n_vox[j], k)))
+        return (ring, j)
+
+    draws = [pool.submit(draw, j) for j in range(len(subjects))]
     clock.tick("setup")
-    eng.load([s.X for s in subjects])
-    clock.tick("load")
-    eng.init_mapping(config.seed, offset, gaussians=draws)
+    # pipelined: upload + demean (+ X^T X on the Gram path) + init draws per subject
+    eng.load([s.X for s in subjects], gaussians=draws, gram=True)
     pool.shutdown(wait=False)
+    clock.tick("load")
+    eng.init_kernels()
     clock.tick("init")
-    eng.prepare_gram()
-    clock.tick("gram")
 
     use_graph = graphs and comm.size == 1
     n_done = 0
