@@ -1,0 +1,156 @@
+"""Multi-rank paths: world_size 2 over gloo (127.0.0.1).
+
+CPU tests cover the communicator and the ordered E-step exchange layout
+(the C plan's slot table), the reduction order and the final rho^2 gather.
+The GPU test runs two ranks of the real fit on one GPU with gloo carrying
+the exchange through host memory (no kernel waits on another rank's kernel)
+and checks bit-identity with the serial fit (srm.py:193-213 contract,
+test_srm.py:200-229).
+"""
+
+import ctypes
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _init(rank, world, port):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _comm_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1608_04647_b200 import _lib
+    from paper_1608_04647_b200.collectives import TorchCommunicator, rank_counts, rank_offsets, shard_bounds
+
+    _init(rank, world, port)
+    comm = TorchCommunicator()
+    n_total = 5
+    a, b = shard_bounds(n_total, world, rank)
+    counts = rank_counts(comm, b - a)
+    off, tot = rank_offsets(comm, b - a)
+    g = comm.gather(bytes([rank]) * 3)
+    bc = comm.broadcast(np.full((2, 2), 7.0) if rank == 0 else None)
+    rs = comm.reduce_sum(np.full((1, 3), float(rank + 1)))
+
+    # ordered exchange with the plan's slot layout: rank r owns slots [r*m, r*m + count_r)
+    lib = _lib.load()
+    p = ctypes.c_void_p()
+    v = (ctypes.c_int64 * (b - a))(*([40] * (b - a)))
+    rc = lib.srm_plan_create(ctypes.byref(p), 0, b - a, v, 16, 3, 2, world, rank,
+                             (ctypes.c_int32 * world)(*counts), _lib.FLAG_ORDERED)
+    assert rc == 0
+    n_slots = lib.srm_plan_dim(p, _lib.D_N_SLOTS)
+    slot0 = lib.srm_plan_dim(p, _lib.D_SLOT_OFFSET)
+    lib.srm_plan_destroy(p)
+    m = n_slots // world
+    rng = np.random.default_rng(3)
+    terms = rng.standard_normal((n_total, 6))          # every subject's "E-step term"
+    table = torch.zeros((n_slots, 6), dtype=torch.float64)
+    for j in range(b - a):
+        table[slot0 + j] = torch.from_numpy(terms[a + j])
+    comm.all_gather_into(table, table[rank * m: (rank + 1) * m].clone())
+    order = [r * m + j for r in range(world) for j in range(counts[r])]
+    acc = table[order[0]].clone()
+    for s in order[1:]:
+        acc += table[s]
+    serial = terms[0].copy()
+    for t in terms[1:]:
+        serial += t
+    buf = torch.full((4,), float(rank + 1), dtype=torch.float64)
+    comm.all_reduce_sum(buf)
+    out.put((rank, counts, off, tot, g, bc.tolist(), None if rs is None else rs.tolist(),
+             np.array_equal(acc.numpy(), serial), buf.tolist(), comm.stats.allgather_calls))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_communicator_and_ordered_exchange():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_comm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r = q.get(timeout=120)
+        res[r[0]] = r
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        _, counts, off, tot, g, bc, rs, ordered_ok, buf, ag = res[rank]
+        assert counts == [3, 2] and tot == 5 and off == (0 if rank == 0 else 3)
+        assert bc == [[7.0, 7.0], [7.0, 7.0]]
+        assert ordered_ok, "ordered all-gather sum differs from the serial ascending sum"
+        assert buf == [3.0] * 4 and ag == 1
+    assert res[0][4] == [b"\x00" * 3, b"\x01" * 3] and res[1][4] is None
+    assert res[0][6] == [[3.0, 3.0, 3.0]] and res[1][6] is None
+
+
+def _fit_worker(rank, world, port, out, algorithm):
+    import torch.distributed as dist
+
+    from conftest import load_golden, golden_subjects
+    from paper_1608_04647_b200 import srm
+    from paper_1608_04647_b200.collectives import TorchCommunicator, shard_bounds
+
+    _init(rank, world, port)
+    g = load_golden("em_ragged")
+    xs = golden_subjects(g)
+    a, b = shard_bounds(len(xs), world, rank)
+    m = srm.fit([srm.SubjectData(f"s{i}", xs[i]) for i in range(a, b)],
+                srm.SrmConfig(k=int(g["k"]), iterations=int(g["iterations"]), seed=int(g["seed"])),
+                TorchCommunicator(), algorithm=algorithm)
+    out.put((rank, m.S, m.W, m.rho2, m.rho0, m.sigma_s, m.rho2_all, m.subject_indices))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algorithm", ["stream", "gram"])
+def test_two_rank_fit_bit_identical_to_serial(algorithm):
+    from conftest import load_golden, golden_subjects
+    from paper_1608_04647_b200 import srm
+
+    g = load_golden("em_ragged")
+    xs = golden_subjects(g)
+    cfg = srm.SrmConfig(k=int(g["k"]), iterations=int(g["iterations"]), seed=int(g["seed"]))
+    serial = srm.fit([srm.SubjectData(f"s{i}", x) for i, x in enumerate(xs)], cfg, algorithm=algorithm)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fit_worker, args=(r, 2, port, q, algorithm)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r = q.get(timeout=300)
+        res[r[0]] = r
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    _, S0, W0, r0, rho0_0, sig0, all0, idx0 = res[0]
+    _, S1, W1, r1, rho0_1, sig1, all1, idx1 = res[1]
+    assert idx0 == [0, 1] and idx1 == [2, 3]
+    assert np.array_equal(S0, serial.S) and np.array_equal(S1, serial.S)
+    for i, w in enumerate(W0 + W1):
+        assert np.array_equal(w, serial.W[i])
+    assert r0 + r1 == serial.rho2
+    assert rho0_0 == serial.rho0 == rho0_1
+    assert np.array_equal(sig0, serial.sigma_s) and sig1 is None and all1 is None
+    assert np.array_equal(all0, serial.rho2_all)
