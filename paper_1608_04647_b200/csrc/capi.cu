@@ -252,7 +252,7 @@ void build_work(srm_plan* p) {
           it.rows = (int32_t)p->V[i];
           it.ncols = (int32_t)std::min<int64_t>(128, p->ldx - n0);
           it.mrows = (int32_t)std::min<int64_t>(128, p->ldx - m0);
-          it.pad = 0;
+          it.pad = (m0 == n0) ? 1 : 0;
           p->items_gram.push_back(it);
         }
       }
@@ -563,7 +563,7 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
   if (e == cudaSuccess)
     e = launch_contract_a((int)p->kp, SRM_F64, d.bred, p->ldo, d.S, p->ldx, p->ldx, d.bred, p->ldo, 0.5, nullptr, 0, 0);
   if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM))
-    e = launch_contract_e(128, p->dtype, p->dtype, d.xhat, p->ldx, d.xhat, p->ldx, d.gram, p->ldx, 1.0, nullptr, 0, 0);
+    e = launch_gram_tiles(p->dtype, d.xhat, p->ldx, d.gram, p->ldx, nullptr, 0, 0);
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
   return SRM_OK;
 }
@@ -702,7 +702,7 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
   cudaStream_t st = as_stream(stream);
   const DevPlan& d = p->dp;
   const int per = (int)(p->items_gram.size() / p->n_local);  // upper tiles per subject (subject-major)
-  cudaError_t e = launch_contract_e(128, p->dtype, p->dtype, d.xhat, p->ldx, d.xhat, p->ldx, d.gram, p->ldx, 1.0,
+  cudaError_t e = launch_gram_tiles(p->dtype, d.xhat, p->ldx, d.gram, p->ldx,
                                     region<ItemE>(p, I_ITEMS_GRAM) + (int64_t)first * per, count * per, st);
   if (e == cudaSuccess) e = launch_mirror_gram(d, first, count, st);
   return check(e, "prepare_gram");

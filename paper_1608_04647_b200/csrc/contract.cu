@@ -262,6 +262,123 @@ __global__ void __launch_bounds__(kThreads) k_contract_a(const TX* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Gram tiles of X^T X (Gram path, one-time): out[m][n] = sum_v X[v][m0+m] X[v][n0+n]
+// for 128 x 128 tiles.  4 x 2 warp grid (each warp 32 rows x 64 columns: 4 A and 8
+// B fragments per 32 DMMA), 32-deep pipeline stages.  Diagonal tiles (item.pad
+// = 1) skip the strictly-lower 64 x 64 block; the mirror kernel fills it.
+// ---------------------------------------------------------------------------
+constexpr int kGBC = 32;
+
+template <typename TX>
+__host__ __device__ constexpr int g_stride() { return sizeof(TX) == 8 ? 132 : 136; }
+
+template <typename TX>
+constexpr int g_stage_bytes() { return 2 * kGBC * g_stride<TX>() * (int)sizeof(TX); }
+
+template <typename TX, int STAGES>
+__global__ void __launch_bounds__(kThreads) k_gram128(const TX* __restrict__ X, int64_t ldx,
+                                                      double* __restrict__ out, int64_t ldo,
+                                                      const ItemE* __restrict__ items) {
+  constexpr int SX = g_stride<TX>();
+  constexpr int EPC = 16 / (int)sizeof(TX);
+  constexpr int CH = 128 / EPC;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TX* Ls = reinterpret_cast<TX*>(smem_raw);
+  TX* Rs = Ls + STAGES * kGBC * SX;
+  const ItemE it = items[blockIdx.x];
+  const TX* Lb = X + it.l_off;
+  const TX* Rb = X + it.r_off;
+  const int rows = it.rows, ncols = it.ncols, mrows = it.mrows;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 1, wn = warp & 1;  // rows [32 wm, +32), cols [64 wn, +64)
+  const bool skip = it.pad && (wm >= 2 * wn + 2);
+  const int nstages = (rows + kGBC - 1) / kGBC;
+
+  auto load_stage = [&](int s, int buf) {
+    const int r0 = s * kGBC;
+    TX* ld = Ls + buf * kGBC * SX;
+    TX* rd = Rs + buf * kGBC * SX;
+    for (int i = tid; i < kGBC * CH; i += kThreads) {
+      const int r = i / CH, c = (i - r * CH) * EPC;
+      const bool okr = (r0 + r) < rows;
+      const bool okl = okr && c < mrows;
+      const bool okc = okr && c < ncols;
+      cp_async16(ld + r * SX + c, Lb + (okl ? (int64_t)(r0 + r) * ldx + c : 0), okl);
+      cp_async16(rd + r * SX + c, Rb + (okc ? (int64_t)(r0 + r) * ldx + c : 0), okc);
+    }
+  };
+
+  double acc[4][8][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 8; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nstages) load_stage(s, s);
+    cp_async_commit();
+  }
+  const int arow = wm * 32 + (lane >> 2);
+  const int bcol = wn * 64 + (lane >> 2);
+  const int kr = lane & 3;
+  for (int s = 0; s < nstages; ++s) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int ns = s + STAGES - 1;
+      if (ns < nstages) load_stage(ns, ns % STAGES);
+      cp_async_commit();
+    }
+    if (skip) continue;
+    const TX* Lt = Ls + (s % STAGES) * kGBC * SX;
+    const TX* Rt = Rs + (s % STAGES) * kGBC * SX;
+#pragma unroll
+    for (int kk = 0; kk < kGBC; kk += 4) {
+      const int cr = (kk + kr) * SX;
+      double a[4], b[8];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) a[m] = to_f64(Lt[cr + arow + m * 8]);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) b[n] = to_f64(Rt[cr + bcol + n * 8]);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < 8; ++n) dmma(acc[m][n][0], acc[m][n][1], a[m], b[n]);
+    }
+  }
+  cp_async_wait<0>();
+  if (skip) return;
+  double* ob = out + it.o_off;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int row = wm * 32 + m * 8 + (lane >> 2);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const int col = wn * 64 + n * 8 + 2 * (lane & 3);
+      if (row < mrows && col < ncols) store2(ob + (int64_t)row * ldo + col, acc[m][n][0], acc[m][n][1]);
+    }
+  }
+}
+
+template <typename TX>
+cudaError_t run_g(const TX* X, int64_t ldx, double* out, int64_t ldo, const ItemE* items, int n_items,
+                  cudaStream_t stream) {
+  constexpr int ST = 3;
+  constexpr int bytes = ST * g_stage_bytes<TX>();
+  auto kern = k_gram128<TX, ST>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (n_items == 0) return cudaSuccess;
+  kern<<<n_items, kThreads, bytes, stream>>>(X, ldx, out, ldo, items);
+  return cudaGetLastError();
+}
+
 template <int KP, typename TL, typename TR>
 cudaError_t run_e(const TL* L, int64_t ldl, const TR* R, int64_t ldr, double* out, int64_t ldo,
                   double alpha, const ItemE* items, int n_items, cudaStream_t stream) {
@@ -300,6 +417,13 @@ cudaError_t run_a(const TX* X, int64_t ldx, const double* S, int64_t lds, int64_
 }  // namespace
 
 bool contract_kp_supported(int kp) { return kp >= 8 && kp <= 128 && kp % 8 == 0; }
+
+cudaError_t launch_gram_tiles(int x_dtype, const void* X, int64_t ldx, double* out, int64_t ldo,
+                              const ItemE* items, int n_items, cudaStream_t stream) {
+  if (x_dtype == SRM_F64)
+    return run_g<double>(static_cast<const double*>(X), ldx, out, ldo, items, n_items, stream);
+  return run_g<float>(static_cast<const float*>(X), ldx, out, ldo, items, n_items, stream);
+}
 
 #define SRM_KP_CASES(F) \
   F(8) F(16) F(24) F(32) F(40) F(48) F(56) F(64) F(72) F(80) F(88) F(96) F(104) F(112) F(120) F(128)

@@ -40,6 +40,10 @@ cudaError_t launch_contract_a(int kp, int x_dtype, const void* X, int64_t ldx, c
 
 bool contract_kp_supported(int kp);
 
+// 128 x 128 tiles of X^T X (items: l_off/r_off column offsets, pad = 1 on diagonal tiles)
+cudaError_t launch_gram_tiles(int x_dtype, const void* X, int64_t ldx, double* out, int64_t ldo,
+                              const ItemE* items, int n_items, cudaStream_t stream);
+
 // thread-local message returned by srm_last_error() (defined in capi.cu)
 void set_last_error(const char* where, cudaError_t e);
 

@@ -636,13 +636,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_sigma(DevPlan p) {
   }
 }
 
-// mirror the upper 128-tiles of every X_i^T X_i into the lower ones
+// mirror the computed upper triangle of every X_i^T X_i into the lower one
 __global__ void k_mirror_gram(DevPlan p, int first) {
   const int64_t n = p.ldx * p.ldx;
   double* g = p.gram + (int64_t)(first + blockIdx.y) * n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = e / p.ldx, b = e - a * p.ldx;
-    if ((a >> 7) > (b >> 7)) g[e] = g[b * p.ldx + a];
+    if (a > b) g[e] = g[b * p.ldx + a];
   }
 }
 
