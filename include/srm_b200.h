@@ -52,9 +52,12 @@ enum srm_flags {
                              from a gathered per-subject table (srm.py:193-213);
                              otherwise per-rank sums are all-reduced */
   SRM_FLAG_TOLERANCE = 2, /* compute |S - S_prev| / |S_prev| every iteration (srm.py:275-287) */
-  SRM_FLAG_GRAM = 4       /* per-iteration contractions through the T x T data Gram
+  SRM_FLAG_GRAM = 4,      /* per-iteration contractions through the T x T data Gram
                              (one-time X^T X); exact algebra, fewer flops when
                              4*K*iterations > T */
+  SRM_FLAG_TC = 8         /* fp32 X-hat: streaming passes on the tcgen05 tensor cores
+                             as 3xTF32 split-precision MMAs (ignored for fp64
+                             storage, K > 128, or with SRM_FLAG_GRAM) */
 };
 
 /* workspace regions (srm_plan_region) */
@@ -90,7 +93,8 @@ enum srm_dim {
   SRM_D_ITEMS_E = 8,      /* work items of the V-contraction kernel     */
   SRM_D_ITEMS_A = 9,      /* work items of the T-contraction kernel     */
   SRM_D_CHUNK_ROWS = 10,  /* rows per V chunk                           */
-  SRM_D_LAUNCHES = 11     /* kernel launches per EM iteration (e+m step) */
+  SRM_D_LAUNCHES = 11,    /* kernel launches per EM iteration (e+m step) */
+  SRM_D_FLAGS = 12        /* effective plan flags                        */
 };
 
 /* per-iteration history columns (SRM_R_HIST, hist_stride doubles per row) */

@@ -61,11 +61,11 @@ SIGNATURES = [
 
 # include/srm_b200.h enums
 SRM_F64, SRM_F32 = 0, 1
-FLAG_ORDERED, FLAG_TOLERANCE, FLAG_GRAM = 1, 2, 4
+FLAG_ORDERED, FLAG_TOLERANCE, FLAG_GRAM, FLAG_TC = 1, 2, 4, 8
 (R_XHAT, R_AMAT, R_WOUT, R_MU, R_TERMS, R_RED, R_REDLOCAL, R_S, R_SIGMA, R_HIST, R_STATUS,
  R_MMAT, R_SCAL, R_GRAM, R_VAR) = range(15)
 (D_LDX, D_KP, D_ROWS, D_TERM_STRIDE, D_RED_STRIDE, D_HIST_STRIDE, D_N_SLOTS, D_SLOT_OFFSET,
- D_ITEMS_E, D_ITEMS_A, D_CHUNK_ROWS, D_LAUNCHES) = range(12)
+ D_ITEMS_E, D_ITEMS_A, D_CHUNK_ROWS, D_LAUNCHES, D_FLAGS) = range(13)
 H_LL, H_TRACE, H_RHO0, H_SDIFF, H_SPREV, H_RHO2 = 0, 1, 2, 3, 4, 8
 REC_RHO2, REC_V, REC_SQNORM, REC_SCALARS = 0, 1, 2, 8
 RED_RHO0, RED_VLOGRHO, RED_SQRHO, RED_VSUM = 0, 1, 2, 3

@@ -59,6 +59,11 @@ enum Internal {
   I_ST,
   I_ITEMS_GRAM,
   I_ITEMS_BG,
+  I_AF,
+  I_SF,
+  I_ITEMS_TB,
+  I_ITEMS_TA,
+  I_ITEMS_TG,
   I_COUNT
 };
 
@@ -84,8 +89,9 @@ struct srm_plan {
   int64_t chunk_rows = 0;
   std::vector<int64_t> chunk0, nchunk;
   int64_t chunks_total = 0;
-  std::vector<ItemE> items_ex, items_ea, items_gram, items_bg;
-  std::vector<ItemA> items_a, items_g;
+  std::vector<ItemE> items_ex, items_ea, items_gram, items_bg, items_tb, items_tg;
+  int np = 0;  // tensor-core feature padding
+  std::vector<ItemA> items_a, items_g, items_ta;
   std::vector<int64_t> subj;
   std::vector<int32_t> order, order_local;
   int64_t off[I_COUNT] = {0};
@@ -145,6 +151,12 @@ void layout(srm_plan* p) {
   sz[I_ST] = p->ldx * p->kp * 8;
   sz[I_ITEMS_GRAM] = (int64_t)p->items_gram.size() * sizeof(ItemE);
   sz[I_ITEMS_BG] = (int64_t)p->items_bg.size() * sizeof(ItemE);
+  const bool tc = (p->flags & SRM_FLAG_TC) != 0;
+  sz[I_AF] = tc ? p->rows_total * p->np * 4 : 0;
+  sz[I_SF] = tc ? 2 * (int64_t)p->np * p->ldx * 4 : 0;
+  sz[I_ITEMS_TB] = (int64_t)p->items_tb.size() * sizeof(ItemE);
+  sz[I_ITEMS_TA] = (int64_t)p->items_ta.size() * sizeof(ItemA);
+  sz[I_ITEMS_TG] = (int64_t)p->items_tg.size() * sizeof(ItemE);
   int64_t cur = 0;
   for (int r = 0; r < I_COUNT; ++r) {
     p->off[r] = cur;
@@ -269,6 +281,51 @@ void build_work(srm_plan* p) {
       }
     }
   }
+  // tensor-core path: A-pass row tiles (A in the fp32 [rows][np] region) and
+  // B-pass tiles of 128 TRs over the same V chunks
+  p->items_tb.clear();
+  p->items_ta.clear();
+  p->items_tg.clear();
+  if (p->flags & SRM_FLAG_TC) {
+    // exact fp64 A^T A of the stored fp32 A (final W only): same V chunks
+    for (int i = 0; i < p->n_local; ++i) {
+      for (int64_t ch = 0; ch < p->nchunk[i]; ++ch) {
+        const int64_t r0 = p->row_off[i] + ch * cr;
+        ItemE g;
+        g.l_off = r0 * p->np;
+        g.r_off = r0 * p->np;
+        g.o_off = (p->chunk0[i] + ch) * p->kp * p->ldo + p->ldx;
+        g.rows = (int32_t)std::max<int64_t>(0, std::min<int64_t>(cr, p->V[i] - ch * cr));
+        g.ncols = (int32_t)p->kp;
+        g.mrows = (int32_t)p->kp;
+        g.pad = 0;
+        p->items_tg.push_back(g);
+      }
+    }
+    for (const ItemA& a : p->items_a) {
+      ItemA t = a;
+      t.o_off = (a.x_off / p->ldx) * p->np;
+      p->items_ta.push_back(t);
+    }
+    for (int i = 0; i < p->n_local; ++i) {
+      for (int64_t ch = 0; ch < p->nchunk[i]; ++ch) {
+        const int64_t r0 = p->row_off[i] + ch * cr;
+        const int64_t rows = std::max<int64_t>(0, std::min<int64_t>(cr, p->V[i] - ch * cr));
+        const int64_t obase = (p->chunk0[i] + ch) * p->kp * p->ldo;
+        for (int64_t n0 = 0; n0 < p->ldx; n0 += 128) {
+          ItemE it;
+          it.l_off = r0 * p->np;
+          it.r_off = r0 * p->ldx + n0;
+          it.o_off = obase + n0;
+          it.rows = (int32_t)rows;
+          it.ncols = (int32_t)std::min<int64_t>(128, p->ldx - n0);
+          it.mrows = (int32_t)p->kp;
+          it.pad = 0;
+          p->items_tb.push_back(it);
+        }
+      }
+    }
+  }
   // subject table
   p->subj.assign((size_t)p->n_local * kSubjCols, 0);
   for (int i = 0; i < p->n_local; ++i) {
@@ -318,6 +375,9 @@ void set_pointers(srm_plan* p) {
   d.scal = region<double>(p, SRM_R_SCAL);
   d.st = region<double>(p, I_ST);
   d.gram = p->size[SRM_R_GRAM] ? region<double>(p, SRM_R_GRAM) : nullptr;
+  d.af = p->size[I_AF] ? region<float>(p, I_AF) : nullptr;
+  d.sf = p->size[I_SF] ? region<float>(p, I_SF) : nullptr;
+  d.np = p->np;
   d.hist = region<double>(p, SRM_R_HIST);
   d.status = region<int32_t>(p, SRM_R_STATUS);
   d.iter = d.status + 4;
@@ -380,6 +440,19 @@ std::vector<Stage> m_stages(srm_plan* p) {
     v.push_back({"advance_iteration", [d](cudaStream_t st) { return launch_set_iteration(d, 0, 1, st); }});
     return v;
   }
+  if (p->flags & SRM_FLAG_TC) {
+    // fp32 X-hat on the tensor cores: A = X S^T / 2 and B = A^T X as 3xTF32
+    v.push_back({"tc_apass", [p, d](cudaStream_t st) {
+                   return launch_tc_apass(p->np, static_cast<const float*>(d.xhat), p->ldx, d.sf,
+                                          d.sf + (int64_t)p->np * p->ldx, p->ldx, p->ldx, d.af, p->np, 0.5f,
+                                          region<ItemA>(p, I_ITEMS_TA), (int)p->items_a.size(), st);
+                 }});
+    v.push_back({"tc_bpass", [p, d](cudaStream_t st) {
+                   return launch_tc_bpass(d.af, p->np, p->np, static_cast<const float*>(d.xhat), p->ldx, d.part,
+                                          p->ldo, (int)p->kp, region<ItemE>(p, I_ITEMS_TB), (int)p->items_tb.size(),
+                                          st);
+                 }});
+  } else {
   v.push_back({"contract_a", [p, d](cudaStream_t st) {
                  return launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
                                           0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
@@ -388,6 +461,7 @@ std::vector<Stage> m_stages(srm_plan* p) {
                  return launch_contract_e((int)p->kp, SRM_F64, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
                                           region<ItemE>(p, I_ITEMS_EX), (int)p->items_ex.size(), st);
                }});
+  }
   v.push_back({"reduce_chunks", [d](cudaStream_t st) { return launch_reduce_chunks(d, st); }});
   v.push_back({"gram_from_b", [p, d](cudaStream_t st) {
                  return launch_contract_a((int)p->kp, SRM_F64, d.bred, p->ldo, d.S, p->ldx, p->ldx, d.bred, p->ldo,
@@ -461,6 +535,9 @@ int srm_plan_create(srm_plan** out, int dtype, int n_local, const int64_t* n_vox
   p->counts.assign(counts_per_rank, counts_per_rank + world_size);
   p->flags = flags;
   if (world_size == 1) p->flags |= SRM_FLAG_ORDERED;
+  if ((p->flags & SRM_FLAG_TC) && (dtype != SRM_F32 || !tc_supported((int)k))) p->flags &= ~SRM_FLAG_TC;
+  if ((p->flags & SRM_FLAG_TC) && (p->flags & SRM_FLAG_GRAM)) p->flags &= ~SRM_FLAG_TC;
+  p->np = tc_np((int)k);
   p->n_total = 0;
   p->max_local = 0;
   p->global0 = 0;
@@ -515,6 +592,7 @@ int64_t srm_plan_dim(const srm_plan* p, int which) {
     case SRM_D_ITEMS_E: return (int64_t)(p->items_ex.size() + p->items_ea.size());
     case SRM_D_ITEMS_A: return (int64_t)p->items_a.size();
     case SRM_D_CHUNK_ROWS: return p->chunk_rows;
+    case SRM_D_FLAGS: return p->flags;
     case SRM_D_LAUNCHES: return (int64_t)(e_stages(const_cast<srm_plan*>(p)).size() + m_stages(const_cast<srm_plan*>(p)).size());
     default: return -1;
   }
@@ -542,7 +620,8 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
              {I_ORDER_LOCAL, p->order_local.data()}, {I_ITEMS_EX, p->items_ex.data()},
              {I_ITEMS_EA, p->items_ea.data()},  {I_ITEMS_A, p->items_a.data()},
              {I_ITEMS_G, p->items_g.data()},     {I_ITEMS_GRAM, p->items_gram.data()},
-             {I_ITEMS_BG, p->items_bg.data()}};
+             {I_ITEMS_BG, p->items_bg.data()},   {I_ITEMS_TB, p->items_tb.data()},
+             {I_ITEMS_TA, p->items_ta.data()},   {I_ITEMS_TG, p->items_tg.data()}};
   for (const Up& u : ups) {
     if (p->size[u.r] == 0) continue;
     e = cudaMemcpy(p->ws + p->off[u.r], u.src, p->size[u.r], cudaMemcpyHostToDevice);
@@ -562,6 +641,12 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     e = launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp, 0.5, nullptr, 0, 0);
   if (e == cudaSuccess)
     e = launch_contract_a((int)p->kp, SRM_F64, d.bred, p->ldo, d.S, p->ldx, p->ldx, d.bred, p->ldo, 0.5, nullptr, 0, 0);
+  if (e == cudaSuccess && (p->flags & SRM_FLAG_TC))
+    e = launch_contract_e((int)p->kp, SRM_F32, SRM_F32, d.af, p->np, d.af, p->np, d.part, p->ldo, 1.0, nullptr, 0, 0);
+  if (e == cudaSuccess && (p->flags & SRM_FLAG_TC))
+    e = launch_tc_apass(p->np, nullptr, p->ldx, nullptr, nullptr, p->ldx, p->ldx, nullptr, p->np, 0.5f, nullptr, 0, 0);
+  if (e == cudaSuccess && (p->flags & SRM_FLAG_TC))
+    e = launch_tc_bpass(nullptr, p->np, p->np, nullptr, p->ldx, nullptr, p->ldo, (int)p->kp, nullptr, 0, 0);
   if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM))
     e = launch_gram_tiles(p->dtype, d.xhat, p->ldx, d.gram, p->ldx, nullptr, 0, 0);
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
@@ -690,6 +775,17 @@ int srm_finalize(srm_plan* p, void* stream) {
     cudaError_t e = launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
                                       0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
     if (e != cudaSuccess) return cuda_fail(e, "finalize contract_a");
+  }
+  if (p->flags & SRM_FLAG_TC) {
+    // W = A M with M from the exact fp64 Gram of the stored fp32 A, so the
+    // returned W is orthonormal to fp64 precision (acceptance criterion 4)
+    // even though the per-iteration passes run in 3xTF32
+    cudaError_t e = launch_contract_e((int)p->kp, SRM_F32, SRM_F32, d.af, p->np, d.af, p->np, d.part, p->ldo, 1.0,
+                                      region<ItemE>(p, I_ITEMS_TG), (int)p->items_tg.size(), st);
+    if (e == cudaSuccess) e = launch_reduce_chunks(d, st);
+    if (e == cudaSuccess) e = launch_eig_polar(d, 1, st);
+    if (e == cudaSuccess) e = launch_apply_w_f32(d, region<ItemA>(p, I_ITEMS_TA), (int)p->items_ta.size(), st);
+    return check(e, "finalize");
   }
   return check(launch_apply_w(d, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st), "finalize");
 }

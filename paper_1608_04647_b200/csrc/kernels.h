@@ -44,6 +44,15 @@ bool contract_kp_supported(int kp);
 cudaError_t launch_gram_tiles(int x_dtype, const void* X, int64_t ldx, double* out, int64_t ldo,
                               const ItemE* items, int n_items, cudaStream_t stream);
 
+// tcgen05 3xTF32 streaming kernels for fp32 X-hat (tc_fp32.cu)
+int tc_np(int k);
+bool tc_supported(int k);
+cudaError_t launch_tc_apass(int np, const float* X, int64_t ldx, const float* Shi, const float* Slo, int64_t lds,
+                            int64_t ncontract, float* A, int64_t lda, float alpha, const ItemA* items, int n_items,
+                            cudaStream_t st);
+cudaError_t launch_tc_bpass(const float* A, int64_t lda, int np, const float* X, int64_t ldx, double* out,
+                            int64_t ldo, int orows, const ItemE* items, int n_items, cudaStream_t st);
+
 // thread-local message returned by srm_last_error() (defined in capi.cu)
 void set_last_error(const char* where, cudaError_t e);
 

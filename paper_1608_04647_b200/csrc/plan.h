@@ -59,6 +59,9 @@ struct DevPlan {
   double* scal;      // [n_local][8]: {jacobi sweeps, ...}
   double* st;        // [ldx][kp]: S^T (Gram path operand)
   double* gram;      // [n_local][ldx][ldx]: X_i^T X_i (Gram path)
+  float* af;         // [rows][np]: A_i in fp32 (tensor-core path)
+  float* sf;         // [2][np][ldx]: S split into tf32 hi / lo (tensor-core path)
+  int np;            // tensor-core feature padding (multiple of 16)
   double* hist;      // [iterations][hist_stride]
   int32_t* status;
   int32_t* iter;          // device iteration counter (one graph serves every iteration)
@@ -84,6 +87,7 @@ cudaError_t launch_tail_sigma(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_mirror_gram(const DevPlan& p, int first, int count, cudaStream_t s);
 cudaError_t launch_reset(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_apply_w(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);
+cudaError_t launch_apply_w_f32(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);
 
 // stateless helpers
 cudaError_t launch_spd_inverse(double* a, int n, int32_t* status, cudaStream_t s);

@@ -565,6 +565,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_s(DevPlan p) {
     quad += Rt[f * 32 + col] * y;
     St[f * 32 + col] = s;
     if (tin && p.st) p.st[t * kp + f] = s;
+    if (tin && p.sf) {
+      const float sfv = (float)s;
+      const float hi = __uint_as_float(__float_as_uint(sfv) & 0xFFFFE000u);
+      p.sf[(int64_t)f * p.ldx + t] = hi;
+      p.sf[(int64_t)(p.np + f) * p.ldx + t] = sfv - hi;
+    }
     if (tin) {
       double* sp = p.S + (int64_t)f * p.ldx + t;
       const double old = *sp;
@@ -663,6 +669,26 @@ __global__ void k_reset(DevPlan p) {
 // ---------------------------------------------------------------------------
 // apply_w: W_i[r][f] = sum_c A_i[r][c] M_i[c][f]  (row tiles of 128)
 // ---------------------------------------------------------------------------
+// fp32 A (tensor-core path): item o_off indexes the [rows][np] fp32 A region
+__global__ void __launch_bounds__(kSmallThreads) k_apply_w_f32(DevPlan p, const ItemA* __restrict__ items) {
+  extern __shared__ __align__(16) double sm[];
+  const ItemA it = items[blockIdx.x];
+  const int i = it.pad;
+  const int K = (int)p.K, kp = (int)p.kp;
+  const double* Mg = p.mmat + (int64_t)i * kp * kp;
+  double* Ms = sm;
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) Ms[e] = Mg[(e / K) * kp + e % K];
+  __syncthreads();
+  const int64_t row0 = it.x_off / p.ldx;
+  for (int e = threadIdx.x; e < it.rows * K; e += blockDim.x) {
+    const int r = e / K, f = e - r * K;
+    const float* a = p.af + (row0 + r) * p.np;
+    double s = 0.0;
+    for (int c = 0; c < K; ++c) s += (double)a[c] * Ms[c * K + f];
+    p.wout[(row0 + r) * K + f] = s;
+  }
+}
+
 __global__ void __launch_bounds__(kSmallThreads) k_apply_w(DevPlan p, const ItemA* __restrict__ items) {
   extern __shared__ __align__(16) double sm[];
   const ItemA it = items[blockIdx.x];
@@ -890,6 +916,15 @@ cudaError_t launch_apply_w(const DevPlan& p, const void* items_a, int n_items, c
   if (e != cudaSuccess) return e;
   if (n_items == 0) return cudaSuccess;
   k_apply_w<<<n_items, kSmallThreads, bytes, s>>>(p, static_cast<const ItemA*>(items_a));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_w_f32(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s) {
+  const size_t bytes = (size_t)p.K * p.K * sizeof(double);
+  cudaError_t e = set_smem((const void*)k_apply_w_f32, bytes);
+  if (e != cudaSuccess) return e;
+  if (n_items == 0) return cudaSuccess;
+  k_apply_w_f32<<<n_items, kSmallThreads, bytes, s>>>(p, static_cast<const ItemA*>(items_a));
   return cudaGetLastError();
 }
 

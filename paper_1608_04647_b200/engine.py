@@ -39,7 +39,7 @@ class SrmEngine:
     """Device state of one worker's subjects for an SRM fit."""
 
     def __init__(self, n_voxels, n_trs, k, iterations, *, storage="f64", world_size=1,
-                 rank=0, counts=None, ordered=True, tolerance=False, gram=False, device=None):
+                 rank=0, counts=None, ordered=True, tolerance=False, gram=False, tc=False, device=None):
         torch = _torch()
         self.lib = _lib.load()
         if not torch.cuda.is_available():
@@ -65,7 +65,8 @@ class SrmEngine:
             flags |= _lib.FLAG_TOLERANCE
         if gram:
             flags |= _lib.FLAG_GRAM
-        self.gram = bool(gram)
+        if tc:
+            flags |= _lib.FLAG_TC
         self.ordered = bool(ordered) or self.world_size == 1
         plan = ctypes.c_void_p()
         varr = (ctypes.c_int64 * self.n_local)(*self.n_voxels)
@@ -88,6 +89,9 @@ class SrmEngine:
         self.n_slots = d(_lib.D_N_SLOTS)
         self.slot0 = d(_lib.D_SLOT_OFFSET)
         self.row_off = np.concatenate([[0], np.cumsum(self.n_voxels)[:-1]]).astype(np.int64)
+        eff = d(_lib.D_FLAGS)
+        self.gram = bool(eff & _lib.FLAG_GRAM)
+        self.tc = bool(eff & _lib.FLAG_TC)
         self._graph = None
         self._staging = {}
 

@@ -338,22 +338,39 @@ def _storage_for(subjects, storage):
     return "f32" if all(f32) else "f64"
 
 
-def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None):
-    """'gram' or 'stream' from the fp64 tensor-core flop count of each path.
+# B200 rates used by the cost model (measured on this pool: DMMA 37.1 TF/s peak, ~30 sustained
+# in the contraction kernels; HBM copy 6.55 TB/s; 3xTF32 tcgen05 ~0.9 PF/s of tf32 MMA)
+_DMMA_FLOPS = 30e12
+_HBM_BYTES = 6.0e12
+_TF32_FLOPS = 0.9e15
 
-    stream: per iteration two passes over X-hat (A = X S^T / 2, B = A^T X),
-            4 V T K flops per subject.
-    gram:   one-time X^T X (upper 128-tiles, V T^2 flops), then 2 K T^2 per
-            subject-iteration for B = S G / 2, plus one final A pass.
+
+def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f64"):
+    """'gram' or 'stream' from an estimate of each path's device time.
+
+    stream: per iteration two passes over X-hat (A = X S^T / 2, B = A^T X):
+            4 V T K flops per subject on the FP64 tensor pipe, or -- for fp32
+            X-hat on the tcgen05 3xTF32 path -- max(HBM time of 2 reads, MMA time).
+    gram:   one-time X^T X (upper 128-tiles, V T^2 flops on DMMA), then 2 K T^2
+            per subject-iteration for B = S G / 2, plus one final A pass.
     """
     kp = -(-k // 8) * 8
     ldx = -(-n_trs // 32) * 32
     nt = -(-ldx // 128)
+    b = 8 if storage == "f64" else 4
+    tc = storage == "f32" and -(-k // 16) * 16 <= 128
     stream = 0.0
     gram = 0.0
     for v in n_voxels:
-        stream += iterations * 2 * (2.0 * v * ldx * kp)
-        gram += nt * (nt + 1) / 2 * 128 * 128 * 2.0 * v + iterations * 2.0 * kp * ldx * ldx + 2.0 * v * ldx * kp
+        if tc:
+            np16 = -(-k // 16) * 16
+            per_pass = max(v * ldx * b / _HBM_BYTES, 3 * 2.0 * v * ldx * max(np16, 128) / _TF32_FLOPS)
+            stream += iterations * 2 * per_pass
+            final_a = per_pass
+        else:
+            stream += iterations * 2 * (2.0 * v * ldx * kp) / _DMMA_FLOPS
+            final_a = 2.0 * v * ldx * kp / _DMMA_FLOPS
+        gram += (nt * (nt + 1) / 2 * 128 * 128 * 2.0 * v + iterations * 2.0 * kp * ldx * ldx) / _DMMA_FLOPS + final_a
     need = len(n_voxels) * ldx * ldx * 8
     if free_bytes is not None and need > 0.25 * free_bytes:
         return "stream"
@@ -361,7 +378,8 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None):
 
 
 def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=True,
-        keep_on_device=False, device=None, engine_out=None, timings=None, algorithm="auto"):
+        keep_on_device=False, device=None, engine_out=None, timings=None, algorithm="auto",
+        tensor_cores=True):
     """Run the distributed EM; ``subjects`` are this worker's share (srm.py:216).
 
     Every worker calls this with the same config and its own communicator
@@ -379,6 +397,9 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     ``"gram"`` (one-time X^T X, then T x T algebra per iteration) or
     ``"auto"`` (:func:`choose_algorithm`).  Both compute the reference's
     iteration exactly; they differ only in rounding.
+    ``tensor_cores``: for fp32 X-hat on the streaming path, run the two passes
+    as 3xTF32 tcgen05 MMAs (error ~1e-6, inside the 1e-4 fp32 tolerance);
+    ``False`` keeps every contraction in fp64 on DMMA.
     """
     clock = _PhaseClock(timings)
     config.validate()
@@ -406,16 +427,18 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
         ordered = comm.size == 1 or table <= (64 << 20) or not hasattr(comm, "all_reduce_sum")
 
     n_vox = [int(s.X.shape[0]) for s in subjects]
+    store = _storage_for(subjects, storage)
     if algorithm == "auto":
         torch = _torch()
         free, _ = torch.cuda.mem_get_info(device)
-        algorithm = choose_algorithm(n_vox, n_trs, k, config.iterations, free)
+        algorithm = choose_algorithm(n_vox, n_trs, k, config.iterations, free,
+                                     storage=store if tensor_cores else "f64")
     if algorithm not in ("stream", "gram"):
         raise ConfigError("algorithm must be 'auto', 'stream' or 'gram'")
     eng = SrmEngine(n_vox, n_trs, k, config.iterations,
-                    storage=_storage_for(subjects, storage), world_size=comm.size, rank=comm.rank,
+                    storage=store, world_size=comm.size, rank=comm.rank,
                     counts=counts, ordered=ordered, tolerance=config.tolerance is not None,
-                    gram=algorithm == "gram", device=device)
+                    gram=algorithm == "gram", tc=bool(tensor_cores) and store == "f32", device=device)
     if engine_out is not None:
         engine_out.append(eng)
     # the init draws depend only on (seed, global index, V, k): overlap them with the upload

@@ -196,3 +196,33 @@ def test_gram_cfg1_full_size_vs_oracle(srm):
     _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, "cfg1 gram")
     ref_ll = np.array([x["ll"] for x in ref["iters"]])
     assert np.max(np.abs(np.array(m.log_likelihood) - ref_ll) / np.abs(ref_ll)) <= TOL64
+
+
+@pytest.mark.parametrize("name", ["em_recipe_f32", "em_smooth_f32"])
+def test_tensor_core_fp32_path(srm, name):
+    """fp32 X-hat through the tcgen05 3xTF32 streaming kernels, every iteration within 1e-4."""
+    g = load_golden(name)
+    xs = golden_subjects(g)
+    k, iters, seed = int(g["k"]), int(g["iterations"]), int(g["seed"])
+    engines = []
+    for n in range(1, iters + 1):
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=k, iterations=n, seed=seed), algorithm="stream",
+                    tensor_cores=True, engine_out=engines)
+        assert engines[-1].tc, "tensor-core path not selected"
+        it = n - 1
+        _check_model(m, g[f"it{it}_S"], g[f"it{it}_sigma_s"], g[f"it{it}_rho2"],
+                     [g[f"it{it}_W{i}"] for i in range(len(xs))], TOL32, f"{name} tc it{it}")
+    # the split-precision error is ~1e-6: far inside the fp32 tolerance
+    assert nrel(m.S, g[f"it{iters - 1}_S"]) <= 1e-5
+
+
+def test_tensor_core_fp32_recipe_vs_oracle(srm):
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(4, 3000, 400, 100, seed=21, dtype="f32")
+    ref = orc.run_em(xs, 100, 4, seed=0)
+    for n in (1, 4):
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=100, iterations=n, seed=0), algorithm="stream",
+                    tensor_cores=True)
+        r = ref["iters"][n - 1]
+        _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL32, f"tc recipe it{n - 1}")
