@@ -302,23 +302,28 @@ void build_work(srm_plan* p) {
         p->items_tg.push_back(g);
       }
     }
-    for (const ItemA& a : p->items_a) {
-      ItemA t = a;
-      t.o_off = (a.x_off / p->ldx) * p->np;
-      p->items_ta.push_back(t);
+    for (int i = 0; i < p->n_local; ++i) {
+      for (int64_t r = 0; r < p->V[i]; r += kTcRows) {
+        ItemA t;
+        t.x_off = (p->row_off[i] + r) * p->ldx;
+        t.o_off = (p->row_off[i] + r) * p->np;
+        t.rows = (int32_t)std::min<int64_t>(kTcRows, p->V[i] - r);
+        t.pad = i;
+        p->items_ta.push_back(t);
+      }
     }
     for (int i = 0; i < p->n_local; ++i) {
       for (int64_t ch = 0; ch < p->nchunk[i]; ++ch) {
         const int64_t r0 = p->row_off[i] + ch * cr;
         const int64_t rows = std::max<int64_t>(0, std::min<int64_t>(cr, p->V[i] - ch * cr));
         const int64_t obase = (p->chunk0[i] + ch) * p->kp * p->ldo;
-        for (int64_t n0 = 0; n0 < p->ldx; n0 += 128) {
+        for (int64_t n0 = 0; n0 < p->ldx; n0 += kTcRows) {
           ItemE it;
           it.l_off = r0 * p->np;
           it.r_off = r0 * p->ldx + n0;
           it.o_off = obase + n0;
           it.rows = (int32_t)rows;
-          it.ncols = (int32_t)std::min<int64_t>(128, p->ldx - n0);
+          it.ncols = (int32_t)std::min<int64_t>(kTcRows, p->ldx - n0);
           it.mrows = (int32_t)p->kp;
           it.pad = 0;
           p->items_tb.push_back(it);
@@ -445,10 +450,10 @@ std::vector<Stage> m_stages(srm_plan* p) {
     v.push_back({"tc_apass", [p, d](cudaStream_t st) {
                    return launch_tc_apass(p->np, static_cast<const float*>(d.xhat), p->ldx, d.sf,
                                           d.sf + (int64_t)p->np * p->ldx, p->ldx, p->ldx, d.af, p->np, 0.5f,
-                                          region<ItemA>(p, I_ITEMS_TA), (int)p->items_a.size(), st);
+                                          region<ItemA>(p, I_ITEMS_TA), (int)p->items_ta.size(), st);
                  }});
     v.push_back({"tc_bpass", [p, d](cudaStream_t st) {
-                   return launch_tc_bpass(d.af, p->np, p->np, static_cast<const float*>(d.xhat), p->ldx, d.part,
+                   return launch_tc_bpass(p->np, d.af, p->np, static_cast<const float*>(d.xhat), p->ldx, d.part,
                                           p->ldo, (int)p->kp, region<ItemE>(p, I_ITEMS_TB), (int)p->items_tb.size(),
                                           st);
                  }});
@@ -646,7 +651,7 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
   if (e == cudaSuccess && (p->flags & SRM_FLAG_TC))
     e = launch_tc_apass(p->np, nullptr, p->ldx, nullptr, nullptr, p->ldx, p->ldx, nullptr, p->np, 0.5f, nullptr, 0, 0);
   if (e == cudaSuccess && (p->flags & SRM_FLAG_TC))
-    e = launch_tc_bpass(nullptr, p->np, p->np, nullptr, p->ldx, nullptr, p->ldo, (int)p->kp, nullptr, 0, 0);
+    e = launch_tc_bpass(p->np, nullptr, p->np, nullptr, p->ldx, nullptr, p->ldo, (int)p->kp, nullptr, 0, 0);
   if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM))
     e = launch_gram_tiles(p->dtype, d.xhat, p->ldx, d.gram, p->ldx, nullptr, 0, 0);
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");

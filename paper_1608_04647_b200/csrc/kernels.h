@@ -50,8 +50,9 @@ bool tc_supported(int k);
 cudaError_t launch_tc_apass(int np, const float* X, int64_t ldx, const float* Shi, const float* Slo, int64_t lds,
                             int64_t ncontract, float* A, int64_t lda, float alpha, const ItemA* items, int n_items,
                             cudaStream_t st);
-cudaError_t launch_tc_bpass(const float* A, int64_t lda, int np, const float* X, int64_t ldx, double* out,
+cudaError_t launch_tc_bpass(int np, const float* A, int64_t lda, const float* X, int64_t ldx, double* out,
                             int64_t ldo, int orows, const ItemE* items, int n_items, cudaStream_t st);
+constexpr int kTcRows = 256;  // A-pass rows per CTA / B-pass TRs per CTA
 
 // thread-local message returned by srm_last_error() (defined in capi.cu)
 void set_last_error(const char* where, cudaError_t e);

@@ -24,7 +24,6 @@ namespace srm {
 
 namespace {
 
-constexpr int kTcThreads = 128;
 constexpr int kTcBK = 32;  // K (contraction) elements per stage
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -94,50 +93,92 @@ __device__ __forceinline__ int kcore(int r, int k) {
 
 __host__ __device__ constexpr int tmem_cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256; }
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+               ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                 "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+
+// A operand from TMEM: D[tmem] (+)= A[tmem] * B[smem desc]
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a, uint64_t db, uint32_t idesc, int acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+               :: "r"(d), "r"(a), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// Each thread owns one TMEM lane of one 128-row half: it writes its 32 raw
+// fp32 values (the MMA reads them as tf32 = hi) and their residuals (lo) into
+// the A-operand buffer at column base `col`.
+__device__ __forceinline__ void store_split_row(uint32_t tmem_lane_base, uint32_t col, const float* vals) {
+  uint32_t raw[16], lo[16];
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float x = vals[half * 16 + j];
+      raw[j] = __float_as_uint(x);
+      lo[j] = __float_as_uint(x - tf32_hi(x));
+    }
+    tmem_st16(tmem_lane_base + col + half * 16, raw);
+    tmem_st16(tmem_lane_base + col + 32 + half * 16, lo);
+  }
+}
+
+constexpr int kTcT = 256;            // threads: two 128-lane halves x 4 warps
+constexpr int kXStride = 36;          // A-pass raw row stride (floats): 16B aligned, LDS.128 conflict-free
+
+// TMEM columns: accumulators of the two halves at [0,128) and [128,256); A
+// operand buffers b in {0,1} at 256 + 128 b + 64 h: raw [0,32), lo [32,64)
+__device__ __forceinline__ uint32_t abuf_col(int b, int h) { return 256u + 128u * b + 64u * h; }
+
 // ---------------------------------------------------------------------------
-// A-pass: Aout[r][f] = alpha * sum_t X[r][t] (S_hi + S_lo)[f][t], r < rows (<= 128)
+// A-pass: Aout[r][f] = alpha * sum_t X[r][t] S[f][t] for r < rows (<= 256)
 // ---------------------------------------------------------------------------
 template <int NP, int STAGES>
-__global__ void __launch_bounds__(kTcThreads) k_tc_apass(const float* __restrict__ X, int64_t ldx,
-                                                          const float* __restrict__ Shi,
-                                                          const float* __restrict__ Slo, int64_t lds,
-                                                          int ncontract, float* __restrict__ Aout,
-                                                          int64_t lda, float alpha,
-                                                          const ItemA* __restrict__ items) {
-  constexpr int XT = 128 * kTcBK;  // floats per X tile
-  constexpr int ST = NP * kTcBK;   // floats per S tile
-  constexpr int STAGE = 2 * XT + 2 * ST;
+__global__ void __launch_bounds__(kTcT) k_tc_apass(const float* __restrict__ X, int64_t ldx,
+                                                    const float* __restrict__ Shi, const float* __restrict__ Slo,
+                                                    int64_t lds, int ncontract, float* __restrict__ Aout,
+                                                    int64_t lda, float alpha, const ItemA* __restrict__ items) {
+  constexpr int XS = 256 * kXStride;  // floats per raw X stage
+  constexpr int SS = NP * kTcBK;      // floats per S tile (hi or lo)
+  constexpr int STAGE = XS + 2 * SS;
   extern __shared__ __align__(1024) float smem[];
-  __shared__ __align__(8) uint64_t mbar[STAGES];
+  __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint32_t tmem_base;
   const ItemA it = items[blockIdx.x];
   const float* Xb = X + it.x_off;
   const int rows = it.rows;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int h = warp >> 2, q = warp & 3;
+  const int row = 128 * h + 32 * q + lane;
   const int nst = ncontract / kTcBK;
 
-  if (tid < 32) tmem_alloc(&tmem_base, tmem_cols(NP));
+  if (warp == 0) tmem_alloc(&tmem_base, 512);
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&mbar[s], 1);
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
+  const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
 
   auto load = [&](int s) {
-    float* base = smem + (s % STAGES) * STAGE;
+    float* xs = smem + (s % STAGES) * STAGE;
+    float* sh = xs + XS;
+    float* sl = sh + SS;
     const int t0 = s * kTcBK;
-    for (int i = tid; i < 128 * (kTcBK / 4); i += kTcThreads) {
+    for (int i = tid; i < 256 * 8; i += kTcT) {
       const int r = i >> 3, c = (i & 7) * 4;
       const bool ok = r < rows;
-      cp_async16(base + kcore(r, c), Xb + (ok ? (int64_t)r * ldx + t0 + c : 0), ok);
+      cp_async16(xs + r * kXStride + c, Xb + (ok ? (int64_t)r * ldx + t0 + c : 0), ok);
     }
-    float* sh = base + 2 * XT;
-    float* sl = sh + ST;
-    for (int i = tid; i < NP * (kTcBK / 4); i += kTcThreads) {
-      const int r = i >> 3, c = (i & 7) * 4;
+    for (int i = tid; i < NP * 8; i += kTcT) {
+      // warp-contiguous core writes: 8 consecutive threads fill one 128-B core matrix
+      const int core = i >> 3, rr = i & 7;
+      const int r = (core >> 3) * 8 + rr, c = (core & 7) * 4;
       cp_async16(sh + kcore(r, c), Shi + (int64_t)r * lds + t0 + c, true);
       cp_async16(sl + kcore(r, c), Slo + (int64_t)r * lds + t0 + c, true);
     }
@@ -150,54 +191,64 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_apass(const float* __restrict
   }
   constexpr uint32_t idesc = idesc_tf32(128, NP);
   for (int s = 0; s < nst; ++s) {
+    const int b = s & 1;
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    float* base = smem + (s % STAGES) * STAGE;
-    float* xh = base;
-    float* xl = base + XT;
-    for (int e = tid; e < XT; e += kTcThreads) {
-      const float x = xh[e];
-      const float h = tf32_hi(x);
-      xh[e] = h;
-      xl[e] = x - h;
+    // the TMEM A buffer b was read by the MMAs of stage s - 2
+    if (s >= 2) mbar_wait(&mbar[b], ((s - 2) >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    {
+      const float* xr = smem + (s % STAGES) * STAGE + row * kXStride;
+      float vals[32];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + 4 * j);
+        vals[4 * j] = v.x;
+        vals[4 * j + 1] = v.y;
+        vals[4 * j + 2] = v.z;
+        vals[4 * j + 3] = v.w;
+      }
+      store_split_row(tlane, abuf_col(b, h), vals);
+      asm volatile("tcgen05.wait::st.sync.aligned;");
     }
     asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t a_h = smem_u32(xh), a_l = smem_u32(xl);
-      const uint32_t b_h = smem_u32(base + 2 * XT), b_l = smem_u32(base + 2 * XT + ST);
+      const float* sh = smem + (s % STAGES) * STAGE + XS;
+      const uint32_t bh = smem_u32(sh), bl = smem_u32(sh + SS);
 #pragma unroll
-      for (int ks = 0; ks < kTcBK / 8; ++ks) {
-        const uint32_t off = ks * 256;
-        const uint64_t dah = umma_desc(a_h + off, 128, kTcBK * 32);
-        const uint64_t dal = umma_desc(a_l + off, 128, kTcBK * 32);
-        const uint64_t dbh = umma_desc(b_h + off, 128, kTcBK * 32);
-        const uint64_t dbl = umma_desc(b_l + off, 128, kTcBK * 32);
-        mma_tf32(tmem, dah, dbh, idesc, (s | ks) != 0);
-        mma_tf32(tmem, dah, dbl, idesc, 1);
-        mma_tf32(tmem, dal, dbh, idesc, 1);
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t acc = tmem + 128u * hh;
+        const uint32_t ar = tmem + abuf_col(b, hh), al = ar + 32;
+#pragma unroll
+        for (int ks = 0; ks < kTcBK / 8; ++ks) {
+          const uint64_t dbh = umma_desc(bh + ks * 256, 128, kTcBK * 32);
+          const uint64_t dbl = umma_desc(bl + ks * 256, 128, kTcBK * 32);
+          mma_tf32_ts(acc, ar + ks * 8, dbh, idesc, (s | ks) != 0);
+          mma_tf32_ts(acc, ar + ks * 8, dbl, idesc, 1);
+          mma_tf32_ts(acc, al + ks * 8, dbh, idesc, 1);
+        }
       }
-      mma_commit(&mbar[s % STAGES]);
+      mma_commit(&mbar[b]);
     }
+    // refill the stage read by the MMAs of s - 1 (its S tile) with stage s + STAGES - 1
     const int ns = s + STAGES - 1;
     if (ns < nst) {
-      if (s >= 1) mbar_wait(&mbar[(s - 1) % STAGES], ((s - 1) / STAGES) & 1);
+      if (s >= 1) mbar_wait(&mbar[(s - 1) & 1], ((s - 1) >> 1) & 1);
       load(ns);
     }
     cp_async_commit();
   }
   cp_async_wait<0>();
-  mbar_wait(&mbar[(nst - 1) % STAGES], ((nst - 1) / STAGES) & 1);
+  mbar_wait(&mbar[(nst - 1) & 1], ((nst - 1) >> 1) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;");
-
-  const int warp = tid >> 5, lane = tid & 31;
-  const int row = warp * 32 + lane;
   float* out = Aout + it.o_off;
 #pragma unroll
   for (int c0 = 0; c0 < NP; c0 += 16) {
     float v[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+    tmem_ld16(tlane + 128u * h + c0, v);
     if (row < rows) {
       float4* o = reinterpret_cast<float4*>(out + (int64_t)row * lda + c0);
 #pragma unroll
@@ -207,7 +258,7 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_apass(const float* __restrict
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (tid < 32) tmem_free(tmem, tmem_cols(NP));
+  if (warp == 0) tmem_free(tmem, 512);
 }
 
 template <int NP>
@@ -215,7 +266,7 @@ cudaError_t run_apass(const float* X, int64_t ldx, const float* Shi, const float
                       int64_t ncontract, float* A, int64_t lda, float alpha, const ItemA* items, int n_items,
                       cudaStream_t st) {
   constexpr int STAGES = 3;
-  constexpr int bytes = STAGES * (2 * 128 * kTcBK + 2 * NP * kTcBK) * 4;
+  constexpr int bytes = STAGES * (256 * kXStride + 2 * NP * kTcBK) * 4;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k_tc_apass<NP, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -223,41 +274,41 @@ cudaError_t run_apass(const float* X, int64_t ldx, const float* Shi, const float
     configured = true;
   }
   if (n_items == 0) return cudaSuccess;
-  k_tc_apass<NP, STAGES><<<n_items, kTcThreads, bytes, st>>>(X, ldx, Shi, Slo, lds, (int)ncontract, A, lda, alpha,
-                                                            items);
+  k_tc_apass<NP, STAGES><<<n_items, kTcT, bytes, st>>>(X, ldx, Shi, Slo, lds, (int)ncontract, A, lda, alpha, items);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
-// B-pass: out[f][t0 + t] = sum_{v < rows} A[v][f] X[v][t0 + t]  (f < 128, t < 128),
-// written in fp64 for the fixed-order chunk reduction.  Raw tiles land
-// row-major (padded) via cp.async; the split writes hi/lo transposed into the
-// K-major core layout (contraction index v contiguous inside a core).
+// B-pass: out[f][t0 + t] = sum_{v < rows} A[v][f] X[v][t0 + t] for t < 256, f < orows.
+// X^T tile (t lanes x 32 v) goes to TMEM as the A operand; the A features tile
+// is split + transposed into the K-major core layout in smem (B operand).
 // ---------------------------------------------------------------------------
-constexpr int kBN = 128;            // TRs per tile (MMA N)
-constexpr int kBM = 128;            // features per tile (MMA M, zero-padded)
-constexpr int kRawS = kBN + 8;      // raw row stride (floats), == 8 mod 32
+constexpr int kBT = 256;      // TRs per tile (two 128-lane halves)
+constexpr int kAStr = 136;    // raw A stage row stride (floats): == 8 mod 32
 
-__global__ void __launch_bounds__(kTcThreads) k_tc_bpass(const float* __restrict__ A, int64_t lda, int np,
-                                                          const float* __restrict__ X, int64_t ldx,
-                                                          double* __restrict__ out, int64_t ldo, int orows,
-                                                          const ItemE* __restrict__ items) {
-  constexpr int RAWX = kTcBK * kRawS;
-  constexpr int RAWA = kTcBK * kRawS;
-  constexpr int CT = kBN * kTcBK;  // floats per core tile (X or A)
+template <int NP, int STAGES>
+__global__ void __launch_bounds__(kTcT) k_tc_bpass(const float* __restrict__ A, int64_t lda,
+                                                    const float* __restrict__ X, int64_t ldx,
+                                                    double* __restrict__ out, int64_t ldo, int orows,
+                                                    const ItemE* __restrict__ items) {
+  constexpr int XR = kTcBK * kBT;     // raw X stage floats
+  constexpr int AR = kTcBK * kAStr;   // raw A stage floats
+  constexpr int CT = NP * kTcBK;      // core tile floats (hi or lo)
   extern __shared__ __align__(1024) float smem[];
-  float* hl = smem;                         // [2 buffers][xh, xl, ah, al] each CT floats
-  float* raw = smem + 2 * 4 * CT;           // [2 buffers][rawX, rawA]
+  float* core = smem;                               // [2 buffers][hi, lo]
+  float* raw = smem + 2 * 2 * CT;                   // [STAGES][rawX, rawA]
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint32_t tmem_base;
   const ItemE it = items[blockIdx.x];
   const float* Ab = A + it.l_off;
   const float* Xb = X + it.r_off;
   const int rows = it.rows, ncols = it.ncols;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int h = warp >> 2, q = warp & 3;
+  const int tcol = 128 * h + 32 * q + lane;
   const int nst = (rows + kTcBK - 1) / kTcBK;
 
-  if (tid < 32) tmem_alloc(&tmem_base, kBN);
+  if (warp == 0) tmem_alloc(&tmem_base, 512);
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
@@ -267,89 +318,112 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_bpass(const float* __restrict
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
+  const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
 
   auto load = [&](int s) {
-    float* rx = raw + (s & 1) * (RAWX + RAWA);
-    float* ra = rx + RAWX;
+    float* rx = raw + (s % STAGES) * (XR + AR);
+    float* ra = rx + XR;
     const int v0 = s * kTcBK;
-    for (int i = tid; i < kTcBK * (kBN / 4); i += kTcThreads) {
-      const int r = i >> 5, c = (i & 31) * 4;
-      const bool okr = (v0 + r) < rows;
-      const bool okx = okr && c < ncols;
-      cp_async16(rx + r * kRawS + c, Xb + (okx ? (int64_t)(v0 + r) * ldx + c : 0), okx);
-      const bool oka = okr && c < np;
-      cp_async16(ra + r * kRawS + c, Ab + (oka ? (int64_t)(v0 + r) * lda + c : 0), oka);
+    for (int i = tid; i < kTcBK * (kBT / 4); i += kTcT) {
+      const int r = i >> 6, c = (i & 63) * 4;
+      const bool ok = (v0 + r) < rows && c < ncols;
+      cp_async16(rx + r * kBT + c, Xb + (ok ? (int64_t)(v0 + r) * ldx + c : 0), ok);
+    }
+    for (int i = tid; i < kTcBK * (NP / 4); i += kTcT) {
+      const int r = i / (NP / 4), c = (i - r * (NP / 4)) * 4;
+      const bool ok = (v0 + r) < rows;
+      cp_async16(ra + r * kAStr + c, Ab + (ok ? (int64_t)(v0 + r) * lda + c : 0), ok);
     }
   };
 
-  load(0);
-  cp_async_commit();
-  if (nst > 1) load(1);
-  cp_async_commit();
-  constexpr uint32_t idesc = idesc_tf32(kBM, kBN);
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nst) load(s);
+    cp_async_commit();
+  }
+  constexpr uint32_t idesc = idesc_tf32(128, NP);
   for (int s = 0; s < nst; ++s) {
-    cp_async_wait<1>();
+    const int b = s & 1;
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
-    // the hi/lo buffer of stage s was last read by the MMAs of stage s - 2
-    if (s >= 2) mbar_wait(&mbar[s & 1], ((s - 2) >> 1) & 1);
-    float* xh = hl + (s & 1) * 4 * CT;
-    float* xl = xh + CT;
-    float* ah = xl + CT;
-    float* al = ah + CT;
-    const float* rx = raw + (s & 1) * (RAWX + RAWA);
-    const float* ra = rx + RAWX;
-    for (int e = tid; e < CT; e += kTcThreads) {
-      // core-major order: e = group*256 + kgroup*32 + (row & 7)*4 + (k & 3)
-      const int row = (e >> 8) * 8 + ((e >> 2) & 7);
-      const int k = ((e >> 5) & 7) * 4 + (e & 3);
-      const float x = rx[k * kRawS + row];
-      const float a = ra[k * kRawS + row];
-      const float xhv = tf32_hi(x), ahv = tf32_hi(a);
-      xh[e] = xhv;
-      xl[e] = x - xhv;
-      ah[e] = ahv;
-      al[e] = a - ahv;
+    if (s >= 2) mbar_wait(&mbar[b], ((s - 2) >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const float* rx = raw + (s % STAGES) * (XR + AR);
+    const float* ra = rx + XR;
+    {
+      float vals[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) vals[k] = rx[k * kBT + tcol];
+      store_split_row(tlane, abuf_col(b, h), vals);
     }
+    float* ch = core + b * 2 * CT;
+    float* cl = ch + CT;
+    for (int e = tid; e < CT; e += kTcT) {
+      const int r = (e >> 8) * 8 + ((e >> 2) & 7);   // feature
+      const int k = ((e >> 5) & 7) * 4 + (e & 3);    // voxel in the stage
+      const float a = ra[k * kAStr + r];
+      const float hi = tf32_hi(a);
+      ch[e] = hi;
+      cl[e] = a - hi;
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;");
     asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t bh = smem_u32(ch), bl = smem_u32(cl);
 #pragma unroll
-      for (int ks = 0; ks < kTcBK / 8; ++ks) {
-        const uint32_t off = ks * 256;
-        const uint64_t dah = umma_desc(smem_u32(ah) + off, 128, kTcBK * 32);
-        const uint64_t dal = umma_desc(smem_u32(al) + off, 128, kTcBK * 32);
-        const uint64_t dxh = umma_desc(smem_u32(xh) + off, 128, kTcBK * 32);
-        const uint64_t dxl = umma_desc(smem_u32(xl) + off, 128, kTcBK * 32);
-        mma_tf32(tmem, dah, dxh, idesc, (s | ks) != 0);
-        mma_tf32(tmem, dah, dxl, idesc, 1);
-        mma_tf32(tmem, dal, dxh, idesc, 1);
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t acc = tmem + 128u * hh;
+        const uint32_t xr = tmem + abuf_col(b, hh), xl = xr + 32;
+#pragma unroll
+        for (int ks = 0; ks < kTcBK / 8; ++ks) {
+          const uint64_t dbh = umma_desc(bh + ks * 256, 128, kTcBK * 32);
+          const uint64_t dbl = umma_desc(bl + ks * 256, 128, kTcBK * 32);
+          mma_tf32_ts(acc, xr + ks * 8, dbh, idesc, (s | ks) != 0);
+          mma_tf32_ts(acc, xr + ks * 8, dbl, idesc, 1);
+          mma_tf32_ts(acc, xl + ks * 8, dbh, idesc, 1);
+        }
       }
-      mma_commit(&mbar[s & 1]);
+      mma_commit(&mbar[b]);
     }
-    if (s + 2 < nst) load(s + 2);
+    if (s + STAGES - 1 < nst) load(s + STAGES - 1);  // raw stage (s-1) % STAGES was consumed above
     cp_async_commit();
   }
   cp_async_wait<0>();
   mbar_wait(&mbar[(nst - 1) & 1], ((nst - 1) >> 1) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const int warp = tid >> 5, lane = tid & 31;
-  const int f = warp * 32 + lane;
   double* ob = out + it.o_off;
 #pragma unroll
-  for (int c0 = 0; c0 < kBN; c0 += 16) {
+  for (int c0 = 0; c0 < NP; c0 += 16) {
     float v[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
-    if (f < orows) {
+    tmem_ld16(tlane + 128u * h + c0, v);
+    if (tcol < ncols) {
 #pragma unroll
-      for (int j = 0; j < 16; j += 2)
-        if (c0 + j < ncols)
-          *reinterpret_cast<double2*>(ob + (int64_t)f * ldo + c0 + j) = make_double2((double)v[j], (double)v[j + 1]);
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < orows) ob[(int64_t)(c0 + j) * ldo + tcol] = (double)v[j];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (tid < 32) tmem_free(tmem, kBN);
+  if (warp == 0) tmem_free(tmem, 512);
+}
+
+template <int NP>
+cudaError_t run_bpass(const float* A, int64_t lda, const float* X, int64_t ldx, double* out, int64_t ldo,
+                      int orows, const ItemE* items, int n_items, cudaStream_t st) {
+  constexpr int STAGES = 3;
+  constexpr int bytes = (2 * 2 * NP * kTcBK + STAGES * (kTcBK * kBT + kTcBK * kAStr)) * 4;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_tc_bpass<NP, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (n_items == 0) return cudaSuccess;
+  k_tc_bpass<NP, STAGES><<<n_items, kTcT, bytes, st>>>(A, lda, X, ldx, out, ldo, orows, items);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -379,18 +453,19 @@ cudaError_t launch_tc_apass(int np, const float* X, int64_t ldx, const float* Sh
 
 namespace srm {
 
-cudaError_t launch_tc_bpass(const float* A, int64_t lda, int np, const float* X, int64_t ldx, double* out,
+cudaError_t launch_tc_bpass(int np, const float* A, int64_t lda, const float* X, int64_t ldx, double* out,
                             int64_t ldo, int orows, const ItemE* items, int n_items, cudaStream_t st) {
-  constexpr int bytes = (2 * 4 * kBN * kTcBK + 2 * 2 * kTcBK * kRawS) * 4;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_tc_bpass, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (e != cudaSuccess) return e;
-    configured = true;
+  switch (np) {
+    case 16: return run_bpass<16>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
+    case 32: return run_bpass<32>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
+    case 48: return run_bpass<48>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
+    case 64: return run_bpass<64>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
+    case 80: return run_bpass<80>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
+    case 96: return run_bpass<96>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
+    case 112: return run_bpass<112>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
+    case 128: return run_bpass<128>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
+    default: return cudaErrorInvalidValue;
   }
-  if (n_items == 0) return cudaSuccess;
-  k_tc_bpass<<<n_items, kTcThreads, bytes, st>>>(A, lda, np, X, ldx, out, ldo, orows, items);
-  return cudaGetLastError();
 }
 
 }  // namespace srm

@@ -167,7 +167,127 @@ void run(int amn, int bmn, int var) {
          maxerr / maxref, D[0], D[1]); (void)MODE; (void)amn;
 }
 
+
+// A operand from TMEM: lane = row m, 32-bit column = k.  raw at cols [128,160), lo at [160,192)
+__global__ void probe_ts(const float* A, const float* B, float* D) {
+  constexpr int M = 128, K = 32, NN = 112;
+  extern __shared__ __align__(1024) float dyn[];
+  float* sb_hi = dyn;
+  float* sb_lo = sb_hi + NN * K;
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto kmaj = [](int mn, int k) { return (mn >> 3) * (K / 4) * 32 + (k >> 2) * 32 + (mn & 7) * 4 + (k & 3); };
+  for (int e = tid; e < NN * K; e += blockDim.x) {
+    const int n = e / K, k = e % K;
+    const float x = B[n * K + k];
+    const float h = tf32_hi(x);
+    sb_hi[kmaj(n, k)] = h;
+    sb_lo[kmaj(n, k)] = x - h;
+  }
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(smem_u32(&tmem_base)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&mbar)), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  // each thread stores its row: raw (32 cols) and lo (32 cols)
+  {
+    const int row = warp * 32 + lane;
+    uint32_t raw[32], lo[32];
+    for (int k = 0; k < K; ++k) {
+      const float x = A[row * K + k];
+      raw[k] = __float_as_uint(x);
+      lo[k] = __float_as_uint(x - tf32_hi(x));
+    }
+    const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16);
+    for (int c = 0; c < 32; c += 16) {
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                   :: "r"(base + 128 + c), "r"(raw[c]), "r"(raw[c+1]), "r"(raw[c+2]), "r"(raw[c+3]), "r"(raw[c+4]), "r"(raw[c+5]), "r"(raw[c+6]), "r"(raw[c+7]),
+                      "r"(raw[c+8]), "r"(raw[c+9]), "r"(raw[c+10]), "r"(raw[c+11]), "r"(raw[c+12]), "r"(raw[c+13]), "r"(raw[c+14]), "r"(raw[c+15]));
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                   :: "r"(base + 160 + c), "r"(lo[c]), "r"(lo[c+1]), "r"(lo[c+2]), "r"(lo[c+3]), "r"(lo[c+4]), "r"(lo[c+5]), "r"(lo[c+6]), "r"(lo[c+7]),
+                      "r"(lo[c+8]), "r"(lo[c+9]), "r"(lo[c+10]), "r"(lo[c+11]), "r"(lo[c+12]), "r"(lo[c+13]), "r"(lo[c+14]), "r"(lo[c+15]));
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t id = idesc_tf32(M, NN, 0, 0);
+    for (int ks = 0; ks < K / 8; ++ks) {
+      const uint64_t dbh = sdesc(smem_u32(sb_hi) + ks * 256, 128, (K / 4) * 128);
+      const uint64_t dbl = sdesc(smem_u32(sb_lo) + ks * 256, 128, (K / 4) * 128);
+      const uint32_t ar = tmem + 128 + ks * 8, al = tmem + 160 + ks * 8;
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                   :: "r"(tmem), "r"(ar), "l"(dbh), "r"(id), "r"(ks > 0 ? 1 : 0));
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                   :: "r"(tmem), "r"(ar), "l"(dbl), "r"(id), "r"(1));
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                   :: "r"(tmem), "r"(al), "l"(dbh), "r"(id), "r"(1));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_u32(&mbar)));
+  }
+  {
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                   : "=r"(done) : "r"(smem_u32(&mbar)), "r"(0));
+    }
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int row = warp * 32 + lane;
+  for (int c0 = 0; c0 < NN; c0 += 16) {
+    uint32_t r[16];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(tmem + ((uint32_t)(warp * 32) << 16) + c0));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    for (int j = 0; j < 16; ++j) D[row * NN + c0 + j] = __uint_as_float(r[j]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(256));
+}
+
+void run_ts() {
+  constexpr int M = 128, K = 32, NN = 112;
+  std::vector<float> A(M * K), B(NN * K), D(M * NN);
+  srand(11);
+  for (auto& x : A) x = (float)rand() / RAND_MAX * 2 - 1;
+  for (auto& x : B) x = (float)rand() / RAND_MAX * 2 - 1;
+  float *dA, *dB, *dD;
+  CK(cudaMalloc(&dA, A.size() * 4)); CK(cudaMalloc(&dB, B.size() * 4)); CK(cudaMalloc(&dD, D.size() * 4));
+  CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemset(dD, 0, D.size() * 4));
+  const int bytes = 2 * NN * K * 4;
+  probe_ts<<<1, 128, bytes>>>(dA, dB, dD);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+  double maxerr = 0, maxref = 0;
+  for (int m = 0; m < M; ++m)
+    for (int n = 0; n < NN; ++n) {
+      double ref = 0;
+      for (int k = 0; k < K; ++k) ref += (double)A[m * K + k] * B[n * K + k];
+      maxerr = fmax(maxerr, fabs(ref - D[m * NN + n]));
+      maxref = fmax(maxref, fabs(ref));
+    }
+  printf("TS (A in TMEM) N=%d: rel err %.3e  D[0]=%f\n", NN, maxerr / maxref, D[0]);
+}
+
 int main() {
+  run_ts();
   for (int var = 0; var < 3; ++var) {
     run<64, 0>(1, 0, var);
     run<64, 0>(0, 1, var);
