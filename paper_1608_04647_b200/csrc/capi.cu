@@ -102,6 +102,7 @@ struct srm_plan {
   cudaStream_t cap_stream = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
+  TmaMap tm_x_a, tm_s, tm_a, tm_x_b;  // tensor-core path TMA maps (bound at srm_plan_bind)
 };
 
 namespace {
@@ -448,14 +449,12 @@ std::vector<Stage> m_stages(srm_plan* p) {
   if (p->flags & SRM_FLAG_TC) {
     // fp32 X-hat on the tensor cores: A = X S^T / 2 and B = A^T X as 3xTF32
     v.push_back({"tc_apass", [p, d](cudaStream_t st) {
-                   return launch_tc_apass(p->np, static_cast<const float*>(d.xhat), p->ldx, d.sf,
-                                          d.sf + (int64_t)p->np * p->ldx, p->ldx, p->ldx, d.af, p->np, 0.5f,
+                   return launch_tc_apass(p->np, p->tm_x_a, p->tm_s, p->ldx, d.af, p->np, 0.5f,
                                           region<ItemA>(p, I_ITEMS_TA), (int)p->items_ta.size(), st);
                  }});
     v.push_back({"tc_bpass", [p, d](cudaStream_t st) {
-                   return launch_tc_bpass(p->np, d.af, p->np, static_cast<const float*>(d.xhat), p->ldx, d.part,
-                                          p->ldo, (int)p->kp, region<ItemE>(p, I_ITEMS_TB), (int)p->items_tb.size(),
-                                          st);
+                   return launch_tc_bpass(p->np, p->tm_a, p->tm_x_b, p->ldx, d.part, p->ldo, (int)p->kp,
+                                          region<ItemE>(p, I_ITEMS_TB), (int)p->items_tb.size(), st);
                  }});
   } else {
   v.push_back({"contract_a", [p, d](cudaStream_t st) {
@@ -648,10 +647,16 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     e = launch_contract_a((int)p->kp, SRM_F64, d.bred, p->ldo, d.S, p->ldx, p->ldx, d.bred, p->ldo, 0.5, nullptr, 0, 0);
   if (e == cudaSuccess && (p->flags & SRM_FLAG_TC))
     e = launch_contract_e((int)p->kp, SRM_F32, SRM_F32, d.af, p->np, d.af, p->np, d.part, p->ldo, 1.0, nullptr, 0, 0);
-  if (e == cudaSuccess && (p->flags & SRM_FLAG_TC))
-    e = launch_tc_apass(p->np, nullptr, p->ldx, nullptr, nullptr, p->ldx, p->ldx, nullptr, p->np, 0.5f, nullptr, 0, 0);
-  if (e == cudaSuccess && (p->flags & SRM_FLAG_TC))
-    e = launch_tc_bpass(p->np, nullptr, p->np, nullptr, p->ldx, nullptr, p->ldo, (int)p->kp, nullptr, 0, 0);
+  if (e == cudaSuccess && (p->flags & SRM_FLAG_TC)) {
+    const float* xf = static_cast<const float*>(d.xhat);
+    e = make_map_f32(&p->tm_x_a, xf, p->ldx, p->rows_total, p->ldx, 32, 256, true);
+    if (e == cudaSuccess) e = make_map_f32(&p->tm_s, d.sf, p->ldx, 2 * p->np, p->ldx, 32, p->np, true);
+    if (e == cudaSuccess) e = make_map_f32(&p->tm_a, d.af, p->np, p->rows_total, p->np, p->np, 32, false);
+    if (e == cudaSuccess) e = make_map_f32(&p->tm_x_b, xf, p->ldx, p->rows_total, p->ldx, 256, 32, false);
+    if (e != cudaSuccess) return cuda_fail(e, "tensor maps");
+    e = launch_tc_apass(p->np, p->tm_x_a, p->tm_s, p->ldx, d.af, p->np, 0.5f, nullptr, 0, 0);
+    if (e == cudaSuccess) e = launch_tc_bpass(p->np, p->tm_a, p->tm_x_b, p->ldx, d.part, p->ldo, (int)p->kp, nullptr, 0, 0);
+  }
   if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM))
     e = launch_gram_tiles(p->dtype, d.xhat, p->ldx, d.gram, p->ldx, nullptr, 0, 0);
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");

@@ -47,11 +47,16 @@ cudaError_t launch_gram_tiles(int x_dtype, const void* X, int64_t ldx, double* o
 // tcgen05 3xTF32 streaming kernels for fp32 X-hat (tc_fp32.cu)
 int tc_np(int k);
 bool tc_supported(int k);
-cudaError_t launch_tc_apass(int np, const float* X, int64_t ldx, const float* Shi, const float* Slo, int64_t lds,
-                            int64_t ncontract, float* A, int64_t lda, float alpha, const ItemA* items, int n_items,
-                            cudaStream_t st);
-cudaError_t launch_tc_bpass(int np, const float* A, int64_t lda, const float* X, int64_t ldx, double* out,
-                            int64_t ldo, int orows, const ItemE* items, int n_items, cudaStream_t st);
+// opaque 128-byte CUtensorMap (cuda.h) so this header stays driver-API free
+struct alignas(64) TmaMap {
+  unsigned long long opaque[16];
+};
+cudaError_t make_map_f32(TmaMap* m, const float* base, int64_t inner, int64_t outer, int64_t pitch,
+                         int box_inner, int box_outer, bool swizzle128);
+cudaError_t launch_tc_apass(int np, const TmaMap& tmX, const TmaMap& tmS, int64_t ncontract, float* A, int64_t lda,
+                            float alpha, const ItemA* items, int n_items, cudaStream_t st);
+cudaError_t launch_tc_bpass(int np, const TmaMap& tmA, const TmaMap& tmXb, int64_t ldx, double* out, int64_t ldo,
+                            int orows, const ItemE* items, int n_items, cudaStream_t st);
 constexpr int kTcRows = 256;  // A-pass rows per CTA / B-pass TRs per CTA
 
 // thread-local message returned by srm_last_error() (defined in capi.cu)

@@ -17,6 +17,8 @@
 // the two K cores of an MMA step, SBO between 8-row groups), described by
 // sm100 UMMA smem descriptors; one elected thread issues tcgen05.mma and
 // commits to an mbarrier that guards the stage's reuse.
+#include <cuda.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -131,129 +133,185 @@ constexpr int kXStride = 36;          // A-pass raw row stride (floats): 16B ali
 // operand buffers b in {0,1} at 256 + 128 b + 64 h: raw [0,32), lo [32,64)
 __device__ __forceinline__ uint32_t abuf_col(int b, int h) { return 256u + 128u * b + 64u * h; }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp roles (both passes): warps 0-7 consumers (split -> TMEM, epilogue; warp w
+// owns TMEM lanes 32 (w % 4) of half w / 4), warps 8-11 producers (cp.async ring),
+// warp 12 MMA issuer.  mbarriers only -- no CTA-wide barrier in the main loop.
+constexpr int kWsThreads = 320;   // warps 0-7 consumers, warp 8 TMA producer, warp 9 MMA issuer
+constexpr int kProducerWarp = 8;
+constexpr int kMmaWarp = 9;
+
+struct WsBars {
+  uint64_t full[3];   // TMA -> consumers/MMA: stage landed (expect_tx)
+  uint64_t xfree[3];  // consumers -> producer: raw stage read (count 256)
+  uint64_t sfree[3];  // MMA -> producer: smem operand of the stage consumed (count 1)
+  uint64_t tfull[2];  // consumers -> MMA: TMEM (and core) operand buffer b written (count 256)
+  uint64_t tfree[2];  // MMA -> consumers: operand buffer b consumed (count 1)
+  uint64_t accdone;   // MMA -> consumers: accumulators final (count 1)
+};
+
+__device__ __forceinline__ void ws_init(WsBars* b) {
+  for (int i = 0; i < 3; ++i) {
+    mbar_init(&b->full[i], 1);
+    mbar_init(&b->xfree[i], 256);
+    mbar_init(&b->sfree[i], 1);
+  }
+  for (int i = 0; i < 2; ++i) {
+    mbar_init(&b->tfull[i], 256);
+    mbar_init(&b->tfree[i], 1);
+  }
+  mbar_init(&b->accdone, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+               ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// UMMA smem descriptor, K-major SWIZZLE_128B (8-row atoms of 1024 B; LBO unused)
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                    // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;          // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                    // version
+  d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
+  return d;
+}
+
+// Producer (one thread): wait until the slot's previous contents were consumed,
+// arm the full barrier with the stage's bytes, issue the TMA loads.
+template <typename IssueFn>
+__device__ __forceinline__ void ws_produce(WsBars* bars, int nst, bool needs_sfree, uint32_t bytes, IssueFn issue) {
+  constexpr int ST = 3;
+  for (int s = 0; s < nst; ++s) {
+    const int slot = s % ST;
+    if (s >= ST) {
+      const uint32_t ph = ((s / ST) - 1) & 1;
+      mbar_wait(&bars->xfree[slot], ph);
+      if (needs_sfree) mbar_wait(&bars->sfree[slot], ph);
+    }
+    mbar_expect_tx(&bars->full[slot], bytes);
+    issue(s, slot, &bars->full[slot]);
+  }
+}
+
 // ---------------------------------------------------------------------------
-// A-pass: Aout[r][f] = alpha * sum_t X[r][t] S[f][t] for r < rows (<= 256)
+// A-pass: Aout[r][f] = alpha * sum_t X[r][t] S[f][t] for r < rows (<= 256).
+// tmX: X-hat [rows_total][ldx] box {32, 256} SW128;  tmS: [2 np][ldx] (hi rows
+// then lo rows) box {32, NP} SW128 -> directly the UMMA K-major SW128 layout.
 // ---------------------------------------------------------------------------
-template <int NP, int STAGES>
-__global__ void __launch_bounds__(kTcT) k_tc_apass(const float* __restrict__ X, int64_t ldx,
-                                                    const float* __restrict__ Shi, const float* __restrict__ Slo,
-                                                    int64_t lds, int ncontract, float* __restrict__ Aout,
-                                                    int64_t lda, float alpha, const ItemA* __restrict__ items) {
-  constexpr int XS = 256 * kXStride;  // floats per raw X stage
-  constexpr int SS = NP * kTcBK;      // floats per S tile (hi or lo)
-  constexpr int STAGE = XS + 2 * SS;
-  extern __shared__ __align__(1024) float smem[];
-  __shared__ __align__(8) uint64_t mbar[2];
+template <int NP>
+__global__ void __launch_bounds__(kWsThreads) k_tc_apass(const __grid_constant__ CUtensorMap tmX,
+                                                          const __grid_constant__ CUtensorMap tmS, int np,
+                                                          int ncontract, float* __restrict__ Aout, int64_t lda,
+                                                          float alpha, const ItemA* __restrict__ items) {
+  constexpr int ST = 3;
+  constexpr int XB = 256 * kTcBK * 4;   // bytes per X tile
+  constexpr int SB = NP * kTcBK * 4;    // bytes per S tile (hi or lo)
+  constexpr int STAGE = XB + 2 * SB;
+  extern __shared__ __align__(1024) uint8_t smem8[];
+  uint8_t* smem = smem8 + ((1024 - (smem_u32(smem8) & 1023)) & 1023);
+  __shared__ __align__(8) WsBars bars;
   __shared__ uint32_t tmem_base;
   const ItemA it = items[blockIdx.x];
-  const float* Xb = X + it.x_off;
+  const int row0 = (int)(it.o_off / lda);   // global voxel row of the tile
   const int rows = it.rows;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int h = warp >> 2, q = warp & 3;
-  const int row = 128 * h + 32 * q + lane;
   const int nst = ncontract / kTcBK;
 
   if (warp == 0) tmem_alloc(&tmem_base, 512);
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
+  if (tid == 0) ws_init(&bars);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
-  const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
 
-  auto load = [&](int s) {
-    float* xs = smem + (s % STAGES) * STAGE;
-    float* sh = xs + XS;
-    float* sl = sh + SS;
-    const int t0 = s * kTcBK;
-    for (int i = tid; i < 256 * 8; i += kTcT) {
-      const int r = i >> 3, c = (i & 7) * 4;
-      const bool ok = r < rows;
-      cp_async16(xs + r * kXStride + c, Xb + (ok ? (int64_t)r * ldx + t0 + c : 0), ok);
+  if (warp == kProducerWarp) {
+    if (lane == 0) {
+      ws_produce(&bars, nst, true, (uint32_t)STAGE, [&](int s, int slot, uint64_t* bar) {
+        uint8_t* st = smem + slot * STAGE;
+        const int t0 = s * kTcBK;
+        tma_load_2d(st, &tmX, t0, row0, bar);
+        tma_load_2d(st + XB, &tmS, t0, 0, bar);
+        tma_load_2d(st + XB + SB, &tmS, t0, np, bar);
+      });
     }
-    for (int i = tid; i < NP * 8; i += kTcT) {
-      // warp-contiguous core writes: 8 consecutive threads fill one 128-B core matrix
-      const int core = i >> 3, rr = i & 7;
-      const int r = (core >> 3) * 8 + rr, c = (core & 7) * 4;
-      cp_async16(sh + kcore(r, c), Shi + (int64_t)r * lds + t0 + c, true);
-      cp_async16(sl + kcore(r, c), Slo + (int64_t)r * lds + t0 + c, true);
-    }
-  };
-
+  } else if (warp == kMmaWarp) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(128, NP);
+      for (int s = 0; s < nst; ++s) {
+        const int b = s & 1, slot = s % ST;
+        mbar_wait(&bars.tfull[b], (s >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t bh = smem_u32(smem + slot * STAGE + XB), bl = bh + SB;
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nst) load(s);
-    cp_async_commit();
-  }
-  constexpr uint32_t idesc = idesc_tf32(128, NP);
-  for (int s = 0; s < nst; ++s) {
-    const int b = s & 1;
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    // the TMEM A buffer b was read by the MMAs of stage s - 2
-    if (s >= 2) mbar_wait(&mbar[b], ((s - 2) >> 1) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    {
-      const float* xr = smem + (s % STAGES) * STAGE + row * kXStride;
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t acc = tmem + 128u * hh;
+          const uint32_t ar = tmem + abuf_col(b, hh), al = ar + 32;
+#pragma unroll
+          for (int ks = 0; ks < kTcBK / 8; ++ks) {
+            const uint64_t dbh = umma_desc_sw128(bh + ks * 32);
+            const uint64_t dbl = umma_desc_sw128(bl + ks * 32);
+            mma_tf32_ts(acc, ar + ks * 8, dbh, idesc, (s | ks) != 0);
+            mma_tf32_ts(acc, ar + ks * 8, dbl, idesc, 1);
+            mma_tf32_ts(acc, al + ks * 8, dbh, idesc, 1);
+          }
+        }
+        mma_commit(&bars.tfree[b]);
+        mma_commit(&bars.sfree[slot]);
+      }
+      mma_commit(&bars.accdone);
+    }
+  } else {
+    const int h = warp >> 2, q = warp & 3;
+    const int row = 128 * h + 32 * q + lane;
+    const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
+    for (int s = 0; s < nst; ++s) {
+      const int b = s & 1, slot = s % ST;
+      mbar_wait(&bars.full[slot], (s / ST) & 1);
+      if (s >= 2) mbar_wait(&bars.tfree[b], ((s - 2) >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      // SW128 row: 16-byte chunk j of row r sits at chunk position j ^ (r & 7)
+      const uint8_t* xr = smem + slot * STAGE + row * 128;
       float vals[32];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float4 v = *reinterpret_cast<const float4*>(xr + 4 * j);
+        const float4 v = *reinterpret_cast<const float4*>(xr + ((j ^ (row & 7)) << 4));
         vals[4 * j] = v.x;
         vals[4 * j + 1] = v.y;
         vals[4 * j + 2] = v.z;
         vals[4 * j + 3] = v.w;
       }
+      mbar_arrive(&bars.xfree[slot]);
       store_split_row(tlane, abuf_col(b, h), vals);
       asm volatile("tcgen05.wait::st.sync.aligned;");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&bars.tfull[b]);
     }
-    asm volatile("fence.proxy.async.shared::cta;");
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const float* sh = smem + (s % STAGES) * STAGE + XS;
-      const uint32_t bh = smem_u32(sh), bl = smem_u32(sh + SS);
+    mbar_wait(&bars.accdone, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    float* out = Aout + it.o_off;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const uint32_t acc = tmem + 128u * hh;
-        const uint32_t ar = tmem + abuf_col(b, hh), al = ar + 32;
+    for (int c0 = 0; c0 < NP; c0 += 16) {
+      float v[16];
+      tmem_ld16(tlane + 128u * h + c0, v);
+      if (row < rows) {
+        float4* o = reinterpret_cast<float4*>(out + (int64_t)row * lda + c0);
 #pragma unroll
-        for (int ks = 0; ks < kTcBK / 8; ++ks) {
-          const uint64_t dbh = umma_desc(bh + ks * 256, 128, kTcBK * 32);
-          const uint64_t dbl = umma_desc(bl + ks * 256, 128, kTcBK * 32);
-          mma_tf32_ts(acc, ar + ks * 8, dbh, idesc, (s | ks) != 0);
-          mma_tf32_ts(acc, ar + ks * 8, dbl, idesc, 1);
-          mma_tf32_ts(acc, al + ks * 8, dbh, idesc, 1);
-        }
+        for (int j = 0; j < 4; ++j)
+          o[j] = make_float4(alpha * v[4 * j], alpha * v[4 * j + 1], alpha * v[4 * j + 2], alpha * v[4 * j + 3]);
       }
-      mma_commit(&mbar[b]);
-    }
-    // refill the stage read by the MMAs of s - 1 (its S tile) with stage s + STAGES - 1
-    const int ns = s + STAGES - 1;
-    if (ns < nst) {
-      if (s >= 1) mbar_wait(&mbar[(s - 1) & 1], ((s - 1) >> 1) & 1);
-      load(ns);
-    }
-    cp_async_commit();
-  }
-  cp_async_wait<0>();
-  mbar_wait(&mbar[(nst - 1) & 1], ((nst - 1) >> 1) & 1);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  float* out = Aout + it.o_off;
-#pragma unroll
-  for (int c0 = 0; c0 < NP; c0 += 16) {
-    float v[16];
-    tmem_ld16(tlane + 128u * h + c0, v);
-    if (row < rows) {
-      float4* o = reinterpret_cast<float4*>(out + (int64_t)row * lda + c0);
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        o[j] = make_float4(alpha * v[4 * j], alpha * v[4 * j + 1], alpha * v[4 * j + 2], alpha * v[4 * j + 3]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -262,147 +320,136 @@ __global__ void __launch_bounds__(kTcT) k_tc_apass(const float* __restrict__ X, 
 }
 
 template <int NP>
-cudaError_t run_apass(const float* X, int64_t ldx, const float* Shi, const float* Slo, int64_t lds,
-                      int64_t ncontract, float* A, int64_t lda, float alpha, const ItemA* items, int n_items,
-                      cudaStream_t st) {
-  constexpr int STAGES = 3;
-  constexpr int bytes = STAGES * (256 * kXStride + 2 * NP * kTcBK) * 4;
+cudaError_t run_apass(const CUtensorMap& tmX, const CUtensorMap& tmS, int np, int64_t ncontract, float* A,
+                      int64_t lda, float alpha, const ItemA* items, int n_items, cudaStream_t st) {
+  constexpr int bytes = 3 * (256 * kTcBK + 2 * NP * kTcBK) * 4 + 1024;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_tc_apass<NP, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaError_t e = cudaFuncSetAttribute(k_tc_apass<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   if (n_items == 0) return cudaSuccess;
-  k_tc_apass<NP, STAGES><<<n_items, kTcT, bytes, st>>>(X, ldx, Shi, Slo, lds, (int)ncontract, A, lda, alpha, items);
+  k_tc_apass<NP><<<n_items, kWsThreads, bytes, st>>>(tmX, tmS, np, (int)ncontract, A, lda, alpha, items);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
 // B-pass: out[f][t0 + t] = sum_{v < rows} A[v][f] X[v][t0 + t] for t < 256, f < orows.
-// X^T tile (t lanes x 32 v) goes to TMEM as the A operand; the A features tile
-// is split + transposed into the K-major core layout in smem (B operand).
+// tmXb: X-hat box {256, 32} (no swizzle); tmA: fp32 A [rows_total][np] box {NP, 32}.
+// The X^T tile goes to TMEM (A operand); the A features tile is split +
+// transposed into the K-major core layout in smem (B operand).  Voxel rows
+// past the chunk are masked by the consumers (TMA loads whole boxes).
 // ---------------------------------------------------------------------------
-constexpr int kBT = 256;      // TRs per tile (two 128-lane halves)
-constexpr int kAStr = 136;    // raw A stage row stride (floats): == 8 mod 32
+constexpr int kBT = 256;
 
-template <int NP, int STAGES>
-__global__ void __launch_bounds__(kTcT) k_tc_bpass(const float* __restrict__ A, int64_t lda,
-                                                    const float* __restrict__ X, int64_t ldx,
-                                                    double* __restrict__ out, int64_t ldo, int orows,
-                                                    const ItemE* __restrict__ items) {
-  constexpr int XR = kTcBK * kBT;     // raw X stage floats
-  constexpr int AR = kTcBK * kAStr;   // raw A stage floats
-  constexpr int CT = NP * kTcBK;      // core tile floats (hi or lo)
-  extern __shared__ __align__(1024) float smem[];
-  float* core = smem;                               // [2 buffers][hi, lo]
-  float* raw = smem + 2 * 2 * CT;                   // [STAGES][rawX, rawA]
-  __shared__ __align__(8) uint64_t mbar[2];
+template <int NP>
+__global__ void __launch_bounds__(kWsThreads) k_tc_bpass(const __grid_constant__ CUtensorMap tmA,
+                                                          const __grid_constant__ CUtensorMap tmXb, int64_t ldx,
+                                                          double* __restrict__ out, int64_t ldo, int orows,
+                                                          const ItemE* __restrict__ items) {
+  constexpr int ST = 3;
+  constexpr int XB = kTcBK * kBT * 4;   // raw X stage bytes
+  constexpr int AB = kTcBK * NP * 4;    // raw A stage bytes
+  constexpr int CT = NP * kTcBK;        // core tile floats (hi or lo)
+  extern __shared__ __align__(1024) uint8_t smem8[];
+  uint8_t* smem = smem8 + ((1024 - (smem_u32(smem8) & 1023)) & 1023);
+  float* core = reinterpret_cast<float*>(smem);                  // [2 buffers][hi, lo]
+  uint8_t* raw = smem + 2 * 2 * CT * 4;                          // [ST][rawX, rawA]
+  __shared__ __align__(8) WsBars bars;
   __shared__ uint32_t tmem_base;
   const ItemE it = items[blockIdx.x];
-  const float* Ab = A + it.l_off;
-  const float* Xb = X + it.r_off;
+  const int vrow0 = (int)(it.l_off / NP);          // first voxel row of the chunk (A row stride np == NP)
+  const int t0 = (int)(it.r_off - (int64_t)vrow0 * ldx);
   const int rows = it.rows, ncols = it.ncols;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int h = warp >> 2, q = warp & 3;
-  const int tcol = 128 * h + 32 * q + lane;
   const int nst = (rows + kTcBK - 1) / kTcBK;
 
   if (warp == 0) tmem_alloc(&tmem_base, 512);
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
+  if (tid == 0) ws_init(&bars);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
-  const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
 
-  auto load = [&](int s) {
-    float* rx = raw + (s % STAGES) * (XR + AR);
-    float* ra = rx + XR;
-    const int v0 = s * kTcBK;
-    for (int i = tid; i < kTcBK * (kBT / 4); i += kTcT) {
-      const int r = i >> 6, c = (i & 63) * 4;
-      const bool ok = (v0 + r) < rows && c < ncols;
-      cp_async16(rx + r * kBT + c, Xb + (ok ? (int64_t)(v0 + r) * ldx + c : 0), ok);
+  if (warp == kProducerWarp) {
+    if (lane == 0) {
+      ws_produce(&bars, nst, false, (uint32_t)(XB + AB), [&](int s, int slot, uint64_t* bar) {
+        uint8_t* rx = raw + slot * (XB + AB);
+        tma_load_2d(rx, &tmXb, t0, vrow0 + s * kTcBK, bar);
+        tma_load_2d(rx + XB, &tmA, 0, vrow0 + s * kTcBK, bar);
+      });
     }
-    for (int i = tid; i < kTcBK * (NP / 4); i += kTcT) {
-      const int r = i / (NP / 4), c = (i - r * (NP / 4)) * 4;
-      const bool ok = (v0 + r) < rows;
-      cp_async16(ra + r * kAStr + c, Ab + (ok ? (int64_t)(v0 + r) * lda + c : 0), ok);
-    }
-  };
-
+  } else if (warp == kMmaWarp) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(128, NP);
+      for (int s = 0; s < nst; ++s) {
+        const int b = s & 1;
+        mbar_wait(&bars.tfull[b], (s >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const float* ch = core + b * 2 * CT;
+        const uint32_t bh = smem_u32(ch), bl = smem_u32(ch + CT);
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nst) load(s);
-    cp_async_commit();
-  }
-  constexpr uint32_t idesc = idesc_tf32(128, NP);
-  for (int s = 0; s < nst; ++s) {
-    const int b = s & 1;
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    if (s >= 2) mbar_wait(&mbar[b], ((s - 2) >> 1) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const float* rx = raw + (s % STAGES) * (XR + AR);
-    const float* ra = rx + XR;
-    {
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t acc = tmem + 128u * hh;
+          const uint32_t xr = tmem + abuf_col(b, hh), xl = xr + 32;
+#pragma unroll
+          for (int ks = 0; ks < kTcBK / 8; ++ks) {
+            const uint64_t dbh = umma_desc(bh + ks * 256, 128, kTcBK * 32);
+            const uint64_t dbl = umma_desc(bl + ks * 256, 128, kTcBK * 32);
+            mma_tf32_ts(acc, xr + ks * 8, dbh, idesc, (s | ks) != 0);
+            mma_tf32_ts(acc, xr + ks * 8, dbl, idesc, 1);
+            mma_tf32_ts(acc, xl + ks * 8, dbh, idesc, 1);
+          }
+        }
+        mma_commit(&bars.tfree[b]);
+      }
+      mma_commit(&bars.accdone);
+    }
+  } else {
+    const int h = warp >> 2, q = warp & 3;
+    const int tcol = 128 * h + 32 * q + lane;
+    const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
+    for (int s = 0; s < nst; ++s) {
+      const int b = s & 1, slot = s % ST;
+      const int valid = min(kTcBK, rows - s * kTcBK);   // voxel rows of this stage inside the chunk
+      mbar_wait(&bars.full[slot], (s / ST) & 1);
+      if (s >= 2) mbar_wait(&bars.tfree[b], ((s - 2) >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const float* rx = reinterpret_cast<const float*>(raw + slot * (XB + AB));
+      const float* ra = reinterpret_cast<const float*>(raw + slot * (XB + AB) + XB);
       float vals[32];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) vals[k] = rx[k * kBT + tcol];
-      store_split_row(tlane, abuf_col(b, h), vals);
-    }
-    float* ch = core + b * 2 * CT;
-    float* cl = ch + CT;
-    for (int e = tid; e < CT; e += kTcT) {
-      const int r = (e >> 8) * 8 + ((e >> 2) & 7);   // feature
-      const int k = ((e >> 5) & 7) * 4 + (e & 3);    // voxel in the stage
-      const float a = ra[k * kAStr + r];
-      const float hi = tf32_hi(a);
-      ch[e] = hi;
-      cl[e] = a - hi;
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;");
-    asm volatile("fence.proxy.async.shared::cta;");
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t bh = smem_u32(ch), bl = smem_u32(cl);
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const uint32_t acc = tmem + 128u * hh;
-        const uint32_t xr = tmem + abuf_col(b, hh), xl = xr + 32;
-#pragma unroll
-        for (int ks = 0; ks < kTcBK / 8; ++ks) {
-          const uint64_t dbh = umma_desc(bh + ks * 256, 128, kTcBK * 32);
-          const uint64_t dbl = umma_desc(bl + ks * 256, 128, kTcBK * 32);
-          mma_tf32_ts(acc, xr + ks * 8, dbh, idesc, (s | ks) != 0);
-          mma_tf32_ts(acc, xr + ks * 8, dbl, idesc, 1);
-          mma_tf32_ts(acc, xl + ks * 8, dbh, idesc, 1);
-        }
+      for (int k = 0; k < 32; ++k) vals[k] = k < valid ? rx[k * kBT + tcol] : 0.0f;
+      float* ch = core + b * 2 * CT;
+      float* cl = ch + CT;
+      for (int e = tid; e < CT; e += 256) {
+        const int r = (e >> 8) * 8 + ((e >> 2) & 7);   // feature
+        const int k = ((e >> 5) & 7) * 4 + (e & 3);    // voxel in the stage
+        const float a = k < valid ? ra[k * NP + r] : 0.0f;
+        const float hi = tf32_hi(a);
+        ch[e] = hi;
+        cl[e] = a - hi;
       }
-      mma_commit(&mbar[b]);
+      mbar_arrive(&bars.xfree[slot]);
+      store_split_row(tlane, abuf_col(b, h), vals);
+      asm volatile("tcgen05.wait::st.sync.aligned;");
+      asm volatile("fence.proxy.async.shared::cta;");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&bars.tfull[b]);
     }
-    if (s + STAGES - 1 < nst) load(s + STAGES - 1);  // raw stage (s-1) % STAGES was consumed above
-    cp_async_commit();
-  }
-  cp_async_wait<0>();
-  mbar_wait(&mbar[(nst - 1) & 1], ((nst - 1) >> 1) & 1);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  double* ob = out + it.o_off;
+    mbar_wait(&bars.accdone, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    double* ob = out + it.o_off;
 #pragma unroll
-  for (int c0 = 0; c0 < NP; c0 += 16) {
-    float v[16];
-    tmem_ld16(tlane + 128u * h + c0, v);
-    if (tcol < ncols) {
+    for (int c0 = 0; c0 < NP; c0 += 16) {
+      float v[16];
+      tmem_ld16(tlane + 128u * h + c0, v);
+      if (tcol < ncols) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (c0 + j < orows) ob[(int64_t)(c0 + j) * ldo + tcol] = (double)v[j];
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < orows) ob[(int64_t)(c0 + j) * ldo + tcol] = (double)v[j];
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -411,18 +458,17 @@ __global__ void __launch_bounds__(kTcT) k_tc_bpass(const float* __restrict__ A, 
 }
 
 template <int NP>
-cudaError_t run_bpass(const float* A, int64_t lda, const float* X, int64_t ldx, double* out, int64_t ldo,
+cudaError_t run_bpass(const CUtensorMap& tmA, const CUtensorMap& tmXb, int64_t ldx, double* out, int64_t ldo,
                       int orows, const ItemE* items, int n_items, cudaStream_t st) {
-  constexpr int STAGES = 3;
-  constexpr int bytes = (2 * 2 * NP * kTcBK + STAGES * (kTcBK * kBT + kTcBK * kAStr)) * 4;
+  constexpr int bytes = (2 * 2 * NP * kTcBK + 3 * (kTcBK * kBT + kTcBK * NP)) * 4 + 1024;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_tc_bpass<NP, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaError_t e = cudaFuncSetAttribute(k_tc_bpass<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   if (n_items == 0) return cudaSuccess;
-  k_tc_bpass<NP, STAGES><<<n_items, kTcT, bytes, st>>>(A, lda, X, ldx, out, ldo, orows, items);
+  k_tc_bpass<NP><<<n_items, kWsThreads, bytes, st>>>(tmA, tmXb, ldx, out, ldo, orows, items);
   return cudaGetLastError();
 }
 
@@ -432,19 +478,51 @@ int tc_np(int k) { return (k + 15) / 16 * 16; }
 
 bool tc_supported(int k) { return k >= 1 && tc_np(k) <= 128; }
 
-cudaError_t launch_tc_apass(int np, const float* X, int64_t ldx, const float* Shi, const float* Slo, int64_t lds,
-                            int64_t ncontract, float* A, int64_t lda, float alpha, const ItemA* items, int n_items,
-                            cudaStream_t st) {
+// ---------------------------------------------------------------------------
+// tensor maps (host): cuTensorMapEncodeTiled through the runtime's driver entry point
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D fp32 map over [outer][inner] (row pitch in floats), box {box_inner, box_outer}
+cudaError_t make_map_f32(TmaMap* m, const float* base, int64_t inner, int64_t outer, int64_t pitch,
+                         int box_inner, int box_outer, bool swizzle128) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(m->opaque), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<float*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_tc_apass(int np, const TmaMap& tmX, const TmaMap& tmS, int64_t ncontract, float* A, int64_t lda,
+                            float alpha, const ItemA* items, int n_items, cudaStream_t st) {
   if (ncontract % kTcBK != 0) return cudaErrorInvalidValue;
+  const CUtensorMap& mx = *reinterpret_cast<const CUtensorMap*>(tmX.opaque);
+  const CUtensorMap& ms = *reinterpret_cast<const CUtensorMap*>(tmS.opaque);
   switch (np) {
-    case 16: return run_apass<16>(X, ldx, Shi, Slo, lds, ncontract, A, lda, alpha, items, n_items, st);
-    case 32: return run_apass<32>(X, ldx, Shi, Slo, lds, ncontract, A, lda, alpha, items, n_items, st);
-    case 48: return run_apass<48>(X, ldx, Shi, Slo, lds, ncontract, A, lda, alpha, items, n_items, st);
-    case 64: return run_apass<64>(X, ldx, Shi, Slo, lds, ncontract, A, lda, alpha, items, n_items, st);
-    case 80: return run_apass<80>(X, ldx, Shi, Slo, lds, ncontract, A, lda, alpha, items, n_items, st);
-    case 96: return run_apass<96>(X, ldx, Shi, Slo, lds, ncontract, A, lda, alpha, items, n_items, st);
-    case 112: return run_apass<112>(X, ldx, Shi, Slo, lds, ncontract, A, lda, alpha, items, n_items, st);
-    case 128: return run_apass<128>(X, ldx, Shi, Slo, lds, ncontract, A, lda, alpha, items, n_items, st);
+#define CASE_TA(N) \
+  case N: return run_apass<N>(mx, ms, np, ncontract, A, lda, alpha, items, n_items, st);
+    CASE_TA(16) CASE_TA(32) CASE_TA(48) CASE_TA(64) CASE_TA(80) CASE_TA(96) CASE_TA(112) CASE_TA(128)
+#undef CASE_TA
     default: return cudaErrorInvalidValue;
   }
 }
@@ -453,17 +531,15 @@ cudaError_t launch_tc_apass(int np, const float* X, int64_t ldx, const float* Sh
 
 namespace srm {
 
-cudaError_t launch_tc_bpass(int np, const float* A, int64_t lda, const float* X, int64_t ldx, double* out,
-                            int64_t ldo, int orows, const ItemE* items, int n_items, cudaStream_t st) {
+cudaError_t launch_tc_bpass(int np, const TmaMap& tmA, const TmaMap& tmXb, int64_t ldx, double* out, int64_t ldo,
+                            int orows, const ItemE* items, int n_items, cudaStream_t st) {
+  const CUtensorMap& ma = *reinterpret_cast<const CUtensorMap*>(tmA.opaque);
+  const CUtensorMap& mx = *reinterpret_cast<const CUtensorMap*>(tmXb.opaque);
   switch (np) {
-    case 16: return run_bpass<16>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
-    case 32: return run_bpass<32>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
-    case 48: return run_bpass<48>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
-    case 64: return run_bpass<64>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
-    case 80: return run_bpass<80>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
-    case 96: return run_bpass<96>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
-    case 112: return run_bpass<112>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
-    case 128: return run_bpass<128>(A, lda, X, ldx, out, ldo, orows, items, n_items, st);
+#define CASE_TB(N) \
+  case N: return run_bpass<N>(ma, mx, ldx, out, ldo, orows, items, n_items, st);
+    CASE_TB(16) CASE_TB(32) CASE_TB(48) CASE_TB(64) CASE_TB(80) CASE_TB(96) CASE_TB(112) CASE_TB(128)
+#undef CASE_TB
     default: return cudaErrorInvalidValue;
   }
 }
