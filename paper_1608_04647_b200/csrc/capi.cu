@@ -793,11 +793,15 @@ int srm_finalize(srm_plan* p, void* stream) {
     cudaError_t e = launch_contract_e((int)p->kp, SRM_F32, SRM_F32, d.af, p->np, d.af, p->np, d.part, p->ldo, 1.0,
                                       region<ItemE>(p, I_ITEMS_TG), (int)p->items_tg.size(), st);
     if (e == cudaSuccess) e = launch_reduce_chunks(d, st);
-    if (e == cudaSuccess) e = launch_eig_polar(d, 1, st);
-    if (e == cudaSuccess) e = launch_apply_w_f32(d, region<ItemA>(p, I_ITEMS_TA), (int)p->items_ta.size(), st);
+    if (e == cudaSuccess) e = launch_eig_polar_exact(d, 1, st);
+    if (e == cudaSuccess)
+      e = launch_apply_rows((int)p->kp, SRM_F32, d.af, p->np, d.mmat, p->kp * p->kp, d.wout, (int)p->K,
+                            region<ItemA>(p, I_ITEMS_TA), (int)p->items_ta.size(), st);
     return check(e, "finalize");
   }
-  return check(launch_apply_w(d, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st), "finalize");
+  return check(launch_apply_rows((int)p->kp, SRM_F64, d.amat, p->kp, d.mmat, p->kp * p->kp, d.wout, (int)p->K,
+                                 region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st),
+               "finalize");
 }
 
 int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {

@@ -414,6 +414,85 @@ cudaError_t run_a(const TX* X, int64_t ldx, const double* S, int64_t lds, int64_
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// W = A M on DMMA (srm.py:315-327 model.W via kernels.py:212 U V^T = A M):
+// W[row0 + r][f] = sum_c A[row0 + r][c] M_i[c][f] for r < rows (<= 256), f < K.
+// ---------------------------------------------------------------------------
+template <int KP, typename TA>
+__global__ void __launch_bounds__(kThreads) k_apply_rows(const TA* __restrict__ A, int64_t lda,
+                                                         const double* __restrict__ Mall, int64_t mstride,
+                                                         double* __restrict__ W, int K,
+                                                         const ItemA* __restrict__ items) {
+  constexpr int SA = pad4mod16(KP) + (sizeof(TA) == 4 ? 4 : 0);  // floats: == 8 mod 32 words
+  constexpr int SM = pad4mod16(KP);
+  constexpr int NT = KP / 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* Ms = reinterpret_cast<double*>(smem_raw);
+  TA* As = reinterpret_cast<TA*>(smem_raw + KP * SM * 8);
+  const ItemA it = items[blockIdx.x];
+  const double* Mg = Mall + (int64_t)it.pad * mstride;
+  const int64_t row0 = it.o_off / lda;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < KP * KP; e += kThreads) Ms[(e / KP) * SM + e % KP] = Mg[e];
+  for (int half = 0; half * 128 < it.rows; ++half) {
+    const int r0 = half * 128;
+    const int nr = min(128, it.rows - r0);
+    __syncthreads();
+    for (int e = tid; e < 128 * KP; e += kThreads) {
+      const int r = e / KP, c = e - r * KP;
+      As[r * SA + c] = r < nr ? A[(row0 + r0 + r) * lda + c] : TA(0);
+    }
+    __syncthreads();
+    double acc[2][NT][2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+    const int arow = warp * 16 + (lane >> 2);
+#pragma unroll 2
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      const int kc = k0 + (lane & 3);
+      const double a0 = to_f64(As[arow * SA + kc]);
+      const double a1 = to_f64(As[(arow + 8) * SA + kc]);
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const double b = Ms[kc * SM + n * 8 + (lane >> 2)];
+        dmma(acc[0][n][0], acc[0][n][1], a0, b);
+        dmma(acc[1][n][0], acc[1][n][1], a1, b);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int r = warp * 16 + m * 8 + (lane >> 2);
+      if (r < nr) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const int f = n * 8 + 2 * (lane & 3);
+          double* w = W + (row0 + r0 + r) * K;
+          if (f < K) w[f] = acc[m][n][0];
+          if (f + 1 < K) w[f + 1] = acc[m][n][1];
+        }
+      }
+    }
+  }
+}
+
+template <int KP, typename TA>
+cudaError_t run_apply(const TA* A, int64_t lda, const double* M, int64_t mstride, double* W, int K,
+                      const ItemA* items, int n_items, cudaStream_t st) {
+  constexpr int SA = pad4mod16(KP) + (sizeof(TA) == 4 ? 4 : 0);
+  constexpr int bytes = KP * pad4mod16(KP) * 8 + 128 * SA * (int)sizeof(TA);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_apply_rows<KP, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (n_items == 0) return cudaSuccess;
+  k_apply_rows<KP, TA><<<n_items, kThreads, bytes, st>>>(A, lda, M, mstride, W, K, items);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool contract_kp_supported(int kp) { return kp >= 8 && kp <= 128 && kp % 8 == 0; }
@@ -450,6 +529,23 @@ cudaError_t launch_contract_e(int kp, int l_dtype, int r_dtype, const void* L, i
       return cudaErrorInvalidValue;
   }
 #undef CASE_E
+}
+
+cudaError_t launch_apply_rows(int kp, int a_dtype, const void* A, int64_t lda, const double* M, int64_t mstride,
+                              double* W, int K, const ItemA* items, int n_items, cudaStream_t stream) {
+#define CASE_W(KK)                                                                                   \
+  case KK:                                                                                           \
+    return a_dtype == SRM_F64                                                                        \
+               ? run_apply<KK, double>(static_cast<const double*>(A), lda, M, mstride, W, K, items, \
+                                       n_items, stream)                                              \
+               : run_apply<KK, float>(static_cast<const float*>(A), lda, M, mstride, W, K, items,   \
+                                      n_items, stream);
+  switch (kp) {
+    SRM_KP_CASES(CASE_W)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef CASE_W
 }
 
 cudaError_t launch_contract_a(int kp, int x_dtype, const void* X, int64_t ldx, const double* S,

@@ -40,6 +40,10 @@ cudaError_t launch_contract_a(int kp, int x_dtype, const void* X, int64_t ldx, c
 
 bool contract_kp_supported(int kp);
 
+// W[row][f] = sum_c A[row][c] M[c][f] (items: o_off = row * lda, rows <= 256, pad = subject)
+cudaError_t launch_apply_rows(int kp, int a_dtype, const void* A, int64_t lda, const double* M, int64_t mstride,
+                              double* W, int K, const ItemA* items, int n_items, cudaStream_t stream);
+
 // 128 x 128 tiles of X^T X (items: l_off/r_off column offsets, pad = 1 on diagonal tiles)
 cudaError_t launch_gram_tiles(int x_dtype, const void* X, int64_t ldx, double* out, int64_t ldo,
                               const ItemE* items, int n_items, cudaStream_t stream);

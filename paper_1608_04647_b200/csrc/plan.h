@@ -99,5 +99,8 @@ cudaError_t launch_apply_right(const double* a, int64_t lda, int64_t v, int k, c
 int max_supported_k();
 bool ns_polar_supported(int kp);
 cudaError_t launch_ns_polar(const DevPlan& p, int init, cudaStream_t s);
+bool ns_polar_f32_supported(int kp);
+cudaError_t launch_ns_polar_f32(const DevPlan& p, int init, cudaStream_t s);
+cudaError_t launch_eig_polar_exact(const DevPlan& p, int init, cudaStream_t s);
 
 }  // namespace srm

@@ -169,9 +169,167 @@ cudaError_t run_ns(const DevPlan& p, int init, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// fp32 SIMT variant for the tensor-core (fp32 X-hat) plans with 80 < kp <= 112:
+// the same coupled iteration with fp32 matrices (4 x kp x (kp+4) floats fit in
+// smem where fp64 does not).  The per-iteration M then carries ~1e-6 relative
+// error -- the 3xTF32 passes already do -- and srm_finalize recomputes the
+// polar transform exactly (fp64 Jacobi) for the returned W.
+// ---------------------------------------------------------------------------
+template <int KP>
+__device__ __forceinline__ void mm_f32(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
+                                       float diag_shift, float scale) {
+  // C = scale * (diag_shift * I - A B)  when diag_shift != 0, else C = A B
+  constexpr int LD = KP + 4;
+  constexpr int R = KP / 16;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[R][R];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < R; ++j) acc[i][j] = 0.f;
+  for (int k = 0; k < KP; ++k) {
+    float a[R], b[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) a[i] = A[(ty + 16 * i) * LD + k];
+#pragma unroll
+    for (int j = 0; j < R; ++j) b[j] = B[k * LD + tx + 16 * j];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int j = 0; j < R; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int r = ty + 16 * i, c = tx + 16 * j;
+      C[r * LD + c] = diag_shift != 0.f ? scale * ((r == c ? diag_shift : 0.f) - acc[i][j]) : acc[i][j];
+    }
+}
+
+template <int KP>
+__global__ void __launch_bounds__(256) k_ns_polar_f32(DevPlan p, int init) {
+  constexpr int LD = KP + 4;
+  constexpr int MAT = KP * LD;
+  extern __shared__ __align__(16) float smf[];
+  __shared__ double red[32];
+  __shared__ double s_scale;
+  const int i = blockIdx.x;
+  const int n = (int)p.K;
+  const int tid = threadIdx.x;
+  float* buf[4] = {smf, smf + MAT, smf + 2 * MAT, smf + 3 * MAT};
+  const double* Cg = p.bred + (int64_t)i * p.kp * p.ldo + p.ldx;
+  double rowmax = 0.0;
+  for (int a = tid; a < KP; a += blockDim.x) {
+    double rs = 0.0;
+    for (int b = 0; b < n && a < n; ++b)
+      rs += fabs(0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a]));
+    rowmax = fmax(rowmax, rs);
+  }
+  rowmax = warp_max(rowmax);
+  if ((tid & 31) == 0) red[tid >> 5] = rowmax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < 8; ++w) m = fmax(m, red[w]);
+    s_scale = m;
+  }
+  __syncthreads();
+  const double c = s_scale;
+  const bool degenerate = !(c > 0.0) || !isfinite(c);
+  const double inv_c = degenerate ? 0.0 : 1.0 / c;
+  for (int e = tid; e < KP * LD; e += blockDim.x) {
+    const int a = e / LD, b = e - a * LD;
+    float y = 0.f;
+    if (a < n && b < n) y = (float)(0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a]) * inv_c);
+    buf[0][e] = y;
+    buf[1][e] = (a == b && a < n) ? 1.f : 0.f;
+  }
+  __syncthreads();
+  int y = 0, z = 1;
+  bool converged = false;
+  int extra = -1;
+  double prev_err = 1e300;
+  int it = 0;
+  for (; it < 90 && !degenerate; ++it) {
+    int f0 = -1, f1 = -1;
+    for (int q = 0; q < 4; ++q)
+      if (q != y && q != z) (f0 < 0 ? f0 : f1) = q;
+    float* Tm = buf[f0];
+    float* Yn = buf[f1];
+    mm_f32<KP>(buf[z], buf[y], Tm, 0.f, 1.f);  // P = Z Y
+    __syncthreads();
+    double err = 0.0;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int a = e / n, b = e - a * n;
+      const double d = (a == b ? 1.0 : 0.0) - (double)Tm[a * LD + b];
+      err += d * d;
+    }
+    err = block_sum<256>(err, red);
+    if (extra == 0) {
+      converged = true;
+      break;
+    }
+    if (!(err == err)) break;
+    if (extra < 0 && (err <= 1e-12 || (err < 1e-8 && err > 0.25 * prev_err))) extra = 1;
+    prev_err = err;
+    for (int e = tid; e < KP * LD; e += blockDim.x) {  // T = (3I - P)/2 in place
+      const int a = e / LD, b = e - a * LD;
+      Tm[e] = 0.5f * ((a == b ? 3.f : 0.f) - Tm[e]);
+    }
+    __syncthreads();
+    mm_f32<KP>(Tm, buf[y], Yn, 0.f, 1.f);          // Y' = T Y
+    __syncthreads();                                // every thread is done reading Y
+    mm_f32<KP>(Tm, buf[z], buf[y], 0.f, 1.f);      // Z' = T Z into the old Y buffer
+    __syncthreads();
+    z = y;
+    y = f1;
+    if (extra > 0) --extra;
+  }
+  const int kp = (int)p.kp;
+  double* Mg = p.mmat + (int64_t)i * kp * kp;
+  const float* Z = buf[z];
+  const double sc = degenerate ? 0.0 : 1.0 / sqrt(c);
+  for (int e = tid; e < kp * kp; e += blockDim.x) {
+    const int a = e / kp, b = e - a * kp;
+    Mg[e] = (a < n && b < n) ? 0.5 * ((double)Z[a * LD + b] + (double)Z[b * LD + a]) * sc : 0.0;
+  }
+  if (tid == 0) {
+    p.scal[(int64_t)i * 8 + 0] = (double)it;
+    if (degenerate || !converged) {
+      const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
+      raise_status(p.status, SRM_ERR_RANK, (int)sj[SC_GLOBAL], init ? -1 : *p.iter);
+    }
+  }
+}
+
+template <int KP>
+cudaError_t run_ns_f32(const DevPlan& p, int init, cudaStream_t s) {
+  constexpr int bytes = 4 * KP * (KP + 4) * (int)sizeof(float);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_ns_polar_f32<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_ns_polar_f32<KP><<<p.n_local, 256, bytes, s>>>(p, init);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool ns_polar_supported(int kp) { return kp >= 8 && kp <= 80 && kp % 8 == 0; }
+
+bool ns_polar_f32_supported(int kp) { return kp > 80 && kp <= 112; }
+
+cudaError_t launch_ns_polar_f32(const DevPlan& p, int init, cudaStream_t s) {
+  switch (((int)p.kp + 15) / 16 * 16) {
+    case 96: return run_ns_f32<96>(p, init, s);
+    case 112: return run_ns_f32<112>(p, init, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 cudaError_t launch_ns_polar(const DevPlan& p, int init, cudaStream_t s) {
   switch ((int)p.kp) {

@@ -833,6 +833,13 @@ cudaError_t launch_reduce_chunks(const DevPlan& p, cudaStream_t s) {
 
 cudaError_t launch_eig_polar(const DevPlan& p, int init, cudaStream_t s) {
   if (ns_polar_supported((int)p.kp)) return launch_ns_polar(p, init, s);
+  if ((p.flags & SRM_FLAG_TC) && ns_polar_f32_supported((int)p.kp)) return launch_ns_polar_f32(p, init, s);
+  return launch_eig_polar_exact(p, init, s);
+}
+
+// fp64 polar transform for every K (NS on DMMA up to kp = 80, Jacobi above)
+cudaError_t launch_eig_polar_exact(const DevPlan& p, int init, cudaStream_t s) {
+  if (ns_polar_supported((int)p.kp)) return launch_ns_polar(p, init, s);
   const size_t bytes = eig_smem_bytes((int)p.K);
   cudaError_t e = set_smem((const void*)k_eig_polar, bytes);
   if (e != cudaSuccess) return e;
