@@ -112,7 +112,7 @@ int64_t esize(int dtype) { return dtype == SRM_F64 ? 8 : 4; }
 void layout(srm_plan* p) {
   const int64_t kp2 = p->kp * p->kp;
   const int ntile_tail = (int)((p->ldx + 31) / 32);
-  const int ntile_apply = (int)((p->ldx + 63) / 64);
+  const int ntile_apply = (int)((p->ldx + kApplyCols - 1) / kApplyCols);
   const int64_t term_stride = p->kp * p->ldx + kRecScalars;
   const int64_t red_stride = p->kp * p->ldx + kRedScalars;
   const int64_t hist_stride = SRM_H_RHO2 + std::max(p->n_local, 1);

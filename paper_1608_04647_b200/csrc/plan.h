@@ -27,11 +27,14 @@ enum RedCol { RD_RHO0 = 0, RD_VLOGRHO = 1, RD_SQRHO = 2, RD_VSUM = 3, kRedScalar
 // tail scratch scalars
 enum TailCol { TS_LOGDET_SIGMA = 0, TS_LOGDET_PREC = 1, TS_TRACE = 2, kTailScalars = 8 };
 
+// column tile width of apply_m (W^T Xhat = M^T B)
+constexpr int kApplyCols = 128;
+
 struct DevPlan {
   int n_local, n_total, n_order;
   int flags;
   int64_t T, K, ldx, kp, ldo;
-  int ntile_apply;  // 64-column tiles of ldx
+  int ntile_apply;  // kApplyCols-column tiles of ldx
   int ntile_tail;   // 32-column tiles of ldx
   int64_t term_stride, red_stride, hist_stride;
   // regions

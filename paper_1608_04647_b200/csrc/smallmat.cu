@@ -11,7 +11,8 @@
 //                   E-step term srm.py:118) + the cross term <., S>
 //   finalize_rho    srm.py:152-155 noise update with the 1e-12 floor
 //   reduce_terms    srm.py:193-213 ordered accumulation of rho^-2 W^T Xhat
-//   tail            srm.py:121-142: two Cholesky inverses (kernels.py:168-187),
+//   tail            srm.py:121-142: two SPD inverses (kernels.py:168-187, by a
+//                   symmetric sweep with the same pivots as Cholesky),
 //                   S, Sigma_s update + trace, Woodbury log-likelihood,
 //                   tolerance statistic (srm.py:275-287)
 //   apply_w         W_i = A_i M_i (model.W)
@@ -320,35 +321,58 @@ __global__ void __launch_bounds__(kSmallThreads) k_eig_polar(DevPlan p, int init
 // apply_m: P_i = M_i^T B_i written into the subject's term record, plus the
 // per-tile cross term sum_{f,t} P[f][t] S[f][t]
 // ---------------------------------------------------------------------------
+// Register-blocked: warp w owns the NF = kp / 8 consecutive rows f = w NF + j,
+// lane l the 4 columns t = l + 32 u of a 128-column tile, so each c step costs
+// NF broadcast + 4 conflict-free shared loads for 4 NF FMAs.
+template <int NF>
 __global__ void __launch_bounds__(kSmallThreads) k_apply_m(DevPlan p, int with_cross) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double scratch[32];
+  constexpr int kp = 8 * NF;
   const int tile = blockIdx.x, i = blockIdx.y;
-  const int kp = (int)p.kp, K = (int)p.K;
-  const int64_t t0 = (int64_t)tile * 64;
-  double* Ms = sm;            // [K][K]
-  double* Bs = Ms + K * K;    // [K][64]
+  const int K = (int)p.K;
+  const int64_t t0 = (int64_t)tile * kApplyCols;
+  double* Ms = sm;             // [K][kp]: Ms[c kp + f] = M_i[c][f]
+  double* Bs = Ms + K * kp;    // [K][128]
   const double* Mg = p.mmat + (int64_t)i * kp * kp;
   const double* Bg = p.bred + (int64_t)i * p.kp * p.ldo;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < K * K; e += blockDim.x) Ms[e] = Mg[(e / K) * kp + (e % K)];
-  for (int e = tid; e < K * 64; e += blockDim.x) {
-    const int c = e >> 6, t = e & 63;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int e = tid; e < K * kp; e += blockDim.x) Ms[e] = (e % kp < K) ? Mg[e] : 0.0;
+  for (int e = tid; e < K * kApplyCols; e += blockDim.x) {
+    const int c = e / kApplyCols, t = e % kApplyCols;
     Bs[e] = (t0 + t < p.ldx) ? Bg[(int64_t)c * p.ldo + t0 + t] : 0.0;
   }
   __syncthreads();
+  double acc[NF][4];
+#pragma unroll
+  for (int j = 0; j < NF; ++j)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[j][u] = 0.0;
+  for (int c = 0; c < K; ++c) {
+    double b[4], m[NF];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) b[u] = Bs[c * kApplyCols + lane + 32 * u];
+#pragma unroll
+    for (int j = 0; j < NF; ++j) m[j] = Ms[c * kp + w * NF + j];
+#pragma unroll
+    for (int j = 0; j < NF; ++j)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[j][u] = fma(m[j], b[u], acc[j][u]);
+  }
   const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
   double* P = rec_ptr(p, (int)sj[SC_SLOT]);
-  const int t = tid & 63;
   double cross = 0.0;
-  if (t0 + t < p.ldx) {
-    for (int f = tid >> 6; f < kp; f += kSmallThreads / 64) {
-      double v = 0.0;
-      if (f < K) {
-        for (int c = 0; c < K; ++c) v += Ms[c * K + f] * Bs[c * 64 + t];
-        if (with_cross) cross += v * p.S[(int64_t)f * p.ldx + t0 + t];
+#pragma unroll
+  for (int j = 0; j < NF; ++j) {
+    const int f = w * NF + j;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = t0 + lane + 32 * u;
+      if (t < p.ldx) {
+        const double v = (f < K) ? acc[j][u] : 0.0;
+        if (with_cross && f < K) cross += v * p.S[(int64_t)f * p.ldx + t];
+        P[(int64_t)f * p.ldx + t] = v;
       }
-      P[(int64_t)f * p.ldx + t0 + t] = v;
     }
   }
   if (with_cross) {
@@ -392,149 +416,250 @@ __global__ void __launch_bounds__(kSmallThreads) k_reduce_terms(DevPlan p, doubl
   const int64_t n = p.kp * p.ldx;
   const int64_t e = (int64_t)blockIdx.x * kSmallThreads + threadIdx.x;
   if (e < n) {
+    // subjects in `order`, summed sequentially; loads batched 8 deep
     double acc = 0.0;
-    for (int j = 0; j < count; ++j) {
+    int j = 0;
+    for (; j + 8 <= count; j += 8) {
+      double x[8], r[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double* rec = rec_ptr(p, order[j + u]);
+        x[u] = rec[e];
+        r[u] = rec[n + RC_RHO2];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = (j + u == 0) ? x[u] / r[u] : acc + x[u] / r[u];
+    }
+    for (; j < count; ++j) {
       const double* rec = rec_ptr(p, order[j]);
       const double v = rec[e] / rec[n + RC_RHO2];
       acc = (j == 0) ? v : acc + v;
     }
     dst[e] = acc;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0) {
+    // per-subject scalar terms in parallel, then one thread sums them in order
+    __shared__ double terms[4][kSmallThreads];
     double rho0 = 0.0, vlog = 0.0, sq = 0.0, vsum = 0.0;
-    for (int j = 0; j < count; ++j) {
-      const double* rec = rec_ptr(p, order[j]) + n;
-      const double r = rec[RC_RHO2];
-      rho0 = (j == 0) ? 1.0 / r : rho0 + 1.0 / r;
-      vlog += rec[RC_V] * log(r);
-      sq += rec[RC_SQNORM] / r;
-      vsum += rec[RC_V];
+    for (int j0 = 0; j0 < count; j0 += kSmallThreads) {
+      const int j = j0 + (int)threadIdx.x;
+      if (j < count) {
+        const double* rec = rec_ptr(p, order[j]) + n;
+        const double r = rec[RC_RHO2];
+        terms[0][threadIdx.x] = 1.0 / r;
+        terms[1][threadIdx.x] = rec[RC_V] * log(r);
+        terms[2][threadIdx.x] = rec[RC_SQNORM] / r;
+        terms[3][threadIdx.x] = rec[RC_V];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int m = min(kSmallThreads, count - j0);
+        for (int u = 0; u < m; ++u) {
+          rho0 = (j0 + u == 0) ? terms[0][u] : rho0 + terms[0][u];
+          vlog += terms[1][u];
+          sq += terms[2][u];
+          vsum += terms[3][u];
+        }
+      }
+      __syncthreads();
     }
-    dst[n + RD_RHO0] = rho0;
-    dst[n + RD_VLOGRHO] = vlog;
-    dst[n + RD_SQRHO] = sq;
-    dst[n + RD_VSUM] = vsum;
+    if (threadIdx.x == 0) {
+      dst[n + RD_RHO0] = rho0;
+      dst[n + RD_VLOGRHO] = vlog;
+      dst[n + RD_SQRHO] = sq;
+      dst[n + RD_VSUM] = vsum;
+    }
   }
 }
+// In-place inverse of an SPD n x n matrix (n <= 112) by the symmetric sweep
+// (Gauss-Jordan without pivoting), register-resident: a 16 x 16 thread grid
+// owns the cyclic R x R blocks a[i][k] = A[ty + 16 i][tx + 16 k]
+// (R = ceil(n / 16)), and each pivot step broadcasts only the pivot row
+// through a double-buffered shared vector (one barrier per step).  The pivot
+// at step j is the LDL^T pivot d_j (the square of Cholesky's L_jj), so
+// logdet = sum log d_j and the first non-positive pivot is the index scipy's
+// cho_factor reports (kernels.py:168-187).  Sweeping every pivot leaves
+// -A^{-1} in a.  Returns the failed pivot or -1; d_j lands in dbuf[j].
+constexpr int kSweepLd = 128;
 
-// ---------------------------------------------------------------------------
-// K x K Cholesky helpers (one CTA, matrices in shared memory)
-// ---------------------------------------------------------------------------
-// In-place lower Cholesky.  Returns -1 on success or the failing 0-based
-// pivot (dpotrf info - 1).  *logdet = 2 sum log L_jj.
-__device__ int chol_lower(double* A, int n, int ld, double* logdet) {
-  __shared__ double s_ljj;
-  __shared__ int s_fail;
-  const int tid = threadIdx.x;
-  double ld_acc = 0.0;
-  for (int j = 0; j < n; ++j) {
-    __syncthreads();
-    if (tid == 0) {
-      const double d = A[j * ld + j];
-      s_fail = (d > 0.0) ? -1 : j;
-      s_ljj = (d > 0.0) ? sqrt(d) : 0.0;
-      if (d > 0.0) A[j * ld + j] = s_ljj;
+struct SweepShared {
+  double pbuf[2 * kSweepLd];  // double-buffered pivot row
+  double dbuf[kSweepLd];      // pivots
+  double scratch[32];
+};
+
+template <int R>
+__device__ __forceinline__ void reg_load(double (&a)[R][R], const double* src, int64_t lds, int n) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int r = ty + 16 * i, c = tx + 16 * k;
+      a[i][k] = (r < n && c < n) ? src[r * lds + c] : 0.0;
     }
-    __syncthreads();
-    if (s_fail >= 0) return s_fail;
-    const double ljj = s_ljj;
-    ld_acc += log(ljj);
-    for (int r = j + 1 + tid; r < n; r += blockDim.x) A[r * ld + j] /= ljj;
-    __syncthreads();
-    const int m = n - j - 1;
-    for (int e = tid; e < m * m; e += blockDim.x) {
-      const int r = j + 1 + e / m, c = j + 1 + e % m;
-      if (c <= r) A[r * ld + c] -= A[r * ld + j] * A[c * ld + j];
-    }
+}
+
+template <int R>
+__device__ __forceinline__ int reg_sweep(double (&a)[R][R], int n, double* pbuf, double* dbuf) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  if (ty == 0) {
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (tx + 16 * k < n) pbuf[tx + 16 * k] = a[0][k];
   }
   __syncthreads();
-  *logdet = 2.0 * ld_acc;
+  for (int j = 0; j < n; ++j) {
+    const double* pv = pbuf + (j & 1) * kSweepLd;
+    const double d = pv[j];
+    if (!(d > 0.0)) return j;  // uniform: every thread reads the same pivot
+    const double inv = 1.0 / d;
+    double pr[R], pc[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = ty + 16 * i;
+      pr[i] = (r < n) ? pv[r] * inv : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int c = tx + 16 * k;
+      pc[k] = (c < n) ? pv[c] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = ty + 16 * i;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int c = tx + 16 * k;
+        const double v = fma(-pr[i], pc[k], a[i][k]);
+        a[i][k] = (r == j) ? ((c == j) ? -inv : pc[k] * inv) : ((c == j) ? pr[i] : v);
+      }
+    }
+    if (threadIdx.x == 0) dbuf[j] = d;
+    const int jn = j + 1;
+    if (jn < n && ty == (jn & 15)) {
+      double* nx = pbuf + (jn & 1) * kSweepLd;
+      const int isel = jn >> 4;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        double v = a[0][k];  // select chain: keeps a[][] in registers
+#pragma unroll
+        for (int i = 1; i < R; ++i) v = (isel == i) ? a[i][k] : v;
+        if (tx + 16 * k < n) nx[tx + 16 * k] = v;
+      }
+    }
+    __syncthreads();
+  }
   return -1;
 }
 
-// Linv (lower) = inverse of lower-triangular L; one thread per column.
-__device__ void tri_inverse(const double* L, double* Li, int n, int ld) {
-  const int tid = threadIdx.x;
-  for (int e = tid; e < n * n; e += blockDim.x) Li[(e / n) * ld + (e % n)] = 0.0;
-  __syncthreads();
-  for (int c = tid; c < n; c += blockDim.x) {
-    Li[c * ld + c] = 1.0 / L[c * ld + c];
-    for (int r = c + 1; r < n; ++r) {
-      double s = 0.0;
-      for (int k = c; k < r; ++k) s += L[r * ld + k] * Li[k * ld + c];
-      Li[r * ld + c] = -s / L[r * ld + r];
-    }
-  }
-  __syncthreads();
-}
-
-// A = Li^T Li (symmetric, lower computed then mirrored: dpotri + symmetrise)
-__device__ void gram_lower(const double* Li, double* A, int n, int ld) {
-  const int tid = threadIdx.x;
-  for (int e = tid; e < n * n; e += blockDim.x) {
-    const int a = e / n, b = e - a * n;
-    if (a >= b) {
-      double s = 0.0;
-      for (int k = a; k < n; ++k) s += Li[k * ld + a] * Li[k * ld + b];
-      A[a * ld + b] = s;
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < n * n; e += blockDim.x) {
-    const int a = e / n, b = e - a * n;
-    if (a < b) A[a * ld + b] = A[b * ld + a];
-  }
-  __syncthreads();
+// sum_j log d_j in a fixed tree order (all threads get it)
+__device__ double sum_log(const double* dbuf, int n, double* scratch) {
+  const double v = ((int)threadIdx.x < n) ? log(dbuf[threadIdx.x]) : 0.0;
+  return block_sum<kSmallThreads>(v, scratch);
 }
 
 // ---------------------------------------------------------------------------
 // tail, stage 1 (one CTA): var_s and C = Sigma_s^T (I - rho0 var_s)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSmallThreads) k_tail_kk(DevPlan p) {
-  const int iteration = *p.iter;
+template <int R>
+__device__ __forceinline__ void tail_kk_body(const DevPlan& p, int iteration, SweepShared& sh) {
   extern __shared__ __align__(16) double sm[];
-  if (failed(p)) return;
+  double* pbuf = sh.pbuf;
+  double* dbuf = sh.dbuf;
+  double* scratch = sh.scratch;
   const int n = (int)p.K, ld = n + 1, kp = (int)p.kp;
-  double* M1 = sm;
-  double* M2 = sm + n * ld;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const double rho0 = p.red[p.kp * p.ldx + RD_RHO0];
-  for (int e = tid; e < n * n; e += blockDim.x) M1[(e / n) * ld + e % n] = p.sigma[(e / n) * kp + e % n];
-  double logdet_sigma = 0.0, logdet_prec = 0.0;
-  int piv = chol_lower(M1, n, ld, &logdet_sigma);
+  double a[R][R];
+  reg_load<R>(a, p.sigma, kp, n);
+  int piv = reg_sweep<R>(a, n, pbuf, dbuf);  // a = -Sigma_s^{-1}
   if (piv >= 0) {
     if (tid == 0) raise_status(p.status, SRM_ERR_DEFINITENESS, piv, iteration);
     return;
   }
-  tri_inverse(M1, M2, n, ld);
-  gram_lower(M2, M1, n, ld);  // Sigma_s^{-1}
-  for (int j = tid; j < n; j += blockDim.x) M1[j * ld + j] += rho0;
-  piv = chol_lower(M1, n, ld, &logdet_prec);
+  const double logdet_sigma = sum_log(dbuf, n, scratch);
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int r = ty + 16 * i, c = tx + 16 * k;
+      a[i][k] = (r < n && c < n) ? (r == c ? rho0 : 0.0) - a[i][k] : 0.0;
+    }
+  piv = reg_sweep<R>(a, n, pbuf, dbuf);  // a = -var_s
   if (piv >= 0) {
     if (tid == 0) raise_status(p.status, SRM_ERR_DEFINITENESS, piv, iteration);
     return;
   }
-  tri_inverse(M1, M2, n, ld);
-  gram_lower(M2, M1, n, ld);  // var_s
+  const double logdet_prec = sum_log(dbuf, n, scratch);
+  double* Vs = sm;           // var_s  [n][ld]
+  double* Ss = sm + n * ld;  // Sigma_s [n][ld]
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int r = ty + 16 * i, c = tx + 16 * k;
+      if (r < n && c < n) {
+        Vs[r * ld + c] = -a[i][k];
+        p.var[r * kp + c] = -a[i][k];
+        Ss[r * ld + c] = p.sigma[r * kp + c];
+      }
+    }
   for (int e = tid; e < kp * kp; e += blockDim.x) {
-    const int a = e / kp, b = e - a * kp;
-    p.var[e] = (a < n && b < n) ? M1[a * ld + b] : 0.0;
-  }
-  for (int e = tid; e < n * n; e += blockDim.x) {
-    const int a = e / n, b = e - a * n;
-    M2[a * ld + b] = (a == b ? 1.0 : 0.0) - rho0 * M1[a * ld + b];
+    const int r = e / kp, c = e - r * kp;
+    if (r >= n || c >= n) {
+      p.var[e] = 0.0;
+      p.cmat[e] = 0.0;
+    }
   }
   __syncthreads();
-  for (int e = tid; e < kp * kp; e += blockDim.x) {
-    const int a = e / kp, b = e - a * kp;
-    double s = 0.0;
-    if (a < n && b < n)
-      for (int k = 0; k < n; ++k) s += p.sigma[k * kp + a] * M2[k * ld + b];
-    p.cmat[e] = s;
+  // C[r][c] = sum_m Sigma[m][r] (delta_mc - rho0 var[m][c])
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int k = 0; k < R; ++k) a[i][k] = 0.0;
+  for (int m = 0; m < n; ++m) {
+    double sr[R], vc[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = ty + 16 * i;
+      sr[i] = (r < n) ? Ss[m * ld + r] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int c = tx + 16 * k;
+      vc[k] = (c < n) ? (m == c ? 1.0 : 0.0) - rho0 * Vs[m * ld + c] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int k = 0; k < R; ++k) a[i][k] = fma(sr[i], vc[k], a[i][k]);
   }
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int r = ty + 16 * i, c = tx + 16 * k;
+      if (r < n && c < n) p.cmat[r * kp + c] = a[i][k];
+    }
   if (tid == 0) {
     p.tailscr[TS_LOGDET_SIGMA] = logdet_sigma;
     p.tailscr[TS_LOGDET_PREC] = logdet_prec;
+  }
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_tail_kk(DevPlan p) {
+  __shared__ SweepShared sh;
+  const int iteration = *p.iter;
+  if (failed(p)) return;
+  switch ((p.K + 15) / 16) {
+    case 1: tail_kk_body<1>(p, iteration, sh); break;
+    case 2: tail_kk_body<2>(p, iteration, sh); break;
+    case 3: tail_kk_body<3>(p, iteration, sh); break;
+    case 4: tail_kk_body<4>(p, iteration, sh); break;
+    case 5: tail_kk_body<5>(p, iteration, sh); break;
+    case 6: tail_kk_body<6>(p, iteration, sh); break;
+    default: tail_kk_body<7>(p, iteration, sh); break;
   }
 }
 
@@ -547,23 +672,38 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_s(DevPlan p) {
   const int K = (int)p.K, kp = (int)p.kp;
   const int tile = blockIdx.x;
   const int64_t t0 = (int64_t)tile * 32;
-  double* Rt = sm;           // [K][32]
-  double* St = sm + K * 32;  // [K][32]
+  constexpr int LD = 33;  // padded rows: conflict-free S S^T reads
+  double* Rt = sm;           // [K][33]
+  double* St = sm + K * LD;  // [K][33]
   const int tid = threadIdx.x, col = tid & 31, rg = tid >> 5;
   const int64_t t = t0 + col;
   const bool tin = t < p.ldx;
-  for (int f = rg; f < K; f += 8) Rt[f * 32 + col] = tin ? p.red[(int64_t)f * p.ldx + t] : 0.0;
+  for (int f = rg; f < K; f += 8) Rt[f * LD + col] = tin ? p.red[(int64_t)f * p.ldx + t] : 0.0;
   __syncthreads();
   double quad = 0.0, dsq = 0.0, osq = 0.0;
   for (int f = rg; f < K; f += 8) {
-    double s = 0.0, y = 0.0;
-    for (int c = 0; c < K; ++c) {
-      const double r = Rt[c * 32 + col];
-      s += p.cmat[f * kp + c] * r;
-      y += p.var[f * kp + c] * r;
+    // rows f of C and var_s, one coalesced load per warp, broadcast by shuffles
+    double cm[4], vr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = q * 32 + col;
+      cm[q] = (c < K) ? p.cmat[f * kp + c] : 0.0;
+      vr[q] = (c < K) ? p.var[f * kp + c] : 0.0;
     }
-    quad += Rt[f * 32 + col] * y;
-    St[f * 32 + col] = s;
+    double s = 0.0, y = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int lmax = min(32, K - q * 32);
+      if (lmax <= 0) break;
+#pragma unroll 8
+      for (int l = 0; l < lmax; ++l) {
+        const double r = Rt[(q * 32 + l) * LD + col];
+        s += __shfl_sync(0xffffffffu, cm[q], l) * r;
+        y += __shfl_sync(0xffffffffu, vr[q], l) * r;
+      }
+    }
+    quad += Rt[f * LD + col] * y;
+    St[f * LD + col] = s;
     if (tin && p.st) p.st[t * kp + f] = s;
     if (tin && p.sf) {
       const float sfv = (float)s;
@@ -583,10 +723,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_s(DevPlan p) {
   double* ssp = p.sspart + (int64_t)tile * kp * kp;
   for (int e = tid; e < K * K; e += blockDim.x) {
     const int a = e / K, b = e - a * K;
+    if (a > b) continue;  // symmetric: the product commutes exactly
     double v = 0.0;
 #pragma unroll 8
-    for (int c = 0; c < 32; ++c) v += St[a * 32 + c] * St[b * 32 + c];
+    for (int c = 0; c < 32; ++c) v += St[a * LD + c] * St[b * LD + c];
     ssp[a * kp + b] = v;
+    ssp[b * kp + a] = v;
   }
   quad = block_sum<kSmallThreads>(quad, scratch);
   dsq = block_sum<kSmallThreads>(dsq, scratch);
@@ -599,18 +741,31 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_s(DevPlan p) {
 }
 
 // tail, stage 3 (one CTA): Sigma_s <- sym(var_s + S S^T / T), trace, LL
-__global__ void __launch_bounds__(kSmallThreads) k_tail_sigma(DevPlan p) {
+constexpr int kSigmaThreads = 1024;
+__global__ void __launch_bounds__(kSigmaThreads) k_tail_sigma(DevPlan p) {
   const int iteration = *p.iter;
   extern __shared__ __align__(16) double sm[];
   if (failed(p)) return;
-  const int K = (int)p.K, kp = (int)p.kp;
+  const int K = (int)p.K, kp = (int)p.kp, nt = p.ntile_tail;
   const int tid = threadIdx.x;
   const double T = (double)p.T;
-  double* Sn = sm;  // [K][K]
+  double* Sn = sm;           // [K][K]
+  double* tp = sm + K * K;   // [nt][4] tile statistics
+  for (int e = tid; e < nt * 4; e += blockDim.x) tp[e] = p.tailpart[e];
+  const int64_t tstride = (int64_t)kp * kp;
   for (int e = tid; e < K * K; e += blockDim.x) {
     const int a = e / K, b = e - a * K;
+    const double* src = p.sspart + a * kp + b;
     double ss = 0.0;
-    for (int tile = 0; tile < p.ntile_tail; ++tile) ss += p.sspart[(int64_t)tile * kp * kp + a * kp + b];
+    int tile = 0;
+    for (; tile + 8 <= nt; tile += 8) {  // 8 loads in flight, summed in tile order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = src[(tile + u) * tstride];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ss += v[u];
+    }
+    for (; tile < nt; ++tile) ss += src[tile * tstride];
     Sn[e] = p.var[a * kp + b] + ss / T;
   }
   __syncthreads();
@@ -622,10 +777,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_sigma(DevPlan p) {
     double trace = 0.0;
     for (int a = 0; a < K; ++a) trace += 0.5 * (Sn[a * K + a] + Sn[a * K + a]);
     double quad = 0.0, dsq = 0.0, osq = 0.0;
-    for (int tile = 0; tile < p.ntile_tail; ++tile) {
-      quad += p.tailpart[tile * 4 + 0];
-      dsq += p.tailpart[tile * 4 + 1];
-      osq += p.tailpart[tile * 4 + 2];
+    for (int tile = 0; tile < nt; ++tile) {
+      quad += tp[tile * 4 + 0];
+      dsq += tp[tile * 4 + 1];
+      osq += tp[tile * 4 + 2];
     }
     const double* rs = p.red + p.kp * p.ldx;
     const double two_pi = 6.283185307179586476925286766559;
@@ -711,21 +866,38 @@ __global__ void __launch_bounds__(kSmallThreads) k_apply_w(DevPlan p, const Item
 // ---------------------------------------------------------------------------
 // stateless: in-place SPD inverse (kernels.py:168-187)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSmallThreads) k_spd_inverse(double* a, int n, int32_t* status) {
-  extern __shared__ __align__(16) double sm[];
-  const int ld = n + 1;
-  double* M1 = sm;
-  double* M2 = sm + n * ld;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) M1[(e / n) * ld + e % n] = a[e];
-  double logdet;
-  const int piv = chol_lower(M1, n, ld, &logdet);
+template <int R>
+__device__ __forceinline__ void spd_inverse_body(double* g, int n, int32_t* status, SweepShared& sh) {
+  double* pbuf = sh.pbuf;
+  double* dbuf = sh.dbuf;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double a[R][R];
+  reg_load<R>(a, g, n, n);
+  const int piv = reg_sweep<R>(a, n, pbuf, dbuf);
   if (piv >= 0) {
     if (threadIdx.x == 0) raise_status(status, SRM_ERR_DEFINITENESS, piv, -1);
     return;
   }
-  tri_inverse(M1, M2, n, ld);
-  gram_lower(M2, M1, n, ld);
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) a[e] = M1[(e / n) * ld + e % n];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int r = ty + 16 * i, c = tx + 16 * k;
+      if (r < n && c < n) g[r * n + c] = -a[i][k];
+    }
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_spd_inverse(double* a, int n, int32_t* status) {
+  __shared__ SweepShared sh;
+  switch ((n + 15) / 16) {
+    case 1: spd_inverse_body<1>(a, n, status, sh); break;
+    case 2: spd_inverse_body<2>(a, n, status, sh); break;
+    case 3: spd_inverse_body<3>(a, n, status, sh); break;
+    case 4: spd_inverse_body<4>(a, n, status, sh); break;
+    case 5: spd_inverse_body<5>(a, n, status, sh); break;
+    case 6: spd_inverse_body<6>(a, n, status, sh); break;
+    default: spd_inverse_body<7>(a, n, status, sh); break;
+  }
 }
 
 // stateless polar transform from a Gram matrix: M = G^{-1/2}
@@ -778,10 +950,12 @@ size_t eig_smem_bytes(int n) {
 
 // Raise a kernel's dynamic smem limit once (never inside a graph capture after
 // the first eager launch of the same shape).
+// Raise a kernel's dynamic shared-memory limit once (static + dynamic may not
+// exceed 48 KB without it); cached per function.
 cudaError_t set_smem(const void* f, size_t bytes) {
-  if (bytes <= 48 * 1024) return cudaSuccess;
-  static const void* funcs[32];
-  static size_t limits[32];
+  if (bytes <= 16 * 1024) return cudaSuccess;
+  static const void* funcs[64];
+  static size_t limits[64];
   static int n = 0;
   for (int i = 0; i < n; ++i) {
     if (funcs[i] == f) {
@@ -792,7 +966,7 @@ cudaError_t set_smem(const void* f, size_t bytes) {
     }
   }
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess && n < 32) {
+  if (e == cudaSuccess && n < 64) {
     funcs[n] = f;
     limits[n] = bytes;
     ++n;
@@ -848,11 +1022,27 @@ cudaError_t launch_eig_polar_exact(const DevPlan& p, int init, cudaStream_t s) {
 }
 
 cudaError_t launch_apply_m(const DevPlan& p, int with_cross, cudaStream_t s) {
-  const size_t bytes = (size_t)(p.K * p.K + p.K * 64) * sizeof(double);
-  cudaError_t e = set_smem((const void*)k_apply_m, bytes);
+  const size_t bytes = (size_t)(p.K * p.kp + p.K * kApplyCols) * sizeof(double);
+  const void* fn = nullptr;
+  switch (p.kp / 8) {
+#define SRM_APPLY_M_CASE(n) \
+  case n:                   \
+    fn = (const void*)k_apply_m<n>; \
+    break;
+    SRM_APPLY_M_CASE(1) SRM_APPLY_M_CASE(2) SRM_APPLY_M_CASE(3) SRM_APPLY_M_CASE(4) SRM_APPLY_M_CASE(5)
+    SRM_APPLY_M_CASE(6) SRM_APPLY_M_CASE(7) SRM_APPLY_M_CASE(8) SRM_APPLY_M_CASE(9) SRM_APPLY_M_CASE(10)
+    SRM_APPLY_M_CASE(11) SRM_APPLY_M_CASE(12) SRM_APPLY_M_CASE(13) SRM_APPLY_M_CASE(14)
+#undef SRM_APPLY_M_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+  cudaError_t e = set_smem(fn, bytes);
   if (e != cudaSuccess) return e;
   const dim3 grid((unsigned)p.ntile_apply, (unsigned)p.n_local);
-  k_apply_m<<<grid, kSmallThreads, bytes, s>>>(p, with_cross);
+  DevPlan arg = p;
+  void* args[] = {&arg, &with_cross};
+  e = cudaLaunchKernel(fn, grid, dim3(kSmallThreads), args, bytes, s);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -884,7 +1074,7 @@ cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s) {
 }
 
 cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s) {
-  const size_t b2 = (size_t)2 * p.K * 32 * sizeof(double);
+  const size_t b2 = (size_t)2 * p.K * 33 * sizeof(double);
   cudaError_t e = set_smem((const void*)k_tail_s, b2);
   if (e != cudaSuccess) return e;
   k_tail_s<<<p.ntile_tail, kSmallThreads, b2, s>>>(p);
@@ -892,10 +1082,10 @@ cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s) {
 }
 
 cudaError_t launch_tail_sigma(const DevPlan& p, cudaStream_t s) {
-  const size_t b3 = (size_t)p.K * p.K * sizeof(double);
+  const size_t b3 = (size_t)(p.K * p.K + 4 * p.ntile_tail) * sizeof(double);
   cudaError_t e = set_smem((const void*)k_tail_sigma, b3);
   if (e != cudaSuccess) return e;
-  k_tail_sigma<<<1, kSmallThreads, b3, s>>>(p);
+  k_tail_sigma<<<1, kSigmaThreads, b3, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -936,10 +1126,7 @@ cudaError_t launch_apply_w_f32(const DevPlan& p, const void* items_a, int n_item
 }
 
 cudaError_t launch_spd_inverse(double* a, int n, int32_t* status, cudaStream_t s) {
-  const size_t bytes = (size_t)2 * n * (n + 1) * sizeof(double);
-  cudaError_t e = set_smem((const void*)k_spd_inverse, bytes);
-  if (e != cudaSuccess) return e;
-  k_spd_inverse<<<1, kSmallThreads, bytes, s>>>(a, n, status);
+  k_spd_inverse<<<1, kSmallThreads, 0, s>>>(a, n, status);
   return cudaGetLastError();
 }
 

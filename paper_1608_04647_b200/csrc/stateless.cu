@@ -171,7 +171,7 @@ int srm_tail_step(const double* reduced, int64_t ldr, const double* sigma, int64
   d.kp = kp;
   d.ldo = ldx + kp;
   d.ntile_tail = ntail;
-  d.ntile_apply = (int)((ldx + 63) / 64);
+  d.ntile_apply = (int)((ldx + kApplyCols - 1) / kApplyCols);
   d.red_stride = kp * ldx + kRedScalars;
   d.hist_stride = 8;
   d.n_hist = 1;
