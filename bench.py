@@ -40,6 +40,7 @@ UNIT = "subject·voxel·TR/s"
 DMMA_PEAK_TFLOPS = 37.1  # tools/fp64_peak.cu on this pool's B200 (mma.sync m8n8k4 f64)
 FALLBACK_HBM_GBS = 6650.0
 TF32_PEAK_TFLOPS = 1664.3 / 2  # tf32 MMA rate = half of the measured bf16 burst (MEASURED_PEAKS.json)
+I8_PEAK_TOPS = 1664.3 * 2      # dense int8 MMA rate = twice the measured bf16 burst (MEASURED_PEAKS.json)
 
 
 def parse_args():
@@ -55,6 +56,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--algorithm", default="auto", choices=["auto", "stream", "gram"])
+    ap.add_argument("--gram-int8", default="on", choices=["on", "off"],
+                    help="fp64 Gram path: X^T X from int8 slices on tcgen05 (on) or fp64 DMMA (off)")
     return ap.parse_args()
 
 
@@ -271,12 +274,16 @@ def run_ours(args):
     # precompute when the Gram path is chosen, K EM iterations, and the final
     # W_i = A_i M_i.  One-time work is therefore charged to the K steps.
     algo = args.algorithm
+    use_i8 = args.gram_int8 == "on" and cfg["dtype"] == "f64"
     if algo == "auto":
         algo = srm.choose_algorithm([V] * cfg["n_subjects"], T, K, args.steps,
-                                    torch.cuda.mem_get_info(dev)[0] * world, storage=cfg["dtype"])
+                                    torch.cuda.mem_get_info(dev)[0] * world, storage=cfg["dtype"],
+                                    gram_int8=use_i8)
     total_iters = max(args.warmup, args.steps) + 8
     eng = SrmEngine([V] * n_local, T, K, total_iters, storage=cfg["dtype"], world_size=world, rank=rank,
-                    counts=counts, ordered=True, gram=(algo == "gram"), tc=(cfg["dtype"] == "f32"), device=dev)
+                    counts=counts, ordered=True, gram=(algo == "gram"), tc=(cfg["dtype"] == "f32"),
+                    gram_i8=(algo == "gram" and use_i8), device=dev)
+    use_i8 = eng.gram_i8
     eng.load(xs)
     use_graph = world == 1
 
@@ -322,7 +329,7 @@ def run_ours(args):
     eng.raise_status()
     units = cfg["n_subjects"] * V * T
     value = units / (ms / 1e3)
-    n_gram_launches = 2 if algo == "gram" else 0
+    n_gram_launches = (4 if use_i8 else 2) if algo == "gram" else 0
     tc = cfg["dtype"] == "f32"
     n_final = 2 if algo == "gram" else (4 if tc else 1)
     launches = eng.launches_per_iteration * args.steps + n_gram_launches + n_final
@@ -335,9 +342,13 @@ def run_ours(args):
             prof_iter.setdefault(name, []).append(t_ms)
     prof_iter = {k_: float(np.mean(v_)) for k_, v_ in prof_iter.items()}
     once = {}
-    for name, fn in (("gram_xtx", eng.prepare_gram), ("finalize", eng.finalize)):
-        if name == "gram_xtx" and algo != "gram":
-            continue
+    if algo == "gram":
+        prof_g = {}
+        for _ in range(3):
+            for name, t_ms in eng.profile_gram():
+                prof_g.setdefault(name, []).append(t_ms)
+        once.update({k_: float(np.mean(v_)) for k_, v_ in prof_g.items()})
+    for name, fn in (("finalize", eng.finalize),):
         a0 = torch.cuda.Event(enable_timing=True)
         a1 = torch.cuda.Event(enable_timing=True)
         a0.record(st)
@@ -358,10 +369,13 @@ def run_ours(args):
     hbm_peak, peak_src = peaks()
     local_units = n_local * V * T
     ldx = -(-T // 32) * 32
-    if dom == "gram_xtx":
-        launch_ms = once["gram_xtx"]
+    nt = -(-ldx // 128)
+    if dom in ("gram_tiles", "oz_gram"):
+        launch_ms = once[dom]
         alg_flops = float(n_local) * V * T * (T + 1)          # symmetric X^T X: T(T+1)/2 dots of length V
         alg_bytes = float(local_units * b)                      # X-hat read once
+        # int8 products issued by oz_gram: 28 slice pairs per upper 128 x 128 tile, 32-voxel blocks
+        i8_ops = 2.0 * 28 * nt * (nt + 1) / 2 * 128 * 128 * (-(-V // 32) * 32) * n_local
     elif dom == "finalize":
         launch_ms = once["finalize"]
         alg_flops = 2.0 * local_units * K
@@ -383,7 +397,21 @@ def run_ours(args):
             traffic = json.loads(tfile.read_text()).get(f"{args.config}:{algo}", {}).get(dom)
         except Exception:  # noqa: BLE001
             traffic = None
-    if dom in ("tc_apass", "tc_bpass"):
+    if dom == "oz_gram":
+        achieved_tops = i8_ops / (launch_ms / 1e3) / 1e12
+        roofline = {
+            "bound": "tensor", "achieved": achieved_tops, "peak": I8_PEAK_TOPS, "unit": "TOPS (int8)",
+            "frac": achieved_tops / I8_PEAK_TOPS, "traffic": traffic, "kernel": dom, "launch_ms": launch_ms,
+            "algorithmic_int8_ops_per_launch": i8_ops, "algorithmic_flops_per_launch": alg_flops,
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "peak_source": "twice the measured bf16 burst peak of MEASURED_PEAKS.json (dense int8 = 2x bf16 rate)",
+        }
+        other_roofline = {
+            "bound": "fp64-equivalent", "achieved": achieved_tf, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved_tf / DMMA_PEAK_TFLOPS, "kernel": dom,
+            "peak_source": "X^T X flops (V T (T+1)) per second against the measured fp64 DMMA peak (37.1 TF/s)",
+        }
+    elif dom in ("tc_apass", "tc_bpass"):
         # fp32 X-hat on tcgen05 (3xTF32): the pass is designed to be HBM-bound
         roofline = {
             "bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
@@ -417,14 +445,14 @@ def run_ours(args):
         torch.cuda.empty_cache()
         subjects = [SubjectData(f"sub-{start + j:04d}", host[j]) for j in range(n_local)]
         conf = srm.SrmConfig(k=K, iterations=cfg["iterations"], seed=args.seed)
-        srm.fit(subjects, conf, comm, algorithm=args.algorithm)  # warm-up (allocator, kernels)
+        srm.fit(subjects, conf, comm, algorithm=args.algorithm, gram_int8=args.gram_int8 == "on")  # warm-up (allocator, kernels)
         times = []
         for _ in range(max(1, args.e2e_fits)):
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            model = srm.fit(subjects, conf, comm, algorithm=args.algorithm)
+            model = srm.fit(subjects, conf, comm, algorithm=args.algorithm, gram_int8=args.gram_int8 == "on")
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             if world > 1:
@@ -453,6 +481,8 @@ def run_ours(args):
             "data": "synthetic: BASELINE generative recipe (seeded, device Philox stream); reference init",
             "config": config_json(cfg, args.config, world),
             "roofline": roofline, "secondary_roofline": other_roofline, "algorithm": algo,
+            "gram_xtx": ("int8 slices on tcgen05 (7 slices, ~2^-48 of column max)" if use_i8 else "fp64 DMMA")
+            if algo == "gram" else None,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "kernel_ms": prof, "kernel_share": step_share, "impl": "ours",
         }

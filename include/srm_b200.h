@@ -55,9 +55,13 @@ enum srm_flags {
   SRM_FLAG_GRAM = 4,      /* per-iteration contractions through the T x T data Gram
                              (one-time X^T X); exact algebra, fewer flops when
                              4*K*iterations > T */
-  SRM_FLAG_TC = 8         /* fp32 X-hat: streaming passes on the tcgen05 tensor cores
+  SRM_FLAG_TC = 8,        /* fp32 X-hat: streaming passes on the tcgen05 tensor cores
                              as 3xTF32 split-precision MMAs (ignored for fp64
                              storage, K > 128, or with SRM_FLAG_GRAM) */
+  SRM_FLAG_GRAM_I8 = 16   /* with SRM_FLAG_GRAM and fp64 storage: X^T X from seven
+                             exact int8 slices per value (power-of-two column
+                             scales) on the tcgen05 int8 tensor cores, ~2^-48
+                             relative to the column maxima; otherwise fp64 DMMA */
 };
 
 /* workspace regions (srm_plan_region) */
@@ -192,6 +196,9 @@ int srm_graph_launch(srm_plan* plan, void* stream);
  * receives the number of kernels.  srm_profile_name(i) names kernel i of the
  * last profiled iteration. */
 int srm_profile_iteration(srm_plan* plan, float* ms_out, int capacity, int* n_out, void* stream);
+/* the same for srm_prepare_gram over all local subjects (SRM_FLAG_GRAM plans;
+ * *n_out = 0 otherwise) */
+int srm_profile_gram(srm_plan* plan, float* ms_out, int capacity, int* n_out, void* stream);
 const char* srm_profile_name(int index);
 
 /* synchronous copy of the device status word {code, arg, iteration, 0} */

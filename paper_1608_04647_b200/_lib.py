@@ -45,6 +45,7 @@ SIGNATURES = [
     ("srm_graph_capture", c_int, [c_vp]),
     ("srm_graph_launch", c_int, [c_vp, c_vp]),
     ("srm_profile_iteration", c_int, [c_vp, ctypes.POINTER(ctypes.c_float), c_int, c_i32p, c_vp]),
+    ("srm_profile_gram", c_int, [c_vp, ctypes.POINTER(ctypes.c_float), c_int, c_i32p, c_vp]),
     ("srm_profile_name", ctypes.c_char_p, [c_int]),
     ("srm_read_status", c_int, [c_vp, c_i32p]),
     ("srm_clear_status", c_int, [c_vp, c_vp]),
@@ -61,7 +62,7 @@ SIGNATURES = [
 
 # include/srm_b200.h enums
 SRM_F64, SRM_F32 = 0, 1
-FLAG_ORDERED, FLAG_TOLERANCE, FLAG_GRAM, FLAG_TC = 1, 2, 4, 8
+FLAG_ORDERED, FLAG_TOLERANCE, FLAG_GRAM, FLAG_TC, FLAG_GRAM_I8 = 1, 2, 4, 8, 16
 (R_XHAT, R_AMAT, R_WOUT, R_MU, R_TERMS, R_RED, R_REDLOCAL, R_S, R_SIGMA, R_HIST, R_STATUS,
  R_MMAT, R_SCAL, R_GRAM, R_VAR) = range(15)
 (D_LDX, D_KP, D_ROWS, D_TERM_STRIDE, D_RED_STRIDE, D_HIST_STRIDE, D_N_SLOTS, D_SLOT_OFFSET,

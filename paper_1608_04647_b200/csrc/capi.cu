@@ -64,6 +64,10 @@ enum Internal {
   I_ITEMS_TB,
   I_ITEMS_TA,
   I_ITEMS_TG,
+  I_OZQ,
+  I_OZCMAX,
+  I_OZEXP,
+  I_ITEMS_OZ,
   I_COUNT
 };
 
@@ -103,6 +107,9 @@ struct srm_plan {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   TmaMap tm_x_a, tm_s, tm_a, tm_x_b;  // tensor-core path TMA maps (bound at srm_plan_bind)
+  std::vector<OzItem> items_oz;       // int8-sliced Gram tiles (SRM_FLAG_GRAM_I8)
+  int64_t oz_lq = 0, max_v = 0;       // bytes per sliced TR row; largest local V
+  TmaMap tm_q;
 };
 
 namespace {
@@ -158,6 +165,11 @@ void layout(srm_plan* p) {
   sz[I_ITEMS_TB] = (int64_t)p->items_tb.size() * sizeof(ItemE);
   sz[I_ITEMS_TA] = (int64_t)p->items_ta.size() * sizeof(ItemA);
   sz[I_ITEMS_TG] = (int64_t)p->items_tg.size() * sizeof(ItemE);
+  const bool i8 = (p->flags & SRM_FLAG_GRAM_I8) != 0;
+  sz[I_OZQ] = i8 ? (int64_t)p->n_local * p->ldx * p->oz_lq : 0;
+  sz[I_OZCMAX] = i8 ? (int64_t)p->n_local * p->ldx * 8 : 0;
+  sz[I_OZEXP] = i8 ? (int64_t)p->n_local * p->ldx * 4 : 0;
+  sz[I_ITEMS_OZ] = (int64_t)p->items_oz.size() * sizeof(OzItem);
   int64_t cur = 0;
   for (int r = 0; r < I_COUNT; ++r) {
     p->off[r] = cur;
@@ -281,6 +293,17 @@ void build_work(srm_plan* p) {
         p->items_bg.push_back(it);
       }
     }
+  }
+  // int8-sliced Gram: the same upper tiles, slices [n_local][ldx][oz_lq]
+  p->items_oz.clear();
+  p->max_v = 0;
+  for (int i = 0; i < p->n_local; ++i) p->max_v = std::max(p->max_v, p->V[i]);
+  p->oz_lq = round_up(std::max<int64_t>(p->max_v, 1), 32) / 32 * kOzRecord;
+  if (p->flags & SRM_FLAG_GRAM_I8) {
+    for (int i = 0; i < p->n_local; ++i)
+      for (int64_t m0 = 0; m0 < p->ldx; m0 += 128)
+        for (int64_t n0 = m0; n0 < p->ldx; n0 += 128)
+          p->items_oz.push_back({i, (int32_t)m0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32)});
   }
   // tensor-core path: A-pass row tiles (A in the fp32 [rows][np] region) and
   // B-pass tiles of 128 TRs over the same V chunks
@@ -494,6 +517,61 @@ int run_contractions(srm_plan* p, cudaStream_t st) {
 
 std::vector<std::string> g_profile_names;
 
+// one-time Gram X_i^T X_i of local subjects [first, first + count): int8
+// slices on the tensor cores (SRM_FLAG_GRAM_I8) or fp64 DMMA tiles, then the
+// lower triangle mirrored from the upper one
+std::vector<Stage> gram_stages(srm_plan* p, int first, int count) {
+  const DevPlan& d = p->dp;
+  std::vector<Stage> v;
+  if (p->flags & SRM_FLAG_GRAM_I8) {
+    const int per = (int)(p->items_oz.size() / p->n_local);  // upper tiles per subject (subject-major)
+    v.push_back({"oz_split", [p, d, first, count](cudaStream_t st) {
+                   return launch_oz_prepare(d, first, count, region<unsigned long long>(p, I_OZCMAX),
+                                            region<int8_t>(p, I_OZQ), p->oz_lq, region<int32_t>(p, I_OZEXP),
+                                            p->max_v, st);
+                 }});
+    v.push_back({"oz_gram", [p, d, first, count, per](cudaStream_t st) {
+                   return launch_oz_gram(p->tm_q, region<int32_t>(p, I_OZEXP), d.gram, p->ldx,
+                                         region<OzItem>(p, I_ITEMS_OZ) + (int64_t)first * per, count * per, st);
+                 }});
+  } else {
+    const int per = (int)(p->items_gram.size() / p->n_local);
+    v.push_back({"gram_tiles", [p, d, first, count, per](cudaStream_t st) {
+                   return launch_gram_tiles(p->dtype, d.xhat, p->ldx, d.gram, p->ldx,
+                                            region<ItemE>(p, I_ITEMS_GRAM) + (int64_t)first * per, count * per, st);
+                 }});
+  }
+  v.push_back({"mirror_gram", [d, first, count](cudaStream_t st) { return launch_mirror_gram(d, first, count, st); }});
+  return v;
+}
+
+// run stages eagerly with an event between kernels; names -> srm_profile_name
+int profile_stages(const std::vector<Stage>& stages, float* ms_out, int capacity, int* n_out, cudaStream_t st) {
+  const int n = (int)stages.size();
+  std::vector<cudaEvent_t> ev(n + 1);
+  for (auto& e : ev) cudaEventCreate(&e);
+  cudaEventRecord(ev[0], st);
+  int rc = SRM_OK;
+  for (int i = 0; i < n && rc == SRM_OK; ++i) {
+    cudaError_t e = stages[i].fn(st);
+    if (e != cudaSuccess) rc = cuda_fail(e, stages[i].name);
+    cudaEventRecord(ev[i + 1], st);
+  }
+  cudaError_t e = cudaEventSynchronize(ev[n]);
+  if (rc == SRM_OK && e != cudaSuccess) rc = cuda_fail(e, "profile sync");
+  g_profile_names.clear();
+  for (int i = 0; i < n; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+    if (i < capacity) ms_out[i] = ms;
+    g_profile_names.push_back(stages[i].name);
+  }
+  for (auto& x : ev) cudaEventDestroy(x);
+  *n_out = n;
+  return rc;
+}
+
+
 }  // namespace
 
 extern "C" {
@@ -541,6 +619,7 @@ int srm_plan_create(srm_plan** out, int dtype, int n_local, const int64_t* n_vox
   if (world_size == 1) p->flags |= SRM_FLAG_ORDERED;
   if ((p->flags & SRM_FLAG_TC) && (dtype != SRM_F32 || !tc_supported((int)k))) p->flags &= ~SRM_FLAG_TC;
   if ((p->flags & SRM_FLAG_TC) && (p->flags & SRM_FLAG_GRAM)) p->flags &= ~SRM_FLAG_TC;
+  if ((p->flags & SRM_FLAG_GRAM_I8) && (!(p->flags & SRM_FLAG_GRAM) || dtype != SRM_F64)) p->flags &= ~SRM_FLAG_GRAM_I8;
   p->np = tc_np((int)k);
   p->n_total = 0;
   p->max_local = 0;
@@ -625,7 +704,8 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
              {I_ITEMS_EA, p->items_ea.data()},  {I_ITEMS_A, p->items_a.data()},
              {I_ITEMS_G, p->items_g.data()},     {I_ITEMS_GRAM, p->items_gram.data()},
              {I_ITEMS_BG, p->items_bg.data()},   {I_ITEMS_TB, p->items_tb.data()},
-             {I_ITEMS_TA, p->items_ta.data()},   {I_ITEMS_TG, p->items_tg.data()}};
+             {I_ITEMS_TA, p->items_ta.data()},   {I_ITEMS_TG, p->items_tg.data()},
+             {I_ITEMS_OZ, p->items_oz.data()}};
   for (const Up& u : ups) {
     if (p->size[u.r] == 0) continue;
     e = cudaMemcpy(p->ws + p->off[u.r], u.src, p->size[u.r], cudaMemcpyHostToDevice);
@@ -659,6 +739,10 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
   }
   if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM))
     e = launch_gram_tiles(p->dtype, d.xhat, p->ldx, d.gram, p->ldx, nullptr, 0, 0);
+  if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM_I8)) {
+    e = make_map_q(&p->tm_q, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local);
+    if (e == cudaSuccess) e = launch_oz_gram(p->tm_q, nullptr, nullptr, p->ldx, nullptr, 0, 0);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
   return SRM_OK;
 }
@@ -744,32 +828,10 @@ int srm_graph_launch(srm_plan* p, void* stream) {
 
 int srm_profile_iteration(srm_plan* p, float* ms_out, int capacity, int* n_out, void* stream) {
   if (!p || !p->ws || !ms_out || !n_out) return fail(SRM_ERR_CONFIG, "plan not bound");
-  cudaStream_t st = as_stream(stream);
   std::vector<Stage> stages = e_stages(p);
   std::vector<Stage> m = m_stages(p);
   stages.insert(stages.end(), m.begin(), m.end());
-  const int n = (int)stages.size();
-  std::vector<cudaEvent_t> ev(n + 1);
-  for (auto& e : ev) cudaEventCreate(&e);
-  cudaEventRecord(ev[0], st);
-  int rc = SRM_OK;
-  for (int i = 0; i < n && rc == SRM_OK; ++i) {
-    cudaError_t e = stages[i].fn(st);
-    if (e != cudaSuccess) rc = cuda_fail(e, stages[i].name);
-    cudaEventRecord(ev[i + 1], st);
-  }
-  cudaError_t e = cudaEventSynchronize(ev[n]);
-  if (rc == SRM_OK && e != cudaSuccess) rc = cuda_fail(e, "profile sync");
-  g_profile_names.clear();
-  for (int i = 0; i < n; ++i) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
-    if (i < capacity) ms_out[i] = ms;
-    g_profile_names.push_back(stages[i].name);
-  }
-  for (auto& x : ev) cudaEventDestroy(x);
-  *n_out = n;
-  return rc;
+  return profile_stages(stages, ms_out, capacity, n_out, as_stream(stream));
 }
 
 const char* srm_profile_name(int index) {
@@ -810,12 +872,20 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
   if (first < 0 || count < 0 || first + count > p->n_local) return fail(SRM_ERR_CONFIG, "subject range out of bounds");
   if (count == 0) return SRM_OK;
   cudaStream_t st = as_stream(stream);
-  const DevPlan& d = p->dp;
-  const int per = (int)(p->items_gram.size() / p->n_local);  // upper tiles per subject (subject-major)
-  cudaError_t e = launch_gram_tiles(p->dtype, d.xhat, p->ldx, d.gram, p->ldx,
-                                    region<ItemE>(p, I_ITEMS_GRAM) + (int64_t)first * per, count * per, st);
-  if (e == cudaSuccess) e = launch_mirror_gram(d, first, count, st);
-  return check(e, "prepare_gram");
+  for (const Stage& s : gram_stages(p, first, count)) {
+    const cudaError_t e = s.fn(st);
+    if (e != cudaSuccess) return cuda_fail(e, s.name);
+  }
+  return SRM_OK;
+}
+
+int srm_profile_gram(srm_plan* p, float* ms_out, int capacity, int* n_out, void* stream) {
+  if (!p || !p->ws || !ms_out || !n_out) return fail(SRM_ERR_CONFIG, "plan not bound");
+  if (!(p->flags & SRM_FLAG_GRAM)) {
+    *n_out = 0;
+    return SRM_OK;
+  }
+  return profile_stages(gram_stages(p, 0, p->n_local), ms_out, capacity, n_out, as_stream(stream));
 }
 
 int srm_prepare_gram(srm_plan* p, void* stream) {

@@ -63,6 +63,20 @@ cudaError_t launch_tc_bpass(int np, const TmaMap& tmA, const TmaMap& tmXb, int64
                             int orows, const ItemE* items, int n_items, cudaStream_t st);
 constexpr int kTcRows = 256;  // A-pass rows per CTA / B-pass TRs per CTA
 
+// int8-sliced fp64 Gram (ozaki.cu): one upper 128 x 128 tile of G_subj
+struct OzItem {
+  int32_t subj;  // local subject
+  int32_t m0;    // first row (TR) of the tile
+  int32_t n0;    // first column (TR) of the tile
+  int32_t nvb;   // 32-voxel blocks of the subject
+};
+constexpr int kOzChunkBlocks = 2048;  // 65536 voxels per exact int32 accumulation
+constexpr int64_t kOzRecord = 256;    // bytes per (TR, 32-voxel block): 8 slots x 32 voxels
+cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, int64_t n);
+size_t oz_gram_smem_bytes();
+cudaError_t launch_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
+                           int n_items, cudaStream_t st);
+
 // thread-local message returned by srm_last_error() (defined in capi.cu)
 void set_last_error(const char* where, cudaError_t e);
 

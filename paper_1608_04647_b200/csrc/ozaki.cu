@@ -1,0 +1,346 @@
+// fp64 Gram X_i^T X_i of the Gram path on the int8 tensor cores.
+//
+// The one-time G_i = Xhat_i^T Xhat_i (V_i x T, fp64) is computed from exact
+// int8 slices of Xhat (an Ozaki-style splitting with a power-of-two scale per
+// column t):
+//
+//   x[v][t] = 2^{e_t} * sum_s q_s[v][t] 2^{-6-7s} + r,   |q_s| <= 64,
+//   |r| <= 2^{e_t} 2^{-7S-6} / 2,
+//
+// where 2^{e_t} >= max_v |x[v][t]|.  Then
+//
+//   G[a][b] ~= 2^{e_a+e_b} sum_{d=0}^{S-1} 2^{-12-7d} sum_{s+s'=d} (Q_s^T Q_s')[a][b]
+//
+// Every inner product of int8 slices is exact in int32 (|q| <= 64, at most
+// S pairs per d, at most kOzChunkBlocks * 32 voxels per accumulation), so the
+// only approximations are the truncation of x to 6 + 7 (S - 1) bits below its
+// column maximum and the dropped pairs s + s' >= S: with S = 7 each product
+// x_a x_b is represented to ~2^-48 of 2^{e_a+e_b}, ~1e-14 relative to G for
+// data with column max/rms ~ 5 (BASELINE recipe).  The fp64 result then feeds
+// the same per-iteration B = S G / 2 as the fp64 DMMA Gram.
+//
+// Kernels:
+//   oz_colmax  max |x| per (subject, column) (bit pattern atomicMax)
+//   oz_split   slices, transposed: Q[i][t][vb][slot][32 voxels] (int8; a
+//              256-byte record per (t, 32-voxel block): slices 0-3 in the low
+//              128 bytes, 4-6 (+ a zero slot) in the high 128 bytes)
+//   oz_gram    one 128 x 128 upper tile per CTA: TMA (SWIZZLE_128B, 128-byte
+//              rows) -> tcgen05.mma kind::i8 (M = N = 128, K = 32 voxels; the
+//              slice is selected by the 32-byte descriptor advance) -> four
+//              int32 accumulators in TMEM (512 columns).  Pass 1 accumulates
+//              d = 0..3 from the low halves, pass 2 d = 4..6 from both halves;
+//              the epilogue warps scale and sum the d-groups in fp64 in order.
+#include <cuda.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "plan.h"
+#include "tcgen05.cuh"
+
+namespace srm {
+
+namespace {
+
+using namespace tc;
+
+constexpr int kOzSlices = 7;
+constexpr int kOzThreads = 192;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue
+constexpr int kOzStages = 3;
+constexpr int kOzBox = 16384;    // one 128-row x 128-byte SW128 box
+constexpr int kOzStageBytes = 4 * kOzBox;
+
+__device__ __forceinline__ int frexp_exp(double m) {
+  int e = 0;
+  frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
+  return e;
+}
+
+// ---------------------------------------------------------------------------
+// column maxima: grid (row blocks, subjects), one thread per column
+// ---------------------------------------------------------------------------
+constexpr int kColmaxRows = 256;
+
+__global__ void __launch_bounds__(256) k_oz_colmax(DevPlan p, const double* __restrict__ xhat,
+                                                   unsigned long long* __restrict__ cmax) {
+  const int i = blockIdx.y;
+  const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
+  const int64_t row0 = sj[SC_ROW_OFF], V = sj[SC_V];
+  const int64_t r0 = (int64_t)blockIdx.x * kColmaxRows;
+  if (r0 >= V) return;
+  const int64_t r1 = min(V, r0 + kColmaxRows);
+  for (int64_t t = threadIdx.x; t < p.ldx; t += blockDim.x) {
+    const double* x = xhat + (row0 + r0) * p.ldx + t;
+    double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
+    int64_t r = r0;
+    for (; r + 4 <= r1; r += 4, x += 4 * p.ldx) {
+      m0 = fmax(m0, fabs(x[0]));
+      m1 = fmax(m1, fabs(x[p.ldx]));
+      m2 = fmax(m2, fabs(x[2 * p.ldx]));
+      m3 = fmax(m3, fabs(x[3 * p.ldx]));
+    }
+    for (; r < r1; ++r, x += p.ldx) m0 = fmax(m0, fabs(x[0]));
+    const double m = fmax(fmax(m0, m1), fmax(m2, m3));
+    if (m > 0.0) atomicMax(cmax + (int64_t)i * p.ldx + t, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// split: grid (32-voxel blocks, 128-column tiles, subjects); thread (t, half)
+// handles 16 voxels of one column, 4 voxels per packed 32-bit word
+// ---------------------------------------------------------------------------
+constexpr int kSplitLdw = 68;  // words per smem row: 16-byte aligned, conflict-free uint4 access
+
+// rint(y) for |y| < 2^51 by the 1.5 * 2^52 shift; the rounded integer is also
+// the low word of the shifted value (two's complement), so no F2I is needed
+__device__ __forceinline__ double round_shift(double y, int* low) {
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52
+  const double t = y + magic;
+  *low = __double2loint(t);
+  return t - magic;
+}
+
+__global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const double* __restrict__ xhat,
+                                                  const unsigned long long* __restrict__ cmax,
+                                                  int8_t* __restrict__ q, int64_t lq, int32_t* __restrict__ expo) {
+  __shared__ __align__(16) uint32_t buf[128 * kSplitLdw];
+  const int i = blockIdx.z;
+  const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
+  const int64_t row0 = sj[SC_ROW_OFF], V = sj[SC_V];
+  const int64_t vb = blockIdx.x;
+  if (vb * 32 >= V) return;
+  const int64_t t0 = (int64_t)blockIdx.y * 128;
+  const int tl = threadIdx.x & 127, half = threadIdx.x >> 7;
+  const int64_t t = t0 + tl;
+  const bool tin = t < p.ldx;
+  int e = 0;
+  if (tin) {
+    const double m = __longlong_as_double((long long)cmax[(int64_t)i * p.ldx + t]);
+    e = (m > 0.0) ? frexp_exp(m) : 0;
+    if (vb == 0 && half == 0) expo[(int64_t)i * p.ldx + t] = e;
+  }
+  // 2^(6 - e) exactly (normal range: |e| < 1000)
+  const double scale = __longlong_as_double((long long)(1023 + 6 - e) << 52);
+  double x[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int64_t v = vb * 32 + half * 16 + u;
+    x[u] = (tin && v < V) ? xhat[(row0 + v) * p.ldx + t] : 0.0;
+  }
+  uint32_t w[kOzSlices][4];
+#pragma unroll
+  for (int s = 0; s < kOzSlices; ++s)
+#pragma unroll
+    for (int g = 0; g < 4; ++g) w[s][g] = 0u;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    double y = x[u] * scale;  // |y| < 64
+#pragma unroll
+    for (int s = 0; s < kOzSlices; ++s) {
+      int low;
+      const double r = round_shift(y, &low);
+      w[s][u >> 2] |= (uint32_t)(low & 0xFF) << (8 * (u & 3));
+      y = (y - r) * 128.0;  // exact: |y - r| <= 1/2
+    }
+  }
+  // record layout per t: 16-byte chunk (slot * 2 + half); slot 7 stays zero
+  uint4* row = reinterpret_cast<uint4*>(buf + tl * kSplitLdw);
+#pragma unroll
+  for (int s = 0; s < kOzSlices; ++s) row[s * 2 + half] = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+  row[7 * 2 + half] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  // 128 rows x 16 chunks of 16 bytes; 16 consecutive threads write one 256-byte record
+  for (int c = threadIdx.x; c < 128 * 16; c += blockDim.x) {
+    const int r = c >> 4, k = c & 15;
+    const int64_t tt = t0 + r;
+    if (tt < p.ldx) {
+      uint4* dst = reinterpret_cast<uint4*>(q + ((int64_t)i * p.ldx + tt) * lq + vb * kOzRecord);
+      dst[k] = reinterpret_cast<const uint4*>(buf + r * kSplitLdw)[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// gram tiles
+// ---------------------------------------------------------------------------
+struct OzBars {
+  uint64_t full[kOzStages];
+  uint64_t empty[kOzStages];
+  uint64_t accfull;
+  uint64_t accfree;
+};
+
+__global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant__ CUtensorMap tmq,
+                                                           const int32_t* __restrict__ expo, double* __restrict__ G,
+                                                           int64_t ldx, const OzItem* __restrict__ items) {
+  extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ OzBars bars;
+  __shared__ uint32_t tmem_base;
+  const OzItem it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool diag = it.m0 == it.n0;
+  const int nvb = it.nvb;
+  const int nchunks = (nvb + kOzChunkBlocks - 1) / kOzChunkBlocks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < kOzStages; ++s) {
+        mbar_init(&bars.full[s], 1);
+        mbar_init(&bars.empty[s], 1);
+      }
+      mbar_init(&bars.accfull, 1);
+      mbar_init(&bars.accfree, 128);
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+  } else if (warp == 1) {
+    tmem_alloc(&tmem_base, 512);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int k = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int vb = b0; vb < b1; ++vb, ++k) {
+            const int slot = k % kOzStages;
+            if (k >= kOzStages) mbar_wait(&bars.empty[slot], ((k / kOzStages) - 1) & 1);
+            const int nbox = (pass ? 2 : 1) * (diag ? 1 : 2);
+            mbar_expect_tx(&bars.full[slot], (uint32_t)(nbox * kOzBox));
+            unsigned char* st = smem + slot * kOzStageBytes;
+            const int x = vb * 256;
+            tma_load_3d(st, &tmq, x, it.m0, it.subj, &bars.full[slot]);
+            if (pass) tma_load_3d(st + kOzBox, &tmq, x + 128, it.m0, it.subj, &bars.full[slot]);
+            if (!diag) {
+              tma_load_3d(st + 2 * kOzBox, &tmq, x, it.n0, it.subj, &bars.full[slot]);
+              if (pass) tma_load_3d(st + 3 * kOzBox, &tmq, x + 128, it.n0, it.subj, &bars.full[slot]);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_s8(128, 128);
+      int k = 0, npass = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
+        for (int pass = 0; pass < 2; ++pass, ++npass) {
+          // the epilogue must have drained the previous pass's accumulators
+          if (npass > 0) mbar_wait(&bars.accfree, (npass - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          for (int vb = b0; vb < b1; ++vb, ++k) {
+            const int slot = k % kOzStages;
+            mbar_wait(&bars.full[slot], (k / kOzStages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t sa = smem_u32(smem + slot * kOzStageBytes);
+            const uint32_t sb = diag ? sa : sa + 2 * kOzBox;
+            const int first = vb == b0;
+            const int dlo = pass ? 4 : 0, dhi = pass ? kOzSlices - 1 : 3;
+            for (int d = dlo; d <= dhi; ++d) {
+              const uint32_t acc = tmem + 128u * (uint32_t)(d - dlo);
+              const int s0 = max(0, d - (kOzSlices - 1)), s1 = min(d, kOzSlices - 1);
+              for (int s = s0; s <= s1; ++s) {
+                const int s2 = d - s;
+                const uint64_t da = umma_desc_sw128(sa + (s >> 2) * kOzBox + 32 * (s & 3));
+                const uint64_t db = umma_desc_sw128(sb + (s2 >> 2) * kOzBox + 32 * (s2 & 3));
+                mma_s8(acc, da, db, idesc, (first && s == s0) ? 0 : 1);
+              }
+            }
+            mma_commit(&bars.empty[slot]);
+          }
+          mma_commit(&bars.accfull);
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2-5 own TMEM lanes 32 (warp % 4) ----------------
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int64_t ta = it.m0 + r;
+    const bool rin = ta < ldx;
+    const int32_t* ex = expo + (int64_t)it.subj * ldx;
+    const int ea = rin ? ex[ta] : 0;
+    double* grow = G + (int64_t)it.subj * ldx * ldx + ta * ldx + it.n0;
+    int npass = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      for (int pass = 0; pass < 2; ++pass, ++npass) {
+        mbar_wait(&bars.accfull, npass & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int dlo = pass ? 4 : 0, dhi = pass ? kOzSlices - 1 : 3;
+        for (int c0 = 0; c0 < 128; c0 += 16) {
+          double val[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) val[j] = 0.0;
+          for (int d = dlo; d <= dhi; ++d) {
+            uint32_t raw[16];
+            tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 128u * (uint32_t)(d - dlo) + c0, raw);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) val[j] += ldexp((double)(int32_t)raw[j], -12 - 7 * d);
+          }
+          if (rin) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int64_t tb = it.n0 + c0 + j;
+              if (tb < ldx) {
+                const double g = ldexp(val[j], ea + ex[tb]);
+                grow[c0 + j] = (npass == 0) ? g : grow[c0 + j] + g;
+              }
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        mbar_arrive(&bars.accfree);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) tmem_free(tmem, 512);
+}
+
+}  // namespace
+
+size_t oz_gram_smem_bytes() { return (size_t)kOzStages * kOzStageBytes + 1024; }
+
+cudaError_t launch_oz_prepare(const DevPlan& p, int first, int count, unsigned long long* cmax, int8_t* q,
+                              int64_t lq, int32_t* expo, int64_t max_v, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  DevPlan sub = p;
+  sub.subj = p.subj + (int64_t)first * kSubjCols;
+  cudaError_t e = cudaMemsetAsync(cmax + (int64_t)first * p.ldx, 0, (size_t)count * p.ldx * sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  const dim3 g1((unsigned)((max_v + kColmaxRows - 1) / kColmaxRows), (unsigned)count);
+  k_oz_colmax<<<g1, 256, 0, st>>>(sub, static_cast<const double*>(p.xhat), cmax + (int64_t)first * p.ldx);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const dim3 g2((unsigned)((max_v + 31) / 32), (unsigned)((p.ldx + 127) / 128), (unsigned)count);
+  k_oz_split<<<g2, 256, 0, st>>>(sub, static_cast<const double*>(p.xhat), cmax + (int64_t)first * p.ldx,
+                                 q + (int64_t)first * p.ldx * lq, lq, expo + (int64_t)first * p.ldx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
+                           int n_items, cudaStream_t st) {
+  const size_t bytes = oz_gram_smem_bytes();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_oz_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (n_items == 0) return cudaSuccess;
+  k_oz_gram<<<n_items, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(tmq.opaque), expo, G, ldx,
+                                                 items);
+  return cudaGetLastError();
+}
+
+}  // namespace srm

@@ -88,6 +88,10 @@ cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_sigma(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_mirror_gram(const DevPlan& p, int first, int count, cudaStream_t s);
+// int8-sliced Gram (ozaki.cu): column maxima, exponents and slices of local
+// subjects [first, first + count)
+cudaError_t launch_oz_prepare(const DevPlan& p, int first, int count, unsigned long long* cmax, int8_t* q,
+                              int64_t lq, int32_t* expo, int64_t max_v, cudaStream_t st);
 cudaError_t launch_reset(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_apply_w(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);
 cudaError_t launch_apply_w_f32(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);

@@ -39,7 +39,8 @@ class SrmEngine:
     """Device state of one worker's subjects for an SRM fit."""
 
     def __init__(self, n_voxels, n_trs, k, iterations, *, storage="f64", world_size=1,
-                 rank=0, counts=None, ordered=True, tolerance=False, gram=False, tc=False, device=None):
+                 rank=0, counts=None, ordered=True, tolerance=False, gram=False, tc=False, gram_i8=False,
+                 device=None):
         torch = _torch()
         self.lib = _lib.load()
         if not torch.cuda.is_available():
@@ -67,6 +68,8 @@ class SrmEngine:
             flags |= _lib.FLAG_GRAM
         if tc:
             flags |= _lib.FLAG_TC
+        if gram_i8:
+            flags |= _lib.FLAG_GRAM_I8
         self.ordered = bool(ordered) or self.world_size == 1
         plan = ctypes.c_void_p()
         varr = (ctypes.c_int64 * self.n_local)(*self.n_voxels)
@@ -92,6 +95,7 @@ class SrmEngine:
         eff = d(_lib.D_FLAGS)
         self.gram = bool(eff & _lib.FLAG_GRAM)
         self.tc = bool(eff & _lib.FLAG_TC)
+        self.gram_i8 = bool(eff & _lib.FLAG_GRAM_I8)
         self._graph = None
         self._staging = {}
 
@@ -372,6 +376,15 @@ class SrmEngine:
         n = ctypes.c_int32()
         _lib.check(self.lib.srm_profile_iteration(self.plan, ms, cap, ctypes.byref(n),
                                                   ctypes.c_void_p(self.stream())), "profile")
+        return [(self.lib.srm_profile_name(i).decode(), float(ms[i])) for i in range(n.value)]
+
+    def profile_gram(self):
+        """The one-time X^T X stages, eagerly, with an event between kernels -> [(name, ms)]."""
+        cap = 16
+        ms = (ctypes.c_float * cap)()
+        n = ctypes.c_int32()
+        _lib.check(self.lib.srm_profile_gram(self.plan, ms, cap, ctypes.byref(n),
+                                             ctypes.c_void_p(self.stream())), "profile_gram")
         return [(self.lib.srm_profile_name(i).decode(), float(ms[i])) for i in range(n.value)]
 
     @property

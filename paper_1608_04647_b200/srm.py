@@ -343,16 +343,26 @@ def _storage_for(subjects, storage):
 _DMMA_FLOPS = 30e12
 _HBM_BYTES = 6.0e12
 _TF32_FLOPS = 0.9e15
+_I8_OPS = 3.2e15       # int8 tcgen05 (dense 4.5e15 nominal), as sustained by the sliced Gram
+_I8_PRODUCTS = 28      # slice pairs s + s' < 7 of the int8-sliced Gram
 
 
-def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f64"):
+def gram_int8_bytes(n_voxels, n_trs):
+    """Device bytes of the int8 slices of the Gram path (256 B per TR and 32 voxels)."""
+    ldx = -(-n_trs // 32) * 32
+    lq = -(-max(n_voxels) // 32) * 256
+    return len(n_voxels) * ldx * (lq + 12)
+
+
+def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f64", gram_int8=False):
     """'gram' or 'stream' from an estimate of each path's device time.
 
     stream: per iteration two passes over X-hat (A = X S^T / 2, B = A^T X):
             4 V T K flops per subject on the FP64 tensor pipe, or -- for fp32
             X-hat on the tcgen05 3xTF32 path -- max(HBM time of 2 reads, MMA time).
-    gram:   one-time X^T X (upper 128-tiles, V T^2 flops on DMMA), then 2 K T^2
-            per subject-iteration for B = S G / 2, plus one final A pass.
+    gram:   one-time X^T X (upper 128-tiles, V T^2 flops on DMMA, or 28 int8
+            slice products plus three HBM passes with ``gram_int8``), then
+            2 K T^2 per subject-iteration for B = S G / 2, plus one final A pass.
     """
     kp = -(-k // 8) * 8
     ldx = -(-n_trs // 32) * 32
@@ -370,7 +380,12 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f
         else:
             stream += iterations * 2 * (2.0 * v * ldx * kp) / _DMMA_FLOPS
             final_a = 2.0 * v * ldx * kp / _DMMA_FLOPS
-        gram += (nt * (nt + 1) / 2 * 128 * 128 * 2.0 * v + iterations * 2.0 * kp * ldx * ldx) / _DMMA_FLOPS + final_a
+        tiles = nt * (nt + 1) / 2 * 128 * 128 * 2.0 * v
+        if gram_int8:
+            one_time = _I8_PRODUCTS * tiles / _I8_OPS + 3.0 * v * ldx * b / _HBM_BYTES
+        else:
+            one_time = tiles / _DMMA_FLOPS
+        gram += one_time + iterations * 2.0 * kp * ldx * ldx / _DMMA_FLOPS + final_a
     need = len(n_voxels) * ldx * ldx * 8
     if free_bytes is not None and need > 0.25 * free_bytes:
         return "stream"
@@ -379,7 +394,7 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f
 
 def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=True,
         keep_on_device=False, device=None, engine_out=None, timings=None, algorithm="auto",
-        tensor_cores=True):
+        tensor_cores=True, gram_int8=True):
     """Run the distributed EM; ``subjects`` are this worker's share (srm.py:216).
 
     Every worker calls this with the same config and its own communicator
@@ -400,6 +415,10 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     ``tensor_cores``: for fp32 X-hat on the streaming path, run the two passes
     as 3xTF32 tcgen05 MMAs (error ~1e-6, inside the 1e-4 fp32 tolerance);
     ``False`` keeps every contraction in fp64 on DMMA.
+    ``gram_int8``: on the Gram path with fp64 X-hat, form the one-time X^T X
+    from seven exact int8 slices per value on the int8 tensor cores (products
+    represented to ~2^-48 of the column maxima; ~1e-14 relative to G) when
+    the slices fit in device memory; ``False`` keeps it on fp64 DMMA.
     """
     clock = _PhaseClock(timings)
     config.validate()
@@ -428,17 +447,22 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
 
     n_vox = [int(s.X.shape[0]) for s in subjects]
     store = _storage_for(subjects, storage)
-    if algorithm == "auto":
+    use_i8 = bool(gram_int8) and store == "f64"
+    if use_i8 or algorithm == "auto":
         torch = _torch()
         free, _ = torch.cuda.mem_get_info(device)
+        x_bytes = sum(n_vox) * (-(-n_trs // 32) * 32) * 8
+        use_i8 = use_i8 and gram_int8_bytes(n_vox, n_trs) + x_bytes < 0.6 * free
+    if algorithm == "auto":
         algorithm = choose_algorithm(n_vox, n_trs, k, config.iterations, free,
-                                     storage=store if tensor_cores else "f64")
+                                     storage=store if tensor_cores else "f64", gram_int8=use_i8)
     if algorithm not in ("stream", "gram"):
         raise ConfigError("algorithm must be 'auto', 'stream' or 'gram'")
     eng = SrmEngine(n_vox, n_trs, k, config.iterations,
                     storage=store, world_size=comm.size, rank=comm.rank,
                     counts=counts, ordered=ordered, tolerance=config.tolerance is not None,
-                    gram=algorithm == "gram", tc=bool(tensor_cores) and store == "f32", device=device)
+                    gram=algorithm == "gram", tc=bool(tensor_cores) and store == "f32",
+                    gram_i8=algorithm == "gram" and use_i8, device=device)
     if engine_out is not None:
         engine_out.append(eng)
     # the init draws depend only on (seed, global index, V, k): overlap them with the upload

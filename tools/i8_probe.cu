@@ -1,0 +1,130 @@
+// Probe: tcgen05.mma kind::i8 (s8 x s8 -> s32) with SWIZZLE_128B K-major smem
+// operands and a TMEM accumulator.  Validates the instruction-descriptor and
+// smem-descriptor encodings of the int8 Gram kernel (exact integer results).
+// Single CTA, M = 128, N = NN, K = 128 (four K = 32 steps).
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, uint32_t dfmt, uint32_t afmt) {
+  return (dfmt << 4) | (afmt << 7) | (afmt << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// row r (128 B of K) of a K-major SW128 tile: 16-byte chunk c lives at chunk c ^ (r & 7)
+__device__ __forceinline__ int sw128_off(int r, int kbyte) {
+  const int c = kbyte >> 4;
+  return r * 128 + ((c ^ (r & 7)) << 4) + (kbyte & 15);
+}
+
+template <int NN>
+__global__ void probe(const int8_t* A, const int8_t* B, int32_t* D, uint32_t idesc) {
+  constexpr int M = 128, K = 128;
+  extern __shared__ __align__(1024) int8_t dyn[];
+  int8_t* sa = dyn;
+  int8_t* sb = dyn + M * K;
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < M * K; e += blockDim.x) sa[sw128_off(e / K, e % K)] = A[e];
+  for (int e = tid; e < NN * K; e += blockDim.x) sb[sw128_off(e / K, e % K)] = B[e];
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  if (tid == 0) {
+    for (int ks = 0; ks < K / 32; ++ks) {
+      const uint64_t da = desc_sw128(smem_u32(sa) + ks * 32);
+      const uint64_t db = desc_sw128(smem_u32(sb) + ks * 32);
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                   "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                   "l"(da), "l"(db), "r"(idesc), "r"(ks));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&mbar)));
+  }
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(smem_u32(&mbar)), "r"(0));
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int warp = tid >> 5, lane = tid & 31, row = warp * 32 + lane;
+  for (int c0 = 0; c0 < NN; c0 += 16) {
+    uint32_t r[16];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + c0;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    for (int j = 0; j < 16; ++j) D[row * NN + c0 + j] = (int32_t)r[j];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+template <int NN>
+void run(uint32_t dfmt, uint32_t afmt, int lim) {
+  constexpr int M = 128, K = 128;
+  std::vector<int8_t> A(M * K), B(NN * K);
+  std::vector<int32_t> D(M * NN);
+  srand(11);
+  for (auto& x : A) x = (int8_t)(rand() % (2 * lim + 1) - lim);
+  for (auto& x : B) x = (int8_t)(rand() % (2 * lim + 1) - lim);
+  int8_t *dA, *dB;
+  int32_t* dD;
+  CK(cudaMalloc(&dA, A.size())); CK(cudaMalloc(&dB, B.size())); CK(cudaMalloc(&dD, D.size() * 4));
+  CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemset(dD, 0, D.size() * 4));
+  const int bytes = (M + NN) * K + 1024;
+  CK(cudaFuncSetAttribute(probe<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  probe<NN><<<1, 128, bytes>>>(dA, dB, dD, idesc_i8(M, NN, dfmt, afmt));
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+  long bad = 0;
+  for (int m = 0; m < M; ++m)
+    for (int n = 0; n < NN; ++n) {
+      int32_t ref = 0;
+      for (int k = 0; k < K; ++k) ref += (int32_t)A[m * K + k] * (int32_t)B[n * K + k];
+      if (ref != D[m * NN + n]) ++bad;
+    }
+  int32_t r00 = 0;
+  for (int k = 0; k < K; ++k) r00 += (int32_t)A[k] * (int32_t)B[k];
+  printf("i8 N=%d dfmt=%u afmt=%u lim=%d: mismatches %ld / %d  D[0]=%d ref %d\n", NN, dfmt, afmt, lim, bad, M * NN, D[0], r00);
+  cudaFree(dA); cudaFree(dB); cudaFree(dD);
+}
+
+int main() {
+  run<128>(2, 1, 64);
+  run<256>(2, 1, 64);
+  run<256>(2, 1, 127);
+  run<64>(2, 1, 127);
+  return 0;
+}
