@@ -226,3 +226,67 @@ def test_tensor_core_fp32_recipe_vs_oracle(srm):
                     tensor_cores=True)
         r = ref["iters"][n - 1]
         _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL32, f"tc recipe it{n - 1}")
+
+
+def _gram_pair(xs):
+    """X_i^T X_i of the demeaned subjects from the fp64 DMMA and the int8-sliced kernels."""
+    import torch
+
+    from paper_1608_04647_b200 import _lib
+    from paper_1608_04647_b200.engine import SrmEngine
+
+    T = xs[0].shape[1]
+    out = []
+    for i8 in (False, True):
+        eng = SrmEngine([x.shape[0] for x in xs], T, 4, 1, gram=True, gram_i8=i8)
+        assert eng.gram_i8 == i8, "int8 Gram flag not effective"
+        eng.load(xs)
+        eng.prepare_gram()
+        torch.cuda.synchronize()
+        eng.raise_status()
+        g = eng.region(_lib.R_GRAM, torch.float64).view(len(xs), eng.ldx, eng.ldx)[:, :T, :T]
+        out.append(g.cpu().numpy())
+        eng.close()
+    return out
+
+
+@pytest.mark.parametrize("case", ["recipe", "ragged_t300", "heavy_tails", "long_v"])
+def test_int8_gram_matches_fp64(srm, case):
+    """The int8-sliced X^T X (7 slices, exact int32 sums) vs fp64 DMMA and numpy."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    rng = np.random.default_rng(7)
+    tol = 1e-13
+    if case == "recipe":
+        xs = recipe_numpy(3, 2000, 256, 10, seed=4)[0]
+    elif case == "ragged_t300":  # T not a multiple of 128 (partial tiles), ragged V
+        xs = [rng.standard_normal((v, 300)) for v in (1000, 777, 1531)]
+    elif case == "heavy_tails":  # Student t (2 dof): column max / rms ~ 10-100
+        xs = [rng.standard_t(2, size=(3000, 200)) for _ in range(2)]
+        tol = 1e-11
+    else:  # > 65536 voxels: the int32 accumulators are flushed per 65536-voxel chunk
+        xs = [rng.standard_normal((70000, 64))]
+    g_dmma, g_i8 = _gram_pair(xs)
+    for i, x in enumerate(xs):
+        xh = x - x.mean(axis=1, keepdims=True)
+        ref = xh.T @ xh
+        assert nrel(g_dmma[i], ref) <= 1e-14, (case, i, "dmma", nrel(g_dmma[i], ref))
+        assert nrel(g_i8[i], ref) <= tol, (case, i, "i8", nrel(g_i8[i], ref))
+        assert np.array_equal(g_i8[i], g_i8[i].T)
+
+
+def test_int8_gram_fit_matches_oracle(srm):
+    """Full fit through the int8-sliced Gram (the default Gram path for fp64) vs the oracle."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(6, 4000, 384, 40, seed=9)
+    ref = orc.run_em(xs, 40, 6, seed=0)
+    for i8 in (True, False):
+        engines = []
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=40, iterations=6, seed=0), algorithm="gram",
+                    gram_int8=i8, engine_out=engines)
+        assert engines[-1].gram and engines[-1].gram_i8 == i8
+        r = ref["iters"][-1]
+        _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, f"gram i8={i8}")
+        ref_ll = np.array([x["ll"] for x in ref["iters"]])
+        assert np.max(np.abs(np.array(m.log_likelihood) - ref_ll) / np.abs(ref_ll)) <= TOL64

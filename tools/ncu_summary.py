@@ -17,7 +17,10 @@ METRICS = [
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %peak"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %peak"),
     ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA pipe %"),
+    ("sm__inst_executed_pipe_tensor_subpipe_imma.avg.pct_of_peak_sustained_active", "IMMA inst %"),
     ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor %"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1/smem %peak"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 %peak"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
     ("launch__registers_per_thread", "regs"),
     ("launch__grid_size", "grid"),
@@ -40,11 +43,9 @@ def summarise(rep):
         name = r[hdr.index("Kernel Name")].split("(")[0].replace("(anonymous namespace)::", "")
         cells = []
         for m, _ in METRICS:
-            if m in hdr:
-                i = hdr.index(m)
-                cells.append(f"{r[i]} {units[i]}".strip())
-            else:
-                cells.append("n/a")
+            # section-prefixed names (e.g. "TPC.TriageCompute.<metric>") count too
+            i = hdr.index(m) if m in hdr else next((j for j, h in enumerate(hdr) if h.endswith("." + m)), None)
+            cells.append(f"{r[i]} {units[i]}".strip() if i is not None else "n/a")
         lines.append(f"| `{name[:70]}` | " + " | ".join(cells) + " |")
     return "\n".join(lines) + "\n"
 
