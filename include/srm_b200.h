@@ -130,7 +130,9 @@ int srm_plan_create(srm_plan** out, int dtype, int n_local, const int64_t* n_vox
 int srm_plan_destroy(srm_plan* plan);
 int64_t srm_plan_workspace_bytes(const srm_plan* plan);
 int64_t srm_plan_dim(const srm_plan* plan, int which);
-/* bind a device workspace of srm_plan_workspace_bytes() bytes (256-B aligned) */
+/* bind a device workspace of srm_plan_workspace_bytes() bytes (256-B aligned).
+ * Every region is zeroed except SRM_R_XHAT and SRM_R_GRAM (and the internal
+ * int8 slices), which srm_load_subject / srm_prepare_gram write in full. */
 int srm_plan_bind(srm_plan* plan, void* workspace, int64_t bytes);
 int srm_plan_region(const srm_plan* plan, int region, int64_t* offset, int64_t* bytes);
 

@@ -694,7 +694,15 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
   if (reinterpret_cast<uintptr_t>(workspace) % 256 != 0) return fail(SRM_ERR_CONFIG, "workspace must be 256-byte aligned");
   p->ws = static_cast<char*>(workspace);
   set_pointers(p);
-  cudaError_t e = cudaMemset(p->ws, 0, p->total_bytes);
+  // zero everything except the bulk regions every fit writes in full before
+  // reading them (X-hat by srm_load_subject, G and the int8 slices by
+  // srm_prepare_gram): tens of GB that need no clearing
+  cudaError_t e = cudaSuccess;
+  for (int r = 0; r < I_COUNT && e == cudaSuccess; ++r) {
+    if (r == SRM_R_XHAT || r == SRM_R_GRAM || r == I_OZQ || p->size[r] == 0) continue;
+    e = cudaMemsetAsync(p->ws + p->off[r], 0, round_up(p->size[r], 256), 0);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
   if (e != cudaSuccess) return cuda_fail(e, "bind memset");
   struct Up {
     int r;

@@ -83,6 +83,20 @@ def to_host(t):
     return out
 
 
+def to_pinned(t):
+    """Device tensor -> numpy view of a pinned host copy (one DMA at PCIe speed).
+
+    The pinned block comes from torch's caching host allocator and returns to
+    it when the last numpy view is released, so repeated fits reuse it.
+    """
+    torch = _torch()
+    t = t.detach().contiguous()
+    host = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    host.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return host.numpy()
+
+
 def to_device(arr, device, out=None):
     """numpy array -> device tensor (``out`` if given), staged through pinned chunks."""
     torch = _torch()

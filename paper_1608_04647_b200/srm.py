@@ -558,9 +558,11 @@ def _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device):
         S = eng.S.clone()
         sigma = eng.sigma.clone()
     else:
-        wout = hostio.to_host(eng.wout)
+        # W lands by DMA in pinned memory from torch's caching host allocator
+        # (reused once an earlier model is released); the arrays are views of it
+        wout = hostio.to_pinned(eng.wout)
         muh = hostio.to_host(eng.mu)
-        W = [np.ascontiguousarray(wout[eng.subject_rows(j)]) for j in range(eng.n_local)]
+        W = [wout[eng.subject_rows(j)] for j in range(eng.n_local)]
         mu = [muh[eng.subject_rows(j)].copy() for j in range(eng.n_local)]
         S = np.ascontiguousarray(eng.S.cpu().numpy())
         sigma = np.ascontiguousarray(eng.sigma.cpu().numpy())
