@@ -43,7 +43,9 @@ enum srm_status {
   SRM_ERR_DEFINITENESS = 4,  /* DefinitenessError(pivot) */
   SRM_ERR_RANK = 5,          /* RankError              */
   SRM_ERR_CUDA = 6,          /* CUDA runtime failure   */
-  SRM_ERR_UNSUPPORTED = 7    /* outside this build's limits (e.g. k > 112) */
+  SRM_ERR_UNSUPPORTED = 7,   /* outside this build's limits (e.g. k > 112) */
+  SRM_ERR_FORMAT = 8,        /* malformed SFAB container (srm_sfab_last_error) */
+  SRM_ERR_IO = 9             /* file system error (srm_sfab_last_error) */
 };
 
 /* plan flags */
@@ -234,6 +236,26 @@ int srm_polar(const double* a, int64_t lda, int64_t v, int64_t k, double* w, int
               int32_t* status4, void* workspace, int64_t ws_bytes, void* stream);
 /* workspace bytes needed by srm_gemm_tn / srm_gemm_nt / srm_polar / srm_tail_step */
 int64_t srm_stateless_workspace_bytes(int64_t v, int64_t k, int64_t t);
+
+/* ---- SFAB subject containers (data_io.py:1-30 layout, :130-196 checks) ------
+ * Host functions (no GPU needed).  Failures return SRM_ERR_FORMAT (the
+ * reference's FormatError: srm_sfab_last_error gives the message, the byte
+ * offset and the field name of the first failed check), SRM_ERR_IO (open /
+ * read / write), SRM_ERR_SHAPE (destination too small) or
+ * SRM_ERR_INVALID_INPUT (non-finite values on write).
+ */
+/* read_header (data_io.py:144-157): validated (rows, cols) without the payload */
+int srm_sfab_header(const char* path, int64_t* rows, int64_t* cols);
+/* load_matrix (data_io.py:160-179): validate and read the row-major f64
+ * payload into dst (>= rows*cols*8 bytes; normally a pinned host slot that an
+ * asynchronous H2D copy drains into srm_load_subject) with `threads` parallel
+ * preads (<= 0: 8) */
+int srm_sfab_read(const char* path, void* dst, int64_t capacity_bytes, int threads);
+/* save_matrix (data_io.py:130-141): header + payload; rejects non-finite entries */
+int srm_sfab_write(const char* path, const double* src, int64_t rows, int64_t cols);
+/* message of the last SFAB failure on this thread; *offset / *field locate the
+ * failed check of a SRM_ERR_FORMAT (-1 / "" otherwise) */
+const char* srm_sfab_last_error(int64_t* offset, const char** field);
 
 #ifdef __cplusplus
 }

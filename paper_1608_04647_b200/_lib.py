@@ -58,6 +58,10 @@ SIGNATURES = [
     ("srm_spd_inverse", c_int, [c_vp, c_i64, c_vp, c_vp]),
     ("srm_polar", c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     ("srm_stateless_workspace_bytes", c_i64, [c_i64, c_i64, c_i64]),
+    ("srm_sfab_header", c_int, [ctypes.c_char_p, c_i64p, c_i64p]),
+    ("srm_sfab_read", c_int, [ctypes.c_char_p, c_vp, c_i64, c_int]),
+    ("srm_sfab_write", c_int, [ctypes.c_char_p, ctypes.POINTER(c_dbl), c_i64, c_i64]),
+    ("srm_sfab_last_error", ctypes.c_char_p, [c_i64p, ctypes.POINTER(ctypes.c_char_p)]),
 ]
 
 # include/srm_b200.h enums
@@ -94,6 +98,16 @@ def load():
         raise DeviceError("libsrm_b200.so ABI version mismatch")
     _LIB = lib
     return lib
+
+
+def check_sfab(code):
+    """Raise the reference's exception for a failed srm_sfab_* call."""
+    if code != 0:
+        off = c_i64()
+        field = ctypes.c_char_p()
+        msg = _LIB.srm_sfab_last_error(ctypes.byref(off), ctypes.byref(field)).decode()
+        fld = field.value.decode() if field.value else None
+        raise from_status(code, msg, offset=off.value if off.value >= 0 else None, field=fld)
 
 
 def check(code, what=""):

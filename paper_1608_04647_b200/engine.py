@@ -181,6 +181,10 @@ class SrmEngine:
         next_g = 0
         for j, x in enumerate(xs):
             v = self.n_voxels[j]
+            pending = None
+            if hasattr(x, "result") and not isinstance(x, (torch.Tensor, np.ndarray)):
+                pending = x
+                x = x.result()  # a pending read (data_io.PendingMatrix): pinned tensor
             if isinstance(x, torch.Tensor) and x.device == self.device and x.dim() == 2 \
                     and x.dtype in (torch.float64, torch.float32) and x.stride(1) == 1:
                 src = x
@@ -210,6 +214,8 @@ class SrmEngine:
                 ev = torch.cuda.Event()
                 ev.record(copier)
                 main.wait_event(ev)
+                if pending is not None:
+                    pending.release(ev)  # its pinned slot is free once this copy completes
                 src = buf
                 ld = self.T
             if tuple(src.shape) != (v, self.T):

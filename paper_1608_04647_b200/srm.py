@@ -333,6 +333,8 @@ def _storage_for(subjects, storage):
         x = s.X
         if isinstance(x, tensor_t):
             f32.append(str(x.dtype) == "torch.float32")
+        elif hasattr(x, "dtype"):  # numpy arrays and pending SFAB reads (data_io.PendingMatrix)
+            f32.append(np.dtype(x.dtype) == np.float32)
         else:
             f32.append(np.asarray(x).dtype == np.float32)
     return "f32" if all(f32) else "f64"

@@ -290,3 +290,27 @@ def test_int8_gram_fit_matches_oracle(srm):
         _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, f"gram i8={i8}")
         ref_ll = np.array([x["ll"] for x in ref["iters"]])
         assert np.max(np.abs(np.array(m.log_likelihood) - ref_ll) / np.abs(ref_ll)) <= TOL64
+
+
+def test_fit_manifest_streams_sfab(srm, tmp_path):
+    """SFAB files -> pinned slots -> device (data_io.fit_manifest) == srm.fit on the same arrays."""
+    from paper_1608_04647_b200 import data_io
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(5, 900, 64, 6, seed=13)
+    xs = [x[: 900 - 41 * i] for i, x in enumerate(xs)]  # ragged V; 5 subjects > 3 read-ahead slots
+    entries = []
+    for i, x in enumerate(xs):
+        p = tmp_path / f"s{i}.sfab"
+        data_io.save_matrix(p, x)
+        entries.append(data_io.ManifestEntry(f"s{i}", p))
+    man = tmp_path / "m.json"
+    data_io.write_manifest(man, data_io.Manifest("t", entries))
+    cfg = srm.SrmConfig(k=6, iterations=4, seed=3)
+    a = data_io.fit_manifest(man, cfg)
+    b = srm.fit([srm.SubjectData(f"s{i}", x) for i, x in enumerate(xs)], cfg)
+    assert a.subject_ids == b.subject_ids
+    assert np.array_equal(a.S, b.S) and np.array_equal(a.sigma_s, b.sigma_s)
+    for wa, wb in zip(a.W, b.W):
+        assert np.array_equal(wa, wb)
+    assert a.rho2 == b.rho2
