@@ -68,6 +68,12 @@ enum Internal {
   I_OZCMAX,
   I_OZEXP,
   I_ITEMS_OZ,
+  I_GFBPART,
+  I_GFBCOUNT,
+  I_OZG,
+  I_OZGEXP,
+  I_OZS,
+  I_OZSEXP,
   I_COUNT
 };
 
@@ -110,6 +116,9 @@ struct srm_plan {
   std::vector<OzItem> items_oz;       // int8-sliced Gram tiles (SRM_FLAG_GRAM_I8)
   int64_t oz_lq = 0, max_v = 0;       // bytes per sliced TR row; largest local V
   TmaMap tm_q;
+  bool oz_sg = false;                 // per-iteration B = S G / 2 from int8 row slices (kp <= 64)
+  int64_t oz_lqg = 0;                 // bytes per sliced row of G_i / S
+  TmaMap tm_g, tm_sq;
 };
 
 namespace {
@@ -170,6 +179,13 @@ void layout(srm_plan* p) {
   sz[I_OZCMAX] = i8 ? (int64_t)p->n_local * p->ldx * 8 : 0;
   sz[I_OZEXP] = i8 ? (int64_t)p->n_local * p->ldx * 4 : 0;
   sz[I_ITEMS_OZ] = (int64_t)p->items_oz.size() * sizeof(OzItem);
+  const int gfb_chunks = (int)((p->ldx + kGfbCols - 1) / kGfbCols);
+  sz[I_GFBPART] = (int64_t)p->n_local * gfb_chunks * kp2 * 8;
+  sz[I_GFBCOUNT] = (int64_t)p->n_local * 4;
+  sz[I_OZG] = p->oz_sg ? (int64_t)p->n_local * p->ldx * p->oz_lqg : 0;
+  sz[I_OZGEXP] = p->oz_sg ? (int64_t)p->n_local * p->ldx * 4 : 0;
+  sz[I_OZS] = p->oz_sg ? p->kp * p->oz_lqg : 0;
+  sz[I_OZSEXP] = p->oz_sg ? p->kp * 4 : 0;
   int64_t cur = 0;
   for (int r = 0; r < I_COUNT; ++r) {
     p->off[r] = cur;
@@ -189,6 +205,7 @@ void layout(srm_plan* p) {
   d.ldo = p->ldo;
   d.ntile_apply = ntile_apply;
   d.ntile_tail = ntile_tail;
+  d.gfb_chunks = gfb_chunks;
   d.term_stride = term_stride;
   d.red_stride = red_stride;
   d.hist_stride = hist_stride;
@@ -299,6 +316,8 @@ void build_work(srm_plan* p) {
   p->max_v = 0;
   for (int i = 0; i < p->n_local; ++i) p->max_v = std::max(p->max_v, p->V[i]);
   p->oz_lq = round_up(std::max<int64_t>(p->max_v, 1), 32) / 32 * kOzRecord;
+  p->oz_sg = (p->flags & SRM_FLAG_GRAM_I8) && p->kp <= 64;
+  p->oz_lqg = p->ldx / 32 * kOzRecord;
   if (p->flags & SRM_FLAG_GRAM_I8) {
     for (int i = 0; i < p->n_local; ++i)
       for (int64_t m0 = 0; m0 < p->ldx; m0 += 128)
@@ -397,6 +416,8 @@ void set_pointers(srm_plan* p) {
   d.tailpart = region<double>(p, I_TAILPART);
   d.part = region<double>(p, I_PART);
   d.bred = region<double>(p, I_BRED);
+  d.gfb_part = region<double>(p, I_GFBPART);
+  d.gfb_count = region<int32_t>(p, I_GFBCOUNT);
   d.mmat = region<double>(p, SRM_R_MMAT);
   d.qmat = region<double>(p, I_QMAT);
   d.qscr = region<double>(p, I_QSCR);
@@ -455,14 +476,23 @@ std::vector<Stage> m_stages(srm_plan* p) {
   std::vector<Stage> v;
   if (p->flags & SRM_FLAG_GRAM) {
     // B_i = S G_i / 2 straight into the reduced slot (G_i = X_i^T X_i, one-time)
-    v.push_back({"gram_b", [p, d](cudaStream_t st) {
-                   return launch_contract_e((int)p->kp, SRM_F64, SRM_F64, d.st, p->kp, d.gram, p->ldx, d.bred, p->ldo,
-                                            0.5, region<ItemE>(p, I_ITEMS_BG), (int)p->items_bg.size(), st);
-                 }});
-    v.push_back({"gram_from_b", [p, d](cudaStream_t st) {
-                   return launch_contract_a((int)p->kp, SRM_F64, d.bred, p->ldo, d.S, p->ldx, p->ldx, d.bred, p->ldo,
-                                            0.5, region<ItemA>(p, I_ITEMS_G), (int)p->items_g.size(), st);
-                 }});
+    if (p->oz_sg) {
+      // B_i = S G_i / 2 on the int8 tensor cores: slice S (rows), then one pass
+      v.push_back({"oz_slice_s", [p, d](cudaStream_t st) {
+                     return launch_oz_slice_rows(d.S, p->ldx, p->kp, p->ldx, region<int8_t>(p, I_OZS), p->oz_lqg,
+                                                 region<int32_t>(p, I_OZSEXP), st);
+                   }});
+      v.push_back({"oz_sg", [p, d](cudaStream_t st) {
+                     return launch_oz_sg(p->tm_g, p->tm_sq, region<int32_t>(p, I_OZGEXP),
+                                         region<int32_t>(p, I_OZSEXP), d.bred, p->ldx, p->kp, p->ldo, p->n_local, st);
+                   }});
+    } else {
+      v.push_back({"gram_b", [p, d](cudaStream_t st) {
+                     return launch_contract_e((int)p->kp, SRM_F64, SRM_F64, d.st, p->kp, d.gram, p->ldx, d.bred,
+                                              p->ldo, 0.5, region<ItemE>(p, I_ITEMS_BG), (int)p->items_bg.size(), st);
+                   }});
+    }
+    v.push_back({"gram_from_b", [d](cudaStream_t st) { return launch_gram_from_b(d, st); }});
     v.push_back({"eig_polar", [d](cudaStream_t st) { return launch_eig_polar(d, 0, st); }});
     v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 1, st); }});
     v.push_back({"finalize_rho", [d](cudaStream_t st) { return launch_finalize_rho(d, 0, st); }});
@@ -490,10 +520,7 @@ std::vector<Stage> m_stages(srm_plan* p) {
                }});
   }
   v.push_back({"reduce_chunks", [d](cudaStream_t st) { return launch_reduce_chunks(d, st); }});
-  v.push_back({"gram_from_b", [p, d](cudaStream_t st) {
-                 return launch_contract_a((int)p->kp, SRM_F64, d.bred, p->ldo, d.S, p->ldx, p->ldx, d.bred, p->ldo,
-                                          0.5, region<ItemA>(p, I_ITEMS_G), (int)p->items_g.size(), st);
-               }});
+  v.push_back({"gram_from_b", [d](cudaStream_t st) { return launch_gram_from_b(d, st); }});
   v.push_back({"eig_polar", [d](cudaStream_t st) { return launch_eig_polar(d, 0, st); }});
   v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 1, st); }});
   v.push_back({"finalize_rho", [d](cudaStream_t st) { return launch_finalize_rho(d, 0, st); }});
@@ -542,6 +569,15 @@ std::vector<Stage> gram_stages(srm_plan* p, int first, int count) {
                  }});
   }
   v.push_back({"mirror_gram", [d, first, count](cudaStream_t st) { return launch_mirror_gram(d, first, count, st); }});
+  if (p->oz_sg) {
+    // row slices of G_i for the per-iteration int8 B = S G / 2
+    v.push_back({"oz_slice_g", [p, d, first, count](cudaStream_t st) {
+                   return launch_oz_slice_rows(d.gram + (int64_t)first * p->ldx * p->ldx, p->ldx,
+                                               (int64_t)count * p->ldx, p->ldx,
+                                               region<int8_t>(p, I_OZG) + (int64_t)first * p->ldx * p->oz_lqg,
+                                               p->oz_lqg, region<int32_t>(p, I_OZGEXP) + (int64_t)first * p->ldx, st);
+                 }});
+  }
   return v;
 }
 
@@ -748,8 +784,14 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
   if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM))
     e = launch_gram_tiles(p->dtype, d.xhat, p->ldx, d.gram, p->ldx, nullptr, 0, 0);
   if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM_I8)) {
-    e = make_map_q(&p->tm_q, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local);
+    e = make_map_q(&p->tm_q, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, 128);
     if (e == cudaSuccess) e = launch_oz_gram(p->tm_q, nullptr, nullptr, p->ldx, nullptr, 0, 0);
+    if (e == cudaSuccess && p->oz_sg) {
+      e = make_map_q(&p->tm_g, region<int8_t>(p, I_OZG), p->oz_lqg, p->ldx, p->n_local, 128);
+      if (e == cudaSuccess) e = make_map_q(&p->tm_sq, region<int8_t>(p, I_OZS), p->oz_lqg, p->kp, 1, 64);
+      if (e == cudaSuccess)
+        e = launch_oz_sg(p->tm_g, p->tm_sq, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, 0, 0);
+    }
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
   return SRM_OK;

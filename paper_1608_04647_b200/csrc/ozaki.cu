@@ -307,9 +307,185 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
   if (warp == 1) tmem_free(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// row slicing: one warp per row of a row-major fp64 matrix M (rows x ldm,
+// columns [0, ncols), ncols % 32 == 0); the row's power-of-two scale 2^e >=
+// max |M[r][:]| goes to expo[r] and its slices to the 256-byte records
+// q[r][b] (b = 32-column block), the same record layout as oz_split.
+// Matrices: the fp64 Gram G_i (rows = TRs, once) and S (rows = features,
+// every iteration) of the int8 B = S G / 2.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_oz_slice_rows(const double* __restrict__ M, int64_t ldm, int64_t rows,
+                                                       int64_t ncols, int8_t* __restrict__ q, int64_t lq,
+                                                       int32_t* __restrict__ expo) {
+  __shared__ __align__(16) uint8_t rec[8][kOzRecord];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * 8 + warp;
+  if (r >= rows) return;
+  const double* row = M + r * ldm;
+  double m = 0.0;
+  for (int64_t c = lane; c < ncols; c += 32) m = fmax(m, fabs(row[c]));
+  m = warp_max(m);
+  const int e = (m > 0.0) ? frexp_exp(m) : 0;
+  if (lane == 0) expo[r] = e;
+  const double scale = __longlong_as_double((long long)(1023 + 6 - e) << 52);
+  uint8_t* rb = rec[warp];
+  for (int64_t b = 0; b * 32 < ncols; ++b) {
+    double y = row[b * 32 + lane] * scale;  // |y| < 64
+#pragma unroll
+    for (int s = 0; s < kOzSlices; ++s) {
+      int low;
+      const double rr = round_shift(y, &low);
+      rb[s * 32 + lane] = (uint8_t)(low & 0xFF);
+      y = (y - rr) * 128.0;
+    }
+    rb[7 * 32 + lane] = 0;
+    __syncwarp();
+    if (lane < 16)
+      reinterpret_cast<uint4*>(q + r * lq + b * kOzRecord)[lane] = reinterpret_cast<const uint4*>(rb)[lane];
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// B_i = S G_i / 2 from the slices: CTA = (128 TRs t of subject i) x all 64
+// features f, contraction over the TRs u of G_i's rows in 32-wide blocks:
+//   B^T[t][f] = 1/2 sum_u G[t][u] S[f][u]
+//             = 1/2 2^{e_t + s_f} sum_d 2^{-12-7d} sum_{s+s'=d} (Qg_s Qs_{s'}^T)[t][f]
+// tcgen05.mma kind::i8 M = 128 (t), N = 64 (f), K = 32; all seven d-groups
+// accumulate in TMEM at once (7 x 64 columns), one pass; the epilogue writes
+// B[f][t] (coalesced over t) into the reduced record bred[i].
+// ---------------------------------------------------------------------------
+constexpr int kSgStages = 4;  // one CTA per SM: the seven accumulators take all 512 TMEM columns
+constexpr int kSgBoxS = 8192;                     // 64 rows x 128 B
+constexpr int kSgStageBytes = 2 * kOzBox + 2 * kSgBoxS;
+
+__global__ void __launch_bounds__(kOzThreads, 1) k_oz_sg(const __grid_constant__ CUtensorMap tmg,
+                                                         const __grid_constant__ CUtensorMap tms,
+                                                         const int32_t* __restrict__ gexp,
+                                                         const int32_t* __restrict__ sexp, double* __restrict__ bred,
+                                                         int64_t ldx, int64_t kp, int64_t ldo) {
+  extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[kSgStages], empty[kSgStages], accfull;
+  __shared__ uint32_t tmem_base;
+  const int t0 = blockIdx.x * 128, i = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nub = (int)(ldx / 32);
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < kSgStages; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      mbar_init(&accfull, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+  } else if (warp == 1) {
+    tmem_alloc(&tmem_base, 512);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int k = 0; k < nub; ++k) {
+        const int slot = k % kSgStages;
+        if (k >= kSgStages) mbar_wait(&empty[slot], ((k / kSgStages) - 1) & 1);
+        mbar_expect_tx(&full[slot], (uint32_t)kSgStageBytes);
+        unsigned char* st = smem + slot * kSgStageBytes;
+        const int x = k * 256;
+        tma_load_3d(st, &tmg, x, t0, i, &full[slot]);
+        tma_load_3d(st + kOzBox, &tmg, x + 128, t0, i, &full[slot]);
+        tma_load_3d(st + 2 * kOzBox, &tms, x, 0, 0, &full[slot]);
+        tma_load_3d(st + 2 * kOzBox + kSgBoxS, &tms, x + 128, 0, 0, &full[slot]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_s8(128, 64);
+      for (int k = 0; k < nub; ++k) {
+        const int slot = k % kSgStages;
+        mbar_wait(&full[slot], (k / kSgStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t sa = smem_u32(smem + slot * kSgStageBytes);
+        const uint32_t sb = sa + 2 * kOzBox;
+        for (int d = 0; d < kOzSlices; ++d) {
+          const uint32_t acc = tmem + 64u * (uint32_t)d;
+          for (int s = 0; s <= d; ++s) {
+            const int s2 = d - s;
+            const uint64_t da = umma_desc_sw128(sa + (s >> 2) * kOzBox + 32 * (s & 3));
+            const uint64_t db = umma_desc_sw128(sb + (s2 >> 2) * kSgBoxS + 32 * (s2 & 3));
+            mma_s8(acc, da, db, idesc, (k == 0 && s == 0) ? 0 : 1);
+          }
+        }
+        mma_commit(&empty[slot]);
+      }
+      mma_commit(&accfull);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int64_t t = t0 + r;
+    mbar_wait(&accfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int et = t < ldx ? gexp[(int64_t)i * ldx + t] : 0;
+    double* out = bred + (int64_t)i * kp * ldo + t;
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      double val[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) val[j] = 0.0;
+      for (int d = 0; d < kOzSlices; ++d) {
+        uint32_t raw[16];
+        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 64u * (uint32_t)d + c0, raw);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) val[j] += ldexp((double)(int32_t)raw[j], -12 - 7 * d);
+      }
+      if (t < ldx) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int f = c0 + j;
+          if (f < kp) out[(int64_t)f * ldo] = ldexp(val[j], et + sexp[f] - 1);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) tmem_free(tmem, 512);
+}
+
 }  // namespace
 
 size_t oz_gram_smem_bytes() { return (size_t)kOzStages * kOzStageBytes + 1024; }
+
+cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int64_t ncols, int8_t* q, int64_t lq,
+                                 int32_t* expo, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  if (ncols % 32 != 0) return cudaErrorInvalidValue;
+  k_oz_slice_rows<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(M, ldm, rows, ncols, q, lq, expo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_oz_sg(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
+                         double* bred, int64_t ldx, int64_t kp, int64_t ldo, int n_local, cudaStream_t st) {
+  const size_t bytes = (size_t)kSgStages * kSgStageBytes + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_oz_sg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (n_local == 0) return cudaSuccess;
+  if (kp > 64 || ldx % 32 != 0) return cudaErrorInvalidValue;
+  const dim3 grid((unsigned)((ldx + 127) / 128), (unsigned)n_local);
+  k_oz_sg<<<grid, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(tmg.opaque),
+                                           *reinterpret_cast<const CUtensorMap*>(tms.opaque), gexp, sexp, bred, ldx, kp,
+                                           ldo);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_oz_prepare(const DevPlan& p, int first, int count, unsigned long long* cmax, int8_t* q,
                               int64_t lq, int32_t* expo, int64_t max_v, cudaStream_t st) {

@@ -29,6 +29,8 @@ enum TailCol { TS_LOGDET_SIGMA = 0, TS_LOGDET_PREC = 1, TS_TRACE = 2, kTailScala
 
 // column tile width of apply_m (W^T Xhat = M^T B)
 constexpr int kApplyCols = 128;
+// TR chunk of gram_from_b (A^T A = B S^T / 2)
+constexpr int kGfbCols = 128;
 
 struct DevPlan {
   int n_local, n_total, n_order;
@@ -55,6 +57,9 @@ struct DevPlan {
   double* tailpart;  // [ntile_tail][4]
   double* part;      // [chunks][kp][ldo]
   double* bred;      // [n_local][kp][ldo]
+  double* gfb_part;  // [n_local][gfb_chunks][kp][kp] partial A^T A = B S^T / 2 per TR chunk
+  int32_t* gfb_count;  // [n_local] CTAs done per subject (reset by the last one)
+  int gfb_chunks;      // kGfbCols-column chunks of ldx
   double* mmat;      // [n_local][kp][kp]
   double* qmat;      // [n_local][kp][kp]
   double* qscr;      // [n_local][kp][kp]
@@ -79,6 +84,9 @@ cudaError_t launch_subject_sqnorm(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_reduce_chunks(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_eig_polar(const DevPlan& p, int init, cudaStream_t s);
 cudaError_t launch_apply_m(const DevPlan& p, int with_cross, cudaStream_t s);
+// A_i^T A_i = B_i S^T / 2 into the K x K block of every subject's reduced
+// record (bred[i][:, ldx:ldx+kp]), split over TR chunks
+cudaError_t launch_gram_from_b(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_finalize_rho(const DevPlan& p, int init, cudaStream_t s);
 cudaError_t launch_set_iteration(const DevPlan& p, int iteration, int advance, cudaStream_t s);
 cudaError_t launch_reduce_terms(const DevPlan& p, double* dst, const int32_t* order, int count,

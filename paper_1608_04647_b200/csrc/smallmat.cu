@@ -381,6 +381,106 @@ __global__ void __launch_bounds__(kSmallThreads) k_apply_m(DevPlan p, int with_c
   }
 }
 
+// A_i^T A_i = B_i S^T / 2 (SURVEY identity 3): CTA (chunk c, subject i) forms
+// the K x K partial over TRs [64 c, 64 c + 64) with a 16 x 16 thread grid (R x R
+// register block per thread); the last CTA of a subject (atomic ticket, reset
+// after use) sums the partials in chunk order -- deterministic -- into
+// bred[i][a][ldx + b] (b < kp; zero for a or b >= K).
+constexpr int kGfbLd = kGfbCols + 1;  // odd row pitch: conflict-free column reads
+
+template <int R>
+__device__ __forceinline__ void gfb_body(const DevPlan& p, double* Bs, double* Ss) {
+  const int c = blockIdx.x, i = blockIdx.y;
+  const int K = (int)p.K, kp = (int)p.kp;
+  const int64_t t0 = (int64_t)c * kGfbCols;
+  const double* Bg = p.bred + (int64_t)i * p.kp * p.ldo;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int e = tid; e < K * kGfbCols; e += blockDim.x) {
+    const int r = e / kGfbCols, t = e % kGfbCols;
+    const bool in = t0 + t < p.ldx;
+    Bs[r * kGfbLd + t] = in ? Bg[(int64_t)r * p.ldo + t0 + t] : 0.0;
+    Ss[r * kGfbLd + t] = in ? p.S[(int64_t)r * p.ldx + t0 + t] : 0.0;
+  }
+  __syncthreads();
+  double acc[R][R];
+#pragma unroll
+  for (int a = 0; a < R; ++a)
+#pragma unroll
+    for (int b = 0; b < R; ++b) acc[a][b] = 0.0;
+  for (int t = 0; t < kGfbCols; ++t) {
+    double bv[R], sv[R];
+#pragma unroll
+    for (int a = 0; a < R; ++a) {
+      const int r = ty + 16 * a;
+      bv[a] = r < K ? Bs[r * kGfbLd + t] : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      const int r = tx + 16 * b;
+      sv[b] = r < K ? Ss[r * kGfbLd + t] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[a][b] = fma(bv[a], sv[b], acc[a][b]);
+  }
+  double* part = p.gfb_part + ((int64_t)i * p.gfb_chunks + c) * kp * kp;
+#pragma unroll
+  for (int a = 0; a < R; ++a)
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      const int ra = ty + 16 * a, rb = tx + 16 * b;
+      if (ra < kp && rb < kp) part[ra * kp + rb] = acc[a][b];
+    }
+  // last CTA of subject i reduces
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(p.gfb_count + i, 1) == p.gfb_chunks - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // 16 elements per thread per batch: each chunk step issues 16 independent
+  // L2 loads (summation order over chunks unchanged)
+  const double* all = p.gfb_part + (int64_t)i * p.gfb_chunks * kp * kp;
+  double* out = p.bred + (int64_t)i * p.kp * p.ldo + p.ldx;
+  const int n = kp * kp;
+  for (int e0 = 0; e0 < n; e0 += 16 * (int)blockDim.x) {
+    double s[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) s[u] = 0.0;
+    for (int q = 0; q < p.gfb_chunks; ++q) {
+      const double* src = all + (int64_t)q * n;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = e0 + tid + u * (int)blockDim.x;
+        if (e < n) s[u] += __ldcg(src + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = e0 + tid + u * (int)blockDim.x;
+      if (e < n) out[(int64_t)(e / kp) * p.ldo + e % kp] = 0.5 * s[u];
+    }
+  }
+  if (tid == 0) p.gfb_count[i] = 0;
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_gram_from_b(DevPlan p) {
+  extern __shared__ __align__(16) double sm[];
+  double* Bs = sm;
+  double* Ss = sm + p.K * kGfbLd;
+  switch ((p.K + 15) / 16) {
+    case 1: gfb_body<1>(p, Bs, Ss); break;
+    case 2: gfb_body<2>(p, Bs, Ss); break;
+    case 3: gfb_body<3>(p, Bs, Ss); break;
+    case 4: gfb_body<4>(p, Bs, Ss); break;
+    case 5: gfb_body<5>(p, Bs, Ss); break;
+    case 6: gfb_body<6>(p, Bs, Ss); break;
+    default: gfb_body<7>(p, Bs, Ss); break;
+  }
+}
+
 __device__ __forceinline__ int64_t hist_row(const DevPlan& p, int it) { return (int64_t)(it % p.n_hist) * p.hist_stride; }
 
 __global__ void k_set_iteration(DevPlan p, int iteration, int advance) {
@@ -1043,6 +1143,14 @@ cudaError_t launch_apply_m(const DevPlan& p, int with_cross, cudaStream_t s) {
   void* args[] = {&arg, &with_cross};
   e = cudaLaunchKernel(fn, grid, dim3(kSmallThreads), args, bytes, s);
   if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_from_b(const DevPlan& p, cudaStream_t s) {
+  const size_t bytes = (size_t)2 * p.K * kGfbLd * sizeof(double);
+  cudaError_t e = set_smem((const void*)k_gram_from_b, bytes);
+  if (e != cudaSuccess) return e;
+  k_gram_from_b<<<dim3((unsigned)p.gfb_chunks, (unsigned)p.n_local), kSmallThreads, bytes, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -513,13 +513,13 @@ cudaError_t make_map_f32(TmaMap* m, const float* base, int64_t inner, int64_t ou
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-// 3-D int8 map over the Gram-path slices Q[n][ldx][lq] (bytes), box {128, 128, 1}, SWIZZLE_128B
-cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, int64_t n) {
+// 3-D int8 map over int8 slice records Q[n][rows][lq] (bytes), box {128, box_rows, 1}, SWIZZLE_128B
+cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n, int box_rows) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
-  cuuint64_t dims[3] = {(cuuint64_t)lq, (cuuint64_t)ldx, (cuuint64_t)n};
-  cuuint64_t strides[2] = {(cuuint64_t)lq, (cuuint64_t)(lq * ldx)};
-  cuuint32_t box[3] = {128, 128, 1};
+  cuuint64_t dims[3] = {(cuuint64_t)lq, (cuuint64_t)rows, (cuuint64_t)n};
+  cuuint64_t strides[2] = {(cuuint64_t)lq, (cuuint64_t)(lq * rows)};
+  cuuint32_t box[3] = {128, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(reinterpret_cast<CUtensorMap*>(m->opaque), CU_TENSOR_MAP_DATA_TYPE_UINT8, 3,
                   const_cast<int8_t*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
