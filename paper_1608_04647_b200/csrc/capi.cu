@@ -74,6 +74,9 @@ enum Internal {
   I_OZGEXP,
   I_OZS,
   I_OZSEXP,
+  I_OZR,
+  I_OZREXP,
+  I_ITEMS_OW,
   I_COUNT
 };
 
@@ -117,8 +120,11 @@ struct srm_plan {
   int64_t oz_lq = 0, max_v = 0;       // bytes per sliced TR row; largest local V
   TmaMap tm_q;
   bool oz_sg = false;                 // per-iteration B = S G / 2 from int8 row slices (kp <= 64)
-  int64_t oz_lqg = 0;                 // bytes per sliced row of G_i / S
+  int64_t oz_lqg = 0;                 // bytes per sliced row of G_i / S / R'^T / Qt
   TmaMap tm_g, tm_sq;
+  bool oz_w = false;                  // final W = Xhat R from the int8 slices (needs oz_sg)
+  std::vector<OzItem> items_ow;       // 128-voxel tiles of the final int8 W = Xhat R
+  TmaMap tm_q32, tm_r;
 };
 
 namespace {
@@ -186,6 +192,9 @@ void layout(srm_plan* p) {
   sz[I_OZGEXP] = p->oz_sg ? (int64_t)p->n_local * p->ldx * 4 : 0;
   sz[I_OZS] = p->oz_sg ? p->kp * p->oz_lqg : 0;
   sz[I_OZSEXP] = p->oz_sg ? p->kp * 4 : 0;
+  sz[I_OZR] = p->oz_w ? (int64_t)p->n_local * p->kp * p->oz_lqg : 0;
+  sz[I_OZREXP] = p->oz_w ? (int64_t)p->n_local * p->kp * 4 : 0;
+  sz[I_ITEMS_OW] = (int64_t)p->items_ow.size() * sizeof(OzItem);
   int64_t cur = 0;
   for (int r = 0; r < I_COUNT; ++r) {
     p->off[r] = cur;
@@ -318,6 +327,14 @@ void build_work(srm_plan* p) {
   p->oz_lq = round_up(std::max<int64_t>(p->max_v, 1), 32) / 32 * kOzRecord;
   p->oz_sg = (p->flags & SRM_FLAG_GRAM_I8) && p->kp <= 64;
   p->oz_lqg = p->ldx / 32 * kOzRecord;
+  p->oz_w = p->oz_sg;
+  p->items_ow.clear();
+  if (p->oz_w) {
+    for (int i = 0; i < p->n_local; ++i)
+      for (int64_t v0 = 0; v0 < p->V[i]; v0 += 128)
+        p->items_ow.push_back({i, (int32_t)v0, (int32_t)(p->row_off[i] + v0),
+                               (int32_t)std::min<int64_t>(128, p->V[i] - v0)});
+  }
   if (p->flags & SRM_FLAG_GRAM_I8) {
     for (int i = 0; i < p->n_local; ++i)
       for (int64_t m0 = 0; m0 < p->ldx; m0 += 128)
@@ -749,7 +766,7 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
              {I_ITEMS_G, p->items_g.data()},     {I_ITEMS_GRAM, p->items_gram.data()},
              {I_ITEMS_BG, p->items_bg.data()},   {I_ITEMS_TB, p->items_tb.data()},
              {I_ITEMS_TA, p->items_ta.data()},   {I_ITEMS_TG, p->items_tg.data()},
-             {I_ITEMS_OZ, p->items_oz.data()}};
+             {I_ITEMS_OZ, p->items_oz.data()},   {I_ITEMS_OW, p->items_ow.data()}};
   for (const Up& u : ups) {
     if (p->size[u.r] == 0) continue;
     e = cudaMemcpy(p->ws + p->off[u.r], u.src, p->size[u.r], cudaMemcpyHostToDevice);
@@ -791,6 +808,11 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
       if (e == cudaSuccess) e = make_map_q(&p->tm_sq, region<int8_t>(p, I_OZS), p->oz_lqg, p->kp, 1, 64);
       if (e == cudaSuccess)
         e = launch_oz_sg(p->tm_g, p->tm_sq, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, 0, 0);
+    }
+    if (e == cudaSuccess && p->oz_w) {
+      e = make_map_q5(&p->tm_q32, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local);
+      if (e == cudaSuccess) e = make_map_q(&p->tm_r, region<int8_t>(p, I_OZR), p->oz_lqg, p->kp, p->n_local, 64);
+      if (e == cudaSuccess) e = launch_oz_w(p->tm_q32, p->tm_r, nullptr, nullptr, nullptr, 0, p->ldx, p->kp, p->K, 0);
     }
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
@@ -893,6 +915,19 @@ int srm_finalize(srm_plan* p, void* stream) {
   if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
   cudaStream_t st = as_stream(stream);
   const DevPlan& d = p->dp;
+  if (p->oz_w) {
+    // W_i = Xhat_i R_i, R_i = S^T M_i / 2, from the int8 slices of Xhat on the
+    // tensor cores (no A pass, no W = A M pass)
+    cudaError_t e = launch_oz_rt(d.mmat, d.S, region<int32_t>(p, I_OZEXP), d.part, p->ldx, p->kp, p->K,
+                                 p->n_local, st);
+    if (e == cudaSuccess)
+      e = launch_oz_slice_rows(d.part, p->ldx, (int64_t)p->n_local * p->kp, p->ldx, region<int8_t>(p, I_OZR),
+                               p->oz_lqg, region<int32_t>(p, I_OZREXP), st);
+    if (e == cudaSuccess)
+      e = launch_oz_w(p->tm_q32, p->tm_r, region<int32_t>(p, I_OZREXP), d.wout, region<OzItem>(p, I_ITEMS_OW),
+                      (int)p->items_ow.size(), p->ldx, p->kp, p->K, st);
+    return check(e, "finalize");
+  }
   if (p->flags & SRM_FLAG_GRAM) {  // A_i = Xhat_i S^T / 2 is not kept per iteration on the Gram path
     cudaError_t e = launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
                                       0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);

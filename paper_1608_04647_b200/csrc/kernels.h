@@ -73,12 +73,19 @@ struct OzItem {
 constexpr int kOzChunkBlocks = 2048;  // 65536 voxels per exact int32 accumulation
 constexpr int64_t kOzRecord = 256;    // bytes per (TR, 32-voxel block): 8 slots x 32 voxels
 cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n, int box_rows);
+cudaError_t make_map_q5(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, int64_t n);
 // int8 slices of the rows of a row-major fp64 matrix (ozaki.cu): 2^e[r] >= max|M[r][:]|
 cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int64_t ncols, int8_t* q, int64_t lq,
                                  int32_t* expo, cudaStream_t st);
 // B_i = S G_i / 2 into bred[i][f][t] from the row slices of G_i and S (kp <= 64)
 cudaError_t launch_oz_sg(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
                          double* bred, int64_t ldx, int64_t kp, int64_t ldo, int n_local, cudaStream_t st);
+// R'^T[i] = 2^{e_t} (M_i^T S) / 2 (kp x ldx per subject) for the final int8 W = Xhat R
+cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* expo, double* rt, int64_t ldx,
+                         int64_t kp, int64_t K, int n_local, cudaStream_t st);
+// W rows = Qt (voxel-major X-hat slices) x the row slices of R'^T (kp <= 64)
+cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* rexp, double* W, const OzItem* items,
+                        int n_items, int64_t ldx, int64_t kp, int64_t K, cudaStream_t st);
 size_t oz_gram_smem_bytes();
 cudaError_t launch_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
                            int n_items, cudaStream_t st);

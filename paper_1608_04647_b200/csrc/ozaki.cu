@@ -355,21 +355,43 @@ __global__ void __launch_bounds__(256) k_oz_slice_rows(const double* __restrict_
 // tcgen05.mma kind::i8 M = 128 (t), N = 64 (f), K = 32; all seven d-groups
 // accumulate in TMEM at once (7 x 64 columns), one pass; the epilogue writes
 // B[f][t] (coalesced over t) into the reduced record bred[i].
+//
+// The same kernel (kRowW) forms the model's W_i = Xhat_i R_i at the end of a
+// Gram-path fit, with R_i = S^T M_i / 2 (srm.py:147 + kernels.py:212 via
+// W = A M): A = the voxel-major slices Qt of Xhat (rows = voxels, K = TRs),
+// B = the row slices of R'^T = (2^{e_t} R_i)^T (the column scales of Xhat
+// folded into R), so W[v][f] = 2^{r_f} sum_d 2^{-12-7d} (...)[v][f].
 // ---------------------------------------------------------------------------
 constexpr int kSgStages = 4;  // one CTA per SM: the seven accumulators take all 512 TMEM columns
 constexpr int kSgBoxS = 8192;                     // 64 rows x 128 B
 constexpr int kSgStageBytes = 2 * kOzBox + 2 * kSgBoxS;
+constexpr int kRowWABytes = 7 * 4 * 32 * 32;  // kRowW A operand per stage: 7 slots x 4 voxel blocks x 32 TRs x 32 B
+enum RowGemmMode { kRowSG = 0, kRowW = 1 };
 
-__global__ void __launch_bounds__(kOzThreads, 1) k_oz_sg(const __grid_constant__ CUtensorMap tmg,
-                                                         const __grid_constant__ CUtensorMap tms,
-                                                         const int32_t* __restrict__ gexp,
-                                                         const int32_t* __restrict__ sexp, double* __restrict__ bred,
-                                                         int64_t ldx, int64_t kp, int64_t ldo) {
+struct RowGemmArgs {
+  const int32_t* aexp;   // kRowSG: G row exponents [n_local][ldx]
+  const int32_t* bexp;   // kRowSG: S row exponents [kp]; kRowW: R'^T row exponents [n_local][kp]
+  double* out;           // kRowSG: bred; kRowW: W [rows_total][K]
+  const OzItem* items;   // kRowW: {subject, local voxel v0, global row of v0, valid rows}
+  int64_t ldx, kp, ldo, K;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_constant__ CUtensorMap tma,
+                                                              const __grid_constant__ CUtensorMap tmb,
+                                                              RowGemmArgs g) {
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kSgStages], empty[kSgStages], accfull;
   __shared__ uint32_t tmem_base;
-  const int t0 = blockIdx.x * 128, i = blockIdx.y;
+  const int64_t ldx = g.ldx, kp = g.kp, ldo = g.ldo;
+  OzItem it{};
+  if (MODE == kRowW) it = g.items[blockIdx.x];
+  const int t0 = MODE == kRowSG ? blockIdx.x * 128 : 0;
+  const int i = MODE == kRowSG ? blockIdx.y : it.subj;
+  const int arow = MODE == kRowSG ? t0 : it.n0;  // first A row (TR of G_i / global voxel row)
+  const int az = MODE == kRowSG ? i : 0;
+  const int bz = MODE == kRowSG ? 0 : i;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nub = (int)(ldx / 32);
   if (warp == 0) {
@@ -393,18 +415,25 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_sg(const __grid_constant__
       for (int k = 0; k < nub; ++k) {
         const int slot = k % kSgStages;
         if (k >= kSgStages) mbar_wait(&empty[slot], ((k / kSgStages) - 1) & 1);
-        mbar_expect_tx(&full[slot], (uint32_t)kSgStageBytes);
         unsigned char* st = smem + slot * kSgStageBytes;
         const int x = k * 256;
-        tma_load_3d(st, &tmg, x, t0, i, &full[slot]);
-        tma_load_3d(st + kOzBox, &tmg, x + 128, t0, i, &full[slot]);
-        tma_load_3d(st + 2 * kOzBox, &tms, x, 0, 0, &full[slot]);
-        tma_load_3d(st + 2 * kOzBox + kSgBoxS, &tms, x + 128, 0, 0, &full[slot]);
+        if (MODE == kRowSG) {
+          mbar_expect_tx(&full[slot], (uint32_t)kSgStageBytes);
+          tma_load_3d(st, &tma, x, arow, az, &full[slot]);
+          tma_load_3d(st + kOzBox, &tma, x + 128, arow, az, &full[slot]);
+        } else {
+          // Q records of 32 TRs x 4 voxel blocks x 7 slots -> [slot][vb][t][32 B]
+          mbar_expect_tx(&full[slot], (uint32_t)(kRowWABytes + 2 * kSgBoxS));
+          tma_load_5d(st, &tma, 0, k * 32, it.m0 / 32, 0, i, &full[slot]);
+        }
+        tma_load_3d(st + 2 * kOzBox, &tmb, x, 0, bz, &full[slot]);
+        tma_load_3d(st + 2 * kOzBox + kSgBoxS, &tmb, x + 128, 0, bz, &full[slot]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_s8(128, 64);
+      // kRowW: A (voxels x TRs) is MN-major (bit 15): voxels contiguous in the Q records
+      constexpr uint32_t idesc = idesc_s8(128, 64) | (MODE == kRowW ? (1u << 15) : 0u);
       for (int k = 0; k < nub; ++k) {
         const int slot = k % kSgStages;
         mbar_wait(&full[slot], (k / kSgStages) & 1);
@@ -415,7 +444,8 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_sg(const __grid_constant__
           const uint32_t acc = tmem + 64u * (uint32_t)d;
           for (int s = 0; s <= d; ++s) {
             const int s2 = d - s;
-            const uint64_t da = umma_desc_sw128(sa + (s >> 2) * kOzBox + 32 * (s & 3));
+            const uint64_t da = MODE == kRowSG ? umma_desc_sw128(sa + (s >> 2) * kOzBox + 32 * (s & 3))
+                                               : umma_desc_sw32_mn(sa + s * 4096, 1024, 256);
             const uint64_t db = umma_desc_sw128(sb + (s2 >> 2) * kSgBoxS + 32 * (s2 & 3));
             mma_s8(acc, da, db, idesc, (k == 0 && s == 0) ? 0 : 1);
           }
@@ -427,11 +457,17 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_sg(const __grid_constant__
   } else {
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
-    const int64_t t = t0 + r;
     mbar_wait(&accfull, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    const int et = t < ldx ? gexp[(int64_t)i * ldx + t] : 0;
-    double* out = bred + (int64_t)i * kp * ldo + t;
+    // kRowSG: B[f][t] of subject i; kRowW: W[row][f]
+    const int64_t t = t0 + r;
+    const bool valid = MODE == kRowSG ? t < ldx : r < it.nvb;
+    const int et = (MODE == kRowSG && valid) ? g.aexp[(int64_t)i * ldx + t] : 0;
+    const int32_t* bexp = MODE == kRowSG ? g.bexp : g.bexp + (int64_t)i * kp;
+    double* out = MODE == kRowSG ? g.out + (int64_t)i * kp * ldo + t : g.out + ((int64_t)it.n0 + r) * g.K;
+    const int64_t fstride = MODE == kRowSG ? ldo : 1;
+    const int fmax_ = MODE == kRowSG ? (int)kp : (int)g.K;
+    const int half = MODE == kRowSG ? -1 : 0;  // the 1/2 of B = S G / 2 (R already holds its 1/2)
     for (int c0 = 0; c0 < 64; c0 += 16) {
       double val[16];
 #pragma unroll
@@ -443,11 +479,11 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_sg(const __grid_constant__
 #pragma unroll
         for (int j = 0; j < 16; ++j) val[j] += ldexp((double)(int32_t)raw[j], -12 - 7 * d);
       }
-      if (t < ldx) {
+      if (valid) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int f = c0 + j;
-          if (f < kp) out[(int64_t)f * ldo] = ldexp(val[j], et + sexp[f] - 1);
+          if (f < fmax_) out[(int64_t)f * fstride] = ldexp(val[j], et + bexp[f] + half);
         }
       }
     }
@@ -455,6 +491,22 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_sg(const __grid_constant__
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 1) tmem_free(tmem, 512);
+}
+
+// R'^T[i][f][t] = 2^{e_t} (M_i^T S)[f][t] / 2 for the final W = Xhat R
+// (M_i = mmat[i], kp x kp; S = kp x ldx); one thread per (f, t), subject = blockIdx.y
+__global__ void __launch_bounds__(256) k_oz_rt(const double* __restrict__ mmat, const double* __restrict__ S,
+                                               const int32_t* __restrict__ expo, double* __restrict__ rt,
+                                               int64_t ldx, int64_t kp, int64_t K) {
+  const int i = blockIdx.y;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= kp * ldx) return;
+  const int64_t f = e / ldx, t = e - f * ldx;
+  const double* M = mmat + (int64_t)i * kp * kp;
+  double s = 0.0;
+  if (f < K)
+    for (int64_t c = 0; c < K; ++c) s += M[c * kp + f] * S[c * ldx + t];
+  rt[(int64_t)i * kp * ldx + e] = ldexp(s, expo[(int64_t)i * ldx + t] - 1);
 }
 
 }  // namespace
@@ -469,22 +521,44 @@ cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_oz_sg(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
-                         double* bred, int64_t ldx, int64_t kp, int64_t ldo, int n_local, cudaStream_t st) {
+namespace {
+
+template <int MODE>
+cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, const RowGemmArgs& g, dim3 grid, cudaStream_t st) {
   const size_t bytes = (size_t)kSgStages * kSgStageBytes + 1024;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_oz_sg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaError_t e = cudaFuncSetAttribute(k_oz_rowgemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  if (n_local == 0) return cudaSuccess;
-  if (kp > 64 || ldx % 32 != 0) return cudaErrorInvalidValue;
-  const dim3 grid((unsigned)((ldx + 127) / 128), (unsigned)n_local);
-  k_oz_sg<<<grid, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(tmg.opaque),
-                                           *reinterpret_cast<const CUtensorMap*>(tms.opaque), gexp, sexp, bred, ldx, kp,
-                                           ldo);
+  if (grid.x == 0 || grid.y == 0) return cudaSuccess;
+  if (g.kp > 64 || g.ldx % 32 != 0) return cudaErrorInvalidValue;
+  k_oz_rowgemm<MODE><<<grid, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(ta.opaque),
+                                                        *reinterpret_cast<const CUtensorMap*>(tb.opaque), g);
   return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_oz_sg(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
+                         double* bred, int64_t ldx, int64_t kp, int64_t ldo, int n_local, cudaStream_t st) {
+  RowGemmArgs g{gexp, sexp, bred, nullptr, ldx, kp, ldo, 0};
+  return run_rowgemm<kRowSG>(tmg, tms, g, dim3((unsigned)((ldx + 127) / 128), (unsigned)n_local), st);
+}
+
+cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* expo, double* rt, int64_t ldx,
+                         int64_t kp, int64_t K, int n_local, cudaStream_t st) {
+  if (n_local == 0) return cudaSuccess;
+  const dim3 grid((unsigned)((kp * ldx + 255) / 256), (unsigned)n_local);
+  k_oz_rt<<<grid, 256, 0, st>>>(mmat, S, expo, rt, ldx, kp, K);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* rexp, double* W, const OzItem* items,
+                        int n_items, int64_t ldx, int64_t kp, int64_t K, cudaStream_t st) {
+  RowGemmArgs g{nullptr, rexp, W, items, ldx, kp, 0, K};
+  return run_rowgemm<kRowW>(tmqt, tmr, g, dim3((unsigned)n_items, 1), st);
 }
 
 cudaError_t launch_oz_prepare(const DevPlan& p, int first, int count, unsigned long long* cmax, int8_t* q,

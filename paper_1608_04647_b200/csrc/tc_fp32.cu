@@ -527,6 +527,24 @@ cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 5-D int8 map over the same records Q[n][ldx][nvb][8 slots][32 voxels] with the
+// dims ordered {32 voxels, TR, voxel block, slot, subject} (non-monotonic
+// strides) and box {32, 32, 4, 7, 1}, SWIZZLE_32B: one load lands as
+// [slot][vb][t][32 B], per slot the MN-major operand of 128 voxels x 32 TRs
+// (layout verified by tools/tma5d_probe.cu)
+cudaError_t make_map_q5(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, int64_t n) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  cuuint64_t dims[5] = {32, (cuuint64_t)ldx, (cuuint64_t)(lq / 256), 8, (cuuint64_t)n};
+  cuuint64_t strides[4] = {(cuuint64_t)lq, 256, 32, (cuuint64_t)(lq * ldx)};
+  cuuint32_t box[5] = {32, 32, 4, 7, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(m->opaque), CU_TENSOR_MAP_DATA_TYPE_UINT8, 5,
+                  const_cast<int8_t*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 cudaError_t launch_tc_apass(int np, const TmaMap& tmX, const TmaMap& tmS, int64_t ncontract, float* A, int64_t lda,
                             float alpha, const ItemA* items, int n_items, cudaStream_t st) {
   if (ncontract % kTcBK != 0) return cudaErrorInvalidValue;

@@ -48,6 +48,29 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
+      "[%7];" ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+// UMMA smem descriptor, MN-major SWIZZLE_32B: atoms of 8 K-rows x 32 bytes of
+// MN (256 B; 16-byte chunk c of row r at c ^ ((r >> 2) & 1), as TMA
+// SWIZZLE_32B writes them); lbo = bytes between 32-byte MN blocks, sbo =
+// bytes between 8-row K groups (verified for kind::i8 in tools/i8_probe.cu)
+__device__ __forceinline__ uint64_t umma_desc_sw32_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  d |= (uint64_t)6 << 61;  // SWIZZLE_32B
+  return d;
+}
+
 // UMMA smem descriptor, K-major SWIZZLE_128B (8-row atoms of 1024 B; LBO unused).
 // Advancing the start address by 32 B selects the next 32-byte K slice of the
 // 128-byte swizzled rows.

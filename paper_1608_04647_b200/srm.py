@@ -350,10 +350,11 @@ _I8_PRODUCTS = 28      # slice pairs s + s' < 7 of the int8-sliced Gram
 
 
 def gram_int8_bytes(n_voxels, n_trs):
-    """Device bytes of the int8 slices of the Gram path (256 B per TR and 32 voxels)."""
+    """Device bytes of the int8 slices of the Gram path: TR-major records (256 B
+    per TR and 32 voxels) for X^T X and the row slices of every G_i."""
     ldx = -(-n_trs // 32) * 32
     lq = -(-max(n_voxels) // 32) * 256
-    return len(n_voxels) * ldx * (lq + 12)
+    return len(n_voxels) * ldx * (lq + 12) + len(n_voxels) * ldx * ldx * 8
 
 
 def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f64", gram_int8=False):
