@@ -329,10 +329,7 @@ def run_ours(args):
     eng.raise_status()
     units = cfg["n_subjects"] * V * T
     value = units / (ms / 1e3)
-    n_gram_launches = (4 if use_i8 else 2) if algo == "gram" else 0
     tc = cfg["dtype"] == "f32"
-    n_final = 2 if algo == "gram" else (4 if tc else 1)
-    launches = eng.launches_per_iteration * args.steps + n_gram_launches + n_final
 
     # per-kernel durations (CUDA events on the launch stream, untimed pass)
     st = torch.cuda.current_stream()
@@ -348,15 +345,16 @@ def run_ours(args):
             for name, t_ms in eng.profile_gram():
                 prof_g.setdefault(name, []).append(t_ms)
         once.update({k_: float(np.mean(v_)) for k_, v_ in prof_g.items()})
-    for name, fn in (("finalize", eng.finalize),):
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        a0.record(st)
-        fn()
-        a1.record(st)
-        torch.cuda.synchronize()
-        once[name] = a0.elapsed_time(a1)
+    prof_f = {}
+    for _ in range(3):
+        for name, t_ms in eng.profile_finalize():
+            prof_f.setdefault(name, []).append(t_ms)
+    once.update({k_: float(np.mean(v_)) for k_, v_ in prof_f.items()})
     eng.raise_status()
+    # kernels of the timed region: every stage is one launch except oz_split
+    # (column maxima + slicing)
+    launches = (eng.launches_per_iteration * args.steps + len(prof_f)
+                + (len(prof_g) + ("oz_split" in prof_g) if algo == "gram" else 0))
     del eng
     torch.cuda.empty_cache()
 
@@ -376,8 +374,8 @@ def run_ours(args):
         alg_bytes = float(local_units * b)                      # X-hat read once
         # int8 products issued by oz_gram: 28 slice pairs per upper 128 x 128 tile, 32-voxel blocks
         i8_ops = 2.0 * 28 * nt * (nt + 1) / 2 * 128 * 128 * (-(-V // 32) * 32) * n_local
-    elif dom == "finalize":
-        launch_ms = once["finalize"]
+    elif dom in ("final_a", "oz_w", "apply_w"):
+        launch_ms = once[dom]
         alg_flops = 2.0 * local_units * K
         alg_bytes = float(local_units * b)
     else:

@@ -203,6 +203,8 @@ int srm_profile_iteration(srm_plan* plan, float* ms_out, int capacity, int* n_ou
 /* the same for srm_prepare_gram over all local subjects (SRM_FLAG_GRAM plans;
  * *n_out = 0 otherwise) */
 int srm_profile_gram(srm_plan* plan, float* ms_out, int capacity, int* n_out, void* stream);
+/* the same for srm_finalize */
+int srm_profile_finalize(srm_plan* plan, float* ms_out, int capacity, int* n_out, void* stream);
 const char* srm_profile_name(int index);
 
 /* synchronous copy of the device status word {code, arg, iteration, 0} */

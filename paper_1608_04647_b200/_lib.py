@@ -46,6 +46,7 @@ SIGNATURES = [
     ("srm_graph_launch", c_int, [c_vp, c_vp]),
     ("srm_profile_iteration", c_int, [c_vp, ctypes.POINTER(ctypes.c_float), c_int, c_i32p, c_vp]),
     ("srm_profile_gram", c_int, [c_vp, ctypes.POINTER(ctypes.c_float), c_int, c_i32p, c_vp]),
+    ("srm_profile_finalize", c_int, [c_vp, ctypes.POINTER(ctypes.c_float), c_int, c_i32p, c_vp]),
     ("srm_profile_name", ctypes.c_char_p, [c_int]),
     ("srm_read_status", c_int, [c_vp, c_i32p]),
     ("srm_clear_status", c_int, [c_vp, c_vp]),

@@ -564,6 +564,57 @@ std::vector<std::string> g_profile_names;
 // one-time Gram X_i^T X_i of local subjects [first, first + count): int8
 // slices on the tensor cores (SRM_FLAG_GRAM_I8) or fp64 DMMA tiles, then the
 // lower triangle mirrored from the upper one
+// model.W (srm.py:315-327): W_i = A_i M_i with M_i from the last M-step
+std::vector<Stage> finalize_stages(srm_plan* p) {
+  const DevPlan& d = p->dp;
+  std::vector<Stage> v;
+  if (p->oz_w) {
+    // W_i = Xhat_i R_i, R_i = S^T M_i / 2, from the int8 slices of Xhat on the
+    // tensor cores (no A pass, no W = A M pass)
+    v.push_back({"oz_rt", [p, d](cudaStream_t st) {
+                   return launch_oz_rt(d.mmat, d.S, region<int32_t>(p, I_OZEXP), d.part, p->ldx, p->kp, p->K,
+                                       p->n_local, st);
+                 }});
+    v.push_back({"oz_slice_r", [p, d](cudaStream_t st) {
+                   return launch_oz_slice_rows(d.part, p->ldx, (int64_t)p->n_local * p->kp, p->ldx,
+                                               region<int8_t>(p, I_OZR), p->oz_lqg, region<int32_t>(p, I_OZREXP), st);
+                 }});
+    v.push_back({"oz_w", [p, d](cudaStream_t st) {
+                   return launch_oz_w(p->tm_q32, p->tm_r, region<int32_t>(p, I_OZREXP), d.wout,
+                                      region<OzItem>(p, I_ITEMS_OW), (int)p->items_ow.size(), p->ldx, p->kp, p->K,
+                                      st);
+                 }});
+    return v;
+  }
+  if (p->flags & SRM_FLAG_GRAM) {  // A_i = Xhat_i S^T / 2 is not kept per iteration on the Gram path
+    v.push_back({"final_a", [p, d](cudaStream_t st) {
+                   return launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
+                                            0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
+                 }});
+  }
+  if (p->flags & SRM_FLAG_TC) {
+    // W = A M with M from the exact fp64 Gram of the stored fp32 A, so the
+    // returned W is orthonormal to fp64 precision (acceptance criterion 4)
+    // even though the per-iteration passes run in 3xTF32
+    v.push_back({"final_gram", [p, d](cudaStream_t st) {
+                   return launch_contract_e((int)p->kp, SRM_F32, SRM_F32, d.af, p->np, d.af, p->np, d.part, p->ldo,
+                                            1.0, region<ItemE>(p, I_ITEMS_TG), (int)p->items_tg.size(), st);
+                 }});
+    v.push_back({"final_reduce", [d](cudaStream_t st) { return launch_reduce_chunks(d, st); }});
+    v.push_back({"final_polar", [d](cudaStream_t st) { return launch_eig_polar_exact(d, 1, st); }});
+    v.push_back({"apply_w", [p, d](cudaStream_t st) {
+                   return launch_apply_rows((int)p->kp, SRM_F32, d.af, p->np, d.mmat, p->kp * p->kp, d.wout,
+                                            (int)p->K, region<ItemA>(p, I_ITEMS_TA), (int)p->items_ta.size(), st);
+                 }});
+    return v;
+  }
+  v.push_back({"apply_w", [p, d](cudaStream_t st) {
+                 return launch_apply_rows((int)p->kp, SRM_F64, d.amat, p->kp, d.mmat, p->kp * p->kp, d.wout,
+                                          (int)p->K, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
+               }});
+  return v;
+}
+
 std::vector<Stage> gram_stages(srm_plan* p, int first, int count) {
   const DevPlan& d = p->dp;
   std::vector<Stage> v;
@@ -913,42 +964,12 @@ const char* srm_profile_name(int index) {
 
 int srm_finalize(srm_plan* p, void* stream) {
   if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
-  cudaStream_t st = as_stream(stream);
-  const DevPlan& d = p->dp;
-  if (p->oz_w) {
-    // W_i = Xhat_i R_i, R_i = S^T M_i / 2, from the int8 slices of Xhat on the
-    // tensor cores (no A pass, no W = A M pass)
-    cudaError_t e = launch_oz_rt(d.mmat, d.S, region<int32_t>(p, I_OZEXP), d.part, p->ldx, p->kp, p->K,
-                                 p->n_local, st);
-    if (e == cudaSuccess)
-      e = launch_oz_slice_rows(d.part, p->ldx, (int64_t)p->n_local * p->kp, p->ldx, region<int8_t>(p, I_OZR),
-                               p->oz_lqg, region<int32_t>(p, I_OZREXP), st);
-    if (e == cudaSuccess)
-      e = launch_oz_w(p->tm_q32, p->tm_r, region<int32_t>(p, I_OZREXP), d.wout, region<OzItem>(p, I_ITEMS_OW),
-                      (int)p->items_ow.size(), p->ldx, p->kp, p->K, st);
-    return check(e, "finalize");
-  }
-  if (p->flags & SRM_FLAG_GRAM) {  // A_i = Xhat_i S^T / 2 is not kept per iteration on the Gram path
-    cudaError_t e = launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
-                                      0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
-    if (e != cudaSuccess) return cuda_fail(e, "finalize contract_a");
-  }
-  if (p->flags & SRM_FLAG_TC) {
-    // W = A M with M from the exact fp64 Gram of the stored fp32 A, so the
-    // returned W is orthonormal to fp64 precision (acceptance criterion 4)
-    // even though the per-iteration passes run in 3xTF32
-    cudaError_t e = launch_contract_e((int)p->kp, SRM_F32, SRM_F32, d.af, p->np, d.af, p->np, d.part, p->ldo, 1.0,
-                                      region<ItemE>(p, I_ITEMS_TG), (int)p->items_tg.size(), st);
-    if (e == cudaSuccess) e = launch_reduce_chunks(d, st);
-    if (e == cudaSuccess) e = launch_eig_polar_exact(d, 1, st);
-    if (e == cudaSuccess)
-      e = launch_apply_rows((int)p->kp, SRM_F32, d.af, p->np, d.mmat, p->kp * p->kp, d.wout, (int)p->K,
-                            region<ItemA>(p, I_ITEMS_TA), (int)p->items_ta.size(), st);
-    return check(e, "finalize");
-  }
-  return check(launch_apply_rows((int)p->kp, SRM_F64, d.amat, p->kp, d.mmat, p->kp * p->kp, d.wout, (int)p->K,
-                                 region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st),
-               "finalize");
+  return run_stages(finalize_stages(p), as_stream(stream));
+}
+
+int srm_profile_finalize(srm_plan* p, float* ms_out, int capacity, int* n_out, void* stream) {
+  if (!p || !p->ws || !ms_out || !n_out) return fail(SRM_ERR_CONFIG, "plan not bound");
+  return profile_stages(finalize_stages(p), ms_out, capacity, n_out, as_stream(stream));
 }
 
 int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {

@@ -50,6 +50,12 @@ constexpr int kOzStages = 3;
 constexpr int kOzBox = 16384;    // one 128-row x 128-byte SW128 box
 constexpr int kOzStageBytes = 4 * kOzBox;
 
+// 2^e as a double for the normal range (|e| < 1023): exact scale factors for the
+// d-group sums and the column/row exponents (a multiply, not an ldexp call)
+__device__ __forceinline__ double pow2(int e) {
+  return (e >= -1022 && e <= 1023) ? __longlong_as_double((long long)(1023 + e) << 52) : ldexp(1.0, e);
+}
+
 __device__ __forceinline__ int frexp_exp(double m) {
   int e = 0;
   frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
@@ -283,15 +289,16 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
             uint32_t raw[16];
             tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 128u * (uint32_t)(d - dlo) + c0, raw);
             tmem_wait_ld();
+            const double sd = pow2(-12 - 7 * d);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) val[j] += ldexp((double)(int32_t)raw[j], -12 - 7 * d);
+            for (int j = 0; j < 16; ++j) val[j] = fma((double)(int32_t)raw[j], sd, val[j]);
           }
           if (rin) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const int64_t tb = it.n0 + c0 + j;
               if (tb < ldx) {
-                const double g = ldexp(val[j], ea + ex[tb]);
+                const double g = val[j] * pow2(ea + ex[tb]);
                 grow[c0 + j] = (npass == 0) ? g : grow[c0 + j] + g;
               }
             }
@@ -476,14 +483,15 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
         uint32_t raw[16];
         tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 64u * (uint32_t)d + c0, raw);
         tmem_wait_ld();
+        const double sd = pow2(-12 - 7 * d);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) val[j] += ldexp((double)(int32_t)raw[j], -12 - 7 * d);
+        for (int j = 0; j < 16; ++j) val[j] = fma((double)(int32_t)raw[j], sd, val[j]);
       }
       if (valid) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int f = c0 + j;
-          if (f < fmax_) out[(int64_t)f * fstride] = ldexp(val[j], et + bexp[f] + half);
+          if (f < fmax_) out[(int64_t)f * fstride] = val[j] * pow2(et + bexp[f] + half);
         }
       }
     }
@@ -506,7 +514,7 @@ __global__ void __launch_bounds__(256) k_oz_rt(const double* __restrict__ mmat, 
   double s = 0.0;
   if (f < K)
     for (int64_t c = 0; c < K; ++c) s += M[c * kp + f] * S[c * ldx + t];
-  rt[(int64_t)i * kp * ldx + e] = ldexp(s, expo[(int64_t)i * ldx + t] - 1);
+  rt[(int64_t)i * kp * ldx + e] = s * pow2(expo[(int64_t)i * ldx + t] - 1);
 }
 
 }  // namespace

@@ -384,14 +384,20 @@ class SrmEngine:
                                                   ctypes.c_void_p(self.stream())), "profile")
         return [(self.lib.srm_profile_name(i).decode(), float(ms[i])) for i in range(n.value)]
 
-    def profile_gram(self):
-        """The one-time X^T X stages, eagerly, with an event between kernels -> [(name, ms)]."""
+    def _profile(self, fn, what):
         cap = 16
         ms = (ctypes.c_float * cap)()
         n = ctypes.c_int32()
-        _lib.check(self.lib.srm_profile_gram(self.plan, ms, cap, ctypes.byref(n),
-                                             ctypes.c_void_p(self.stream())), "profile_gram")
+        _lib.check(fn(self.plan, ms, cap, ctypes.byref(n), ctypes.c_void_p(self.stream())), what)
         return [(self.lib.srm_profile_name(i).decode(), float(ms[i])) for i in range(n.value)]
+
+    def profile_gram(self):
+        """The one-time X^T X stages, eagerly, with an event between kernels -> [(name, ms)]."""
+        return self._profile(self.lib.srm_profile_gram, "profile_gram")
+
+    def profile_finalize(self):
+        """The final W stages, eagerly, with an event between kernels -> [(name, ms)]."""
+        return self._profile(self.lib.srm_profile_finalize, "profile_finalize")
 
     @property
     def launches_per_iteration(self):
