@@ -471,7 +471,11 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
     const bool valid = MODE == kRowSG ? t < ldx : r < it.nvb;
     const int et = (MODE == kRowSG && valid) ? g.aexp[(int64_t)i * ldx + t] : 0;
     const int32_t* bexp = MODE == kRowSG ? g.bexp : g.bexp + (int64_t)i * kp;
-    double* out = MODE == kRowSG ? g.out + (int64_t)i * kp * ldo + t : g.out + ((int64_t)it.n0 + r) * g.K;
+    // kRowW stages its 128 x K tile in the (drained) pipeline smem, pitch K + 1,
+    // and then writes the tile's contiguous rows with coalesced stores
+    constexpr int kWPitch = 65;
+    double* wst = reinterpret_cast<double*>(smem);
+    double* out = MODE == kRowSG ? g.out + (int64_t)i * kp * ldo + t : wst + r * kWPitch;
     const int64_t fstride = MODE == kRowSG ? ldo : 1;
     const int fmax_ = MODE == kRowSG ? (int)kp : (int)g.K;
     const int half = MODE == kRowSG ? -1 : 0;  // the 1/2 of B = S G / 2 (R already holds its 1/2)
@@ -494,6 +498,12 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
           if (f < fmax_) out[(int64_t)f * fstride] = val[j] * pow2(et + bexp[f] + half);
         }
       }
+    }
+    if (MODE == kRowW) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the four epilogue warps
+      const int K = (int)g.K;
+      double* dst = g.out + (int64_t)it.n0 * K;
+      for (int e = (warp - 2) * 32 + lane; e < it.nvb * K; e += 128) dst[e] = wst[(e / K) * kWPitch + e % K];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
