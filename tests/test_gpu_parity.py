@@ -314,3 +314,17 @@ def test_fit_manifest_streams_sfab(srm, tmp_path):
     for wa, wb in zip(a.W, b.W):
         assert np.array_equal(wa, wb)
     assert a.rho2 == b.rho2
+
+
+def test_int8_gram_large_k_falls_back(srm):
+    """K = 72 (> 64): int8 X^T X, fp64 DMMA for B = S G / 2 and the final W."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(3, 2500, 256, 72, seed=15)
+    ref = orc.run_em(xs, 72, 3, seed=2)
+    engines = []
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=72, iterations=3, seed=2), algorithm="gram",
+                engine_out=engines)
+    assert engines[-1].gram_i8
+    r = ref["iters"][-1]
+    _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, "gram i8 k=72")
