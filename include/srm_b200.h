@@ -152,6 +152,10 @@ int srm_load_subject(srm_plan* plan, int local_index, const void* x, int x_dtype
                      int64_t ld, void* stream);
 int srm_finish_load(srm_plan* plan, void* stream);
 int srm_init_mapping(srm_plan* plan, void* stream);
+/* the same for local subjects [first, first + count) only (their draws and
+ * X-hat must be in place), so the loader can overlap it with later uploads;
+ * srm_init_mapping = this over all subjects + iteration counter reset */
+int srm_init_mapping_range(srm_plan* plan, int first, int count, void* stream);
 /* SRM_FLAG_GRAM plans: G_i = Xhat_i^T Xhat_i (T x T, fp64) for every local
  * subject, after srm_load_subject.  The per-iteration M-step then needs
  * B_i = A_i^T Xhat_i = S G_i / 2 and A_i^T A_i = B_i S^T / 2 only; A_i itself is

@@ -34,6 +34,7 @@ SIGNATURES = [
     ("srm_load_subject", c_int, [c_vp, c_int, c_vp, c_int, c_i64, c_vp]),
     ("srm_finish_load", c_int, [c_vp, c_vp]),
     ("srm_init_mapping", c_int, [c_vp, c_vp]),
+    ("srm_init_mapping_range", c_int, [c_vp, c_int, c_int, c_vp]),
     ("srm_prepare_gram", c_int, [c_vp, c_vp]),
     ("srm_prepare_gram_range", c_int, [c_vp, c_int, c_int, c_vp]),
     ("srm_reset", c_int, [c_vp, c_vp]),

@@ -204,6 +204,8 @@ void layout(srm_plan* p) {
   p->total_bytes = std::max<int64_t>(cur, 256);
   DevPlan& d = p->dp;
   d.n_local = p->n_local;
+  d.sub0 = 0;
+  d.nsub = p->n_local;
   d.n_total = p->n_total;
   d.n_order = (int)p->order.size();
   d.flags = p->flags;
@@ -883,16 +885,39 @@ int srm_finish_load(srm_plan* p, void* stream) {
   return check(launch_subject_sqnorm(p->dp, as_stream(stream)), "sqnorm");
 }
 
+int srm_init_mapping_range(srm_plan* p, int first, int count, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  if (first < 0 || count < 0 || first + count > p->n_local) return fail(SRM_ERR_CONFIG, "subject range out of bounds");
+  if (count == 0) return SRM_OK;
+  cudaStream_t st = as_stream(stream);
+  DevPlan d = p->dp;
+  d.sub0 = first;
+  d.nsub = count;
+  // the split-V items are subject-major: nchunk[i] x (ldx / 128) tiles (ex) and nchunk[i] (ea) per subject
+  const int64_t ntiles = (p->ldx + 127) / 128;
+  int64_t ex0 = 0, exn = 0, ean = 0;
+  for (int i = 0; i < first; ++i) ex0 += p->nchunk[i] * ntiles;
+  for (int i = first; i < first + count; ++i) {
+    exn += p->nchunk[i] * ntiles;
+    ean += p->nchunk[i];
+  }
+  cudaError_t e = launch_contract_e((int)p->kp, SRM_F64, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
+                                    region<ItemE>(p, I_ITEMS_EX) + ex0, (int)exn, st);
+  if (e == cudaSuccess)
+    e = launch_contract_e((int)p->kp, SRM_F64, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0,
+                          region<ItemE>(p, I_ITEMS_EA) + p->chunk0[first], (int)ean, st);
+  if (e == cudaSuccess) e = launch_reduce_chunks(d, st);
+  if (e == cudaSuccess) e = launch_eig_polar(d, 1, st);
+  if (e == cudaSuccess) e = launch_apply_m(d, 0, st);
+  if (e == cudaSuccess) e = launch_finalize_rho(d, 1, st);
+  return check(e, "init_mapping");
+}
+
 int srm_init_mapping(srm_plan* p, void* stream) {
   if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
-  cudaStream_t st = as_stream(stream);
-  int rc = run_contractions(p, st);
+  const int rc = srm_init_mapping_range(p, 0, p->n_local, stream);
   if (rc) return rc;
-  cudaError_t e = launch_eig_polar(p->dp, 1, st);
-  if (e == cudaSuccess) e = launch_apply_m(p->dp, 0, st);
-  if (e == cudaSuccess) e = launch_finalize_rho(p->dp, 1, st);
-  if (e == cudaSuccess) e = launch_set_iteration(p->dp, 0, 0, st);
-  return check(e, "init_mapping");
+  return check(launch_set_iteration(p->dp, 0, 0, as_stream(stream)), "init_mapping");
 }
 
 int srm_reduce_local(srm_plan* p, void* stream) {

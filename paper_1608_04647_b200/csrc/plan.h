@@ -34,6 +34,7 @@ constexpr int kGfbCols = 128;
 
 struct DevPlan {
   int n_local, n_total, n_order;
+  int sub0, nsub;  // subject window [sub0, sub0 + nsub) of the per-subject kernels (default: all)
   int flags;
   int64_t T, K, ldx, kp, ldo;
   int ntile_apply;  // kApplyCols-column tiles of ldx

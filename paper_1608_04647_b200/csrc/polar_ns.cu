@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar(DevPlan p, int init) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32];
   __shared__ double s_scale;
-  const int i = blockIdx.x;
+  const int i = p.sub0 + blockIdx.x;
   const int n = (int)p.K;
   const int tid = threadIdx.x;
   double* buf[4] = {sm, sm + MAT, sm + 2 * MAT, sm + 3 * MAT};
@@ -165,7 +165,7 @@ cudaError_t run_ns(const DevPlan& p, int init, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_ns_polar<KP><<<p.n_local, kNsThreads, bytes, s>>>(p, init);
+  k_ns_polar<KP><<<p.nsub, kNsThreads, bytes, s>>>(p, init);
   return cudaGetLastError();
 }
 
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(256) k_ns_polar_f32(DevPlan p, int init) {
   extern __shared__ __align__(16) float smf[];
   __shared__ double red[32];
   __shared__ double s_scale;
-  const int i = blockIdx.x;
+  const int i = p.sub0 + blockIdx.x;
   const int n = (int)p.K;
   const int tid = threadIdx.x;
   float* buf[4] = {smf, smf + MAT, smf + 2 * MAT, smf + 3 * MAT};
@@ -313,7 +313,7 @@ cudaError_t run_ns_f32(const DevPlan& p, int init, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_ns_polar_f32<KP><<<p.n_local, 256, bytes, s>>>(p, init);
+  k_ns_polar_f32<KP><<<p.nsub, 256, bytes, s>>>(p, init);
   return cudaGetLastError();
 }
 

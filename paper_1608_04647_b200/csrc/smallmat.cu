@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_subject_sqnorm(DevPlan p) {
 // reduce_chunks: bred[i] = sum_c part[chunk0 + c] (fixed order)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSmallThreads) k_reduce_chunks(DevPlan p) {
-  const int i = blockIdx.y;
+  const int i = p.sub0 + blockIdx.y;
   const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
   const int64_t c0 = sj[SC_CHUNK0], nc = sj[SC_NCHUNK];
   const int64_t n2 = p.kp * p.ldo / 2;  // double2 elements
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_eig_polar(DevPlan p, int init
   const int iteration = init ? -1 : *p.iter;
   const int cold = (init || iteration == 0) ? 1 : 0;
   extern __shared__ __align__(16) double sm[];
-  const int i = blockIdx.x;
+  const int i = p.sub0 + blockIdx.x;
   const int n = (int)p.K;
   const int ld = n + 1;
   const int kp = (int)p.kp;
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_apply_m(DevPlan p, int with_c
   extern __shared__ __align__(16) double sm[];
   __shared__ double scratch[32];
   constexpr int kp = 8 * NF;
-  const int tile = blockIdx.x, i = blockIdx.y;
+  const int tile = blockIdx.x, i = p.sub0 + blockIdx.y;
   const int K = (int)p.K;
   const int64_t t0 = (int64_t)tile * kApplyCols;
   double* Ms = sm;             // [K][kp]: Ms[c kp + f] = M_i[c][f]
@@ -490,8 +490,9 @@ __global__ void k_set_iteration(DevPlan p, int iteration, int advance) {
 
 __global__ void k_finalize_rho(DevPlan p, int init) {
   const int iteration = init ? -1 : *p.iter;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= p.n_local) return;
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= p.nsub) return;
+  const int i = p.sub0 + w;
   const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
   double* rec = rec_ptr(p, (int)sj[SC_SLOT]) + p.kp * p.ldx;
   double rho2 = 1.0;
@@ -1100,7 +1101,7 @@ cudaError_t launch_subject_sqnorm(const DevPlan& p, cudaStream_t s) {
 
 cudaError_t launch_reduce_chunks(const DevPlan& p, cudaStream_t s) {
   const int64_t n2 = p.kp * p.ldo / 2;
-  const dim3 grid((unsigned)((n2 + kSmallThreads - 1) / kSmallThreads), (unsigned)p.n_local);
+  const dim3 grid((unsigned)((n2 + kSmallThreads - 1) / kSmallThreads), (unsigned)p.nsub);
   k_reduce_chunks<<<grid, kSmallThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
@@ -1117,7 +1118,7 @@ cudaError_t launch_eig_polar_exact(const DevPlan& p, int init, cudaStream_t s) {
   const size_t bytes = eig_smem_bytes((int)p.K);
   cudaError_t e = set_smem((const void*)k_eig_polar, bytes);
   if (e != cudaSuccess) return e;
-  k_eig_polar<<<p.n_local, kSmallThreads, bytes, s>>>(p, init);
+  k_eig_polar<<<p.nsub, kSmallThreads, bytes, s>>>(p, init);
   return cudaGetLastError();
 }
 
@@ -1138,7 +1139,7 @@ cudaError_t launch_apply_m(const DevPlan& p, int with_cross, cudaStream_t s) {
   }
   cudaError_t e = set_smem(fn, bytes);
   if (e != cudaSuccess) return e;
-  const dim3 grid((unsigned)p.ntile_apply, (unsigned)p.n_local);
+  const dim3 grid((unsigned)p.ntile_apply, (unsigned)p.nsub);
   DevPlan arg = p;
   void* args[] = {&arg, &with_cross};
   e = cudaLaunchKernel(fn, grid, dim3(kSmallThreads), args, bytes, s);
@@ -1155,7 +1156,7 @@ cudaError_t launch_gram_from_b(const DevPlan& p, cudaStream_t s) {
 }
 
 cudaError_t launch_finalize_rho(const DevPlan& p, int init, cudaStream_t s) {
-  k_finalize_rho<<<(p.n_local + 127) / 128, 128, 0, s>>>(p, init);
+  k_finalize_rho<<<(p.nsub + 127) / 128, 128, 0, s>>>(p, init);
   return cudaGetLastError();
 }
 

@@ -163,22 +163,62 @@ class SrmEngine:
             self._staging[key] = buf
         return buf[:numel]
 
-    def load(self, xs, gaussians=None, gram=False):
+    def load(self, xs, gaussians=None, gram=False, init=False):
         """Upload (if needed) and demean every local subject (srm.py:238-240).
 
         Pipelined per subject: the host-to-device copy of subject j+1 (copy
         stream) overlaps the demean -- and, with ``gram``, the one-time
         X_j^T X_j -- of subject j (compute stream).  ``gaussians`` (arrays or
-        futures of the init draws) are uploaded into the A region on the way.
+        futures of the init draws) are uploaded into the A region on the way;
+        with ``init`` the initial mapping (srm.py:101-118) of each batch of
+        subjects runs there too, so only the iteration counter remains
+        (:meth:`set_iteration`).
         """
         torch = _torch()
         if len(xs) != self.n_local:
             raise ConfigError("subject count does not match the plan")
+        if init and gaussians is None:
+            raise ConfigError("init needs the initial draws")
         main = torch.cuda.current_stream(self.device)
         copier = torch.cuda.Stream(device=self.device)
         gram_stream = torch.cuda.Stream(device=self.device)
-        done = [None, None]
+        # demean gates the reuse of the staging buffers, so it runs at high priority
+        # ahead of the side-stream Gram / init kernels that overlap the upload
+        prep = torch.cuda.Stream(device=self.device, priority=-1)
+        prep.wait_stream(main)
+        n_stage = 3
+        done = [None] * n_stage
         next_g = 0
+        # side-stream batches: each Gram launch should fill the 148 SMs (1 CTA/SM per
+        # 128 x 128 tile); without the Gram, about eight batches per load
+        nt = -(-self.ldx // 128)
+        batch = max(1, -(-148 // (nt * (nt + 1) // 2))) if (gram and self.gram) else max(1, -(-self.n_local // 8))
+        init_pending = []  # (first, end, demean event) batches waiting for their draws
+
+        def upload_ready_draws(nxt, upto):
+            # draws of subjects <= upto always (they free pinned ring slots for the
+            # producers); later ones only when already drawn
+            while nxt < self.n_local:
+                g = gaussians[nxt]
+                if nxt > upto and hasattr(g, "done") and not g.done():
+                    break
+                with torch.cuda.stream(copier):
+                    self._upload_gaussian(nxt, g, stream=copier)
+                gaussians[nxt] = None
+                nxt += 1
+            return nxt
+
+        def flush_init(uploaded):
+            # batches whose draws are all on the device: initial mapping on the side stream
+            while init_pending and init_pending[0][1] <= uploaded:
+                first, end, ev_x = init_pending.pop(0)
+                evd = torch.cuda.Event()
+                evd.record(copier)
+                gram_stream.wait_event(evd)
+                gram_stream.wait_event(ev_x)
+                _lib.check(self.lib.srm_init_mapping_range(self.plan, first, end - first,
+                                                           ctypes.c_void_p(gram_stream.cuda_stream)),
+                           "init_mapping")
         for j, x in enumerate(xs):
             v = self.n_voxels[j]
             pending = None
@@ -200,7 +240,7 @@ class SrmEngine:
                     if arr.dtype not in (np.float64, np.float32):
                         arr = arr.astype(np.float64)
                     host = torch.from_numpy(np.ascontiguousarray(arr))
-                b = j % 2
+                b = j % n_stage
                 buf = self._staging_buf(b, host.dtype, v * self.T).view(v, self.T)
                 if done[b] is not None:
                     copier.wait_event(done[b])
@@ -213,7 +253,7 @@ class SrmEngine:
                     hostio.to_device(host.numpy(), self.device, out=buf)
                 ev = torch.cuda.Event()
                 ev.record(copier)
-                main.wait_event(ev)
+                prep.wait_event(ev)
                 if pending is not None:
                     pending.release(ev)  # its pinned slot is free once this copy completes
                 src = buf
@@ -222,36 +262,29 @@ class SrmEngine:
                 raise ConfigError("subject shape does not match the plan")
             dt = _lib.SRM_F64 if src.dtype == torch.float64 else _lib.SRM_F32
             _lib.check(self.lib.srm_load_subject(self.plan, j, ctypes.c_void_p(src.data_ptr()), dt, ld,
-                                                 ctypes.c_void_p(main.cuda_stream)), "load_subject")
+                                                 ctypes.c_void_p(prep.cuda_stream)), "load_subject")
             ev2 = torch.cuda.Event()
-            ev2.record(main)
-            done[j % 2] = ev2
-            if gram and self.gram:
-                # batch subjects so each Gram launch fills the 148 SMs (1 CTA/SM per 128x128
-                # tile); it runs on its own stream so staging-buffer reuse only waits on demean
-                nt = -(-self.ldx // 128)
-                batch = max(1, -(-148 // (nt * (nt + 1) // 2)))
-                if (j + 1) % batch == 0 or j + 1 == self.n_local:
-                    first = (j // batch) * batch
-                    gram_stream.wait_event(ev2)
+            ev2.record(prep)
+            done[j % n_stage] = ev2
+            if (j + 1) % batch == 0 or j + 1 == self.n_local:
+                # per batch of subjects, on a side stream (staging-buffer reuse only
+                # waits on demean): the one-time X^T X and the initial mapping
+                first = (j // batch) * batch
+                gram_stream.wait_event(ev2)
+                if gram and self.gram:
                     _lib.check(self.lib.srm_prepare_gram_range(self.plan, first, j + 1 - first,
                                                                ctypes.c_void_p(gram_stream.cuda_stream)),
                                "prepare_gram")
+                if init:
+                    init_pending.append((first, j + 1, ev2))
             if gaussians is not None:
-                # upload the init draws that are ready without stalling the copy stream
-                while next_g < self.n_local and (next_g <= j or not hasattr(gaussians[next_g], "done")
-                                                 or gaussians[next_g].done()):
-                    if hasattr(gaussians[next_g], "done") and not gaussians[next_g].done() and next_g > j - 2:
-                        break
-                    with torch.cuda.stream(copier):
-                        self._upload_gaussian(next_g, gaussians[next_g], stream=copier)
-                    gaussians[next_g] = None
-                    next_g += 1
-        while gaussians is not None and next_g < self.n_local:
-            with torch.cuda.stream(copier):
-                self._upload_gaussian(next_g, gaussians[next_g], stream=copier)
-            gaussians[next_g] = None
-            next_g += 1
+                # upload the init draws that are ready, never stalling the copy stream
+                next_g = upload_ready_draws(next_g, upto=j)
+                flush_init(next_g)
+        if gaussians is not None:
+            next_g = upload_ready_draws(next_g, upto=self.n_local)
+            flush_init(next_g)
+        main.wait_stream(prep)
         _lib.check(self.lib.srm_finish_load(self.plan, ctypes.c_void_p(main.cuda_stream)), "finish_load")
         main.wait_stream(gram_stream)
         main.wait_stream(copier)

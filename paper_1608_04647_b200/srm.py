@@ -397,7 +397,7 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f
 
 def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=True,
         keep_on_device=False, device=None, engine_out=None, timings=None, algorithm="auto",
-        tensor_cores=True, gram_int8=True):
+        tensor_cores=True, gram_int8=True, init_overlap=True):
     """Run the distributed EM; ``subjects`` are this worker's share (srm.py:216).
 
     Every worker calls this with the same config and its own communicator
@@ -422,6 +422,9 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     from seven exact int8 slices per value on the int8 tensor cores (products
     represented to ~2^-48 of the column maxima; ~1e-14 relative to G) when
     the slices fit in device memory; ``False`` keeps it on fp64 DMMA.
+    ``init_overlap``: run the initial mapping (srm.py:101-118 after the draw)
+    batch by batch while later subjects are still uploading (default), or
+    once after the upload.
     """
     clock = _PhaseClock(timings)
     config.validate()
@@ -481,11 +484,14 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
 
     draws = [pool.submit(draw, j) for j in range(len(subjects))]
     clock.tick("setup")
-    # pipelined: upload + demean (+ X^T X on the Gram path) + init draws per subject
-    eng.load([s.X for s in subjects], gaussians=draws, gram=True)
+    # pipelined: upload + demean (+ X^T X) (+ the initial mapping) per batch of subjects
+    eng.load([s.X for s in subjects], gaussians=draws, gram=True, init=init_overlap)
     pool.shutdown(wait=False)
     clock.tick("load")
-    eng.init_kernels()
+    if init_overlap:
+        eng.set_iteration(0)
+    else:
+        eng.init_kernels()
     clock.tick("init")
 
     use_graph = graphs and comm.size == 1

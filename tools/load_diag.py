@@ -14,7 +14,7 @@ xs, _, _ = recipe_torch(n, V, T, K, seed=0, dtype="f64")
 host = [x.cpu().pin_memory() for x in xs]
 del xs
 torch.cuda.empty_cache()
-eng = SrmEngine([V] * n, T, K, 20, storage="f64", gram=True)
+eng = SrmEngine([V] * n, T, K, 20, storage="f64", gram=True, gram_i8=True)
 def run(gaussians, gram, label):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     eng.load(host, gaussians=gaussians, gram=gram)
