@@ -55,7 +55,6 @@ enum Internal {
   I_ITEMS_EX,
   I_ITEMS_EA,
   I_ITEMS_A,
-  I_ITEMS_G,
   I_ST,
   I_ITEMS_GRAM,
   I_ITEMS_BG,
@@ -104,7 +103,7 @@ struct srm_plan {
   int64_t chunks_total = 0;
   std::vector<ItemE> items_ex, items_ea, items_gram, items_bg, items_tb, items_tg;
   int np = 0;  // tensor-core feature padding
-  std::vector<ItemA> items_a, items_g, items_ta;
+  std::vector<ItemA> items_a, items_ta;
   std::vector<int64_t> subj;
   std::vector<int32_t> order, order_local;
   int64_t off[I_COUNT] = {0};
@@ -170,7 +169,6 @@ void layout(srm_plan* p) {
   sz[I_ITEMS_EX] = (int64_t)p->items_ex.size() * sizeof(ItemE);
   sz[I_ITEMS_EA] = (int64_t)p->items_ea.size() * sizeof(ItemE);
   sz[I_ITEMS_A] = (int64_t)p->items_a.size() * sizeof(ItemA);
-  sz[I_ITEMS_G] = (int64_t)p->items_g.size() * sizeof(ItemA);
   sz[I_ST] = p->ldx * p->kp * 8;
   sz[I_ITEMS_GRAM] = (int64_t)p->items_gram.size() * sizeof(ItemE);
   sz[I_ITEMS_BG] = (int64_t)p->items_bg.size() * sizeof(ItemE);
@@ -246,16 +244,6 @@ void build_work(srm_plan* p) {
   p->items_ex.clear();
   p->items_ea.clear();
   p->items_a.clear();
-  p->items_g.clear();
-  for (int i = 0; i < p->n_local; ++i) {
-    // A_i^T A_i = (A_i^T Xhat_i) S^T / 2 = B_i S^T / 2 over the reduced B_i
-    ItemA g;
-    g.x_off = (int64_t)i * p->kp * p->ldo;
-    g.o_off = (int64_t)i * p->kp * p->ldo + p->ldx;
-    g.rows = (int32_t)p->K;
-    g.pad = i;
-    p->items_g.push_back(g);
-  }
   for (int i = 0; i < p->n_local; ++i) {
     for (int64_t ch = 0; ch < p->nchunk[i]; ++ch) {
       const int64_t r0 = p->row_off[i] + ch * cr;
@@ -816,7 +804,7 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
   } ups[] = {{I_SUBJ, p->subj.data()},         {I_ORDER, p->order.data()},
              {I_ORDER_LOCAL, p->order_local.data()}, {I_ITEMS_EX, p->items_ex.data()},
              {I_ITEMS_EA, p->items_ea.data()},  {I_ITEMS_A, p->items_a.data()},
-             {I_ITEMS_G, p->items_g.data()},     {I_ITEMS_GRAM, p->items_gram.data()},
+             {I_ITEMS_GRAM, p->items_gram.data()},
              {I_ITEMS_BG, p->items_bg.data()},   {I_ITEMS_TB, p->items_tb.data()},
              {I_ITEMS_TA, p->items_ta.data()},   {I_ITEMS_TG, p->items_tg.data()},
              {I_ITEMS_OZ, p->items_oz.data()},   {I_ITEMS_OW, p->items_ow.data()}};
