@@ -274,7 +274,7 @@ def run_ours(args):
     # precompute when the Gram path is chosen, K EM iterations, and the final
     # W_i = A_i M_i.  One-time work is therefore charged to the K steps.
     algo = args.algorithm
-    use_i8 = args.gram_int8 == "on" and cfg["dtype"] == "f64"
+    use_i8 = args.gram_int8 == "on"
     if algo == "auto":
         algo = srm.choose_algorithm([V] * cfg["n_subjects"], T, K, args.steps,
                                     torch.cuda.mem_get_info(dev)[0] * world, storage=cfg["dtype"],
@@ -373,7 +373,8 @@ def run_ours(args):
         alg_flops = float(n_local) * V * T * (T + 1)          # symmetric X^T X: T(T+1)/2 dots of length V
         alg_bytes = float(local_units * b)                      # X-hat read once
         # int8 products issued by oz_gram: 28 slice pairs per upper 128 x 128 tile, 32-voxel blocks
-        i8_ops = 2.0 * 28 * nt * (nt + 1) / 2 * 128 * 128 * (-(-V // 32) * 32) * n_local
+        products = 28 if cfg["dtype"] == "f64" else 16  # slice pairs: 7 or 4 slices per value
+        i8_ops = 2.0 * products * nt * (nt + 1) / 2 * 128 * 128 * (-(-V // 32) * 32) * n_local
     elif dom in ("final_a", "oz_w", "apply_w"):
         launch_ms = once[dom]
         alg_flops = 2.0 * local_units * K
@@ -479,7 +480,9 @@ def run_ours(args):
             "data": "synthetic: BASELINE generative recipe (seeded, device Philox stream); reference init",
             "config": config_json(cfg, args.config, world),
             "roofline": roofline, "secondary_roofline": other_roofline, "algorithm": algo,
-            "gram_xtx": ("int8 slices on tcgen05 (7 slices, ~2^-48 of column max)" if use_i8 else "fp64 DMMA")
+            "gram_xtx": (("int8 slices on tcgen05 (7 slices, ~2^-48 of column max)" if cfg["dtype"] == "f64"
+                          else "int8 slices on tcgen05 (4 slices, ~2^-27 of column max; fp32 data)")
+                         if use_i8 else "fp64 DMMA")
             if algo == "gram" else None,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "kernel_ms": prof, "kernel_share": step_share, "impl": "ours",

@@ -117,6 +117,7 @@ struct srm_plan {
   TmaMap tm_x_a, tm_s, tm_a, tm_x_b;  // tensor-core path TMA maps (bound at srm_plan_bind)
   std::vector<OzItem> items_oz;       // int8-sliced Gram tiles (SRM_FLAG_GRAM_I8)
   int64_t oz_lq = 0, max_v = 0;       // bytes per sliced TR row; largest local V
+  int oz_nsl = 7;                     // int8 slices per X-hat value: 7 (fp64), 4 (fp32)
   TmaMap tm_q;
   bool oz_sg = false;                 // per-iteration B = S G / 2 from int8 row slices (kp <= 64)
   int64_t oz_lqg = 0;                 // bytes per sliced row of G_i / S / R'^T / Qt
@@ -207,6 +208,7 @@ void layout(srm_plan* p) {
   d.n_total = p->n_total;
   d.n_order = (int)p->order.size();
   d.flags = p->flags;
+  d.xf32 = p->dtype == SRM_F32 ? 1 : 0;
   d.T = p->T;
   d.K = p->K;
   d.ldx = p->ldx;
@@ -314,8 +316,9 @@ void build_work(srm_plan* p) {
   p->items_oz.clear();
   p->max_v = 0;
   for (int i = 0; i < p->n_local; ++i) p->max_v = std::max(p->max_v, p->V[i]);
-  p->oz_lq = round_up(std::max<int64_t>(p->max_v, 1), 32) / 32 * kOzRecord;
-  p->oz_sg = (p->flags & SRM_FLAG_GRAM_I8) && p->kp <= 64;
+  p->oz_nsl = p->dtype == SRM_F64 ? 7 : 4;
+  p->oz_lq = round_up(std::max<int64_t>(p->max_v, 1), 32) / 32 * oz_record_bytes(p->oz_nsl);
+  p->oz_sg = (p->flags & SRM_FLAG_GRAM_I8) && p->kp <= 128;
   p->oz_lqg = p->ldx / 32 * kOzRecord;
   p->oz_w = p->oz_sg;
   p->items_ow.clear();
@@ -558,6 +561,12 @@ std::vector<std::string> g_profile_names;
 std::vector<Stage> finalize_stages(srm_plan* p) {
   const DevPlan& d = p->dp;
   std::vector<Stage> v;
+  if ((p->flags & SRM_FLAG_GRAM) && p->dtype == SRM_F32 && !ns_polar_supported((int)p->kp) &&
+      ns_polar_f32_supported((int)p->kp)) {
+    // the per-iteration polar ran in fp32 (K > 80): the returned W takes the
+    // exact fp64 transform of the last M-step's A^T A (still in bred)
+    v.push_back({"final_polar", [d](cudaStream_t st) { return launch_eig_polar_exact(d, 1, st); }});
+  }
   if (p->oz_w) {
     // W_i = Xhat_i R_i, R_i = S^T M_i / 2, from the int8 slices of Xhat on the
     // tensor cores (no A pass, no W = A M pass)
@@ -572,7 +581,7 @@ std::vector<Stage> finalize_stages(srm_plan* p) {
     v.push_back({"oz_w", [p, d](cudaStream_t st) {
                    return launch_oz_w(p->tm_q32, p->tm_r, region<int32_t>(p, I_OZREXP), d.wout,
                                       region<OzItem>(p, I_ITEMS_OW), (int)p->items_ow.size(), p->ldx, p->kp, p->K,
-                                      st);
+                                      p->oz_nsl, st);
                  }});
     return v;
   }
@@ -611,13 +620,14 @@ std::vector<Stage> gram_stages(srm_plan* p, int first, int count) {
   if (p->flags & SRM_FLAG_GRAM_I8) {
     const int per = (int)(p->items_oz.size() / p->n_local);  // upper tiles per subject (subject-major)
     v.push_back({"oz_split", [p, d, first, count](cudaStream_t st) {
-                   return launch_oz_prepare(d, first, count, region<unsigned long long>(p, I_OZCMAX),
-                                            region<int8_t>(p, I_OZQ), p->oz_lq, region<int32_t>(p, I_OZEXP),
-                                            p->max_v, st);
+                   return launch_oz_prepare(d, p->dtype, p->oz_nsl, first, count,
+                                            region<unsigned long long>(p, I_OZCMAX), region<int8_t>(p, I_OZQ),
+                                            p->oz_lq, region<int32_t>(p, I_OZEXP), p->max_v, st);
                  }});
     v.push_back({"oz_gram", [p, d, first, count, per](cudaStream_t st) {
                    return launch_oz_gram(p->tm_q, region<int32_t>(p, I_OZEXP), d.gram, p->ldx,
-                                         region<OzItem>(p, I_ITEMS_OZ) + (int64_t)first * per, count * per, st);
+                                         region<OzItem>(p, I_ITEMS_OZ) + (int64_t)first * per, count * per,
+                                         p->oz_nsl, st);
                  }});
   } else {
     const int per = (int)(p->items_gram.size() / p->n_local);
@@ -713,7 +723,7 @@ int srm_plan_create(srm_plan** out, int dtype, int n_local, const int64_t* n_vox
   if (world_size == 1) p->flags |= SRM_FLAG_ORDERED;
   if ((p->flags & SRM_FLAG_TC) && (dtype != SRM_F32 || !tc_supported((int)k))) p->flags &= ~SRM_FLAG_TC;
   if ((p->flags & SRM_FLAG_TC) && (p->flags & SRM_FLAG_GRAM)) p->flags &= ~SRM_FLAG_TC;
-  if ((p->flags & SRM_FLAG_GRAM_I8) && (!(p->flags & SRM_FLAG_GRAM) || dtype != SRM_F64)) p->flags &= ~SRM_FLAG_GRAM_I8;
+  if ((p->flags & SRM_FLAG_GRAM_I8) && !(p->flags & SRM_FLAG_GRAM)) p->flags &= ~SRM_FLAG_GRAM_I8;
   p->np = tc_np((int)k);
   p->n_total = 0;
   p->max_local = 0;
@@ -843,7 +853,7 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     e = launch_gram_tiles(p->dtype, d.xhat, p->ldx, d.gram, p->ldx, nullptr, 0, 0);
   if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM_I8)) {
     e = make_map_q(&p->tm_q, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, 128);
-    if (e == cudaSuccess) e = launch_oz_gram(p->tm_q, nullptr, nullptr, p->ldx, nullptr, 0, 0);
+    if (e == cudaSuccess) e = launch_oz_gram(p->tm_q, nullptr, nullptr, p->ldx, nullptr, 0, p->oz_nsl, 0);
     if (e == cudaSuccess && p->oz_sg) {
       e = make_map_q(&p->tm_g, region<int8_t>(p, I_OZG), p->oz_lqg, p->ldx, p->n_local, 128);
       if (e == cudaSuccess) e = make_map_q(&p->tm_sq, region<int8_t>(p, I_OZS), p->oz_lqg, p->kp, 1, 64);
@@ -851,9 +861,10 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
         e = launch_oz_sg(p->tm_g, p->tm_sq, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, 0, 0);
     }
     if (e == cudaSuccess && p->oz_w) {
-      e = make_map_q5(&p->tm_q32, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local);
+      e = make_map_q5(&p->tm_q32, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, p->oz_nsl);
       if (e == cudaSuccess) e = make_map_q(&p->tm_r, region<int8_t>(p, I_OZR), p->oz_lqg, p->kp, p->n_local, 64);
-      if (e == cudaSuccess) e = launch_oz_w(p->tm_q32, p->tm_r, nullptr, nullptr, nullptr, 0, p->ldx, p->kp, p->K, 0);
+      if (e == cudaSuccess)
+        e = launch_oz_w(p->tm_q32, p->tm_r, nullptr, nullptr, nullptr, 0, p->ldx, p->kp, p->K, p->oz_nsl, 0);
     }
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");

@@ -71,9 +71,12 @@ struct OzItem {
   int32_t nvb;   // 32-voxel blocks of the subject
 };
 constexpr int kOzChunkBlocks = 2048;  // 65536 voxels per exact int32 accumulation
-constexpr int64_t kOzRecord = 256;    // bytes per (TR, 32-voxel block): 8 slots x 32 voxels
+constexpr int64_t kOzRecord = 256;    // bytes per (row, 32-column block): 8 slots x 32
+// record bytes of the X-hat slices: 8 slots (256 B) for fp64's seven slices,
+// 4 slots (128 B) for fp32's four
+inline __host__ __device__ int oz_record_bytes(int nsl) { return nsl <= 4 ? 128 : 256; }
 cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n, int box_rows);
-cudaError_t make_map_q5(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, int64_t n);
+cudaError_t make_map_q5(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, int64_t n, int nsl);
 // int8 slices of the rows of a row-major fp64 matrix (ozaki.cu): 2^e[r] >= max|M[r][:]|
 cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int64_t ncols, int8_t* q, int64_t lq,
                                  int32_t* expo, cudaStream_t st);
@@ -85,10 +88,11 @@ cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* exp
                          int64_t kp, int64_t K, int n_local, cudaStream_t st);
 // W rows = Qt (voxel-major X-hat slices) x the row slices of R'^T (kp <= 64)
 cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* rexp, double* W, const OzItem* items,
-                        int n_items, int64_t ldx, int64_t kp, int64_t K, cudaStream_t st);
+                        int n_items, int64_t ldx, int64_t kp, int64_t K, int nsl, cudaStream_t st);
 size_t oz_gram_smem_bytes();
+// X_i^T X_i tiles from the nsl-slice records (nsl = 7 for fp64 X-hat, 4 for fp32)
 cudaError_t launch_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
-                           int n_items, cudaStream_t st);
+                           int n_items, int nsl, cudaStream_t st);
 
 // thread-local message returned by srm_last_error() (defined in capi.cu)
 void set_last_error(const char* where, cudaError_t e);

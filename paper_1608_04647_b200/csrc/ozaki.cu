@@ -67,7 +67,8 @@ __device__ __forceinline__ int frexp_exp(double m) {
 // ---------------------------------------------------------------------------
 constexpr int kColmaxRows = 256;
 
-__global__ void __launch_bounds__(256) k_oz_colmax(DevPlan p, const double* __restrict__ xhat,
+template <typename TX>
+__global__ void __launch_bounds__(256) k_oz_colmax(DevPlan p, const TX* __restrict__ xhat,
                                                    unsigned long long* __restrict__ cmax) {
   const int i = blockIdx.y;
   const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
@@ -76,16 +77,16 @@ __global__ void __launch_bounds__(256) k_oz_colmax(DevPlan p, const double* __re
   if (r0 >= V) return;
   const int64_t r1 = min(V, r0 + kColmaxRows);
   for (int64_t t = threadIdx.x; t < p.ldx; t += blockDim.x) {
-    const double* x = xhat + (row0 + r0) * p.ldx + t;
+    const TX* x = xhat + (row0 + r0) * p.ldx + t;
     double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
     int64_t r = r0;
     for (; r + 4 <= r1; r += 4, x += 4 * p.ldx) {
-      m0 = fmax(m0, fabs(x[0]));
-      m1 = fmax(m1, fabs(x[p.ldx]));
-      m2 = fmax(m2, fabs(x[2 * p.ldx]));
-      m3 = fmax(m3, fabs(x[3 * p.ldx]));
+      m0 = fmax(m0, fabs(to_f64(x[0])));
+      m1 = fmax(m1, fabs(to_f64(x[p.ldx])));
+      m2 = fmax(m2, fabs(to_f64(x[2 * p.ldx])));
+      m3 = fmax(m3, fabs(to_f64(x[3 * p.ldx])));
     }
-    for (; r < r1; ++r, x += p.ldx) m0 = fmax(m0, fabs(x[0]));
+    for (; r < r1; ++r, x += p.ldx) m0 = fmax(m0, fabs(to_f64(x[0])));
     const double m = fmax(fmax(m0, m1), fmax(m2, m3));
     if (m > 0.0) atomicMax(cmax + (int64_t)i * p.ldx + t, (unsigned long long)__double_as_longlong(m));
   }
@@ -106,9 +107,14 @@ __device__ __forceinline__ double round_shift(double y, int* low) {
   return t - magic;
 }
 
-__global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const double* __restrict__ xhat,
+// nsl slices per value (7 for fp64 X-hat, 4 for fp32); records of `rec` bytes
+// (256: eight 32-voxel slots; 128: four), slots beyond nsl zero
+template <typename TX, int NSL>
+__global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restrict__ xhat,
                                                   const unsigned long long* __restrict__ cmax,
                                                   int8_t* __restrict__ q, int64_t lq, int32_t* __restrict__ expo) {
+  constexpr int nsl = NSL;
+  constexpr int rec = NSL <= 4 ? 128 : 256;
   __shared__ __align__(16) uint32_t buf[128 * kSplitLdw];
   const int i = blockIdx.z;
   const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
@@ -131,7 +137,7 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const double* __res
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     const int64_t v = vb * 32 + half * 16 + u;
-    x[u] = (tin && v < V) ? xhat[(row0 + v) * p.ldx + t] : 0.0;
+    x[u] = (tin && v < V) ? to_f64(xhat[(row0 + v) * p.ldx + t]) : 0.0;
   }
   uint32_t w[kOzSlices][4];
 #pragma unroll
@@ -149,18 +155,22 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const double* __res
       y = (y - r) * 128.0;  // exact: |y - r| <= 1/2
     }
   }
-  // record layout per t: 16-byte chunk (slot * 2 + half); slot 7 stays zero
+  // record layout per t: 16-byte chunk (slot * 2 + half); slots >= nsl stay zero
   uint4* row = reinterpret_cast<uint4*>(buf + tl * kSplitLdw);
+  const int nslot = rec / 32;
 #pragma unroll
-  for (int s = 0; s < kOzSlices; ++s) row[s * 2 + half] = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
-  row[7 * 2 + half] = make_uint4(0u, 0u, 0u, 0u);
+  for (int s = 0; s < 8; ++s)
+    if (s < nslot)
+      row[s * 2 + half] = (s < nsl && s < kOzSlices) ? make_uint4(w[s][0], w[s][1], w[s][2], w[s][3])
+                                                      : make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
-  // 128 rows x 16 chunks of 16 bytes; 16 consecutive threads write one 256-byte record
-  for (int c = threadIdx.x; c < 128 * 16; c += blockDim.x) {
-    const int r = c >> 4, k = c & 15;
+  // 128 rows x rec / 16 chunks of 16 bytes; consecutive threads write one record
+  const int nch = rec / 16;
+  for (int c = threadIdx.x; c < 128 * nch; c += blockDim.x) {
+    const int r = c / nch, k = c % nch;
     const int64_t tt = t0 + r;
     if (tt < p.ldx) {
-      uint4* dst = reinterpret_cast<uint4*>(q + ((int64_t)i * p.ldx + tt) * lq + vb * kOzRecord);
+      uint4* dst = reinterpret_cast<uint4*>(q + ((int64_t)i * p.ldx + tt) * lq + vb * rec);
       dst[k] = reinterpret_cast<const uint4*>(buf + r * kSplitLdw)[k];
     }
   }
@@ -176,9 +186,11 @@ struct OzBars {
   uint64_t accfree;
 };
 
+template <int NSL>
 __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant__ CUtensorMap tmq,
                                                            const int32_t* __restrict__ expo, double* __restrict__ G,
                                                            int64_t ldx, const OzItem* __restrict__ items) {
+  constexpr int nsl = NSL;  // compile time: the MMA issue loops unroll
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ OzBars bars;
@@ -217,15 +229,17 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
           for (int vb = b0; vb < b1; ++vb, ++k) {
             const int slot = k % kOzStages;
             if (k >= kOzStages) mbar_wait(&bars.empty[slot], ((k / kOzStages) - 1) & 1);
-            const int nbox = (pass ? 2 : 1) * (diag ? 1 : 2);
+            // slices 4..6 (the records' high halves) only for pass 2 of seven-slice data
+            const bool hi = pass && nsl > 4;
+            const int nbox = (hi ? 2 : 1) * (diag ? 1 : 2);
             mbar_expect_tx(&bars.full[slot], (uint32_t)(nbox * kOzBox));
             unsigned char* st = smem + slot * kOzStageBytes;
-            const int x = vb * 256;
+            const int x = vb * oz_record_bytes(nsl);
             tma_load_3d(st, &tmq, x, it.m0, it.subj, &bars.full[slot]);
-            if (pass) tma_load_3d(st + kOzBox, &tmq, x + 128, it.m0, it.subj, &bars.full[slot]);
+            if (hi) tma_load_3d(st + kOzBox, &tmq, x + 128, it.m0, it.subj, &bars.full[slot]);
             if (!diag) {
               tma_load_3d(st + 2 * kOzBox, &tmq, x, it.n0, it.subj, &bars.full[slot]);
-              if (pass) tma_load_3d(st + 3 * kOzBox, &tmq, x + 128, it.n0, it.subj, &bars.full[slot]);
+              if (hi) tma_load_3d(st + 3 * kOzBox, &tmq, x + 128, it.n0, it.subj, &bars.full[slot]);
             }
           }
         }
@@ -252,7 +266,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
             const int dlo = pass ? 4 : 0, dhi = pass ? kOzSlices - 1 : 3;
             for (int d = dlo; d <= dhi; ++d) {
               const uint32_t acc = tmem + 128u * (uint32_t)(d - dlo);
-              const int s0 = max(0, d - (kOzSlices - 1)), s1 = min(d, kOzSlices - 1);
+              const int s0 = max(0, d - (nsl - 1)), s1 = min(d, nsl - 1);
               for (int s = s0; s <= s1; ++s) {
                 const int s2 = d - s;
                 const uint64_t da = umma_desc_sw128(sa + (s >> 2) * kOzBox + 32 * (s & 3));
@@ -372,7 +386,6 @@ __global__ void __launch_bounds__(256) k_oz_slice_rows(const double* __restrict_
 constexpr int kSgStages = 4;  // one CTA per SM: the seven accumulators take all 512 TMEM columns
 constexpr int kSgBoxS = 8192;                     // 64 rows x 128 B
 constexpr int kSgStageBytes = 2 * kOzBox + 2 * kSgBoxS;
-constexpr int kRowWABytes = 7 * 4 * 32 * 32;  // kRowW A operand per stage: 7 slots x 4 voxel blocks x 32 TRs x 32 B
 enum RowGemmMode { kRowSG = 0, kRowW = 1 };
 
 struct RowGemmArgs {
@@ -383,7 +396,9 @@ struct RowGemmArgs {
   int64_t ldx, kp, ldo, K;
 };
 
-template <int MODE>
+// NSA: slices of the A operand (kRowW: X-hat's 7 or 4; kRowSG: G's 7).
+// blockIdx.z selects the 64-feature half of N (kp <= 128).
+template <int MODE, int NSA>
 __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_constant__ CUtensorMap tma,
                                                               const __grid_constant__ CUtensorMap tmb,
                                                               RowGemmArgs g) {
@@ -399,6 +414,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
   const int arow = MODE == kRowSG ? t0 : it.n0;  // first A row (TR of G_i / global voxel row)
   const int az = MODE == kRowSG ? i : 0;
   const int bz = MODE == kRowSG ? 0 : i;
+  const int f0 = blockIdx.z * 64;  // first feature of this CTA's N = 64 columns
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nub = (int)(ldx / 32);
   if (warp == 0) {
@@ -429,12 +445,12 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
           tma_load_3d(st, &tma, x, arow, az, &full[slot]);
           tma_load_3d(st + kOzBox, &tma, x + 128, arow, az, &full[slot]);
         } else {
-          // Q records of 32 TRs x 4 voxel blocks x 7 slots -> [slot][vb][t][32 B]
-          mbar_expect_tx(&full[slot], (uint32_t)(kRowWABytes + 2 * kSgBoxS));
+          // Q records of 32 TRs x 4 voxel blocks x nsa slots -> [slot][vb][t][32 B]
+          mbar_expect_tx(&full[slot], (uint32_t)(NSA * 4096 + 2 * kSgBoxS));
           tma_load_5d(st, &tma, 0, k * 32, it.m0 / 32, 0, i, &full[slot]);
         }
-        tma_load_3d(st + 2 * kOzBox, &tmb, x, 0, bz, &full[slot]);
-        tma_load_3d(st + 2 * kOzBox + kSgBoxS, &tmb, x + 128, 0, bz, &full[slot]);
+        tma_load_3d(st + 2 * kOzBox, &tmb, x, f0, bz, &full[slot]);
+        tma_load_3d(st + 2 * kOzBox + kSgBoxS, &tmb, x + 128, f0, bz, &full[slot]);
       }
     }
   } else if (warp == 1) {
@@ -449,7 +465,8 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
         const uint32_t sb = sa + 2 * kOzBox;
         for (int d = 0; d < kOzSlices; ++d) {
           const uint32_t acc = tmem + 64u * (uint32_t)d;
-          for (int s = 0; s <= d; ++s) {
+          const int s1 = min(d, NSA - 1);
+          for (int s = 0; s <= s1; ++s) {
             const int s2 = d - s;
             const uint64_t da = MODE == kRowSG ? umma_desc_sw128(sa + (s >> 2) * kOzBox + 32 * (s & 3))
                                                : umma_desc_sw32_mn(sa + s * 4096, 1024, 256);
@@ -494,16 +511,19 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
       if (valid) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int f = c0 + j;
-          if (f < fmax_) out[(int64_t)f * fstride] = val[j] * pow2(et + bexp[f] + half);
+          const int f = f0 + c0 + j;
+          if (f < fmax_)
+            out[(int64_t)(MODE == kRowSG ? f : c0 + j) * fstride] = val[j] * pow2(et + bexp[f] + half);
         }
       }
     }
     if (MODE == kRowW) {
       asm volatile("bar.sync 1, 128;" ::: "memory");  // the four epilogue warps
       const int K = (int)g.K;
-      double* dst = g.out + (int64_t)it.n0 * K;
-      for (int e = (warp - 2) * 32 + lane; e < it.nvb * K; e += 128) dst[e] = wst[(e / K) * kWPitch + e % K];
+      const int nc = min(64, K - f0);  // this CTA's columns f0 .. f0 + nc - 1 of W
+      double* dst = g.out + (int64_t)it.n0 * K + f0;
+      for (int e = (warp - 2) * 32 + lane; e < it.nvb * nc; e += 128)
+        dst[(int64_t)(e / nc) * K + e % nc] = wst[(e / nc) * kWPitch + e % nc];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -541,19 +561,21 @@ cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int
 
 namespace {
 
-template <int MODE>
+template <int MODE, int NSA>
 cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, const RowGemmArgs& g, dim3 grid, cudaStream_t st) {
   const size_t bytes = (size_t)kSgStages * kSgStageBytes + 1024;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_oz_rowgemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_oz_rowgemm<MODE, NSA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   if (grid.x == 0 || grid.y == 0) return cudaSuccess;
-  if (g.kp > 64 || g.ldx % 32 != 0) return cudaErrorInvalidValue;
-  k_oz_rowgemm<MODE><<<grid, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(ta.opaque),
-                                                        *reinterpret_cast<const CUtensorMap*>(tb.opaque), g);
+  if (g.kp > 128 || g.ldx % 32 != 0) return cudaErrorInvalidValue;
+  grid.z = (unsigned)((g.kp + 63) / 64);  // 64-feature halves of N
+  k_oz_rowgemm<MODE, NSA><<<grid, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(ta.opaque),
+                                                             *reinterpret_cast<const CUtensorMap*>(tb.opaque), g);
   return cudaGetLastError();
 }
 
@@ -562,7 +584,7 @@ cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, const RowGemmArgs& g
 cudaError_t launch_oz_sg(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
                          double* bred, int64_t ldx, int64_t kp, int64_t ldo, int n_local, cudaStream_t st) {
   RowGemmArgs g{gexp, sexp, bred, nullptr, ldx, kp, ldo, 0};
-  return run_rowgemm<kRowSG>(tmg, tms, g, dim3((unsigned)((ldx + 127) / 128), (unsigned)n_local), st);
+  return run_rowgemm<kRowSG, kOzSlices>(tmg, tms, g, dim3((unsigned)((ldx + 127) / 128), (unsigned)n_local), st);
 }
 
 cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* expo, double* rt, int64_t ldx,
@@ -574,41 +596,65 @@ cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* exp
 }
 
 cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* rexp, double* W, const OzItem* items,
-                        int n_items, int64_t ldx, int64_t kp, int64_t K, cudaStream_t st) {
+                        int n_items, int64_t ldx, int64_t kp, int64_t K, int nsl, cudaStream_t st) {
   RowGemmArgs g{nullptr, rexp, W, items, ldx, kp, 0, K};
-  return run_rowgemm<kRowW>(tmqt, tmr, g, dim3((unsigned)n_items, 1), st);
+  if (nsl == 7) return run_rowgemm<kRowW, 7>(tmqt, tmr, g, dim3((unsigned)n_items, 1), st);
+  if (nsl == 4) return run_rowgemm<kRowW, 4>(tmqt, tmr, g, dim3((unsigned)n_items, 1), st);
+  return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_oz_prepare(const DevPlan& p, int first, int count, unsigned long long* cmax, int8_t* q,
-                              int64_t lq, int32_t* expo, int64_t max_v, cudaStream_t st) {
+cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first, int count,
+                              unsigned long long* cmax, int8_t* q, int64_t lq, int32_t* expo, int64_t max_v,
+                              cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
+  // seven slices for fp64 X-hat, four for fp32 (the instantiated pairs)
+  if (nsl != (x_dtype == SRM_F64 ? 7 : 4)) return cudaErrorInvalidValue;
   DevPlan sub = p;
   sub.subj = p.subj + (int64_t)first * kSubjCols;
   cudaError_t e = cudaMemsetAsync(cmax + (int64_t)first * p.ldx, 0, (size_t)count * p.ldx * sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
+  unsigned long long* cm = cmax + (int64_t)first * p.ldx;
+  int8_t* qs = q + (int64_t)first * p.ldx * lq;
+  int32_t* ex = expo + (int64_t)first * p.ldx;
   const dim3 g1((unsigned)((max_v + kColmaxRows - 1) / kColmaxRows), (unsigned)count);
-  k_oz_colmax<<<g1, 256, 0, st>>>(sub, static_cast<const double*>(p.xhat), cmax + (int64_t)first * p.ldx);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
   const dim3 g2((unsigned)((max_v + 31) / 32), (unsigned)((p.ldx + 127) / 128), (unsigned)count);
-  k_oz_split<<<g2, 256, 0, st>>>(sub, static_cast<const double*>(p.xhat), cmax + (int64_t)first * p.ldx,
-                                 q + (int64_t)first * p.ldx * lq, lq, expo + (int64_t)first * p.ldx);
+  if (x_dtype == SRM_F64) {
+    const double* x = static_cast<const double*>(p.xhat);
+    k_oz_colmax<double><<<g1, 256, 0, st>>>(sub, x, cm);
+    k_oz_split<double, 7><<<g2, 256, 0, st>>>(sub, x, cm, qs, lq, ex);
+  } else {
+    const float* x = static_cast<const float*>(p.xhat);
+    k_oz_colmax<float><<<g1, 256, 0, st>>>(sub, x, cm);
+    k_oz_split<float, 4><<<g2, 256, 0, st>>>(sub, x, cm, qs, lq, ex);
+  }
   return cudaGetLastError();
 }
 
-cudaError_t launch_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
-                           int n_items, cudaStream_t st) {
+namespace {
+
+template <int NSL>
+cudaError_t run_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
+                        int n_items, cudaStream_t st) {
   const size_t bytes = oz_gram_smem_bytes();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_oz_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaError_t e = cudaFuncSetAttribute(k_oz_gram<NSL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   if (n_items == 0) return cudaSuccess;
-  k_oz_gram<<<n_items, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(tmq.opaque), expo, G, ldx,
-                                                 items);
+  k_oz_gram<NSL><<<n_items, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(tmq.opaque), expo, G,
+                                                      ldx, items);
   return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
+                           int n_items, int nsl, cudaStream_t st) {
+  if (nsl == 7) return run_oz_gram<7>(tmq, expo, G, ldx, items, n_items, st);
+  if (nsl == 4) return run_oz_gram<4>(tmq, expo, G, ldx, items, n_items, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace srm

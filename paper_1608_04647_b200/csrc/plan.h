@@ -36,6 +36,7 @@ struct DevPlan {
   int n_local, n_total, n_order;
   int sub0, nsub;  // subject window [sub0, sub0 + nsub) of the per-subject kernels (default: all)
   int flags;
+  int xf32;  // X-hat stored in fp32 (per-iteration polar may run in fp32; the final one is exact)
   int64_t T, K, ldx, kp, ldo;
   int ntile_apply;  // kApplyCols-column tiles of ldx
   int ntile_tail;   // 32-column tiles of ldx
@@ -99,8 +100,9 @@ cudaError_t launch_tail_sigma(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_mirror_gram(const DevPlan& p, int first, int count, cudaStream_t s);
 // int8-sliced Gram (ozaki.cu): column maxima, exponents and slices of local
 // subjects [first, first + count)
-cudaError_t launch_oz_prepare(const DevPlan& p, int first, int count, unsigned long long* cmax, int8_t* q,
-                              int64_t lq, int32_t* expo, int64_t max_v, cudaStream_t st);
+cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first, int count,
+                              unsigned long long* cmax, int8_t* q, int64_t lq, int32_t* expo, int64_t max_v,
+                              cudaStream_t st);
 cudaError_t launch_reset(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_apply_w(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);
 cudaError_t launch_apply_w_f32(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);

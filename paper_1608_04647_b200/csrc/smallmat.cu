@@ -1108,7 +1108,9 @@ cudaError_t launch_reduce_chunks(const DevPlan& p, cudaStream_t s) {
 
 cudaError_t launch_eig_polar(const DevPlan& p, int init, cudaStream_t s) {
   if (ns_polar_supported((int)p.kp)) return launch_ns_polar(p, init, s);
-  if ((p.flags & SRM_FLAG_TC) && ns_polar_f32_supported((int)p.kp)) return launch_ns_polar_f32(p, init, s);
+  // fp32 X-hat (1e-4 tolerance): fp32 Newton-Schulz where fp64 does not fit;
+  // srm_finalize recomputes the last transform exactly
+  if (p.xf32 && ns_polar_f32_supported((int)p.kp)) return launch_ns_polar_f32(p, init, s);
   return launch_eig_polar_exact(p, init, s);
 }
 

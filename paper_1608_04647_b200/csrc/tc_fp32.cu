@@ -488,12 +488,13 @@ cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, 
 // strides) and box {32, 32, 4, 7, 1}, SWIZZLE_32B: one load lands as
 // [slot][vb][t][32 B], per slot the MN-major operand of 128 voxels x 32 TRs
 // (layout verified by tools/tma5d_probe.cu)
-cudaError_t make_map_q5(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, int64_t n) {
+cudaError_t make_map_q5(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, int64_t n, int nsl) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
-  cuuint64_t dims[5] = {32, (cuuint64_t)ldx, (cuuint64_t)(lq / 256), 8, (cuuint64_t)n};
-  cuuint64_t strides[4] = {(cuuint64_t)lq, 256, 32, (cuuint64_t)(lq * ldx)};
-  cuuint32_t box[5] = {32, 32, 4, 7, 1};
+  const int rec = oz_record_bytes(nsl);
+  cuuint64_t dims[5] = {32, (cuuint64_t)ldx, (cuuint64_t)(lq / rec), (cuuint64_t)(rec / 32), (cuuint64_t)n};
+  cuuint64_t strides[4] = {(cuuint64_t)lq, (cuuint64_t)rec, 32, (cuuint64_t)(lq * ldx)};
+  cuuint32_t box[5] = {32, 32, 4, (cuuint32_t)nsl, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult r = fn(reinterpret_cast<CUtensorMap*>(m->opaque), CU_TENSOR_MAP_DATA_TYPE_UINT8, 5,
                   const_cast<int8_t*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -346,14 +346,15 @@ _DMMA_FLOPS = 30e12
 _HBM_BYTES = 6.0e12
 _TF32_FLOPS = 0.9e15
 _I8_OPS = 3.2e15       # int8 tcgen05 (dense 4.5e15 nominal), as sustained by the sliced Gram
-_I8_PRODUCTS = 28      # slice pairs s + s' < 7 of the int8-sliced Gram
+_I8_PRODUCTS = {"f64": 28, "f32": 16}  # slice pairs of the int8-sliced Gram: 7 or 4 slices per value
 
 
-def gram_int8_bytes(n_voxels, n_trs):
-    """Device bytes of the int8 slices of the Gram path: TR-major records (256 B
-    per TR and 32 voxels) for X^T X and the row slices of every G_i."""
+def gram_int8_bytes(n_voxels, n_trs, storage="f64"):
+    """Device bytes of the int8 slices of the Gram path: TR-major records per
+    TR and 32 voxels (256 B for fp64's seven slices, 128 B for fp32's four)
+    for X^T X and the row slices of every G_i."""
     ldx = -(-n_trs // 32) * 32
-    lq = -(-max(n_voxels) // 32) * 256
+    lq = -(-max(n_voxels) // 32) * (256 if storage == "f64" else 128)
     return len(n_voxels) * ldx * (lq + 12) + len(n_voxels) * ldx * ldx * 8
 
 
@@ -363,9 +364,10 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f
     stream: per iteration two passes over X-hat (A = X S^T / 2, B = A^T X):
             4 V T K flops per subject on the FP64 tensor pipe, or -- for fp32
             X-hat on the tcgen05 3xTF32 path -- max(HBM time of 2 reads, MMA time).
-    gram:   one-time X^T X (upper 128-tiles, V T^2 flops on DMMA, or 28 int8
-            slice products plus three HBM passes with ``gram_int8``), then
-            2 K T^2 per subject-iteration for B = S G / 2, plus one final A pass.
+    gram:   one-time X^T X (upper 128-tiles, V T^2 flops on DMMA, or 28 / 16
+            int8 slice products for fp64 / fp32 plus the slicing passes with
+            ``gram_int8``), then 2 K T^2 per subject-iteration for B = S G / 2
+            (a read of G's slices on the int8 path), plus one final W pass.
     """
     kp = -(-k // 8) * 8
     ldx = -(-n_trs // 32) * 32
@@ -384,11 +386,17 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f
             stream += iterations * 2 * (2.0 * v * ldx * kp) / _DMMA_FLOPS
             final_a = 2.0 * v * ldx * kp / _DMMA_FLOPS
         tiles = nt * (nt + 1) / 2 * 128 * 128 * 2.0 * v
+        per_iter = 2.0 * kp * ldx * ldx / _DMMA_FLOPS
         if gram_int8:
-            one_time = _I8_PRODUCTS * tiles / _I8_OPS + 3.0 * v * ldx * b / _HBM_BYTES
+            products = _I8_PRODUCTS[storage]
+            slice_bytes = v * ldx * (8 if storage == "f64" else 4)
+            one_time = products * tiles / _I8_OPS + (2.0 * v * ldx * b + slice_bytes) / _HBM_BYTES
+            if kp <= 64:  # B = S G / 2 and the final W on int8 slices too
+                per_iter = 8.0 * ldx * ldx / _HBM_BYTES
+                final_a = max(slice_bytes / _HBM_BYTES, products * 2.0 * v * ldx * 64 / _I8_OPS)
         else:
             one_time = tiles / _DMMA_FLOPS
-        gram += one_time + iterations * 2.0 * kp * ldx * ldx / _DMMA_FLOPS + final_a
+        gram += one_time + iterations * per_iter + final_a
     need = len(n_voxels) * ldx * ldx * 8
     if free_bytes is not None and need > 0.25 * free_bytes:
         return "stream"
@@ -453,12 +461,12 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
 
     n_vox = [int(s.X.shape[0]) for s in subjects]
     store = _storage_for(subjects, storage)
-    use_i8 = bool(gram_int8) and store == "f64"
+    use_i8 = bool(gram_int8)
     if use_i8 or algorithm == "auto":
         torch = _torch()
         free, _ = torch.cuda.mem_get_info(device)
-        x_bytes = sum(n_vox) * (-(-n_trs // 32) * 32) * 8
-        use_i8 = use_i8 and gram_int8_bytes(n_vox, n_trs) + x_bytes < 0.6 * free
+        x_bytes = sum(n_vox) * (-(-n_trs // 32) * 32) * (8 if store == "f64" else 4)
+        use_i8 = use_i8 and gram_int8_bytes(n_vox, n_trs, store) + x_bytes < 0.6 * free
     if algorithm == "auto":
         algorithm = choose_algorithm(n_vox, n_trs, k, config.iterations, free,
                                      storage=store if tensor_cores else "f64", gram_int8=use_i8)

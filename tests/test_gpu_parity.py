@@ -328,3 +328,33 @@ def test_int8_gram_large_k_falls_back(srm):
     assert engines[-1].gram_i8
     r = ref["iters"][-1]
     _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, "gram i8 k=72")
+
+
+def test_int8_gram_fp32_four_slices(srm):
+    """fp32 X-hat on the int8 Gram path: 4 slices per value (2^-27 of the column max)."""
+    from paper_1608_04647_b200 import _lib
+    from paper_1608_04647_b200.data import recipe_numpy
+    from paper_1608_04647_b200.engine import SrmEngine
+    import torch
+
+    xs, _, _ = recipe_numpy(3, 3000, 300, 20, seed=8, dtype="f32")
+    eng = SrmEngine([x.shape[0] for x in xs], 300, 20, 1, storage="f32", gram=True, gram_i8=True)
+    assert eng.gram_i8 and not eng.tc
+    eng.load(xs)
+    eng.prepare_gram()
+    torch.cuda.synchronize()
+    eng.raise_status()
+    g = eng.region(_lib.R_GRAM, torch.float64).view(3, eng.ldx, eng.ldx)[:, :300, :300].cpu().numpy()
+    xh = [eng.xhat[eng.subject_rows(i)][:, :300].double().cpu().numpy() for i in range(3)]
+    eng.close()
+    for i in range(3):
+        ref = xh[i].T @ xh[i]
+        assert nrel(g[i], ref) <= 1e-6, (i, nrel(g[i], ref))
+    # and a full fit at the fp32 tolerance
+    ref = orc.run_em(xs, 20, 4, seed=1)
+    engines = []
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=20, iterations=4, seed=1), algorithm="gram",
+                engine_out=engines)
+    assert engines[-1].gram_i8
+    r = ref["iters"][-1]
+    _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL32, "gram i8 fp32")
