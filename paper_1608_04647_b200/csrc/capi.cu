@@ -427,6 +427,7 @@ void set_pointers(srm_plan* p) {
   d.part = region<double>(p, I_PART);
   d.bred = region<double>(p, I_BRED);
   d.gfb_part = region<double>(p, I_GFBPART);
+  d.cmax = (p->flags & SRM_FLAG_GRAM_I8) ? region<unsigned long long>(p, I_OZCMAX) : nullptr;
   d.gfb_count = region<int32_t>(p, I_GFBCOUNT);
   d.mmat = region<double>(p, SRM_R_MMAT);
   d.qmat = region<double>(p, I_QMAT);

@@ -19,11 +19,11 @@
 // data with column max/rms ~ 5 (BASELINE recipe).  The fp64 result then feeds
 // the same per-iteration B = S G / 2 as the fp64 DMMA Gram.
 //
-// Kernels:
-//   oz_colmax  max |x| per (subject, column) (bit pattern atomicMax)
+// Kernels (the column maxima max |x[:, t]| come from the demean pass, k_prep):
 //   oz_split   slices, transposed: Q[i][t][vb][slot][32 voxels] (int8; a
 //              256-byte record per (t, 32-voxel block): slices 0-3 in the low
-//              128 bytes, 4-6 (+ a zero slot) in the high 128 bytes)
+//              128 bytes, 4-6 (+ a zero slot) in the high 128 bytes; fp32
+//              X-hat: four slices in 128-byte records)
 //   oz_gram    one 128 x 128 upper tile per CTA: TMA (SWIZZLE_128B, 128-byte
 //              rows) -> tcgen05.mma kind::i8 (M = N = 128, K = 32 voxels; the
 //              slice is selected by the 32-byte descriptor advance) -> four
@@ -60,36 +60,6 @@ __device__ __forceinline__ int frexp_exp(double m) {
   int e = 0;
   frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
   return e;
-}
-
-// ---------------------------------------------------------------------------
-// column maxima: grid (row blocks, subjects), one thread per column
-// ---------------------------------------------------------------------------
-constexpr int kColmaxRows = 256;
-
-template <typename TX>
-__global__ void __launch_bounds__(256) k_oz_colmax(DevPlan p, const TX* __restrict__ xhat,
-                                                   unsigned long long* __restrict__ cmax) {
-  const int i = blockIdx.y;
-  const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
-  const int64_t row0 = sj[SC_ROW_OFF], V = sj[SC_V];
-  const int64_t r0 = (int64_t)blockIdx.x * kColmaxRows;
-  if (r0 >= V) return;
-  const int64_t r1 = min(V, r0 + kColmaxRows);
-  for (int64_t t = threadIdx.x; t < p.ldx; t += blockDim.x) {
-    const TX* x = xhat + (row0 + r0) * p.ldx + t;
-    double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
-    int64_t r = r0;
-    for (; r + 4 <= r1; r += 4, x += 4 * p.ldx) {
-      m0 = fmax(m0, fabs(to_f64(x[0])));
-      m1 = fmax(m1, fabs(to_f64(x[p.ldx])));
-      m2 = fmax(m2, fabs(to_f64(x[2 * p.ldx])));
-      m3 = fmax(m3, fabs(to_f64(x[3 * p.ldx])));
-    }
-    for (; r < r1; ++r, x += p.ldx) m0 = fmax(m0, fabs(to_f64(x[0])));
-    const double m = fmax(fmax(m0, m1), fmax(m2, m3));
-    if (m > 0.0) atomicMax(cmax + (int64_t)i * p.ldx + t, (unsigned long long)__double_as_longlong(m));
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -611,22 +581,15 @@ cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first,
   if (nsl != (x_dtype == SRM_F64 ? 7 : 4)) return cudaErrorInvalidValue;
   DevPlan sub = p;
   sub.subj = p.subj + (int64_t)first * kSubjCols;
-  cudaError_t e = cudaMemsetAsync(cmax + (int64_t)first * p.ldx, 0, (size_t)count * p.ldx * sizeof(unsigned long long), st);
-  if (e != cudaSuccess) return e;
-  unsigned long long* cm = cmax + (int64_t)first * p.ldx;
+  // column maxima: kept by the demean pass (k_prep) as each subject loads
+  const unsigned long long* cm = cmax + (int64_t)first * p.ldx;
   int8_t* qs = q + (int64_t)first * p.ldx * lq;
   int32_t* ex = expo + (int64_t)first * p.ldx;
-  const dim3 g1((unsigned)((max_v + kColmaxRows - 1) / kColmaxRows), (unsigned)count);
   const dim3 g2((unsigned)((max_v + 31) / 32), (unsigned)((p.ldx + 127) / 128), (unsigned)count);
-  if (x_dtype == SRM_F64) {
-    const double* x = static_cast<const double*>(p.xhat);
-    k_oz_colmax<double><<<g1, 256, 0, st>>>(sub, x, cm);
-    k_oz_split<double, 7><<<g2, 256, 0, st>>>(sub, x, cm, qs, lq, ex);
-  } else {
-    const float* x = static_cast<const float*>(p.xhat);
-    k_oz_colmax<float><<<g1, 256, 0, st>>>(sub, x, cm);
-    k_oz_split<float, 4><<<g2, 256, 0, st>>>(sub, x, cm, qs, lq, ex);
-  }
+  if (x_dtype == SRM_F64)
+    k_oz_split<double, 7><<<g2, 256, 0, st>>>(sub, static_cast<const double*>(p.xhat), cm, qs, lq, ex);
+  else
+    k_oz_split<float, 4><<<g2, 256, 0, st>>>(sub, static_cast<const float*>(p.xhat), cm, qs, lq, ex);
   return cudaGetLastError();
 }
 

@@ -47,6 +47,7 @@ struct DevPlan {
   double* wout;
   double* mu;
   double* rowsq;
+  unsigned long long* cmax;  // [n_local][ldx] max |Xhat[:, t]| as IEEE bits (int8 Gram path; else null)
   double* terms;
   double* red;
   double* redlocal;

@@ -38,41 +38,65 @@ __device__ __forceinline__ bool failed(const DevPlan& p) { return p.status[0] !=
 // ---------------------------------------------------------------------------
 // prep: one warp per voxel row
 // ---------------------------------------------------------------------------
+// One warp per voxel row, kPrepRows rows per CTA.  On the int8 Gram path
+// (p.cmax) the pass also keeps the per-column maxima of the stored |Xhat|
+// (the slice exponents, like rowsq a statistic of the demeaned data):
+// shared-memory atomics, then one global atomic per column per CTA.
+constexpr int kPrepRows = 32;
+
 template <typename TIN, typename TOUT>
 __global__ void __launch_bounds__(kSmallThreads) k_prep(DevPlan p, int local, const TIN* __restrict__ x,
                                                         int64_t ld) {
+  extern __shared__ unsigned long long cmax_s[];  // [ldx] when p.cmax
   const int64_t* sj = p.subj + (int64_t)local * kSubjCols;
   const int64_t row0 = sj[SC_ROW_OFF];
   const int64_t V = sj[SC_V];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (kSmallThreads / 32) + warp;
-  if (row >= V) return;
-  const TIN* xr = x + row * ld;
-  double s = 0.0;
-  bool finite = true;
-  for (int64_t t = lane; t < p.T; t += 32) {
-    const double v = to_f64(xr[t]);
-    finite &= isfinite(v);
-    s += v;
+  const bool track = p.cmax != nullptr;
+  if (track) {
+    for (int64_t t = threadIdx.x; t < p.ldx; t += blockDim.x) cmax_s[t] = 0ull;
+    __syncthreads();
   }
-  s = warp_sum(s);
-  const bool all_finite = __all_sync(0xffffffffu, finite);
-  if (!all_finite && lane == 0) raise_status(p.status, SRM_ERR_INVALID_INPUT, (int)sj[SC_GLOBAL], -1);
-  const double mean = s / (double)p.T;
-  TOUT* out = static_cast<TOUT*>(p.xhat) + (row0 + row) * p.ldx;
-  double sq = 0.0;
-  for (int64_t t = lane; t < p.ldx; t += 32) {
-    double v = 0.0;
-    if (t < p.T) {
-      v = to_f64(xr[t]) - mean;
-      sq += v * v;
+  for (int rr = 0; rr < kPrepRows / 8; ++rr) {
+    const int64_t row = (int64_t)blockIdx.x * kPrepRows + rr * 8 + warp;
+    if (row >= V) break;
+    const TIN* xr = x + row * ld;
+    double s = 0.0;
+    bool finite = true;
+    for (int64_t t = lane; t < p.T; t += 32) {
+      const double v = to_f64(xr[t]);
+      finite &= isfinite(v);
+      s += v;
     }
-    out[t] = static_cast<TOUT>(v);
+    s = warp_sum(s);
+    const bool all_finite = __all_sync(0xffffffffu, finite);
+    if (!all_finite && lane == 0) raise_status(p.status, SRM_ERR_INVALID_INPUT, (int)sj[SC_GLOBAL], -1);
+    const double mean = s / (double)p.T;
+    TOUT* out = static_cast<TOUT*>(p.xhat) + (row0 + row) * p.ldx;
+    double sq = 0.0;
+    for (int64_t t = lane; t < p.ldx; t += 32) {
+      double v = 0.0;
+      if (t < p.T) {
+        v = to_f64(xr[t]) - mean;
+        sq += v * v;
+      }
+      const TOUT stored = static_cast<TOUT>(v);
+      out[t] = stored;
+      if (track && t < p.T) {
+        const double a = fabs(to_f64(stored));
+        if (a > 0.0) atomicMax(cmax_s + t, (unsigned long long)__double_as_longlong(a));
+      }
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) {
+      p.mu[row0 + row] = mean;
+      p.rowsq[row0 + row] = sq;
+    }
   }
-  sq = warp_sum(sq);
-  if (lane == 0) {
-    p.mu[row0 + row] = mean;
-    p.rowsq[row0 + row] = sq;
+  if (track) {
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < p.ldx; t += blockDim.x)
+      if (cmax_s[t]) atomicMax(p.cmax + (int64_t)local * p.ldx + t, cmax_s[t]);
   }
 }
 
@@ -1081,16 +1105,25 @@ int max_supported_k() { return kMaxK; }
 
 cudaError_t launch_prep(const DevPlan& p, int local, int64_t V, const void* x, int x_dtype,
                         int64_t ld, int xhat_dtype, cudaStream_t s) {
-  const dim3 grid((unsigned)((V + 7) / 8));
+  const dim3 grid((unsigned)((V + kPrepRows - 1) / kPrepRows));
   if (V == 0) return cudaSuccess;
-  if (x_dtype == SRM_F64 && xhat_dtype == SRM_F64)
-    k_prep<double, double><<<grid, kSmallThreads, 0, s>>>(p, local, static_cast<const double*>(x), ld);
-  else if (x_dtype == SRM_F64 && xhat_dtype == SRM_F32)
-    k_prep<double, float><<<grid, kSmallThreads, 0, s>>>(p, local, static_cast<const double*>(x), ld);
-  else if (x_dtype == SRM_F32 && xhat_dtype == SRM_F32)
-    k_prep<float, float><<<grid, kSmallThreads, 0, s>>>(p, local, static_cast<const float*>(x), ld);
-  else
-    k_prep<float, double><<<grid, kSmallThreads, 0, s>>>(p, local, static_cast<const float*>(x), ld);
+  size_t smem = 0;
+  if (p.cmax) {  // fresh column maxima for this subject
+    cudaError_t e = cudaMemsetAsync(p.cmax + (int64_t)local * p.ldx, 0, (size_t)p.ldx * 8, s);
+    if (e != cudaSuccess) return e;
+    smem = (size_t)p.ldx * 8;
+  }
+  const void* fn = nullptr;
+  if (x_dtype == SRM_F64 && xhat_dtype == SRM_F64) fn = (const void*)k_prep<double, double>;
+  else if (x_dtype == SRM_F64 && xhat_dtype == SRM_F32) fn = (const void*)k_prep<double, float>;
+  else if (x_dtype == SRM_F32 && xhat_dtype == SRM_F32) fn = (const void*)k_prep<float, float>;
+  else fn = (const void*)k_prep<float, double>;
+  cudaError_t e = set_smem(fn, smem);
+  if (e != cudaSuccess) return e;
+  DevPlan arg = p;
+  void* args[] = {&arg, &local, &x, &ld};
+  e = cudaLaunchKernel(fn, grid, dim3(kSmallThreads), args, smem, s);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
