@@ -358,3 +358,21 @@ def test_int8_gram_fp32_four_slices(srm):
     assert engines[-1].gram_i8
     r = ref["iters"][-1]
     _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL32, "gram i8 fp32")
+
+
+def test_int8_gram_fp32_large_k_ragged(srm):
+    """fp32, K = 100 (two 64-feature halves, fp32 polar per iteration, exact final polar),
+    ragged V and T = 330 (partial 128-TR tiles) on the int8 Gram path."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(3, 2600, 330, 100, seed=23, dtype="f32")
+    xs = [x[: 2600 - 97 * i] for i, x in enumerate(xs)]
+    ref = orc.run_em(xs, 100, 3, seed=4)
+    engines = []
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=100, iterations=3, seed=4), algorithm="gram",
+                engine_out=engines)
+    assert engines[-1].gram_i8
+    r = ref["iters"][-1]
+    _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL32, "gram i8 fp32 k=100")
+    for w in m.W:  # the exact final polar: orthonormal to fp64 precision
+        assert np.max(np.abs(w.T @ w - np.eye(100))) <= 1e-8
