@@ -163,7 +163,7 @@ class SrmEngine:
             self._staging[key] = buf
         return buf[:numel]
 
-    def load(self, xs, gaussians=None, gram=False, init=False):
+    def load(self, xs, gaussians=None, gram=False, init=False, capture=False):
         """Upload (if needed) and demean every local subject (srm.py:238-240).
 
         Pipelined per subject: the host-to-device copy of subject j+1 (copy
@@ -172,7 +172,8 @@ class SrmEngine:
         futures of the init draws) are uploaded into the A region on the way;
         with ``init`` the initial mapping (srm.py:101-118) of each batch of
         subjects runs there too, so only the iteration counter remains
-        (:meth:`set_iteration`).
+        (:meth:`set_iteration`).  With ``capture`` the EM iteration graph is
+        recorded while the first subject uploads (:meth:`capture`).
         """
         torch = _torch()
         if len(xs) != self.n_local:
@@ -277,9 +278,12 @@ class SrmEngine:
                                "prepare_gram")
                 if init:
                     init_pending.append((first, j + 1, ev2))
+            if capture and j == 0:
+                self.capture()  # host-side work, overlapped with the first uploads
             if gaussians is not None:
-                # upload the init draws that are ready, never stalling the copy stream
-                next_g = upload_ready_draws(next_g, upto=j)
+                # upload the init draws that are ready; force only those eight
+                # subjects behind (the first draws take longer than an upload)
+                next_g = upload_ready_draws(next_g, upto=j - 8)
                 flush_init(next_g)
         if gaussians is not None:
             next_g = upload_ready_draws(next_g, upto=self.n_local)

@@ -493,7 +493,8 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     draws = [pool.submit(draw, j) for j in range(len(subjects))]
     clock.tick("setup")
     # pipelined: upload + demean (+ X^T X) (+ the initial mapping) per batch of subjects
-    eng.load([s.X for s in subjects], gaussians=draws, gram=True, init=init_overlap)
+    use_graph = graphs and comm.size == 1
+    eng.load([s.X for s in subjects], gaussians=draws, gram=True, init=init_overlap, capture=use_graph)
     pool.shutdown(wait=False)
     clock.tick("load")
     if init_overlap:
@@ -502,13 +503,10 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
         eng.init_kernels()
     clock.tick("init")
 
-    use_graph = graphs and comm.size == 1
     n_done = 0
     for it in range(config.iterations):
-        if use_graph and it == 1:
-            eng.capture()
-        if use_graph and it >= 1:
-            eng.replay()
+        if use_graph:
+            eng.replay()  # one EM iteration; the graph was captured during the upload
         else:
             eng.step(comm)
         n_done = it + 1
