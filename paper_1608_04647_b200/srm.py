@@ -405,7 +405,7 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f
 
 def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=True,
         keep_on_device=False, device=None, engine_out=None, timings=None, algorithm="auto",
-        tensor_cores=True, gram_int8=True, init_overlap=True):
+        tensor_cores=True, gram_int8=True, init_overlap=False):
     """Run the distributed EM; ``subjects`` are this worker's share (srm.py:216).
 
     Every worker calls this with the same config and its own communicator
@@ -431,8 +431,9 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     represented to ~2^-48 of the column maxima; ~1e-14 relative to G) when
     the slices fit in device memory; ``False`` keeps it on fp64 DMMA.
     ``init_overlap``: run the initial mapping (srm.py:101-118 after the draw)
-    batch by batch while later subjects are still uploading (default), or
-    once after the upload.
+    batch by batch while later subjects are still uploading, or (default)
+    once after the upload -- measured equal end to end on cfg 2, where the
+    draws of the last batches arrive after the upload anyway.
     """
     clock = _PhaseClock(timings)
     config.validate()
