@@ -376,3 +376,17 @@ def test_int8_gram_fp32_large_k_ragged(srm):
     _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL32, "gram i8 fp32 k=100")
     for w in m.W:  # the exact final polar: orthonormal to fp64 precision
         assert np.max(np.abs(w.T @ w - np.eye(100))) <= 1e-8
+
+
+def test_init_overlap_is_bit_identical(srm):
+    """The initial mapping run batch by batch during the upload == run once after it."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(9, 1200, 160, 12, seed=31)
+    cfg = srm.SrmConfig(k=12, iterations=3, seed=6)
+    for algorithm in ("gram", "stream"):
+        a = srm.fit(_subjects(srm, xs), cfg, algorithm=algorithm, init_overlap=True)
+        b = srm.fit(_subjects(srm, xs), cfg, algorithm=algorithm, init_overlap=False)
+        assert np.array_equal(a.S, b.S) and np.array_equal(a.sigma_s, b.sigma_s), algorithm
+        for wa, wb in zip(a.W, b.W):
+            assert np.array_equal(wa, wb), algorithm
