@@ -372,8 +372,9 @@ def run_ours(args):
         launch_ms = once[dom]
         alg_flops = float(n_local) * V * T * (T + 1)          # symmetric X^T X: T(T+1)/2 dots of length V
         alg_bytes = float(local_units * b)                      # X-hat read once
-        # int8 products issued by oz_gram: 28 slice pairs per upper 128 x 128 tile, 32-voxel blocks
-        products = 28 if cfg["dtype"] == "f64" else 16  # slice pairs: 7 or 4 slices per value
+        # int8 products issued by oz_gram per upper 128 x 128 tile and 32-voxel block: the slice
+        # pairs s + s' < 7 (28 for fp64's 7 slices; all 16 for fp32's 4)
+        products = 28 if cfg["dtype"] == "f64" else 16
         i8_ops = 2.0 * products * nt * (nt + 1) / 2 * 128 * 128 * (-(-V // 32) * 32) * n_local
     elif dom in ("final_a", "oz_w", "apply_w"):
         launch_ms = once[dom]

@@ -28,8 +28,9 @@
 //              rows) -> tcgen05.mma kind::i8 (M = N = 128, K = 32 voxels; the
 //              slice is selected by the 32-byte descriptor advance) -> four
 //              int32 accumulators in TMEM (512 columns).  Pass 1 accumulates
-//              d = 0..3 from the low halves, pass 2 d = 4..6 from both halves;
-//              the epilogue warps scale and sum the d-groups in fp64 in order.
+//              d = 0..3 from the low halves, pass 2 d = 4..6 from both halves
+//              (four-slice data: the low halves again, all 16 pairs); the
+//              epilogue warps scale and sum the d-groups in fp64 in order.
 #include <cuda.h>
 #include <math.h>
 
@@ -101,28 +102,51 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
     e = (m > 0.0) ? frexp_exp(m) : 0;
     if (vb == 0 && half == 0) expo[(int64_t)i * p.ldx + t] = e;
   }
-  // 2^(6 - e) exactly (normal range: |e| < 1000)
-  const double scale = __longlong_as_double((long long)(1023 + 6 - e) << 52);
-  double x[16];
+  TX xv[16];
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     const int64_t v = vb * 32 + half * 16 + u;
-    x[u] = (tin && v < V) ? to_f64(xhat[(row0 + v) * p.ldx + t]) : 0.0;
+    xv[u] = (tin && v < V) ? xhat[(row0 + v) * p.ldx + t] : TX(0);
   }
-  uint32_t w[kOzSlices][4];
+  uint32_t w[NSL][4];
 #pragma unroll
-  for (int s = 0; s < kOzSlices; ++s)
+  for (int s = 0; s < NSL; ++s)
 #pragma unroll
     for (int g = 0; g < 4; ++g) w[s][g] = 0u;
+  // y = x 2^(6 - e), |y| < 64; digit s = rint(y), then y = (y - rint(y)) * 128.
+  // Every step is exact in the input's own precision, so fp32 X-hat slices in
+  // fp32 arithmetic (twice the fp64 rate) with the same digits as in fp64.
+  bool done = false;
+  if constexpr (sizeof(TX) == 4) {
+    if (e >= -120 && e <= 130) {  // 2^(6 - e) is a normal float
+      const float scale = __int_as_float((127 + 6 - e) << 23);
+      const float magic = 12582912.0f;  // 1.5 * 2^23: rint for |y| < 2^22, low byte = digit
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    double y = x[u] * scale;  // |y| < 64
+      for (int u = 0; u < 16; ++u) {
+        float y = xv[u] * scale;
 #pragma unroll
-    for (int s = 0; s < kOzSlices; ++s) {
-      int low;
-      const double r = round_shift(y, &low);
-      w[s][u >> 2] |= (uint32_t)(low & 0xFF) << (8 * (u & 3));
-      y = (y - r) * 128.0;  // exact: |y - r| <= 1/2
+        for (int s = 0; s < NSL; ++s) {
+          const float tt = y + magic;
+          w[s][u >> 2] |= (uint32_t)(__float_as_int(tt) & 0xFF) << (8 * (u & 3));
+          y = (y - (tt - magic)) * 128.0f;
+        }
+      }
+      done = true;
+    }
+  }
+  if (!done) {
+    // 2^(6 - e) exactly (normal range: |e| < 1000)
+    const double scale = __longlong_as_double((long long)(1023 + 6 - e) << 52);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      double y = to_f64(xv[u]) * scale;  // |y| < 64
+#pragma unroll
+      for (int s = 0; s < NSL; ++s) {
+        int low;
+        const double r = round_shift(y, &low);
+        w[s][u >> 2] |= (uint32_t)(low & 0xFF) << (8 * (u & 3));
+        y = (y - r) * 128.0;  // exact: |y - r| <= 1/2
+      }
     }
   }
   // record layout per t: 16-byte chunk (slot * 2 + half); slots >= nsl stay zero
@@ -131,7 +155,7 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
 #pragma unroll
   for (int s = 0; s < 8; ++s)
     if (s < nslot)
-      row[s * 2 + half] = (s < nsl && s < kOzSlices) ? make_uint4(w[s][0], w[s][1], w[s][2], w[s][3])
+      row[s * 2 + half] = (s < nsl) ? make_uint4(w[s][0], w[s][1], w[s][2], w[s][3])
                                                       : make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
   // 128 rows x rec / 16 chunks of 16 bytes; consecutive threads write one record
@@ -161,6 +185,12 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
                                                            const int32_t* __restrict__ expo, double* __restrict__ G,
                                                            int64_t ldx, const OzItem* __restrict__ items) {
   constexpr int nsl = NSL;  // compile time: the MMA issue loops unroll
+  // d-groups 0..3 fill the 512 TMEM columns; pass 2 accumulates d = 4..6.
+  // Four-slice (fp32) data keeps all 16 pairs, so G = Xt^T Xt exactly for the
+  // sliced Xt: dropping the pairs s + s' >= 4 would bias the diagonal by
+  // ~2^-28 relative (the q_2^2 terms are all positive) and cost W^T W = I at
+  // the 1e-8 level.
+  constexpr int kPasses = 2;
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ OzBars bars;
@@ -195,7 +225,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
       int k = 0;
       for (int c = 0; c < nchunks; ++c) {
         const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int pass = 0; pass < kPasses; ++pass) {
           for (int vb = b0; vb < b1; ++vb, ++k) {
             const int slot = k % kOzStages;
             if (k >= kOzStages) mbar_wait(&bars.empty[slot], ((k / kOzStages) - 1) & 1);
@@ -222,7 +252,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
       int k = 0, npass = 0;
       for (int c = 0; c < nchunks; ++c) {
         const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
-        for (int pass = 0; pass < 2; ++pass, ++npass) {
+        for (int pass = 0; pass < kPasses; ++pass, ++npass) {
           // the epilogue must have drained the previous pass's accumulators
           if (npass > 0) mbar_wait(&bars.accfree, (npass - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
@@ -261,7 +291,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
     double* grow = G + (int64_t)it.subj * ldx * ldx + ta * ldx + it.n0;
     int npass = 0;
     for (int c = 0; c < nchunks; ++c) {
-      for (int pass = 0; pass < 2; ++pass, ++npass) {
+      for (int pass = 0; pass < kPasses; ++pass, ++npass) {
         mbar_wait(&bars.accfull, npass & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int dlo = pass ? 4 : 0, dhi = pass ? kOzSlices - 1 : 3;
@@ -353,10 +383,24 @@ __global__ void __launch_bounds__(256) k_oz_slice_rows(const double* __restrict_
 // B = the row slices of R'^T = (2^{e_t} R_i)^T (the column scales of Xhat
 // folded into R), so W[v][f] = 2^{r_f} sum_d 2^{-12-7d} (...)[v][f].
 // ---------------------------------------------------------------------------
-constexpr int kSgStages = 4;  // one CTA per SM: the seven accumulators take all 512 TMEM columns
-constexpr int kSgBoxS = 8192;                     // 64 rows x 128 B
-constexpr int kSgStageBytes = 2 * kOzBox + 2 * kSgBoxS;
+constexpr int kSgStages = 4;
+constexpr int kSgBoxS = 8192;  // 64 rows x 128 B
 enum RowGemmMode { kRowSG = 0, kRowW = 1 };
+
+// Per-stage shared memory of k_oz_rowgemm<MODE, NSA, ND>: the A boxes (kRowSG:
+// the G record halves holding the slices used; kRowW: NSA MN-major slices of
+// 128 voxels x 32 TRs) and the B record halves.  ND = 7 d-groups take 448 of
+// the 512 TMEM columns (one CTA per SM); ND = 4 (four-slice operands, pairs
+// s + s' >= 4 dropped) takes 256 and two CTAs share an SM.
+template <int MODE, int NSA, int ND>
+struct RowGemmShape {
+  static constexpr int halves = ND > 4 ? 2 : 1;
+  static constexpr int a_bytes = MODE == kRowSG ? halves * kOzBox : NSA * 4096;
+  static constexpr int stage_bytes = a_bytes + halves * kSgBoxS;
+  static constexpr uint32_t tmem_cols = ND > 4 ? 512 : 256;
+  static constexpr int ctas_per_sm = ND > 4 ? 1 : 2;
+  static constexpr size_t smem_bytes = (size_t)kSgStages * stage_bytes + 1024;
+};
 
 struct RowGemmArgs {
   const int32_t* aexp;   // kRowSG: G row exponents [n_local][ldx]
@@ -367,11 +411,14 @@ struct RowGemmArgs {
 };
 
 // NSA: slices of the A operand (kRowW: X-hat's 7 or 4; kRowSG: G's 7).
+// ND: d-groups kept (all 7 in the current uses; ND = 4 would keep only the
+// pairs s + s' < 4 and fit two CTAs per SM).
 // blockIdx.z selects the 64-feature half of N (kp <= 128).
-template <int MODE, int NSA>
-__global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_constant__ CUtensorMap tma,
-                                                              const __grid_constant__ CUtensorMap tmb,
-                                                              RowGemmArgs g) {
+template <int MODE, int NSA, int ND>
+__global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_per_sm)
+    k_oz_rowgemm(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, RowGemmArgs g) {
+  using Shape = RowGemmShape<MODE, NSA, ND>;
+  constexpr int kStage = Shape::stage_bytes;
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kSgStages], empty[kSgStages], accfull;
@@ -397,7 +444,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
       asm volatile("fence.mbarrier_init.release.cluster;");
     }
   } else if (warp == 1) {
-    tmem_alloc(&tmem_base, 512);
+    tmem_alloc(&tmem_base, Shape::tmem_cols);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -408,19 +455,18 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
       for (int k = 0; k < nub; ++k) {
         const int slot = k % kSgStages;
         if (k >= kSgStages) mbar_wait(&empty[slot], ((k / kSgStages) - 1) & 1);
-        unsigned char* st = smem + slot * kSgStageBytes;
+        unsigned char* st = smem + slot * kStage;
         const int x = k * 256;
+        mbar_expect_tx(&full[slot], (uint32_t)kStage);
         if (MODE == kRowSG) {
-          mbar_expect_tx(&full[slot], (uint32_t)kSgStageBytes);
           tma_load_3d(st, &tma, x, arow, az, &full[slot]);
-          tma_load_3d(st + kOzBox, &tma, x + 128, arow, az, &full[slot]);
+          if (Shape::halves > 1) tma_load_3d(st + kOzBox, &tma, x + 128, arow, az, &full[slot]);
         } else {
           // Q records of 32 TRs x 4 voxel blocks x nsa slots -> [slot][vb][t][32 B]
-          mbar_expect_tx(&full[slot], (uint32_t)(NSA * 4096 + 2 * kSgBoxS));
           tma_load_5d(st, &tma, 0, k * 32, it.m0 / 32, 0, i, &full[slot]);
         }
-        tma_load_3d(st + 2 * kOzBox, &tmb, x, f0, bz, &full[slot]);
-        tma_load_3d(st + 2 * kOzBox + kSgBoxS, &tmb, x + 128, f0, bz, &full[slot]);
+        tma_load_3d(st + Shape::a_bytes, &tmb, x, f0, bz, &full[slot]);
+        if (Shape::halves > 1) tma_load_3d(st + Shape::a_bytes + kSgBoxS, &tmb, x + 128, f0, bz, &full[slot]);
       }
     }
   } else if (warp == 1) {
@@ -431,11 +477,13 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
         const int slot = k % kSgStages;
         mbar_wait(&full[slot], (k / kSgStages) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t sa = smem_u32(smem + slot * kSgStageBytes);
-        const uint32_t sb = sa + 2 * kOzBox;
-        for (int d = 0; d < kOzSlices; ++d) {
+        const uint32_t sa = smem_u32(smem + slot * kStage);
+        const uint32_t sb = sa + Shape::a_bytes;
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
           const uint32_t acc = tmem + 64u * (uint32_t)d;
           const int s1 = min(d, NSA - 1);
+#pragma unroll
           for (int s = 0; s <= s1; ++s) {
             const int s2 = d - s;
             const uint64_t da = MODE == kRowSG ? umma_desc_sw128(sa + (s >> 2) * kOzBox + 32 * (s & 3))
@@ -470,7 +518,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
       double val[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) val[j] = 0.0;
-      for (int d = 0; d < kOzSlices; ++d) {
+      for (int d = 0; d < ND; ++d) {
         uint32_t raw[16];
         tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 64u * (uint32_t)d + c0, raw);
         tmem_wait_ld();
@@ -498,7 +546,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_rowgemm(const __grid_const
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 1) tmem_free(tmem, 512);
+  if (warp == 1) tmem_free(tmem, Shape::tmem_cols);
 }
 
 // R'^T[i][f][t] = 2^{e_t} (M_i^T S)[f][t] / 2 for the final W = Xhat R
@@ -531,20 +579,20 @@ cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int
 
 namespace {
 
-template <int MODE, int NSA>
+template <int MODE, int NSA, int ND>
 cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, const RowGemmArgs& g, dim3 grid, cudaStream_t st) {
-  const size_t bytes = (size_t)kSgStages * kSgStageBytes + 1024;
+  const size_t bytes = RowGemmShape<MODE, NSA, ND>::smem_bytes;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(k_oz_rowgemm<MODE, NSA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        cudaFuncSetAttribute(k_oz_rowgemm<MODE, NSA, ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   if (grid.x == 0 || grid.y == 0) return cudaSuccess;
   if (g.kp > 128 || g.ldx % 32 != 0) return cudaErrorInvalidValue;
   grid.z = (unsigned)((g.kp + 63) / 64);  // 64-feature halves of N
-  k_oz_rowgemm<MODE, NSA><<<grid, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(ta.opaque),
+  k_oz_rowgemm<MODE, NSA, ND><<<grid, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(ta.opaque),
                                                              *reinterpret_cast<const CUtensorMap*>(tb.opaque), g);
   return cudaGetLastError();
 }
@@ -554,7 +602,7 @@ cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, const RowGemmArgs& g
 cudaError_t launch_oz_sg(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
                          double* bred, int64_t ldx, int64_t kp, int64_t ldo, int n_local, cudaStream_t st) {
   RowGemmArgs g{gexp, sexp, bred, nullptr, ldx, kp, ldo, 0};
-  return run_rowgemm<kRowSG, kOzSlices>(tmg, tms, g, dim3((unsigned)((ldx + 127) / 128), (unsigned)n_local), st);
+  return run_rowgemm<kRowSG, kOzSlices, 7>(tmg, tms, g, dim3((unsigned)((ldx + 127) / 128), (unsigned)n_local), st);
 }
 
 cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* expo, double* rt, int64_t ldx,
@@ -568,8 +616,10 @@ cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* exp
 cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* rexp, double* W, const OzItem* items,
                         int n_items, int64_t ldx, int64_t kp, int64_t K, int nsl, cudaStream_t st) {
   RowGemmArgs g{nullptr, rexp, W, items, ldx, kp, 0, K};
-  if (nsl == 7) return run_rowgemm<kRowW, 7>(tmqt, tmr, g, dim3((unsigned)n_items, 1), st);
-  if (nsl == 4) return run_rowgemm<kRowW, 4>(tmqt, tmr, g, dim3((unsigned)n_items, 1), st);
+  if (nsl == 7) return run_rowgemm<kRowW, 7, 7>(tmqt, tmr, g, dim3((unsigned)n_items, 1), st);
+  // all seven d-groups for fp32 X-hat too: R's slices beyond the fourth carry
+  // bits the orthonormality of W needs (W^T W = I to ~1e-13)
+  if (nsl == 4) return run_rowgemm<kRowW, 4, 7>(tmqt, tmr, g, dim3((unsigned)n_items, 1), st);
   return cudaErrorInvalidValue;
 }
 

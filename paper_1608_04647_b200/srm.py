@@ -391,7 +391,7 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f
             products = _I8_PRODUCTS[storage]
             slice_bytes = v * ldx * (8 if storage == "f64" else 4)
             one_time = products * tiles / _I8_OPS + (2.0 * v * ldx * b + slice_bytes) / _HBM_BYTES
-            if kp <= 64:  # B = S G / 2 and the final W on int8 slices too
+            if kp <= 128:  # B = S G / 2 and the final W on int8 slices too
                 per_iter = 8.0 * ldx * ldx / _HBM_BYTES
                 final_a = max(slice_bytes / _HBM_BYTES, products * 2.0 * v * ldx * 64 / _I8_OPS)
         else:
