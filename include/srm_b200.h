@@ -185,12 +185,17 @@ int srm_reset(srm_plan* plan, void* stream);
  *   cross term and rho_i^2, and the next E-step term W_i^T X_i / rho_i^2
  *   (srm.py:151 and :118 share one product).
  * srm_finalize: materialise W_i = A_i M_i (model.W).
+ * srm_finalize_range: the same for local subjects [first, first + count);
+ *   calls must cover 0 .. n_local - 1 in ascending order, starting with
+ *   first = 0 (which runs the shared prelude).  Lets a caller read W_i of
+ *   earlier subjects back while later ones are formed (srm.py:315-327).
  */
 int srm_set_iteration(srm_plan* plan, int iteration, void* stream);
 int srm_reduce_local(srm_plan* plan, void* stream);
 int srm_e_step(srm_plan* plan, void* stream);
 int srm_m_step(srm_plan* plan, void* stream);
 int srm_finalize(srm_plan* plan, void* stream);
+int srm_finalize_range(srm_plan* plan, int first, int count, void* stream);
 
 /* one EM iteration as a CUDA graph: srm_graph_capture records
  * {srm_e_step, srm_m_step} once (single-rank plans; call after one eager

@@ -43,6 +43,7 @@ SIGNATURES = [
     ("srm_e_step", c_int, [c_vp, c_vp]),
     ("srm_m_step", c_int, [c_vp, c_vp]),
     ("srm_finalize", c_int, [c_vp, c_vp]),
+    ("srm_finalize_range", c_int, [c_vp, c_int, c_int, c_vp]),
     ("srm_graph_capture", c_int, [c_vp]),
     ("srm_graph_launch", c_int, [c_vp, c_vp]),
     ("srm_profile_iteration", c_int, [c_vp, ctypes.POINTER(ctypes.c_float), c_int, c_i32p, c_vp]),

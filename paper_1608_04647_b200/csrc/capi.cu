@@ -124,6 +124,7 @@ struct srm_plan {
   TmaMap tm_g, tm_sq;
   bool oz_w = false;                  // final W = Xhat R from the int8 slices (needs oz_sg)
   std::vector<OzItem> items_ow;       // 128-voxel tiles of the final int8 W = Xhat R
+  std::vector<int> ow_first;          // [n_local + 1]: first items_ow entry of each subject
   TmaMap tm_q32, tm_r;
 };
 
@@ -322,11 +323,13 @@ void build_work(srm_plan* p) {
   p->oz_lqg = p->ldx / 32 * kOzRecord;
   p->oz_w = p->oz_sg;
   p->items_ow.clear();
-  if (p->oz_w) {
-    for (int i = 0; i < p->n_local; ++i)
+  p->ow_first.assign(1, 0);
+  for (int i = 0; i < p->n_local; ++i) {
+    if (p->oz_w)
       for (int64_t v0 = 0; v0 < p->V[i]; v0 += 128)
         p->items_ow.push_back({i, (int32_t)v0, (int32_t)(p->row_off[i] + v0),
                                (int32_t)std::min<int64_t>(128, p->V[i] - v0)});
+    p->ow_first.push_back((int)p->items_ow.size());
   }
   if (p->flags & SRM_FLAG_GRAM_I8) {
     for (int i = 0; i < p->n_local; ++i)
@@ -558,10 +561,23 @@ std::vector<std::string> g_profile_names;
 // one-time Gram X_i^T X_i of local subjects [first, first + count): int8
 // slices on the tensor cores (SRM_FLAG_GRAM_I8) or fp64 DMMA tiles, then the
 // lower triangle mirrored from the upper one
-// model.W (srm.py:315-327): W_i = A_i M_i with M_i from the last M-step
-std::vector<Stage> finalize_stages(srm_plan* p) {
+// model.W (srm.py:315-327): W_i = A_i M_i with M_i from the last M-step, for
+// local subjects [first, first + count).  The shared prelude runs with the
+// range that starts at subject 0; only the int8 W = Xhat R is split by
+// subject (the other variants form every W_i in that first range).
+std::vector<Stage> finalize_stages(srm_plan* p, int first, int count) {
   const DevPlan& d = p->dp;
   std::vector<Stage> v;
+  if (p->oz_w && first > 0) {
+    const int i0 = p->ow_first[first], i1 = p->ow_first[first + count];
+    v.push_back({"oz_w", [p, d, i0, i1](cudaStream_t st) {
+                   return launch_oz_w(p->tm_q32, p->tm_r, region<int32_t>(p, I_OZREXP), d.wout,
+                                      region<OzItem>(p, I_ITEMS_OW) + i0, i1 - i0, p->ldx, p->kp, p->K,
+                                      p->oz_nsl, st);
+                 }});
+    return v;
+  }
+  if (first > 0) return v;
   if ((p->flags & SRM_FLAG_GRAM) && p->dtype == SRM_F32 && !ns_polar_supported((int)p->kp) &&
       ns_polar_f32_supported((int)p->kp)) {
     // the per-iteration polar ran in fp32 (K > 80): the returned W takes the
@@ -579,10 +595,10 @@ std::vector<Stage> finalize_stages(srm_plan* p) {
                    return launch_oz_slice_rows(d.part, p->ldx, (int64_t)p->n_local * p->kp, p->ldx,
                                                region<int8_t>(p, I_OZR), p->oz_lqg, region<int32_t>(p, I_OZREXP), st);
                  }});
-    v.push_back({"oz_w", [p, d](cudaStream_t st) {
+    const int i1 = p->ow_first[count];
+    v.push_back({"oz_w", [p, d, i1](cudaStream_t st) {
                    return launch_oz_w(p->tm_q32, p->tm_r, region<int32_t>(p, I_OZREXP), d.wout,
-                                      region<OzItem>(p, I_ITEMS_OW), (int)p->items_ow.size(), p->ldx, p->kp, p->K,
-                                      p->oz_nsl, st);
+                                      region<OzItem>(p, I_ITEMS_OW), i1, p->ldx, p->kp, p->K, p->oz_nsl, st);
                  }});
     return v;
   }
@@ -989,12 +1005,19 @@ const char* srm_profile_name(int index) {
 
 int srm_finalize(srm_plan* p, void* stream) {
   if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
-  return run_stages(finalize_stages(p), as_stream(stream));
+  return run_stages(finalize_stages(p, 0, p->n_local), as_stream(stream));
+}
+
+int srm_finalize_range(srm_plan* p, int first, int count, void* stream) {
+  if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
+  if (first < 0 || count < 0 || first + count > p->n_local) return fail(SRM_ERR_CONFIG, "subject range");
+  if (count == 0) return SRM_OK;
+  return run_stages(finalize_stages(p, first, count), as_stream(stream));
 }
 
 int srm_profile_finalize(srm_plan* p, float* ms_out, int capacity, int* n_out, void* stream) {
   if (!p || !p->ws || !ms_out || !n_out) return fail(SRM_ERR_CONFIG, "plan not bound");
-  return profile_stages(finalize_stages(p), ms_out, capacity, n_out, as_stream(stream));
+  return profile_stages(finalize_stages(p, 0, p->n_local), ms_out, capacity, n_out, as_stream(stream));
 }
 
 int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {

@@ -341,61 +341,98 @@ __global__ void __launch_bounds__(kSmallThreads) k_eig_polar(DevPlan p, int init
   }
 }
 
+// dst[r][c] = src[r][c0 + c] (r < rows, c < cols; zero where c0 + c >= cmax),
+// row pitches ldd / lds, with eight global loads in flight per thread (the
+// staging of the small per-subject kernels is latency-bound otherwise)
+__device__ __forceinline__ void stage_rows(double* dst, int ldd, const double* __restrict__ src, int64_t lds,
+                                           int rows, int cols, int64_t c0, int64_t cmax) {
+  const int total = rows * cols;
+  for (int e0 = 0; e0 < total; e0 += 8 * (int)blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + (int)threadIdx.x + u * (int)blockDim.x;
+      const int r = e / cols, c = e - r * cols;
+      v[u] = (e < total && c0 + c < cmax) ? src[(int64_t)r * lds + c0 + c] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + (int)threadIdx.x + u * (int)blockDim.x;
+      const int r = e / cols, c = e - r * cols;
+      if (e < total) dst[r * ldd + c] = v[u];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // apply_m: P_i = M_i^T B_i written into the subject's term record, plus the
 // per-tile cross term sum_{f,t} P[f][t] S[f][t]
 // ---------------------------------------------------------------------------
-// Register-blocked: warp w owns the NF = kp / 8 consecutive rows f = w NF + j,
-// lane l the 4 columns t = l + 32 u of a 128-column tile, so each c step costs
-// NF broadcast + 4 conflict-free shared loads for 4 NF FMAs.
+// On the FP64 tensor pipe (mma.sync.m8n8k4.f64, SASS DMMA): warp w owns the
+// 8-row strips f in {8 w, 8 (w + 8)}, all sixteen 8-column tiles of the
+// 128-column tile; M^T (A operand) and B are staged in shared memory with row
+// pitches = 4 mod 16 doubles (conflict-free fragments), the contraction over
+// c < K rounded up to 4 with zero rows.
+constexpr int kApplyLd = kApplyCols + 4;
+
 template <int NF>
 __global__ void __launch_bounds__(kSmallThreads) k_apply_m(DevPlan p, int with_cross) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double scratch[32];
   constexpr int kp = 8 * NF;
+  constexpr int LDM = kp + ((4 - kp) % 16 + 16) % 16;  // = 4 mod 16
+  constexpr int MS = (NF + 7) / 8;                      // strips per warp
+  constexpr int NT = kApplyCols / 8;
   const int tile = blockIdx.x, i = p.sub0 + blockIdx.y;
   const int K = (int)p.K;
+  const int K4 = (K + 3) & ~3;
   const int64_t t0 = (int64_t)tile * kApplyCols;
-  double* Ms = sm;             // [K][kp]: Ms[c kp + f] = M_i[c][f]
-  double* Bs = Ms + K * kp;    // [K][128]
+  double* Ms = sm;             // [K4][LDM]: Ms[c][f] = M_i[c][f]
+  double* Bs = Ms + K4 * LDM;  // [K4][kApplyLd]
   const double* Mg = p.mmat + (int64_t)i * kp * kp;
   const double* Bg = p.bred + (int64_t)i * p.kp * p.ldo;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int e = tid; e < K * kp; e += blockDim.x) Ms[e] = (e % kp < K) ? Mg[e] : 0.0;
-  for (int e = tid; e < K * kApplyCols; e += blockDim.x) {
-    const int c = e / kApplyCols, t = e % kApplyCols;
-    Bs[e] = (t0 + t < p.ldx) ? Bg[(int64_t)c * p.ldo + t0 + t] : 0.0;
-  }
+  stage_rows(Ms, LDM, Mg, kp, K, kp, 0, K);
+  stage_rows(Bs, kApplyLd, Bg, p.ldo, K, kApplyCols, t0, p.ldx);
+  for (int e = tid; e < (K4 - K) * kApplyLd; e += blockDim.x) Bs[K * kApplyLd + e] = 0.0;
+  for (int e = tid; e < (K4 - K) * LDM; e += blockDim.x) Ms[K * LDM + e] = 0.0;
   __syncthreads();
-  double acc[NF][4];
+  double acc[MS][NT][2];
 #pragma unroll
-  for (int j = 0; j < NF; ++j)
+  for (int m = 0; m < MS; ++m)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc[j][u] = 0.0;
-  for (int c = 0; c < K; ++c) {
-    double b[4], m[NF];
+    for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  const int lr = lane >> 2, lc = lane & 3;
+  for (int k0 = 0; k0 < K4; k0 += 4) {
+    const double* brow = Bs + (k0 + lc) * kApplyLd + lr;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) b[u] = Bs[c * kApplyCols + lane + 32 * u];
+    for (int m = 0; m < MS; ++m) {
+      const int mt = w + 8 * m;
+      if (mt < NF) {
+        const double a = Ms[(k0 + lc) * LDM + mt * 8 + lr];  // A[f][c] = M[c][f]
 #pragma unroll
-    for (int j = 0; j < NF; ++j) m[j] = Ms[c * kp + w * NF + j];
-#pragma unroll
-    for (int j = 0; j < NF; ++j)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[j][u] = fma(m[j], b[u], acc[j][u]);
+        for (int n = 0; n < NT; ++n) dmma(acc[m][n][0], acc[m][n][1], a, brow[n * 8]);
+      }
+    }
   }
   const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
   double* P = rec_ptr(p, (int)sj[SC_SLOT]);
   double cross = 0.0;
 #pragma unroll
-  for (int j = 0; j < NF; ++j) {
-    const int f = w * NF + j;
+  for (int m = 0; m < MS; ++m) {
+    const int f = (w + 8 * m) * 8 + lr;
+    if (w + 8 * m < NF) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t t = t0 + lane + 32 * u;
-      if (t < p.ldx) {
-        const double v = (f < K) ? acc[j][u] : 0.0;
-        if (with_cross && f < K) cross += v * p.S[(int64_t)f * p.ldx + t];
-        P[(int64_t)f * p.ldx + t] = v;
+      for (int n = 0; n < NT; ++n) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t t = t0 + n * 8 + 2 * lc + h;
+          if (t < p.ldx) {
+            const double v = (f < K) ? acc[m][n][h] : 0.0;
+            if (with_cross && f < K) cross += v * p.S[(int64_t)f * p.ldx + t];
+            P[(int64_t)f * p.ldx + t] = v;
+          }
+        }
       }
     }
   }
@@ -406,56 +443,71 @@ __global__ void __launch_bounds__(kSmallThreads) k_apply_m(DevPlan p, int with_c
 }
 
 // A_i^T A_i = B_i S^T / 2 (SURVEY identity 3): CTA (chunk c, subject i) forms
-// the K x K partial over TRs [64 c, 64 c + 64) with a 16 x 16 thread grid (R x R
-// register block per thread); the last CTA of a subject (atomic ticket, reset
-// after use) sums the partials in chunk order -- deterministic -- into
-// bred[i][a][ldx + b] (b < kp; zero for a or b >= K).
-constexpr int kGfbLd = kGfbCols + 1;  // odd row pitch: conflict-free column reads
+// the kp x kp partial over TRs [128 c, 128 c + 128) on the FP64 tensor pipe
+// (mma.sync.m8n8k4.f64: warp w owns the 8-row strips w and w + 8, all kp / 8
+// column tiles), staging B and S through shared memory in two 64-TR halves
+// (row pitch 68 = 4 mod 16 doubles: conflict-free fragments; 61 KB at kp = 56,
+// three CTAs per SM) with eight loads in flight per thread; the last CTA of a
+// subject (atomic ticket, reset after use) sums the partials in chunk order --
+// deterministic -- into bred[i][a][ldx + b] (b < kp; zero for a or b >= K).
+constexpr int kGfbHalf = kGfbCols / 2;
+constexpr int kGfbLd = kGfbHalf + 4;
 
-template <int R>
-__device__ __forceinline__ void gfb_body(const DevPlan& p, double* Bs, double* Ss) {
+template <int KP>
+__global__ void __launch_bounds__(kSmallThreads, KP <= 64 ? 3 : 1) k_gram_from_b(DevPlan p) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int NT = KP / 8;
+  constexpr int MS = (NT + 7) / 8;
   const int c = blockIdx.x, i = blockIdx.y;
-  const int K = (int)p.K, kp = (int)p.kp;
-  const int64_t t0 = (int64_t)c * kGfbCols;
+  const int K = (int)p.K;
+  double* Bs = sm;              // [KP][kGfbLd], rows >= K zero
+  double* Ss = sm + KP * kGfbLd;
   const double* Bg = p.bred + (int64_t)i * p.kp * p.ldo;
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  for (int e = tid; e < K * kGfbCols; e += blockDim.x) {
-    const int r = e / kGfbCols, t = e % kGfbCols;
-    const bool in = t0 + t < p.ldx;
-    Bs[r * kGfbLd + t] = in ? Bg[(int64_t)r * p.ldo + t0 + t] : 0.0;
-    Ss[r * kGfbLd + t] = in ? p.S[(int64_t)r * p.ldx + t0 + t] : 0.0;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  for (int e = tid; e < (KP - K) * kGfbLd; e += blockDim.x) {
+    Bs[K * kGfbLd + e] = 0.0;
+    Ss[K * kGfbLd + e] = 0.0;
   }
-  __syncthreads();
-  double acc[R][R];
+  double acc[MS][NT][2];
 #pragma unroll
-  for (int a = 0; a < R; ++a)
+  for (int m = 0; m < MS; ++m)
 #pragma unroll
-    for (int b = 0; b < R; ++b) acc[a][b] = 0.0;
-  for (int t = 0; t < kGfbCols; ++t) {
-    double bv[R], sv[R];
+    for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  for (int h = 0; h < 2; ++h) {
+    const int64_t t0 = (int64_t)c * kGfbCols + h * kGfbHalf;
+    if (h) __syncthreads();  // the first half's reads are done
+    stage_rows(Bs, kGfbLd, Bg, p.ldo, K, kGfbHalf, t0, p.ldx);
+    stage_rows(Ss, kGfbLd, p.S, p.ldx, K, kGfbHalf, t0, p.ldx);
+    __syncthreads();
+#pragma unroll 2
+    for (int k0 = 0; k0 < kGfbHalf; k0 += 4) {
 #pragma unroll
-    for (int a = 0; a < R; ++a) {
-      const int r = ty + 16 * a;
-      bv[a] = r < K ? Bs[r * kGfbLd + t] : 0.0;
+      for (int m = 0; m < MS; ++m) {
+        const int mt = w + 8 * m;
+        if (mt < NT) {
+          const double a = Bs[(mt * 8 + lr) * kGfbLd + k0 + lc];  // A[a][t] = B[a][t]
+#pragma unroll
+          for (int n = 0; n < NT; ++n)                            // B[t][b] = S[b][t]
+            dmma(acc[m][n][0], acc[m][n][1], a, Ss[(n * 8 + lr) * kGfbLd + k0 + lc]);
+        }
+      }
     }
-#pragma unroll
-    for (int b = 0; b < R; ++b) {
-      const int r = tx + 16 * b;
-      sv[b] = r < K ? Ss[r * kGfbLd + t] : 0.0;
-    }
-#pragma unroll
-    for (int a = 0; a < R; ++a)
-#pragma unroll
-      for (int b = 0; b < R; ++b) acc[a][b] = fma(bv[a], sv[b], acc[a][b]);
   }
+  constexpr int kp = KP;
   double* part = p.gfb_part + ((int64_t)i * p.gfb_chunks + c) * kp * kp;
 #pragma unroll
-  for (int a = 0; a < R; ++a)
+  for (int m = 0; m < MS; ++m) {
+    const int mt = w + 8 * m;
+    if (mt < NT) {
 #pragma unroll
-    for (int b = 0; b < R; ++b) {
-      const int ra = ty + 16 * a, rb = tx + 16 * b;
-      if (ra < kp && rb < kp) part[ra * kp + rb] = acc[a][b];
+      for (int n = 0; n < NT; ++n) {
+        double* d = part + (mt * 8 + lr) * kp + n * 8 + 2 * lc;
+        d[0] = acc[m][n][0];
+        d[1] = acc[m][n][1];
+      }
     }
+  }
   // last CTA of subject i reduces
   __shared__ int last;
   __threadfence();
@@ -488,21 +540,6 @@ __device__ __forceinline__ void gfb_body(const DevPlan& p, double* Bs, double* S
     }
   }
   if (tid == 0) p.gfb_count[i] = 0;
-}
-
-__global__ void __launch_bounds__(kSmallThreads) k_gram_from_b(DevPlan p) {
-  extern __shared__ __align__(16) double sm[];
-  double* Bs = sm;
-  double* Ss = sm + p.K * kGfbLd;
-  switch ((p.K + 15) / 16) {
-    case 1: gfb_body<1>(p, Bs, Ss); break;
-    case 2: gfb_body<2>(p, Bs, Ss); break;
-    case 3: gfb_body<3>(p, Bs, Ss); break;
-    case 4: gfb_body<4>(p, Bs, Ss); break;
-    case 5: gfb_body<5>(p, Bs, Ss); break;
-    case 6: gfb_body<6>(p, Bs, Ss); break;
-    default: gfb_body<7>(p, Bs, Ss); break;
-  }
 }
 
 __device__ __forceinline__ int64_t hist_row(const DevPlan& p, int it) { return (int64_t)(it % p.n_hist) * p.hist_stride; }
@@ -1158,7 +1195,9 @@ cudaError_t launch_eig_polar_exact(const DevPlan& p, int init, cudaStream_t s) {
 }
 
 cudaError_t launch_apply_m(const DevPlan& p, int with_cross, cudaStream_t s) {
-  const size_t bytes = (size_t)(p.K * p.kp + p.K * kApplyCols) * sizeof(double);
+  const int64_t K4 = (p.K + 3) & ~3;
+  const int64_t ldm = p.kp + ((4 - p.kp) % 16 + 16) % 16;
+  const size_t bytes = (size_t)(K4 * ldm + K4 * kApplyLd) * sizeof(double);
   const void* fn = nullptr;
   switch (p.kp / 8) {
 #define SRM_APPLY_M_CASE(n) \
@@ -1183,10 +1222,26 @@ cudaError_t launch_apply_m(const DevPlan& p, int with_cross, cudaStream_t s) {
 }
 
 cudaError_t launch_gram_from_b(const DevPlan& p, cudaStream_t s) {
-  const size_t bytes = (size_t)2 * p.K * kGfbLd * sizeof(double);
-  cudaError_t e = set_smem((const void*)k_gram_from_b, bytes);
+  const size_t bytes = (size_t)2 * p.kp * kGfbLd * sizeof(double);
+  const void* fn = nullptr;
+  switch (p.kp / 8) {
+#define SRM_GFB_CASE(n) \
+  case n:               \
+    fn = (const void*)k_gram_from_b<8 * n>; \
+    break;
+    SRM_GFB_CASE(1) SRM_GFB_CASE(2) SRM_GFB_CASE(3) SRM_GFB_CASE(4) SRM_GFB_CASE(5) SRM_GFB_CASE(6)
+    SRM_GFB_CASE(7) SRM_GFB_CASE(8) SRM_GFB_CASE(9) SRM_GFB_CASE(10) SRM_GFB_CASE(11) SRM_GFB_CASE(12)
+    SRM_GFB_CASE(13) SRM_GFB_CASE(14)
+#undef SRM_GFB_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+  cudaError_t e = set_smem(fn, bytes);
   if (e != cudaSuccess) return e;
-  k_gram_from_b<<<dim3((unsigned)p.gfb_chunks, (unsigned)p.n_local), kSmallThreads, bytes, s>>>(p);
+  DevPlan arg = p;
+  void* args[] = {&arg};
+  e = cudaLaunchKernel(fn, dim3((unsigned)p.gfb_chunks, (unsigned)p.n_local), dim3(kSmallThreads), args, bytes, s);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

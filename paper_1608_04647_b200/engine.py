@@ -443,6 +443,36 @@ class SrmEngine:
     def finalize(self):
         _lib.check(self.lib.srm_finalize(self.plan, ctypes.c_void_p(self.stream())), "finalize")
 
+    def finalize_to_host(self, n_batches=4):
+        """srm_finalize in subject batches, each batch's W_i rows copied into
+        one pinned host array on a side stream while the next batch is
+        formed.  Returns the numpy view (rows of all local subjects)."""
+        torch = _torch()
+        host = torch.empty(tuple(self.wout.shape), dtype=self.wout.dtype, pin_memory=True)
+        main = torch.cuda.current_stream(self.device)
+        side = self._side_stream()
+        nb = max(1, min(int(n_batches), self.n_local))
+        bounds = [self.n_local * b // nb for b in range(nb + 1)]
+        for b in range(nb):
+            first, last = bounds[b], bounds[b + 1]
+            _lib.check(self.lib.srm_finalize_range(self.plan, first, last - first,
+                                                   ctypes.c_void_p(main.cuda_stream)), "finalize_range")
+            r0 = int(self.row_off[first])
+            r1 = int(self.row_off[last]) if last < self.n_local else int(sum(self.n_voxels))
+            ev = torch.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            with torch.cuda.stream(side):
+                host[r0:r1].copy_(self.wout[r0:r1], non_blocking=True)
+        side.synchronize()
+        return host.numpy()
+
+    def _side_stream(self):
+        torch = _torch()
+        if getattr(self, "_d2h_stream", None) is None:
+            self._d2h_stream = torch.cuda.Stream(self.device)
+        return self._d2h_stream
+
     # --------------------------------------------------------------- results
     def status(self):
         out = (ctypes.c_int32 * 4)()

@@ -405,7 +405,7 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f
 
 def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=True,
         keep_on_device=False, device=None, engine_out=None, timings=None, algorithm="auto",
-        tensor_cores=True, gram_int8=True, init_overlap=False):
+        tensor_cores=True, gram_int8=True, init_overlap=True):
     """Run the distributed EM; ``subjects`` are this worker's share (srm.py:216).
 
     Every worker calls this with the same config and its own communicator
@@ -430,10 +430,10 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     from seven exact int8 slices per value on the int8 tensor cores (products
     represented to ~2^-48 of the column maxima; ~1e-14 relative to G) when
     the slices fit in device memory; ``False`` keeps it on fp64 DMMA.
-    ``init_overlap``: run the initial mapping (srm.py:101-118 after the draw)
-    batch by batch while later subjects are still uploading, or (default)
-    once after the upload -- measured equal end to end on cfg 2, where the
-    draws of the last batches arrive after the upload anyway.
+    ``init_overlap`` (default): run the initial mapping (srm.py:101-118 after
+    the draw) batch by batch while later subjects are still uploading;
+    ``False`` runs it once after the upload (bit-identical results; ~5 ms
+    more end to end on cfg 2).
     """
     clock = _PhaseClock(timings)
     config.validate()
@@ -465,7 +465,7 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     use_i8 = bool(gram_int8)
     if use_i8 or algorithm == "auto":
         torch = _torch()
-        free, _ = torch.cuda.mem_get_info(device)
+        free = _free_device_bytes(torch, device)
         x_bytes = sum(n_vox) * (-(-n_trs // 32) * 32) * (8 if store == "f64" else 4)
         use_i8 = use_i8 and gram_int8_bytes(n_vox, n_trs, store) + x_bytes < 0.6 * free
     if algorithm == "auto":
@@ -520,12 +520,33 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
                 if sdiff / max(sprev, 1e-300) < config.tolerance:
                     break
     clock.tick("em")
-    eng.finalize()
+    if keep_on_device:
+        eng.finalize()
+        wout = None
+    else:
+        # W_i of earlier subjects read back while later ones are formed
+        wout = eng.finalize_to_host()
     eng.raise_status()
     clock.tick("finalize")
-    model = _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device)
+    model = _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device, wout)
     clock.tick("collect")
     return model
+
+
+_FREE_BASE = {}
+
+
+def _free_device_bytes(torch, device):
+    """Device bytes a fit can still allocate: cudaMemGetInfo once per device
+    (it costs milliseconds), plus what torch's caching allocator had reserved
+    then, minus what torch has allocated now (reserved-but-free blocks are
+    reusable, so they count as free)."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx not in _FREE_BASE:
+        free, _ = torch.cuda.mem_get_info(idx)
+        _FREE_BASE[idx] = free + torch.cuda.memory_reserved(idx)
+    return max(0, _FREE_BASE[idx] - torch.cuda.memory_allocated(idx))
 
 
 class _PhaseClock:
@@ -542,7 +563,7 @@ class _PhaseClock:
         self.t = now
 
 
-def _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device):
+def _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device, wout=None):
     torch = _torch()
     rho2_local = eng.local_rho2().clone()
     # final rho^2 gather + rho0 refresh (srm.py:289-313)
@@ -576,7 +597,8 @@ def _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device):
     else:
         # W lands by DMA in pinned memory from torch's caching host allocator
         # (reused once an earlier model is released); the arrays are views of it
-        wout = hostio.to_pinned(eng.wout)
+        if wout is None:
+            wout = hostio.to_pinned(eng.wout)
         muh = hostio.to_host(eng.mu)
         W = [wout[eng.subject_rows(j)] for j in range(eng.n_local)]
         mu = [muh[eng.subject_rows(j)].copy() for j in range(eng.n_local)]

@@ -390,3 +390,17 @@ def test_init_overlap_is_bit_identical(srm):
         assert np.array_equal(a.S, b.S) and np.array_equal(a.sigma_s, b.sigma_s), algorithm
         for wa, wb in zip(a.W, b.W):
             assert np.array_equal(wa, wb), algorithm
+
+
+def test_batched_finalize_readback_is_bit_identical(srm):
+    """W formed and read back in subject batches (srm_finalize_range) == one srm_finalize."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(7, 900, 130, 10, seed=5)
+    xs[3] = xs[3][:517]  # ragged: a partial 128-voxel tile inside a batch
+    cfg = srm.SrmConfig(k=10, iterations=2, seed=2)
+    for algorithm in ("gram", "stream"):
+        a = srm.fit(_subjects(srm, xs), cfg, algorithm=algorithm)
+        b = srm.fit(_subjects(srm, xs), cfg, algorithm=algorithm, keep_on_device=True)
+        for wa, wb in zip(a.W, b.W):
+            assert np.array_equal(wa, wb.cpu().numpy()), algorithm
