@@ -42,6 +42,7 @@ enum Internal {
   I_ROWSQ = SRM_R_COUNT,
   I_CMAT,
   I_TAILSCR,
+  I_SINV,
   I_SSPART,
   I_TAILPART,
   I_PART,
@@ -85,6 +86,12 @@ void srm::set_last_error(const char* where, cudaError_t e) {
   g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
 }
 
+// side stream + fork/join events of a plan (the stage lists' second lane)
+struct Lanes {
+  cudaStream_t side;
+  cudaEvent_t fork, join;
+};
+
 struct srm_plan {
   int dtype = SRM_F64;
   int n_local = 0;
@@ -112,6 +119,9 @@ struct srm_plan {
   char* ws = nullptr;
   DevPlan dp{};
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t side_stream = nullptr;  // second lane of the stage lists
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  Lanes lanes{};
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   TmaMap tm_x_a, tm_s, tm_a, tm_x_b;  // tensor-core path TMA maps (bound at srm_plan_bind)
@@ -158,6 +168,7 @@ void layout(srm_plan* p) {
   sz[I_ROWSQ] = p->rows_total * 8;
   sz[I_CMAT] = kp2 * 8;
   sz[I_TAILSCR] = kTailScalars * 8;
+  sz[I_SINV] = kp2 * 8;
   sz[I_SSPART] = (int64_t)ntile_tail * kp2 * 8;
   sz[I_TAILPART] = (int64_t)ntile_tail * 4 * 8;
   sz[I_PART] = p->chunks_total * p->kp * p->ldo * 8;
@@ -425,6 +436,7 @@ void set_pointers(srm_plan* p) {
   d.var = region<double>(p, SRM_R_VAR);
   d.cmat = region<double>(p, I_CMAT);
   d.tailscr = region<double>(p, I_TAILSCR);
+  d.sinv = region<double>(p, I_SINV);
   d.sspart = region<double>(p, I_SSPART);
   d.tailpart = region<double>(p, I_TAILPART);
   d.part = region<double>(p, I_PART);
@@ -457,6 +469,8 @@ int check(cudaError_t e, const char* where) { return e == cudaSuccess ? SRM_OK :
 struct Stage {
   const char* name;
   std::function<cudaError_t(cudaStream_t)> fn;
+  int lane = 0;       // 1: on the plan's side stream, after everything issued before it
+  bool join = false;  // the side stream's work completes before this stage
 };
 
 void contraction_stages(srm_plan* p, std::vector<Stage>& out) {
@@ -475,14 +489,29 @@ void contraction_stages(srm_plan* p, std::vector<Stage>& out) {
 std::vector<Stage> e_stages(srm_plan* p) {
   const DevPlan& d = p->dp;
   std::vector<Stage> v;
+  // var_s and C (needs only Sigma_s^{-1} and rho0) beside the ordered sum
+  v.push_back({"tail_kk", [d](cudaStream_t st) { return launch_tail_kk(d, st); }, 1});
   if (p->flags & SRM_FLAG_ORDERED) {
     const int n = (int)p->order.size();
     v.push_back({"reduce_terms", [d, n](cudaStream_t st) { return launch_reduce_terms(d, d.red, d.order, n, st); }});
   }
-  v.push_back({"tail_kk", [d](cudaStream_t st) { return launch_tail_kk(d, st); }});
-  v.push_back({"tail_s", [d](cudaStream_t st) { return launch_tail_s(d, st); }});
-  v.push_back({"tail_sigma", [d](cudaStream_t st) { return launch_tail_sigma(d, st); }});
+  v.push_back({"tail_s", [d](cudaStream_t st) { return launch_tail_s(d, st); }, 0, true});
+  // Sigma_s, the LL and the next E-step's Sigma_s^{-1} on the side lane: the
+  // M-step needs only S (tail_s) until finalize_rho reads tr(Sigma_s)
+  v.push_back({"tail_sigma", [d](cudaStream_t st) { return launch_tail_sigma(d, st); }, 1});
+  v.push_back({"tail_inv", [d](cudaStream_t st) { return launch_tail_inv(d, st); }, 1});
   return v;
+}
+
+// rho_i^2 of the M-step, then the device iteration counter moves on
+void push_finalize_rho(const DevPlan& d, std::vector<Stage>& v) {
+  // joins the side lane: tr(Sigma_s) comes from tail_sigma
+  if (finalize_rho_advances(d)) {
+    v.push_back({"finalize_rho", [d](cudaStream_t st) { return launch_finalize_rho_advance(d, st); }, 0, true});
+  } else {
+    v.push_back({"finalize_rho", [d](cudaStream_t st) { return launch_finalize_rho(d, 0, st); }, 0, true});
+    v.push_back({"advance_iteration", [d](cudaStream_t st) { return launch_set_iteration(d, 0, 1, st); }});
+  }
 }
 
 std::vector<Stage> m_stages(srm_plan* p) {
@@ -509,8 +538,7 @@ std::vector<Stage> m_stages(srm_plan* p) {
     v.push_back({"gram_from_b", [d](cudaStream_t st) { return launch_gram_from_b(d, st); }});
     v.push_back({"eig_polar", [d](cudaStream_t st) { return launch_eig_polar(d, 0, st); }});
     v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 1, st); }});
-    v.push_back({"finalize_rho", [d](cudaStream_t st) { return launch_finalize_rho(d, 0, st); }});
-    v.push_back({"advance_iteration", [d](cudaStream_t st) { return launch_set_iteration(d, 0, 1, st); }});
+    push_finalize_rho(d, v);
     return v;
   }
   if (p->flags & SRM_FLAG_TC) {
@@ -537,16 +565,51 @@ std::vector<Stage> m_stages(srm_plan* p) {
   v.push_back({"gram_from_b", [d](cudaStream_t st) { return launch_gram_from_b(d, st); }});
   v.push_back({"eig_polar", [d](cudaStream_t st) { return launch_eig_polar(d, 0, st); }});
   v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 1, st); }});
-  v.push_back({"finalize_rho", [d](cudaStream_t st) { return launch_finalize_rho(d, 0, st); }});
-  v.push_back({"advance_iteration", [d](cudaStream_t st) { return launch_set_iteration(d, 0, 1, st); }});
+  push_finalize_rho(d, v);
   return v;
 }
 
-int run_stages(const std::vector<Stage>& stages, cudaStream_t st) {
+// Without `ln` every stage runs in order on `st`; with it, lane-1 stages run
+// on the side stream (forked from `st` where they appear) and `st` waits for
+// them at the next join stage and at the end of the list.  Graph capture
+// turns the fork/join events into graph edges.
+int run_stages(const std::vector<Stage>& stages, cudaStream_t st, const Lanes* ln = nullptr) {
+  bool pending = false;
   for (const Stage& s : stages) {
-    cudaError_t e = s.fn(st);
+    cudaStream_t target = st;
+    cudaError_t e = cudaSuccess;
+    if (ln && s.join && pending) {
+      e = cudaStreamWaitEvent(st, ln->join, 0);
+      pending = false;
+    }
+    if (ln && s.lane == 1 && e == cudaSuccess) {
+      e = cudaEventRecord(ln->fork, st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(ln->side, ln->fork, 0);
+      target = ln->side;
+    }
+    if (e == cudaSuccess) e = s.fn(target);
+    if (ln && s.lane == 1 && e == cudaSuccess) {
+      e = cudaEventRecord(ln->join, ln->side);
+      pending = true;
+    }
     if (e != cudaSuccess) return cuda_fail(e, s.name);
   }
+  if (pending) {
+    cudaError_t e = cudaStreamWaitEvent(st, ln->join, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "join");
+  }
+  return SRM_OK;
+}
+
+int plan_lanes(srm_plan* p, const Lanes** out) {
+  if (!p->side_stream) {
+    cudaError_t e = cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "side stream");
+  }
+  p->lanes = Lanes{p->side_stream, p->ev_fork, p->ev_join};
+  *out = &p->lanes;
   return SRM_OK;
 }
 
@@ -775,6 +838,9 @@ int srm_plan_destroy(srm_plan* plan) {
     if (plan->graph_exec) cudaGraphExecDestroy(plan->graph_exec);
     if (plan->graph) cudaGraphDestroy(plan->graph);
     if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
+    if (plan->side_stream) cudaStreamDestroy(plan->side_stream);
+    if (plan->ev_fork) cudaEventDestroy(plan->ev_fork);
+    if (plan->ev_join) cudaEventDestroy(plan->ev_join);
   }
   delete plan;
   return SRM_OK;
@@ -845,6 +911,10 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
   for (int64_t j = 0; j < p->K; ++j) eye[(size_t)j * p->kp + j] = 1.0;
   e = cudaMemcpy(region<double>(p, SRM_R_SIGMA), eye.data(), eye.size() * 8, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "bind sigma");
+  // its inverse as k_tail_inv leaves it (-I; log det 0 from the memset)
+  for (double& x : eye) x = -x;
+  e = cudaMemcpy(region<double>(p, I_SINV), eye.data(), eye.size() * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "bind sigma inverse");
   // warm up kernel attributes outside any graph capture
   const DevPlan& d = p->dp;
   e = launch_contract_e((int)p->kp, SRM_F64, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0, nullptr, 0, 0);
@@ -951,7 +1021,10 @@ int srm_set_iteration(srm_plan* p, int iteration, void* stream) {
 
 int srm_e_step(srm_plan* p, void* stream) {
   if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
-  return run_stages(e_stages(p), as_stream(stream));
+  const Lanes* ln = nullptr;
+  const int rc = plan_lanes(p, &ln);
+  if (rc) return rc;
+  return run_stages(e_stages(p), as_stream(stream), ln);
 }
 
 int srm_m_step(srm_plan* p, void* stream) {
@@ -967,8 +1040,13 @@ int srm_graph_capture(srm_plan* p) {
   if (e != cudaSuccess) return cuda_fail(e, "capture stream");
   e = cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return cuda_fail(e, "begin capture");
-  int rc = run_stages(e_stages(p), p->cap_stream);
-  if (rc == SRM_OK) rc = run_stages(m_stages(p), p->cap_stream);
+  // one list: the side-stream stages of the E-step overlap the M-step
+  std::vector<Stage> stages = e_stages(p);
+  std::vector<Stage> m = m_stages(p);
+  stages.insert(stages.end(), m.begin(), m.end());
+  const Lanes* ln = nullptr;
+  int rc = plan_lanes(p, &ln);
+  if (rc == SRM_OK) rc = run_stages(stages, p->cap_stream, ln);
   cudaGraph_t g = nullptr;
   e = cudaStreamEndCapture(p->cap_stream, &g);
   if (rc != SRM_OK) {

@@ -53,6 +53,7 @@ struct DevPlan {
   double* redlocal;
   double* S;
   double* sigma;
+  double* sinv;      // [kp][kp] -Sigma_s^{-1} of the coming E-step (k_tail_inv)
   double* var;
   double* cmat;
   double* tailscr;
@@ -91,10 +92,15 @@ cudaError_t launch_apply_m(const DevPlan& p, int with_cross, cudaStream_t s);
 // record (bred[i][:, ldx:ldx+kp]), split over TR chunks
 cudaError_t launch_gram_from_b(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_finalize_rho(const DevPlan& p, int init, cudaStream_t s);
+// finalize_rho of an iteration plus the iteration-counter advance, one block
+// (when nsub <= 1024)
+bool finalize_rho_advances(const DevPlan& p);
+cudaError_t launch_finalize_rho_advance(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_set_iteration(const DevPlan& p, int iteration, int advance, cudaStream_t s);
 cudaError_t launch_reduce_terms(const DevPlan& p, double* dst, const int32_t* order, int count,
                                 cudaStream_t s);
 cudaError_t launch_tail(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_tail_inv(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_sigma(const DevPlan& p, cudaStream_t s);

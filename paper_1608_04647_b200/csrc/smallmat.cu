@@ -549,8 +549,14 @@ __global__ void k_set_iteration(DevPlan p, int iteration, int advance) {
   else *p.iter = iteration;
 }
 
-__global__ void k_finalize_rho(DevPlan p, int init) {
+// advance (single-block launches): thread 0 then moves the device iteration
+// counter on, after every thread has read it
+__global__ void k_finalize_rho(DevPlan p, int init, int advance) {
   const int iteration = init ? -1 : *p.iter;
+  if (advance) {
+    __syncthreads();
+    if (threadIdx.x == 0) *p.iter = iteration + 1;
+  }
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= p.nsub) return;
   const int i = p.sub0 + w;
@@ -722,25 +728,81 @@ __device__ double sum_log(const double* dbuf, int n, double* scratch) {
 }
 
 // ---------------------------------------------------------------------------
-// tail, stage 1 (one CTA): var_s and C = Sigma_s^T (I - rho0 var_s)
+// tail, stage 0 (one CTA): -Sigma_s^{-1} and log det Sigma_s (srm.py:127 inner
+// spd_inverse).  Sigma_s is final after k_tail_sigma, so the next E-step's
+// inverse runs on a side stream while the M-step of this iteration does.
+// ---------------------------------------------------------------------------
+template <int R>
+__device__ __forceinline__ void tail_inv_body(const DevPlan& p, SweepShared& sh) {
+  const int n = (int)p.K, kp = (int)p.kp;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double a[R][R];
+  reg_load<R>(a, p.sigma, kp, n);
+  const int piv = reg_sweep<R>(a, n, sh.pbuf, sh.dbuf);  // a = -Sigma_s^{-1}
+  if (piv >= 0) {
+    if (tid == 0) raise_status(p.status, SRM_ERR_DEFINITENESS, piv, -1);
+    return;
+  }
+  const double logdet_sigma = sum_log(sh.dbuf, n, sh.scratch);
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int r = ty + 16 * i, c = tx + 16 * k;
+      if (r < n && c < n) p.sinv[r * kp + c] = a[i][k];
+    }
+  if (tid == 0) p.tailscr[TS_LOGDET_SIGMA] = logdet_sigma;
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_tail_inv(DevPlan p) {
+  __shared__ SweepShared sh;
+  if (failed(p)) return;
+  switch ((p.K + 15) / 16) {
+    case 1: tail_inv_body<1>(p, sh); break;
+    case 2: tail_inv_body<2>(p, sh); break;
+    case 3: tail_inv_body<3>(p, sh); break;
+    case 4: tail_inv_body<4>(p, sh); break;
+    case 5: tail_inv_body<5>(p, sh); break;
+    case 6: tail_inv_body<6>(p, sh); break;
+    default: tail_inv_body<7>(p, sh); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tail, stage 1 (one CTA): var_s = (rho0 I + Sigma_s^{-1})^{-1} and
+// C = Sigma_s^T (I - rho0 var_s) (srm.py:127-128).  rho0 = sum 1 / rho_j^2 in
+// ascending order straight from the term table (ordered plans: the same sum
+// k_reduce_terms forms, so this stage runs beside it), else from `red`.
 // ---------------------------------------------------------------------------
 template <int R>
 __device__ __forceinline__ void tail_kk_body(const DevPlan& p, int iteration, SweepShared& sh) {
   extern __shared__ __align__(16) double sm[];
   double* pbuf = sh.pbuf;
   double* dbuf = sh.dbuf;
-  double* scratch = sh.scratch;
   const int n = (int)p.K, ld = n + 1, kp = (int)p.kp;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const double rho0 = p.red[p.kp * p.ldx + RD_RHO0];
+  __shared__ double s_rho0;
   double a[R][R];
-  reg_load<R>(a, p.sigma, kp, n);
-  int piv = reg_sweep<R>(a, n, pbuf, dbuf);  // a = -Sigma_s^{-1}
-  if (piv >= 0) {
-    if (tid == 0) raise_status(p.status, SRM_ERR_DEFINITENESS, piv, iteration);
-    return;
+  reg_load<R>(a, p.sinv, kp, n);  // -Sigma_s^{-1} (k_tail_inv)
+  if (p.flags & SRM_FLAG_ORDERED) {
+    // 1 / rho_j^2 loaded in parallel, summed by one thread in ascending order
+    double* rinv = sh.pbuf;
+    const int64_t nrec = p.kp * p.ldx;
+    double rho0 = 0.0;
+    for (int j0 = 0; j0 < p.n_order; j0 += 2 * kSweepLd) {
+      const int m = min(2 * kSweepLd, p.n_order - j0);
+      for (int u = tid; u < m; u += blockDim.x) rinv[u] = 1.0 / rec_ptr(p, p.order[j0 + u])[nrec + RC_RHO2];
+      __syncthreads();
+      if (tid == 0)
+        for (int u = 0; u < m; ++u) rho0 = (j0 + u == 0) ? rinv[u] : rho0 + rinv[u];
+      __syncthreads();
+    }
+    if (tid == 0) s_rho0 = rho0;
+  } else if (tid == 0) {
+    s_rho0 = p.red[p.kp * p.ldx + RD_RHO0];
   }
-  const double logdet_sigma = sum_log(dbuf, n, scratch);
+  __syncthreads();
+  const double rho0 = s_rho0;
 #pragma unroll
   for (int i = 0; i < R; ++i)
 #pragma unroll
@@ -748,12 +810,12 @@ __device__ __forceinline__ void tail_kk_body(const DevPlan& p, int iteration, Sw
       const int r = ty + 16 * i, c = tx + 16 * k;
       a[i][k] = (r < n && c < n) ? (r == c ? rho0 : 0.0) - a[i][k] : 0.0;
     }
-  piv = reg_sweep<R>(a, n, pbuf, dbuf);  // a = -var_s
+  const int piv = reg_sweep<R>(a, n, pbuf, dbuf);  // a = -var_s
   if (piv >= 0) {
     if (tid == 0) raise_status(p.status, SRM_ERR_DEFINITENESS, piv, iteration);
     return;
   }
-  const double logdet_prec = sum_log(dbuf, n, scratch);
+  const double logdet_prec = sum_log(dbuf, n, sh.scratch);
   double* Vs = sm;           // var_s  [n][ld]
   double* Ss = sm + n * ld;  // Sigma_s [n][ld]
 #pragma unroll
@@ -804,10 +866,7 @@ __device__ __forceinline__ void tail_kk_body(const DevPlan& p, int iteration, Sw
       const int r = ty + 16 * i, c = tx + 16 * k;
       if (r < n && c < n) p.cmat[r * kp + c] = a[i][k];
     }
-  if (tid == 0) {
-    p.tailscr[TS_LOGDET_SIGMA] = logdet_sigma;
-    p.tailscr[TS_LOGDET_PREC] = logdet_prec;
-  }
+  if (tid == 0) p.tailscr[TS_LOGDET_PREC] = logdet_prec;
 }
 
 __global__ void __launch_bounds__(kSmallThreads) k_tail_kk(DevPlan p) {
@@ -976,10 +1035,12 @@ __global__ void k_reset(DevPlan p) {
   for (int e = threadIdx.x; e < kp * kp; e += blockDim.x) {
     const int a = e / kp, b = e - a * kp;
     p.sigma[e] = (a == b && a < p.K) ? 1.0 : 0.0;
+    p.sinv[e] = (a == b && a < p.K) ? -1.0 : 0.0;  // the sweep of I
   }
   if (threadIdx.x == 0) {
     p.status[0] = p.status[1] = p.status[2] = 0;
     *p.iter = 0;
+    p.tailscr[TS_LOGDET_SIGMA] = 0.0;
   }
 }
 
@@ -1246,7 +1307,15 @@ cudaError_t launch_gram_from_b(const DevPlan& p, cudaStream_t s) {
 }
 
 cudaError_t launch_finalize_rho(const DevPlan& p, int init, cudaStream_t s) {
-  k_finalize_rho<<<(p.nsub + 127) / 128, 128, 0, s>>>(p, init);
+  k_finalize_rho<<<(p.nsub + 127) / 128, 128, 0, s>>>(p, init, 0);
+  return cudaGetLastError();
+}
+
+bool finalize_rho_advances(const DevPlan& p) { return p.nsub <= 1024; }
+
+cudaError_t launch_finalize_rho_advance(const DevPlan& p, cudaStream_t s) {
+  if (!finalize_rho_advances(p)) return cudaErrorInvalidValue;
+  k_finalize_rho<<<1, (p.nsub + 31) / 32 * 32, 0, s>>>(p, 0, 1);
   return cudaGetLastError();
 }
 
@@ -1260,6 +1329,11 @@ cudaError_t launch_reduce_terms(const DevPlan& p, double* dst, const int32_t* or
   const int64_t n = p.kp * p.ldx;
   k_reduce_terms<<<(unsigned)((n + kSmallThreads - 1) / kSmallThreads), kSmallThreads, 0, s>>>(
       p, dst, order, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tail_inv(const DevPlan& p, cudaStream_t s) {
+  k_tail_inv<<<1, kSmallThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -1289,7 +1363,8 @@ cudaError_t launch_tail_sigma(const DevPlan& p, cudaStream_t s) {
 }
 
 cudaError_t launch_tail(const DevPlan& p, cudaStream_t s) {
-  cudaError_t e = launch_tail_kk(p, s);
+  cudaError_t e = launch_tail_inv(p, s);
+  if (e == cudaSuccess) e = launch_tail_kk(p, s);
   if (e == cudaSuccess) e = launch_tail_s(p, s);
   if (e == cudaSuccess) e = launch_tail_sigma(p, s);
   return e;

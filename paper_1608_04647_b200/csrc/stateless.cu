@@ -91,7 +91,7 @@ int64_t srm_stateless_workspace_bytes(int64_t v, int64_t k, int64_t t) {
   b += rup(nch * ntile * (int64_t)sizeof(ItemE) + ((v + 127) / 128) * (int64_t)sizeof(ItemA), 256);
   // tail step: red, S (kp x ldx), sigma/var/cmat, per-tile partials
   const int64_t ntail = ldxp / 32;
-  b += rup((2 * kp * ldxp + 16) * 8, 256) + rup((3 + ntail) * kp * kp * 8, 256) + rup((ntail * 4 + 64) * 8, 256);
+  b += rup((2 * kp * ldxp + 16) * 8, 256) + rup((4 + ntail) * kp * kp * 8, 256) + rup((ntail * 4 + 64) * 8, 256);
   return b + 4096;
 }
 
@@ -178,6 +178,7 @@ int srm_tail_step(const double* reduced, int64_t ldr, const double* sigma, int64
   d.red = c.take<double>(d.red_stride);
   d.S = c.take<double>(kp * ldx);
   d.sigma = c.take<double>(kp * kp);
+  d.sinv = c.take<double>(kp * kp);
   d.var = c.take<double>(kp * kp);
   d.cmat = c.take<double>(kp * kp);
   d.sspart = c.take<double>(ntail * kp * kp);
