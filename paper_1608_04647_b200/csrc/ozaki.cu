@@ -345,14 +345,25 @@ __global__ void __launch_bounds__(256) k_oz_slice_rows(const double* __restrict_
   if (r >= rows) return;
   const double* row = M + r * ldm;
   double m = 0.0;
-  for (int64_t c = lane; c < ncols; c += 32) m = fmax(m, fabs(row[c]));
+  for (int64_t c0 = 0; c0 < ncols; c0 += 256) {  // eight loads in flight per lane
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t c = c0 + lane + 32 * u;
+      v[u] = c < ncols ? fabs(row[c]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) m = fmax(m, v[u]);
+  }
   m = warp_max(m);
   const int e = (m > 0.0) ? frexp_exp(m) : 0;
   if (lane == 0) expo[r] = e;
   const double scale = __longlong_as_double((long long)(1023 + 6 - e) << 52);
   uint8_t* rb = rec[warp];
+  double next = row[lane];  // the block's value, loaded one block ahead
   for (int64_t b = 0; b * 32 < ncols; ++b) {
-    double y = row[b * 32 + lane] * scale;  // |y| < 64
+    double y = next * scale;  // |y| < 64
+    if ((b + 1) * 32 < ncols) next = row[(b + 1) * 32 + lane];
 #pragma unroll
     for (int s = 0; s < kOzSlices; ++s) {
       int low;

@@ -8,7 +8,8 @@
 //     Y_{k+1} = T_k Y_k,  Z_{k+1} = T_k Z_k
 // converges quadratically to Y -> (C/c)^{1/2}, Z -> (C/c)^{-1/2} (all iterates
 // are polynomials in C, so they commute and stay symmetric).  Each step is three
-// K x K products done with mma.sync.m8n8k4.f64 from shared memory -- a
+// K x K products done with mma.sync.m8n8k4.f64 from shared memory, upper tiles
+// only (the products are symmetric) -- a
 // tensor-core replacement for the latency-bound Jacobi rotations.  A direction
 // with lambda ~ 0 never converges: that is reported as RankError
 // (kernels.py:202-206).
@@ -19,33 +20,60 @@ namespace srm {
 
 namespace {
 
-constexpr int kNsThreads = 256;
+constexpr int kNsThreads = 512;
 
 __host__ __device__ constexpr int ns_ld(int kp) { return kp + ((4 - kp) % 16 + 16) % 16; }
 
-// D = A * B for KP x KP matrices in smem (row stride LD); warp w computes the
-// 8-row strips w, w+8, ...; `epi(row, col, v0, v1)` consumes D[row][col..col+1].
+// D = A * B for symmetric products (A, B commuting polynomials in C): only
+// the NT (NT + 1) / 2 upper 8 x 8 tiles are computed, split evenly over the
+// warps (consecutive tiles, so a warp's tiles share row strips), with every
+// tile's k-chain interleaved; `epi(row, col, v0, v1, diag)` consumes
+// D[row][col..col+1] and stores the mirrored entries itself.
+template <int KP>
+struct SymTiles {
+  static constexpr int NT = KP / 8;
+  static constexpr int N = NT * (NT + 1) / 2;
+  static constexpr int W = kNsThreads / 32;
+  static constexpr int PER = (N + W - 1) / W;
+};
+
 template <int KP, typename Epi>
-__device__ __forceinline__ void mm(const double* __restrict__ A, const double* __restrict__ B, Epi epi) {
+__device__ __forceinline__ void mm_sym(const double* __restrict__ A, const double* __restrict__ B, Epi epi) {
   constexpr int LD = ns_ld(KP);
-  constexpr int NT = KP / 8;
+  using TL = SymTiles<KP>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int mt = warp; mt < NT; mt += kNsThreads / 32) {
-    double acc[NT][2];
+  int tm[TL::PER], tn[TL::PER];
+  bool on[TL::PER];
 #pragma unroll
-    for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
-    const double* arow = A + (mt * 8 + (lane >> 2)) * LD + (lane & 3);
-#pragma unroll 2
-    for (int k0 = 0; k0 < KP; k0 += 4) {
-      const double a = arow[k0];
-      const double* brow = B + (k0 + (lane & 3)) * LD + (lane >> 2);
-#pragma unroll
-      for (int n = 0; n < NT; ++n) dmma(acc[n][0], acc[n][1], a, brow[n * 8]);
+  for (int q = 0; q < TL::PER; ++q) {
+    // upper tile index -> (m, n), m <= n, row-major over the upper triangle
+    int idx = warp * TL::PER + q, m = 0;
+    on[q] = idx < TL::N;
+    if (!on[q]) idx = 0;
+    while (idx >= TL::NT - m) {
+      idx -= TL::NT - m;
+      ++m;
     }
-    const int row = mt * 8 + (lane >> 2);
-#pragma unroll
-    for (int n = 0; n < NT; ++n) epi(row, n * 8 + 2 * (lane & 3), acc[n][0], acc[n][1]);
+    tm[q] = m;
+    tn[q] = m + idx;
   }
+  double acc[TL::PER][2];
+#pragma unroll
+  for (int q = 0; q < TL::PER; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll 2
+  for (int k0 = 0; k0 < KP; k0 += 4) {
+#pragma unroll
+    for (int q = 0; q < TL::PER; ++q) {
+      if (on[q]) {
+        const double a = A[(tm[q] * 8 + (lane >> 2)) * LD + k0 + (lane & 3)];
+        const double b = B[(k0 + (lane & 3)) * LD + tn[q] * 8 + (lane >> 2)];
+        dmma(acc[q][0], acc[q][1], a, b);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < TL::PER; ++q)
+    if (on[q]) epi(tm[q] * 8 + (lane >> 2), tn[q] * 8 + 2 * (lane & 3), acc[q][0], acc[q][1], tm[q] == tn[q]);
 }
 
 template <int KP>
@@ -61,12 +89,28 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar(DevPlan p, int init) {
   double* buf[4] = {sm, sm + MAT, sm + 2 * MAT, sm + 3 * MAT};
   const double* Cg = p.bred + (int64_t)i * p.kp * p.ldo + p.ldx;  // A^T A block, row stride ldo
 
-  // Y0 = sym(C) / c (c: Gershgorin bound on lambda_max), Z0 = I; pads are zero
+  // C staged in buf[2] (eight loads in flight per thread), then Y0 = sym(C) / c
+  // (c: Gershgorin bound on lambda_max), Z0 = I; pads are zero
+  double* Cs = buf[2];
+  for (int e0 = 0; e0 < KP * KP; e0 += 8 * kNsThreads) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + tid + u * kNsThreads;
+      const int a = e / KP, b = e - a * KP;
+      v[u] = (e < KP * KP && a < n && b < n) ? Cg[(int64_t)a * p.ldo + b] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + tid + u * kNsThreads;
+      if (e < KP * KP) Cs[(e / KP) * LD + e % KP] = v[u];
+    }
+  }
+  __syncthreads();
   double rowmax = 0.0;
   for (int a = tid; a < KP; a += blockDim.x) {
     double rs = 0.0;
-    for (int b = 0; b < n && a < n; ++b)
-      rs += fabs(0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a]));
+    for (int b = 0; b < n && a < n; ++b) rs += fabs(0.5 * (Cs[a * LD + b] + Cs[b * LD + a]));
     rowmax = fmax(rowmax, rs);
   }
   rowmax = warp_max(rowmax);
@@ -84,7 +128,7 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar(DevPlan p, int init) {
   for (int e = tid; e < KP * LD; e += blockDim.x) {
     const int a = e / LD, b = e - a * LD;
     double y = 0.0;
-    if (a < n && b < n) y = 0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a]) * inv_c;
+    if (a < n && b < n) y = 0.5 * (Cs[a * LD + b] + Cs[b * LD + a]) * inv_c;
     buf[0][e] = y;
     buf[1][e] = (a == b && a < n) ? 1.0 : 0.0;
   }
@@ -103,14 +147,21 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar(DevPlan p, int init) {
       if (q != y && q != z) (f0 < 0 ? f0 : f1) = q;
     double* Tm = buf[f0];
     double* Yn = buf[f1];
-    // P = Z Y -> T = (3I - P)/2 in place, and |I - P|_F^2
+    // P = Z Y -> T = (3I - P)/2 in place, and |I - P|_F^2 (P is symmetric:
+    // off-diagonal tiles count twice)
     double err = 0.0;
-    mm<KP>(buf[z], buf[y], [&](int r, int col, double v0, double v1) {
+    mm_sym<KP>(buf[z], buf[y], [&](int r, int col, double v0, double v1, bool dg) {
       const double d0 = (r == col ? 1.0 : 0.0) - v0, d1 = (r == col + 1 ? 1.0 : 0.0) - v1;
-      if (r < n && col < n) err += d0 * d0;
-      if (r < n && col + 1 < n) err += d1 * d1;
-      Tm[r * LD + col] = 0.5 * (r == col ? 3.0 - v0 : -v0);
-      Tm[r * LD + col + 1] = 0.5 * (r == col + 1 ? 3.0 - v1 : -v1);
+      const double wgt = dg ? 1.0 : 2.0;
+      if (r < n && col < n) err += wgt * d0 * d0;
+      if (r < n && col + 1 < n) err += wgt * d1 * d1;
+      const double t0 = 0.5 * (r == col ? 3.0 - v0 : -v0), t1 = 0.5 * (r == col + 1 ? 3.0 - v1 : -v1);
+      Tm[r * LD + col] = t0;
+      Tm[r * LD + col + 1] = t1;
+      if (!dg) {
+        Tm[col * LD + r] = t0;
+        Tm[(col + 1) * LD + r] = t1;
+      }
     });
     err = block_sum<kNsThreads>(err, red);  // includes a barrier: T is complete
     if (extra == 0) {
@@ -123,15 +174,23 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar(DevPlan p, int init) {
     if (extra < 0 && (err <= 1e-26 || (err < 1e-18 && err > 0.25 * prev_err))) extra = 1;
     prev_err = err;
     // Y_new = T Y  (-> Yn),  Z_new = T Z (-> old Y buffer once Y is consumed)
-    mm<KP>(Tm, buf[y], [&](int r, int col, double v0, double v1) {
+    mm_sym<KP>(Tm, buf[y], [&](int r, int col, double v0, double v1, bool dg) {
       Yn[r * LD + col] = v0;
       Yn[r * LD + col + 1] = v1;
+      if (!dg) {
+        Yn[col * LD + r] = v0;
+        Yn[(col + 1) * LD + r] = v1;
+      }
     });
     __syncthreads();
     double* Zn = buf[y];
-    mm<KP>(Tm, buf[z], [&](int r, int col, double v0, double v1) {
+    mm_sym<KP>(Tm, buf[z], [&](int r, int col, double v0, double v1, bool dg) {
       Zn[r * LD + col] = v0;
       Zn[r * LD + col + 1] = v1;
+      if (!dg) {
+        Zn[col * LD + r] = v0;
+        Zn[(col + 1) * LD + r] = v1;
+      }
     });
     __syncthreads();
     z = y;   // Z now lives in the old Y buffer
@@ -223,8 +282,17 @@ __global__ void __launch_bounds__(256) k_ns_polar_f32(DevPlan p, int init) {
   double rowmax = 0.0;
   for (int a = tid; a < KP; a += blockDim.x) {
     double rs = 0.0;
-    for (int b = 0; b < n && a < n; ++b)
-      rs += fabs(0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a]));
+    for (int b0 = 0; b0 < n && a < n; b0 += 8) {  // eight loads in flight, summed in order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b = b0 + u;
+        v[u] = b < n ? fabs(0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a])) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (b0 + u < n) rs += v[u];
+    }
     rowmax = fmax(rowmax, rs);
   }
   rowmax = warp_max(rowmax);
@@ -239,12 +307,25 @@ __global__ void __launch_bounds__(256) k_ns_polar_f32(DevPlan p, int init) {
   const double c = s_scale;
   const bool degenerate = !(c > 0.0) || !isfinite(c);
   const double inv_c = degenerate ? 0.0 : 1.0 / c;
-  for (int e = tid; e < KP * LD; e += blockDim.x) {
-    const int a = e / LD, b = e - a * LD;
-    float y = 0.f;
-    if (a < n && b < n) y = (float)(0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a]) * inv_c);
-    buf[0][e] = y;
-    buf[1][e] = (a == b && a < n) ? 1.f : 0.f;
+  for (int e0 = 0; e0 < KP * LD; e0 += 4 * 256) {
+    float y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + tid + u * 256;
+      const int a = e / LD, b = e - a * LD;
+      y[u] = (e < KP * LD && a < n && b < n)
+                 ? (float)(0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a]) * inv_c)
+                 : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + tid + u * 256;
+      if (e < KP * LD) {
+        const int a = e / LD, b = e - a * LD;
+        buf[0][e] = y[u];
+        buf[1][e] = (a == b && a < n) ? 1.f : 0.f;
+      }
+    }
   }
   __syncthreads();
   int y = 0, z = 1;

@@ -896,20 +896,30 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_s(DevPlan p) {
   constexpr int LD = 33;  // padded rows: conflict-free S S^T reads
   double* Rt = sm;           // [K][33]
   double* St = sm + K * LD;  // [K][33]
+  double* So = St + K * LD;  // [K][33] S before this E-step (tolerance statistic)
   const int tid = threadIdx.x, col = tid & 31, rg = tid >> 5;
   const int64_t t = t0 + col;
   const bool tin = t < p.ldx;
-  for (int f = rg; f < K; f += 8) Rt[f * LD + col] = tin ? p.red[(int64_t)f * p.ldx + t] : 0.0;
+  stage_rows(Rt, LD, p.red, p.ldx, K, 32, t0, p.ldx);
+  stage_rows(So, LD, p.S, p.ldx, K, 32, t0, p.ldx);
   __syncthreads();
   double quad = 0.0, dsq = 0.0, osq = 0.0;
+  // rows f of C and var_s, one coalesced load per warp, broadcast by shuffles;
+  // the next row's loads are issued before this row's products
+  double cm[4], vr[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = q * 32 + col;
+    cm[q] = (c < K && rg < K) ? p.cmat[rg * kp + c] : 0.0;
+    vr[q] = (c < K && rg < K) ? p.var[rg * kp + c] : 0.0;
+  }
   for (int f = rg; f < K; f += 8) {
-    // rows f of C and var_s, one coalesced load per warp, broadcast by shuffles
-    double cm[4], vr[4];
+    double cmn[4], vrn[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int c = q * 32 + col;
-      cm[q] = (c < K) ? p.cmat[f * kp + c] : 0.0;
-      vr[q] = (c < K) ? p.var[f * kp + c] : 0.0;
+      cmn[q] = (c < K && f + 8 < K) ? p.cmat[(f + 8) * kp + c] : 0.0;
+      vrn[q] = (c < K && f + 8 < K) ? p.var[(f + 8) * kp + c] : 0.0;
     }
     double s = 0.0, y = 0.0;
 #pragma unroll
@@ -933,11 +943,15 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_s(DevPlan p) {
       p.sf[(int64_t)(p.np + f) * p.ldx + t] = sfv - hi;
     }
     if (tin) {
-      double* sp = p.S + (int64_t)f * p.ldx + t;
-      const double old = *sp;
+      const double old = So[f * LD + col];
       dsq += (s - old) * (s - old);
       osq += old * old;
-      *sp = s;
+      p.S[(int64_t)f * p.ldx + t] = s;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      cm[q] = cmn[q];
+      vr[q] = vrn[q];
     }
   }
   __syncthreads();
@@ -1347,7 +1361,7 @@ cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s) {
 }
 
 cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s) {
-  const size_t b2 = (size_t)2 * p.K * 33 * sizeof(double);
+  const size_t b2 = (size_t)3 * p.K * 33 * sizeof(double);
   cudaError_t e = set_smem((const void*)k_tail_s, b2);
   if (e != cudaSuccess) return e;
   k_tail_s<<<p.ntile_tail, kSmallThreads, b2, s>>>(p);
