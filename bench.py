@@ -40,7 +40,20 @@ UNIT = "subject·voxel·TR/s"
 DMMA_PEAK_TFLOPS = 37.1  # tools/fp64_peak.cu on this pool's B200 (mma.sync m8n8k4 f64)
 FALLBACK_HBM_GBS = 6650.0
 TF32_PEAK_TFLOPS = 1664.3 / 2  # tf32 MMA rate = half of the measured bf16 burst (MEASURED_PEAKS.json)
-I8_PEAK_TOPS = 1664.3 * 2      # dense int8 MMA rate = twice the measured bf16 burst (MEASURED_PEAKS.json)
+I8_PEAK_TOPS = 1664.3 * 2      # fallback: twice the measured bf16 burst (MEASURED_PEAKS.json)
+
+
+def i8_peak():
+    """Dense int8 tcgen05 rate measured on this pool by tools/i8_peak.cu
+    (profiles/i8_peak.json, the M = N = 128 shape k_oz_gram issues), else the
+    2 x bf16 fallback."""
+    f = ROOT / "profiles" / "i8_peak.json"
+    try:
+        d = json.loads(f.read_text())
+        return float(d["tops_1sm_128x128"]), ("measured by tools/i8_peak.cu on this pool (profiles/i8_peak.json: "
+                                              "tcgen05.mma kind::i8 M=N=128 from resident smem operands, 148 SMs)")
+    except Exception:  # noqa: BLE001
+        return I8_PEAK_TOPS, "twice the measured bf16 burst peak of MEASURED_PEAKS.json (dense int8 = 2x bf16 rate)"
 
 
 def parse_args():
@@ -399,12 +412,12 @@ def run_ours(args):
             traffic = None
     if dom == "oz_gram":
         achieved_tops = i8_ops / (launch_ms / 1e3) / 1e12
+        i8_pk, i8_src = i8_peak()
         roofline = {
-            "bound": "tensor", "achieved": achieved_tops, "peak": I8_PEAK_TOPS, "unit": "TOPS (int8)",
-            "frac": achieved_tops / I8_PEAK_TOPS, "traffic": traffic, "kernel": dom, "launch_ms": launch_ms,
+            "bound": "tensor", "achieved": achieved_tops, "peak": i8_pk, "unit": "TOPS (int8)",
+            "frac": achieved_tops / i8_pk, "traffic": traffic, "kernel": dom, "launch_ms": launch_ms,
             "algorithmic_int8_ops_per_launch": i8_ops, "algorithmic_flops_per_launch": alg_flops,
-            "algorithmic_bytes_per_launch": alg_bytes,
-            "peak_source": "twice the measured bf16 burst peak of MEASURED_PEAKS.json (dense int8 = 2x bf16 rate)",
+            "algorithmic_bytes_per_launch": alg_bytes, "peak_source": i8_src,
         }
         other_roofline = {
             "bound": "fp64-equivalent", "achieved": achieved_tf, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
