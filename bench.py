@@ -44,14 +44,16 @@ I8_PEAK_TOPS = 1664.3 * 2      # fallback: twice the measured bf16 burst (MEASUR
 
 
 def i8_peak():
-    """Dense int8 tcgen05 rate measured on this pool by tools/i8_peak.cu
-    (profiles/i8_peak.json, the M = N = 128 shape k_oz_gram issues), else the
-    2 x bf16 fallback."""
+    """Sustained dense int8 tcgen05 rate measured on this pool by
+    tools/i8_peak.cu (profiles/i8_peak.json, the M = N = 128 shape k_oz_gram
+    issues), else the 2 x bf16 fallback."""
     f = ROOT / "profiles" / "i8_peak.json"
     try:
         d = json.loads(f.read_text())
-        return float(d["tops_1sm_128x128"]), ("measured by tools/i8_peak.cu on this pool (profiles/i8_peak.json: "
-                                              "tcgen05.mma kind::i8 M=N=128 from resident smem operands, 148 SMs)")
+        return float(d["tops_1sm_128x128_sustained"]), (
+            "sustained dense int8 rate measured by tools/i8_peak.cu on this pool (profiles/i8_peak.json: "
+            "tcgen05.mma kind::i8 M=N=128 from resident smem operands, 148 SMs, ~0.3 s; the burst rate is "
+            f"{d['tops_1sm_128x128']:.0f} TOPS); oz_gram runs 13 ms inside a long step")
     except Exception:  # noqa: BLE001
         return I8_PEAK_TOPS, "twice the measured bf16 burst peak of MEASURED_PEAKS.json (dense int8 = 2x bf16 rate)"
 

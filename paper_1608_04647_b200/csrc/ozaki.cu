@@ -180,6 +180,27 @@ struct OzBars {
   uint64_t accfree;
 };
 
+// descriptor address-field offset (16-byte units) of slice s in a stage: the
+// low half-record box holds slices 0-3 at 32-byte steps, the high box 4-7
+__host__ __device__ constexpr uint64_t oz_slice_off(int s) { return (uint64_t)((s >> 2) * (kOzBox >> 4) + 2 * (s & 3)); }
+
+// the MMAs of one 32-voxel block in pass P: d-groups 0-3 (P = 0) or 4-6
+// (P = 1), pairs s + s' = d with s, s' < NSL, fully unrolled; `keep` = 0
+// starts the accumulators (first block of a chunk)
+template <int NSL, int P>
+__device__ __forceinline__ void oz_issue_pass(uint32_t tmem, uint64_t da0, uint64_t db0, uint32_t idesc,
+                                              uint32_t keep) {
+  constexpr int dlo = P ? 4 : 0, dhi = P ? kOzSlices - 1 : 3;
+#pragma unroll
+  for (int d = dlo; d <= dhi; ++d) {
+    const uint32_t acc = tmem + 128u * (uint32_t)(d - dlo);
+    const int s0 = d - (NSL - 1) > 0 ? d - (NSL - 1) : 0, s1 = d < NSL - 1 ? d : NSL - 1;
+#pragma unroll
+    for (int s = s0; s <= s1; ++s)
+      mma_s8(acc, da0 + oz_slice_off(s), db0 + oz_slice_off(d - s), idesc, s == s0 ? keep : 1u);
+  }
+}
+
 template <int NSL>
 __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant__ CUtensorMap tmq,
                                                            const int32_t* __restrict__ expo, double* __restrict__ G,
@@ -262,18 +283,14 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t sa = smem_u32(smem + slot * kOzStageBytes);
             const uint32_t sb = diag ? sa : sa + 2 * kOzBox;
-            const int first = vb == b0;
-            const int dlo = pass ? 4 : 0, dhi = pass ? kOzSlices - 1 : 3;
-            for (int d = dlo; d <= dhi; ++d) {
-              const uint32_t acc = tmem + 128u * (uint32_t)(d - dlo);
-              const int s0 = max(0, d - (nsl - 1)), s1 = min(d, nsl - 1);
-              for (int s = s0; s <= s1; ++s) {
-                const int s2 = d - s;
-                const uint64_t da = umma_desc_sw128(sa + (s >> 2) * kOzBox + 32 * (s & 3));
-                const uint64_t db = umma_desc_sw128(sb + (s2 >> 2) * kOzBox + 32 * (s2 & 3));
-                mma_s8(acc, da, db, idesc, (first && s == s0) ? 0 : 1);
-              }
-            }
+            // one descriptor per operand; slices are fixed offsets added to
+            // its address field, so each MMA costs two 64-bit adds to issue
+            const uint64_t da0 = umma_desc_sw128(sa), db0 = umma_desc_sw128(sb);
+            const uint32_t keep = vb == b0 ? 0u : 1u;
+            if (pass == 0)
+              oz_issue_pass<nsl, 0>(tmem, da0, db0, idesc, keep);
+            else
+              oz_issue_pass<nsl, 1>(tmem, da0, db0, idesc, keep);
             mma_commit(&bars.empty[slot]);
           }
           mma_commit(&bars.accfull);

@@ -25,6 +25,14 @@
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+__device__ unsigned long long g_clk[2];  // CTA 0: SM cycles and globaltimer ns of its MMA loop
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
@@ -39,10 +47,12 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int CG, int M, int N>
+template <int CG, int M, int N, int NST, int SW = 0>
 __global__ void __launch_bounds__(128, 1) peak(int iters, unsigned long long seed) {
-  // per CTA: A 128 rows x 128 B, B (N / CG) rows x 128 B, SW128 K-major
+  // per CTA and stage: A 128 rows x 128 B, B (N / CG) rows x 128 B, SW128 K-major;
+  // NST stages cycled (NST = 1: the same operands every MMA)
   constexpr int kRowsB = N / CG;
+  constexpr int kStage = (128 + kRowsB) * 128;
   extern __shared__ __align__(1024) unsigned char raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bar;
@@ -50,7 +60,7 @@ __global__ void __launch_bounds__(128, 1) peak(int iters, unsigned long long see
   const int tid = threadIdx.x;
   // random operands (data-dependent power is part of the real workload)
   unsigned long long x = seed ^ (0x9E3779B97F4A7C15ull * (blockIdx.x * 128 + tid + 1));
-  for (int e = tid; e < (128 + kRowsB) * 128 / 8; e += blockDim.x) {
+  for (int e = tid; e < NST * kStage / 8; e += blockDim.x) {
     x ^= x << 13;
     x ^= x >> 7;
     x ^= x << 17;
@@ -83,14 +93,17 @@ __global__ void __launch_bounds__(128, 1) peak(int iters, unsigned long long see
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
   constexpr uint32_t idesc = idesc_i8(M, N);
+  const unsigned long long c0 = clock64(), g0 = gtimer();
   if (tid == 0 && rank == 0) {
-    const uint32_t sa = smem_u32(sm), sb = sa + 128 * 128;
     for (int it = 0; it < iters; ++it) {
+      const uint32_t sa = smem_u32(sm) + (uint32_t)((it % NST) * kStage), sb = sa + 128 * 128;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint64_t da = desc_sw128(sa + 32 * k), db = desc_sw128(sb + 32 * k);
-        const uint32_t acc = tmem + (uint32_t)((it & 1) * (N <= 256 ? N : 0)) % 512u;
-        const uint32_t en = (it | k) ? 1u : 0u;
+        // SW = 0: one accumulator per 4-MMA group (alternating); SW = 1: four
+        // accumulators round-robin, a switch after every MMA (the k_oz_gram d-groups)
+        const uint32_t acc = SW ? tmem + (uint32_t)(k * N) % 512u : tmem + (uint32_t)((it & 1) * (N <= 256 ? N : 0)) % 512u;
+        const uint32_t en = (SW ? it : (it | k)) ? 1u : 0u;
         if (CG == 1)
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -118,6 +131,10 @@ __global__ void __launch_bounds__(128, 1) peak(int iters, unsigned long long see
           "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
           : "=r"(done)
           : "r"(smem_u32(&bar)), "r"(0));
+    if (blockIdx.x == 0) {
+      g_clk[0] = clock64() - c0;
+      g_clk[1] = gtimer() - g0;
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -133,10 +150,12 @@ __global__ void __launch_bounds__(128, 1) peak(int iters, unsigned long long see
   }
 }
 
-template <int CG, int M, int N>
-double run(int sms, int iters) {
-  const size_t smem = (size_t)(128 + N / CG) * 128 + 1024;
-  CK(cudaFuncSetAttribute(peak<CG, M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+static double g_mhz = 0.0;  // effective SM clock of the last run (CTA 0)
+
+template <int CG, int M, int N, int NST = 1, int SW = 0>
+double run(int sms, int iters, int reps = 5) {
+  const size_t smem = (size_t)NST * (128 + N / CG) * 128 + 1024;
+  CK(cudaFuncSetAttribute(peak<CG, M, N, NST, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sms / CG * CG);
   cfg.blockDim = dim3(128);
@@ -148,15 +167,15 @@ double run(int sms, int iters) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  for (int w = 0; w < 2; ++w) CK(cudaLaunchKernelEx(&cfg, peak<CG, M, N>, iters / 8, 7ull));
+  for (int w = 0; w < 2; ++w) CK(cudaLaunchKernelEx(&cfg, peak<CG, M, N, NST, SW>, iters / 8, 7ull));
   CK(cudaDeviceSynchronize());
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   float best = 1e30f;
-  for (int rep = 0; rep < 5; ++rep) {
+  for (int rep = 0; rep < reps; ++rep) {
     CK(cudaEventRecord(a));
-    CK(cudaLaunchKernelEx(&cfg, peak<CG, M, N>, iters, 11ull + rep));
+    CK(cudaLaunchKernelEx(&cfg, peak<CG, M, N, NST, SW>, iters, 11ull + rep));
     CK(cudaEventRecord(b));
     CK(cudaEventSynchronize(b));
     float ms = 0.f;
@@ -164,6 +183,9 @@ double run(int sms, int iters) {
     if (ms < best) best = ms;
   }
   CK(cudaGetLastError());
+  unsigned long long clk[2];
+  CK(cudaMemcpyFromSymbol(clk, g_clk, sizeof(clk)));
+  g_mhz = clk[1] ? (double)clk[0] / (double)clk[1] * 1e3 : 0.0;
   const double ops = 2.0 * M * N * 32.0 * 4.0 * iters * (double)(sms / CG);
   return ops / (best * 1e-3) / 1e12;
 }
@@ -175,8 +197,19 @@ int main(int argc, char** argv) {
   const double a = run<1, 128, 128>(sms, iters);
   const double b = run<1, 128, 256>(sms, iters);
   const double c = run<2, 256, 256>(sms, iters);
+  const double ar = run<1, 128, 128, 6>(sms, iters);
+  const double br = run<1, 128, 256, 4>(sms, iters);
+  const double cr = run<2, 256, 256, 6>(sms, iters);
+  const double asw = run<1, 128, 128, 6, 1>(sms, iters);
+  const double burst_mhz = g_mhz;
+  // sustained: ~0.3 s of back-to-back MMAs (the clock the power controller
+  // settles at under a long int8 load, as inside the Gram precompute)
+  const double sus = run<1, 128, 128, 6>(sms, iters * 256, 2);
+  const double sus_mhz = g_mhz;
   printf("{\"sms\": %d, \"iters\": %d, \"tops_1sm_128x128\": %.1f, \"tops_1sm_128x256\": %.1f, "
-         "\"tops_2sm_256x256\": %.1f}\n",
-         sms, iters, a, b, c);
+         "\"tops_2sm_256x256\": %.1f, \"tops_1sm_128x128_rot6\": %.1f, \"tops_1sm_128x256_rot4\": %.1f, "
+         "\"tops_2sm_256x256_rot6\": %.1f, \"tops_1sm_128x128_rot6_accswitch\": %.1f, \"burst_sm_mhz\": %.0f, "
+         "\"tops_1sm_128x128_sustained\": %.1f, \"sustained_sm_mhz\": %.0f}\n",
+         sms, iters, a, b, c, ar, br, cr, asw, burst_mhz, sus, sus_mhz);
   return 0;
 }
