@@ -404,3 +404,19 @@ def test_batched_finalize_readback_is_bit_identical(srm):
         b = srm.fit(_subjects(srm, xs), cfg, algorithm=algorithm, keep_on_device=True)
         for wa, wb in zip(a.W, b.W):
             assert np.array_equal(wa, wb.cpu().numpy()), algorithm
+
+
+def test_eager_two_lane_iteration_matches_graph(srm):
+    """srm_e_step / srm_m_step issued eagerly (side-stream stages joined per
+    call) == the captured one-iteration graph, bit for bit, on both paths."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(6, 800, 140, 9, seed=21)
+    cfg = srm.SrmConfig(k=9, iterations=4, seed=3)
+    for algorithm in ("gram", "stream"):
+        a = srm.fit(_subjects(srm, xs), cfg, algorithm=algorithm, graphs=True)
+        b = srm.fit(_subjects(srm, xs), cfg, algorithm=algorithm, graphs=False)
+        assert np.array_equal(a.S, b.S) and np.array_equal(a.sigma_s, b.sigma_s), algorithm
+        assert a.log_likelihood == b.log_likelihood, algorithm
+        for wa, wb in zip(a.W, b.W):
+            assert np.array_equal(wa, wb), algorithm
