@@ -467,6 +467,37 @@ class SrmEngine:
         side.synchronize()
         return host.numpy()
 
+    def start_mu_readback(self):
+        """Copy model.mu (final once the upload and demean are done) into
+        pinned memory on the side stream while the EM runs."""
+        torch = _torch()
+        main = torch.cuda.current_stream(self.device)
+        side = self._side_stream()
+        self._mu_host = torch.empty(tuple(self.mu.shape), dtype=self.mu.dtype, pin_memory=True)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            self._mu_host.copy_(self.mu, non_blocking=True)
+        self._mu_event = torch.cuda.Event()
+        self._mu_event.record(side)
+
+    def mu_host(self):
+        """numpy model.mu from start_mu_readback (or a synchronous copy)."""
+        if getattr(self, "_mu_host", None) is None:
+            return hostio.to_host(self.mu)
+        self._mu_event.synchronize()
+        return self._mu_host.numpy()
+
+    def small_results_to_host(self, n_done):
+        """rho^2 of the local subjects, the history rows, S and Sigma_s in one
+        batch of asynchronous copies to pinned memory and one synchronise."""
+        torch = _torch()
+        srcs = [self.local_rho2(), self.hist[:n_done], self.S.contiguous(), self.sigma.contiguous()]
+        outs = [torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True) for t in srcs]
+        for o, t in zip(outs, srcs):
+            o.copy_(t, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return [o.numpy() for o in outs]
+
     def _side_stream(self):
         torch = _torch()
         if getattr(self, "_d2h_stream", None) is None:

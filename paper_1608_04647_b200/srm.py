@@ -502,6 +502,8 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
         eng.set_iteration(0)
     else:
         eng.init_kernels()
+    if not keep_on_device:
+        eng.start_mu_readback()  # mu is final after the demean: read it back under the EM
     clock.tick("init")
 
     n_done = 0
@@ -565,7 +567,11 @@ class _PhaseClock:
 
 def _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device, wout=None):
     torch = _torch()
-    rho2_local = eng.local_rho2().clone()
+    if not keep_on_device:
+        rho2_np, hist, S_np, sigma_np = eng.small_results_to_host(n_done)
+        rho2_local = torch.from_numpy(rho2_np.copy())
+    else:
+        rho2_local = eng.local_rho2().clone()
     # final rho^2 gather + rho0 refresh (srm.py:289-313)
     if comm.size > 1:
         m = max(eng.counts)
@@ -585,7 +591,8 @@ def _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device, wo
     else:
         rho2_all = rho2_local.cpu().numpy()
     rho0 = float(np.add.reduce(1.0 / rho2_all))
-    hist = eng.hist[:n_done].cpu().numpy()
+    if keep_on_device:
+        hist = eng.hist[:n_done].cpu().numpy()
     rho2_hist = hist[:, _lib.H_RHO2: _lib.H_RHO2 + eng.n_local]
     objective = [float(np.mean(r)) for r in rho2_hist]
     lls = [float(x) for x in hist[:, _lib.H_LL]]
@@ -599,11 +606,11 @@ def _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device, wo
         # (reused once an earlier model is released); the arrays are views of it
         if wout is None:
             wout = hostio.to_pinned(eng.wout)
-        muh = hostio.to_host(eng.mu)
+        muh = eng.mu_host()  # pinned too; mu_i are views of it like W_i
         W = [wout[eng.subject_rows(j)] for j in range(eng.n_local)]
-        mu = [muh[eng.subject_rows(j)].copy() for j in range(eng.n_local)]
-        S = np.ascontiguousarray(eng.S.cpu().numpy())
-        sigma = np.ascontiguousarray(eng.sigma.cpu().numpy())
+        mu = [muh[eng.subject_rows(j)] for j in range(eng.n_local)]
+        S = np.array(S_np)
+        sigma = np.array(sigma_np)
     model = SrmModel(
         subject_ids=[s.subject_id for s in subjects],
         subject_indices=list(range(offset, offset + len(subjects))),

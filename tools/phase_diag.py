@@ -38,8 +38,13 @@ timed(srm, "_storage_for")
 timed(srm, "gram_int8_bytes")
 timed(srm, "choose_algorithm")
 timed(torch.cuda, "mem_get_info")
+timed(engine.SrmEngine, "small_results_to_host")
+timed(engine.SrmEngine, "mu_host")
+timed(engine.SrmEngine, "finalize_to_host")
+timed(engine.SrmEngine, "start_mu_readback")
 timed(srm, "ThreadPoolExecutor", "pool_create")
 timed(srm.SrmConfig, "validate")
+timed(srm, "_collect")
 
 n, V, T, K, iters = (int(a) for a in sys.argv[1:6])
 xs, _, _ = recipe_torch(n, V, T, K, seed=0, dtype="f64")
