@@ -190,10 +190,12 @@ class SrmEngine:
         n_stage = 3
         done = [None] * n_stage
         next_g = 0
-        # side-stream batches: each Gram launch should fill the 148 SMs (1 CTA/SM per
-        # 128 x 128 tile); without the Gram, about eight batches per load
+        # side-stream batches: each Gram launch should fill the 148 SMs in one wave
+        # (1 CTA/SM per 128 x 128 tile; cfg 2: 4 subjects x 36 tiles), which also
+        # keeps the work left after the last upload to one wave; without the
+        # Gram, about eight batches per load
         nt = -(-self.ldx // 128)
-        batch = max(1, -(-148 // (nt * (nt + 1) // 2))) if (gram and self.gram) else max(1, -(-self.n_local // 8))
+        batch = max(1, 148 // (nt * (nt + 1) // 2)) if (gram and self.gram) else max(1, -(-self.n_local // 8))
         init_pending = []  # (first, end, demean event) batches waiting for their draws
 
         def upload_ready_draws(nxt, upto):
