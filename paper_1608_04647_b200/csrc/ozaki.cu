@@ -313,16 +313,27 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int dlo = pass ? 4 : 0, dhi = pass ? kOzSlices - 1 : 3;
         for (int c0 = 0; c0 < 128; c0 += 16) {
+          // pass 2 adds to pass 1's values: their loads go out first
+          double prev[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            prev[j] = (npass > 0 && rin && it.n0 + c0 + j < ldx) ? grow[c0 + j] : 0.0;
           double val[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) val[j] = 0.0;
-          for (int d = dlo; d <= dhi; ++d) {
-            uint32_t raw[16];
-            tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 128u * (uint32_t)(d - dlo) + c0, raw);
-            tmem_wait_ld();
-            const double sd = pow2(-12 - 7 * d);
+          // the (up to four) d-groups of these 16 columns in flight, one wait
+          uint32_t raw[4][16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) val[j] = fma((double)(int32_t)raw[j], sd, val[j]);
+          for (int q = 0; q < 4; ++q)
+            if (dlo + q <= dhi) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 128u * (uint32_t)q + c0, raw[q]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (dlo + q <= dhi) {
+              const double sd = pow2(-12 - 7 * (dlo + q));
+#pragma unroll
+              for (int j = 0; j < 16; ++j) val[j] = fma((double)(int32_t)raw[q][j], sd, val[j]);
+            }
           }
           if (rin) {
 #pragma unroll
@@ -330,7 +341,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
               const int64_t tb = it.n0 + c0 + j;
               if (tb < ldx) {
                 const double g = val[j] * pow2(ea + ex[tb]);
-                grow[c0 + j] = (npass == 0) ? g : grow[c0 + j] + g;
+                grow[c0 + j] = (npass == 0) ? g : prev[j] + g;
               }
             }
           }
@@ -546,13 +557,16 @@ __global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_
       double val[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) val[j] = 0.0;
+      // all d-groups of the 16 columns in flight, one wait
+      uint32_t raw[ND][16];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 64u * (uint32_t)d + c0, raw[d]);
+      tmem_wait_ld();
+#pragma unroll
       for (int d = 0; d < ND; ++d) {
-        uint32_t raw[16];
-        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 64u * (uint32_t)d + c0, raw);
-        tmem_wait_ld();
         const double sd = pow2(-12 - 7 * d);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) val[j] = fma((double)(int32_t)raw[j], sd, val[j]);
+        for (int j = 0; j < 16; ++j) val[j] = fma((double)(int32_t)raw[d][j], sd, val[j]);
       }
       if (valid) {
 #pragma unroll
