@@ -122,6 +122,8 @@ struct srm_plan {
   cudaStream_t side_stream = nullptr;  // second lane of the stage lists
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   Lanes lanes{};
+  std::vector<cudaEvent_t> gram_events;  // per-batch "slices ready" of the pipelined Gram
+  cudaStream_t hi_stream = nullptr;      // high-priority stream of the pipelined Gram
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   TmaMap tm_x_a, tm_s, tm_a, tm_x_b;  // tensor-core path TMA maps (bound at srm_plan_bind)
@@ -841,6 +843,8 @@ int srm_plan_destroy(srm_plan* plan) {
     if (plan->side_stream) cudaStreamDestroy(plan->side_stream);
     if (plan->ev_fork) cudaEventDestroy(plan->ev_fork);
     if (plan->ev_join) cudaEventDestroy(plan->ev_join);
+    for (cudaEvent_t ev : plan->gram_events) cudaEventDestroy(ev);
+    if (plan->hi_stream) cudaStreamDestroy(plan->hi_stream);
   }
   delete plan;
   return SRM_OK;
@@ -1104,6 +1108,49 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
   if (first < 0 || count < 0 || first + count > p->n_local) return fail(SRM_ERR_CONFIG, "subject range out of bounds");
   if (count == 0) return SRM_OK;
   cudaStream_t st = as_stream(stream);
+  // int8 Gram of more than one wave of tiles: batches of one wave, the
+  // slicing of every batch on the side stream (17 KB CTAs that fit beside the
+  // Gram's) and each batch's Gram, mirror and G slices on `st` after its slices
+  const int per = p->ldx / 128 > 0 ? (int)(p->items_oz.size() / std::max(p->n_local, 1)) : 1;
+  const int batch = std::max(1, 148 / std::max(per, 1));
+  if ((p->flags & SRM_FLAG_GRAM_I8) && count > batch) {
+    const Lanes* ln = nullptr;
+    int rc = plan_lanes(p, &ln);
+    if (rc) return rc;
+    const int nb = (count + batch - 1) / batch;
+    while ((int)p->gram_events.size() < nb) {
+      cudaEvent_t ev;
+      const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "gram events");
+      p->gram_events.push_back(ev);
+    }
+    // the Gram batches run on a high-priority stream, so their CTAs are
+    // dispatched ahead of pending slicing CTAs as SMs free up
+    if (!p->hi_stream) {
+      int lo = 0, hi = 0;
+      cudaError_t e0 = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if (e0 == cudaSuccess) e0 = cudaStreamCreateWithPriority(&p->hi_stream, cudaStreamNonBlocking, hi);
+      if (e0 != cudaSuccess) return cuda_fail(e0, "gram stream");
+    }
+    cudaStream_t gs = p->hi_stream;
+    cudaError_t e = cudaEventRecord(ln->fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ln->side, ln->fork, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(gs, ln->fork, 0);
+    for (int b = 0; b < nb && e == cudaSuccess; ++b) {
+      const int f = first + b * batch, n = std::min(batch, first + count - f);
+      e = gram_stages(p, f, n)[0].fn(ln->side);  // oz_split
+      if (e == cudaSuccess) e = cudaEventRecord(p->gram_events[b], ln->side);
+    }
+    for (int b = 0; b < nb && e == cudaSuccess; ++b) {
+      const int f = first + b * batch, n = std::min(batch, first + count - f);
+      e = cudaStreamWaitEvent(gs, p->gram_events[b], 0);
+      const std::vector<Stage> v = gram_stages(p, f, n);
+      for (size_t k = 1; k < v.size() && e == cudaSuccess; ++k) e = v[k].fn(gs);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(ln->join, gs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ln->join, 0);
+    return check(e, "prepare_gram");
+  }
   for (const Stage& s : gram_stages(p, first, count)) {
     const cudaError_t e = s.fn(st);
     if (e != cudaSuccess) return cuda_fail(e, s.name);

@@ -22,7 +22,7 @@
 // Kernels (the column maxima max |x[:, t]| come from the demean pass, k_prep):
 //   oz_split   slices, transposed: Q[i][t][vb][slot][32 voxels] (int8; a
 //              256-byte record per (t, 32-voxel block): slices 0-3 in the low
-//              128 bytes, 4-6 (+ a zero slot) in the high 128 bytes; fp32
+//              128 bytes, 4-6 (+ an unused slot) in the high 128 bytes; fp32
 //              X-hat: four slices in 128-byte records)
 //   oz_gram    one 128 x 128 upper tile per CTA: TMA (SWIZZLE_128B, 128-byte
 //              rows) -> tcgen05.mma kind::i8 (M = N = 128, K = 32 voxels; the
@@ -64,9 +64,12 @@ __device__ __forceinline__ int frexp_exp(double m) {
 }
 
 // ---------------------------------------------------------------------------
-// split: grid (32-voxel blocks, 128-column tiles, subjects); thread (t, half)
-// handles 16 voxels of one column, 4 voxels per packed 32-bit word
+// split: grid (32-voxel blocks, 64-column tiles, subjects); thread (t, quarter)
+// handles 8 voxels of one column, 4 voxels per packed 32-bit word.  17 KB of
+// shared memory per CTA, so split CTAs fit beside a resident k_oz_gram CTA
+// (193 KB) and the slicing of later subjects overlaps the Gram of earlier ones.
 // ---------------------------------------------------------------------------
+constexpr int kSplitCols = 64;
 constexpr int kSplitLdw = 68;  // words per smem row: 16-byte aligned, conflict-free uint4 access
 
 // rint(y) for |y| < 2^51 by the 1.5 * 2^52 shift; the rounded integer is also
@@ -86,33 +89,33 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
                                                   int8_t* __restrict__ q, int64_t lq, int32_t* __restrict__ expo) {
   constexpr int nsl = NSL;
   constexpr int rec = NSL <= 4 ? 128 : 256;
-  __shared__ __align__(16) uint32_t buf[128 * kSplitLdw];
+  __shared__ __align__(16) uint32_t buf[kSplitCols * kSplitLdw];
   const int i = blockIdx.z;
   const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
   const int64_t row0 = sj[SC_ROW_OFF], V = sj[SC_V];
   const int64_t vb = blockIdx.x;
   if (vb * 32 >= V) return;
-  const int64_t t0 = (int64_t)blockIdx.y * 128;
-  const int tl = threadIdx.x & 127, half = threadIdx.x >> 7;
+  const int64_t t0 = (int64_t)blockIdx.y * kSplitCols;
+  const int tl = threadIdx.x & (kSplitCols - 1), quarter = threadIdx.x / kSplitCols;
   const int64_t t = t0 + tl;
   const bool tin = t < p.ldx;
   int e = 0;
   if (tin) {
     const double m = __longlong_as_double((long long)cmax[(int64_t)i * p.ldx + t]);
     e = (m > 0.0) ? frexp_exp(m) : 0;
-    if (vb == 0 && half == 0) expo[(int64_t)i * p.ldx + t] = e;
+    if (vb == 0 && quarter == 0) expo[(int64_t)i * p.ldx + t] = e;
   }
-  TX xv[16];
+  TX xv[8];
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int64_t v = vb * 32 + half * 16 + u;
+  for (int u = 0; u < 8; ++u) {
+    const int64_t v = vb * 32 + quarter * 8 + u;
     xv[u] = (tin && v < V) ? xhat[(row0 + v) * p.ldx + t] : TX(0);
   }
-  uint32_t w[NSL][4];
+  uint32_t w[NSL][2];
 #pragma unroll
   for (int s = 0; s < NSL; ++s)
 #pragma unroll
-    for (int g = 0; g < 4; ++g) w[s][g] = 0u;
+    for (int g = 0; g < 2; ++g) w[s][g] = 0u;
   // y = x 2^(6 - e), |y| < 64; digit s = rint(y), then y = (y - rint(y)) * 128.
   // Every step is exact in the input's own precision, so fp32 X-hat slices in
   // fp32 arithmetic (twice the fp64 rate) with the same digits as in fp64.
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
       const float scale = __int_as_float((127 + 6 - e) << 23);
       const float magic = 12582912.0f;  // 1.5 * 2^23: rint for |y| < 2^22, low byte = digit
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < 8; ++u) {
         float y = xv[u] * scale;
 #pragma unroll
         for (int s = 0; s < NSL; ++s) {
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
     // 2^(6 - e) exactly (normal range: |e| < 1000)
     const double scale = __longlong_as_double((long long)(1023 + 6 - e) << 52);
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
+    for (int u = 0; u < 8; ++u) {
       double y = to_f64(xv[u]) * scale;  // |y| < 64
 #pragma unroll
       for (int s = 0; s < NSL; ++s) {
@@ -149,18 +152,18 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
       }
     }
   }
-  // record layout per t: 16-byte chunk (slot * 2 + half); slots >= nsl stay zero
-  uint4* row = reinterpret_cast<uint4*>(buf + tl * kSplitLdw);
+  // record layout per t: slot s = 8 words (32 voxels), this quarter's 8 voxels
+  // at words 2 quarter, 2 quarter + 1 (slots >= nsl: zero in smem, not stored)
+  uint2* row = reinterpret_cast<uint2*>(buf + tl * kSplitLdw);
   const int nslot = rec / 32;
 #pragma unroll
   for (int s = 0; s < 8; ++s)
-    if (s < nslot)
-      row[s * 2 + half] = (s < nsl) ? make_uint4(w[s][0], w[s][1], w[s][2], w[s][3])
-                                                      : make_uint4(0u, 0u, 0u, 0u);
+    if (s < nslot) row[s * 4 + quarter] = (s < nsl) ? make_uint2(w[s][0], w[s][1]) : make_uint2(0u, 0u);
   __syncthreads();
-  // 128 rows x rec / 16 chunks of 16 bytes; consecutive threads write one record
-  const int nch = rec / 16;
-  for (int c = threadIdx.x; c < 128 * nch; c += blockDim.x) {
+  // kSplitCols rows x rec / 16 chunks of 16 bytes; consecutive threads write one
+  // record.  Slot 7 of a seven-slice record is never read by an MMA: not written.
+  const int nch = nsl == 7 ? 14 : rec / 16;
+  for (int c = threadIdx.x; c < kSplitCols * nch; c += blockDim.x) {
     const int r = c / nch, k = c % nch;
     const int64_t tt = t0 + r;
     if (tt < p.ldx) {
@@ -677,7 +680,7 @@ cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first,
   const unsigned long long* cm = cmax + (int64_t)first * p.ldx;
   int8_t* qs = q + (int64_t)first * p.ldx * lq;
   int32_t* ex = expo + (int64_t)first * p.ldx;
-  const dim3 g2((unsigned)((max_v + 31) / 32), (unsigned)((p.ldx + 127) / 128), (unsigned)count);
+  const dim3 g2((unsigned)((max_v + 31) / 32), (unsigned)((p.ldx + kSplitCols - 1) / kSplitCols), (unsigned)count);
   if (x_dtype == SRM_F64)
     k_oz_split<double, 7><<<g2, 256, 0, st>>>(sub, static_cast<const double*>(p.xhat), cm, qs, lq, ex);
   else

@@ -105,8 +105,8 @@ cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_sigma(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_mirror_gram(const DevPlan& p, int first, int count, cudaStream_t s);
-// int8-sliced Gram (ozaki.cu): column maxima, exponents and slices of local
-// subjects [first, first + count)
+// int8-sliced Gram (ozaki.cu): exponents and slices of local subjects
+// [first, first + count) (the column maxima come from the demean pass)
 cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first, int count,
                               unsigned long long* cmax, int8_t* q, int64_t lq, int32_t* expo, int64_t max_v,
                               cudaStream_t st);
