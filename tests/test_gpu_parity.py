@@ -250,7 +250,7 @@ def _gram_pair(xs):
     return out
 
 
-@pytest.mark.parametrize("case", ["recipe", "ragged_t300", "heavy_tails", "long_v"])
+@pytest.mark.parametrize("case", ["recipe", "ragged_t300", "heavy_tails", "long_v", "pipelined"])
 def test_int8_gram_matches_fp64(srm, case):
     """The int8-sliced X^T X (7 slices, exact int32 sums) vs fp64 DMMA and numpy."""
     from paper_1608_04647_b200.data import recipe_numpy
@@ -264,6 +264,8 @@ def test_int8_gram_matches_fp64(srm, case):
     elif case == "heavy_tails":  # Student t (2 dof): column max / rms ~ 10-100
         xs = [rng.standard_t(2, size=(3000, 200)) for _ in range(2)]
         tol = 1e-11
+    elif case == "pipelined":  # T = 1000: 36 tiles per subject, Gram batches of 4 behind the side-stream slicing
+        xs = [rng.standard_normal((v, 1000)) for v in (700, 911, 640, 1003, 777, 850, 690, 1200, 530, 960)]
     else:  # > 65536 voxels: the int32 accumulators are flushed per 65536-voxel chunk
         xs = [rng.standard_normal((70000, 64))]
     g_dmma, g_i8 = _gram_pair(xs)
@@ -420,3 +422,4 @@ def test_eager_two_lane_iteration_matches_graph(srm):
         assert a.log_likelihood == b.log_likelihood, algorithm
         for wa, wb in zip(a.W, b.W):
             assert np.array_equal(wa, wb), algorithm
+
