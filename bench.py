@@ -350,7 +350,10 @@ def run_ours(args):
     st = torch.cuda.current_stream()
     prof_iter = {}
     for _ in range(5):
-        for name, t_ms in eng.profile_iteration():
+        one = {}
+        for name, t_ms in eng.profile_iteration():  # a stage may run once per subject half
+            one[name] = one.get(name, 0.0) + t_ms
+        for name, t_ms in one.items():
             prof_iter.setdefault(name, []).append(t_ms)
     prof_iter = {k_: float(np.mean(v_)) for k_, v_ in prof_iter.items()}
     once = {}

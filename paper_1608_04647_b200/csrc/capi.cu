@@ -86,10 +86,10 @@ void srm::set_last_error(const char* where, cudaError_t e) {
   g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
 }
 
-// side stream + fork/join events of a plan (the stage lists' second lane)
+// side streams + fork/join events of a plan (the stage lists' lanes 1 and 2)
 struct Lanes {
-  cudaStream_t side;
-  cudaEvent_t fork, join;
+  cudaStream_t side[3];
+  cudaEvent_t fork[3], join[3];
 };
 
 struct srm_plan {
@@ -119,9 +119,8 @@ struct srm_plan {
   char* ws = nullptr;
   DevPlan dp{};
   cudaStream_t cap_stream = nullptr;
-  cudaStream_t side_stream = nullptr;  // second lane of the stage lists
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  Lanes lanes{};
+  Lanes lanes{};            // side lanes of the stage lists (created on first use)
+  bool lanes_ready = false;
   std::vector<cudaEvent_t> gram_events;  // per-batch "slices ready" of the pipelined Gram
   cudaStream_t hi_stream = nullptr;      // high-priority stream of the pipelined Gram
   cudaGraph_t graph = nullptr;
@@ -471,8 +470,9 @@ int check(cudaError_t e, const char* where) { return e == cudaSuccess ? SRM_OK :
 struct Stage {
   const char* name;
   std::function<cudaError_t(cudaStream_t)> fn;
-  int lane = 0;       // 1: on the plan's side stream, after everything issued before it
-  bool join = false;  // the side stream's work completes before this stage
+  int lane = 0;       // 1 or 2: on that side stream
+  bool join = false;  // both side streams' work completes before this stage
+  bool fork = true;   // a side-lane stage starts after everything issued on the main lane so far
 };
 
 void contraction_stages(srm_plan* p, std::vector<Stage>& out) {
@@ -527,9 +527,37 @@ std::vector<Stage> m_stages(srm_plan* p) {
                      return launch_oz_slice_rows(d.S, p->ldx, p->kp, p->ldx, region<int8_t>(p, I_OZS), p->oz_lqg,
                                                  region<int32_t>(p, I_OZSEXP), st);
                    }});
+      if (p->n_local >= 2) {
+        // two subject halves, the second on side lane 2: the first half's
+        // A^T A, polar and next E-step term fill the SMs the second half's
+        // last wave of B tiles leaves idle
+        const int h = p->n_local / 2;
+        DevPlan da = d, db = d;
+        da.sub0 = 0;
+        da.nsub = h;
+        db.sub0 = h;
+        db.nsub = p->n_local - h;
+        auto sg = [p, d](int first, int count) {
+          return [p, d, first, count](cudaStream_t st) {
+            return launch_oz_sg(p->tm_g, p->tm_sq, region<int32_t>(p, I_OZGEXP), region<int32_t>(p, I_OZSEXP),
+                                d.bred, p->ldx, p->kp, p->ldo, first, count, st);
+          };
+        };
+        v.push_back({"oz_sg", sg(h, p->n_local - h), 2});
+        v.push_back({"oz_sg", sg(0, h)});
+        v.push_back({"gram_from_b", [db](cudaStream_t st) { return launch_gram_from_b(db, st); }, 2, false, false});
+        v.push_back({"gram_from_b", [da](cudaStream_t st) { return launch_gram_from_b(da, st); }});
+        v.push_back({"eig_polar", [db](cudaStream_t st) { return launch_eig_polar(db, 0, st); }, 2, false, false});
+        v.push_back({"eig_polar", [da](cudaStream_t st) { return launch_eig_polar(da, 0, st); }});
+        v.push_back({"apply_m", [db](cudaStream_t st) { return launch_apply_m(db, 1, st); }, 2, false, false});
+        v.push_back({"apply_m", [da](cudaStream_t st) { return launch_apply_m(da, 1, st); }});
+        push_finalize_rho(d, v);
+        return v;
+      }
       v.push_back({"oz_sg", [p, d](cudaStream_t st) {
                      return launch_oz_sg(p->tm_g, p->tm_sq, region<int32_t>(p, I_OZGEXP),
-                                         region<int32_t>(p, I_OZSEXP), d.bred, p->ldx, p->kp, p->ldo, p->n_local, st);
+                                         region<int32_t>(p, I_OZSEXP), d.bred, p->ldx, p->kp, p->ldo, 0, p->n_local,
+                                         st);
                    }});
     } else {
       v.push_back({"gram_b", [p, d](cudaStream_t st) {
@@ -571,46 +599,55 @@ std::vector<Stage> m_stages(srm_plan* p) {
   return v;
 }
 
-// Without `ln` every stage runs in order on `st`; with it, lane-1 stages run
-// on the side stream (forked from `st` where they appear) and `st` waits for
-// them at the next join stage and at the end of the list.  Graph capture
+// Without `ln` every stage runs in order on `st`; with it, lane-1/2 stages run
+// on the side streams (forked from `st` where they appear, unless fork is
+// false: then they only follow their lane's earlier stages) and `st` waits
+// for them at the next join stage and at the end of the list.  Graph capture
 // turns the fork/join events into graph edges.
 int run_stages(const std::vector<Stage>& stages, cudaStream_t st, const Lanes* ln = nullptr) {
-  bool pending = false;
+  bool pending[3] = {false, false, false};
   for (const Stage& s : stages) {
     cudaStream_t target = st;
     cudaError_t e = cudaSuccess;
-    if (ln && s.join && pending) {
-      e = cudaStreamWaitEvent(st, ln->join, 0);
-      pending = false;
-    }
-    if (ln && s.lane == 1 && e == cudaSuccess) {
-      e = cudaEventRecord(ln->fork, st);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(ln->side, ln->fork, 0);
-      target = ln->side;
+    if (ln && s.join)
+      for (int l = 1; l <= 2 && e == cudaSuccess; ++l)
+        if (pending[l]) {
+          e = cudaStreamWaitEvent(st, ln->join[l], 0);
+          pending[l] = false;
+        }
+    const int L = ln ? s.lane : 0;
+    if (L > 0 && e == cudaSuccess) {
+      if (s.fork) {
+        e = cudaEventRecord(ln->fork[L], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ln->side[L], ln->fork[L], 0);
+      }
+      target = ln->side[L];
     }
     if (e == cudaSuccess) e = s.fn(target);
-    if (ln && s.lane == 1 && e == cudaSuccess) {
-      e = cudaEventRecord(ln->join, ln->side);
-      pending = true;
+    if (L > 0 && e == cudaSuccess) {
+      e = cudaEventRecord(ln->join[L], ln->side[L]);
+      pending[L] = true;
     }
     if (e != cudaSuccess) return cuda_fail(e, s.name);
   }
-  if (pending) {
-    cudaError_t e = cudaStreamWaitEvent(st, ln->join, 0);
-    if (e != cudaSuccess) return cuda_fail(e, "join");
-  }
+  for (int l = 1; l <= 2; ++l)
+    if (pending[l]) {
+      cudaError_t e = cudaStreamWaitEvent(st, ln->join[l], 0);
+      if (e != cudaSuccess) return cuda_fail(e, "join");
+    }
   return SRM_OK;
 }
 
 int plan_lanes(srm_plan* p, const Lanes** out) {
-  if (!p->side_stream) {
-    cudaError_t e = cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming);
-    if (e != cudaSuccess) return cuda_fail(e, "side stream");
+  if (!p->lanes_ready) {
+    for (int l = 1; l <= 2; ++l) {
+      cudaError_t e = cudaStreamCreateWithFlags(&p->lanes.side[l], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->lanes.fork[l], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->lanes.join[l], cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "side stream");
+    }
+    p->lanes_ready = true;
   }
-  p->lanes = Lanes{p->side_stream, p->ev_fork, p->ev_join};
   *out = &p->lanes;
   return SRM_OK;
 }
@@ -840,9 +877,12 @@ int srm_plan_destroy(srm_plan* plan) {
     if (plan->graph_exec) cudaGraphExecDestroy(plan->graph_exec);
     if (plan->graph) cudaGraphDestroy(plan->graph);
     if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
-    if (plan->side_stream) cudaStreamDestroy(plan->side_stream);
-    if (plan->ev_fork) cudaEventDestroy(plan->ev_fork);
-    if (plan->ev_join) cudaEventDestroy(plan->ev_join);
+    if (plan->lanes_ready)
+      for (int l = 1; l <= 2; ++l) {
+        cudaStreamDestroy(plan->lanes.side[l]);
+        cudaEventDestroy(plan->lanes.fork[l]);
+        cudaEventDestroy(plan->lanes.join[l]);
+      }
     for (cudaEvent_t ev : plan->gram_events) cudaEventDestroy(ev);
     if (plan->hi_stream) cudaStreamDestroy(plan->hi_stream);
   }
@@ -949,7 +989,7 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
       e = make_map_q(&p->tm_g, region<int8_t>(p, I_OZG), p->oz_lqg, p->ldx, p->n_local, 128);
       if (e == cudaSuccess) e = make_map_q(&p->tm_sq, region<int8_t>(p, I_OZS), p->oz_lqg, p->kp, 1, 64);
       if (e == cudaSuccess)
-        e = launch_oz_sg(p->tm_g, p->tm_sq, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, 0, 0);
+        e = launch_oz_sg(p->tm_g, p->tm_sq, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, 0, 0, 0);
     }
     if (e == cudaSuccess && p->oz_w) {
       e = make_map_q5(&p->tm_q32, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, p->oz_nsl);
@@ -1133,13 +1173,13 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
       if (e0 != cudaSuccess) return cuda_fail(e0, "gram stream");
     }
     cudaStream_t gs = p->hi_stream;
-    cudaError_t e = cudaEventRecord(ln->fork, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ln->side, ln->fork, 0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(gs, ln->fork, 0);
+    cudaError_t e = cudaEventRecord(ln->fork[1], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ln->side[1], ln->fork[1], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(gs, ln->fork[1], 0);
     for (int b = 0; b < nb && e == cudaSuccess; ++b) {
       const int f = first + b * batch, n = std::min(batch, first + count - f);
-      e = gram_stages(p, f, n)[0].fn(ln->side);  // oz_split
-      if (e == cudaSuccess) e = cudaEventRecord(p->gram_events[b], ln->side);
+      e = gram_stages(p, f, n)[0].fn(ln->side[1]);  // oz_split
+      if (e == cudaSuccess) e = cudaEventRecord(p->gram_events[b], ln->side[1]);
     }
     for (int b = 0; b < nb && e == cudaSuccess; ++b) {
       const int f = first + b * batch, n = std::min(batch, first + count - f);
@@ -1147,8 +1187,8 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
       const std::vector<Stage> v = gram_stages(p, f, n);
       for (size_t k = 1; k < v.size() && e == cudaSuccess; ++k) e = v[k].fn(gs);
     }
-    if (e == cudaSuccess) e = cudaEventRecord(ln->join, gs);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ln->join, 0);
+    if (e == cudaSuccess) e = cudaEventRecord(ln->join[1], gs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ln->join[1], 0);
     return check(e, "prepare_gram");
   }
   for (const Stage& s : gram_stages(p, first, count)) {

@@ -450,6 +450,7 @@ struct RowGemmArgs {
   double* out;           // kRowSG: bred; kRowW: W [rows_total][K]
   const OzItem* items;   // kRowW: {subject, local voxel v0, global row of v0, valid rows}
   int64_t ldx, kp, ldo, K;
+  int first;             // kRowSG: subject of blockIdx.y = 0
 };
 
 // NSA: slices of the A operand (kRowW: X-hat's 7 or 4; kRowSG: G's 7).
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_
   OzItem it{};
   if (MODE == kRowW) it = g.items[blockIdx.x];
   const int t0 = MODE == kRowSG ? blockIdx.x * 128 : 0;
-  const int i = MODE == kRowSG ? blockIdx.y : it.subj;
+  const int i = MODE == kRowSG ? g.first + (int)blockIdx.y : it.subj;
   const int arow = MODE == kRowSG ? t0 : it.n0;  // first A row (TR of G_i / global voxel row)
   const int az = MODE == kRowSG ? i : 0;
   const int bz = MODE == kRowSG ? 0 : i;
@@ -645,9 +646,9 @@ cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, const RowGemmArgs& g
 }  // namespace
 
 cudaError_t launch_oz_sg(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
-                         double* bred, int64_t ldx, int64_t kp, int64_t ldo, int n_local, cudaStream_t st) {
-  RowGemmArgs g{gexp, sexp, bred, nullptr, ldx, kp, ldo, 0};
-  return run_rowgemm<kRowSG, kOzSlices, 7>(tmg, tms, g, dim3((unsigned)((ldx + 127) / 128), (unsigned)n_local), st);
+                         double* bred, int64_t ldx, int64_t kp, int64_t ldo, int first, int count, cudaStream_t st) {
+  RowGemmArgs g{gexp, sexp, bred, nullptr, ldx, kp, ldo, 0, first};
+  return run_rowgemm<kRowSG, kOzSlices, 7>(tmg, tms, g, dim3((unsigned)((ldx + 127) / 128), (unsigned)count), st);
 }
 
 cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* expo, double* rt, int64_t ldx,
@@ -660,7 +661,7 @@ cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* exp
 
 cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* rexp, double* W, const OzItem* items,
                         int n_items, int64_t ldx, int64_t kp, int64_t K, int nsl, cudaStream_t st) {
-  RowGemmArgs g{nullptr, rexp, W, items, ldx, kp, 0, K};
+  RowGemmArgs g{nullptr, rexp, W, items, ldx, kp, 0, K, 0};
   if (nsl == 7) return run_rowgemm<kRowW, 7, 7>(tmqt, tmr, g, dim3((unsigned)n_items, 1), st);
   // all seven d-groups for fp32 X-hat too: R's slices beyond the fourth carry
   // bits the orthonormality of W needs (W^T W = I to ~1e-13)

@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(kSmallThreads, KP <= 64 ? 3 : 1) k_gram_from_b
   extern __shared__ __align__(16) double sm[];
   constexpr int NT = KP / 8;
   constexpr int MS = (NT + 7) / 8;
-  const int c = blockIdx.x, i = blockIdx.y;
+  const int c = blockIdx.x, i = p.sub0 + blockIdx.y;
   const int K = (int)p.K;
   double* Bs = sm;              // [KP][kGfbLd], rows >= K zero
   double* Ss = sm + KP * kGfbLd;
@@ -1315,7 +1315,8 @@ cudaError_t launch_gram_from_b(const DevPlan& p, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   DevPlan arg = p;
   void* args[] = {&arg};
-  e = cudaLaunchKernel(fn, dim3((unsigned)p.gfb_chunks, (unsigned)p.n_local), dim3(kSmallThreads), args, bytes, s);
+  if (p.nsub == 0) return cudaSuccess;
+  e = cudaLaunchKernel(fn, dim3((unsigned)p.gfb_chunks, (unsigned)p.nsub), dim3(kSmallThreads), args, bytes, s);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
