@@ -250,20 +250,31 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
       for (int c = 0; c < nchunks; ++c) {
         const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
         for (int pass = 0; pass < kPasses; ++pass) {
-          for (int vb = b0; vb < b1; ++vb, ++k) {
+          // slices 4..6 (the records' high halves) only for pass 2 of seven-slice
+          // data; a low-half-only pass packs two 32-voxel blocks per stage
+          const bool hi = pass && nsl > 4;
+          const int step = hi ? 1 : 2;
+          for (int vb = b0; vb < b1; vb += step, ++k) {
             const int slot = k % kOzStages;
             if (k >= kOzStages) mbar_wait(&bars.empty[slot], ((k / kOzStages) - 1) & 1);
-            // slices 4..6 (the records' high halves) only for pass 2 of seven-slice data
-            const bool hi = pass && nsl > 4;
-            const int nbox = (hi ? 2 : 1) * (diag ? 1 : 2);
+            const int nj = min(step, b1 - vb);
+            const int nbox = (hi ? 2 : nj) * (diag ? 1 : 2);
             mbar_expect_tx(&bars.full[slot], (uint32_t)(nbox * kOzBox));
             unsigned char* st = smem + slot * kOzStageBytes;
             const int x = vb * oz_record_bytes(nsl);
-            tma_load_3d(st, &tmq, x, it.m0, it.subj, &bars.full[slot]);
-            if (hi) tma_load_3d(st + kOzBox, &tmq, x + 128, it.m0, it.subj, &bars.full[slot]);
-            if (!diag) {
-              tma_load_3d(st + 2 * kOzBox, &tmq, x, it.n0, it.subj, &bars.full[slot]);
-              if (hi) tma_load_3d(st + 3 * kOzBox, &tmq, x + 128, it.n0, it.subj, &bars.full[slot]);
+            if (hi) {  // [A lo][A hi][B lo][B hi]
+              tma_load_3d(st, &tmq, x, it.m0, it.subj, &bars.full[slot]);
+              tma_load_3d(st + kOzBox, &tmq, x + 128, it.m0, it.subj, &bars.full[slot]);
+              if (!diag) {
+                tma_load_3d(st + 2 * kOzBox, &tmq, x, it.n0, it.subj, &bars.full[slot]);
+                tma_load_3d(st + 3 * kOzBox, &tmq, x + 128, it.n0, it.subj, &bars.full[slot]);
+              }
+            } else {   // [A lo vb][A lo vb + 1][B lo vb][B lo vb + 1]
+              for (int j = 0; j < nj; ++j) {
+                const int xj = (vb + j) * oz_record_bytes(nsl);
+                tma_load_3d(st + j * kOzBox, &tmq, xj, it.m0, it.subj, &bars.full[slot]);
+                if (!diag) tma_load_3d(st + (2 + j) * kOzBox, &tmq, xj, it.n0, it.subj, &bars.full[slot]);
+              }
             }
           }
         }
@@ -280,7 +291,9 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
           // the epilogue must have drained the previous pass's accumulators
           if (npass > 0) mbar_wait(&bars.accfree, (npass - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          for (int vb = b0; vb < b1; ++vb, ++k) {
+          const bool hi = pass && nsl > 4;
+          const int step = hi ? 1 : 2;
+          for (int vb = b0; vb < b1; vb += step, ++k) {
             const int slot = k % kOzStages;
             mbar_wait(&bars.full[slot], (k / kOzStages) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -290,10 +303,20 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
             // its address field, so each MMA costs two 64-bit adds to issue
             const uint64_t da0 = umma_desc_sw128(sa), db0 = umma_desc_sw128(sb);
             const uint32_t keep = vb == b0 ? 0u : 1u;
-            if (pass == 0)
-              oz_issue_pass<nsl, 0>(tmem, da0, db0, idesc, keep);
-            else
+            if (hi) {
               oz_issue_pass<nsl, 1>(tmem, da0, db0, idesc, keep);
+            } else {
+              // the stage's second block sits one box after the first (A and B alike)
+              const uint64_t box = (uint64_t)(kOzBox >> 4);
+              const int nj = min(step, b1 - vb);
+              if (pass == 0) {
+                oz_issue_pass<nsl, 0>(tmem, da0, db0, idesc, keep);
+                if (nj > 1) oz_issue_pass<nsl, 0>(tmem, da0 + box, db0 + box, idesc, 1u);
+              } else {
+                oz_issue_pass<nsl, 1>(tmem, da0, db0, idesc, keep);
+                if (nj > 1) oz_issue_pass<nsl, 1>(tmem, da0 + box, db0 + box, idesc, 1u);
+              }
+            }
             mma_commit(&bars.empty[slot]);
           }
           mma_commit(&bars.accfull);
