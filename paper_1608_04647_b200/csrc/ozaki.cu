@@ -545,17 +545,22 @@ __global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t sa = smem_u32(smem + slot * kStage);
         const uint32_t sb = sa + Shape::a_bytes;
+        // one descriptor per operand and stage; a slice is a constant offset of
+        // the 16-byte address field (no carry: smem addresses < 2^18)
+        const uint64_t da0 = MODE == kRowSG ? umma_desc_sw128(sa) : umma_desc_sw32_mn(sa, 1024, 256);
+        const uint64_t db0 = umma_desc_sw128(sb);
+        const uint32_t keep = k == 0 ? 0u : 1u;
 #pragma unroll
         for (int d = 0; d < ND; ++d) {
           const uint32_t acc = tmem + 64u * (uint32_t)d;
-          const int s1 = min(d, NSA - 1);
+          const int s1 = d < NSA - 1 ? d : NSA - 1;
 #pragma unroll
           for (int s = 0; s <= s1; ++s) {
             const int s2 = d - s;
-            const uint64_t da = MODE == kRowSG ? umma_desc_sw128(sa + (s >> 2) * kOzBox + 32 * (s & 3))
-                                               : umma_desc_sw32_mn(sa + s * 4096, 1024, 256);
-            const uint64_t db = umma_desc_sw128(sb + (s2 >> 2) * kSgBoxS + 32 * (s2 & 3));
-            mma_s8(acc, da, db, idesc, (k == 0 && s == 0) ? 0 : 1);
+            const uint64_t aoff = MODE == kRowSG ? (uint64_t)((s >> 2) * (kOzBox >> 4) + 2 * (s & 3))
+                                                 : (uint64_t)(s * (4096 >> 4));
+            const uint64_t boff = (uint64_t)((s2 >> 2) * (kSgBoxS >> 4) + 2 * (s2 & 3));
+            mma_s8(acc, da0 + aoff, db0 + boff, idesc, s == 0 ? keep : 1u);
           }
         }
         mma_commit(&empty[slot]);
