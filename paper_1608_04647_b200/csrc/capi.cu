@@ -987,13 +987,13 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     if (e == cudaSuccess) e = launch_oz_gram(p->tm_q, nullptr, nullptr, p->ldx, nullptr, 0, p->oz_nsl, 0);
     if (e == cudaSuccess && p->oz_sg) {
       e = make_map_q(&p->tm_g, region<int8_t>(p, I_OZG), p->oz_lqg, p->ldx, p->n_local, 128);
-      if (e == cudaSuccess) e = make_map_q(&p->tm_sq, region<int8_t>(p, I_OZS), p->oz_lqg, p->kp, 1, 64);
+      if (e == cudaSuccess) e = make_map_q8(&p->tm_sq, region<int8_t>(p, I_OZS), p->oz_lqg, p->kp, 1);
       if (e == cudaSuccess)
         e = launch_oz_sg(p->tm_g, p->tm_sq, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, 0, 0, 0);
     }
     if (e == cudaSuccess && p->oz_w) {
       e = make_map_q5(&p->tm_q32, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, p->oz_nsl);
-      if (e == cudaSuccess) e = make_map_q(&p->tm_r, region<int8_t>(p, I_OZR), p->oz_lqg, p->kp, p->n_local, 64);
+      if (e == cudaSuccess) e = make_map_q8(&p->tm_r, region<int8_t>(p, I_OZR), p->oz_lqg, p->kp, p->n_local);
       if (e == cudaSuccess)
         e = launch_oz_w(p->tm_q32, p->tm_r, nullptr, nullptr, nullptr, 0, p->ldx, p->kp, p->K, p->oz_nsl, 0);
     }

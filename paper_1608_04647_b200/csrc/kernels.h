@@ -77,6 +77,7 @@ constexpr int64_t kOzRecord = 256;    // bytes per (row, 32-column block): 8 slo
 inline __host__ __device__ int oz_record_bytes(int nsl) { return nsl <= 4 ? 128 : 256; }
 cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n, int box_rows);
 cudaError_t make_map_q5(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, int64_t n, int nsl);
+cudaError_t make_map_q8(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n);
 // int8 slices of the rows of a row-major fp64 matrix (ozaki.cu): 2^e[r] >= max|M[r][:]|
 cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int64_t ncols, int8_t* q, int64_t lq,
                                  int32_t* expo, cudaStream_t st);

@@ -449,7 +449,6 @@ __global__ void __launch_bounds__(256) k_oz_slice_rows(const double* __restrict_
 // folded into R), so W[v][f] = 2^{r_f} sum_d 2^{-12-7d} (...)[v][f].
 // ---------------------------------------------------------------------------
 constexpr int kSgStages = 4;
-constexpr int kSgBoxS = 8192;  // 64 rows x 128 B
 enum RowGemmMode { kRowSG = 0, kRowW = 1 };
 
 // Per-stage shared memory of k_oz_rowgemm<MODE, NSA, ND>: the A boxes (kRowSG:
@@ -461,9 +460,11 @@ template <int MODE, int NSA, int ND>
 struct RowGemmShape {
   static constexpr int halves = ND > 4 ? 2 : 1;
   static constexpr int a_bytes = MODE == kRowSG ? halves * kOzBox : NSA * 4096;
-  static constexpr int stage_bytes = a_bytes + halves * kSgBoxS;
-  static constexpr uint32_t tmem_cols = ND > 4 ? 512 : 256;
-  static constexpr int ctas_per_sm = ND > 4 ? 1 : 2;
+  // B: the eight slots of 64 rows x 32 B (k-block of 32 TRs), slot-major
+  static constexpr int b_bytes = 8 * 64 * 32;
+  static constexpr int stage_bytes = a_bytes + b_bytes;
+  static constexpr uint32_t tmem_cols = 512;  // eight 64-column d-groups (d = 7 unused)
+  static constexpr int ctas_per_sm = 1;
   static constexpr size_t smem_bytes = (size_t)kSgStages * stage_bytes + 1024;
 };
 
@@ -531,14 +532,16 @@ __global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_
           // Q records of 32 TRs x 4 voxel blocks x nsa slots -> [slot][vb][t][32 B]
           tma_load_5d(st, &tma, 0, k * 32, it.m0 / 32, 0, i, &full[slot]);
         }
-        tma_load_3d(st + Shape::a_bytes, &tmb, x, f0, bz, &full[slot]);
-        if (Shape::halves > 1) tma_load_3d(st + Shape::a_bytes + kSgBoxS, &tmb, x + 128, f0, bz, &full[slot]);
+        tma_load_4d(st + Shape::a_bytes, &tmb, 0, f0, k * 8, bz, &full[slot]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // kRowW: A (voxels x TRs) is MN-major (bit 15): voxels contiguous in the Q records
-      constexpr uint32_t idesc = idesc_s8(128, 64) | (MODE == kRowW ? (1u << 15) : 0u);
+      // kRowW: A (voxels x TRs) is MN-major (bit 15): voxels contiguous in the Q records.
+      // N = 128: B is the slot pair (s2, s2 + 1) of 64 features each, so one MMA
+      // feeds d-groups s + s2 and s + s2 + 1 (adjacent 64-column accumulators);
+      // an N = 64 MMA costs the same tensor-pipe time as N = 128 (tools/i8_peak.cu)
+      constexpr uint32_t idesc = idesc_s8(128, 128) | (MODE == kRowW ? (1u << 15) : 0u);
       for (int k = 0; k < nub; ++k) {
         const int slot = k % kSgStages;
         mbar_wait(&full[slot], (k / kSgStages) & 1);
@@ -548,20 +551,19 @@ __global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_
         // one descriptor per operand and stage; a slice is a constant offset of
         // the 16-byte address field (no carry: smem addresses < 2^18)
         const uint64_t da0 = MODE == kRowSG ? umma_desc_sw128(sa) : umma_desc_sw32_mn(sa, 1024, 256);
-        const uint64_t db0 = umma_desc_sw128(sb);
+        // K-major SWIZZLE_32B: 8-row atoms of 256 B (SBO); slot j starts at 2 KB j
+        const uint64_t db0 = umma_desc_sw32_mn(sb, 16, 256);
         const uint32_t keep = k == 0 ? 0u : 1u;
+        // s = 0 first: its four pairs cover all eight d-groups once, so they alone
+        // start the accumulators of a fresh tile
 #pragma unroll
-        for (int d = 0; d < ND; ++d) {
-          const uint32_t acc = tmem + 64u * (uint32_t)d;
-          const int s1 = d < NSA - 1 ? d : NSA - 1;
+        for (int s = 0; s < NSA; ++s) {
+          const uint64_t aoff = MODE == kRowSG ? (uint64_t)((s >> 2) * (kOzBox >> 4) + 2 * (s & 3))
+                                               : (uint64_t)(s * (4096 >> 4));
 #pragma unroll
-          for (int s = 0; s <= s1; ++s) {
-            const int s2 = d - s;
-            const uint64_t aoff = MODE == kRowSG ? (uint64_t)((s >> 2) * (kOzBox >> 4) + 2 * (s & 3))
-                                                 : (uint64_t)(s * (4096 >> 4));
-            const uint64_t boff = (uint64_t)((s2 >> 2) * (kSgBoxS >> 4) + 2 * (s2 & 3));
-            mma_s8(acc, da0 + aoff, db0 + boff, idesc, s == 0 ? keep : 1u);
-          }
+          for (int s2 = 0; s2 + s <= ND - 1; s2 += 2)
+            mma_s8(tmem + 64u * (uint32_t)(s + s2), da0 + aoff, db0 + (uint64_t)(s2 * (2048 >> 4)), idesc,
+                   s == 0 ? keep : 1u);
         }
         mma_commit(&empty[slot]);
       }

@@ -483,6 +483,24 @@ cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 4-D int8 map over row-slice records R[n][rows][ldx / 32][8 slots][32 B] with
+// the dims ordered {32 B, row, slot index (k-block * 8 + slot), n}
+// (non-monotonic strides) and box {32, 64, 8, 1}, SWIZZLE_32B: one load lands
+// as [slot][row][32 B], so slots j and j + 1 of 64 rows form one 128-row
+// K-major SW32 operand (the N = 128 slice pairs of the int8 row GEMMs)
+cudaError_t make_map_q8(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  cuuint64_t dims[4] = {32, (cuuint64_t)rows, (cuuint64_t)(lq / 32), (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)lq, 32, (cuuint64_t)(lq * rows)};
+  cuuint32_t box[4] = {32, 64, 8, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(m->opaque), CU_TENSOR_MAP_DATA_TYPE_UINT8, 4,
+                  const_cast<int8_t*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 // 5-D int8 map over the same records Q[n][ldx][nvb][8 slots][32 voxels] with the
 // dims ordered {32 voxels, TR, voxel block, slot, subject} (non-monotonic
 // strides) and box {32, 32, 4, 7, 1}, SWIZZLE_32B: one load lands as

@@ -201,6 +201,8 @@ int main(int argc, char** argv) {
   const double br = run<1, 128, 256, 4>(sms, iters);
   const double cr = run<2, 256, 256, 6>(sms, iters);
   const double asw = run<1, 128, 128, 6, 1>(sms, iters);
+  const double n64 = run<1, 128, 64, 6>(sms, iters);
+  const double n32 = run<1, 128, 32, 6>(sms, iters);
   const double burst_mhz = g_mhz;
   // sustained: ~0.3 s of back-to-back MMAs (the clock the power controller
   // settles at under a long int8 load, as inside the Gram precompute)
@@ -209,7 +211,8 @@ int main(int argc, char** argv) {
   printf("{\"sms\": %d, \"iters\": %d, \"tops_1sm_128x128\": %.1f, \"tops_1sm_128x256\": %.1f, "
          "\"tops_2sm_256x256\": %.1f, \"tops_1sm_128x128_rot6\": %.1f, \"tops_1sm_128x256_rot4\": %.1f, "
          "\"tops_2sm_256x256_rot6\": %.1f, \"tops_1sm_128x128_rot6_accswitch\": %.1f, \"burst_sm_mhz\": %.0f, "
-         "\"tops_1sm_128x128_sustained\": %.1f, \"sustained_sm_mhz\": %.0f}\n",
-         sms, iters, a, b, c, ar, br, cr, asw, burst_mhz, sus, sus_mhz);
+         "\"tops_1sm_128x128_sustained\": %.1f, \"sustained_sm_mhz\": %.0f, \"tops_1sm_128x64_rot6\": %.1f, "
+         "\"tops_1sm_128x32_rot6\": %.1f}\n",
+         sms, iters, a, b, c, ar, br, cr, asw, burst_mhz, sus, sus_mhz, n64, n32);
   return 0;
 }
