@@ -591,6 +591,11 @@ __global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_
       double val[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) val[j] = 0.0;
+      // the columns' scale exponents, loaded ahead of the stores (no aliasing
+      // with them to wait on)
+      int be[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) be[j] = (f0 + c0 + j < fmax_) ? __ldg(bexp + f0 + c0 + j) : 0;
       // all d-groups of the 16 columns in flight, one wait
       uint32_t raw[ND][16];
 #pragma unroll
@@ -606,8 +611,7 @@ __global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int f = f0 + c0 + j;
-          if (f < fmax_)
-            out[(int64_t)(MODE == kRowSG ? f : c0 + j) * fstride] = val[j] * pow2(et + bexp[f] + half);
+          if (f < fmax_) out[(int64_t)(MODE == kRowSG ? f : c0 + j) * fstride] = val[j] * pow2(et + be[j] + half);
         }
       }
     }
