@@ -423,3 +423,25 @@ def test_eager_two_lane_iteration_matches_graph(srm):
         for wa, wb in zip(a.W, b.W):
             assert np.array_equal(wa, wb), algorithm
 
+
+
+def test_cfg2_full_size_vs_oracle(srm):
+    """BASELINE cfg 2 at full size (40 x 30000 x 1000, K=50, fp64) through the
+    default path (int8 Gram, int8 B = S G, int8 final W) vs the oracle, every
+    one of the first three iterations."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(40, 30000, 1000, 50, seed=2)
+    ref = orc.run_em(xs, 50, 3, seed=0)
+    for n in (1, 3):
+        eng = []
+        # the path auto picks at the BASELINE's 20 iterations (at 1-3 it would stream)
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=50, iterations=n, seed=0), engine_out=eng,
+                    algorithm="gram")
+        assert eng[0].gram and eng[0].gram_i8
+        r = ref["iters"][n - 1]
+        _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, f"cfg2 it{n - 1}")
+        for j in range(n):
+            assert abs(m.log_likelihood[j] - ref["iters"][j]["ll"]) <= TOL64 * abs(ref["iters"][j]["ll"])
+        for w in m.W:
+            assert np.max(np.abs(w.T @ w - np.eye(50))) <= 1e-8
