@@ -318,8 +318,8 @@ def test_fit_manifest_streams_sfab(srm, tmp_path):
     assert a.rho2 == b.rho2
 
 
-def test_int8_gram_large_k_falls_back(srm):
-    """K = 72 (> 64): int8 X^T X, fp64 DMMA for B = S G / 2 and the final W."""
+def test_int8_gram_k72_two_feature_halves(srm):
+    """K = 72 (kp > 64): the int8 row GEMMs (B = S G / 2, final W) in two 64-feature halves."""
     from paper_1608_04647_b200.data import recipe_numpy
 
     xs, _, _ = recipe_numpy(3, 2500, 256, 72, seed=15)
@@ -445,3 +445,21 @@ def test_cfg2_full_size_vs_oracle(srm):
             assert abs(m.log_likelihood[j] - ref["iters"][j]["ll"]) <= TOL64 * abs(ref["iters"][j]["ll"])
         for w in m.W:
             assert np.max(np.abs(w.T @ w - np.eye(50))) <= 1e-8
+
+
+def test_int8_path_extreme_magnitudes(srm):
+    """Subjects scaled by 1e40, 1e-40 and 1: the per-column / per-row
+    power-of-two scales of the int8 slices span ~2^±133 (G and S G ~2^±270),
+    far outside int8 and fp32 range, and the fit still matches the oracle.
+    (The polar through A^T A squares |A|: the fp64 range bounds |A| < 1e154,
+    a limit the reference's SVD of A does not have.)"""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(3, 600, 200, 5, seed=17)
+    xs = [xs[0] * 1e40, xs[1] * 1e-40, xs[2]]
+    ref = orc.run_em(xs, 5, 3, seed=4)
+    eng = []
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=5, iterations=3, seed=4), algorithm="gram", engine_out=eng)
+    assert eng[0].gram_i8
+    r = ref["iters"][-1]
+    _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, "extreme magnitudes")
