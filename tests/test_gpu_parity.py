@@ -463,3 +463,47 @@ def test_int8_path_extreme_magnitudes(srm):
     assert eng[0].gram_i8
     r = ref["iters"][-1]
     _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, "extreme magnitudes")
+
+
+# --------------------------------------------------------------------------
+# BASELINE cfg 3 / 4 / 5 at their full per-subject shapes (V, T, K, fp32
+# storage, cfg 4's smoothed W_i).  The oracle cannot run 16 / 256 / 128
+# subjects of these sizes in a test, so each case takes the first few
+# subjects of the config's seeded recipe (same V, T, K, dtype, recipe) and
+# two EM iterations on both device algorithms; the fp32 tolerance applies.
+# --------------------------------------------------------------------------
+
+_FULL_SHAPES = {
+    # name: (subjects kept, V, T, K, smooth)
+    "cfg3": (2, 200000, 2000, 100, None),
+    "cfg4": (4, 50000, 1000, 64, 5.0),
+    "cfg5": (3, 100000, 1000, 100, None),
+}
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5"])
+def test_fp32_configs_full_shape_vs_oracle(srm, cfg):
+    import torch
+
+    from paper_1608_04647_b200.data import recipe_torch
+
+    n, V, T, K, smooth = _FULL_SHAPES[cfg]
+    xd, _, _ = recipe_torch(n, V, T, K, seed=5, smooth=smooth, dtype="f32")
+    xs = [x.cpu().numpy() for x in xd]
+    del xd
+    torch.cuda.empty_cache()
+    iters = 2
+    ref = orc.run_em(xs, K, iters, seed=0)
+    for algorithm in ("gram", "stream"):
+        eng = []
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=K, iterations=iters, seed=0), algorithm=algorithm,
+                    engine_out=eng)
+        assert eng[0].gram == (algorithm == "gram"), (cfg, algorithm)
+        r = ref["iters"][-1]
+        _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL32, f"{cfg} {algorithm}")
+        for j in range(iters):
+            assert abs(m.log_likelihood[j] - ref["iters"][j]["ll"]) <= TOL32 * abs(ref["iters"][j]["ll"])
+        for w in m.W:
+            assert np.max(np.abs(w.T @ w - np.eye(K))) <= 1e-8, (cfg, algorithm)
+        del m
+        torch.cuda.empty_cache()
