@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <functional>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -77,6 +78,8 @@ enum Internal {
   I_OZR,
   I_OZREXP,
   I_ITEMS_OW,
+  I_OZSKPART,
+  I_OZSKFLAG,
   I_COUNT
 };
 
@@ -137,6 +140,8 @@ struct srm_plan {
   std::vector<OzItem> items_ow;       // 128-voxel tiles of the final int8 W = Xhat R
   std::vector<int> ow_first;          // [n_local + 1]: first items_ow entry of each subject
   TmaMap tm_q32, tm_r;
+  bool sk_off = false;                // SRM_B200_SG_PER_TILE=1: per-tile B = S G / 2 (test knob)
+  int sk_ctas = 0;                    // stream-K B = S G / 2: persistent CTAs (SMs less two for the side lane)
 };
 
 namespace {
@@ -200,13 +205,15 @@ void layout(srm_plan* p) {
   const int gfb_chunks = (int)((p->ldx + kGfbCols - 1) / kGfbCols);
   sz[I_GFBPART] = (int64_t)p->n_local * gfb_chunks * kp2 * 8;
   sz[I_GFBCOUNT] = (int64_t)p->n_local * 4;
-  sz[I_OZG] = p->oz_sg ? (int64_t)p->n_local * p->ldx * p->oz_lqg : 0;
+  sz[I_OZG] = p->oz_sg ? (int64_t)p->n_local * (int64_t)oz_tiled_bytes(p->ldx, p->ldx) : 0;
   sz[I_OZGEXP] = p->oz_sg ? (int64_t)p->n_local * p->ldx * 4 : 0;
   sz[I_OZS] = p->oz_sg ? p->kp * p->oz_lqg : 0;
   sz[I_OZSEXP] = p->oz_sg ? p->kp * 4 : 0;
   sz[I_OZR] = p->oz_w ? (int64_t)p->n_local * p->kp * p->oz_lqg : 0;
   sz[I_OZREXP] = p->oz_w ? (int64_t)p->n_local * p->kp * 4 : 0;
   sz[I_ITEMS_OW] = (int64_t)p->items_ow.size() * sizeof(OzItem);
+  sz[I_OZSKPART] = p->oz_sg ? (int64_t)p->sk_ctas * oz_sk_park_bytes() : 0;
+  sz[I_OZSKFLAG] = p->oz_sg ? (int64_t)p->sk_ctas * 4 : 0;
   int64_t cur = 0;
   for (int r = 0; r < I_COUNT; ++r) {
     p->off[r] = cur;
@@ -334,6 +341,18 @@ void build_work(srm_plan* p) {
   p->oz_sg = (p->flags & SRM_FLAG_GRAM_I8) && p->kp <= 128;
   p->oz_lqg = p->ldx / 32 * kOzRecord;
   p->oz_w = p->oz_sg;
+  {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        sms <= 0) {
+      cudaGetLastError();
+      sms = 148;
+    }
+    p->sk_ctas = std::max(1, sms - 2);
+    // test knob: the per-tile grid (k_oz_rowgemm<kRowSG>) instead of stream-K, to show both agree bit for bit
+    const char* env = getenv("SRM_B200_SG_PER_TILE");
+    p->sk_off = env && env[0] == '1';
+  }
   p->items_ow.clear();
   p->ow_first.assign(1, 0);
   for (int i = 0; i < p->n_local; ++i) {
@@ -527,37 +546,19 @@ std::vector<Stage> m_stages(srm_plan* p) {
                      return launch_oz_slice_rows(d.S, p->ldx, p->kp, p->ldx, region<int8_t>(p, I_OZS), p->oz_lqg,
                                                  region<int32_t>(p, I_OZSEXP), st);
                    }});
-      if (p->n_local >= 2) {
-        // two subject halves, the second on side lane 2: the first half's
-        // A^T A, polar and next E-step term fill the SMs the second half's
-        // last wave of B tiles leaves idle
-        const int h = p->n_local / 2;
-        DevPlan da = d, db = d;
-        da.sub0 = 0;
-        da.nsub = h;
-        db.sub0 = h;
-        db.nsub = p->n_local - h;
-        auto sg = [p, d](int first, int count) {
-          return [p, d, first, count](cudaStream_t st) {
-            return launch_oz_sg(p->tm_g, p->tm_sq, region<int32_t>(p, I_OZGEXP), region<int32_t>(p, I_OZSEXP),
-                                d.bred, p->ldx, p->kp, p->ldo, first, count, st);
-          };
-        };
-        v.push_back({"oz_sg", sg(h, p->n_local - h), 2});
-        v.push_back({"oz_sg", sg(0, h)});
-        v.push_back({"gram_from_b", [db](cudaStream_t st) { return launch_gram_from_b(db, st); }, 2, false, false});
-        v.push_back({"gram_from_b", [da](cudaStream_t st) { return launch_gram_from_b(da, st); }});
-        v.push_back({"eig_polar", [db](cudaStream_t st) { return launch_eig_polar(db, 0, st); }, 2, false, false});
-        v.push_back({"eig_polar", [da](cudaStream_t st) { return launch_eig_polar(da, 0, st); }});
-        v.push_back({"apply_m", [db](cudaStream_t st) { return launch_apply_m(db, 1, st); }, 2, false, false});
-        v.push_back({"apply_m", [da](cudaStream_t st) { return launch_apply_m(da, 1, st); }});
-        push_finalize_rho(d, v);
-        return v;
-      }
+      // stream-K over all local subjects: every SM the same number of MMAs
+      if (p->sk_off)
+        v.push_back({"oz_sg", [p, d](cudaStream_t st) {
+                       return launch_oz_sg(p->tm_g, p->tm_sq, region<int32_t>(p, I_OZGEXP),
+                                           region<int32_t>(p, I_OZSEXP), d.bred, p->ldx, p->kp, p->ldo, 0, p->n_local,
+                                           st);
+                     }});
+      else
       v.push_back({"oz_sg", [p, d](cudaStream_t st) {
-                     return launch_oz_sg(p->tm_g, p->tm_sq, region<int32_t>(p, I_OZGEXP),
-                                         region<int32_t>(p, I_OZSEXP), d.bred, p->ldx, p->kp, p->ldo, 0, p->n_local,
-                                         st);
+                     return launch_oz_sg_sk(p->tm_g, p->tm_sq, region<int32_t>(p, I_OZGEXP),
+                                            region<int32_t>(p, I_OZSEXP), d.bred, region<int32_t>(p, I_OZSKPART),
+                                            region<int32_t>(p, I_OZSKFLAG), p->ldx, p->kp, p->ldo, 0, p->n_local,
+                                            p->sk_ctas, st);
                    }});
     } else {
       v.push_back({"gram_b", [p, d](cudaStream_t st) {
@@ -761,8 +762,9 @@ std::vector<Stage> gram_stages(srm_plan* p, int first, int count) {
     v.push_back({"oz_slice_g", [p, d, first, count](cudaStream_t st) {
                    return launch_oz_slice_rows(d.gram + (int64_t)first * p->ldx * p->ldx, p->ldx,
                                                (int64_t)count * p->ldx, p->ldx,
-                                               region<int8_t>(p, I_OZG) + (int64_t)first * p->ldx * p->oz_lqg,
-                                               p->oz_lqg, region<int32_t>(p, I_OZGEXP) + (int64_t)first * p->ldx, st);
+                                               region<int8_t>(p, I_OZG) + (int64_t)first * (int64_t)oz_tiled_bytes(p->ldx, p->ldx),
+                                               p->oz_lqg, region<int32_t>(p, I_OZGEXP) + (int64_t)first * p->ldx, st,
+                                               p->ldx);
                  }});
   }
   return v;
@@ -986,10 +988,15 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     e = make_map_q(&p->tm_q, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, 128);
     if (e == cudaSuccess) e = launch_oz_gram(p->tm_q, nullptr, nullptr, p->ldx, nullptr, 0, p->oz_nsl, 0);
     if (e == cudaSuccess && p->oz_sg) {
-      e = make_map_q(&p->tm_g, region<int8_t>(p, I_OZG), p->oz_lqg, p->ldx, p->n_local, 128);
+      // tiled G slices: rows of 128 B, oz_tiled_bytes / 128 rows per subject
+      e = make_map_q(&p->tm_g, region<int8_t>(p, I_OZG), 128, (int64_t)oz_tiled_bytes(p->ldx, p->ldx) / 128,
+                     p->n_local, 128);
       if (e == cudaSuccess) e = make_map_q8(&p->tm_sq, region<int8_t>(p, I_OZS), p->oz_lqg, p->kp, 1);
       if (e == cudaSuccess)
         e = launch_oz_sg(p->tm_g, p->tm_sq, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, 0, 0, 0);
+      if (e == cudaSuccess)
+        e = launch_oz_sg_sk(p->tm_g, p->tm_sq, nullptr, nullptr, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, 0, 0,
+                            p->sk_ctas, 0);
     }
     if (e == cudaSuccess && p->oz_w) {
       e = make_map_q5(&p->tm_q32, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, p->oz_nsl);

@@ -79,12 +79,20 @@ cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, 
 cudaError_t make_map_q5(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, int64_t n, int nsl);
 cudaError_t make_map_q8(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n);
 // int8 slices of the rows of a row-major fp64 matrix (ozaki.cu): 2^e[r] >= max|M[r][:]|
+// tile_rows > 0: the tiled layout of the G_i slices (rows per G_i; oz_tiled_bytes per G_i)
 cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int64_t ncols, int8_t* q, int64_t lq,
-                                 int32_t* expo, cudaStream_t st);
+                                 int32_t* expo, cudaStream_t st, int64_t tile_rows = 0);
+size_t oz_tiled_bytes(int64_t rows, int64_t ncols);
 // B_i = S G_i / 2 into bred[i][f][t] from the row slices of G_i and S (kp <= 128),
 // local subjects [first, first + count)
 cudaError_t launch_oz_sg(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
                          double* bred, int64_t ldx, int64_t kp, int64_t ldo, int first, int count, cudaStream_t st);
+// the same B_i, stream-K over at most max_ctas persistent CTAs; part holds
+// max_ctas x oz_sk_park_bytes(), flag max_ctas int32 (zero between launches)
+size_t oz_sk_park_bytes();
+cudaError_t launch_oz_sg_sk(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
+                            double* bred, int32_t* part, int32_t* flag, int64_t ldx, int64_t kp, int64_t ldo,
+                            int first, int count, int max_ctas, cudaStream_t st);
 // R'^T[i] = 2^{e_t} (M_i^T S) / 2 (kp x ldx per subject) for the final int8 W = Xhat R
 cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* expo, double* rt, int64_t ldx,
                          int64_t kp, int64_t K, int n_local, cudaStream_t st);

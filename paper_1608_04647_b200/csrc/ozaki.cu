@@ -34,6 +34,8 @@
 #include <cuda.h>
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "plan.h"
@@ -386,13 +388,16 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
 // row slicing: one warp per row of a row-major fp64 matrix M (rows x ldm,
 // columns [0, ncols), ncols % 32 == 0); the row's power-of-two scale 2^e >=
 // max |M[r][:]| goes to expo[r] and its slices to the 256-byte records
-// q[r][b] (b = 32-column block), the same record layout as oz_split.
+// q[r][b] (b = 32-column block), the same record layout as oz_split, or --
+// tile_rows > 0, the G_i of the int8 B = S G / 2 (tile_rows = rows per G_i) --
+// tiled: [subject][128-row block][32-column block][record half][128 rows][128 B],
+// so each k-block of an M = 128 tile is one contiguous 32 KB read.
 // Matrices: the fp64 Gram G_i (rows = TRs, once) and S (rows = features,
 // every iteration) of the int8 B = S G / 2.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_oz_slice_rows(const double* __restrict__ M, int64_t ldm, int64_t rows,
                                                        int64_t ncols, int8_t* __restrict__ q, int64_t lq,
-                                                       int32_t* __restrict__ expo) {
+                                                       int32_t* __restrict__ expo, int64_t tile_rows) {
   __shared__ __align__(16) uint8_t rec[8][kOzRecord];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * 8 + warp;
@@ -427,8 +432,18 @@ __global__ void __launch_bounds__(256) k_oz_slice_rows(const double* __restrict_
     }
     rb[7 * 32 + lane] = 0;
     __syncwarp();
-    if (lane < 16)
-      reinterpret_cast<uint4*>(q + r * lq + b * kOzRecord)[lane] = reinterpret_cast<const uint4*>(rb)[lane];
+    if (lane < 16) {
+      int8_t* dst;
+      if (tile_rows == 0) {
+        dst = q + r * lq + b * kOzRecord + lane * 16;
+      } else {
+        // tiled (G_i): record halves of 128 rows x one k-block contiguous
+        const int64_t i = r / tile_rows, t = r - i * tile_rows;
+        const int64_t ntb = (tile_rows + 127) / 128, nub = ncols / 32;
+        dst = q + ((i * ntb + t / 128) * nub + b) * (2 * kOzBox) + (lane >> 3) * kOzBox + (t & 127) * 128 + (lane & 7) * 16;
+      }
+      *reinterpret_cast<uint4*>(dst) = reinterpret_cast<const uint4*>(rb)[lane];
+    }
     __syncwarp();
   }
 }
@@ -477,12 +492,41 @@ struct RowGemmArgs {
   int first;             // kRowSG: subject of blockIdx.y = 0
 };
 
+// Row GEMM CTAs: warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue
+// (two warps per TMEM lane quarter, each on 32 of the 64 columns: the
+// epilogue is latency-bound, and its TMEM release gates the next tile's MMAs)
+constexpr int kRowThreads = 320;
+constexpr int kRowEpi = kRowThreads - 64;
+
+// Seven d-groups of 8 accumulator columns -> two exact int64 partial sums
+//   H = sum_{d<4} raw_d 2^{7(3-d)},  L = sum_{d>=4} raw_d 2^{7(6-d)}
+// (|raw| < 2^31: |H| < 2^53, |L| < 2^46), so that
+//   sum_d raw_d 2^{-12-7d} = H 2^-33 + L 2^-54
+// is formed with two exact conversions and one rounding (oz_hl_value).  H and
+// L are linear in the accumulators: parts of a split contraction add exactly.
+__device__ __forceinline__ void oz_load_hl(uint32_t taddr, long long* H, long long* L) {
+  uint32_t raw[7][8];
+#pragma unroll
+  for (int d = 0; d < 7; ++d) tmem_ld8(taddr + 64u * (uint32_t)d, raw[d]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    H[j] = ((long long)(int32_t)raw[0][j] << 21) + ((long long)(int32_t)raw[1][j] << 14) +
+           ((long long)(int32_t)raw[2][j] << 7) + (long long)(int32_t)raw[3][j];
+    L[j] = ((long long)(int32_t)raw[4][j] << 14) + ((long long)(int32_t)raw[5][j] << 7) + (long long)(int32_t)raw[6][j];
+  }
+}
+
+__device__ __forceinline__ double oz_hl_value(long long H, long long L) {
+  return fma((double)L, 0x1p-54, (double)H * 0x1p-33);
+}
+
 // NSA: slices of the A operand (kRowW: X-hat's 7 or 4; kRowSG: G's 7).
 // ND: d-groups kept (all 7 in the current uses; ND = 4 would keep only the
 // pairs s + s' < 4 and fit two CTAs per SM).
 // blockIdx.z selects the 64-feature half of N (kp <= 128).
 template <int MODE, int NSA, int ND>
-__global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_per_sm)
+__global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas_per_sm)
     k_oz_rowgemm(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, RowGemmArgs g) {
   using Shape = RowGemmShape<MODE, NSA, ND>;
   constexpr int kStage = Shape::stage_bytes;
@@ -526,8 +570,10 @@ __global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_
         const int x = k * 256;
         mbar_expect_tx(&full[slot], (uint32_t)kStage);
         if (MODE == kRowSG) {
-          tma_load_3d(st, &tma, x, arow, az, &full[slot]);
-          if (Shape::halves > 1) tma_load_3d(st + kOzBox, &tma, x + 128, arow, az, &full[slot]);
+          // tiled G slices: (128-row block, k-block, record half) rows of 128 B
+          const int grow = ((t0 / 128) * nub + k) * 256;
+          tma_load_3d(st, &tma, 0, grow, az, &full[slot]);
+          if (Shape::halves > 1) tma_load_3d(st + kOzBox, &tma, 0, grow + 128, az, &full[slot]);
         } else {
           // Q records of 32 TRs x 4 voxel blocks x nsa slots -> [slot][vb][t][32 B]
           tma_load_5d(st, &tma, 0, k * 32, it.m0 / 32, 0, i, &full[slot]);
@@ -570,7 +616,9 @@ __global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_
       mma_commit(&accfull);
     }
   } else {
-    const int quarter = warp & 3;
+    static_assert(ND == 7, "the H/L epilogue combines seven d-groups");
+    const int quarter = warp & 3;       // TMEM lanes 32 quarter .. + 31 (warp % 4)
+    const int cbase = ((warp - 2) >> 2) * 32;  // this warp's 32 of the 64 columns
     const int r = quarter * 32 + lane;
     mbar_wait(&accfull, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -587,41 +635,239 @@ __global__ void __launch_bounds__(kOzThreads, RowGemmShape<MODE, NSA, ND>::ctas_
     const int64_t fstride = MODE == kRowSG ? ldo : 1;
     const int fmax_ = MODE == kRowSG ? (int)kp : (int)g.K;
     const int half = MODE == kRowSG ? -1 : 0;  // the 1/2 of B = S G / 2 (R already holds its 1/2)
-    for (int c0 = 0; c0 < 64; c0 += 16) {
-      double val[16];
+#pragma unroll 1
+    for (int c0 = cbase; c0 < cbase + 32; c0 += 8) {
+      // the columns' scale exponents, loaded ahead of the stores
+      int be[8];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) val[j] = 0.0;
-      // the columns' scale exponents, loaded ahead of the stores (no aliasing
-      // with them to wait on)
-      int be[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) be[j] = (f0 + c0 + j < fmax_) ? __ldg(bexp + f0 + c0 + j) : 0;
-      // all d-groups of the 16 columns in flight, one wait
-      uint32_t raw[ND][16];
-#pragma unroll
-      for (int d = 0; d < ND; ++d) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 64u * (uint32_t)d + c0, raw[d]);
-      tmem_wait_ld();
-#pragma unroll
-      for (int d = 0; d < ND; ++d) {
-        const double sd = pow2(-12 - 7 * d);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) val[j] = fma((double)(int32_t)raw[d][j], sd, val[j]);
-      }
+      for (int j = 0; j < 8; ++j) be[j] = (f0 + c0 + j < fmax_) ? __ldg(bexp + f0 + c0 + j) : 0;
+      long long H[8], L[8];
+      oz_load_hl(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, H, L);
       if (valid) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 8; ++j) {
           const int f = f0 + c0 + j;
-          if (f < fmax_) out[(int64_t)(MODE == kRowSG ? f : c0 + j) * fstride] = val[j] * pow2(et + be[j] + half);
+          if (f < fmax_) out[(int64_t)(MODE == kRowSG ? f : c0 + j) * fstride] = oz_hl_value(H[j], L[j]) * pow2(et + be[j] + half);
         }
       }
     }
     if (MODE == kRowW) {
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // the four epilogue warps
+      asm volatile("bar.sync 1, %0;" ::"r"(kRowEpi) : "memory");  // the epilogue warps
       const int K = (int)g.K;
       const int nc = min(64, K - f0);  // this CTA's columns f0 .. f0 + nc - 1 of W
       double* dst = g.out + (int64_t)it.n0 * K + f0;
-      for (int e = (warp - 2) * 32 + lane; e < it.nvb * nc; e += 128)
+      for (int e = (warp - 2) * 32 + lane; e < it.nvb * nc; e += kRowEpi)
         dst[(int64_t)(e / nc) * K + e % nc] = wst[(e / nc) * kWPitch + e % nc];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) tmem_free(tmem, Shape::tmem_cols);
+}
+
+// ---------------------------------------------------------------------------
+// B_i = S G_i / 2, stream-K: the (subject, 128-TR block, 64-feature half)
+// tiles of all subjects laid end to end as one run of 32-TR k-blocks, and
+// persistent CTA c (one per SM, a few SMs left to the side lane's one-CTA
+// tail kernels) takes k-blocks [c L, (c + 1) L), L >= a tile's k-blocks, so
+// every CTA does the same number of MMAs (the per-tile grid ran 2.2 waves of
+// 320 CTAs in 3) and the next tile's TMA loads run under the epilogue.
+//
+// A tile cut by a range boundary has two parts: its tail (first segment of
+// CTA c + 1) parks its raw int32 d-group sums in part[c + 1] and raises
+// flag[c + 1]; its head (last segment of CTA c) waits for the flag, adds the
+// parked sums in int32 -- exact, so B_i is bit-identical to the per-tile
+// kernel's for any split, shard layout or SM count -- and stores the tile.
+// Same MMAs, TMEM layout and epilogue arithmetic as k_oz_rowgemm<kRowSG>.
+// ---------------------------------------------------------------------------
+constexpr int kSkParkPairs = 64 * 128;  // (H, L) per (feature, TR) of a tile
+
+struct SkArgs {
+  const int32_t* aexp;  // G row exponents [n_local][ldx]
+  const int32_t* bexp;  // S row exponents [kp]
+  double* out;          // bred
+  long long* part;      // [grid][2][kSkParkPairs]: parked (H, L) of a tile's tail
+  int32_t* flag;        // [grid], zero between launches
+  int64_t ldx, kp, ldo;
+  int first;            // subject of the first tile
+  int ntb, nz, nub;     // TR blocks per subject, feature halves, k-blocks per tile
+  int64_t units, span;  // total k-blocks, k-blocks per CTA
+};
+
+// the tile and k-block range [kb0, kb1) of the segment starting at unit u
+__device__ __forceinline__ void sk_segment(const SkArgs& g, int64_t u, int64_t u1, int* tile, int* kb0, int* kb1) {
+  *tile = (int)(u / g.nub);
+  *kb0 = (int)(u - (int64_t)*tile * g.nub);
+  *kb1 = (int)(u1 - u < (int64_t)(g.nub - *kb0) ? *kb0 + (u1 - u) : g.nub);
+}
+
+__global__ void __launch_bounds__(kRowThreads, 1)
+    k_oz_sg_sk(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, SkArgs g) {
+  using Shape = RowGemmShape<kRowSG, kOzSlices, 7>;
+  constexpr int kStage = Shape::stage_bytes;
+  constexpr int ND = 7;
+  extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[kSgStages], empty[kSgStages], accfull, accempty;
+  __shared__ uint32_t tmem_base;
+  const int64_t u_begin = (int64_t)blockIdx.x * g.span;
+  const int64_t u_end = min(g.units, u_begin + g.span);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < kSgStages; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      mbar_init(&accfull, 1);
+      mbar_init(&accempty, kRowEpi / 32);  // one arrive per epilogue warp
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+  } else if (warp == 1) {
+    tmem_alloc(&tmem_base, Shape::tmem_cols);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  if (warp == 0) {
+    if (lane == 0) {
+      int k = 0;
+      for (int64_t u = u_begin; u < u_end; ++u, ++k) {
+        const int tile = (int)(u / g.nub), kb = (int)(u - (int64_t)tile * g.nub);
+        const int z = tile % g.nz, tb = (tile / g.nz) % g.ntb, i = g.first + tile / (g.nz * g.ntb);
+        const int slot = k % kSgStages;
+        if (k >= kSgStages) mbar_wait(&empty[slot], ((k / kSgStages) - 1) & 1);
+        unsigned char* st = smem + slot * kStage;
+        mbar_expect_tx(&full[slot], (uint32_t)kStage);
+        const int grow = (tb * g.nub + kb) * 256;  // tiled G slices
+        tma_load_3d(st, &tma, 0, grow, i, &full[slot]);
+        tma_load_3d(st + kOzBox, &tma, 0, grow + 128, i, &full[slot]);
+        tma_load_4d(st + Shape::a_bytes, &tmb, 0, z * 64, kb * 8, 0, &full[slot]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_s8(128, 128);
+      int k = 0, seg = 0;
+      for (int64_t u = u_begin; u < u_end; ++seg) {
+        int tile, kb0, kb1;
+        sk_segment(g, u, u_end, &tile, &kb0, &kb1);
+        // the epilogue has drained the previous segment's accumulators
+        if (seg > 0) mbar_wait(&accempty, (seg - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        for (int kb = kb0; kb < kb1; ++kb, ++k) {
+          const int slot = k % kSgStages;
+          mbar_wait(&full[slot], (k / kSgStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t sa = smem_u32(smem + slot * kStage);
+          const uint64_t da0 = umma_desc_sw128(sa);
+          const uint64_t db0 = umma_desc_sw32_mn(sa + Shape::a_bytes, 16, 256);
+          const uint32_t keep = kb == kb0 ? 0u : 1u;
+#pragma unroll
+          for (int s = 0; s < kOzSlices; ++s) {
+            const uint64_t aoff = (uint64_t)((s >> 2) * (kOzBox >> 4) + 2 * (s & 3));
+#pragma unroll
+            for (int s2 = 0; s2 + s <= ND - 1; s2 += 2)
+              mma_s8(tmem + 64u * (uint32_t)(s + s2), da0 + aoff, db0 + (uint64_t)(s2 * (2048 >> 4)), idesc,
+                     s == 0 ? keep : 1u);
+          }
+          mma_commit(&empty[slot]);
+        }
+        mma_commit(&accfull);
+        u += kb1 - kb0;
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int cbase = ((warp - 2) >> 2) * 32;
+    const int r = quarter * 32 + lane;
+    const int etid = (warp - 2) * 32 + lane;  // 0 .. kRowEpi - 1
+    int seg = 0;
+    for (int64_t u = u_begin; u < u_end; ++seg) {
+      int tile, kb0, kb1;
+      sk_segment(g, u, u_end, &tile, &kb0, &kb1);
+      u += kb1 - kb0;
+      const int z = tile % g.nz, tb = (tile / g.nz) % g.ntb, i = g.first + tile / (g.nz * g.ntb);
+      const bool tail = kb0 > 0;      // park for the previous CTA
+      const bool head = kb1 < g.nub;  // finish with the next CTA's parked part
+      mbar_wait(&accfull, seg & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      long long* pout = g.part + (int64_t)blockIdx.x * 2 * kSkParkPairs;
+      const long long* pin = g.part + (int64_t)(blockIdx.x + 1) * 2 * kSkParkPairs;
+      if (tail) {
+        // drain and park (the stores do not hold the warp), then release
+#pragma unroll 1
+        for (int c0 = cbase; c0 < cbase + 32; c0 += 8) {
+          long long H[8], L[8];
+          oz_load_hl(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, H, L);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            pout[(c0 + j) * 128 + r] = H[j];
+            pout[kSkParkPairs + (c0 + j) * 128 + r] = L[j];
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&accempty);
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"r"(kRowEpi) : "memory");
+        if (etid == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(g.flag + blockIdx.x), "r"(1) : "memory");
+        continue;
+      }
+      if (head) {
+        // the next CTA parks this tile's tail first thing in its range
+        if (etid == 0) {
+          const int32_t* fl = g.flag + blockIdx.x + 1;
+          int v = 0;
+          do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(fl) : "memory");
+          } while (v == 0);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kRowEpi) : "memory");
+      }
+      const int f0 = z * 64;
+      const int64_t t = (int64_t)tb * 128 + r;
+      const bool valid = t < g.ldx;
+      const int et = valid ? g.aexp[(int64_t)i * g.ldx + t] : 0;
+      double* out = g.out + (int64_t)i * g.kp * g.ldo + t;
+#pragma unroll 1
+      for (int c0 = cbase; c0 < cbase + 32; c0 += 8) {
+        int be[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) be[j] = (f0 + c0 + j < g.kp) ? __ldg(g.bexp + f0 + c0 + j) : 0;
+        // the parked part: all sixteen L2 loads in flight before the TMEM drain
+        // (ld.global.cg: the lines may be cached nowhere but L2)
+        long long ph[8], pl[8];
+        if (head) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            asm volatile("ld.global.cg.b64 %0, [%1];" : "=l"(ph[j]) : "l"(pin + (c0 + j) * 128 + r));
+            asm volatile("ld.global.cg.b64 %0, [%1];" : "=l"(pl[j]) : "l"(pin + kSkParkPairs + (c0 + j) * 128 + r));
+          }
+        }
+        long long H[8], L[8];
+        oz_load_hl(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, H, L);
+        if (head) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            H[j] += ph[j];
+            L[j] += pl[j];
+          }
+        }
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int f = f0 + c0 + j;
+            if (f < g.kp) out[(int64_t)f * g.ldo] = oz_hl_value(H[j], L[j]) * pow2(et + be[j] - 1);
+          }
+        }
+      }
+      // accumulators drained: the MMA warp may start the next segment
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&accempty);
+      if (head && etid == 0) g.flag[blockIdx.x + 1] = 0;  // consumed: ready for the next launch
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -649,11 +895,13 @@ __global__ void __launch_bounds__(256) k_oz_rt(const double* __restrict__ mmat, 
 
 size_t oz_gram_smem_bytes() { return (size_t)kOzStages * kOzStageBytes + 1024; }
 
+size_t oz_tiled_bytes(int64_t rows, int64_t ncols) { return (size_t)((rows + 127) / 128) * (ncols / 32) * 2 * kOzBox; }
+
 cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int64_t ncols, int8_t* q, int64_t lq,
-                                 int32_t* expo, cudaStream_t st) {
+                                 int32_t* expo, cudaStream_t st, int64_t tile_rows) {
   if (rows <= 0) return cudaSuccess;
   if (ncols % 32 != 0) return cudaErrorInvalidValue;
-  k_oz_slice_rows<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(M, ldm, rows, ncols, q, lq, expo);
+  k_oz_slice_rows<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(M, ldm, rows, ncols, q, lq, expo, tile_rows);
   return cudaGetLastError();
 }
 
@@ -672,7 +920,7 @@ cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, const RowGemmArgs& g
   if (grid.x == 0 || grid.y == 0) return cudaSuccess;
   if (g.kp > 128 || g.ldx % 32 != 0) return cudaErrorInvalidValue;
   grid.z = (unsigned)((g.kp + 63) / 64);  // 64-feature halves of N
-  k_oz_rowgemm<MODE, NSA, ND><<<grid, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(ta.opaque),
+  k_oz_rowgemm<MODE, NSA, ND><<<grid, kRowThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(ta.opaque),
                                                              *reinterpret_cast<const CUtensorMap*>(tb.opaque), g);
   return cudaGetLastError();
 }
@@ -683,6 +931,34 @@ cudaError_t launch_oz_sg(const TmaMap& tmg, const TmaMap& tms, const int32_t* ge
                          double* bred, int64_t ldx, int64_t kp, int64_t ldo, int first, int count, cudaStream_t st) {
   RowGemmArgs g{gexp, sexp, bred, nullptr, ldx, kp, ldo, 0, first};
   return run_rowgemm<kRowSG, kOzSlices, 7>(tmg, tms, g, dim3((unsigned)((ldx + 127) / 128), (unsigned)count), st);
+}
+
+size_t oz_sk_park_bytes() { return (size_t)kSkParkPairs * 16; }
+
+cudaError_t launch_oz_sg_sk(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
+                            double* bred, int32_t* part, int32_t* flag, int64_t ldx, int64_t kp, int64_t ldo,
+                            int first, int count, int max_ctas, cudaStream_t st) {
+  using Shape = RowGemmShape<kRowSG, kOzSlices, 7>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_oz_sg_sk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Shape::smem_bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (count <= 0) return cudaSuccess;
+  if (kp > 128 || ldx % 32 != 0 || max_ctas <= 0) return cudaErrorInvalidValue;
+  SkArgs g{gexp, sexp, bred, reinterpret_cast<long long*>(part), flag, ldx, kp, ldo, first, 0, 0, 0, 0, 0};
+  g.ntb = (int)((ldx + 127) / 128);
+  g.nz = (int)((kp + 63) / 64);
+  g.nub = (int)(ldx / 32);
+  g.units = (int64_t)count * g.ntb * g.nz * g.nub;
+  // at least one tile per CTA, so a tile meets at most two CTA ranges
+  g.span = std::max<int64_t>(g.nub, (g.units + max_ctas - 1) / max_ctas);
+  const unsigned grid = (unsigned)((g.units + g.span - 1) / g.span);
+  k_oz_sg_sk<<<grid, kRowThreads, Shape::smem_bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(tmg.opaque),
+                                                          *reinterpret_cast<const CUtensorMap*>(tms.opaque), g);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* expo, double* rt, int64_t ldx,

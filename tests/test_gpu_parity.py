@@ -507,3 +507,31 @@ def test_fp32_configs_full_shape_vs_oracle(srm, cfg):
             assert np.max(np.abs(w.T @ w - np.eye(K))) <= 1e-8, (cfg, algorithm)
         del m
         torch.cuda.empty_cache()
+
+
+def _sg_fit(srm, xs, k, per_tile, monkeypatch):
+    monkeypatch.setenv("SRM_B200_SG_PER_TILE", "1" if per_tile else "0")
+    eng = []
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=k, iterations=3, seed=2), algorithm="gram", engine_out=eng)
+    assert eng[0].gram_i8
+    return m
+
+
+@pytest.mark.parametrize("k", [20, 72])
+def test_stream_k_sg_bit_identical_to_per_tile(srm, monkeypatch, k):
+    """B = S G / 2 stream-K (tiles cut between persistent CTAs, the parts
+    joined in int32) against the per-tile grid: the same fit bit for bit.
+    10 subjects x T = 2000 make ~70 k-blocks per CTA, so most CTAs split a
+    tile; K = 72 adds the second 64-feature half."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(10, 400, 2000, k, seed=8)
+    a = _sg_fit(srm, xs, k, False, monkeypatch)
+    b = _sg_fit(srm, xs, k, True, monkeypatch)
+    assert np.array_equal(a.S, b.S) and np.array_equal(a.sigma_s, b.sigma_s)
+    assert np.array_equal(a.rho2, b.rho2) and a.log_likelihood == b.log_likelihood
+    for wa, wb in zip(a.W, b.W):
+        assert np.array_equal(wa, wb)
+    ref = orc.run_em(xs, k, 3, seed=2)
+    r = ref["iters"][-1]
+    _check_model(a, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, f"stream-K k={k}")

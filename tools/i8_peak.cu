@@ -47,7 +47,20 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int CG, int M, int N, int NST, int SW = 0>
+__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;
+  return d;
+}
+
+// BL = 0: both operands K-major SW128; BL = 1: B K-major SWIZZLE_32B (rows of
+// 32 B, one K step per N x 32 B block: the k_oz_sg_sk / k_oz_rowgemm B);
+// BL = 2: additionally A MN-major SWIZZLE_32B (the k_oz_rowgemm<kRowW> A)
+template <int CG, int M, int N, int NST, int SW = 0, int BL = 0>
 __global__ void __launch_bounds__(128, 1) peak(int iters, unsigned long long seed) {
   // per CTA and stage: A 128 rows x 128 B, B (N / CG) rows x 128 B, SW128 K-major;
   // NST stages cycled (NST = 1: the same operands every MMA)
@@ -92,14 +105,15 @@ __global__ void __launch_bounds__(128, 1) peak(int iters, unsigned long long see
   }
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
-  constexpr uint32_t idesc = idesc_i8(M, N);
+  constexpr uint32_t idesc = idesc_i8(M, N) | (BL == 2 ? (1u << 15) : 0u);
   const unsigned long long c0 = clock64(), g0 = gtimer();
   if (tid == 0 && rank == 0) {
     for (int it = 0; it < iters; ++it) {
       const uint32_t sa = smem_u32(sm) + (uint32_t)((it % NST) * kStage), sb = sa + 128 * 128;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint64_t da = desc_sw128(sa + 32 * k), db = desc_sw128(sb + 32 * k);
+        const uint64_t da = BL == 2 ? desc_sw32(sa + 4096 * k, 256, 1024) : desc_sw128(sa + 32 * k);
+        const uint64_t db = BL >= 1 ? desc_sw32(sb + (N / CG) * 32 * k, 16, 256) : desc_sw128(sb + 32 * k);
         // SW = 0: one accumulator per 4-MMA group (alternating); SW = 1: four
         // accumulators round-robin, a switch after every MMA (the k_oz_gram d-groups)
         const uint32_t acc = SW ? tmem + (uint32_t)(k * N) % 512u : tmem + (uint32_t)((it & 1) * (N <= 256 ? N : 0)) % 512u;
@@ -152,10 +166,10 @@ __global__ void __launch_bounds__(128, 1) peak(int iters, unsigned long long see
 
 static double g_mhz = 0.0;  // effective SM clock of the last run (CTA 0)
 
-template <int CG, int M, int N, int NST = 1, int SW = 0>
+template <int CG, int M, int N, int NST = 1, int SW = 0, int BL = 0>
 double run(int sms, int iters, int reps = 5) {
   const size_t smem = (size_t)NST * (128 + N / CG) * 128 + 1024;
-  CK(cudaFuncSetAttribute(peak<CG, M, N, NST, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(peak<CG, M, N, NST, SW, BL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sms / CG * CG);
   cfg.blockDim = dim3(128);
@@ -167,7 +181,7 @@ double run(int sms, int iters, int reps = 5) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  for (int w = 0; w < 2; ++w) CK(cudaLaunchKernelEx(&cfg, peak<CG, M, N, NST, SW>, iters / 8, 7ull));
+  for (int w = 0; w < 2; ++w) CK(cudaLaunchKernelEx(&cfg, peak<CG, M, N, NST, SW, BL>, iters / 8, 7ull));
   CK(cudaDeviceSynchronize());
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
@@ -175,7 +189,7 @@ double run(int sms, int iters, int reps = 5) {
   float best = 1e30f;
   for (int rep = 0; rep < reps; ++rep) {
     CK(cudaEventRecord(a));
-    CK(cudaLaunchKernelEx(&cfg, peak<CG, M, N, NST, SW>, iters, 11ull + rep));
+    CK(cudaLaunchKernelEx(&cfg, peak<CG, M, N, NST, SW, BL>, iters, 11ull + rep));
     CK(cudaEventRecord(b));
     CK(cudaEventSynchronize(b));
     float ms = 0.f;
@@ -204,6 +218,9 @@ int main(int argc, char** argv) {
   const double n64 = run<1, 128, 64, 6>(sms, iters);
   const double n32 = run<1, 128, 32, 6>(sms, iters);
   const double burst_mhz = g_mhz;
+  const double bsw32 = run<1, 128, 128, 6, 1, 1>(sms, iters);
+  const double bsw32_64 = run<1, 128, 64, 6, 1, 1>(sms, iters);
+  const double absw32 = run<1, 128, 128, 6, 1, 2>(sms, iters);
   // sustained: ~0.3 s of back-to-back MMAs (the clock the power controller
   // settles at under a long int8 load, as inside the Gram precompute)
   const double sus = run<1, 128, 128, 6>(sms, iters * 256, 2);
@@ -212,7 +229,8 @@ int main(int argc, char** argv) {
          "\"tops_2sm_256x256\": %.1f, \"tops_1sm_128x128_rot6\": %.1f, \"tops_1sm_128x256_rot4\": %.1f, "
          "\"tops_2sm_256x256_rot6\": %.1f, \"tops_1sm_128x128_rot6_accswitch\": %.1f, \"burst_sm_mhz\": %.0f, "
          "\"tops_1sm_128x128_sustained\": %.1f, \"sustained_sm_mhz\": %.0f, \"tops_1sm_128x64_rot6\": %.1f, "
-         "\"tops_1sm_128x32_rot6\": %.1f}\n",
-         sms, iters, a, b, c, ar, br, cr, asw, burst_mhz, sus, sus_mhz, n64, n32);
+         "\"tops_1sm_128x32_rot6\": %.1f, \"tops_128x128_accswitch_b_sw32\": %.1f, "
+         "\"tops_128x64_accswitch_b_sw32\": %.1f, \"tops_128x128_accswitch_a_mn_sw32_b_sw32\": %.1f}\n",
+         sms, iters, a, b, c, ar, br, cr, asw, burst_mhz, sus, sus_mhz, n64, n32, bsw32, bsw32_64, absw32);
   return 0;
 }

@@ -1,0 +1,38 @@
+"""Per-iteration stage times on cfg 2 (40 x 30000 x 1000, K = 50, fp64, int8
+Gram path), eager with events between kernels, median of five iterations;
+with SRM_B200_SG_PER_TILE=1 in the environment B = S G / 2 runs per tile.
+
+    python tools/sg_probe.py
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1608_04647_b200.data import recipe_torch  # noqa: E402
+from paper_1608_04647_b200.engine import SrmEngine  # noqa: E402
+
+V, T, K, N = 30000, 1000, 50, 40
+xs, _, _ = recipe_torch(N, V, T, K, seed=0, dtype="f64")
+eng = SrmEngine([V] * N, T, K, 16, storage="f64", gram=True, gram_i8=True, device=torch.device("cuda:0"))
+eng.load(xs)
+eng.init_mapping(0, 0)
+eng.prepare_gram()
+eng.step(None)
+torch.cuda.synchronize()
+ts = {}
+for _ in range(6):
+    seen = {}
+    for name, t in eng.profile_iteration():
+        seen[name] = seen.get(name, 0) + 1
+        ts.setdefault(name if seen[name] == 1 else f"{name}#{seen[name]}", []).append(t)
+fin = {}
+for _ in range(2):
+    for name, t in eng.profile_finalize():
+        fin.setdefault(name, []).append(t)
+print(json.dumps({"per_iteration_ms": {k: float(np.median(v[1:])) for k, v in ts.items()},
+                  "finalize_ms": {k: float(np.median(v)) for k, v in fin.items()}}), flush=True)
+
