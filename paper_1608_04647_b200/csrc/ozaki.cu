@@ -478,9 +478,14 @@ struct RowGemmShape {
   // B: the eight slots of 64 rows x 32 B (k-block of 32 TRs), slot-major
   static constexpr int b_bytes = 8 * 64 * 32;
   static constexpr int stage_bytes = a_bytes + b_bytes;
+  // kRowW keeps a W staging tile (128 rows x 64 features, pitch 65) beside the
+  // ring: three stages of seven-slice operands fit with it, four otherwise
+  static constexpr int stages = (MODE == kRowW && NSA > 4) ? 3 : kSgStages;
+  static constexpr int wst_pitch = 65;
+  static constexpr int wst_bytes = MODE == kRowW ? 128 * wst_pitch * 8 : 0;
   static constexpr uint32_t tmem_cols = 512;  // eight 64-column d-groups (d = 7 unused)
   static constexpr int ctas_per_sm = 1;
-  static constexpr size_t smem_bytes = (size_t)kSgStages * stage_bytes + 1024;
+  static constexpr size_t smem_bytes = (size_t)stages * stage_bytes + wst_bytes + 1024;
 };
 
 struct RowGemmArgs {
@@ -489,8 +494,36 @@ struct RowGemmArgs {
   double* out;           // kRowSG: bred; kRowW: W [rows_total][K]
   const OzItem* items;   // kRowW: {subject, local voxel v0, global row of v0, valid rows}
   int64_t ldx, kp, ldo, K;
-  int first;             // kRowSG: subject of blockIdx.y = 0
+  int first;             // kRowSG: subject of the first tile
+  int n_work;            // tiles: kRowSG (subject, 128-TR block, feature half); kRowW (item, feature half)
+  int nz, ntb;           // feature halves; kRowSG: 128-TR blocks per subject
 };
+
+// the operands of work tile w: subject, first A row, feature half
+struct RowTile {
+  int i, arow, z, nvb;
+  int64_t n0;
+};
+
+template <int MODE>
+__device__ __forceinline__ RowTile row_tile(const RowGemmArgs& g, int w) {
+  RowTile r;
+  r.z = w % g.nz;
+  if (MODE == kRowSG) {
+    const int tb = (w / g.nz) % g.ntb;
+    r.i = g.first + w / (g.nz * g.ntb);
+    r.arow = tb * 128;
+    r.nvb = 128;
+    r.n0 = 0;
+  } else {
+    const OzItem it = g.items[w / g.nz];
+    r.i = it.subj;
+    r.arow = it.m0;
+    r.nvb = it.nvb;
+    r.n0 = it.n0;
+  }
+  return r;
+}
 
 // Row GEMM CTAs: warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue
 // (two warps per TMEM lane quarter, each on 32 of the 64 columns: the
@@ -522,36 +555,31 @@ __device__ __forceinline__ double oz_hl_value(long long H, long long L) {
 }
 
 // NSA: slices of the A operand (kRowW: X-hat's 7 or 4; kRowSG: G's 7).
-// ND: d-groups kept (all 7 in the current uses; ND = 4 would keep only the
-// pairs s + s' < 4 and fit two CTAs per SM).
-// blockIdx.z selects the 64-feature half of N (kp <= 128).
+// ND: d-groups kept (all 7 in the current uses).  Persistent: CTA c takes
+// work tiles c, c + gridDim.x, ...; the producer streams the next tile's
+// k-blocks while the epilogue drains the last, and the MMA warp waits only
+// for the accumulators to be drained (accempty).
 template <int MODE, int NSA, int ND>
 __global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas_per_sm)
     k_oz_rowgemm(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, RowGemmArgs g) {
   using Shape = RowGemmShape<MODE, NSA, ND>;
   constexpr int kStage = Shape::stage_bytes;
+  constexpr int kSt = Shape::stages;
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t full[kSgStages], empty[kSgStages], accfull;
+  __shared__ uint64_t full[kSt], empty[kSt], accfull, accempty;
   __shared__ uint32_t tmem_base;
   const int64_t ldx = g.ldx, kp = g.kp, ldo = g.ldo;
-  OzItem it{};
-  if (MODE == kRowW) it = g.items[blockIdx.x];
-  const int t0 = MODE == kRowSG ? blockIdx.x * 128 : 0;
-  const int i = MODE == kRowSG ? g.first + (int)blockIdx.y : it.subj;
-  const int arow = MODE == kRowSG ? t0 : it.n0;  // first A row (TR of G_i / global voxel row)
-  const int az = MODE == kRowSG ? i : 0;
-  const int bz = MODE == kRowSG ? 0 : i;
-  const int f0 = blockIdx.z * 64;  // first feature of this CTA's N = 64 columns
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nub = (int)(ldx / 32);
   if (warp == 0) {
     if (lane == 0) {
-      for (int s = 0; s < kSgStages; ++s) {
+      for (int s = 0; s < kSt; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], 1);
       }
       mbar_init(&accfull, 1);
+      mbar_init(&accempty, kRowEpi / 32);
       asm volatile("fence.mbarrier_init.release.cluster;");
     }
   } else if (warp == 1) {
@@ -563,22 +591,25 @@ __global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas
   const uint32_t tmem = tmem_base;
   if (warp == 0) {
     if (lane == 0) {
-      for (int k = 0; k < nub; ++k) {
-        const int slot = k % kSgStages;
-        if (k >= kSgStages) mbar_wait(&empty[slot], ((k / kSgStages) - 1) & 1);
-        unsigned char* st = smem + slot * kStage;
-        const int x = k * 256;
-        mbar_expect_tx(&full[slot], (uint32_t)kStage);
-        if (MODE == kRowSG) {
-          // tiled G slices: (128-row block, k-block, record half) rows of 128 B
-          const int grow = ((t0 / 128) * nub + k) * 256;
-          tma_load_3d(st, &tma, 0, grow, az, &full[slot]);
-          if (Shape::halves > 1) tma_load_3d(st + kOzBox, &tma, 0, grow + 128, az, &full[slot]);
-        } else {
-          // Q records of 32 TRs x 4 voxel blocks x nsa slots -> [slot][vb][t][32 B]
-          tma_load_5d(st, &tma, 0, k * 32, it.m0 / 32, 0, i, &full[slot]);
+      int kk = 0;
+      for (int w = blockIdx.x; w < g.n_work; w += gridDim.x) {
+        const RowTile tl = row_tile<MODE>(g, w);
+        for (int k = 0; k < nub; ++k, ++kk) {
+          const int slot = kk % kSt;
+          if (kk >= kSt) mbar_wait(&empty[slot], ((kk / kSt) - 1) & 1);
+          unsigned char* st = smem + slot * kStage;
+          mbar_expect_tx(&full[slot], (uint32_t)kStage);
+          if (MODE == kRowSG) {
+            // tiled G slices: (128-row block, k-block, record half) rows of 128 B
+            const int grow = ((tl.arow / 128) * nub + k) * 256;
+            tma_load_3d(st, &tma, 0, grow, tl.i, &full[slot]);
+            if (Shape::halves > 1) tma_load_3d(st + kOzBox, &tma, 0, grow + 128, tl.i, &full[slot]);
+          } else {
+            // Q records of 32 TRs x 4 voxel blocks x nsa slots -> [slot][vb][t][32 B]
+            tma_load_5d(st, &tma, 0, k * 32, tl.arow / 32, 0, tl.i, &full[slot]);
+          }
+          tma_load_4d(st + Shape::a_bytes, &tmb, 0, tl.z * 64, k * 8, MODE == kRowSG ? 0 : tl.i, &full[slot]);
         }
-        tma_load_4d(st + Shape::a_bytes, &tmb, 0, f0, k * 8, bz, &full[slot]);
       }
     }
   } else if (warp == 1) {
@@ -588,76 +619,91 @@ __global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas
       // feeds d-groups s + s2 and s + s2 + 1 (adjacent 64-column accumulators);
       // an N = 64 MMA costs the same tensor-pipe time as N = 128 (tools/i8_peak.cu)
       constexpr uint32_t idesc = idesc_s8(128, 128) | (MODE == kRowW ? (1u << 15) : 0u);
-      for (int k = 0; k < nub; ++k) {
-        const int slot = k % kSgStages;
-        mbar_wait(&full[slot], (k / kSgStages) & 1);
+      int kk = 0, li = 0;
+      for (int w = blockIdx.x; w < g.n_work; w += gridDim.x, ++li) {
+        if (li > 0) mbar_wait(&accempty, (li - 1) & 1);  // the last tile's accumulators drained
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t sa = smem_u32(smem + slot * kStage);
-        const uint32_t sb = sa + Shape::a_bytes;
-        // one descriptor per operand and stage; a slice is a constant offset of
-        // the 16-byte address field (no carry: smem addresses < 2^18)
-        const uint64_t da0 = MODE == kRowSG ? umma_desc_sw128(sa) : umma_desc_sw32_mn(sa, 1024, 256);
-        // K-major SWIZZLE_32B: 8-row atoms of 256 B (SBO); slot j starts at 2 KB j
-        const uint64_t db0 = umma_desc_sw32_mn(sb, 16, 256);
-        const uint32_t keep = k == 0 ? 0u : 1u;
-        // s = 0 first: its four pairs cover all eight d-groups once, so they alone
-        // start the accumulators of a fresh tile
+        for (int k = 0; k < nub; ++k, ++kk) {
+          const int slot = kk % kSt;
+          mbar_wait(&full[slot], (kk / kSt) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t sa = smem_u32(smem + slot * kStage);
+          const uint32_t sb = sa + Shape::a_bytes;
+          // one descriptor per operand and stage; a slice is a constant offset of
+          // the 16-byte address field (no carry: smem addresses < 2^18)
+          const uint64_t da0 = MODE == kRowSG ? umma_desc_sw128(sa) : umma_desc_sw32_mn(sa, 1024, 256);
+          // K-major SWIZZLE_32B: 8-row atoms of 256 B (SBO); slot j starts at 2 KB j
+          const uint64_t db0 = umma_desc_sw32_mn(sb, 16, 256);
+          const uint32_t keep = k == 0 ? 0u : 1u;
+          // s = 0 first: its four pairs cover all eight d-groups once, so they alone
+          // start the accumulators of a fresh tile
 #pragma unroll
-        for (int s = 0; s < NSA; ++s) {
-          const uint64_t aoff = MODE == kRowSG ? (uint64_t)((s >> 2) * (kOzBox >> 4) + 2 * (s & 3))
-                                               : (uint64_t)(s * (4096 >> 4));
+          for (int s = 0; s < NSA; ++s) {
+            const uint64_t aoff = MODE == kRowSG ? (uint64_t)((s >> 2) * (kOzBox >> 4) + 2 * (s & 3))
+                                                 : (uint64_t)(s * (4096 >> 4));
 #pragma unroll
-          for (int s2 = 0; s2 + s <= ND - 1; s2 += 2)
-            mma_s8(tmem + 64u * (uint32_t)(s + s2), da0 + aoff, db0 + (uint64_t)(s2 * (2048 >> 4)), idesc,
-                   s == 0 ? keep : 1u);
+            for (int s2 = 0; s2 + s <= ND - 1; s2 += 2)
+              mma_s8(tmem + 64u * (uint32_t)(s + s2), da0 + aoff, db0 + (uint64_t)(s2 * (2048 >> 4)), idesc,
+                     s == 0 ? keep : 1u);
+          }
+          mma_commit(&empty[slot]);
         }
-        mma_commit(&empty[slot]);
+        mma_commit(&accfull);
       }
-      mma_commit(&accfull);
     }
   } else {
     static_assert(ND == 7, "the H/L epilogue combines seven d-groups");
-    const int quarter = warp & 3;       // TMEM lanes 32 quarter .. + 31 (warp % 4)
+    const int quarter = warp & 3;              // TMEM lanes 32 quarter .. + 31 (warp % 4)
     const int cbase = ((warp - 2) >> 2) * 32;  // this warp's 32 of the 64 columns
     const int r = quarter * 32 + lane;
-    mbar_wait(&accfull, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    // kRowSG: B[f][t] of subject i; kRowW: W[row][f]
-    const int64_t t = t0 + r;
-    const bool valid = MODE == kRowSG ? t < ldx : r < it.nvb;
-    const int et = (MODE == kRowSG && valid) ? g.aexp[(int64_t)i * ldx + t] : 0;
-    const int32_t* bexp = MODE == kRowSG ? g.bexp : g.bexp + (int64_t)i * kp;
-    // kRowW stages its 128 x K tile in the (drained) pipeline smem, pitch K + 1,
-    // and then writes the tile's contiguous rows with coalesced stores
-    constexpr int kWPitch = 65;
-    double* wst = reinterpret_cast<double*>(smem);
-    double* out = MODE == kRowSG ? g.out + (int64_t)i * kp * ldo + t : wst + r * kWPitch;
-    const int64_t fstride = MODE == kRowSG ? ldo : 1;
+    const int etid = (warp - 2) * 32 + lane;
+    double* wst = reinterpret_cast<double*>(smem + kSt * kStage);  // kRowW staging tile
     const int fmax_ = MODE == kRowSG ? (int)kp : (int)g.K;
     const int half = MODE == kRowSG ? -1 : 0;  // the 1/2 of B = S G / 2 (R already holds its 1/2)
-#pragma unroll 1
-    for (int c0 = cbase; c0 < cbase + 32; c0 += 8) {
-      // the columns' scale exponents, loaded ahead of the stores
-      int be[8];
+    int li = 0;
+    for (int w = blockIdx.x; w < g.n_work; w += gridDim.x, ++li) {
+      const RowTile tl = row_tile<MODE>(g, w);
+      const int f0 = tl.z * 64;
+      // kRowSG: B[f][t] of subject i; kRowW: W[row][f]
+      const int64_t t = tl.arow + r;
+      const bool valid = MODE == kRowSG ? t < ldx : r < tl.nvb;
+      const int32_t* bexp = MODE == kRowSG ? g.bexp : g.bexp + (int64_t)tl.i * kp;
+      // scale exponents ahead of the accumulators
+      const int et = (MODE == kRowSG && valid) ? __ldg(g.aexp + (int64_t)tl.i * ldx + t) : 0;
+      int be[32];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) be[j] = (f0 + c0 + j < fmax_) ? __ldg(bexp + f0 + c0 + j) : 0;
-      long long H[8], L[8];
-      oz_load_hl(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, H, L);
-      if (valid) {
+      for (int j = 0; j < 32; ++j) be[j] = (f0 + cbase + j < fmax_) ? __ldg(bexp + f0 + cbase + j) : 0;
+      mbar_wait(&accfull, li & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      double* out = MODE == kRowSG ? g.out + (int64_t)tl.i * kp * ldo + t : wst + r * Shape::wst_pitch;
+      const int64_t fstride = MODE == kRowSG ? ldo : 1;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int f = f0 + c0 + j;
-          if (f < fmax_) out[(int64_t)(MODE == kRowSG ? f : c0 + j) * fstride] = oz_hl_value(H[j], L[j]) * pow2(et + be[j] + half);
+      for (int c = 0; c < 4; ++c) {
+        const int c0 = cbase + 8 * c;
+        long long H[8], L[8];
+        oz_load_hl(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, H, L);
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int f = f0 + c0 + j;
+            if (f < fmax_)
+              out[(int64_t)(MODE == kRowSG ? f : c0 + j) * fstride] = oz_hl_value(H[j], L[j]) * pow2(et + be[8 * c + j] + half);
+          }
         }
       }
-    }
-    if (MODE == kRowW) {
-      asm volatile("bar.sync 1, %0;" ::"r"(kRowEpi) : "memory");  // the epilogue warps
-      const int K = (int)g.K;
-      const int nc = min(64, K - f0);  // this CTA's columns f0 .. f0 + nc - 1 of W
-      double* dst = g.out + (int64_t)it.n0 * K + f0;
-      for (int e = (warp - 2) * 32 + lane; e < it.nvb * nc; e += kRowEpi)
-        dst[(int64_t)(e / nc) * K + e % nc] = wst[(e / nc) * kWPitch + e % nc];
+      // accumulators drained: the MMA warp may start the next tile
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&accempty);
+      if (MODE == kRowW) {
+        asm volatile("bar.sync 1, %0;" ::"r"(kRowEpi) : "memory");  // the staged tile is complete
+        const int K = (int)g.K;
+        const int nc = min(64, K - f0);  // this tile's columns f0 .. f0 + nc - 1 of W
+        double* dst = g.out + tl.n0 * K + f0;
+        for (int e = etid; e < tl.nvb * nc; e += kRowEpi)
+          dst[(int64_t)(e / nc) * K + e % nc] = wst[(e / nc) * Shape::wst_pitch + e % nc];
+        asm volatile("bar.sync 1, %0;" ::"r"(kRowEpi) : "memory");  // staging free for the next tile
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -791,6 +837,14 @@ __global__ void __launch_bounds__(kRowThreads, 1)
       const int z = tile % g.nz, tb = (tile / g.nz) % g.ntb, i = g.first + tile / (g.nz * g.ntb);
       const bool tail = kb0 > 0;      // park for the previous CTA
       const bool head = kb1 < g.nub;  // finish with the next CTA's parked part
+      // scale exponents ahead of the accumulators
+      const int f0 = z * 64;
+      const int64_t t = (int64_t)tb * 128 + r;
+      const bool valid = t < g.ldx;
+      const int et = (valid && !tail) ? __ldg(g.aexp + (int64_t)i * g.ldx + t) : 0;
+      int be[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) be[j] = (!tail && f0 + cbase + j < g.kp) ? __ldg(g.bexp + f0 + cbase + j) : 0;
       mbar_wait(&accfull, seg & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       long long* pout = g.part + (int64_t)blockIdx.x * 2 * kSkParkPairs;
@@ -826,16 +880,10 @@ __global__ void __launch_bounds__(kRowThreads, 1)
         }
         asm volatile("bar.sync 1, %0;" ::"r"(kRowEpi) : "memory");
       }
-      const int f0 = z * 64;
-      const int64_t t = (int64_t)tb * 128 + r;
-      const bool valid = t < g.ldx;
-      const int et = valid ? g.aexp[(int64_t)i * g.ldx + t] : 0;
       double* out = g.out + (int64_t)i * g.kp * g.ldo + t;
-#pragma unroll 1
-      for (int c0 = cbase; c0 < cbase + 32; c0 += 8) {
-        int be[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) be[j] = (f0 + c0 + j < g.kp) ? __ldg(g.bexp + f0 + c0 + j) : 0;
+      for (int c = 0; c < 4; ++c) {
+        const int c0 = cbase + 8 * c;
         // the parked part: all sixteen L2 loads in flight before the TMEM drain
         // (ld.global.cg: the lines may be cached nowhere but L2)
         long long ph[8], pl[8];
@@ -859,7 +907,7 @@ __global__ void __launch_bounds__(kRowThreads, 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int f = f0 + c0 + j;
-            if (f < g.kp) out[(int64_t)f * g.ldo] = oz_hl_value(H[j], L[j]) * pow2(et + be[j] - 1);
+            if (f < g.kp) out[(int64_t)f * g.ldo] = oz_hl_value(H[j], L[j]) * pow2(et + be[8 * c + j] - 1);
           }
         }
       }
@@ -907,8 +955,22 @@ cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int
 
 namespace {
 
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+  }
+  return n;
+}
+
+// max_ctas > 0: persistent grid of at most max_ctas CTAs; else one CTA per tile
 template <int MODE, int NSA, int ND>
-cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, const RowGemmArgs& g, dim3 grid, cudaStream_t st) {
+cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, RowGemmArgs g, int max_ctas, cudaStream_t st) {
   const size_t bytes = RowGemmShape<MODE, NSA, ND>::smem_bytes;
   static bool configured = false;
   if (!configured) {
@@ -917,11 +979,11 @@ cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, const RowGemmArgs& g
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  if (grid.x == 0 || grid.y == 0) return cudaSuccess;
+  if (g.n_work <= 0) return cudaSuccess;
   if (g.kp > 128 || g.ldx % 32 != 0) return cudaErrorInvalidValue;
-  grid.z = (unsigned)((g.kp + 63) / 64);  // 64-feature halves of N
+  const int grid = max_ctas > 0 ? std::min(g.n_work, max_ctas) : g.n_work;
   k_oz_rowgemm<MODE, NSA, ND><<<grid, kRowThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(ta.opaque),
-                                                             *reinterpret_cast<const CUtensorMap*>(tb.opaque), g);
+                                                               *reinterpret_cast<const CUtensorMap*>(tb.opaque), g);
   return cudaGetLastError();
 }
 
@@ -929,8 +991,9 @@ cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, const RowGemmArgs& g
 
 cudaError_t launch_oz_sg(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
                          double* bred, int64_t ldx, int64_t kp, int64_t ldo, int first, int count, cudaStream_t st) {
-  RowGemmArgs g{gexp, sexp, bred, nullptr, ldx, kp, ldo, 0, first};
-  return run_rowgemm<kRowSG, kOzSlices, 7>(tmg, tms, g, dim3((unsigned)((ldx + 127) / 128), (unsigned)count), st);
+  RowGemmArgs g{gexp, sexp, bred, nullptr, ldx, kp, ldo, 0, first, 0, (int)((kp + 63) / 64), (int)((ldx + 127) / 128)};
+  g.n_work = count * g.nz * g.ntb;
+  return run_rowgemm<kRowSG, kOzSlices, 7>(tmg, tms, g, 0, st);
 }
 
 size_t oz_sk_park_bytes() { return (size_t)kSkParkPairs * 16; }
@@ -971,11 +1034,12 @@ cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* exp
 
 cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* rexp, double* W, const OzItem* items,
                         int n_items, int64_t ldx, int64_t kp, int64_t K, int nsl, cudaStream_t st) {
-  RowGemmArgs g{nullptr, rexp, W, items, ldx, kp, 0, K, 0};
-  if (nsl == 7) return run_rowgemm<kRowW, 7, 7>(tmqt, tmr, g, dim3((unsigned)n_items, 1), st);
+  RowGemmArgs g{nullptr, rexp, W, items, ldx, kp, 0, K, 0, 0, (int)((kp + 63) / 64), 0};
+  g.n_work = n_items * g.nz;
+  if (nsl == 7) return run_rowgemm<kRowW, 7, 7>(tmqt, tmr, g, sm_count(), st);
   // all seven d-groups for fp32 X-hat too: R's slices beyond the fourth carry
   // bits the orthonormality of W needs (W^T W = I to ~1e-13)
-  if (nsl == 4) return run_rowgemm<kRowW, 4, 7>(tmqt, tmr, g, dim3((unsigned)n_items, 1), st);
+  if (nsl == 4) return run_rowgemm<kRowW, 4, 7>(tmqt, tmr, g, sm_count(), st);
   return cudaErrorInvalidValue;
 }
 
