@@ -448,6 +448,45 @@ __global__ void __launch_bounds__(256) k_oz_slice_rows(const double* __restrict_
   }
 }
 
+// the same slices for a few long rows (S: kp rows, every iteration): one CTA
+// of eight warps per row, the row maximum by a block reduction and the
+// 32-column blocks spread over the warps (plain layout only)
+__global__ void __launch_bounds__(256) k_oz_slice_rows_wide(const double* __restrict__ M, int64_t ldm,
+                                                            int64_t ncols, int8_t* __restrict__ q, int64_t lq,
+                                                            int32_t* __restrict__ expo) {
+  __shared__ __align__(16) uint8_t rec[8][kOzRecord];
+  __shared__ double wmax[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x;
+  const double* row = M + r * ldm;
+  double m = 0.0;
+  for (int64_t c = threadIdx.x; c < ncols; c += 256) m = fmax(m, fabs(row[c]));
+  m = warp_max(m);
+  if (lane == 0) wmax[warp] = m;
+  __syncthreads();
+  m = wmax[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) m = fmax(m, wmax[w]);
+  const int e = (m > 0.0) ? frexp_exp(m) : 0;
+  if (threadIdx.x == 0) expo[r] = e;
+  const double scale = __longlong_as_double((long long)(1023 + 6 - e) << 52);
+  uint8_t* rb = rec[warp];
+  for (int64_t b = warp; b * 32 < ncols; b += 8) {
+    double y = row[b * 32 + lane] * scale;  // |y| < 64
+#pragma unroll
+    for (int s = 0; s < kOzSlices; ++s) {
+      int low;
+      const double rr = round_shift(y, &low);
+      rb[s * 32 + lane] = (uint8_t)(low & 0xFF);
+      y = (y - rr) * 128.0;
+    }
+    rb[7 * 32 + lane] = 0;
+    __syncwarp();
+    if (lane < 16) reinterpret_cast<uint4*>(q + r * lq + b * kOzRecord)[lane] = reinterpret_cast<const uint4*>(rb)[lane];
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // B_i = S G_i / 2 from the slices: CTA = (128 TRs t of subject i) x all 64
 // features f, contraction over the TRs u of G_i's rows in 32-wide blocks:
@@ -949,7 +988,10 @@ cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int
                                  int32_t* expo, cudaStream_t st, int64_t tile_rows) {
   if (rows <= 0) return cudaSuccess;
   if (ncols % 32 != 0) return cudaErrorInvalidValue;
-  k_oz_slice_rows<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(M, ldm, rows, ncols, q, lq, expo, tile_rows);
+  if (tile_rows == 0 && rows <= 1024)
+    k_oz_slice_rows_wide<<<(unsigned)rows, 256, 0, st>>>(M, ldm, ncols, q, lq, expo);
+  else
+    k_oz_slice_rows<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(M, ldm, rows, ncols, q, lq, expo, tile_rows);
   return cudaGetLastError();
 }
 
