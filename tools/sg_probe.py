@@ -17,7 +17,7 @@ from paper_1608_04647_b200.engine import SrmEngine  # noqa: E402
 
 V, T, K, N = 30000, 1000, 50, 40
 xs, _, _ = recipe_torch(N, V, T, K, seed=0, dtype="f64")
-eng = SrmEngine([V] * N, T, K, 16, storage="f64", gram=True, gram_i8=True, device=torch.device("cuda:0"))
+eng = SrmEngine([V] * N, T, K, 40, storage="f64", gram=True, gram_i8=True, device=torch.device("cuda:0"))
 eng.load(xs)
 eng.init_mapping(0, 0)
 eng.prepare_gram()
@@ -36,3 +36,26 @@ for _ in range(2):
 print(json.dumps({"per_iteration_ms": {k: float(np.median(v[1:])) for k, v in ts.items()},
                   "finalize_ms": {k: float(np.median(v)) for k, v in fin.items()}}), flush=True)
 
+
+# phases of a timed fit (events on the engine stream): Gram precompute, 20
+# replayed iterations, final W
+eng.reset()
+eng.init_mapping(0, 0)
+st = torch.cuda.current_stream()
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+torch.cuda.synchronize()
+ev[0].record(st)
+eng.prepare_gram()
+ev[1].record(st)
+for it in range(20):
+    if eng._graph is not None:
+        eng.replay()
+    else:
+        eng.step(None)
+        eng.capture()
+ev[2].record(st)
+eng.finalize()
+ev[3].record(st)
+torch.cuda.synchronize()
+print(json.dumps({"phase_ms": {"prepare_gram": ev[0].elapsed_time(ev[1]), "iterations_20": ev[1].elapsed_time(ev[2]),
+                               "finalize": ev[2].elapsed_time(ev[3])}}), flush=True)
