@@ -169,9 +169,10 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar(DevPlan p, int init) {
       break;
     }
     if (!(err == err)) break;  // NaN
-    // |I - P|_F <= 1e-13, or quadratic convergence has hit the roundoff floor
-    // (|I - P| no longer shrinking while below 1e-9): one more step, then stop
-    if (extra < 0 && (err <= 1e-26 || (err < 1e-18 && err > 0.25 * prev_err))) extra = 1;
+    // |I - P|_F <= 1e-10 (quadratic convergence: one more step reaches the
+    // roundoff floor), or the floor is already hit (|I - P| no longer shrinking
+    // while below 1e-9): one more step, then stop
+    if (extra < 0 && (err <= 1e-20 || (err < 1e-18 && err > 0.25 * prev_err))) extra = 1;
     prev_err = err;
     // Y_new = T Y  (-> Yn),  Z_new = T Z (-> old Y buffer once Y is consumed)
     mm_sym<KP>(Tm, buf[y], [&](int r, int col, double v0, double v1, bool dg) {
@@ -195,7 +196,11 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar(DevPlan p, int init) {
     __syncthreads();
     z = y;   // Z now lives in the old Y buffer
     y = f1;  // Y in Yn
-    if (extra > 0) --extra;
+    if (extra > 0 && --extra == 0) {
+      ++it;
+      converged = true;  // the step after the trigger: no check product needed
+      break;
+    }
   }
   // M = sym(Z) / sqrt(c)
   const int kp = (int)p.kp;

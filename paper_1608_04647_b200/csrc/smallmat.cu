@@ -584,19 +584,31 @@ __global__ void __launch_bounds__(kSmallThreads) k_reduce_terms(DevPlan p, doubl
   const int64_t n = p.kp * p.ldx;
   const int64_t e = (int64_t)blockIdx.x * kSmallThreads + threadIdx.x;
   if (e < n) {
-    // subjects in `order`, summed sequentially; loads batched 8 deep
+    // subjects in `order`, summed sequentially; loads batched 16 deep (the
+    // per-subject rho^2 are the same for every element: L1 broadcasts)
     double acc = 0.0;
     int j = 0;
-    for (; j + 8 <= count; j += 8) {
-      double x[8], r[8];
+    for (; j + 16 <= count; j += 16) {
+      double x[16], r[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 16; ++u) {
         const double* rec = rec_ptr(p, order[j + u]);
         x[u] = rec[e];
         r[u] = rec[n + RC_RHO2];
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc = (j + u == 0) ? x[u] / r[u] : acc + x[u] / r[u];
+      for (int u = 0; u < 16; ++u) acc = (j + u == 0) ? x[u] / r[u] : acc + x[u] / r[u];
+    }
+    for (; j + 4 <= count; j += 4) {
+      double x[4], r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* rec = rec_ptr(p, order[j + u]);
+        x[u] = rec[e];
+        r[u] = rec[n + RC_RHO2];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = (j + u == 0) ? x[u] / r[u] : acc + x[u] / r[u];
     }
     for (; j < count; ++j) {
       const double* rec = rec_ptr(p, order[j]);

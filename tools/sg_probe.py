@@ -59,3 +59,8 @@ ev[3].record(st)
 torch.cuda.synchronize()
 print(json.dumps({"phase_ms": {"prepare_gram": ev[0].elapsed_time(ev[1]), "iterations_20": ev[1].elapsed_time(ev[2]),
                                "finalize": ev[2].elapsed_time(ev[3])}}), flush=True)
+
+# Newton-Schulz steps of the last polar per subject (SRM_R_SCAL[i][0])
+SRM_R_SCAL = 12  # include/srm_b200.h
+scal = eng.region(SRM_R_SCAL, torch.float64)
+print(json.dumps({"ns_steps": scal.view(-1, 8)[:, 0].cpu().tolist()}), flush=True)
