@@ -685,7 +685,7 @@ std::vector<Stage> finalize_stages(srm_plan* p, int first, int count) {
       ns_polar_f32_supported((int)p->kp)) {
     // the per-iteration polar ran in fp32 (K > 80): the returned W takes the
     // exact fp64 transform of the last M-step's A^T A (still in bred)
-    v.push_back({"final_polar", [d](cudaStream_t st) { return launch_eig_polar_exact(d, 1, st); }});
+    v.push_back({"final_polar", [d](cudaStream_t st) { return launch_final_polar(d, st); }});
   }
   if (p->oz_w) {
     // W_i = Xhat_i R_i, R_i = S^T M_i / 2, from the int8 slices of Xhat on the
@@ -720,7 +720,7 @@ std::vector<Stage> finalize_stages(srm_plan* p, int first, int count) {
                                             1.0, region<ItemE>(p, I_ITEMS_TG), (int)p->items_tg.size(), st);
                  }});
     v.push_back({"final_reduce", [d](cudaStream_t st) { return launch_reduce_chunks(d, st); }});
-    v.push_back({"final_polar", [d](cudaStream_t st) { return launch_eig_polar_exact(d, 1, st); }});
+    v.push_back({"final_polar", [d](cudaStream_t st) { return launch_final_polar(d, st); }});
     v.push_back({"apply_w", [p, d](cudaStream_t st) {
                    return launch_apply_rows((int)p->kp, SRM_F32, d.af, p->np, d.mmat, p->kp * p->kp, d.wout,
                                             (int)p->K, region<ItemA>(p, I_ITEMS_TA), (int)p->items_ta.size(), st);

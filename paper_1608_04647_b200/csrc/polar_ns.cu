@@ -403,7 +403,98 @@ cudaError_t run_ns_f32(const DevPlan& p, int init, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Final fp64 polar transform for fp32 X-hat with 80 < kp <= 112, where the
+// per-iteration polar ran as the fp32 Newton-Schulz: refine its M (fp32
+// accuracy) by the symmetric Newton iteration for the inverse square root
+//     E_k = Z_k C Z_k - I,   Z_{k+1} = Z_k - (Z_k E_k + E_k Z_k) / 4,
+// which converges quadratically to the SPD solution of Z C Z = I, i.e.
+// C^{-1/2} (kernels.py:190-212 via W = A C^{-1/2}); from |E_0| ~ 1e-6 two
+// steps reach the fp64 roundoff floor.  One CTA per subject; each K x K
+// product stages its two operands in shared memory (2 x K (K + 1) doubles),
+// T and E live in the subject's qscr / qmat scratch, Z in mmat (in place).
+// A subject whose iteration does not converge keeps scal[i][1] = 0 and is
+// recomputed by the Jacobi kernel that follows (RankError semantics there).
+// ---------------------------------------------------------------------------
+constexpr int kRefThreads = 512;
+
+// D = op(A) op(B) for n x n row-major operands; `sym_a` stages A as (A + A^T) / 2
+__device__ __forceinline__ void ref_mm(const double* A, int64_t lda, bool sym_a, const double* B, int64_t ldb,
+                                       double* D, int64_t ldd, int n, double* sa, double* sb) {
+  const int ld = n + 1;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int a = e / n, b = e - a * n;
+    sa[a * ld + b] = sym_a ? 0.5 * (A[(int64_t)a * lda + b] + A[(int64_t)b * lda + a]) : A[(int64_t)a * lda + b];
+    sb[a * ld + b] = B[(int64_t)a * ldb + b];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int a = e / n, b = e - a * n;
+    double acc = 0.0;
+    for (int c = 0; c < n; ++c) acc = fma(sa[a * ld + c], sb[c * ld + b], acc);
+    D[(int64_t)a * ldd + b] = acc;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kRefThreads, 1) k_ns_refine(DevPlan p) {
+  extern __shared__ __align__(16) double rsm[];
+  __shared__ double red[kRefThreads / 32];
+  const int i = p.sub0 + blockIdx.x;
+  const int n = (int)p.K, kp = (int)p.kp;
+  double* sa = rsm;
+  double* sb = rsm + n * (n + 1);
+  const double* C = p.bred + (int64_t)i * p.kp * p.ldo + p.ldx;  // A^T A of the last M-step
+  double* Z = p.mmat + (int64_t)i * kp * kp;
+  double* T = p.qscr + (int64_t)i * kp * kp;
+  double* E = p.qmat + (int64_t)i * kp * kp;
+  bool ok = false;
+  int extra = -1;
+  double prev = 1e300;
+  for (int step = 0; step < 8; ++step) {
+    ref_mm(C, p.ldo, true, Z, kp, T, kp, n, sa, sb);  // T = C Z
+    ref_mm(Z, kp, false, T, kp, E, kp, n, sa, sb);    // E = Z C Z (- I below)
+    double err = 0.0;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int a = e / n, b = e - a * n;
+      const double d = E[(int64_t)a * kp + b] - (a == b ? 1.0 : 0.0);
+      E[(int64_t)a * kp + b] = d;
+      err += d * d;
+    }
+    err = block_sum<kRefThreads>(err, red);  // barrier: E complete
+    if (!(err == err)) break;
+    // |E|_F <= 1e-10, or no longer shrinking below 1e-9: one more step, then stop
+    if (extra < 0 && (err <= 1e-20 || (err < 1e-18 && err > 0.25 * prev))) extra = 1;
+    prev = err;
+    ref_mm(Z, kp, false, E, kp, T, kp, n, sa, sb);    // F = Z E
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int a = e / n, b = e - a * n;
+      Z[(int64_t)a * kp + b] -= 0.25 * (T[(int64_t)a * kp + b] + T[(int64_t)b * kp + a]);
+    }
+    __syncthreads();
+    if (extra > 0 && --extra == 0) {
+      ok = true;
+      break;
+    }
+  }
+  if (threadIdx.x == 0) p.scal[(int64_t)i * 8 + 1] = ok ? 1.0 : 0.0;
+}
+
 }  // namespace
+
+cudaError_t launch_ns_refine(const DevPlan& p, cudaStream_t s) {
+  const int n = (int)p.K;
+  const size_t bytes = (size_t)2 * n * (n + 1) * sizeof(double);
+  if (bytes > 227 * 1024) return cudaErrorInvalidValue;
+  static size_t configured = 0;
+  if (configured < bytes) {
+    cudaError_t e = cudaFuncSetAttribute(k_ns_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    configured = bytes;
+  }
+  k_ns_refine<<<p.nsub, kRefThreads, bytes, s>>>(p);
+  return cudaGetLastError();
+}
 
 bool ns_polar_supported(int kp) { return kp >= 8 && kp <= 80 && kp % 8 == 0; }
 

@@ -274,7 +274,9 @@ __device__ bool polar_from_eig(const double* C, const double* Q, int n, int ld, 
   return bad;
 }
 
+// init = 2: the final transform after k_ns_refine -- subjects it refined are skipped
 __global__ void __launch_bounds__(kSmallThreads) k_eig_polar(DevPlan p, int init) {
+  if (init == 2 && p.scal[(int64_t)(p.sub0 + blockIdx.x) * 8 + 1] != 0.0) return;
   const int iteration = init ? -1 : *p.iter;
   const int cold = (init || iteration == 0) ? 1 : 0;
   extern __shared__ __align__(16) double sm[];
@@ -1278,6 +1280,21 @@ cudaError_t launch_eig_polar_exact(const DevPlan& p, int init, cudaStream_t s) {
   cudaError_t e = set_smem((const void*)k_eig_polar, bytes);
   if (e != cudaSuccess) return e;
   k_eig_polar<<<p.nsub, kSmallThreads, bytes, s>>>(p, init);
+  return cudaGetLastError();
+}
+
+// the returned W's exact fp64 transform after a fit: fp64 Newton-Schulz up to
+// kp = 80; above, where the iterations ran the fp32 Newton-Schulz, its M refined
+// in fp64 (k_ns_refine) with Jacobi only for subjects the refinement leaves
+cudaError_t launch_final_polar(const DevPlan& p, cudaStream_t s) {
+  if (ns_polar_supported((int)p.kp)) return launch_ns_polar(p, 1, s);
+  if (!(p.xf32 && ns_polar_f32_supported((int)p.kp))) return launch_eig_polar_exact(p, 1, s);
+  cudaError_t e = launch_ns_refine(p, s);
+  if (e != cudaSuccess) return e;
+  const size_t bytes = eig_smem_bytes((int)p.K);
+  e = set_smem((const void*)k_eig_polar, bytes);
+  if (e != cudaSuccess) return e;
+  k_eig_polar<<<p.nsub, kSmallThreads, bytes, s>>>(p, 2);
   return cudaGetLastError();
 }
 
