@@ -48,7 +48,7 @@ namespace {
 using namespace tc;
 
 constexpr int kOzSlices = 7;
-constexpr int kOzThreads = 192;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue
+constexpr int kOzThreads = 320;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue
 constexpr int kOzStages = 3;
 constexpr int kOzBox = 16384;    // one 128-row x 128-byte SW128 box
 constexpr int kOzStageBytes = 4 * kOzBox;
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
         mbar_init(&bars.empty[s], 1);
       }
       mbar_init(&bars.accfull, 1);
-      mbar_init(&bars.accfree, 128);
+      mbar_init(&bars.accfree, kOzThreads - 64);
       asm volatile("fence.mbarrier_init.release.cluster;");
     }
   } else if (warp == 1) {
@@ -326,8 +326,9 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
       }
     }
   } else {
-    // ---------------- epilogue: warps 2-5 own TMEM lanes 32 (warp % 4) ----------------
+    // ---------------- epilogue: warps 2-9, TMEM lanes 32 (warp % 4), 64-column halves ----------------
     const int quarter = warp & 3;
+    const int cbase = ((warp - 2) >> 2) * 64;
     const int r = quarter * 32 + lane;
     const int64_t ta = it.m0 + r;
     const bool rin = ta < ldx;
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
         mbar_wait(&bars.accfull, npass & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int dlo = pass ? 4 : 0, dhi = pass ? kOzSlices - 1 : 3;
-        for (int c0 = 0; c0 < 128; c0 += 16) {
+        for (int c0 = cbase; c0 < cbase + 64; c0 += 16) {
           // pass 2 adds to pass 1's values: their loads go out first
           double prev[16];
 #pragma unroll
