@@ -347,22 +347,23 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             prev[j] = (npass > 0 && rin && it.n0 + c0 + j < ldx) ? grow[c0 + j] : 0.0;
-          double val[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) val[j] = 0.0;
           // the (up to four) d-groups of these 16 columns in flight, one wait
           uint32_t raw[4][16];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             if (dlo + q <= dhi) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 128u * (uint32_t)q + c0, raw[q]);
           tmem_wait_ld();
+          // the pass's d-groups as one exact int64 (|raw| < 2^31): pass 1
+          // H = sum_{d<4} raw_d 2^{7(3-d)} (x 2^-33), pass 2 L = sum_{d>=4}
+          // raw_d 2^{7(6-d)} (x 2^-54) -- one conversion and one rounding
+          double val[16];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (dlo + q <= dhi) {
-              const double sd = pow2(-12 - 7 * (dlo + q));
+          for (int j = 0; j < 16; ++j) {
+            long long h = 0;
 #pragma unroll
-              for (int j = 0; j < 16; ++j) val[j] = fma((double)(int32_t)raw[q][j], sd, val[j]);
-            }
+            for (int q = 0; q < 4; ++q)
+              if (dlo + q <= dhi) h = h * 128 + (long long)(int32_t)raw[q][j];
+            val[j] = (double)h * (pass ? 0x1p-54 : 0x1p-33);
           }
           if (rin) {
 #pragma unroll
@@ -584,9 +585,10 @@ __device__ __forceinline__ void oz_load_hl(uint32_t taddr, long long* H, long lo
   tmem_wait_ld();
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    H[j] = ((long long)(int32_t)raw[0][j] << 21) + ((long long)(int32_t)raw[1][j] << 14) +
-           ((long long)(int32_t)raw[2][j] << 7) + (long long)(int32_t)raw[3][j];
-    L[j] = ((long long)(int32_t)raw[4][j] << 14) + ((long long)(int32_t)raw[5][j] << 7) + (long long)(int32_t)raw[6][j];
+    // (multiplications, not shifts: the sums are signed)
+    H[j] = (long long)(int32_t)raw[0][j] * (1LL << 21) + (long long)(int32_t)raw[1][j] * (1LL << 14) +
+           (long long)(int32_t)raw[2][j] * 128 + (long long)(int32_t)raw[3][j];
+    L[j] = (long long)(int32_t)raw[4][j] * (1LL << 14) + (long long)(int32_t)raw[5][j] * 128 + (long long)(int32_t)raw[6][j];
   }
 }
 
