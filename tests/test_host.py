@@ -69,3 +69,34 @@ def test_recipe_is_seeded_and_row_centred():
     assert np.array_equal(sub[0], xs[1])
     x32, _, _ = recipe_numpy(2, 100, 20, 4, seed=1, smooth=5.0, dtype="f32")
     assert x32[0].dtype == np.float32
+
+
+def _sk_ranges(count, ldx, kp, max_ctas):
+    """The stream-K partition of launch_oz_sg_sk (ozaki.cu): k-blocks of all
+    (subject, 128-TR block, 64-feature half) tiles end to end, CTA c taking
+    [c span, (c + 1) span) with span >= the k-blocks of one tile."""
+    ntb, nz, nub = -(-ldx // 128), -(-kp // 64), ldx // 32
+    units = count * ntb * nz * nub
+    span = max(nub, -(-units // max_ctas))
+    grid = -(-units // span)
+    return [(c * span, min(units, (c + 1) * span)) for c in range(grid)], nub, units
+
+
+@pytest.mark.parametrize("count,ldx,kp,max_ctas", [(40, 1024, 56, 146), (10, 2016, 72, 146), (3, 96, 8, 146),
+                                                   (256, 1024, 64, 146), (5, 1024, 56, 1), (7, 320, 104, 30)])
+def test_stream_k_partition_joins_at_most_two_parts(count, ldx, kp, max_ctas):
+    """Every tile meets at most two CTA ranges, so a cut tile has exactly one
+    tail (first segment of CTA c + 1) and one head (last segment of CTA c):
+    the single park slot and flag per CTA of k_oz_sg_sk suffice, and the grid
+    never exceeds the co-resident CTAs it was sized for."""
+    ranges, nub, units = _sk_ranges(count, ldx, kp, max_ctas)
+    assert len(ranges) <= max_ctas
+    assert ranges[0][0] == 0 and ranges[-1][1] == units
+    assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+    for tile in range(units // nub):
+        lo, hi = tile * nub, (tile + 1) * nub
+        parts = [c for c, (a, b) in enumerate(ranges) if a < hi and b > lo]
+        assert 1 <= len(parts) <= 2
+        if len(parts) == 2:
+            c = parts[0]
+            assert parts[1] == c + 1 and ranges[c][1] < hi and ranges[c + 1][0] > lo
