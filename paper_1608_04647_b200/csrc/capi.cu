@@ -514,7 +514,11 @@ std::vector<Stage> e_stages(srm_plan* p) {
   v.push_back({"tail_kk", [d](cudaStream_t st) { return launch_tail_kk(d, st); }, 1});
   if (p->flags & SRM_FLAG_ORDERED) {
     const int n = (int)p->order.size();
-    v.push_back({"reduce_terms", [d, n](cudaStream_t st) { return launch_reduce_terms(d, d.red, d.order, n, st); }});
+    bool ident = true;
+    for (int j = 0; j < n; ++j) ident = ident && p->order[j] == j;
+    v.push_back({"reduce_terms", [d, n, ident](cudaStream_t st) {
+                   return launch_reduce_terms(d, d.red, d.order, n, st, ident);
+                 }});
   }
   v.push_back({"tail_s", [d](cudaStream_t st) { return launch_tail_s(d, st); }, 0, true});
   // Sigma_s, the LL and the next E-step's Sigma_s^{-1} on the side lane: the

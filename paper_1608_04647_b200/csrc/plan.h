@@ -98,7 +98,7 @@ bool finalize_rho_advances(const DevPlan& p);
 cudaError_t launch_finalize_rho_advance(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_set_iteration(const DevPlan& p, int iteration, int advance, cudaStream_t s);
 cudaError_t launch_reduce_terms(const DevPlan& p, double* dst, const int32_t* order, int count,
-                                cudaStream_t s);
+                                cudaStream_t s, bool ident = false);
 cudaError_t launch_tail(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_inv(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s);

@@ -582,7 +582,7 @@ __global__ void k_finalize_rho(DevPlan p, int init, int advance) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSmallThreads) k_reduce_terms(DevPlan p, double* dst,
                                                                 const int32_t* __restrict__ order,
-                                                                int count) {
+                                                                int count, int ident) {
   const int64_t n = p.kp * p.ldx;
   const int64_t e = (int64_t)blockIdx.x * kSmallThreads + threadIdx.x;
   if (e < n) {
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_reduce_terms(DevPlan p, doubl
       double x[16], r[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
-        const double* rec = rec_ptr(p, order[j + u]);
+        const double* rec = rec_ptr(p, ident ? j + u : order[j + u]);
         x[u] = rec[e];
         r[u] = rec[n + RC_RHO2];
       }
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_reduce_terms(DevPlan p, doubl
       double x[4], r[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const double* rec = rec_ptr(p, order[j + u]);
+        const double* rec = rec_ptr(p, ident ? j + u : order[j + u]);
         x[u] = rec[e];
         r[u] = rec[n + RC_RHO2];
       }
@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_reduce_terms(DevPlan p, doubl
       for (int u = 0; u < 4; ++u) acc = (j + u == 0) ? x[u] / r[u] : acc + x[u] / r[u];
     }
     for (; j < count; ++j) {
-      const double* rec = rec_ptr(p, order[j]);
+      const double* rec = rec_ptr(p, ident ? j : order[j]);
       const double v = rec[e] / rec[n + RC_RHO2];
       acc = (j == 0) ? v : acc + v;
     }
@@ -1369,10 +1369,11 @@ cudaError_t launch_set_iteration(const DevPlan& p, int iteration, int advance, c
 }
 
 cudaError_t launch_reduce_terms(const DevPlan& p, double* dst, const int32_t* order, int count,
-                                cudaStream_t s) {
+                                cudaStream_t s, bool ident) {
   const int64_t n = p.kp * p.ldx;
+  // ident: order[j] == j (one rank, or equal shards): no dependent index load
   k_reduce_terms<<<(unsigned)((n + kSmallThreads - 1) / kSmallThreads), kSmallThreads, 0, s>>>(
-      p, dst, order, count);
+      p, dst, order, count, ident ? 1 : 0);
   return cudaGetLastError();
 }
 
