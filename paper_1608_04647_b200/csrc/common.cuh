@@ -93,6 +93,14 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
   return t;
 }
 
+// L2 load of data another CTA wrote before a fence + atomic handshake: a weak
+// ld.global.cg (L1 bypassed), so independent loads stay in flight together
+__device__ __forceinline__ double ld_cg(const double* ptr) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(ptr));
+  return v;
+}
+
 template <typename T>
 __device__ __forceinline__ double to_f64(T x) { return static_cast<double>(x); }
 

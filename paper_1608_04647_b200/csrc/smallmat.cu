@@ -519,7 +519,8 @@ __global__ void __launch_bounds__(kSmallThreads, KP <= 64 ? 3 : 1) k_gram_from_b
   if (!last) return;
   __threadfence();
   // 16 elements per thread per batch: each chunk step issues 16 independent
-  // L2 loads (summation order over chunks unchanged)
+  // L2 loads (summation order over chunks unchanged); ld_cg, not __ldcg,
+  // whose strong loads the compiler keeps in order, a few in flight
   const double* all = p.gfb_part + (int64_t)i * p.gfb_chunks * kp * kp;
   double* out = p.bred + (int64_t)i * p.kp * p.ldo + p.ldx;
   const int n = kp * kp;
@@ -532,7 +533,7 @@ __global__ void __launch_bounds__(kSmallThreads, KP <= 64 ? 3 : 1) k_gram_from_b
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int e = e0 + tid + u * (int)blockDim.x;
-        if (e < n) s[u] += __ldcg(src + e);
+        if (e < n) s[u] += ld_cg(src + e);
       }
     }
 #pragma unroll
