@@ -231,6 +231,15 @@ int srm_gemm_tn(const double* w, int64_t ldw, const void* x, int x_dtype, int64_
 int srm_gemm_nt(const void* x, int x_dtype, int64_t ldx, const double* s, int64_t lds,
                 int64_t v, int64_t t, int64_t k, double alpha, double* out, int64_t ldo,
                 void* workspace, int64_t ws_bytes, void* stream);
+/* trace(A^T A) = sum of squares of a [rows x cols] f64 block (kernels.py:152-155)
+ * into *out (device), summed in a fixed order; non-finite entries raise
+ * InvalidInputError through status4 (kernels.py:45-46).  workspace >= 8 KB. */
+int srm_trace_ata(const double* a, int64_t lda, int64_t rows, int64_t cols, double* out,
+                  int32_t* status4, void* workspace, int64_t ws_bytes, void* stream);
+/* out = A + c I for a [n x n] f64 matrix (kernels.py:158-165); off-diagonal
+ * entries are copied bit for bit. */
+int srm_add_diag(const double* a, int64_t lda, int64_t n, double c, double* out, int64_t ldo,
+                 void* stream);
 /* in-place SPD inverse of a [n x n] f64 matrix (kernels.py:168-187).  Status
  * (DefinitenessError pivot) goes to status4 (device int32[4]). */
 int srm_spd_inverse(double* a, int64_t n, int32_t* status4, void* stream);
@@ -241,8 +250,11 @@ int srm_tail_step(const double* reduced, int64_t ldr, const double* sigma, int64
                   int64_t k, int64_t t, double rho0, double* s_out, int64_t lds_out,
                   double* var_out, double* sigma_out, double* trace_out, int32_t* status4,
                   void* workspace, int64_t ws_bytes, void* stream);
-/* orthogonal polar factor W = A (A^T A)^{-1/2} of a [v x k] f64 matrix
- * (kernels.py:190-212); rank failures go to status4. */
+/* orthogonal polar factor W = U V^T of a [v x k] f64 matrix (kernels.py:190-212):
+ * Householder TSQR A = Q R, one-sided Jacobi SVD of R (never forms A^T A, so
+ * singular values resolve to ~eps sigma_max like gesdd), W = A V diag(1/sigma) V^T,
+ * then one exact polar step of W.  RankError (sigma_min < 1e-12 sigma_max, or
+ * sigma_max = 0) goes to status4.  Synchronous. */
 int srm_polar(const double* a, int64_t lda, int64_t v, int64_t k, double* w, int64_t ldw,
               int32_t* status4, void* workspace, int64_t ws_bytes, void* stream);
 /* workspace bytes needed by srm_gemm_tn / srm_gemm_nt / srm_polar / srm_tail_step */

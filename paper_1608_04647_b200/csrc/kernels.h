@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace srm {
 
 // One CTA of the V-contraction kernel: out[m][n0+j] += sum_{c<rows} L[c][m] R[c][n0+j]
@@ -103,6 +105,44 @@ size_t oz_gram_smem_bytes();
 // X_i^T X_i tiles from the nsl-slice records (nsl = 7 for fp64 X-hat, 4 for fp32)
 cudaError_t launch_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
                            int n_items, int nsl, cudaStream_t st);
+
+// accurate polar transform (qr_polar.cu): Householder TSQR of a tall V x K
+// matrix, then a one-sided Jacobi SVD of R -> M = V diag(1/sigma) V^T
+struct QrJob {
+  const double* a;  // first row of this job's matrix (or the stacked factors of the last level)
+  int64_t lda;
+  int64_t rows;
+  int64_t rpc;      // rows per CTA
+  double* rout;     // nctas x (K x K) upper-triangular factors
+  int32_t nctas;
+  int32_t pad;
+};
+struct SvdJob {
+  const double* r;  // K x K factor (pitch K)
+  double* m;        // output transform, pitch ldm, zero-padded to mp x mp
+  int64_t ldm;
+  int32_t mp;
+  int32_t subject;  // reported with RankError
+};
+struct TsqrSchedule {
+  struct Job {
+    int64_t rows, rpc;
+    int nctas;
+    int64_t out_off;  // doubles into this level's output buffer
+  };
+  std::vector<std::vector<Job>> levels;  // level 0 reads the matrices, level L the factors of L - 1
+  int64_t buf_doubles = 0;               // per ping-pong buffer
+};
+bool qr_polar_supported(int K);
+int tsqr_block_rows(int K);
+TsqrSchedule tsqr_schedule(const std::vector<int64_t>& rows, int K, int target_ctas);
+std::vector<std::vector<QrJob>> tsqr_jobs(const TsqrSchedule& s, const std::vector<const double*>& a,
+                                          const std::vector<int64_t>& lda, int K, double* buf0, double* buf1,
+                                          std::vector<const double*>* r_final);
+int tsqr_max_ctas(const std::vector<TsqrSchedule::Job>& lvl);
+cudaError_t launch_tsqr(const QrJob* jobs_dev, int n_jobs, int max_ctas, int K, cudaStream_t st);
+cudaError_t launch_svd_polar(const SvdJob* jobs_dev, int n_jobs, int K, int32_t* status, const int32_t* iter,
+                             cudaStream_t st);
 
 // thread-local message returned by srm_last_error() (defined in capi.cu)
 void set_last_error(const char* where, cudaError_t e);

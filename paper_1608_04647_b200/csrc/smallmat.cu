@@ -1135,7 +1135,12 @@ __device__ __forceinline__ void spd_inverse_body(double* g, int n, int32_t* stat
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const int r = ty + 16 * i, c = tx + 16 * k;
-      if (r < n && c < n) g[r * n + c] = -a[i][k];
+      // the lower triangle, mirrored: kernels.py:185-187 symmetrizes dpotri's
+      // lower factor exactly (tril + tril(-1)^T), so the result equals its transpose
+      if (r < n && c < n && r >= c) {
+        g[r * n + c] = -a[i][k];
+        g[c * n + r] = -a[i][k];
+      }
     }
 }
 

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/srm_b200.h"
+#include "common.cuh"
 #include "kernels.h"
 #include "plan.h"
 
@@ -37,6 +38,47 @@ __global__ void k_sum_chunks(const double* __restrict__ part, int64_t stride, in
   double acc = part[e];
   for (int c = 1; c < nch; ++c) acc += part[(int64_t)c * stride + e];
   out[e] = acc;
+}
+
+// sum of squares of an [rows x cols] block (pitch lda) in a fixed order:
+// CTA c takes elements [c per, (c + 1) per) of the row-major enumeration, a
+// second single-CTA pass sums the CTA partials; non-finite entries raise
+// InvalidInputError (kernels.py:45-46)
+constexpr int kSqThreads = 256;
+
+__global__ void __launch_bounds__(kSqThreads) k_sumsq_part(const double* __restrict__ a, int64_t lda, int64_t rows,
+                                                          int64_t cols, int64_t per, double* __restrict__ part,
+                                                          int32_t* status) {
+  __shared__ double scratch[32];
+  const int64_t n = rows * cols;
+  const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min(n, e0 + per);
+  double s = 0.0;
+  bool bad = false;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += kSqThreads) {
+    const int64_t r = e / cols, c = e - r * cols;
+    const double x = a[r * lda + c];
+    bad |= !isfinite(x);
+    s = fma(x, x, s);
+  }
+  s = block_sum<kSqThreads>(s, scratch);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) raise_status(status, SRM_ERR_INVALID_INPUT, 0, -1);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kSqThreads) k_sum_final(const double* __restrict__ part, int n, double* out) {
+  __shared__ double scratch[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += kSqThreads) s += part[i];
+  s = block_sum<kSqThreads>(s, scratch);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void k_add_diag(const double* __restrict__ a, int64_t lda, int64_t n, double c, double* __restrict__ out,
+                           int64_t ldo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * n) return;
+  const int64_t r = e / n, col = e - r * n;
+  out[r * ldo + col] = r == col ? a[r * lda + col] + c : a[r * lda + col];
 }
 
 int ret(cudaError_t e, const char* where = "stateless") {
@@ -73,6 +115,22 @@ cudaError_t split_v(const double* L, int64_t kp, const void* R, int r_dtype, int
   return cudaGetLastError();
 }
 
+constexpr int kPolarCtas = 296;  // level-0 TSQR CTAs: two per SM
+
+int64_t polar_workspace_bytes(int64_t v, int64_t k) {
+  if (k < 1 || v < 1) return 0;
+  const int64_t kp = rup(k, 8);
+  const int64_t nch = std::max<int64_t>(1, (v + kChunk - 1) / kChunk);
+  const TsqrSchedule sch = tsqr_schedule({v}, (int)k, kPolarCtas);
+  int64_t b = 0;
+  b += 2 * rup(v * kp * 8, 256);                              // A copy, W = A M
+  b += 2 * rup(sch.buf_doubles * 8, 256);                     // TSQR factors (ping-pong)
+  b += rup(nch * kp * kp * 8, 256) + 3 * rup(kp * kp * 8, 256);  // W^T W partials, G, M, M2
+  b += rup((int64_t)sch.levels.size() * sizeof(QrJob), 256) + rup(sizeof(SvdJob), 256);
+  b += rup(nch * (int64_t)sizeof(ItemE), 256);
+  return b;
+}
+
 }  // namespace
 
 extern "C" {
@@ -92,7 +150,7 @@ int64_t srm_stateless_workspace_bytes(int64_t v, int64_t k, int64_t t) {
   // tail step: red, S (kp x ldx), sigma/var/cmat, per-tile partials
   const int64_t ntail = ldxp / 32;
   b += rup((2 * kp * ldxp + 16) * 8, 256) + rup((4 + ntail) * kp * kp * 8, 256) + rup((ntail * 4 + 64) * 8, 256);
-  return b + 4096;
+  return std::max(b, polar_workspace_bytes(v, k)) + 4096;
 }
 
 int srm_gemm_tn(const double* w, int64_t ldw, const void* x, int x_dtype, int64_t ldx, int64_t v, int64_t k,
@@ -201,6 +259,27 @@ int srm_tail_step(const double* reduced, int64_t ldr, const double* sigma, int64
   return ret(e);
 }
 
+int srm_trace_ata(const double* a, int64_t lda, int64_t rows, int64_t cols, double* out, int32_t* status4,
+                  void* workspace, int64_t ws_bytes, void* stream) {
+  if (rows < 1 || cols < 1 || lda < cols) return SRM_ERR_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n = rows * cols;
+  const int nct = (int)std::min<int64_t>(1024, (n + 4095) / 4096);
+  const int64_t per = (n + nct - 1) / nct;
+  if (ws_bytes < nct * 8) return SRM_ERR_CONFIG;
+  double* part = static_cast<double*>(workspace);
+  k_sumsq_part<<<nct, kSqThreads, 0, st>>>(a, lda, rows, cols, per, part, status4);
+  k_sum_final<<<1, kSqThreads, 0, st>>>(part, nct, out);
+  return ret(cudaGetLastError(), "trace_ata");
+}
+
+int srm_add_diag(const double* a, int64_t lda, int64_t n, double c, double* out, int64_t ldo, void* stream) {
+  if (n < 1 || lda < n || ldo < n) return SRM_ERR_SHAPE;
+  const int64_t tot = n * n;
+  k_add_diag<<<(unsigned)((tot + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(a, lda, n, c, out, ldo);
+  return ret(cudaGetLastError(), "add_diag");
+}
+
 int srm_spd_inverse(double* a, int64_t n, int32_t* status4, void* stream) {
   if (n < 1 || n > max_supported_k()) return n < 1 ? SRM_ERR_SHAPE : SRM_ERR_UNSUPPORTED;
   return ret(launch_spd_inverse(a, (int)n, status4, static_cast<cudaStream_t>(stream)));
@@ -210,23 +289,51 @@ int srm_polar(const double* a, int64_t lda, int64_t v, int64_t k, double* w, int
               void* workspace, int64_t ws_bytes, void* stream) {
   if (v < k) return SRM_ERR_SHAPE;
   if (k < 1) return SRM_ERR_SHAPE;
-  if (k > max_supported_k()) return SRM_ERR_UNSUPPORTED;
+  if (k > max_supported_k() || !qr_polar_supported((int)k)) return SRM_ERR_UNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t kp = rup(k, 8);
   const int64_t nch = std::max<int64_t>(1, (v + kChunk - 1) / kChunk);
+  const TsqrSchedule sch = tsqr_schedule({v}, (int)k, kPolarCtas);
   Carve c{static_cast<char*>(workspace), 0, ws_bytes};
   double* Ap = c.take<double>(v * kp);
+  double* Wt = c.take<double>(v * kp);
+  double* rb0 = c.take<double>(sch.buf_doubles);
+  double* rb1 = c.take<double>(sch.buf_doubles);
   double* part = c.take<double>(nch * kp * kp);
   double* G = c.take<double>(kp * kp);
   double* M = c.take<double>(kp * kp);
+  double* M2 = c.take<double>(kp * kp);
+  QrJob* qj = c.take<QrJob>((int64_t)sch.levels.size());
+  SvdJob* sj = c.take<SvdJob>(1);
   ItemE* items = c.take<ItemE>(nch);
   if (!items) return SRM_ERR_CONFIG;
+  // (1) R of A = Q R (Householder TSQR), (2) SVD of R (one-sided Jacobi) ->
+  // M = V diag(1/sigma) V^T and the rank test of kernels.py:202-206, (3) W = A M
+  // (the polar factor up to eps cond(A)), (4) one exact polar step of W itself,
+  // W <- W (W^T W)^{-1/2}: W^T W is within eps cond(A) of I, so this restores
+  // orthonormality to fp64 roundoff (W = U V^T of gesdd is orthonormal to eps)
+  std::vector<const double*> rfin;
+  const std::vector<std::vector<QrJob>> jobs = tsqr_jobs(sch, {Ap}, {kp}, (int)k, rb0, rb1, &rfin);
+  std::vector<QrJob> flat;
+  for (const auto& l : jobs) flat.push_back(l[0]);
+  const char* where = "polar: stage A";
   cudaError_t e = cudaMemsetAsync(Ap, 0, v * kp * 8, st);
   if (e == cudaSuccess) e = cudaMemcpy2DAsync(Ap, kp * 8, a, lda * 8, k * 8, v, cudaMemcpyDeviceToDevice, st);
-  if (e == cudaSuccess) e = split_v(Ap, kp, Ap, SRM_F64, kp, kp, v, 1.0, part, G, items, st);
-  if (e == cudaSuccess) e = launch_polar_small(G, kp, (int)k, M, kp, status4, st);
-  if (e == cudaSuccess) e = launch_apply_right(Ap, kp, v, (int)k, M, kp, w, ldw, st);
-  return ret(e);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(qj, flat.data(), flat.size() * sizeof(QrJob), cudaMemcpyHostToDevice, st);
+  for (size_t L = 0; L < jobs.size() && e == cudaSuccess; ++L) {
+    where = "polar: tsqr";
+    e = launch_tsqr(qj + L, 1, tsqr_max_ctas(sch.levels[L]), (int)k, st);
+  }
+  SvdJob sv{rfin[0], M, kp, (int32_t)kp, 0};
+  if (e == cudaSuccess) { where = "polar: svd"; e = cudaMemcpyAsync(sj, &sv, sizeof(SvdJob), cudaMemcpyHostToDevice, st); }
+  if (e == cudaSuccess) e = launch_svd_polar(sj, 1, (int)k, status4, nullptr, st);
+  if (e == cudaSuccess) { where = "polar: A M"; e = cudaMemsetAsync(Wt, 0, v * kp * 8, st); }
+  if (e == cudaSuccess) e = launch_apply_right(Ap, kp, v, (int)k, M, kp, Wt, kp, st);
+  if (e == cudaSuccess) { where = "polar: W^T W"; e = split_v(Wt, kp, Wt, SRM_F64, kp, kp, v, 1.0, part, G, items, st); }
+  if (e == cudaSuccess) { where = "polar: refine"; e = launch_polar_small(G, kp, (int)k, M2, kp, status4, st); }
+  if (e == cudaSuccess) e = launch_apply_right(Wt, kp, v, (int)k, M2, kp, w, ldw, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the job tables were staged from the host stack
+  return ret(e, where);
 }
 
 }  // extern "C"
