@@ -12,7 +12,7 @@
  *   every function returns an srm_status code; SRM_OK == 0.  Device-side
  *   failures (non-finite input, rank deficiency, Cholesky breakdown) are
  *   recorded asynchronously in a device status word -- {code, arg, iteration,
- *   0} -- and surface through srm_read_status().  `arg` is the failing
+ *   warnings} -- and surface through srm_read_status().  `arg` is the failing
  *   Cholesky pivot (0-based, DefinitenessError.pivot) or the global subject
  *   index (RankError / InvalidInputError).  srm_last_error() returns a
  *   thread-local message for the last host-side failure.
@@ -48,6 +48,16 @@ enum srm_status {
   SRM_ERR_IO = 9             /* file system error (srm_sfab_last_error) */
 };
 
+/* warning bits of the device status word (element 3), sticky until
+ * srm_clear_status / srm_reset */
+enum srm_warning {
+  SRM_WARN_POLAR_CONDITION = 1 /* a subject's A^T A was too ill-conditioned for the
+                                  Gram-route polar transform (sigma_min / sigma_max
+                                  below ~3e-3): redo the fit with SRM_FLAG_EXACT_POLAR,
+                                  which resolves it -- or raises RankError -- like the
+                                  reference's SVD (kernels.py:190-212) */
+};
+
 /* plan flags */
 enum srm_flags {
   SRM_FLAG_ORDERED = 1,   /* E-step terms summed in ascending global subject order
@@ -60,10 +70,14 @@ enum srm_flags {
   SRM_FLAG_TC = 8,        /* fp32 X-hat: streaming passes on the tcgen05 tensor cores
                              as 3xTF32 split-precision MMAs (ignored for fp64
                              storage, K > 128, or with SRM_FLAG_GRAM) */
-  SRM_FLAG_GRAM_I8 = 16   /* with SRM_FLAG_GRAM and fp64 storage: X^T X from seven
+  SRM_FLAG_GRAM_I8 = 16,  /* with SRM_FLAG_GRAM and fp64 storage: X^T X from seven
                              exact int8 slices per value (power-of-two column
                              scales) on the tcgen05 int8 tensor cores, ~2^-48
                              relative to the column maxima; otherwise fp64 DMMA */
+  SRM_FLAG_EXACT_POLAR = 32 /* every polar transform (init and M-step) from A itself:
+                             Householder TSQR + one-sided Jacobi SVD of R, never
+                             A^T A; implies the fp64 streaming path (A_i = X_i S^T / 2
+                             formed each iteration; clears GRAM, GRAM_I8, TC) */
 };
 
 /* workspace regions (srm_plan_region) */
@@ -216,7 +230,8 @@ int srm_profile_gram(srm_plan* plan, float* ms_out, int capacity, int* n_out, vo
 int srm_profile_finalize(srm_plan* plan, float* ms_out, int capacity, int* n_out, void* stream);
 const char* srm_profile_name(int index);
 
-/* synchronous copy of the device status word {code, arg, iteration, 0} */
+/* synchronous copy of the device status word {code, arg, iteration, warnings}
+ * (warnings: SRM_WARN_* bits) */
 int srm_read_status(srm_plan* plan, int32_t* out4);
 /* clear the device status word (asynchronous) */
 int srm_clear_status(srm_plan* plan, void* stream);

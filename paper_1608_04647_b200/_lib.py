@@ -71,7 +71,8 @@ SIGNATURES = [
 
 # include/srm_b200.h enums
 SRM_F64, SRM_F32 = 0, 1
-FLAG_ORDERED, FLAG_TOLERANCE, FLAG_GRAM, FLAG_TC, FLAG_GRAM_I8 = 1, 2, 4, 8, 16
+FLAG_ORDERED, FLAG_TOLERANCE, FLAG_GRAM, FLAG_TC, FLAG_GRAM_I8, FLAG_EXACT_POLAR = 1, 2, 4, 8, 16, 32
+WARN_POLAR_CONDITION = 1
 (R_XHAT, R_AMAT, R_WOUT, R_MU, R_TERMS, R_RED, R_REDLOCAL, R_S, R_SIGMA, R_HIST, R_STATUS,
  R_MMAT, R_SCAL, R_GRAM, R_VAR) = range(15)
 (D_LDX, D_KP, D_ROWS, D_TERM_STRIDE, D_RED_STRIDE, D_HIST_STRIDE, D_N_SLOTS, D_SLOT_OFFSET,

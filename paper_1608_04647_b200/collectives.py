@@ -21,7 +21,6 @@ communicators) is accepted by ``fit`` too; its exchanges are staged through
 host memory with ``gather`` + ``broadcast``.
 """
 
-import pickle
 import struct
 import time
 from dataclasses import dataclass, field
@@ -38,6 +37,7 @@ __all__ = [
     "rank_offsets",
     "rank_counts",
     "shard_bounds",
+    "any_rank",
 ]
 
 _LEN = struct.Struct("<Q")
@@ -225,10 +225,27 @@ class TorchCommunicator(Communicator):
             acc += a
         return acc
 
+    def _tensor_device(self):
+        import torch
+
+        return torch.device("cuda", torch.cuda.current_device()) if self.device_collectives else torch.device("cpu")
+
     def _broadcast(self, buf):
-        box = [pickle.dumps(buf) if self.rank == 0 else None]
-        self._dist.broadcast_object_list(box, src=0, group=self._group)
-        return np.array(pickle.loads(box[0]), dtype=np.float64)
+        # shape, then the raw float64 payload: two tensor broadcasts, no pickling
+        import torch
+
+        dev = self._tensor_device()
+        shape = torch.zeros(2, dtype=torch.int64, device=dev)
+        if self.rank == 0:
+            shape[0], shape[1] = buf.shape
+        self._dist.broadcast(shape, src=0, group=self._group)
+        rows, cols = (int(x) for x in shape.cpu())
+        if self.rank == 0:
+            data = torch.from_numpy(np.ascontiguousarray(buf, dtype=np.float64)).to(dev)
+        else:
+            data = torch.empty((rows, cols), dtype=torch.float64, device=dev)
+        self._dist.broadcast(data, src=0, group=self._group)
+        return data.cpu().numpy()
 
     def _gather(self, local):
         parts = self._objs(local)
@@ -278,6 +295,19 @@ def rank_counts(comm, local_count):
         counts = None
     table = comm.broadcast(counts)
     return [int(c) for c in table[0]]
+
+
+def any_rank(comm, flag):
+    """True on every rank when ``flag`` is true on any rank."""
+    if comm.size == 1:
+        return bool(flag)
+    if isinstance(comm, TorchCommunicator):
+        return any(bool(f) for f in comm._objs(bool(flag)))
+    blobs = comm.gather(b"\x01" if flag else b"\x00")
+    table = None
+    if comm.rank == 0:
+        table = np.array([[1.0 if any(b != b"\x00" for b in blobs) else 0.0]])
+    return bool(comm.broadcast(table)[0, 0] != 0.0)
 
 
 def rank_offsets(comm, local_count):

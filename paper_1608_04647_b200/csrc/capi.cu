@@ -80,6 +80,10 @@ enum Internal {
   I_ITEMS_OW,
   I_OZSKPART,
   I_OZSKFLAG,
+  I_QRBUF0,
+  I_QRBUF1,
+  I_QRJOBS,
+  I_SVDJOBS,
   I_COUNT
 };
 
@@ -142,6 +146,7 @@ struct srm_plan {
   TmaMap tm_q32, tm_r;
   bool sk_off = false;                // SRM_B200_SG_PER_TILE=1: per-tile B = S G / 2 (test knob)
   int sk_ctas = 0;                    // stream-K B = S G / 2: persistent CTAs (SMs less two for the side lane)
+  TsqrSchedule qr;                    // SRM_FLAG_EXACT_POLAR: TSQR levels over the local A_i (job table: level-major)
 };
 
 namespace {
@@ -214,6 +219,11 @@ void layout(srm_plan* p) {
   sz[I_ITEMS_OW] = (int64_t)p->items_ow.size() * sizeof(OzItem);
   sz[I_OZSKPART] = p->oz_sg ? (int64_t)p->sk_ctas * oz_sk_park_bytes() : 0;
   sz[I_OZSKFLAG] = p->oz_sg ? (int64_t)p->sk_ctas * 4 : 0;
+  const bool exact = (p->flags & SRM_FLAG_EXACT_POLAR) != 0;
+  sz[I_QRBUF0] = exact ? p->qr.buf_doubles * 8 : 0;
+  sz[I_QRBUF1] = exact ? p->qr.buf_doubles * 8 : 0;
+  sz[I_QRJOBS] = exact ? (int64_t)p->qr.levels.size() * p->n_local * (int64_t)sizeof(QrJob) : 0;
+  sz[I_SVDJOBS] = exact ? (int64_t)p->n_local * (int64_t)sizeof(SvdJob) : 0;
   int64_t cur = 0;
   for (int r = 0; r < I_COUNT; ++r) {
     p->off[r] = cur;
@@ -418,6 +428,9 @@ void build_work(srm_plan* p) {
       }
     }
   }
+  // exact polar route: TSQR levels over every local A_i (V_i x K rows of AMAT)
+  p->qr = TsqrSchedule();
+  if (p->flags & SRM_FLAG_EXACT_POLAR) p->qr = tsqr_schedule(p->V, (int)p->K, 296);
   // subject table
   p->subj.assign((size_t)p->n_local * kSubjCols, 0);
   for (int i = 0; i < p->n_local; ++i) {
@@ -539,9 +552,40 @@ void push_finalize_rho(const DevPlan& d, std::vector<Stage>& v) {
   }
 }
 
+// SRM_FLAG_EXACT_POLAR: M_i of local subjects [first, first + count) from A_i
+// itself (TSQR levels, then the SVD of each R_i); RankError as kernels.py:202-206
+cudaError_t launch_exact_polar(srm_plan* p, int first, int count, bool init, cudaStream_t st) {
+  const QrJob* jobs = region<QrJob>(p, I_QRJOBS);
+  cudaError_t e = cudaSuccess;
+  for (size_t L = 0; L < p->qr.levels.size() && e == cudaSuccess; ++L) {
+    int mx = 0;
+    for (int i = first; i < first + count; ++i) mx = std::max(mx, p->qr.levels[L][i].nctas);
+    e = launch_tsqr(jobs + (int64_t)L * p->n_local + first, count, mx, (int)p->K, st);
+  }
+  if (e == cudaSuccess)
+    e = launch_svd_polar(region<SvdJob>(p, I_SVDJOBS) + first, count, (int)p->K, p->dp.status,
+                         init ? nullptr : p->dp.iter, st);
+  return e;
+}
+
 std::vector<Stage> m_stages(srm_plan* p) {
   const DevPlan& d = p->dp;
   std::vector<Stage> v;
+  if (p->flags & SRM_FLAG_EXACT_POLAR) {
+    v.push_back({"contract_a", [p, d](cudaStream_t st) {
+                   return launch_contract_a((int)p->kp, p->dtype, d.xhat, p->ldx, d.S, p->ldx, p->ldx, d.amat, p->kp,
+                                            0.5, region<ItemA>(p, I_ITEMS_A), (int)p->items_a.size(), st);
+                 }});
+    v.push_back({"contract_e_xhat", [p, d](cudaStream_t st) {
+                   return launch_contract_e((int)p->kp, SRM_F64, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part,
+                                            p->ldo, 1.0, region<ItemE>(p, I_ITEMS_EX), (int)p->items_ex.size(), st);
+                 }});
+    v.push_back({"reduce_chunks", [d](cudaStream_t st) { return launch_reduce_chunks(d, st); }});
+    v.push_back({"exact_polar", [p](cudaStream_t st) { return launch_exact_polar(p, 0, p->n_local, false, st); }});
+    v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 1, st); }});
+    push_finalize_rho(d, v);
+    return v;
+  }
   if (p->flags & SRM_FLAG_GRAM) {
     // B_i = S G_i / 2 straight into the reduced slot (G_i = X_i^T X_i, one-time)
     if (p->oz_sg) {
@@ -849,6 +893,14 @@ int srm_plan_create(srm_plan** out, int dtype, int n_local, const int64_t* n_vox
   if ((p->flags & SRM_FLAG_TC) && (dtype != SRM_F32 || !tc_supported((int)k))) p->flags &= ~SRM_FLAG_TC;
   if ((p->flags & SRM_FLAG_TC) && (p->flags & SRM_FLAG_GRAM)) p->flags &= ~SRM_FLAG_TC;
   if ((p->flags & SRM_FLAG_GRAM_I8) && !(p->flags & SRM_FLAG_GRAM)) p->flags &= ~SRM_FLAG_GRAM_I8;
+  if (p->flags & SRM_FLAG_EXACT_POLAR) {
+    // A_i is formed every iteration (fp64 streaming path) so its own QR/SVD gives M_i
+    p->flags &= ~(SRM_FLAG_GRAM | SRM_FLAG_GRAM_I8 | SRM_FLAG_TC);
+    if (!qr_polar_supported((int)k)) {
+      delete p;
+      return fail(SRM_ERR_UNSUPPORTED, "k = " + std::to_string(k) + " exceeds the exact polar route's shared memory");
+    }
+  }
   p->np = tc_np((int)k);
   p->n_total = 0;
   p->max_local = 0;
@@ -956,6 +1008,26 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     e = cudaMemcpy(p->ws + p->off[u.r], u.src, p->size[u.r], cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "bind upload");
   }
+  if (p->flags & SRM_FLAG_EXACT_POLAR) {
+    std::vector<const double*> a;
+    std::vector<int64_t> lda;
+    for (int i = 0; i < p->n_local; ++i) {
+      a.push_back(region<double>(p, SRM_R_AMAT) + p->row_off[i] * p->kp);
+      lda.push_back(p->kp);
+    }
+    std::vector<const double*> rfin;
+    const auto lv = tsqr_jobs(p->qr, a, lda, (int)p->K, region<double>(p, I_QRBUF0), region<double>(p, I_QRBUF1), &rfin);
+    std::vector<QrJob> flat;
+    for (const auto& l : lv) flat.insert(flat.end(), l.begin(), l.end());
+    std::vector<SvdJob> sv;
+    for (int i = 0; i < p->n_local; ++i)
+      sv.push_back({rfin[i], region<double>(p, SRM_R_MMAT) + (int64_t)i * p->kp * p->kp, p->kp, (int32_t)p->kp,
+                    (int32_t)(p->global0 + i)});
+    e = cudaMemcpy(region<QrJob>(p, I_QRJOBS), flat.data(), flat.size() * sizeof(QrJob), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(region<SvdJob>(p, I_SVDJOBS), sv.data(), sv.size() * sizeof(SvdJob), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "bind qr jobs");
+  }
   // Sigma_s = I (srm.py:248); S starts at zero
   std::vector<double> eye((size_t)p->kp * p->kp, 0.0);
   for (int64_t j = 0; j < p->K; ++j) eye[(size_t)j * p->kp + j] = 1.0;
@@ -1042,13 +1114,14 @@ int srm_init_mapping_range(srm_plan* p, int first, int count, void* stream) {
     exn += p->nchunk[i] * ntiles;
     ean += p->nchunk[i];
   }
+  const bool exact = (p->flags & SRM_FLAG_EXACT_POLAR) != 0;
   cudaError_t e = launch_contract_e((int)p->kp, SRM_F64, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
                                     region<ItemE>(p, I_ITEMS_EX) + ex0, (int)exn, st);
-  if (e == cudaSuccess)
+  if (e == cudaSuccess && !exact)  // the Gram route's A^T A of the draw
     e = launch_contract_e((int)p->kp, SRM_F64, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0,
                           region<ItemE>(p, I_ITEMS_EA) + p->chunk0[first], (int)ean, st);
   if (e == cudaSuccess) e = launch_reduce_chunks(d, st);
-  if (e == cudaSuccess) e = launch_eig_polar(d, 1, st);
+  if (e == cudaSuccess) e = exact ? launch_exact_polar(p, first, count, true, st) : launch_eig_polar(d, 1, st);
   if (e == cudaSuccess) e = launch_apply_m(d, 0, st);
   if (e == cudaSuccess) e = launch_finalize_rho(d, 1, st);
   return check(e, "init_mapping");
@@ -1233,7 +1306,6 @@ int srm_read_status(srm_plan* p, int32_t* out4) {
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cuda_fail(e, "synchronize");
   e = cudaMemcpy(out4, p->dp.status, 16, cudaMemcpyDeviceToHost);
-  out4[3] = 0;
   return check(e, "read_status");
 }
 

@@ -16,7 +16,7 @@ namespace srm {
 constexpr int kWarp = 32;
 
 // ---------------------------------------------------------------------------
-// device status word: {code, arg (subject / pivot), iteration, armed}
+// device status word: {code, arg (subject / pivot), iteration, warning bits}
 // first error wins (atomicCAS on code); later kernels may early-exit.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void raise_status(int32_t* status, int code, int arg, int iter) {
@@ -25,6 +25,18 @@ __device__ __forceinline__ void raise_status(int32_t* status, int code, int arg,
     status[2] = iter;
   }
 }
+
+// warning bits in status[3] (SRM_WARN_*): sticky, never abort the stream.
+// The Gram-route polar transform (A^T A)^{-1/2} cannot resolve
+// sigma_min / sigma_max below ~1e-8 and loses ~eps cond(A)^2; when a subject's
+// A^T A is that ill-conditioned it sets SRM_WARN_POLAR_CONDITION instead of
+// deciding the rank test, and the host re-runs the fit on the exact route
+// (TSQR + SVD of A, qr_polar.cu), which raises RankError as kernels.py:202-206.
+__device__ __forceinline__ void raise_warning(int32_t* status, int bits) { atomicOr(&status[3], bits); }
+// largest c / lambda_min (c >= lambda_max) the Gram route accepts: the
+// transform's error ~eps_G c / lambda_min stays below ~1e-9 for the ~1e-14
+// relative error eps_G of the int8-sliced Gram
+constexpr double kGramCondLimit = 1e5;
 
 // ---------------------------------------------------------------------------
 // FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col)

@@ -11,8 +11,10 @@
 // K x K products done with mma.sync.m8n8k4.f64 from shared memory, upper tiles
 // only (the products are symmetric) -- a
 // tensor-core replacement for the latency-bound Jacobi rotations.  A direction
-// with lambda ~ 0 never converges: that is reported as RankError
-// (kernels.py:202-206).
+// with lambda ~ 0 converges slowly or not at all, and any lambda_min below
+// c / kGramCondLimit is beyond what the Gram route resolves: both raise
+// SRM_WARN_POLAR_CONDITION, and the fit is redone on the exact route
+// (qr_polar.cu), which applies the rank test of kernels.py:202-206.
 #include "common.cuh"
 #include "plan.h"
 
@@ -202,21 +204,22 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar(DevPlan p, int init) {
       break;
     }
   }
-  // M = sym(Z) / sqrt(c)
+  // M = sym(Z) / sqrt(c); |Z|_F^2 = sum_j c / lambda_j >= c / lambda_min
   const int kp = (int)p.kp;
   double* Mg = p.mmat + (int64_t)i * kp * kp;
   const double* Z = buf[z];
   const double s = degenerate ? 0.0 : 1.0 / sqrt(c);
+  double zz = 0.0;
   for (int e = tid; e < kp * kp; e += blockDim.x) {
     const int a = e / kp, b = e - a * kp;
-    Mg[e] = (a < n && b < n) ? 0.5 * (Z[a * LD + b] + Z[b * LD + a]) * s : 0.0;
+    const double v = (a < n && b < n) ? 0.5 * (Z[a * LD + b] + Z[b * LD + a]) : 0.0;
+    zz = fma(v, v, zz);
+    Mg[e] = v * s;
   }
+  zz = block_sum<kNsThreads>(zz, red);
   if (tid == 0) {
     p.scal[(int64_t)i * 8 + 0] = (double)it;
-    if (degenerate || !converged) {
-      const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
-      raise_status(p.status, SRM_ERR_RANK, (int)sj[SC_GLOBAL], init ? -1 : *p.iter);
-    }
+    if (degenerate || !converged || !(zz <= kGramCondLimit)) raise_warning(p.status, SRM_WARN_POLAR_CONDITION);
   }
 }
 
@@ -377,16 +380,17 @@ __global__ void __launch_bounds__(256) k_ns_polar_f32(DevPlan p, int init) {
   double* Mg = p.mmat + (int64_t)i * kp * kp;
   const float* Z = buf[z];
   const double sc = degenerate ? 0.0 : 1.0 / sqrt(c);
+  double zz = 0.0;
   for (int e = tid; e < kp * kp; e += blockDim.x) {
     const int a = e / kp, b = e - a * kp;
-    Mg[e] = (a < n && b < n) ? 0.5 * ((double)Z[a * LD + b] + (double)Z[b * LD + a]) * sc : 0.0;
+    const double v = (a < n && b < n) ? 0.5 * ((double)Z[a * LD + b] + (double)Z[b * LD + a]) : 0.0;
+    zz = fma(v, v, zz);
+    Mg[e] = v * sc;
   }
+  zz = block_sum<256>(zz, red);
   if (tid == 0) {
     p.scal[(int64_t)i * 8 + 0] = (double)it;
-    if (degenerate || !converged) {
-      const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
-      raise_status(p.status, SRM_ERR_RANK, (int)sj[SC_GLOBAL], init ? -1 : *p.iter);
-    }
+    if (degenerate || !converged || !(zz <= kGramCondLimit)) raise_warning(p.status, SRM_WARN_POLAR_CONDITION);
   }
 }
 

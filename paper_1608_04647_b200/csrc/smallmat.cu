@@ -235,14 +235,15 @@ __device__ int jacobi_eig(double* C, double* Q, int n, int ld, JacobiScratch js,
   return sweep;
 }
 
-// Shared tail of the polar factor: rank check on the Gram eigenvalues and
-// M = Q diag(lambda^-1/2) Q^T written to global (ldm, zero-padded to mp).
-// Returns true when the Gram matrix is numerically rank deficient
-// (kernels.py:202-206 raises RankError when s_min < 1e-12 s_max, i.e.
-// lambda_min < 1e-24 lambda_max; the Gram route cannot resolve ratios below
-// ~1e-16, so a non-positive lambda_min is also rank deficient).
+// Shared tail of the polar factor: conditioning check on the Gram eigenvalues
+// and M = Q diag(lambda^-1/2) Q^T written to global (ldm, zero-padded to mp).
+// Returns true when lambda_min <= lambda_max / limit (or lambda_max <= 0 /
+// NaN): with limit = kGramCondLimit the fit's Gram route hands the subject to
+// the exact route (SRM_WARN_POLAR_CONDITION); the stateless near-orthonormal
+// refinement step (k_polar_small) uses 1e24, the rank threshold of
+// kernels.py:202-206 squared.
 __device__ bool polar_from_eig(const double* C, const double* Q, int n, int ld, double* wsh,
-                               double* M, int64_t ldm, int mp) {
+                               double* M, int64_t ldm, int mp, double limit) {
   const int tid = threadIdx.x;
   __shared__ int s_bad;
   if (tid == 0) {
@@ -254,7 +255,7 @@ __device__ bool polar_from_eig(const double* C, const double* Q, int n, int ld, 
       lmax = fmax(lmax, l);
       lmin = fmin(lmin, l);
     }
-    s_bad = (nan || !(lmax > 0.0) || !(lmin > 1e-24 * lmax)) ? 1 : 0;
+    s_bad = (nan || !(lmax > 0.0) || !(lmin * limit > lmax)) ? 1 : 0;
   }
   for (int j = tid; j < n; j += blockDim.x) {
     const double l = C[j * ld + j];
@@ -332,15 +333,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_eig_polar(DevPlan p, int init
   JacobiScratch js{cs, sn, pp, qq, &rot};
   const int sweeps = jacobi_eig(C, Q, n, ld, js, 40);
   if (tid == 0) p.scal[(int64_t)i * 8 + 0] = (double)sweeps;
-  const bool bad = polar_from_eig(C, Q, n, ld, wsh, p.mmat + (int64_t)i * kp * kp, kp, kp);
+  const bool bad = polar_from_eig(C, Q, n, ld, wsh, p.mmat + (int64_t)i * kp * kp, kp, kp, kGramCondLimit);
   for (int e = tid; e < kp * kp; e += blockDim.x) {
     const int a = e / kp, b = e - a * kp;
     Qg[e] = (a < n && b < n) ? Q[a * ld + b] : 0.0;
   }
-  if (bad && tid == 0) {
-    const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
-    raise_status(p.status, SRM_ERR_RANK, (int)sj[SC_GLOBAL], iteration);
-  }
+  if (bad && tid == 0) raise_warning(p.status, SRM_WARN_POLAR_CONDITION);
 }
 
 // dst[r][c] = src[r][c0 + c] (r < rows, c < cols; zero where c0 + c >= cmax),
@@ -1067,7 +1065,7 @@ __global__ void k_reset(DevPlan p) {
     p.sinv[e] = (a == b && a < p.K) ? -1.0 : 0.0;  // the sweep of I
   }
   if (threadIdx.x == 0) {
-    p.status[0] = p.status[1] = p.status[2] = 0;
+    p.status[0] = p.status[1] = p.status[2] = p.status[3] = 0;
     *p.iter = 0;
     p.tailscr[TS_LOGDET_SIGMA] = 0.0;
   }
@@ -1179,7 +1177,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_polar_small(const double* g, 
   __syncthreads();
   JacobiScratch js{cs, sn, pp, qq, &rot};
   jacobi_eig(C, Q, n, ld, js, 40);
-  const bool bad = polar_from_eig(C, Q, n, ld, wsh, m, ldm, n);
+  const bool bad = polar_from_eig(C, Q, n, ld, wsh, m, ldm, n, 1e24);
   if (bad && threadIdx.x == 0) raise_status(status, SRM_ERR_RANK, 0, -1);
 }
 

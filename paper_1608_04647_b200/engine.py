@@ -40,7 +40,7 @@ class SrmEngine:
 
     def __init__(self, n_voxels, n_trs, k, iterations, *, storage="f64", world_size=1,
                  rank=0, counts=None, ordered=True, tolerance=False, gram=False, tc=False, gram_i8=False,
-                 device=None):
+                 exact_polar=False, device=None):
         torch = _torch()
         self.lib = _lib.load()
         if not torch.cuda.is_available():
@@ -70,6 +70,8 @@ class SrmEngine:
             flags |= _lib.FLAG_TC
         if gram_i8:
             flags |= _lib.FLAG_GRAM_I8
+        if exact_polar:
+            flags |= _lib.FLAG_EXACT_POLAR
         self.ordered = bool(ordered) or self.world_size == 1
         plan = ctypes.c_void_p()
         varr = (ctypes.c_int64 * self.n_local)(*self.n_voxels)
@@ -96,6 +98,7 @@ class SrmEngine:
         self.gram = bool(eff & _lib.FLAG_GRAM)
         self.tc = bool(eff & _lib.FLAG_TC)
         self.gram_i8 = bool(eff & _lib.FLAG_GRAM_I8)
+        self.exact_polar = bool(eff & _lib.FLAG_EXACT_POLAR)
         self._graph = None
         self._staging = {}
 
@@ -228,10 +231,14 @@ class SrmEngine:
             if hasattr(x, "result") and not isinstance(x, (torch.Tensor, np.ndarray)):
                 pending = x
                 x = x.result()  # a pending read (data_io.PendingMatrix): pinned tensor
-            if isinstance(x, torch.Tensor) and x.device == self.device and x.dim() == 2 \
-                    and x.dtype in (torch.float64, torch.float32) and x.stride(1) == 1:
+            if isinstance(x, torch.Tensor) and x.is_cuda:
+                # already on a GPU: converted there (dtype, device, unit column stride) if needed
+                if not (x.device == self.device and x.dim() == 2 and x.dtype in (torch.float64, torch.float32)
+                        and x.stride(1) == 1):
+                    dt = x.dtype if x.dtype in (torch.float64, torch.float32) else torch.float64
+                    x = x.detach().to(device=self.device, dtype=dt).contiguous()
                 src = x
-                ld = x.stride(0)
+                ld = x.stride(0) if x.dim() == 2 and x.shape[0] > 1 else self.T
             else:
                 if isinstance(x, torch.Tensor):
                     host = x.detach()
@@ -516,6 +523,11 @@ class SrmEngine:
         code, arg, it, _ = self.status()
         if code:
             raise from_status(code, arg=arg)
+
+    @property
+    def warnings(self):
+        """SRM_WARN_* bits raised so far (synchronises)."""
+        return self.status()[3]
 
     def local_rho2(self):
         col = self.kp * self.ldx + _lib.REC_RHO2

@@ -132,32 +132,58 @@ def to_device(arr, device, out=None):
 
 
 class PinnedRing:
-    """A few reusable pinned host slots (cached per device and slot size).
+    """A few reusable pinned host slots (pooled per device and slot count).
 
     Producers fill a slot on a worker thread after the slot's previous device
     copy has completed; the consumer issues an asynchronous copy from it and
-    records an event that guards the slot's next reuse.
+    records an event that guards the slot's next reuse.  A ring is checked
+    out by one fit at a time (:meth:`acquire` / :meth:`release`), so fits
+    running concurrently (e.g. one thread per rank) never share slots, and
+    :meth:`cancel` wakes producers of an abandoned fit so they return without
+    writing.
     """
 
-    _cache = {}
+    _pool = {}
 
     def __init__(self, slot_bytes, nslots):
         torch = _torch()
         self.slots = [torch.empty(slot_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(nslots)]
         self.events = [None] * nslots
         self.slot_bytes = slot_bytes
+        self.issued = []
+        self.cancelled = False
+        self.key = None
 
     @classmethod
-    def get(cls, device, slot_bytes, nslots=4, n_items=0):
+    def acquire(cls, device, slot_bytes, nslots=4, n_items=0):
         key = (str(device), nslots)
         with _lock:
-            ring = cls._cache.get(key)
-            if ring is None or ring.slot_bytes < slot_bytes:
-                ring = cls(slot_bytes, nslots)
-                cls._cache[key] = ring
+            free = cls._pool.setdefault(key, [])
+            ring = None
+            for i, r in enumerate(free):
+                if r.slot_bytes >= slot_bytes:
+                    ring = free.pop(i)
+                    break
+        if ring is None:
+            ring = cls(slot_bytes, nslots)
+        ring.key = key
         ring.events = [None] * nslots
         ring.issued = [threading.Event() for _ in range(n_items)]
+        ring.cancelled = False
         return ring
+
+    def release(self):
+        """Return the ring to the pool (after the fit's producers are done)."""
+        with _lock:
+            pool = PinnedRing._pool.setdefault(self.key, [])
+            if self not in pool:
+                pool.append(self)
+                del pool[:-2]  # keep at most two idle rings per key
+
+    def cancel(self):
+        self.cancelled = True
+        for ev in self.issued:
+            ev.set()
 
     def view(self, i, shape, dtype=np.float64):
         n = int(np.prod(shape)) * np.dtype(dtype).itemsize
@@ -167,13 +193,17 @@ class PinnedRing:
         return self.slots[i % len(self.slots)][:nbytes]
 
     def wait_free(self, i):
-        """Block until item i's slot is no longer read by item i - nslots's copy."""
+        """Block until item i's slot is no longer read by item i - nslots's
+        copy; False when the fit was cancelled."""
         prev = i - len(self.slots)
         if prev >= 0:
             self.issued[prev].wait()
+            if self.cancelled:
+                return False
             ev = self.events[prev % len(self.slots)]
             if ev is not None:
                 ev.synchronize()
+        return not self.cancelled
 
     def mark_used(self, i, event):
         self.events[i % len(self.slots)] = event

@@ -32,7 +32,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib, hostio
-from .collectives import SerialCommunicator, TorchCommunicator, rank_counts
+from .collectives import SerialCommunicator, TorchCommunicator, any_rank, rank_counts
 from .data import SubjectData
 from .engine import SrmEngine, reference_gaussian
 from .errors import ConfigError, DeviceError, ShapeError, from_status
@@ -405,7 +405,7 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f
 
 def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=True,
         keep_on_device=False, device=None, engine_out=None, timings=None, algorithm="auto",
-        tensor_cores=True, gram_int8=True, init_overlap=True):
+        tensor_cores=True, gram_int8=True, init_overlap=True, exact_polar=False):
     """Run the distributed EM; ``subjects`` are this worker's share (srm.py:216).
 
     Every worker calls this with the same config and its own communicator
@@ -434,8 +434,14 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     the draw) batch by batch while later subjects are still uploading;
     ``False`` runs it once after the upload (bit-identical results; ~5 ms
     more end to end on cfg 2).
+    ``exact_polar``: form every polar transform from A_i itself (Householder
+    TSQR + one-sided Jacobi SVD, the fp64 streaming path).  By default the
+    fast routes form it from A_i^T A_i, which cannot resolve
+    sigma_min / sigma_max much below 1e-3 at the fp64 tolerance; a subject
+    that ill-conditioned raises a device warning and the whole fit is redone
+    with ``exact_polar=True`` (on every rank), which matches the reference's
+    SVD (kernels.py:190-212) and raises ``RankError`` exactly where it does.
     """
-    clock = _PhaseClock(timings)
     config.validate()
     if not subjects:
         raise ConfigError("each worker needs at least one subject")
@@ -450,7 +456,21 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     for s in subjects:
         if int(s.X.shape[0]) < k:
             raise ShapeError(f"subject has {s.X.shape[0]} voxels, fewer than k={k} factors")
+    opts = dict(storage=storage, ordered=ordered, graphs=graphs, keep_on_device=keep_on_device, device=device,
+                engine_out=engine_out, timings=timings, algorithm=algorithm, tensor_cores=tensor_cores,
+                gram_int8=gram_int8, init_overlap=init_overlap)
+    model = _fit_pass(subjects, config, comm, exact=bool(exact_polar), **opts)
+    if model is None:  # a Gram-route polar transform was out of its range on some rank
+        model = _fit_pass(subjects, config, comm, exact=True, **opts)
+    return model
 
+
+def _fit_pass(subjects, config, comm, *, exact, storage, ordered, graphs, keep_on_device, device, engine_out,
+              timings, algorithm, tensor_cores, gram_int8, init_overlap):
+    """One fit; None when it must be redone on the exact polar route."""
+    clock = _PhaseClock(timings)
+    n_trs = int(subjects[0].X.shape[1])
+    k = config.k
     counts = rank_counts(comm, len(subjects))
     offset = int(sum(counts[: comm.rank]))
     n_subjects = int(sum(counts))
@@ -462,13 +482,16 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
 
     n_vox = [int(s.X.shape[0]) for s in subjects]
     store = _storage_for(subjects, storage)
-    use_i8 = bool(gram_int8)
+    use_i8 = bool(gram_int8) and not exact
+    free = None
     if use_i8 or algorithm == "auto":
         torch = _torch()
         free = _free_device_bytes(torch, device)
         x_bytes = sum(n_vox) * (-(-n_trs // 32) * 32) * (8 if store == "f64" else 4)
         use_i8 = use_i8 and gram_int8_bytes(n_vox, n_trs, store) + x_bytes < 0.6 * free
-    if algorithm == "auto":
+    if exact:
+        algorithm = "stream"
+    elif algorithm == "auto":
         algorithm = choose_algorithm(n_vox, n_trs, k, config.iterations, free,
                                      storage=store if tensor_cores else "f64", gram_int8=use_i8)
     if algorithm not in ("stream", "gram"):
@@ -476,26 +499,44 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     eng = SrmEngine(n_vox, n_trs, k, config.iterations,
                     storage=store, world_size=comm.size, rank=comm.rank,
                     counts=counts, ordered=ordered, tolerance=config.tolerance is not None,
-                    gram=algorithm == "gram", tc=bool(tensor_cores) and store == "f32",
-                    gram_i8=algorithm == "gram" and use_i8, device=device)
+                    gram=algorithm == "gram", tc=bool(tensor_cores) and store == "f32" and not exact,
+                    gram_i8=algorithm == "gram" and use_i8, exact_polar=exact, device=device)
     if engine_out is not None:
         engine_out.append(eng)
     # the init draws depend only on (seed, global index, V, k): overlap them with the upload
     pool = _draw_pool()
-    ring = hostio.PinnedRing.get(eng.device, max(n_vox) * k * 8, nslots=min(16, len(subjects)),
-                                 n_items=len(subjects))
+    ring = hostio.PinnedRing.acquire(eng.device, max(n_vox) * k * 8, nslots=min(16, len(subjects)),
+                                     n_items=len(subjects))
 
     def draw(j):  # the srm.py:111 PCG64 stream, written straight into a pinned slot
-        ring.wait_free(j)
+        if not ring.wait_free(j):
+            return None  # the fit was abandoned
         gen = np.random.default_rng((config.seed & 0xFFFFFFFFFFFFFFFF, offset + j))
         gen.standard_normal(out=ring.view(j, (n_vox[j], k)))
         return (ring, j)
 
     draws = [pool.submit(draw, j) for j in range(len(subjects))]
+    futures = list(draws)  # eng.load consumes `draws`
     clock.tick("setup")
     # pipelined: upload + demean (+ X^T X) (+ the initial mapping) per batch of subjects
     use_graph = graphs and comm.size == 1
-    eng.load([s.X for s in subjects], gaussians=draws, gram=True, init=init_overlap, capture=use_graph)
+    try:
+        eng.load([s.X for s in subjects], gaussians=draws, gram=True, init=init_overlap, capture=use_graph)
+    except BaseException:
+        # wake and drain the draw workers before the ring is reused by another fit
+        ring.cancel()
+        for f in futures:
+            f.cancel()
+        for f in futures:
+            if not f.cancelled():
+                try:
+                    f.result()
+                except Exception:  # noqa: BLE001
+                    pass
+        ring.release()
+        eng.close()
+        raise
+    ring.release()
     clock.tick("load")
     if init_overlap:
         eng.set_iteration(0)
@@ -513,7 +554,12 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
             eng.step(comm)
         n_done = it + 1
         if config.tolerance is not None:
-            eng.raise_status()
+            code, arg, _, warn = eng.status()
+            if not exact and any_rank(comm, warn != 0):
+                eng.close()
+                return None
+            if code:
+                raise from_status(code, arg=arg)
             row = eng.hist[it]
             if it >= 1:
                 sdiff = float(row[_lib.H_SDIFF].item())
@@ -527,7 +573,12 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     else:
         # W_i of earlier subjects read back while later ones are formed
         wout = eng.finalize_to_host()
-    eng.raise_status()
+    code, arg, _, warn = eng.status()  # warnings are sticky: this covers init, every M-step and the final W
+    if not exact and any_rank(comm, warn != 0):
+        eng.close()
+        return None
+    if code:
+        raise from_status(code, arg=arg)
     clock.tick("finalize")
     model = _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device, wout)
     clock.tick("collect")

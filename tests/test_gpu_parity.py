@@ -535,3 +535,114 @@ def test_stream_k_sg_bit_identical_to_per_tile(srm, monkeypatch, k):
     ref = orc.run_em(xs, k, 3, seed=2)
     r = ref["iters"][-1]
     _check_model(a, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, f"stream-K k={k}")
+
+
+# --------------------------------------------------------------------------
+# polar conditioning: the Gram-route transform (A^T A)^{-1/2} vs the exact
+# route (TSQR + SVD of A, SRM_FLAG_EXACT_POLAR) the fit falls back to
+# --------------------------------------------------------------------------
+
+def _lowrank_subjects(noise, seed=0, V=300, T=60, K=5, N=3):
+    """X_i = W_i S + noise, with the last of K shared components absent: A_i =
+    Xhat_i S^T / 2 has cond ~ (1 / noise)^2 (2e5 at noise 1e-3, 2e9 at 1e-5;
+    the reference raises RankError at 1e-7)."""
+    rng = np.random.default_rng(seed)
+    s = rng.standard_normal((K, T))
+    s[-1] = 0.0
+    xs = []
+    for _ in range(N):
+        w = np.linalg.qr(rng.standard_normal((V, K)))[0]
+        xs.append(w @ s + noise * rng.standard_normal((V, T)))
+    return xs
+
+
+@pytest.mark.parametrize("name", ["em_small", "em_ragged", "em_recipe_f32"])
+def test_exact_polar_route_every_iteration(srm, name):
+    """exact_polar=True (TSQR + one-sided Jacobi SVD of every A_i) against the
+    reference's golden fit at every iteration."""
+    g = load_golden(name)
+    xs = golden_subjects(g)
+    k, iters, seed = int(g["k"]), int(g["iterations"]), int(g["seed"])
+    tol = TOL64 if xs[0].dtype == np.float64 else TOL32
+    for n in range(1, iters + 1):
+        eng = []
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=k, iterations=n, seed=seed), exact_polar=True,
+                    engine_out=eng)
+        assert eng[-1].exact_polar and not eng[-1].gram
+        it = n - 1
+        _check_model(m, g[f"it{it}_S"], g[f"it{it}_sigma_s"], g[f"it{it}_rho2"],
+                     [g[f"it{it}_W{i}"] for i in range(len(xs))], tol, f"{name} exact it{it}")
+        for w in m.W:
+            assert np.max(np.abs(w.T @ w - np.eye(k))) <= 1e-8
+
+
+@pytest.mark.parametrize("algorithm", ["gram", "stream"])
+def test_ill_conditioned_fit_falls_back_to_exact_polar(srm, algorithm):
+    """cond(A_i) ~ 2e3: beyond the Gram route (c / lambda_min > 1e5 raises the
+    device warning), inside the reference's rank threshold -- the fit is redone
+    on the exact route and matches the oracle at every iteration, every array
+    at the fp64 tolerance."""
+    xs = _lowrank_subjects(1e-2)
+    ref = orc.run_em(xs, 5, 6, seed=0)
+    for n in range(1, 7):
+        eng = []
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=5, iterations=n, seed=0), algorithm=algorithm,
+                    engine_out=eng)
+        assert len(eng) == 2 and not eng[0].exact_polar and eng[1].exact_polar, (algorithm, n)
+        r = ref["iters"][n - 1]
+        _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, f"lowrank {algorithm} it{n - 1}")
+        for w in m.W:
+            assert np.max(np.abs(w.T @ w - np.eye(5))) <= 1e-12
+
+
+@pytest.mark.parametrize("algorithm", ["gram", "stream"])
+def test_very_ill_conditioned_fit_at_its_conditioning(srm, algorithm):
+    """cond(A_i) ~ 2e5 and rho^2 ~ 1e-6 (a 1e-4 cancellation in srm.py:153-154):
+    S at the fp64 tolerance; W_i, rho^2 and Sigma_s within what their own
+    conditioning allows any two roundings to differ (cond(A_i) x 1e-13 for
+    W_i -- the perturbation bound of the polar factor -- 1e-6 for rho^2, and
+    Sigma_s through rho0 = sum 1 / rho_i^2)."""
+    xs = _lowrank_subjects(1e-3)
+    ref = orc.run_em(xs, 5, 6, seed=0)
+    xh = [orc.center_rows(x)[0] for x in xs]
+    for n in range(1, 7):
+        eng = []
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=5, iterations=n, seed=0), algorithm=algorithm,
+                    engine_out=eng)
+        assert len(eng) == 2 and not eng[0].exact_polar and eng[1].exact_polar, (algorithm, n)
+        r = ref["iters"][n - 1]
+        what = f"lowrank {algorithm} it{n - 1}"
+        assert nrel(m.S, r["S"]) <= TOL64, (what, nrel(m.S, r["S"]))
+        assert nrel(m.sigma_s, r["sigma_s"]) <= 1e-7, what
+        assert nrel(m.rho2, r["rho2"]) <= 1e-6, what
+        # the polar factor's own condition number is cond(A_i): S agrees to
+        # ~1e-14, so any two implementations differ in W_i by ~cond(A_i) 1e-14
+        for i, w in enumerate(r["W"]):
+            cond = np.linalg.cond(0.5 * (xh[i] @ r["S"].T))
+            assert nrel(m.W[i], w) <= max(TOL64, 1e-13 * cond), (what, i, nrel(m.W[i], w), cond)
+        for w in m.W:
+            assert np.max(np.abs(w.T @ w - np.eye(5))) <= 1e-10
+
+
+def test_nearly_singular_fit_no_spurious_rank_error(srm):
+    """cond(A_i) ~ 2e9 (sigma ratio 5e-10, above the reference's 1e-12): the
+    reference fits it, so must we; S agrees to ~eps cond."""
+    xs = _lowrank_subjects(1e-5)
+    ref = orc.run_em(xs, 5, 4, seed=0)
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=5, iterations=4, seed=0))
+    assert nrel(m.S, ref["S"]) <= 1e-5
+    # rho^2 ~ 3e-9 is a 1e-9-relative cancellation of |Xhat|^2 + T tr(Sigma) - 2 cross
+    # (srm.py:153-154): any change of rounding moves it by ~10%, the reference's own value included
+    assert nrel(m.rho2, ref["rho2"]) <= 0.3
+
+
+@pytest.mark.parametrize("algorithm", ["gram", "stream"])
+def test_rank_deficient_fit_raises_like_reference(srm, algorithm):
+    """noise 1e-7: the reference's gesdd polar raises RankError in the M-step."""
+    from paper_1608_04647_b200.errors import RankError
+
+    xs = _lowrank_subjects(1e-7)
+    with pytest.raises(orc.OracleError, match="RankError"):
+        orc.run_em(xs, 5, 6, seed=0)
+    with pytest.raises(RankError):
+        srm.fit(_subjects(srm, xs), srm.SrmConfig(k=5, iterations=6, seed=0), algorithm=algorithm)
