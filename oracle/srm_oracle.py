@@ -296,6 +296,86 @@ def run_em(xs, k, iterations, seed=0, tolerance=None, record=True,
     }
 
 
+def _update_keep_product(xhat, s, trace_new, sqnorm):
+    """``subject_update`` keeping W_new^T Xhat (srm.py:151), which is also the
+    next iteration's ``e_step_local`` product (srm.py:118): the same matmul of
+    the same operands, so reusing it is bit-identical; ``sqnorm`` is the
+    loop-invariant ``trace_ata(Xhat)`` (srm.py:152)."""
+    a = 0.5 * (xhat @ s.T)
+    w = orthogonal_polar(a)
+    wtx = w.T @ xhat
+    cross = float(np.einsum("kt,kt->", wtx, s))
+    n_trs, n_vox = s.shape[1], xhat.shape[0]
+    rho2 = (sqnorm + n_trs * trace_new - 2.0 * cross) / (n_trs * n_vox)
+    return w, max(rho2, RHO_FLOOR), wtx
+
+
+def em_iterations(xs, k, iterations, seed=0, workers=1, keep_xhat=True):
+    """``run_em`` for BASELINE-sized configs: yields one record per EM
+    iteration (S, Sigma_s, trace, rho0, rho2, W list, Woodbury LL) instead of
+    keeping them all.
+
+    Same steps and arithmetic as ``run_em`` (bit-identical records; tested),
+    restructured for memory and time only:
+
+    * the loop-invariant ``trace_ata(Xhat_i)`` is computed once, and the
+      M-step's W_new^T Xhat product is reused as the next E-step term (the
+      reference computes both twice, with identical results);
+    * ``workers`` > 1 runs the per-subject steps in threads with one BLAS
+      thread each (the ordered reduction stays in ascending subject order);
+    * ``keep_xhat=False`` keeps only the caller's arrays and re-forms
+      Xhat_i = demean(X_i) (srm.py:94-98, deterministic) each time it is
+      read, so a config whose fp64 Xhat exceeds host RAM still fits.
+    """
+    from concurrent.futures import ThreadPoolExecutor
+
+    n = len(xs)
+    n_trs = xs[0].shape[1]
+
+    def xhat(j):
+        return cached[j] if keep_xhat else center_rows(xs[j])[0]
+
+    limits = None
+    if workers > 1:
+        from threadpoolctl import threadpool_limits
+
+        limits = threadpool_limits(limits=1)
+    try:
+        pool = ThreadPoolExecutor(max(1, workers))
+        cached = list(pool.map(lambda x: center_rows(x)[0], xs)) if keep_xhat else None
+        n_vox = [x.shape[0] for x in xs]
+
+        def start(j):
+            xh = xhat(j)
+            w = initial_mapping(xh.shape[0], k, seed, j)[0]
+            return w, w.T @ xh, sum_of_squares(xh)
+
+        first = list(pool.map(start, range(n)))
+        ws = [f[0] for f in first]
+        wtx = [f[1] for f in first]
+        sqnorms = [f[2] for f in first]
+        del first
+        rho2s = [1.0] * n
+        sigma_s = np.eye(k)
+        for it in range(iterations):
+            terms = [wtx[j] / rho2s[j] for j in range(n)]  # local_term, srm.py:118
+            reduced, rho0 = ordered_reduce(terms, rho2s)
+            del terms
+            ll = woodbury_loglik(reduced, rho0, sigma_s, rho2s, n_vox, sqnorms, n_trs)
+            s, _ = shared_posterior(reduced, sigma_s, rho0)
+            sigma_s, trace_new = shared_covariance(sigma_s, rho0, s)
+            out = list(pool.map(lambda j: _update_keep_product(xhat(j), s, trace_new, sqnorms[j]), range(n)))
+            ws = [o[0] for o in out]
+            rho2s = [o[1] for o in out]
+            wtx = [o[2] for o in out]
+            del out
+            yield {"it": it, "S": s, "sigma_s": sigma_s.copy(), "trace": trace_new, "rho0": rho0,
+                   "rho2": np.array(rho2s), "W": ws, "ll": ll}
+    finally:
+        if limits is not None:
+            limits.restore_original_limits()
+
+
 def final_loglik(ws, rho2s, sigma_s, xhats):
     """Woodbury log-likelihood of a fitted model (post-M-step parameters)."""
     terms = [local_term(w, r, xh) for w, r, xh in zip(ws, rho2s, xhats)]

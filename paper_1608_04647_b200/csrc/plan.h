@@ -125,8 +125,9 @@ int max_supported_k();
 bool ns_polar_supported(int kp);
 cudaError_t launch_ns_polar(const DevPlan& p, int init, cudaStream_t s);
 bool ns_polar_f32_supported(int kp);
-// final fp64 polar from the fp32 Newton-Schulz M (80 < kp <= 112); scal[i][1] = 1 where it converged
-cudaError_t launch_ns_refine(const DevPlan& p, cudaStream_t s);
+// fp64 polar from the fp32 Newton-Schulz M (80 < kp <= 112); scal[i][1] = 1 where it converged,
+// with `warn` a subject it leaves raises SRM_WARN_POLAR_CONDITION
+cudaError_t launch_ns_refine(const DevPlan& p, cudaStream_t s, int warn = 0);
 cudaError_t launch_final_polar(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_ns_polar_f32(const DevPlan& p, int init, cudaStream_t s);
 cudaError_t launch_eig_polar_exact(const DevPlan& p, int init, cudaStream_t s);

@@ -441,7 +441,7 @@ __device__ __forceinline__ void ref_mm(const double* A, int64_t lda, bool sym_a,
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kRefThreads, 1) k_ns_refine(DevPlan p) {
+__global__ void __launch_bounds__(kRefThreads, 1) k_ns_refine(DevPlan p, int warn) {
   extern __shared__ __align__(16) double rsm[];
   __shared__ double red[kRefThreads / 32];
   const int i = p.sub0 + blockIdx.x;
@@ -481,12 +481,15 @@ __global__ void __launch_bounds__(kRefThreads, 1) k_ns_refine(DevPlan p) {
       break;
     }
   }
-  if (threadIdx.x == 0) p.scal[(int64_t)i * 8 + 1] = ok ? 1.0 : 0.0;
+  if (threadIdx.x == 0) {
+    p.scal[(int64_t)i * 8 + 1] = ok ? 1.0 : 0.0;
+    if (warn && !ok) raise_warning(p.status, SRM_WARN_POLAR_CONDITION);
+  }
 }
 
 }  // namespace
 
-cudaError_t launch_ns_refine(const DevPlan& p, cudaStream_t s) {
+cudaError_t launch_ns_refine(const DevPlan& p, cudaStream_t s, int warn) {
   const int n = (int)p.K;
   const size_t bytes = (size_t)2 * n * (n + 1) * sizeof(double);
   if (bytes > 227 * 1024) return cudaErrorInvalidValue;
@@ -496,7 +499,7 @@ cudaError_t launch_ns_refine(const DevPlan& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured = bytes;
   }
-  k_ns_refine<<<p.nsub, kRefThreads, bytes, s>>>(p);
+  k_ns_refine<<<p.nsub, kRefThreads, bytes, s>>>(p, warn);
   return cudaGetLastError();
 }
 

@@ -334,10 +334,14 @@ __global__ void __launch_bounds__(kSmallThreads) k_eig_polar(DevPlan p, int init
   const int sweeps = jacobi_eig(C, Q, n, ld, js, 40);
   if (tid == 0) p.scal[(int64_t)i * 8 + 0] = (double)sweeps;
   const bool bad = polar_from_eig(C, Q, n, ld, wsh, p.mmat + (int64_t)i * kp * kp, kp, kp, kGramCondLimit);
-  for (int e = tid; e < kp * kp; e += blockDim.x) {
-    const int a = e / kp, b = e - a * kp;
-    Qg[e] = (a < n && b < n) ? Q[a * ld + b] : 0.0;
-  }
+  // the eigenbasis warm-starts the next iteration's sweep; the transforms of
+  // init (1) and of a formed W (2) are not iterations, so they leave it alone
+  // (iteration 0 starts cold anyway) and forming W mid-fit changes nothing
+  if (!init)
+    for (int e = tid; e < kp * kp; e += blockDim.x) {
+      const int a = e / kp, b = e - a * kp;
+      Qg[e] = (a < n && b < n) ? Q[a * ld + b] : 0.0;
+    }
   if (bad && tid == 0) raise_warning(p.status, SRM_WARN_POLAR_CONDITION);
 }
 
@@ -1271,9 +1275,16 @@ cudaError_t launch_reduce_chunks(const DevPlan& p, cudaStream_t s) {
 
 cudaError_t launch_eig_polar(const DevPlan& p, int init, cudaStream_t s) {
   if (ns_polar_supported((int)p.kp)) return launch_ns_polar(p, init, s);
-  // fp32 X-hat (1e-4 tolerance): fp32 Newton-Schulz where fp64 does not fit;
-  // srm_finalize recomputes the last transform exactly
-  if (p.xf32 && ns_polar_f32_supported((int)p.kp)) return launch_ns_polar_f32(p, init, s);
+  // fp32 X-hat, 80 < kp <= 112, where the fp64 iteration does not fit in shared
+  // memory: the fp32 Newton-Schulz (~1e-6 relative), refined to fp64 accuracy
+  // by the symmetric Newton iteration for C^{-1/2} (two steps; a subject it
+  // does not converge for hands the fit to the exact route) -- an fp32 M would
+  // carry ~4e-7 into S every iteration and ~1e-6 into W (tools/fp32_accuracy.py)
+  if (p.xf32 && ns_polar_f32_supported((int)p.kp)) {
+    cudaError_t e = launch_ns_polar_f32(p, init, s);
+    if (e == cudaSuccess) e = launch_ns_refine(p, s, 1);
+    return e;
+  }
   return launch_eig_polar_exact(p, init, s);
 }
 

@@ -51,6 +51,7 @@ __all__ = [
     "project",
     "map_between",
     "project_batch",
+    "IterationState",
 ]
 
 RHO_FLOOR = 1e-12
@@ -341,10 +342,13 @@ def _storage_for(subjects, storage):
 
 
 # B200 rates used by the cost model (measured on this pool: DMMA 37.1 TF/s peak, ~30 sustained
-# in the contraction kernels; HBM copy 6.55 TB/s; 3xTF32 tcgen05 ~0.9 PF/s of tf32 MMA)
+# in the contraction kernels; HBM copy 6.55 TB/s; 3xTF32 tcgen05 ~0.9 PF/s of tf32 MMA; the
+# tcgen05 fp32 streaming passes sustain ~3.0 TB/s of X-hat per iteration, reductions included:
+# cfg 3 17.4 ms per iteration for 2 x 25.8 GB)
 _DMMA_FLOPS = 30e12
 _HBM_BYTES = 6.0e12
 _TF32_FLOPS = 0.9e15
+_TC_STREAM_BYTES = 3.0e12
 _I8_OPS = 3.2e15       # int8 tcgen05 (dense 4.5e15 nominal), as sustained by the sliced Gram
 _I8_PRODUCTS = {"f64": 28, "f32": 16}  # slice pairs of the int8-sliced Gram: 7 or 4 slices per value
 
@@ -379,7 +383,7 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f
     for v in n_voxels:
         if tc:
             np16 = -(-k // 16) * 16
-            per_pass = max(v * ldx * b / _HBM_BYTES, 3 * 2.0 * v * ldx * max(np16, 128) / _TF32_FLOPS)
+            per_pass = max(v * ldx * b / _TC_STREAM_BYTES, 3 * 2.0 * v * ldx * max(np16, 128) / _TF32_FLOPS)
             stream += iterations * 2 * per_pass
             final_a = per_pass
         else:
@@ -405,7 +409,7 @@ def choose_algorithm(n_voxels, n_trs, k, iterations, free_bytes=None, storage="f
 
 def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=True,
         keep_on_device=False, device=None, engine_out=None, timings=None, algorithm="auto",
-        tensor_cores=True, gram_int8=True, init_overlap=True, exact_polar=False):
+        tensor_cores=True, gram_int8=True, init_overlap=True, exact_polar=False, on_iteration=None):
     """Run the distributed EM; ``subjects`` are this worker's share (srm.py:216).
 
     Every worker calls this with the same config and its own communicator
@@ -441,6 +445,13 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     that ill-conditioned raises a device warning and the whole fit is redone
     with ``exact_polar=True`` (on every rank), which matches the reference's
     SVD (kernels.py:190-212) and raises ``RankError`` exactly where it does.
+    ``on_iteration``: called after every EM iteration with an
+    :class:`IterationState` (S, Sigma_s, this worker's rho_i^2 and W_i as they
+    stand after that iteration's M-step, and its log-likelihood) -- the
+    per-iteration trace of the reference's loop (srm.py:254-287), for
+    checking a long fit against an oracle without refitting.  Forming W_i
+    reads the EM state only, so the fit is bit-identical with or without it
+    (tested); it synchronises once per iteration.
     """
     config.validate()
     if not subjects:
@@ -458,15 +469,40 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
             raise ShapeError(f"subject has {s.X.shape[0]} voxels, fewer than k={k} factors")
     opts = dict(storage=storage, ordered=ordered, graphs=graphs, keep_on_device=keep_on_device, device=device,
                 engine_out=engine_out, timings=timings, algorithm=algorithm, tensor_cores=tensor_cores,
-                gram_int8=gram_int8, init_overlap=init_overlap)
+                gram_int8=gram_int8, init_overlap=init_overlap, on_iteration=on_iteration)
     model = _fit_pass(subjects, config, comm, exact=bool(exact_polar), **opts)
     if model is None:  # a Gram-route polar transform was out of its range on some rank
         model = _fit_pass(subjects, config, comm, exact=True, **opts)
     return model
 
 
+@dataclass
+class IterationState:
+    """One EM iteration of a fit as seen by this worker (``fit(on_iteration=)``)."""
+
+    iteration: int
+    S: np.ndarray
+    sigma_s: np.ndarray
+    rho2: list
+    W: list
+    log_likelihood: float
+
+
+def _snapshot(eng, it):
+    eng.finalize()  # W_i = A_i M_i of this M-step; writes only W (and finalize scratch)
+    code, arg, _, _ = eng.status()
+    if code:
+        raise from_status(code, arg=arg)
+    w = hostio.to_host(eng.wout)
+    return IterationState(
+        iteration=it, S=eng.S.cpu().numpy(), sigma_s=eng.sigma.cpu().numpy(),
+        rho2=[float(r) for r in eng.local_rho2().cpu().numpy()],
+        W=[w[eng.subject_rows(j)] for j in range(eng.n_local)],
+        log_likelihood=float(eng.hist[it % eng.iterations][_lib.H_LL].item()))
+
+
 def _fit_pass(subjects, config, comm, *, exact, storage, ordered, graphs, keep_on_device, device, engine_out,
-              timings, algorithm, tensor_cores, gram_int8, init_overlap):
+              timings, algorithm, tensor_cores, gram_int8, init_overlap, on_iteration):
     """One fit; None when it must be redone on the exact polar route."""
     clock = _PhaseClock(timings)
     n_trs = int(subjects[0].X.shape[1])
@@ -553,6 +589,8 @@ def _fit_pass(subjects, config, comm, *, exact, storage, ordered, graphs, keep_o
         else:
             eng.step(comm)
         n_done = it + 1
+        if on_iteration is not None:
+            on_iteration(_snapshot(eng, it))
         if config.tolerance is not None:
             code, arg, _, warn = eng.status()
             if not exact and any_rank(comm, warn != 0):

@@ -1,0 +1,201 @@
+"""The five BASELINE.json configs at parity with the CPU oracle at every EM
+iteration of their fixed iteration counts (north_star: "S, W_i, rho_i^2,
+log-likelihood ... within 1e-9 relative for fp64 and 1e-4 relative for fp32,
+per EM iteration over a fixed iteration count").
+
+Each test runs ONE device fit of the config's iteration count through the
+default path (what ``bench.py`` times) with ``on_iteration`` snapshots, and
+advances the oracle (``oracle.srm_oracle.em_iterations``, bit-identical to
+the reference's ``srm.fit`` on the golden vectors) one iteration inside each
+snapshot, so the comparison is iteration by iteration: S, Sigma_s, every
+rho_i^2, every W_i (normwise relative) and the log-likelihood, plus W_i
+orthonormality (acceptance criterion 4).
+
+Sizes: cfg 1 and cfg 2 in full; cfg 3 (16 subjects), cfg 4 (256) and cfg 5
+(128 -- its 1-GPU configuration) in full, with the same device-generated
+bytes (``recipe_torch``) on both sides.  ``SRM_PARITY_REPORT=<dir>`` writes
+the per-iteration error table of each config there as JSON.
+"""
+
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+from conftest import nrel
+from oracle import srm_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-9
+TOL32 = 1e-4
+
+
+@pytest.fixture(scope="module")
+def srm():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a CUDA device")
+    from paper_1608_04647_b200 import srm as mod
+
+    return mod
+
+
+def _host_subjects(cfg, seed=0):
+    """BASELINE recipe subjects generated on the device (Philox, bench.py's
+    stream), copied to host memory one at a time."""
+    import torch
+
+    from paper_1608_04647_b200.data import recipe_torch
+
+    xs = []
+    for i in range(cfg["n_subjects"]):
+        x, _, _ = recipe_torch(cfg["n_subjects"], cfg["n_voxels"], cfg["n_trs"], cfg["k"], seed=seed,
+                               smooth=cfg["smooth"], dtype=cfg["dtype"], first_subject=i, count=1)
+        xs.append(x[0].cpu().numpy())
+        del x
+    torch.cuda.empty_cache()
+    return xs
+
+
+def _run(srm, name, xs, tol, *, keep_xhat=True, check_w_every=1, **fit_kw):
+    from paper_1608_04647_b200.data import config_by_name
+
+    cfg = config_by_name(name)
+    k, iters = cfg["k"], cfg["iterations"]
+    t0 = time.perf_counter()
+    gen = orc.em_iterations(xs, k, iters, seed=0, workers=os.cpu_count() or 1, keep_xhat=keep_xhat)
+    rows = []
+
+    def check(state):
+        r = next(gen)
+        assert r["it"] == state.iteration
+        row = {
+            "it": state.iteration,
+            "S": nrel(state.S, r["S"]),
+            "sigma_s": nrel(state.sigma_s, r["sigma_s"]),
+            "rho2": nrel(state.rho2, r["rho2"]),
+            "ll": abs(state.log_likelihood - r["ll"]) / abs(r["ll"]),
+        }
+        werr, orth = 0.0, 0.0
+        for j in range(0, len(r["W"]), check_w_every):
+            werr = max(werr, nrel(state.W[j], r["W"][j]))
+            w = state.W[j]
+            orth = max(orth, float(np.max(np.abs(w.T @ w - np.eye(k)))))
+        row["W_max"] = werr
+        row["orth_max"] = orth
+        rows.append(row)
+
+    eng = []
+    model = srm.fit([srm.SubjectData(f"s{j}", x) for j, x in enumerate(xs)],
+                    srm.SrmConfig(k=k, iterations=iters, seed=0), on_iteration=check, engine_out=eng, **fit_kw)
+    out = os.environ.get("SRM_PARITY_REPORT")
+    if out:
+        os.makedirs(out, exist_ok=True)
+        e = eng[-1]
+        path = {"gram": e.gram, "gram_i8": e.gram_i8, "tc": e.tc, "exact_polar": e.exact_polar,
+                "storage": e.storage}
+        tag = fit_kw.get("algorithm", "auto")
+        with open(os.path.join(out, f"parity_{name}_{tag}.json"), "w") as f:
+            json.dump({"config": name, "subjects": len(xs), "iterations": iters, "tolerance": tol,
+                       "path": path, "seconds": time.perf_counter() - t0, "per_iteration": rows}, f, indent=1)
+    assert len(rows) == iters, (name, len(rows))
+    with pytest.raises(StopIteration):
+        next(gen)
+    for row in rows:
+        bad = {key: v for key, v in row.items() if key not in ("it", "orth_max") and not v <= tol}
+        assert not bad, (name, row["it"], bad)
+        assert row["orth_max"] <= 1e-8, (name, row["it"], row["orth_max"])
+    return model, eng[-1], rows
+
+
+@pytest.mark.parametrize("algorithm", ["auto", "gram", "stream"])
+def test_cfg1_every_iteration(srm, algorithm):
+    """cfg 1: 10 x 5,000 x 500, K = 50, fp64, 10 iterations (host numpy input)."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(10, 5000, 500, 50, seed=1)
+    _run(srm, "cfg1", xs, TOL64, algorithm=algorithm)
+
+
+def test_cfg2_every_iteration(srm):
+    """cfg 2: 40 x 30,000 x 1,000, K = 50, fp64, 20 iterations through the
+    benched path (int8-sliced X^T X, int8 B = S G / 2, int8 final W)."""
+    from paper_1608_04647_b200.data import config_by_name
+
+    xs = _host_subjects(config_by_name("cfg2"))
+    _, eng, _ = _run(srm, "cfg2", xs, TOL64)
+    assert eng.gram and eng.gram_i8
+
+
+def test_cfg3_every_iteration(srm):
+    """cfg 3: 16 x 200,000 x 2,000, K = 100, fp32 (25.6 GB), 10 iterations."""
+    from paper_1608_04647_b200.data import config_by_name
+
+    xs = _host_subjects(config_by_name("cfg3"))
+    _run(srm, "cfg3", xs, TOL32)
+
+
+def test_cfg4_every_iteration(srm):
+    """cfg 4: 256 x 50,000 x 1,000, K = 64, fp32, Gaussian-smoothed W_i, 10
+    iterations (the oracle re-forms fp64 Xhat per read: 102 GB otherwise)."""
+    from paper_1608_04647_b200.data import config_by_name
+
+    xs = _host_subjects(config_by_name("cfg4"))
+    _run(srm, "cfg4", xs, TOL32, keep_xhat=False, check_w_every=4)
+
+
+def test_cfg5_every_iteration(srm):
+    """cfg 5 at one GPU: 128 x 100,000 x 1,000, K = 100, fp32, 5 iterations."""
+    from paper_1608_04647_b200.data import config_by_name
+
+    xs = _host_subjects(config_by_name("cfg5"))
+    _run(srm, "cfg5", xs, TOL32, keep_xhat=False, check_w_every=2)
+
+
+# --------------------------------------------------------------------------
+# the snapshots do not perturb the fit
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["gram_i8_f64", "gram_i8_f32_k100", "gram_f64", "stream_f64", "tc_f32",
+                                  "jacobi_f64_k96"])
+def test_on_iteration_snapshots_bit_identical(srm, case):
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    kw = {}
+    if case == "gram_i8_f64":
+        xs, k = recipe_numpy(4, 900, 200, 12, seed=3)[0], 12
+        kw = dict(algorithm="gram")
+    elif case == "gram_i8_f32_k100":
+        xs, k = recipe_numpy(3, 1500, 260, 100, seed=4, dtype="f32")[0], 100
+        kw = dict(algorithm="gram")
+    elif case == "gram_f64":
+        xs, k = recipe_numpy(4, 900, 200, 12, seed=3)[0], 12
+        kw = dict(algorithm="gram", gram_int8=False)
+    elif case == "stream_f64":
+        xs, k = recipe_numpy(4, 900, 200, 12, seed=3)[0], 12
+        kw = dict(algorithm="stream")
+    elif case == "tc_f32":
+        xs, k = recipe_numpy(3, 1200, 256, 40, seed=5, dtype="f32")[0], 40
+        kw = dict(algorithm="stream", tensor_cores=True)
+    else:  # fp64, kp = 96 > 80: the Jacobi polar with its warm-started eigenbasis
+        xs, k = recipe_numpy(3, 1500, 300, 96, seed=6)[0], 96
+        kw = dict(algorithm="stream")
+    subj = [srm.SubjectData(f"s{j}", x) for j, x in enumerate(xs)]
+    cfg = srm.SrmConfig(k=k, iterations=4, seed=2)
+    states = []
+    a = srm.fit(subj, cfg, on_iteration=states.append, **kw)
+    b = srm.fit(subj, cfg, **kw)
+    assert len(states) == 4
+    assert np.array_equal(a.S, b.S) and np.array_equal(a.sigma_s, b.sigma_s) and a.rho2 == b.rho2
+    for wa, wb, ws in zip(a.W, b.W, states[-1].W):
+        assert np.array_equal(wa, wb) and np.array_equal(ws, wb)
+    assert np.array_equal(states[-1].S, b.S) and states[-1].rho2 == b.rho2
+    # and each snapshot equals the fit of that many iterations
+    c = srm.fit(subj, srm.SrmConfig(k=k, iterations=2, seed=2), **kw)
+    assert np.array_equal(states[1].S, c.S) and states[1].rho2 == c.rho2
+    for ws, wc in zip(states[1].W, c.W):
+        assert np.array_equal(ws, wc)

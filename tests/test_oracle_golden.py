@@ -145,3 +145,20 @@ def test_flop_model():
 
 def test_nrel_helper():
     assert nrel([1.0, 2.0], [1.0, 2.0]) == 0.0
+
+
+@pytest.mark.parametrize("workers,keep", [(1, True), (3, False)])
+def test_em_iterations_bit_identical_to_run_em(workers, keep):
+    """The streaming oracle driver used at BASELINE sizes (cached trace_ata and
+    W^T Xhat, threads, re-formed Xhat) == run_em, bit for bit, every iteration."""
+    g = load_golden("em_ragged")
+    xs = golden_subjects(g)
+    k, iters, seed = int(g["k"]), int(g["iterations"]), int(g["seed"])
+    ref = orc.run_em(xs, k, iters, seed=seed)
+    recs = list(orc.em_iterations(xs, k, iters, seed=seed, workers=workers, keep_xhat=keep))
+    assert len(recs) == iters
+    for a, b in zip(recs, ref["iters"]):
+        assert np.array_equal(a["S"], b["S"]) and np.array_equal(a["sigma_s"], b["sigma_s"])
+        assert np.array_equal(a["rho2"], b["rho2"]) and a["ll"] == b["ll"] and a["rho0"] == b["rho0"]
+        for wa, wb in zip(a["W"], b["W"]):
+            assert np.array_equal(wa, wb)
