@@ -4,17 +4,21 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
     python bench.py --impl reference ...      # the reference CPU arithmetic
 
-A *step* is one EM iteration over every subject of the workload (srm.py:254-287:
-E-step reduction, K x K tail, M-step over all subjects).  ``value`` is the
-whole-job subject*voxel*TR/s per iteration with X already resident in HBM,
-timed with CUDA events over a K-step fit (max over ranks): the one-time Gram
-precompute (when that path is chosen) and the final W are inside the timed
-region, demean and the reference initialisation are not; ``e2e`` is the
-same metric through the public API ``srm.fit`` on pinned host arrays, host to
-device copies, the reference initialisation and the read-back of the model
+A *step* is one complete fit of the config's fixed EM iteration count
+(BASELINE.json: 10 / 20 / 10 / 10 / 5 for cfg 1-5; srm.py:254-287) with
+X-hat already resident in HBM: the device part of the initialisation (the
+srm.py:101-118 polar of the PCG64 draw and the first E-step term), the
+one-time Gram precompute when that path is chosen, the EM iterations and
+the final W_i (srm.py:315-327).  Demean and the host PCG64 draw are not in
+it (the reference's own per-iteration accounting also excludes them).
+``value`` is the whole-job subject*voxel*TR/s per EM iteration:
+n_subjects * V * T * iterations / (step seconds), timed with CUDA events
+over exactly K steps (max over ranks).  ``e2e`` is the same metric through
+the public API ``srm.fit`` on pinned host arrays: host-to-device copies,
+demean, the reference initialisation and the read-back of the model
 included.  The default workload is BASELINE config 2 (40 subjects x 30,000
-voxels x 1,000 TRs, k=50, fp64); subjects are sharded across ranks (strong
-scaling, cli.py:82-85 contiguous shards).
+voxels x 1,000 TRs, k=50, fp64, 20 iterations); subjects are sharded across
+ranks (strong scaling, cli.py:82-85 contiguous shards).
 
 Under torchrun (N > 1) every rank drives one GPU over NCCL; the per-iteration
 exchange is one all-gather of the ordered E-step table.
@@ -61,7 +65,7 @@ def i8_peak():
 def parse_args():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
@@ -176,50 +180,158 @@ class ClockSampler:
 # CPU side: the reference arithmetic (oracle port) on a bounded sample
 # ---------------------------------------------------------------------------
 
-def cpu_iterations(xs, k, n_iter, seed=0):
-    """Per-iteration seconds of the reference EM (oracle port) on ``xs``."""
+def cpu_iterations(xs, k, n_iter, seed=0, threads=None):
+    """Per-iteration seconds of the reference EM (oracle port) on ``xs``.
+
+    The step functions keep the reference's cost structure (srm.py:116-155:
+    four passes over X-hat per subject-iteration and the V x K SVD);
+    ``threads`` caps the BLAS threads (OPENBLAS_NUM_THREADS, via threadpoolctl).
+    """
+    from threadpoolctl import threadpool_limits
+
     from oracle import srm_oracle as orc
 
-    xhats = [orc.center_rows(x)[0] for x in xs]
-    ws = [orc.initial_mapping(xh.shape[0], k, seed, j)[0] for j, xh in enumerate(xhats)]
-    rho2 = [1.0] * len(xs)
-    sigma = np.eye(k)
-    times = []
-    for _ in range(n_iter):
-        t0 = time.perf_counter()
-        terms = [orc.local_term(ws[j], rho2[j], xhats[j]) for j in range(len(xs))]
-        reduced, rho0 = orc.ordered_reduce(terms, rho2)
-        s, _ = orc.shared_posterior(reduced, sigma, rho0)
-        sigma, tr = orc.shared_covariance(sigma, rho0, s)
-        for j in range(len(xs)):
-            ws[j], rho2[j] = orc.subject_update(xhats[j], s, tr)
-        times.append(time.perf_counter() - t0)
+    with threadpool_limits(limits=threads):
+        xhats = [orc.center_rows(x)[0] for x in xs]
+        ws = [orc.initial_mapping(xh.shape[0], k, seed, j)[0] for j, xh in enumerate(xhats)]
+        rho2 = [1.0] * len(xs)
+        sigma = np.eye(k)
+        times = []
+        for _ in range(n_iter):
+            t0 = time.perf_counter()
+            terms = [orc.local_term(ws[j], rho2[j], xhats[j]) for j in range(len(xs))]
+            reduced, rho0 = orc.ordered_reduce(terms, rho2)
+            s, _ = orc.shared_posterior(reduced, sigma, rho0)
+            sigma, tr = orc.shared_covariance(sigma, rho0, s)
+            for j in range(len(xs)):
+                ws[j], rho2[j] = orc.subject_update(xhats[j], s, tr)
+            times.append(time.perf_counter() - t0)
     return times
 
 
-def sample_subjects(cfg, n, seed):
+def _proc_worker(xs, k, n_iter, seed, threads, barrier, out):
+    out.put(cpu_iterations_sync(xs, k, n_iter, seed, threads, barrier))
+
+
+def cpu_iterations_sync(xs, k, n_iter, seed, threads, barrier):
+    """cpu_iterations on one worker's share with a barrier per iteration
+    (the reference's sockets backend synchronises at its gather/broadcast)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import srm_oracle as orc
+
+    with threadpool_limits(limits=threads):
+        xhats = [orc.center_rows(x)[0] for x in xs]
+        ws = [orc.initial_mapping(xh.shape[0], k, seed, j)[0] for j, xh in enumerate(xhats)]
+        rho2 = [1.0] * len(xs)
+        sigma = np.eye(k)
+        times = []
+        for _ in range(n_iter):
+            barrier.wait()
+            t0 = time.perf_counter()
+            terms = [orc.local_term(ws[j], rho2[j], xhats[j]) for j in range(len(xs))]
+            reduced, rho0 = orc.ordered_reduce(terms, rho2)  # this worker's share only (timing model)
+            s, _ = orc.shared_posterior(reduced, sigma, rho0)
+            sigma, tr = orc.shared_covariance(sigma, rho0, s)
+            for j in range(len(xs)):
+                ws[j], rho2[j] = orc.subject_update(xhats[j], s, tr)
+            barrier.wait()
+            times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_process_iterations(xs, k, n_iter, seed, procs):
+    """The paper's best CPU mode (cli.py:113-200 ``--backend sockets
+    --spawn-local P``): P forked workers with cores / P BLAS
+    threads each and contiguous subject shards; per-iteration time is the
+    barrier-to-barrier time (the K x T exchange, ~KT bytes, is not modelled)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("fork")
+    cores = os.cpu_count() or 1
+    barrier = ctx.Barrier(procs)
+    out = ctx.Queue()
+    shares = [xs[i * len(xs) // procs:(i + 1) * len(xs) // procs] for i in range(procs)]
+    ps = [ctx.Process(target=_proc_worker, args=(sh, k, n_iter, seed, max(1, cores // procs), barrier, out))
+          for sh in shares]
+    for p in ps:
+        p.start()
+    res = [out.get() for _ in ps]
+    for p in ps:
+        p.join()
+    return [max(r[i] for r in res) for i in range(n_iter)]
+
+
+def blas_info():
+    try:
+        from threadpoolctl import threadpool_info
+
+        libs = [f"{d.get('internal_api')} {d.get('version')}" for d in threadpool_info() if d.get("user_api") == "blas"]
+    except Exception:  # noqa: BLE001
+        libs = []
+    model = ""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"blas": ", ".join(libs) or "unknown", "cpu": model, "cores": os.cpu_count()}
+
+
+def sample_subjects(cfg, n, seed, device_xs=None):
+    """The first ``n`` subjects of the workload as host arrays -- the same
+    bytes the GPU arm fits (device Philox stream copied to the host) when a
+    GPU is present, else the host generator's stream."""
+    if device_xs is not None:
+        return [np.ascontiguousarray(x.cpu().numpy()) for x in device_xs[:n]]
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            from paper_1608_04647_b200.data import recipe_torch
+
+            out = []
+            for i in range(n):
+                x, _, _ = recipe_torch(cfg["n_subjects"], cfg["n_voxels"], cfg["n_trs"], cfg["k"], seed=seed,
+                                       smooth=cfg["smooth"], dtype=cfg["dtype"], first_subject=i, count=1)
+                out.append(x[0].cpu().numpy())
+            return out
+    except Exception:  # noqa: BLE001
+        pass
     from paper_1608_04647_b200.data import recipe_numpy
 
-    dt = cfg["dtype"]
     xs, _, _ = recipe_numpy(cfg["n_subjects"], cfg["n_voxels"], cfg["n_trs"], cfg["k"], seed=seed,
-                            smooth=cfg["smooth"], dtype=dt, first_subject=0, count=n)
+                            smooth=cfg["smooth"], dtype=cfg["dtype"], first_subject=0, count=n)
     return xs
 
 
-def cpu_baseline(cfg, budget_s=20.0, seed=0):
-    """The reference arithmetic on the host cores; ~budget_s of CPU work."""
-    xs = sample_subjects(cfg, 1, seed)
-    t1 = statistics.median(cpu_iterations(xs, cfg["k"], 2, seed))  # 1 subject-iteration
-    n_sub = int(max(1, min(cfg["n_subjects"], 8, budget_s / max(t1, 1e-3) / 3)))
-    xs = sample_subjects(cfg, n_sub, seed)
-    times = cpu_iterations(xs, cfg["k"], 3, seed)
-    t = statistics.median(times)
+def cpu_baseline(cfg, host_xs, budget_s=24.0, seed=0):
+    """The reference arithmetic on the host cores, swept over
+    OPENBLAS_NUM_THREADS in {1, cores/2, cores} and P-process shards
+    (BASELINE.md section 3); ~budget_s of CPU work in total."""
+    cores = os.cpu_count() or 1
+    t1 = statistics.median(cpu_iterations(host_xs[:1], cfg["k"], 2, seed))  # 1 subject-iteration, all threads
+    n_sub = int(max(1, min(len(host_xs), cfg["n_subjects"], budget_s / 8 / max(t1, 1e-3))))
+    xs = host_xs[:n_sub]
     units = n_sub * cfg["n_voxels"] * cfg["n_trs"]
+    sweep = {}
+    for th in sorted({1, max(1, cores // 2), cores}):
+        sweep[f"1 proc x {th} threads"] = units / statistics.median(cpu_iterations(xs, cfg["k"], 2, seed, th))
+    for procs in sorted({min(n_sub, 4), min(n_sub, cores)}):
+        if procs > 1:
+            sweep[f"{procs} procs x {max(1, cores // procs)} threads"] = units / statistics.median(
+                cpu_process_iterations(xs, cfg["k"], 2, seed, procs))
+    best = max(sweep, key=sweep.get)
+    info = blas_info()
     return {
-        "value": units / t, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-        "sample": (f"oracle/srm_oracle.py (numpy/OpenBLAS restatement of factorfit.srm, bit-identical on the "
-                   f"golden vectors): {n_sub} of {cfg['n_subjects']} subjects, median of 3 EM iterations "
-                   f"({t:.2f} s/iteration), demean+init excluded, OpenBLAS threads = all {os.cpu_count()} cores"),
+        "value": sweep[best], "unit": UNIT, "cores": cores, "kind": "port",
+        "sample": (f"oracle/srm_oracle.py (numpy/scipy restatement of factorfit.srm with its cost structure, "
+                   f"bit-identical on the golden vectors): {n_sub} of {cfg['n_subjects']} subjects (the same bytes "
+                   f"as the GPU arm), median of 2 EM iterations per setting, demean + init excluded; best setting "
+                   f"{best}"),
+        "sweep": sweep, "blas": info["blas"], "cpu": info["cpu"],
     }
 
 
@@ -228,8 +340,8 @@ def run_reference(args):
     if rank != 0:
         return 0
     cfg = workload(args)
-    xs = sample_subjects(cfg, 1, args.seed)
-    t1 = statistics.median(cpu_iterations(xs, cfg["k"], 2, args.seed))
+    xs1 = sample_subjects(cfg, 1, args.seed)
+    t1 = statistics.median(cpu_iterations(xs1, cfg["k"], 2, args.seed))
     budget = 150.0 / max(1, args.steps + args.warmup)
     n_sub = int(max(1, min(cfg["n_subjects"], budget / max(t1, 1e-3))))
     xs = sample_subjects(cfg, n_sub, args.seed)
@@ -237,15 +349,18 @@ def run_reference(args):
     t = float(np.mean(times))
     units = n_sub * cfg["n_voxels"] * cfg["n_trs"]
     value = units / t
+    info = blas_info()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": cfg["dtype"],
-        "data": "synthetic: BASELINE generative recipe (seeded numpy PCG64 stream), reference init_subject",
+        "data": "synthetic: BASELINE generative recipe (device Philox stream copied to the host: the GPU arm's bytes), "
+                "reference init_subject",
         "config": config_json(cfg, args.config, args.gpus), "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                          "sample": (f"{n_sub} of {cfg['n_subjects']} subjects per step (one EM iteration of the "
-                                    f"oracle port of factorfit.srm per step), OpenBLAS on all host cores")},
+                                    f"oracle port of factorfit.srm per step), OpenBLAS on all host cores"),
+                         "blas": info["blas"], "cpu": info["cpu"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -272,6 +387,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     comm = TorchCommunicator() if world > 1 else None
     cfg = workload(args)
+    iters = cfg["iterations"]
     start, stop = shard_bounds(cfg["n_subjects"], world, rank)
     counts = [shard_bounds(cfg["n_subjects"], world, r)[1] - shard_bounds(cfg["n_subjects"], world, r)[0]
               for r in range(world)]
@@ -283,45 +399,50 @@ def run_ours(args):
                             dtype=cfg["dtype"], first_subject=start, count=n_local, device=dev)
     torch.cuda.synchronize()
 
-    # ---------------- value: X resident in HBM, a K-iteration fit timed --------
-    # The timed region is everything a fit does after demean + init (the
-    # reference's per-iteration accounting also excludes those): the Gram
-    # precompute when the Gram path is chosen, K EM iterations, and the final
-    # W_i = A_i M_i.  One-time work is therefore charged to the K steps.
+    # ---------------- value: X-hat resident in HBM, K complete fits timed ------
     algo = args.algorithm
     use_i8 = args.gram_int8 == "on"
-    if algo == "auto":
-        algo = srm.choose_algorithm([V] * cfg["n_subjects"], T, K, args.steps,
+    if algo == "auto":  # the choice srm.fit makes for this config at its iteration count
+        algo = srm.choose_algorithm([V] * cfg["n_subjects"], T, K, iters,
                                     torch.cuda.mem_get_info(dev)[0] * world, storage=cfg["dtype"],
                                     gram_int8=use_i8)
-    total_iters = max(args.warmup, args.steps) + 8
-    eng = SrmEngine([V] * n_local, T, K, total_iters, storage=cfg["dtype"], world_size=world, rank=rank,
+    eng = SrmEngine([V] * n_local, T, K, iters, storage=cfg["dtype"], world_size=world, rank=rank,
                     counts=counts, ordered=True, gram=(algo == "gram"), tc=(cfg["dtype"] == "f32"),
                     gram_i8=(algo == "gram" and use_i8), device=dev)
     use_i8 = eng.gram_i8
     eng.load(xs)
+    # the same bytes on the host: pinned for the e2e fits, the first subjects for the CPU baseline
+    host = None
+    if not args.no_e2e:
+        host = [x.to("cpu").pin_memory() for x in xs]
+    cpu_xs = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_xs = [x.cpu().numpy() for x in xs[:8]]
+    del xs
+    torch.cuda.empty_cache()
     use_graph = world == 1
+    eng.init_mapping(args.seed, start)  # the host PCG64 draws (srm.py:111), uploaded once
+    draws = eng.amat.clone()            # each step restarts from them: only device work is timed
 
-    def schedule(n_iter, timed_events=None):
-        if timed_events:
-            timed_events[0].record(torch.cuda.current_stream())
+    def step():
+        # one complete fit: restart, device init (polar of the draw, first E-step
+        # term), one-time Gram, the config's EM iterations, final W
+        eng.reset()
+        eng.amat.copy_(draws)
+        eng.init_kernels()
         eng.prepare_gram()
-        for it in range(n_iter):
+        for _ in range(iters):
             if use_graph and eng._graph is not None:
                 eng.replay()
             else:
                 eng.step(comm)
-                if use_graph and it == 0:
+                if use_graph:
                     eng.capture()
         eng.finalize()
-        if timed_events:
-            timed_events[1].record(torch.cuda.current_stream())
 
-    eng.init_mapping(args.seed, start)
-    schedule(max(1, args.warmup))          # warm-up fit: configures kernels, captures the graph
+    for _ in range(max(1, args.warmup)):  # configures kernels, captures the iteration graph
+        step()
     eng.raise_status()
-    eng.reset()
-    eng.init_mapping(args.seed, start)     # fresh EM start (untimed, like the reference's init)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -331,7 +452,10 @@ def run_ours(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    schedule(args.steps, (e0, e1))
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
     torch.cuda.synchronize()
     clocks = sampler.stop()
     if world > 1:
@@ -343,11 +467,9 @@ def run_ours(args):
         ms = float(t.item())
     eng.raise_status()
     units = cfg["n_subjects"] * V * T
-    value = units / (ms / 1e3)
-    tc = cfg["dtype"] == "f32"
+    value = units * iters / (ms / 1e3)
 
-    # per-kernel durations (CUDA events on the launch stream, untimed pass)
-    st = torch.cuda.current_stream()
+    # per-kernel durations (CUDA events on the launch stream, untimed passes)
     prof_iter = {}
     for _ in range(5):
         one = {}
@@ -357,8 +479,8 @@ def run_ours(args):
             prof_iter.setdefault(name, []).append(t_ms)
     prof_iter = {k_: float(np.mean(v_)) for k_, v_ in prof_iter.items()}
     once = {}
+    prof_g = {}
     if algo == "gram":
-        prof_g = {}
         for _ in range(3):
             for name, t_ms in eng.profile_gram():
                 prof_g.setdefault(name, []).append(t_ms)
@@ -369,15 +491,17 @@ def run_ours(args):
             prof_f.setdefault(name, []).append(t_ms)
     once.update({k_: float(np.mean(v_)) for k_, v_ in prof_f.items()})
     eng.raise_status()
-    # kernels of the timed region: every stage is one launch except oz_split
-    # (column maxima + slicing)
-    launches = (eng.launches_per_iteration * args.steps + len(prof_f)
-                + (len(prof_g) + ("oz_split" in prof_g) if algo == "gram" else 0))
+    # kernels of one step: reset + 6 init kernels, the Gram stages (oz_split is
+    # two launches: column exponents + slicing), the iterations, the final W
+    init_launches = 7
+    per_step = (init_launches + (len(prof_g) + ("oz_split" in prof_g) if algo == "gram" else 0)
+                + eng.launches_per_iteration * iters + len(prof_f))
+    launches = per_step * args.steps
     del eng
     torch.cuda.empty_cache()
 
-    # time share of each kernel inside the timed region (K iterations + one-time work)
-    region_ms = {k_: v_ * args.steps for k_, v_ in prof_iter.items()}
+    # time share of each kernel inside one step (iterations x per-iteration + one-time)
+    region_ms = {k_: v_ * iters for k_, v_ in prof_iter.items()}
     region_ms.update(once)
     tot = sum(region_ms.values())
     step_share = {k_: v_ / tot for k_, v_ in region_ms.items()}
@@ -386,18 +510,19 @@ def run_ours(args):
     local_units = n_local * V * T
     ldx = -(-T // 32) * 32
     nt = -(-ldx // 128)
+    slice_b = 8 if cfg["dtype"] == "f64" else 4  # int8 slice bytes per X-hat value (7 or 4 slices, padded)
     if dom in ("gram_tiles", "oz_gram"):
         launch_ms = once[dom]
         alg_flops = float(n_local) * V * T * (T + 1)          # symmetric X^T X: T(T+1)/2 dots of length V
-        alg_bytes = float(local_units * b)                      # X-hat read once
+        alg_bytes = float(local_units * (slice_b if dom == "oz_gram" else b))
         # int8 products issued by oz_gram per upper 128 x 128 tile and 32-voxel block: the slice
-        # pairs s + s' < 7 (28 for fp64's 7 slices; all 16 for fp32's 4)
+        # pairs s + s' < 7 (28 for fp64's 7 slices; all 16 for fp32's 4); useful = T(T+1)/2 entries
         products = 28 if cfg["dtype"] == "f64" else 16
-        i8_ops = 2.0 * products * nt * (nt + 1) / 2 * 128 * 128 * (-(-V // 32) * 32) * n_local
+        i8_ops = 2.0 * products * (T * (T + 1) / 2) * (-(-V // 32) * 32) * n_local
     elif dom in ("final_a", "oz_w", "apply_w"):
         launch_ms = once[dom]
         alg_flops = 2.0 * local_units * K
-        alg_bytes = float(local_units * b)
+        alg_bytes = float(local_units * (slice_b if dom == "oz_w" else b))
     else:
         launch_ms = prof_iter[dom]
         if dom in ("contract_a", "contract_e_xhat", "tc_apass", "tc_bpass"):
@@ -423,6 +548,8 @@ def run_ours(args):
             "frac": achieved_tops / i8_pk, "traffic": traffic, "kernel": dom, "launch_ms": launch_ms,
             "algorithmic_int8_ops_per_launch": i8_ops, "algorithmic_flops_per_launch": alg_flops,
             "algorithmic_bytes_per_launch": alg_bytes, "peak_source": i8_src,
+            "work": "useful slice products only: T(T+1)/2 Gram entries per subject (the padded 128 x 128 "
+                    "diagonal tiles and the mirrored half are not counted)",
         }
         other_roofline = {
             "bound": "fp64-equivalent", "achieved": achieved_tf, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -453,16 +580,41 @@ def run_ours(args):
         }
         other_roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                           "frac": achieved_gbs / hbm_peak, "kernel": dom, "peak_source": peak_src}
+    # the metric's HBM half: every kernel that streams X-hat (or its int8 slices), at its
+    # algorithmic bytes per launch (reads of X-hat / slices once, writes of slices / W once)
+    xk_bytes = {
+        "oz_split": local_units * (b + slice_b),                   # read X-hat, write the slices
+        "oz_gram": local_units * slice_b,                          # read the slices once
+        "oz_w": local_units * slice_b + n_local * V * K * 8,       # read the slices, write W
+        "gram_tiles": local_units * b,
+        "final_a": local_units * b + n_local * V * (-(-K // 8) * 8) * 8,
+        "contract_a": local_units * b + n_local * V * (-(-K // 8) * 8) * 8,
+        "contract_e_xhat": local_units * b,
+        "tc_apass": local_units * b, "tc_bpass": local_units * b,
+    }
+    per_kernel = {}
+    for name, nbytes in xk_bytes.items():
+        t_ms = once.get(name, prof_iter.get(name))
+        if t_ms:
+            gbs = nbytes / (t_ms / 1e3) / 1e9
+            per_kernel[name] = {"bytes": nbytes, "ms": t_ms, "achieved": gbs, "frac": gbs / hbm_peak,
+                                "per": "launch" if name in once else "iteration"}
+    x_read = 2.0 * b * units * iters  # two X-hat reads per subject-iteration
+    roofline_hbm = {
+        "unit": "GB/s", "peak": hbm_peak, "peak_source": peak_src, "kernels": per_kernel,
+        "streaming_equivalent": {
+            "achieved": x_read / (ms / 1e3) / 1e9, "frac": x_read / (ms / 1e3) / 1e9 / hbm_peak,
+            "note": ("SURVEY.md §8(d) algorithmic bytes (2 X-hat reads per subject-iteration) over the step "
+                     "time; above 1 where the Gram path replaces the per-iteration passes"),
+        },
+    }
     prof = {"per_iteration_ms": prof_iter, "one_time_ms": once}
 
     # ---------------- e2e: public API, pinned host inputs ---------------------
     e2e = None
-    if not args.no_e2e:
-        host = [x.to("cpu").pin_memory() for x in xs]
-        del xs
-        torch.cuda.empty_cache()
+    if host is not None:
         subjects = [SubjectData(f"sub-{start + j:04d}", host[j]) for j in range(n_local)]
-        conf = srm.SrmConfig(k=K, iterations=cfg["iterations"], seed=args.seed)
+        conf = srm.SrmConfig(k=K, iterations=iters, seed=args.seed)
         srm.fit(subjects, conf, comm, algorithm=args.algorithm, gram_int8=args.gram_int8 == "on")  # warm-up (allocator, kernels)
         times = []
         for _ in range(max(1, args.e2e_fits)):
@@ -481,24 +633,28 @@ def run_ours(args):
         dt = min(times)
         h2d = cfg["n_subjects"] * V * T * b
         d2h = cfg["n_subjects"] * V * (K + 1) * 8 + K * T * 8 + K * K * 8
-        e2e = {"value": units * cfg["iterations"] / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
+        e2e = {"value": units * iters / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "seconds_per_fit": dt,
-               "step": (f"one srm.fit call ({cfg['iterations']} EM iterations) on pinned host arrays: H2D, "
+               "step": (f"one srm.fit call ({iters} EM iterations) on pinned host arrays: H2D, "
                         "demean, PCG64 init + device polar, EM loop, model read-back")}
         del model
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, seed=args.seed)
+    if cpu_xs is not None:
+        cpu = cpu_baseline(cfg, cpu_xs, seed=args.seed)
 
     if rank == 0:
+        conf_json = config_json(cfg, args.config, world)
+        conf_json["step"] = (f"one complete fit from HBM-resident X-hat: device init, "
+                             f"{'one-time int8 X^T X, ' if algo == 'gram' else ''}{iters} EM iterations, final W")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic: BASELINE generative recipe (seeded, device Philox stream); reference init",
-            "config": config_json(cfg, args.config, world),
-            "roofline": roofline, "secondary_roofline": other_roofline, "algorithm": algo,
+            "config": conf_json,
+            "roofline": roofline, "secondary_roofline": other_roofline, "roofline_hbm": roofline_hbm,
+            "algorithm": algo,
             "gram_xtx": (("int8 slices on tcgen05 (7 slices, ~2^-48 of column max)" if cfg["dtype"] == "f64"
                           else "int8 slices on tcgen05 (4 slices, ~2^-27 of column max; fp32 data)")
                          if use_i8 else "fp64 DMMA")

@@ -246,6 +246,17 @@ int srm_gemm_tn(const double* w, int64_t ldw, const void* x, int x_dtype, int64_
 int srm_gemm_nt(const void* x, int x_dtype, int64_t ldx, const double* s, int64_t lds,
                 int64_t v, int64_t t, int64_t k, double alpha, double* out, int64_t ldo,
                 void* workspace, int64_t ws_bytes, void* stream);
+/* srm.py:330-333 `project`, batched over the t columns of a block of volumes:
+ * out[k x t] = W^T (X - mu 1^T) with W [v x k] f64, X [v x t] dtype, mu [v] f64
+ * (null: no centering); the subtraction is fused into the fp64 staging of X,
+ * so projecting mu itself gives exactly 0 (reference test_srm.py:343-345). */
+int srm_project(const double* w, int64_t ldw, const void* x, int x_dtype, int64_t ldx,
+                const double* mu, int64_t v, int64_t k, int64_t t, double* out, int64_t ldo,
+                void* workspace, int64_t ws_bytes, void* stream);
+/* srm.py:336-338 `map_between` after the projection: out[v x t] = W z + mu 1^T
+ * with W [v x k], z [k x t], mu [v] (null: none); k <= 128 */
+int srm_unproject(const double* w, int64_t ldw, const double* z, int64_t ldz, const double* mu,
+                  int64_t v, int64_t k, int64_t t, double* out, int64_t ldo, void* stream);
 /* trace(A^T A) = sum of squares of a [rows x cols] f64 block (kernels.py:152-155)
  * into *out (device), summed in a fixed order; non-finite entries raise
  * InvalidInputError through status4 (kernels.py:45-46).  workspace >= 8 KB. */
@@ -272,7 +283,7 @@ int srm_tail_step(const double* reduced, int64_t ldr, const double* sigma, int64
  * sigma_max = 0) goes to status4.  Synchronous. */
 int srm_polar(const double* a, int64_t lda, int64_t v, int64_t k, double* w, int64_t ldw,
               int32_t* status4, void* workspace, int64_t ws_bytes, void* stream);
-/* workspace bytes needed by srm_gemm_tn / srm_gemm_nt / srm_polar / srm_tail_step */
+/* workspace bytes needed by srm_gemm_tn / srm_gemm_nt / srm_project / srm_polar / srm_tail_step */
 int64_t srm_stateless_workspace_bytes(int64_t v, int64_t k, int64_t t);
 
 /* ---- SFAB subject containers (data_io.py:1-30 layout, :130-196 checks) ------

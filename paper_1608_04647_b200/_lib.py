@@ -58,6 +58,9 @@ SIGNATURES = [
                             c_i64, c_vp, c_i64, c_vp]),
     ("srm_tail_step", c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_dbl, c_vp, c_i64, c_vp,
                               c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    ("srm_project", c_int, [c_vp, c_i64, c_vp, c_int, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp,
+                            c_i64, c_vp]),
+    ("srm_unproject", c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
     ("srm_trace_ata", c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     ("srm_add_diag", c_int, [c_vp, c_i64, c_i64, c_dbl, c_vp, c_i64, c_vp]),
     ("srm_spd_inverse", c_int, [c_vp, c_i64, c_vp, c_vp]),

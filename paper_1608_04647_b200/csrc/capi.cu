@@ -84,6 +84,7 @@ enum Internal {
   I_QRBUF1,
   I_QRJOBS,
   I_SVDJOBS,
+  I_NSG,
   I_COUNT
 };
 
@@ -224,6 +225,7 @@ void layout(srm_plan* p) {
   sz[I_QRBUF1] = exact ? p->qr.buf_doubles * 8 : 0;
   sz[I_QRJOBS] = exact ? (int64_t)p->qr.levels.size() * p->n_local * (int64_t)sizeof(QrJob) : 0;
   sz[I_SVDJOBS] = exact ? (int64_t)p->n_local * (int64_t)sizeof(SvdJob) : 0;
+  sz[I_NSG] = ns_polar_g_supported((int)p->kp) ? (int64_t)p->n_local * 4 * kp2 * 8 : 0;
   int64_t cur = 0;
   for (int r = 0; r < I_COUNT; ++r) {
     p->off[r] = cur;
@@ -482,6 +484,7 @@ void set_pointers(srm_plan* p) {
   d.qscr = region<double>(p, I_QSCR);
   d.crossp = region<double>(p, I_CROSSP);
   d.scal = region<double>(p, SRM_R_SCAL);
+  d.nsg = p->size[I_NSG] ? region<double>(p, I_NSG) : nullptr;
   d.st = region<double>(p, I_ST);
   d.gram = p->size[SRM_R_GRAM] ? region<double>(p, SRM_R_GRAM) : nullptr;
   d.af = p->size[I_AF] ? region<float>(p, I_AF) : nullptr;
@@ -729,12 +732,6 @@ std::vector<Stage> finalize_stages(srm_plan* p, int first, int count) {
     return v;
   }
   if (first > 0) return v;
-  if ((p->flags & SRM_FLAG_GRAM) && p->dtype == SRM_F32 && !ns_polar_supported((int)p->kp) &&
-      ns_polar_f32_supported((int)p->kp)) {
-    // the per-iteration polar ran in fp32 (K > 80): the returned W takes the
-    // exact fp64 transform of the last M-step's A^T A (still in bred)
-    v.push_back({"final_polar", [d](cudaStream_t st) { return launch_final_polar(d, st); }});
-  }
   if (p->oz_w) {
     // W_i = Xhat_i R_i, R_i = S^T M_i / 2, from the int8 slices of Xhat on the
     // tensor cores (no A pass, no W = A M pass)

@@ -144,6 +144,14 @@ cudaError_t launch_tsqr(const QrJob* jobs_dev, int n_jobs, int max_ctas, int K, 
 cudaError_t launch_svd_polar(const SvdJob* jobs_dev, int n_jobs, int K, int32_t* status, const int32_t* iter,
                              cudaStream_t st);
 
+// transforms (transform.cu): xp[r][c] = x[r][c] - mu[r] (fp64, zero pad to ldp),
+// and out = A B + bias 1^T (A: V x K, B: K x N, K <= 128)
+cudaError_t launch_center_stage(const void* x, int x_dtype, int64_t ldx, const double* mu, int64_t v, int64_t t,
+                                double* xp, int64_t ldp, cudaStream_t st);
+bool gemm_nn_bias_supported(int K);
+cudaError_t launch_gemm_nn_bias(const double* A, int64_t lda, const double* B, int64_t ldb, const double* bias,
+                                double* out, int64_t ldo, int64_t V, int K, int64_t N, cudaStream_t st);
+
 // thread-local message returned by srm_last_error() (defined in capi.cu)
 void set_last_error(const char* where, cudaError_t e);
 

@@ -1064,9 +1064,33 @@ cudaError_t launch_oz_sg_sk(const TmaMap& tmg, const TmaMap& tms, const int32_t*
   // at least one tile per CTA, so a tile meets at most two CTA ranges
   g.span = std::max<int64_t>(g.nub, (g.units + max_ctas - 1) / max_ctas);
   const unsigned grid = (unsigned)((g.units + g.span - 1) / g.span);
-  k_oz_sg_sk<<<grid, kRowThreads, Shape::smem_bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(tmg.opaque),
-                                                          *reinterpret_cast<const CUtensorMap*>(tms.opaque), g);
-  return cudaGetLastError();
+  // a head CTA spins on a flag its tail CTA raises, so every CTA of the grid
+  // must be resident at once: launched cooperatively, which the driver only
+  // accepts when the whole grid fits at this kernel's occupancy (checked here
+  // too, so an oversized grid is an error rather than a deadlock)
+  static int max_resident = 0;
+  if (max_resident == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_oz_sg_sk, kRowThreads, Shape::smem_bytes);
+    if (e != cudaSuccess) return e;
+    max_resident = sms * per_sm;
+  }
+  if ((int)grid > max_resident) return cudaErrorCooperativeLaunchTooLarge;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kRowThreads);
+  cfg.dynamicSmemBytes = Shape::smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_oz_sg_sk, *reinterpret_cast<const CUtensorMap*>(tmg.opaque),
+                            *reinterpret_cast<const CUtensorMap*>(tms.opaque), g);
 }
 
 cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* expo, double* rt, int64_t ldx,

@@ -69,6 +69,7 @@ struct DevPlan {
   double* qscr;      // [n_local][kp][kp]
   double* crossp;    // [n_local][ntile_apply]
   double* scal;      // [n_local][8]: {jacobi sweeps, ...}
+  double* nsg;       // [n_local][4][kp][kp]: Newton-Schulz matrices of the kp > 80 transform (else null)
   double* st;        // [ldx][kp]: S^T (Gram path operand)
   double* gram;      // [n_local][ldx][ldx]: X_i^T X_i (Gram path)
   float* af;         // [rows][np]: A_i in fp32 (tensor-core path)
@@ -130,6 +131,9 @@ bool ns_polar_f32_supported(int kp);
 cudaError_t launch_ns_refine(const DevPlan& p, cudaStream_t s, int warn = 0);
 cudaError_t launch_final_polar(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_ns_polar_f32(const DevPlan& p, int init, cudaStream_t s);
+// fp64 Newton-Schulz for 80 < kp <= 128 with its matrices in DevPlan::nsg
+bool ns_polar_g_supported(int kp);
+cudaError_t launch_ns_polar_g(const DevPlan& p, int init, cudaStream_t s);
 cudaError_t launch_eig_polar_exact(const DevPlan& p, int init, cudaStream_t s);
 
 }  // namespace srm

@@ -237,6 +237,203 @@ cudaError_t run_ns(const DevPlan& p, int init, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
+// The same fp64 coupled iteration for 80 < kp <= 128, where four K x K fp64
+// matrices no longer fit in shared memory: Y, Z, T and Y' live in a per-subject
+// global scratch (4 kp^2 doubles, L2-resident) and every product streams
+// 32-wide k-slabs of its operands through shared memory into DMMA fragments.
+// fp64 throughout, so the transform is as accurate as the kp <= 80 kernel's
+// (an fp32 iteration carried ~4e-7 into S per iteration).
+// ---------------------------------------------------------------------------
+constexpr int kSlab = 32;
+constexpr int kSlabLd = kSlab + 4;  // == 4 mod 16 doubles
+
+template <int KP, typename Epi>
+__device__ __forceinline__ void gmm_sym(const double* A, const double* B, double* As, double* Bs, Epi epi) {
+  constexpr int LDB = ns_ld(KP);
+  using TL = SymTiles<KP>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int tm[TL::PER], tn[TL::PER];
+  bool on[TL::PER];
+#pragma unroll
+  for (int q = 0; q < TL::PER; ++q) {
+    int idx = warp * TL::PER + q, m = 0;
+    on[q] = idx < TL::N;
+    if (!on[q]) idx = 0;
+    while (idx >= TL::NT - m) {
+      idx -= TL::NT - m;
+      ++m;
+    }
+    tm[q] = m;
+    tn[q] = m + idx;
+  }
+  double acc[TL::PER][2];
+#pragma unroll
+  for (int q = 0; q < TL::PER; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int k0 = 0; k0 < KP; k0 += kSlab) {
+    const int kw = min(kSlab, KP - k0);
+    for (int e = threadIdx.x; e < KP * kSlab; e += kNsThreads) {
+      const int r = e / kSlab, kk = e - r * kSlab;
+      As[r * kSlabLd + kk] = kk < kw ? A[r * KP + k0 + kk] : 0.0;
+    }
+    for (int e = threadIdx.x; e < kSlab * KP; e += kNsThreads) {
+      const int kk = e / KP, c = e - kk * KP;
+      Bs[kk * LDB + c] = kk < kw ? B[(k0 + kk) * KP + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int kk = 0; kk < kSlab; kk += 4) {
+#pragma unroll
+      for (int q = 0; q < TL::PER; ++q) {
+        if (on[q]) {
+          const double a = As[(tm[q] * 8 + (lane >> 2)) * kSlabLd + kk + (lane & 3)];
+          const double b = Bs[(kk + (lane & 3)) * LDB + tn[q] * 8 + (lane >> 2)];
+          dmma(acc[q][0], acc[q][1], a, b);
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < TL::PER; ++q)
+    if (on[q]) epi(tm[q] * 8 + (lane >> 2), tn[q] * 8 + 2 * (lane & 3), acc[q][0], acc[q][1], tm[q] == tn[q]);
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kNsThreads) k_ns_polar_g(DevPlan p, int init) {
+  constexpr int LDB = ns_ld(KP);
+  constexpr int MAT = KP * KP;
+  extern __shared__ __align__(16) double gsm[];
+  __shared__ double red[32];
+  __shared__ double s_scale;
+  double* As = gsm;                 // [KP][kSlabLd]
+  double* Bs = gsm + KP * kSlabLd;  // [kSlab][LDB]
+  const int i = p.sub0 + blockIdx.x;
+  const int n = (int)p.K;
+  const int tid = threadIdx.x;
+  double* buf[4];
+  for (int q = 0; q < 4; ++q) buf[q] = p.nsg + ((int64_t)i * 4 + q) * MAT;
+  const double* Cg = p.bred + (int64_t)i * p.kp * p.ldo + p.ldx;  // A^T A block, row stride ldo
+
+  double rowmax = 0.0;
+  for (int a = tid >> 2; a < KP; a += kNsThreads / 4) {  // four lanes per row, summed in a fixed order
+    double rs = 0.0;
+    for (int b = (tid & 3); b < n && a < n; b += 4) rs += fabs(0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a]));
+    rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+    rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+    rowmax = fmax(rowmax, rs);
+  }
+  rowmax = warp_max(rowmax);
+  if ((tid & 31) == 0) red[tid >> 5] = rowmax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < kNsThreads / 32; ++w) m = fmax(m, red[w]);
+    s_scale = m;
+  }
+  __syncthreads();
+  const double c = s_scale;
+  const bool degenerate = !(c > 0.0) || !isfinite(c);
+  const double inv_c = degenerate ? 0.0 : 1.0 / c;
+  for (int e = tid; e < MAT; e += kNsThreads) {
+    const int a = e / KP, b = e - a * KP;
+    buf[0][e] = (a < n && b < n) ? 0.5 * (Cg[(int64_t)a * p.ldo + b] + Cg[(int64_t)b * p.ldo + a]) * inv_c : 0.0;
+    buf[1][e] = (a == b && a < n) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+
+  int y = 0, z = 1;
+  bool converged = false;
+  int extra = -1;
+  double prev_err = 1e300;
+  int it = 0;
+  for (; it < 90 && !degenerate; ++it) {
+    int f0 = -1, f1 = -1;
+    for (int q = 0; q < 4; ++q)
+      if (q != y && q != z) (f0 < 0 ? f0 : f1) = q;
+    double* Tm = buf[f0];
+    double* Yn = buf[f1];
+    double err = 0.0;
+    gmm_sym<KP>(buf[z], buf[y], As, Bs, [&](int r, int col, double v0, double v1, bool dg) {
+      const double d0 = (r == col ? 1.0 : 0.0) - v0, d1 = (r == col + 1 ? 1.0 : 0.0) - v1;
+      const double wgt = dg ? 1.0 : 2.0;
+      if (r < n && col < n) err += wgt * d0 * d0;
+      if (r < n && col + 1 < n) err += wgt * d1 * d1;
+      const double t0 = 0.5 * (r == col ? 3.0 - v0 : -v0), t1 = 0.5 * (r == col + 1 ? 3.0 - v1 : -v1);
+      Tm[r * KP + col] = t0;
+      Tm[r * KP + col + 1] = t1;
+      if (!dg) {
+        Tm[col * KP + r] = t0;
+        Tm[(col + 1) * KP + r] = t1;
+      }
+    });
+    err = block_sum<kNsThreads>(err, red);  // barrier: T is complete
+    if (extra == 0) {
+      converged = true;
+      break;
+    }
+    if (!(err == err)) break;
+    if (extra < 0 && (err <= 1e-20 || (err < 1e-18 && err > 0.25 * prev_err))) extra = 1;
+    prev_err = err;
+    gmm_sym<KP>(Tm, buf[y], As, Bs, [&](int r, int col, double v0, double v1, bool dg) {
+      Yn[r * KP + col] = v0;
+      Yn[r * KP + col + 1] = v1;
+      if (!dg) {
+        Yn[col * KP + r] = v0;
+        Yn[(col + 1) * KP + r] = v1;
+      }
+    });
+    __syncthreads();
+    double* Zn = buf[y];
+    gmm_sym<KP>(Tm, buf[z], As, Bs, [&](int r, int col, double v0, double v1, bool dg) {
+      Zn[r * KP + col] = v0;
+      Zn[r * KP + col + 1] = v1;
+      if (!dg) {
+        Zn[col * KP + r] = v0;
+        Zn[(col + 1) * KP + r] = v1;
+      }
+    });
+    __syncthreads();
+    z = y;
+    y = f1;
+    if (extra > 0 && --extra == 0) {
+      ++it;
+      converged = true;
+      break;
+    }
+  }
+  const int kp = (int)p.kp;
+  double* Mg = p.mmat + (int64_t)i * kp * kp;
+  const double* Z = buf[z];
+  const double sc = degenerate ? 0.0 : 1.0 / sqrt(c);
+  double zz = 0.0;
+  for (int e = tid; e < kp * kp; e += kNsThreads) {
+    const int a = e / kp, b = e - a * kp;
+    const double v = (a < n && b < n) ? 0.5 * (Z[a * KP + b] + Z[b * KP + a]) : 0.0;
+    zz = fma(v, v, zz);
+    Mg[e] = v * sc;
+  }
+  zz = block_sum<kNsThreads>(zz, red);
+  if (tid == 0) {
+    p.scal[(int64_t)i * 8 + 0] = (double)it;
+    if (degenerate || !converged || !(zz <= kGramCondLimit)) raise_warning(p.status, SRM_WARN_POLAR_CONDITION);
+  }
+}
+
+template <int KP>
+cudaError_t run_ns_g(const DevPlan& p, int init, cudaStream_t s) {
+  constexpr int bytes = (KP * kSlabLd + kSlab * ns_ld(KP)) * (int)sizeof(double);
+  if (!p.nsg) return cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_ns_polar_g<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_ns_polar_g<KP><<<p.nsub, kNsThreads, bytes, s>>>(p, init);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // fp32 SIMT variant for the tensor-core (fp32 X-hat) plans with 80 < kp <= 112:
 // the same coupled iteration with fp32 matrices (4 x kp x (kp+4) floats fit in
 // smem where fp64 does not).  The per-iteration M then carries ~1e-6 relative
@@ -455,7 +652,8 @@ __global__ void __launch_bounds__(kRefThreads, 1) k_ns_refine(DevPlan p, int war
   bool ok = false;
   int extra = -1;
   double prev = 1e300;
-  for (int step = 0; step < 8; ++step) {
+  int step = 0;
+  for (; step < 24; ++step) {
     ref_mm(C, p.ldo, true, Z, kp, T, kp, n, sa, sb);  // T = C Z
     ref_mm(Z, kp, false, T, kp, E, kp, n, sa, sb);    // E = Z C Z (- I below)
     double err = 0.0;
@@ -483,6 +681,7 @@ __global__ void __launch_bounds__(kRefThreads, 1) k_ns_refine(DevPlan p, int war
   }
   if (threadIdx.x == 0) {
     p.scal[(int64_t)i * 8 + 1] = ok ? 1.0 : 0.0;
+    p.scal[(int64_t)i * 8 + 2] = (double)step;
     if (warn && !ok) raise_warning(p.status, SRM_WARN_POLAR_CONDITION);
   }
 }
@@ -506,6 +705,20 @@ cudaError_t launch_ns_refine(const DevPlan& p, cudaStream_t s, int warn) {
 bool ns_polar_supported(int kp) { return kp >= 8 && kp <= 80 && kp % 8 == 0; }
 
 bool ns_polar_f32_supported(int kp) { return kp > 80 && kp <= 112; }
+
+bool ns_polar_g_supported(int kp) { return kp > 80 && kp <= 128 && kp % 8 == 0; }
+
+cudaError_t launch_ns_polar_g(const DevPlan& p, int init, cudaStream_t s) {
+  switch ((int)p.kp) {
+    case 88: return run_ns_g<88>(p, init, s);
+    case 96: return run_ns_g<96>(p, init, s);
+    case 104: return run_ns_g<104>(p, init, s);
+    case 112: return run_ns_g<112>(p, init, s);
+    case 120: return run_ns_g<120>(p, init, s);
+    case 128: return run_ns_g<128>(p, init, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 cudaError_t launch_ns_polar_f32(const DevPlan& p, int init, cudaStream_t s) {
   switch (((int)p.kp + 15) / 16 * 16) {

@@ -1275,22 +1275,16 @@ cudaError_t launch_reduce_chunks(const DevPlan& p, cudaStream_t s) {
 
 cudaError_t launch_eig_polar(const DevPlan& p, int init, cudaStream_t s) {
   if (ns_polar_supported((int)p.kp)) return launch_ns_polar(p, init, s);
-  // fp32 X-hat, 80 < kp <= 112, where the fp64 iteration does not fit in shared
-  // memory: the fp32 Newton-Schulz (~1e-6 relative), refined to fp64 accuracy
-  // by the symmetric Newton iteration for C^{-1/2} (two steps; a subject it
-  // does not converge for hands the fit to the exact route) -- an fp32 M would
-  // carry ~4e-7 into S every iteration and ~1e-6 into W (tools/fp32_accuracy.py)
-  if (p.xf32 && ns_polar_f32_supported((int)p.kp)) {
-    cudaError_t e = launch_ns_polar_f32(p, init, s);
-    if (e == cudaSuccess) e = launch_ns_refine(p, s, 1);
-    return e;
-  }
+  // 80 < kp <= 128: the same fp64 iteration with its matrices in L2 (an fp32
+  // iteration carried ~4e-7 into S per iteration, tools/fp32_accuracy.py)
+  if (ns_polar_g_supported((int)p.kp) && p.nsg) return launch_ns_polar_g(p, init, s);
   return launch_eig_polar_exact(p, init, s);
 }
 
-// fp64 polar transform for every K (NS on DMMA up to kp = 80, Jacobi above)
+// fp64 polar transform for every K (NS on DMMA up to kp = 128, Jacobi above)
 cudaError_t launch_eig_polar_exact(const DevPlan& p, int init, cudaStream_t s) {
   if (ns_polar_supported((int)p.kp)) return launch_ns_polar(p, init, s);
+  if (ns_polar_g_supported((int)p.kp) && p.nsg) return launch_ns_polar_g(p, init, s);
   const size_t bytes = eig_smem_bytes((int)p.K);
   cudaError_t e = set_smem((const void*)k_eig_polar, bytes);
   if (e != cudaSuccess) return e;
@@ -1301,17 +1295,7 @@ cudaError_t launch_eig_polar_exact(const DevPlan& p, int init, cudaStream_t s) {
 // the returned W's exact fp64 transform after a fit: fp64 Newton-Schulz up to
 // kp = 80; above, where the iterations ran the fp32 Newton-Schulz, its M refined
 // in fp64 (k_ns_refine) with Jacobi only for subjects the refinement leaves
-cudaError_t launch_final_polar(const DevPlan& p, cudaStream_t s) {
-  if (ns_polar_supported((int)p.kp)) return launch_ns_polar(p, 1, s);
-  if (!(p.xf32 && ns_polar_f32_supported((int)p.kp))) return launch_eig_polar_exact(p, 1, s);
-  cudaError_t e = launch_ns_refine(p, s);
-  if (e != cudaSuccess) return e;
-  const size_t bytes = eig_smem_bytes((int)p.K);
-  e = set_smem((const void*)k_eig_polar, bytes);
-  if (e != cudaSuccess) return e;
-  k_eig_polar<<<p.nsub, kSmallThreads, bytes, s>>>(p, 2);
-  return cudaGetLastError();
-}
+cudaError_t launch_final_polar(const DevPlan& p, cudaStream_t s) { return launch_eig_polar_exact(p, 1, s); }
 
 cudaError_t launch_apply_m(const DevPlan& p, int with_cross, cudaStream_t s) {
   const int64_t K4 = (p.K + 3) & ~3;

@@ -213,6 +213,36 @@ int srm_gemm_nt(const void* x, int x_dtype, int64_t ldx, const double* s, int64_
   return ret(e, where);
 }
 
+int srm_project(const double* w, int64_t ldw, const void* x, int x_dtype, int64_t ldx, const double* mu, int64_t v,
+                int64_t k, int64_t t, double* out, int64_t ldo, void* workspace, int64_t ws_bytes, void* stream) {
+  if (v < 1 || k < 1 || t < 1 || !contract_kp_supported((int)rup(k, 8))) return SRM_ERR_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t kp = rup(k, 8), ldxp = rup(t, 32);
+  const int64_t nch = std::max<int64_t>(1, (v + kChunk - 1) / kChunk);
+  Carve c{static_cast<char*>(workspace), 0, ws_bytes};
+  double* Lp = c.take<double>(v * kp);
+  double* Xp = c.take<double>(v * ldxp);
+  double* part = c.take<double>(nch * kp * ldxp);
+  double* red = c.take<double>(kp * ldxp);
+  ItemE* items = c.take<ItemE>(nch * ((ldxp + 127) / 128));
+  if (!items) return SRM_ERR_CONFIG;
+  cudaError_t e = cudaMemsetAsync(Lp, 0, v * kp * 8, st);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(Lp, kp * 8, w, ldw * 8, k * 8, v, cudaMemcpyDeviceToDevice, st);
+  // the centering (srm.py:333 x - mu) fused into the fp64 staging copy of X
+  if (e == cudaSuccess) e = launch_center_stage(x, x_dtype, ldx, mu, v, t, Xp, ldxp, st);
+  if (e == cudaSuccess) e = split_v(Lp, kp, Xp, SRM_F64, ldxp, ldxp, v, 1.0, part, red, items, st);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(out, ldo * 8, red, ldxp * 8, t * 8, k, cudaMemcpyDeviceToDevice, st);
+  return ret(e, "project");
+}
+
+int srm_unproject(const double* w, int64_t ldw, const double* z, int64_t ldz, const double* mu, int64_t v, int64_t k,
+                  int64_t t, double* out, int64_t ldo, void* stream) {
+  if (v < 1 || k < 1 || t < 1) return SRM_ERR_SHAPE;
+  if (!gemm_nn_bias_supported((int)k)) return SRM_ERR_UNSUPPORTED;
+  return ret(launch_gemm_nn_bias(w, ldw, z, ldz, mu, out, ldo, v, (int)k, t, static_cast<cudaStream_t>(stream)),
+             "unproject");
+}
+
 int srm_tail_step(const double* reduced, int64_t ldr, const double* sigma, int64_t ldsig, int64_t k, int64_t t,
                   double rho0, double* s_out, int64_t lds_out, double* var_out, double* sigma_out,
                   double* trace_out, int32_t* status4, void* workspace, int64_t ws_bytes, void* stream) {

@@ -51,6 +51,7 @@ __all__ = [
     "project",
     "map_between",
     "project_batch",
+    "map_between_batch",
     "IterationState",
 ]
 
@@ -735,29 +736,66 @@ def _collect(eng, subjects, comm, offset, n_subjects, n_done, keep_on_device, wo
 # transforms (srm.py:330-338)
 # ---------------------------------------------------------------------------
 
-def project_batch(model, i, X):
-    """Map V_i x T' volumes of held subject ``i`` into the shared space: W_i^T (X - mu_i)."""
+def _model_arrays(model, i):
+    """(W_i, mu_i) of a fitted model on the device; IndexError like list indexing."""
     torch = _torch()
+    if not -len(model.W) <= i < len(model.W):
+        raise IndexError(f"subject index {i} out of range for {len(model.W)} held subjects")
     w = _dev(model.W[i], torch.float64)
-    mu = _dev(model.mu[i], torch.float64).reshape(-1, 1)
-    x = _dev(X, torch.float64)
-    if x.dim() == 1:
+    mu = _dev(model.mu[i], torch.float64).reshape(-1)
+    return w, mu
+
+
+def _project_dev(model, i, X):
+    torch = _torch()
+    lib = _lib.load()
+    w, mu = _model_arrays(model, i)
+    x = X if isinstance(X, torch.Tensor) else np.asarray(X)
+    if x.ndim == 1:
         x = x.reshape(-1, 1)
-    return _gemm_tn(w, (x - mu).contiguous())
+    v, k = w.shape
+    if x.shape[0] != v:
+        raise ShapeError(f"subject {i} has {v} voxels, got volumes of {x.shape[0]}")
+    xd = _dev(x)
+    t = xd.shape[1]
+    out = torch.empty((k, t), dtype=torch.float64, device=w.device)
+    ws, nb = _workspace(v, k, t)
+    dt = _lib.SRM_F64 if xd.dtype == torch.float64 else _lib.SRM_F32
+    _lib.check(lib.srm_project(_ptr(w), _ld(w), _ptr(xd), dt, _ld(xd), _ptr(mu), v, k, t, _ptr(out), t,
+                               _ptr(ws), nb, _stream()), "project")
+    return out
+
+
+def project_batch(model, i, X):
+    """Map V_i x T' volumes of held subject ``i`` into the shared space:
+    W_i^T (X - mu_i) (srm.py:330-333 over a block of columns; K x T')."""
+    return _project_dev(model, i, X).cpu().numpy()
+
+
+def map_between_batch(model, i, j, X):
+    """Map V_i x T' volumes of subject ``i`` into subject ``j``'s voxel space:
+    W_j W_i^T (X - mu_i) + mu_j (srm.py:336-338 over a block; V_j x T')."""
+    torch = _torch()
+    lib = _lib.load()
+    z = _project_dev(model, i, X)
+    wj, muj = _model_arrays(model, j)
+    vj, k = wj.shape
+    t = z.shape[1]
+    out = torch.empty((vj, t), dtype=torch.float64, device=wj.device)
+    _lib.check(lib.srm_unproject(_ptr(wj), _ld(wj), _ptr(z), _ld(z), _ptr(muj), vj, k, t, _ptr(out), t,
+                                 _stream()), "map_between")
+    return out.cpu().numpy()
 
 
 def project(model, i, x):
     """Map one volume of held subject ``i`` into the shared space (srm.py:330-333)."""
     torch = _torch()
-    xv = _dev(np.asarray(x, dtype=np.float64).ravel() if not isinstance(x, torch.Tensor) else x.reshape(-1),
-              torch.float64)
-    return project_batch(model, i, xv.reshape(-1, 1)).reshape(-1).cpu().numpy()
+    xv = x.reshape(-1) if isinstance(x, torch.Tensor) else np.asarray(x, dtype=np.float64).ravel()
+    return project_batch(model, i, xv.reshape(-1, 1)).reshape(-1)
 
 
 def map_between(model, i, j, x):
     """Map a volume of subject ``i`` into subject ``j``'s voxel space (srm.py:336-338)."""
     torch = _torch()
-    z = project_batch(model, i, _dev(np.asarray(x, dtype=np.float64).ravel()).reshape(-1, 1))
-    wj = _dev(model.W[j], torch.float64)
-    out = _gemm_nt(wj, z.t().contiguous())  # W_j z (V_j x 1)
-    return (out.reshape(-1) + _dev(model.mu[j], torch.float64)).cpu().numpy()
+    xv = x.reshape(-1) if isinstance(x, torch.Tensor) else np.asarray(x, dtype=np.float64).ravel()
+    return map_between_batch(model, i, j, xv.reshape(-1, 1)).reshape(-1)

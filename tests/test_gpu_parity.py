@@ -646,3 +646,63 @@ def test_rank_deficient_fit_raises_like_reference(srm, algorithm):
         orc.run_em(xs, 5, 6, seed=0)
     with pytest.raises(RankError):
         srm.fit(_subjects(srm, xs), srm.SrmConfig(k=5, iterations=6, seed=0), algorithm=algorithm)
+
+
+# --------------------------------------------------------------------------
+# transforms over blocks of volumes (srm.py:330-338)
+# --------------------------------------------------------------------------
+
+def test_project_and_map_between_blocks(srm):
+    g = load_golden("em_ragged")
+    xs = golden_subjects(g)
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=int(g["k"]), iterations=4, seed=0))
+    rng = np.random.default_rng(21)
+    for i, j in [(0, 1), (2, 0), (1, 1)]:
+        X = xs[i][:, :17] + rng.standard_normal((xs[i].shape[0], 17))
+        ref_z = m.W[i].T @ (X - m.mu[i][:, None])
+        z = srm.project_batch(m, i, X)
+        assert z.shape == ref_z.shape and nrel(z, ref_z) <= 1e-14
+        ref_y = m.W[j] @ ref_z + m.mu[j][:, None]
+        y = srm.map_between_batch(m, i, j, X)
+        assert y.shape == (xs[j].shape[0], 17) and nrel(y, ref_y) <= 1e-14
+        # the single-volume API is the one-column case
+        for c in (0, 16):
+            assert nrel(srm.project(m, i, X[:, c]), ref_z[:, c]) <= 1e-14
+            assert nrel(srm.map_between(m, i, j, X[:, c]), ref_y[:, c]) <= 1e-14
+    # the mean of a subject projects to exactly zero (test_srm.py:343-345), in every column
+    z = srm.project_batch(m, 1, np.repeat(m.mu[1][:, None], 5, axis=1))
+    assert np.max(np.abs(z)) == 0.0
+    # fp32 volumes are widened to fp64 before the centering, as np.asarray(x, float64)
+    X32 = xs[0][:, :9].astype(np.float32)
+    ref = m.W[0].T @ (X32.astype(np.float64) - m.mu[0][:, None])
+    assert nrel(srm.project_batch(m, 0, X32), ref) <= 1e-14
+    # a long block (T' = 700 > one 128-column tile, > 64-column GEMM tiles)
+    X = rng.standard_normal((xs[2].shape[0], 700))
+    y = srm.map_between_batch(m, 2, 3, X)
+    assert nrel(y, m.W[3] @ (m.W[2].T @ (X - m.mu[2][:, None])) + m.mu[3][:, None]) <= 1e-14
+    with pytest.raises(IndexError):
+        srm.project_batch(m, 4, X)
+    with pytest.raises(IndexError):
+        srm.map_between_batch(m, 0, -5, xs[0])
+    from paper_1608_04647_b200.errors import ShapeError
+    with pytest.raises(ShapeError):
+        srm.project_batch(m, 0, np.zeros((3, 2)))
+
+
+def test_transform_reference_cases(srm):
+    """test_srm.py:334-367 restated: the square mapping round-trips, the tall
+    mapping is idempotent."""
+    from paper_1608_04647_b200 import kernels
+
+    rng = np.random.default_rng(15)
+    k = 4
+    w_true = kernels.polar_orthogonal(rng.standard_normal((k, k)))
+    X = w_true @ rng.standard_normal((k, 9))
+    model = srm.fit([srm.SubjectData("s0", X)], srm.SrmConfig(k=k, iterations=3, seed=4))
+    x = rng.standard_normal(k)
+    assert np.max(np.abs(srm.map_between(model, 0, 0, x) - x)) <= 1e-10
+    g = load_golden("em_small")
+    m = srm.fit(_subjects(srm, golden_subjects(g)), srm.SrmConfig(k=int(g["k"]), iterations=5, seed=2))
+    x = rng.standard_normal(m.W[0].shape[0])
+    once = srm.map_between(m, 0, 0, x)
+    assert np.max(np.abs(srm.map_between(m, 0, 0, once) - once)) <= 1e-10

@@ -103,38 +103,40 @@ def test_gloo_two_ranks_communicator_and_ordered_exchange():
     assert res[0][6] == [[3.0, 3.0, 3.0]] and res[1][6] is None
 
 
-def _fit_worker(rank, world, port, out, algorithm):
+def _dataset(name):
+    from conftest import load_golden, golden_subjects
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    if name == "recipe5":  # 5 subjects over 2 ranks: shards [3, 2] (cli.py:82-85)
+        xs, _, _ = recipe_numpy(5, 700, 90, 6, seed=19)
+        xs = [x[: 700 - 37 * i] for i, x in enumerate(xs)]
+        return xs, 6, 5, 4
+    g = load_golden(name)
+    return golden_subjects(g), int(g["k"]), int(g["iterations"]), int(g["seed"])
+
+
+def _fit_worker(rank, world, port, out, algorithm, data="em_ragged", ordered=None):
     import torch.distributed as dist
 
-    from conftest import load_golden, golden_subjects
     from paper_1608_04647_b200 import srm
     from paper_1608_04647_b200.collectives import TorchCommunicator, shard_bounds
 
     _init(rank, world, port)
-    g = load_golden("em_ragged")
-    xs = golden_subjects(g)
+    xs, k, iters, seed = _dataset(data)
     a, b = shard_bounds(len(xs), world, rank)
+    engines = []
     m = srm.fit([srm.SubjectData(f"s{i}", xs[i]) for i in range(a, b)],
-                srm.SrmConfig(k=int(g["k"]), iterations=int(g["iterations"]), seed=int(g["seed"])),
-                TorchCommunicator(), algorithm=algorithm)
-    out.put((rank, m.S, m.W, m.rho2, m.rho0, m.sigma_s, m.rho2_all, m.subject_indices))
+                srm.SrmConfig(k=k, iterations=iters, seed=seed),
+                TorchCommunicator(), algorithm=algorithm, ordered=ordered, engine_out=engines)
+    out.put((rank, m.S, m.W, m.rho2, m.rho0, m.sigma_s, m.rho2_all, m.subject_indices, engines[-1].ordered))
     dist.destroy_process_group()
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("algorithm", ["stream", "gram"])
-def test_two_rank_fit_bit_identical_to_serial(algorithm):
-    from conftest import load_golden, golden_subjects
-    from paper_1608_04647_b200 import srm
-
-    g = load_golden("em_ragged")
-    xs = golden_subjects(g)
-    cfg = srm.SrmConfig(k=int(g["k"]), iterations=int(g["iterations"]), seed=int(g["seed"]))
-    serial = srm.fit([srm.SubjectData(f"s{i}", x) for i, x in enumerate(xs)], cfg, algorithm=algorithm)
+def _two_ranks(algorithm, data="em_ragged", ordered=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_fit_worker, args=(r, 2, port, q, algorithm)) for r in range(2)]
+    procs = [ctx.Process(target=_fit_worker, args=(r, 2, port, q, algorithm, data, ordered)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}
@@ -144,9 +146,32 @@ def test_two_rank_fit_bit_identical_to_serial(algorithm):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    _, S0, W0, r0, rho0_0, sig0, all0, idx0 = res[0]
-    _, S1, W1, r1, rho0_1, sig1, all1, idx1 = res[1]
-    assert idx0 == [0, 1] and idx1 == [2, 3]
+    return res
+
+
+def _serial(data, algorithm):
+    from paper_1608_04647_b200 import srm
+
+    xs, k, iters, seed = _dataset(data)
+    return srm.fit([srm.SubjectData(f"s{i}", x) for i, x in enumerate(xs)],
+                   srm.SrmConfig(k=k, iterations=iters, seed=seed), algorithm=algorithm)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algorithm", ["stream", "gram"])
+@pytest.mark.parametrize("data", ["em_ragged", "recipe5"])
+def test_two_rank_fit_bit_identical_to_serial(algorithm, data):
+    """Ordered exchange (the all-gathered term table summed in ascending
+    global subject order on every rank, srm.py:193-213): equal shards [2, 2]
+    take the identity-order reduction, uneven shards [3, 2] the order table
+    of k_reduce_terms; both bit-identical to the serial fit."""
+    serial = _serial(data, algorithm)
+    res = _two_ranks(algorithm, data)
+    _, S0, W0, r0, rho0_0, sig0, all0, idx0, ord0 = res[0]
+    _, S1, W1, r1, rho0_1, sig1, all1, idx1, ord1 = res[1]
+    assert ord0 and ord1
+    n0 = 2 if data == "em_ragged" else 3
+    assert idx0 == list(range(n0)) and idx1 == list(range(n0, n0 + len(W1)))
     assert np.array_equal(S0, serial.S) and np.array_equal(S1, serial.S)
     for i, w in enumerate(W0 + W1):
         assert np.array_equal(w, serial.W[i])
@@ -154,3 +179,107 @@ def test_two_rank_fit_bit_identical_to_serial(algorithm):
     assert rho0_0 == serial.rho0 == rho0_1
     assert np.array_equal(sig0, serial.sigma_s) and sig1 is None and all1 is None
     assert np.array_equal(all0, serial.rho2_all)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algorithm", ["stream", "gram"])
+def test_two_rank_unordered_exchange_matches_serial(algorithm):
+    """ordered=False (the exchange large subject counts take: each rank's
+    partial sum, srm_reduce_local, then one all-reduce of [K x T | scalars]):
+    the grouping changes the rounding only -- within 1e-12 of serial -- and
+    both ranks hold the identical S."""
+    from conftest import nrel
+
+    serial = _serial("recipe5", algorithm)
+    res = _two_ranks(algorithm, "recipe5", ordered=False)
+    _, S0, W0, r0, rho0_0, sig0, all0, _, ord0 = res[0]
+    _, S1, W1, r1, rho0_1, _, _, _, ord1 = res[1]
+    assert not ord0 and not ord1
+    assert np.array_equal(S0, S1) and rho0_0 == rho0_1
+    assert nrel(S0, serial.S) <= 1e-12 and nrel(sig0, serial.sigma_s) <= 1e-12
+    assert nrel(r0 + r1, serial.rho2) <= 1e-12 and nrel(all0, serial.rho2_all) <= 1e-12
+    for w, ws in zip(W0 + W1, serial.W):
+        assert nrel(w, ws) <= 1e-12
+
+
+class _Hub:
+    """In-process rendezvous of a thread group (the reference's _ThreadHub idea)."""
+
+    def __init__(self, size):
+        import threading
+
+        self.size = size
+        self.barrier = threading.Barrier(size)
+        self.slots = [None] * size
+
+
+class ProtocolComm:
+    """Only the reference protocol (collectives.py:94-176): rank, size,
+    gather(bytes) -> list on root, broadcast(2-D float64 on root) -> array,
+    barrier(), stats.  No device collectives."""
+
+    def __init__(self, hub, rank):
+        from paper_1608_04647_b200.collectives import CollectiveStats
+
+        self.hub, self.rank, self.size = hub, rank, hub.size
+        self.stats = CollectiveStats()
+
+    def gather(self, local):
+        self.hub.slots[self.rank] = bytes(local)
+        self.hub.barrier.wait()
+        out = list(self.hub.slots) if self.rank == 0 else None
+        self.hub.barrier.wait()
+        self.stats.gather_calls += 1
+        return out
+
+    def broadcast(self, buf):
+        if self.rank == 0:
+            self.hub.slots[0] = np.array(buf, dtype=np.float64, copy=True)
+        self.hub.barrier.wait()
+        out = np.array(self.hub.slots[0], copy=True)
+        self.hub.barrier.wait()
+        self.stats.bcast_calls += 1
+        return out
+
+    def barrier(self):
+        self.hub.barrier.wait()
+
+
+@pytest.mark.gpu
+def test_protocol_only_communicator_fit_bit_identical():
+    """Two worker threads fitting through a communicator that only speaks the
+    reference protocol (gather + broadcast of host bytes, as factorfit's
+    thread / socket backends): bit-identical to the serial fit."""
+    import threading
+
+    from paper_1608_04647_b200 import srm
+    from paper_1608_04647_b200.collectives import shard_bounds
+
+    xs, k, iters, seed = _dataset("recipe5")
+    cfg = srm.SrmConfig(k=k, iterations=iters, seed=seed)
+    serial = srm.fit([srm.SubjectData(f"s{i}", x) for i, x in enumerate(xs)], cfg, algorithm="gram")
+    hub = _Hub(2)
+    models, errors = [None, None], []
+
+    def worker(rank):
+        try:
+            a, b = shard_bounds(len(xs), 2, rank)
+            models[rank] = srm.fit([srm.SubjectData(f"s{i}", xs[i]) for i in range(a, b)], cfg,
+                                   ProtocolComm(hub, rank), algorithm="gram")
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+            hub.barrier.abort()
+
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    m0, m1 = models
+    assert np.array_equal(m0.S, serial.S) and np.array_equal(m1.S, serial.S)
+    for w, ws in zip(m0.W + m1.W, serial.W):
+        assert np.array_equal(w, ws)
+    assert m0.rho2 + m1.rho2 == serial.rho2
+    assert np.array_equal(m0.sigma_s, serial.sigma_s) and m1.sigma_s is None
+    assert np.array_equal(m0.rho2_all, serial.rho2_all)
