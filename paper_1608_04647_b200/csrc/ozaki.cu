@@ -84,19 +84,24 @@ __device__ __forceinline__ double round_shift(double y, int* low) {
 }
 
 // nsl slices per value (7 for fp64 X-hat, 4 for fp32); records of `rec` bytes
-// (256: eight 32-voxel slots; 128: four), slots beyond nsl zero
-template <typename TX, int NSL>
+// (256: eight 32-voxel slots; 128: four), slots beyond nsl zero.  NB
+// consecutive 32-voxel blocks per CTA, so every column's records go out as one
+// contiguous NB x rec-byte run (fp32's 128-byte records alone are too short a
+// DRAM burst at the lq stride between columns: 0.35 of HBM with NB = 1)
+template <typename TX, int NSL, int NB>
 __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restrict__ xhat,
                                                   const unsigned long long* __restrict__ cmax,
                                                   int8_t* __restrict__ q, int64_t lq, int32_t* __restrict__ expo) {
   constexpr int nsl = NSL;
   constexpr int rec = NSL <= 4 ? 128 : 256;
+  static_assert(NB * rec <= 256, "a column's NB records must fit one shared-memory row");
   __shared__ __align__(16) uint32_t buf[kSplitCols * kSplitLdw];
   const int i = blockIdx.z;
   const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
   const int64_t row0 = sj[SC_ROW_OFF], V = sj[SC_V];
-  const int64_t vb = blockIdx.x;
-  if (vb * 32 >= V) return;
+  const int64_t vb0 = (int64_t)blockIdx.x * NB;
+  if (vb0 * 32 >= V) return;
+  const int nb = (int)min((int64_t)NB, (V + 31) / 32 - vb0);  // blocks of this subject in the CTA
   const int64_t t0 = (int64_t)blockIdx.y * kSplitCols;
   const int tl = threadIdx.x & (kSplitCols - 1), quarter = threadIdx.x / kSplitCols;
   const int64_t t = t0 + tl;
@@ -105,71 +110,182 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
   if (tin) {
     const double m = __longlong_as_double((long long)cmax[(int64_t)i * p.ldx + t]);
     e = (m > 0.0) ? frexp_exp(m) : 0;
-    if (vb == 0 && quarter == 0) expo[(int64_t)i * p.ldx + t] = e;
+    if (vb0 == 0 && quarter == 0) expo[(int64_t)i * p.ldx + t] = e;
   }
-  TX xv[8];
+  TX xv[NB][8];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int64_t v = vb * 32 + quarter * 8 + u;
-    xv[u] = (tin && v < V) ? xhat[(row0 + v) * p.ldx + t] : TX(0);
-  }
-  uint32_t w[NSL][2];
-#pragma unroll
-  for (int s = 0; s < NSL; ++s)
-#pragma unroll
-    for (int g = 0; g < 2; ++g) w[s][g] = 0u;
-  // y = x 2^(6 - e), |y| < 64; digit s = rint(y), then y = (y - rint(y)) * 128.
-  // Every step is exact in the input's own precision, so fp32 X-hat slices in
-  // fp32 arithmetic (twice the fp64 rate) with the same digits as in fp64.
-  bool done = false;
-  if constexpr (sizeof(TX) == 4) {
-    if (e >= -120 && e <= 130) {  // 2^(6 - e) is a normal float
-      const float scale = __int_as_float((127 + 6 - e) << 23);
-      const float magic = 12582912.0f;  // 1.5 * 2^23: rint for |y| < 2^22, low byte = digit
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        float y = xv[u] * scale;
-#pragma unroll
-        for (int s = 0; s < NSL; ++s) {
-          const float tt = y + magic;
-          w[s][u >> 2] |= (uint32_t)(__float_as_int(tt) & 0xFF) << (8 * (u & 3));
-          y = (y - (tt - magic)) * 128.0f;
-        }
-      }
-      done = true;
-    }
-  }
-  if (!done) {
-    // 2^(6 - e) exactly (normal range: |e| < 1000)
-    const double scale = __longlong_as_double((long long)(1023 + 6 - e) << 52);
+  for (int j = 0; j < NB; ++j)
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      double y = to_f64(xv[u]) * scale;  // |y| < 64
-#pragma unroll
-      for (int s = 0; s < NSL; ++s) {
-        int low;
-        const double r = round_shift(y, &low);
-        w[s][u >> 2] |= (uint32_t)(low & 0xFF) << (8 * (u & 3));
-        y = (y - r) * 128.0;  // exact: |y - r| <= 1/2
-      }
+      const int64_t v = (vb0 + j) * 32 + quarter * 8 + u;
+      xv[j][u] = (tin && v < V) ? xhat[(row0 + v) * p.ldx + t] : TX(0);
     }
-  }
-  // record layout per t: slot s = 8 words (32 voxels), this quarter's 8 voxels
-  // at words 2 quarter, 2 quarter + 1 (slots >= nsl: zero in smem, not stored)
   uint2* row = reinterpret_cast<uint2*>(buf + tl * kSplitLdw);
   const int nslot = rec / 32;
 #pragma unroll
-  for (int s = 0; s < 8; ++s)
-    if (s < nslot) row[s * 4 + quarter] = (s < nsl) ? make_uint2(w[s][0], w[s][1]) : make_uint2(0u, 0u);
+  for (int j = 0; j < NB; ++j) {
+    uint32_t w[NSL][2];
+#pragma unroll
+    for (int s = 0; s < NSL; ++s)
+#pragma unroll
+      for (int g = 0; g < 2; ++g) w[s][g] = 0u;
+    // y = x 2^(6 - e), |y| < 64; digit s = rint(y), then y = (y - rint(y)) * 128.
+    // Every step is exact in the input's own precision, so fp32 X-hat slices in
+    // fp32 arithmetic (twice the fp64 rate) with the same digits as in fp64.
+    bool done = false;
+    if constexpr (sizeof(TX) == 4) {
+      if (e >= -120 && e <= 130) {  // 2^(6 - e) is a normal float
+        const float scale = __int_as_float((127 + 6 - e) << 23);
+        const float magic = 12582912.0f;  // 1.5 * 2^23: rint for |y| < 2^22, low byte = digit
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float y = xv[j][u] * scale;
+#pragma unroll
+          for (int s = 0; s < NSL; ++s) {
+            const float tt = y + magic;
+            w[s][u >> 2] |= (uint32_t)(__float_as_int(tt) & 0xFF) << (8 * (u & 3));
+            y = (y - (tt - magic)) * 128.0f;
+          }
+        }
+        done = true;
+      }
+    }
+    if (!done) {
+      // 2^(6 - e) exactly (normal range: |e| < 1000)
+      const double scale = __longlong_as_double((long long)(1023 + 6 - e) << 52);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        double y = to_f64(xv[j][u]) * scale;  // |y| < 64
+#pragma unroll
+        for (int s = 0; s < NSL; ++s) {
+          int low;
+          const double r = round_shift(y, &low);
+          w[s][u >> 2] |= (uint32_t)(low & 0xFF) << (8 * (u & 3));
+          y = (y - r) * 128.0;  // exact: |y - r| <= 1/2
+        }
+      }
+    }
+    // record layout per t: slot s = 8 words (32 voxels), this quarter's 8 voxels
+    // at words 2 quarter, 2 quarter + 1 (slots >= nsl: zero in smem, not stored);
+    // block j's record at byte j * rec of the column's row
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      if (s < nslot) row[j * (rec / 8) + s * 4 + quarter] = (s < nsl) ? make_uint2(w[s][0], w[s][1]) : make_uint2(0u, 0u);
+  }
   __syncthreads();
-  // kSplitCols rows x rec / 16 chunks of 16 bytes; consecutive threads write one
-  // record.  Slot 7 of a seven-slice record is never read by an MMA: not written.
-  const int nch = nsl == 7 ? 14 : rec / 16;
+  // kSplitCols rows x nb x rec / 16 chunks of 16 bytes; consecutive threads write
+  // one column's run.  Slot 7 of a seven-slice record is never read by an MMA:
+  // not written (NB = 1 there).
+  const int nch = nsl == 7 ? 14 : nb * rec / 16;
   for (int c = threadIdx.x; c < kSplitCols * nch; c += blockDim.x) {
     const int r = c / nch, k = c % nch;
     const int64_t tt = t0 + r;
     if (tt < p.ldx) {
-      uint4* dst = reinterpret_cast<uint4*>(q + ((int64_t)i * p.ldx + tt) * lq + vb * rec);
+      uint4* dst = reinterpret_cast<uint4*>(q + ((int64_t)i * p.ldx + tt) * lq + vb0 * rec);
+      dst[k] = reinterpret_cast<const uint4*>(buf + r * kSplitLdw)[k];
+    }
+  }
+}
+
+// fp32 X-hat: the four slices from one integer per value.  N = rint(x 2^(27-e))
+// (|N| <= 2^27; the same 2^-27-of-the-column-max truncation as the digit
+// recurrence above) is cut into balanced base-128 digits, least significant
+// first: d = sext7(N), N = (N - d) >> 7 -- integer ops instead of a float
+// round/subtract/scale chain per digit, and four voxels' digits are packed
+// with byte permutes.  The reconstructed value sum_s q_s 2^{-7s} equals the
+// recurrence's except for which way an exact tie rounds.  Full tiles (the
+// common case) skip the per-value bounds checks.
+template <int NB>
+__global__ void __launch_bounds__(256) k_oz_split_f32(DevPlan p, const float* __restrict__ xhat,
+                                                      const unsigned long long* __restrict__ cmax,
+                                                      int8_t* __restrict__ q, int64_t lq, int32_t* __restrict__ expo) {
+  constexpr int rec = 128;
+  __shared__ __align__(16) uint32_t buf[kSplitCols * kSplitLdw];
+  const int i = blockIdx.z;
+  const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
+  const int64_t row0 = sj[SC_ROW_OFF], V = sj[SC_V];
+  const int64_t vb0 = (int64_t)blockIdx.x * NB;
+  if (vb0 * 32 >= V) return;
+  const int64_t ldx = p.ldx;
+  const int nb = (int)min((int64_t)NB, (V + 31) / 32 - vb0);
+  const int64_t t0 = (int64_t)blockIdx.y * kSplitCols;
+  const int tl = threadIdx.x & (kSplitCols - 1), quarter = threadIdx.x / kSplitCols;
+  const int64_t t = t0 + tl;
+  const bool tin = t < ldx;
+  int e = 0;
+  if (tin) {
+    const double m = __longlong_as_double((long long)cmax[(int64_t)i * ldx + t]);
+    e = (m > 0.0) ? frexp_exp(m) : 0;
+    if (vb0 == 0 && quarter == 0) expo[(int64_t)i * ldx + t] = e;
+  }
+  float xv[NB][8];
+  const float* px = xhat + (row0 + vb0 * 32 + quarter * 8) * ldx + t;
+  if (tin && (vb0 + NB) * 32 <= V) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[j][u] = px[(int64_t)(j * 32 + u) * ldx];
+  } else {
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t v = (vb0 + j) * 32 + quarter * 8 + u;
+        xv[j][u] = (tin && v < V) ? px[(int64_t)(j * 32 + u) * ldx] : 0.f;
+      }
+  }
+  // N = rint(x 2^(27 - e)): the scale as a float when it is a normal one
+  // (|e| of any fp32 column maximum short of the tiny / huge extremes), else fp64
+  int nv[NB][8];
+  if (e >= -100 && e <= 153) {
+    const float sf = __int_as_float((127 + 27 - e) << 23);
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) nv[j][u] = __float2int_rn(xv[j][u] * sf);
+  } else {
+    const double sd = ldexp(1.0, 27 - e);
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) nv[j][u] = __double2int_rn((double)xv[j][u] * sd);
+  }
+  uint2* row = reinterpret_cast<uint2*>(buf + tl * kSplitLdw);
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    int dg[4][8];  // [slice][voxel]
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      // balanced base-128 digits, least significant first: with n' = (n + 64) >> 7
+      // the digit n - 128 n' lies in [-64, 63]
+      int n = nv[j][u];
+#pragma unroll
+      for (int sl = 3; sl >= 1; --sl) {
+        const int n1 = (n + 64) >> 7;
+        dg[sl][u] = n - (n1 << 7);
+        n = n1;
+      }
+      dg[0][u] = n;  // |n| <= 64
+    }
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) {
+      uint32_t w[2];
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const uint32_t lo = __byte_perm((uint32_t)dg[sl][4 * g], (uint32_t)dg[sl][4 * g + 1], 0x0040);
+        const uint32_t hi = __byte_perm((uint32_t)dg[sl][4 * g + 2], (uint32_t)dg[sl][4 * g + 3], 0x0040);
+        w[g] = __byte_perm(lo, hi, 0x5410);
+      }
+      row[j * (rec / 8) + sl * 4 + quarter] = make_uint2(w[0], w[1]);
+    }
+  }
+  __syncthreads();
+  const int nch = nb * rec / 16;
+  for (int c = threadIdx.x; c < kSplitCols * nch; c += blockDim.x) {
+    const int r = c / nch, k = c - r * nch;
+    const int64_t tt = t0 + r;
+    if (tt < ldx) {
+      uint4* dst = reinterpret_cast<uint4*>(q + ((int64_t)i * ldx + tt) * lq + vb0 * rec);
       dst[k] = reinterpret_cast<const uint4*>(buf + r * kSplitLdw)[k];
     }
   }
@@ -1124,11 +1240,13 @@ cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first,
   const unsigned long long* cm = cmax + (int64_t)first * p.ldx;
   int8_t* qs = q + (int64_t)first * p.ldx * lq;
   int32_t* ex = expo + (int64_t)first * p.ldx;
-  const dim3 g2((unsigned)((max_v + 31) / 32), (unsigned)((p.ldx + kSplitCols - 1) / kSplitCols), (unsigned)count);
+  const unsigned gy = (unsigned)((p.ldx + kSplitCols - 1) / kSplitCols);
   if (x_dtype == SRM_F64)
-    k_oz_split<double, 7><<<g2, 256, 0, st>>>(sub, static_cast<const double*>(p.xhat), cm, qs, lq, ex);
-  else
-    k_oz_split<float, 4><<<g2, 256, 0, st>>>(sub, static_cast<const float*>(p.xhat), cm, qs, lq, ex);
+    k_oz_split<double, 7, 1><<<dim3((unsigned)((max_v + 31) / 32), gy, (unsigned)count), 256, 0, st>>>(
+        sub, static_cast<const double*>(p.xhat), cm, qs, lq, ex);
+  else  // two 128-byte records per column per CTA: 256-byte runs
+    k_oz_split_f32<2><<<dim3((unsigned)((max_v + 63) / 64), gy, (unsigned)count), 256, 0, st>>>(
+        sub, static_cast<const float*>(p.xhat), cm, qs, lq, ex);
   return cudaGetLastError();
 }
 
