@@ -159,8 +159,11 @@ int srm_plan_region(const srm_plan* plan, int region, int64_t* offset, int64_t* 
  *   modified (srm.py:98 returns a copy).
  * srm_init_mapping: srm.py:101-113 `init_subject` after the host RNG draw
  *   (the N(0,1) matrix, PCG64-seeded as the reference, is written to
- *   SRM_R_AMAT first): polar factor via Gram + Jacobi eigensolver, and the
- *   first E-step term W_i^T X_i (srm.py:116-118) with rho_i^2 = 1.
+ *   SRM_R_AMAT first): polar transform of the draw, and the first E-step term
+ *   W_i^T X_i = M_0^T (G^T X_i) (srm.py:116-118) with rho_i^2 = 1.  On int8
+ *   Gram plans G^T X_i runs on the int8 tensor cores from seven-slice records
+ *   of G and the slices of X-hat (srm_prepare_gram_range is enqueued first for
+ *   any subject it has not covered yet).
  */
 int srm_load_subject(srm_plan* plan, int local_index, const void* x, int x_dtype,
                      int64_t ld, void* stream);

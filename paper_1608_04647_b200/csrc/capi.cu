@@ -85,6 +85,9 @@ enum Internal {
   I_QRJOBS,
   I_SVDJOBS,
   I_NSG,
+  I_OZGIEXP,
+  I_OZGICMAX,
+  I_ITEMS_TN,
   I_COUNT
 };
 
@@ -143,6 +146,10 @@ struct srm_plan {
   TmaMap tm_g, tm_sq;
   bool oz_w = false;                  // final W = Xhat R from the int8 slices (needs oz_sg)
   std::vector<OzItem> items_ow;       // 128-voxel tiles of the final int8 W = Xhat R
+  std::vector<OzItem> items_tn;       // (subject, 128-TR tile) of the int8 init term B_0 = G^T Xhat
+  int64_t oz_lqg_init = 0;            // bytes per sliced row (feature) of the init draw G (records in WOUT)
+  TmaMap tm_gi;
+  std::vector<char> sliced;           // srm_prepare_gram_range has been enqueued for the subject
   std::vector<int> ow_first;          // [n_local + 1]: first items_ow entry of each subject
   TmaMap tm_q32, tm_r;
   bool sk_off = false;                // SRM_B200_SG_PER_TILE=1: per-tile B = S G / 2 (test knob)
@@ -164,7 +171,8 @@ void layout(srm_plan* p) {
   int64_t sz[I_COUNT] = {0};
   sz[SRM_R_XHAT] = p->rows_total * p->ldx * esize(p->dtype);
   sz[SRM_R_AMAT] = p->rows_total * p->kp * 8;
-  sz[SRM_R_WOUT] = p->rows_total * p->K * 8;
+  // W_i (final) -- and, on int8 Gram plans, the slices of the init draw G before it
+  sz[SRM_R_WOUT] = std::max(p->rows_total * p->K * 8, (int64_t)p->n_local * p->K * p->oz_lqg_init);
   sz[SRM_R_MU] = p->rows_total * 8;
   sz[SRM_R_TERMS] = (int64_t)p->n_slots * term_stride * 8;
   sz[SRM_R_RED] = red_stride * 8;
@@ -226,6 +234,9 @@ void layout(srm_plan* p) {
   sz[I_QRJOBS] = exact ? (int64_t)p->qr.levels.size() * p->n_local * (int64_t)sizeof(QrJob) : 0;
   sz[I_SVDJOBS] = exact ? (int64_t)p->n_local * (int64_t)sizeof(SvdJob) : 0;
   sz[I_NSG] = ns_polar_g_supported((int)p->kp) ? (int64_t)p->n_local * 4 * kp2 * 8 : 0;
+  sz[I_OZGIEXP] = p->oz_lqg_init ? (int64_t)p->n_local * p->K * 4 : 0;
+  sz[I_OZGICMAX] = p->oz_lqg_init ? (int64_t)p->n_local * p->K * 8 : 0;
+  sz[I_ITEMS_TN] = (int64_t)p->items_tn.size() * sizeof(OzItem);
   int64_t cur = 0;
   for (int r = 0; r < I_COUNT; ++r) {
     p->off[r] = cur;
@@ -379,6 +390,15 @@ void build_work(srm_plan* p) {
       for (int64_t m0 = 0; m0 < p->ldx; m0 += 128)
         for (int64_t n0 = m0; n0 < p->ldx; n0 += 128)
           p->items_oz.push_back({i, (int32_t)m0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32)});
+  }
+  // the init E-step term B_0 = G^T Xhat from int8 slices too (with the int8 B = S G)
+  p->items_tn.clear();
+  p->oz_lqg_init = 0;
+  if (p->oz_sg) {
+    p->oz_lqg_init = round_up(std::max<int64_t>(p->max_v, 1), 32) / 32 * 256;
+    for (int i = 0; i < p->n_local; ++i)
+      for (int64_t n0 = 0; n0 < p->ldx; n0 += 128)
+        p->items_tn.push_back({i, 0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32)});
   }
   // tensor-core path: A-pass row tiles (A in the fp32 [rows][np] region) and
   // B-pass tiles of 128 TRs over the same V chunks
@@ -923,6 +943,7 @@ int srm_plan_create(srm_plan** out, int dtype, int n_local, const int64_t* n_vox
   p->rows_total = r;
   build_work(p);
   layout(p);
+  p->sliced.assign(n_local, 0);
   *out = p;
   return SRM_OK;
 }
@@ -999,7 +1020,8 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
              {I_ITEMS_GRAM, p->items_gram.data()},
              {I_ITEMS_BG, p->items_bg.data()},   {I_ITEMS_TB, p->items_tb.data()},
              {I_ITEMS_TA, p->items_ta.data()},   {I_ITEMS_TG, p->items_tg.data()},
-             {I_ITEMS_OZ, p->items_oz.data()},   {I_ITEMS_OW, p->items_ow.data()}};
+             {I_ITEMS_OZ, p->items_oz.data()},   {I_ITEMS_OW, p->items_ow.data()},
+             {I_ITEMS_TN, p->items_tn.data()}};
   for (const Up& u : ups) {
     if (p->size[u.r] == 0) continue;
     e = cudaMemcpy(p->ws + p->off[u.r], u.src, p->size[u.r], cudaMemcpyHostToDevice);
@@ -1071,6 +1093,12 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
         e = launch_oz_sg_sk(p->tm_g, p->tm_sq, nullptr, nullptr, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, 0, 0,
                             p->sk_ctas, 0);
     }
+    if (e == cudaSuccess && p->oz_lqg_init) {
+      e = make_map_q(&p->tm_gi, region<int8_t>(p, SRM_R_WOUT), p->oz_lqg_init, p->K, p->n_local, 128);
+      if (e == cudaSuccess)
+        e = launch_oz_tn(p->tm_gi, p->tm_q, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, p->K, nullptr, 0,
+                         p->oz_nsl, 0);
+    }
     if (e == cudaSuccess && p->oz_w) {
       e = make_map_q5(&p->tm_q32, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, p->oz_nsl);
       if (e == cudaSuccess) e = make_map_q8(&p->tm_r, region<int8_t>(p, I_OZR), p->oz_lqg, p->kp, p->n_local);
@@ -1112,12 +1140,36 @@ int srm_init_mapping_range(srm_plan* p, int first, int count, void* stream) {
     ean += p->nchunk[i];
   }
   const bool exact = (p->flags & SRM_FLAG_EXACT_POLAR) != 0;
-  cudaError_t e = launch_contract_e((int)p->kp, SRM_F64, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
-                                    region<ItemE>(p, I_ITEMS_EX) + ex0, (int)exn, st);
+  // B_0 = G^T Xhat: on int8 Gram plans from the slices of G and of Xhat (the
+  // caller has run srm_prepare_gram_range over these subjects), after the
+  // chunk reduction of G^T G; otherwise one more split-V DMMA contraction
+  const bool i8 = p->oz_lqg_init != 0;
+  cudaError_t e = cudaSuccess;
+  if (!i8)
+    e = launch_contract_e((int)p->kp, SRM_F64, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
+                          region<ItemE>(p, I_ITEMS_EX) + ex0, (int)exn, st);
   if (e == cudaSuccess && !exact)  // the Gram route's A^T A of the draw
     e = launch_contract_e((int)p->kp, SRM_F64, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0,
                           region<ItemE>(p, I_ITEMS_EA) + p->chunk0[first], (int)ean, st);
   if (e == cudaSuccess) e = launch_reduce_chunks(d, st);
+  if (e == cudaSuccess && i8) {
+    // Xhat's slices must exist: prepare subjects no srm_prepare_gram_range call
+    // has covered yet (stream order; the loader already does it on this stream)
+    for (int i = first; i < first + count; ++i)
+      if (!p->sliced[i]) {
+        const int rc = srm_prepare_gram_range(p, i, 1, stream);
+        if (rc) return rc;
+      }
+    int64_t maxv = 0;
+    for (int i = first; i < first + count; ++i) maxv = std::max(maxv, p->V[i]);
+    e = launch_oz_init_slices(d, first, count, region<int8_t>(p, SRM_R_WOUT), p->oz_lqg_init,
+                              region<int32_t>(p, I_OZGIEXP), region<unsigned long long>(p, I_OZGICMAX), maxv, st);
+    const int per = (int)((p->ldx + 127) / 128);
+    if (e == cudaSuccess)
+      e = launch_oz_tn(p->tm_gi, p->tm_q, region<int32_t>(p, I_OZGIEXP), region<int32_t>(p, I_OZEXP), d.bred, p->ldx,
+                       p->kp, p->ldo, p->K, region<OzItem>(p, I_ITEMS_TN) + (int64_t)first * per, count * per,
+                       p->oz_nsl, st);
+  }
   if (e == cudaSuccess) e = exact ? launch_exact_polar(p, first, count, true, st) : launch_eig_polar(d, 1, st);
   if (e == cudaSuccess) e = launch_apply_m(d, 0, st);
   if (e == cudaSuccess) e = launch_finalize_rho(d, 1, st);
@@ -1228,6 +1280,7 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
   if (!(p->flags & SRM_FLAG_GRAM)) return SRM_OK;
   if (first < 0 || count < 0 || first + count > p->n_local) return fail(SRM_ERR_CONFIG, "subject range out of bounds");
   if (count == 0) return SRM_OK;
+  for (int i = first; i < first + count; ++i) p->sliced[i] = 1;
   cudaStream_t st = as_stream(stream);
   // int8 Gram of more than one wave of tiles: batches of one wave, the
   // slicing of every batch on the side stream (17 KB CTAs that fit beside the

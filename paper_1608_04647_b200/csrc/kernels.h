@@ -102,6 +102,12 @@ cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* exp
 cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* rexp, double* W, const OzItem* items,
                         int n_items, int64_t ldx, int64_t kp, int64_t K, int nsl, cudaStream_t st);
 size_t oz_gram_smem_bytes();
+// init E-step on the int8 tensor cores: B_i = G_i^T Xhat_i (G = the N(0,1) draw
+// in AMAT) into bred, from G's seven-slice records [i][k][vb] (qg, pitch lqg)
+// and Xhat's nslb-slice records; items = one per (subject, 128-TR tile)
+cudaError_t launch_oz_tn(const TmaMap& tma, const TmaMap& tmb, const int32_t* aexp, const int32_t* bexp, double* bred,
+                         int64_t ldx, int64_t kp, int64_t ldo, int64_t K, const OzItem* items, int n_items, int nslb,
+                         cudaStream_t st);
 // X_i^T X_i tiles from the nsl-slice records (nsl = 7 for fp64 X-hat, 4 for fp32)
 cudaError_t launch_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
                            int n_items, int nsl, cudaStream_t st);

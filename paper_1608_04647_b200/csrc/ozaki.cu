@@ -89,7 +89,7 @@ __device__ __forceinline__ double round_shift(double y, int* low) {
 // contiguous NB x rec-byte run (fp32's 128-byte records alone are too short a
 // DRAM burst at the lq stride between columns: 0.35 of HBM with NB = 1)
 template <typename TX, int NSL, int NB>
-__global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restrict__ xhat,
+__global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restrict__ xhat, int64_t ldsrc, int64_t ncols,
                                                   const unsigned long long* __restrict__ cmax,
                                                   int8_t* __restrict__ q, int64_t lq, int32_t* __restrict__ expo) {
   constexpr int nsl = NSL;
@@ -105,12 +105,12 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
   const int64_t t0 = (int64_t)blockIdx.y * kSplitCols;
   const int tl = threadIdx.x & (kSplitCols - 1), quarter = threadIdx.x / kSplitCols;
   const int64_t t = t0 + tl;
-  const bool tin = t < p.ldx;
+  const bool tin = t < ncols;
   int e = 0;
   if (tin) {
-    const double m = __longlong_as_double((long long)cmax[(int64_t)i * p.ldx + t]);
+    const double m = __longlong_as_double((long long)cmax[(int64_t)i * ncols + t]);
     e = (m > 0.0) ? frexp_exp(m) : 0;
-    if (vb0 == 0 && quarter == 0) expo[(int64_t)i * p.ldx + t] = e;
+    if (vb0 == 0 && quarter == 0) expo[(int64_t)i * ncols + t] = e;
   }
   TX xv[NB][8];
 #pragma unroll
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int64_t v = (vb0 + j) * 32 + quarter * 8 + u;
-      xv[j][u] = (tin && v < V) ? xhat[(row0 + v) * p.ldx + t] : TX(0);
+      xv[j][u] = (tin && v < V) ? xhat[(row0 + v) * ldsrc + t] : TX(0);
     }
   uint2* row = reinterpret_cast<uint2*>(buf + tl * kSplitLdw);
   const int nslot = rec / 32;
@@ -180,8 +180,8 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
   for (int c = threadIdx.x; c < kSplitCols * nch; c += blockDim.x) {
     const int r = c / nch, k = c % nch;
     const int64_t tt = t0 + r;
-    if (tt < p.ldx) {
-      uint4* dst = reinterpret_cast<uint4*>(q + ((int64_t)i * p.ldx + tt) * lq + vb0 * rec);
+    if (tt < ncols) {
+      uint4* dst = reinterpret_cast<uint4*>(q + ((int64_t)i * ncols + tt) * lq + vb0 * rec);
       dst[k] = reinterpret_cast<const uint4*>(buf + r * kSplitLdw)[k];
     }
   }
@@ -500,6 +500,217 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 1) tmem_free(tmem, 512);
+}
+
+// ---------------------------------------------------------------------------
+// B_i = G_i^T Xhat_i on the int8 tensor cores (the E-step term of the initial
+// mapping, srm.py:101-118: W_0 = G M_0, so W_0^T Xhat = M_0^T (G^T Xhat)).
+// The same machinery as k_oz_gram with two record tensors: A = the seven
+// slices of the N(0,1) draw G (records [k][32-voxel block], the draw's column
+// scales), B = Xhat's slices (seven or four) -- one M = 128 feature tile by
+// N = 128 TRs per CTA, contracted over the subject's voxels.  Pairs
+// (s, s') with s + s' <= 6 (all of them for four-slice Xhat); the result goes
+// to the subject's reduced record (bred[i][k][t], row stride ldo) for k < kp.
+// ---------------------------------------------------------------------------
+template <int NSA, int NSB, int P>
+__device__ __forceinline__ void oz_issue_pass_ab(uint32_t tmem, uint64_t da0, uint64_t db0, uint32_t idesc,
+                                                 uint32_t keep) {
+  constexpr int dlo = P ? 4 : 0, dhi = P ? kOzSlices - 1 : 3;
+#pragma unroll
+  for (int d = dlo; d <= dhi; ++d) {
+    const uint32_t acc = tmem + 128u * (uint32_t)(d - dlo);
+    const int s0 = d - (NSB - 1) > 0 ? d - (NSB - 1) : 0, s1 = d < NSA - 1 ? d : NSA - 1;
+#pragma unroll
+    for (int s = s0; s <= s1; ++s)
+      mma_s8(acc, da0 + oz_slice_off(s), db0 + oz_slice_off(d - s), idesc, s == s0 ? keep : 1u);
+  }
+}
+
+struct OzTnArgs {
+  const int32_t* aexp;  // [n_local][K] column exponents of G
+  const int32_t* bexp;  // [n_local][ldx] column exponents of Xhat
+  double* out;          // bred
+  int64_t ldx, kp, ldo, K;
+};
+
+template <int NSB>
+__global__ void __launch_bounds__(kOzThreads, 1) k_oz_tn(const __grid_constant__ CUtensorMap tma,
+                                                         const __grid_constant__ CUtensorMap tmb, OzTnArgs g,
+                                                         const OzItem* __restrict__ items) {
+  constexpr int NSA = kOzSlices;
+  constexpr int recb = NSB <= 4 ? 128 : 256;
+  constexpr int kPasses = 2;
+  extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ OzBars bars;
+  __shared__ uint32_t tmem_base;
+  const OzItem it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nvb = it.nvb;
+  const int nchunks = (nvb + kOzChunkBlocks - 1) / kOzChunkBlocks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < kOzStages; ++s) {
+        mbar_init(&bars.full[s], 1);
+        mbar_init(&bars.empty[s], 1);
+      }
+      mbar_init(&bars.accfull, 1);
+      mbar_init(&bars.accfree, kOzThreads - 64);
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+  } else if (warp == 1) {
+    tmem_alloc(&tmem_base, 512);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int k = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
+        for (int pass = 0; pass < kPasses; ++pass) {
+          // pass 1 reads G's high halves (slices 4-6) and, for seven-slice
+          // Xhat, its high halves too; the low-half pass packs two blocks a stage
+          const bool hi = pass != 0;
+          const int step = hi ? 1 : 2;
+          for (int vb = b0; vb < b1; vb += step, ++k) {
+            const int slot = k % kOzStages;
+            if (k >= kOzStages) mbar_wait(&bars.empty[slot], ((k / kOzStages) - 1) & 1);
+            const int nj = min(step, b1 - vb);
+            const int nbox = hi ? (NSB > 4 ? 4 : 3) : 2 * nj;
+            mbar_expect_tx(&bars.full[slot], (uint32_t)(nbox * kOzBox));
+            unsigned char* st = smem + slot * kOzStageBytes;
+            if (hi) {  // [A lo][A hi][B lo][B hi]
+              tma_load_3d(st, &tma, vb * 256, 0, it.subj, &bars.full[slot]);
+              tma_load_3d(st + kOzBox, &tma, vb * 256 + 128, 0, it.subj, &bars.full[slot]);
+              tma_load_3d(st + 2 * kOzBox, &tmb, vb * recb, it.n0, it.subj, &bars.full[slot]);
+              if (NSB > 4) tma_load_3d(st + 3 * kOzBox, &tmb, vb * recb + 128, it.n0, it.subj, &bars.full[slot]);
+            } else {   // [A lo vb][A lo vb + 1][B lo vb][B lo vb + 1]
+              for (int j = 0; j < nj; ++j) {
+                tma_load_3d(st + j * kOzBox, &tma, (vb + j) * 256, 0, it.subj, &bars.full[slot]);
+                tma_load_3d(st + (2 + j) * kOzBox, &tmb, (vb + j) * recb, it.n0, it.subj, &bars.full[slot]);
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_s8(128, 128);
+      int k = 0, npass = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
+        for (int pass = 0; pass < kPasses; ++pass, ++npass) {
+          if (npass > 0) mbar_wait(&bars.accfree, (npass - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const bool hi = pass != 0;
+          const int step = hi ? 1 : 2;
+          for (int vb = b0; vb < b1; vb += step, ++k) {
+            const int slot = k % kOzStages;
+            mbar_wait(&bars.full[slot], (k / kOzStages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t sa = smem_u32(smem + slot * kOzStageBytes);
+            const uint64_t da0 = umma_desc_sw128(sa), db0 = umma_desc_sw128(sa + 2 * kOzBox);
+            const uint32_t keep = vb == b0 ? 0u : 1u;
+            if (hi) {
+              oz_issue_pass_ab<NSA, NSB, 1>(tmem, da0, db0, idesc, keep);
+            } else {
+              const uint64_t box = (uint64_t)(kOzBox >> 4);
+              oz_issue_pass_ab<NSA, NSB, 0>(tmem, da0, db0, idesc, keep);
+              if (min(step, b1 - vb) > 1) oz_issue_pass_ab<NSA, NSB, 0>(tmem, da0 + box, db0 + box, idesc, 1u);
+            }
+            mma_commit(&bars.empty[slot]);
+          }
+          mma_commit(&bars.accfull);
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2-9, TMEM lanes 32 (warp % 4), 64-column halves ----------------
+    const int quarter = warp & 3;
+    const int cbase = ((warp - 2) >> 2) * 64;
+    const int r = quarter * 32 + lane;  // feature k
+    const bool rin = r < g.kp;
+    const int ea = r < g.K ? g.aexp[(int64_t)it.subj * g.K + r] : 0;
+    const int32_t* ex = g.bexp + (int64_t)it.subj * g.ldx;
+    double* orow = g.out + (int64_t)it.subj * g.kp * g.ldo + (int64_t)r * g.ldo + it.n0;
+    int npass = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      for (int pass = 0; pass < kPasses; ++pass, ++npass) {
+        mbar_wait(&bars.accfull, npass & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int dlo = pass ? 4 : 0, dhi = pass ? kOzSlices - 1 : 3;
+        for (int c0 = cbase; c0 < cbase + 64; c0 += 16) {
+          double prev[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) prev[j] = (npass > 0 && rin && it.n0 + c0 + j < g.ldx) ? orow[c0 + j] : 0.0;
+          uint32_t raw[4][16];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (dlo + q <= dhi) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 128u * (uint32_t)q + c0, raw[q]);
+          tmem_wait_ld();
+          double val[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            long long h = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (dlo + q <= dhi) h = h * 128 + (long long)(int32_t)raw[q][j];
+            val[j] = (double)h * (pass ? 0x1p-54 : 0x1p-33);
+          }
+          if (rin) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int64_t tb = it.n0 + c0 + j;
+              if (tb < g.ldx) {
+                const double v = val[j] * pow2(ea + ex[tb]);
+                orow[c0 + j] = (npass == 0) ? v : prev[j] + v;
+              }
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        mbar_arrive(&bars.accfree);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) tmem_free(tmem, 512);
+}
+
+// column maxima |a[:, c]| of each subject's rows (c < ncols), as IEEE bits: one
+// CTA per 256 rows, eight row groups reduced in shared memory, one atomic per
+// column per CTA
+__global__ void __launch_bounds__(256) k_oz_colmax(DevPlan p, const double* __restrict__ a, int64_t lda, int ncols,
+                                                   unsigned long long* __restrict__ cmax) {
+  __shared__ double red[8][33];
+  const int i = p.sub0 + blockIdx.y;
+  const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
+  const int64_t row0 = sj[SC_ROW_OFF], V = sj[SC_V];
+  const int lane = threadIdx.x & 31, rsub = threadIdx.x >> 5;
+  const int64_t v1 = min(V, (int64_t)(blockIdx.x + 1) * 256);
+  for (int c0 = 0; c0 < ncols; c0 += 32) {
+    const int col = c0 + lane;
+    double m = 0.0;
+    if (col < ncols)
+      for (int64_t v = (int64_t)blockIdx.x * 256 + rsub; v < v1; v += 8) m = fmax(m, fabs(a[(row0 + v) * lda + col]));
+    red[rsub][lane] = m;
+    __syncthreads();
+    if (rsub == 0) {
+      for (int r = 1; r < 8; ++r) m = fmax(m, red[r][lane]);
+      if (col < ncols && m > 0.0)
+        atomicMax(&cmax[(int64_t)i * ncols + col], (unsigned long long)__double_as_longlong(m));
+    }
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1243,7 +1454,7 @@ cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first,
   const unsigned gy = (unsigned)((p.ldx + kSplitCols - 1) / kSplitCols);
   if (x_dtype == SRM_F64)
     k_oz_split<double, 7, 1><<<dim3((unsigned)((max_v + 31) / 32), gy, (unsigned)count), 256, 0, st>>>(
-        sub, static_cast<const double*>(p.xhat), cm, qs, lq, ex);
+        sub, static_cast<const double*>(p.xhat), p.ldx, p.ldx, cm, qs, lq, ex);
   else  // two 128-byte records per column per CTA: 256-byte runs
     k_oz_split_f32<2><<<dim3((unsigned)((max_v + 63) / 64), gy, (unsigned)count), 256, 0, st>>>(
         sub, static_cast<const float*>(p.xhat), cm, qs, lq, ex);
@@ -1269,6 +1480,50 @@ cudaError_t run_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64
 }
 
 }  // namespace
+
+cudaError_t launch_oz_init_slices(const DevPlan& p, int first, int count, int8_t* qg, int64_t lqg, int32_t* expog,
+                                  unsigned long long* cmaxg, int64_t max_v, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const int K = (int)p.K;
+  cudaError_t e = cudaMemsetAsync(cmaxg + (int64_t)first * K, 0, (size_t)count * K * 8, st);
+  if (e != cudaSuccess) return e;
+  DevPlan sub = p;
+  sub.sub0 = first;
+  k_oz_colmax<<<dim3((unsigned)((max_v + 255) / 256), (unsigned)count), 256, 0, st>>>(sub, p.amat, p.kp, K, cmaxg);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  DevPlan sub2 = p;
+  sub2.subj = p.subj + (int64_t)first * kSubjCols;
+  k_oz_split<double, 7, 1><<<dim3((unsigned)((max_v + 31) / 32), (unsigned)((K + kSplitCols - 1) / kSplitCols),
+                                  (unsigned)count), 256, 0, st>>>(sub2, p.amat, p.kp, K, cmaxg + (int64_t)first * K,
+                                                                  qg + (int64_t)first * K * lqg, lqg,
+                                                                  expog + (int64_t)first * K);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_oz_tn(const TmaMap& tma, const TmaMap& tmb, const int32_t* aexp, const int32_t* bexp, double* bred,
+                         int64_t ldx, int64_t kp, int64_t ldo, int64_t K, const OzItem* items, int n_items, int nslb,
+                         cudaStream_t st) {
+  const size_t bytes = oz_gram_smem_bytes();
+  static bool configured[2] = {false, false};
+  const void* fn = nslb == 7 ? (const void*)k_oz_tn<7> : (const void*)k_oz_tn<4>;
+  if (nslb != 7 && nslb != 4) return cudaErrorInvalidValue;
+  if (!configured[nslb == 7]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    configured[nslb == 7] = true;
+  }
+  if (n_items == 0) return cudaSuccess;
+  if (kp > 128) return cudaErrorInvalidValue;
+  OzTnArgs g{aexp, bexp, bred, ldx, kp, ldo, K};
+  const CUtensorMap* a = reinterpret_cast<const CUtensorMap*>(tma.opaque);
+  const CUtensorMap* b = reinterpret_cast<const CUtensorMap*>(tmb.opaque);
+  if (nslb == 7)
+    k_oz_tn<7><<<n_items, kOzThreads, bytes, st>>>(*a, *b, g, items);
+  else
+    k_oz_tn<4><<<n_items, kOzThreads, bytes, st>>>(*a, *b, g, items);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
                            int n_items, int nsl, cudaStream_t st) {

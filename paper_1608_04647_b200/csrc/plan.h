@@ -111,6 +111,10 @@ cudaError_t launch_mirror_gram(const DevPlan& p, int first, int count, cudaStrea
 cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first, int count,
                               unsigned long long* cmax, int8_t* q, int64_t lq, int32_t* expo, int64_t max_v,
                               cudaStream_t st);
+// slices of the init draw G (AMAT) of local subjects [first, first + count):
+// column maxima, exponents and seven-slice records [i][k][vb] (pitch lqg)
+cudaError_t launch_oz_init_slices(const DevPlan& p, int first, int count, int8_t* qg, int64_t lqg, int32_t* expog,
+                                  unsigned long long* cmaxg, int64_t max_v, cudaStream_t st);
 cudaError_t launch_reset(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_apply_w(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);
 cudaError_t launch_apply_w_f32(const DevPlan& p, const void* items_a, int n_items, cudaStream_t s);

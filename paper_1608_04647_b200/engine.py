@@ -123,7 +123,9 @@ class SrmEngine:
 
     @property
     def wout(self):
-        return self.region(_lib.R_WOUT).view(self.rows, self.K)
+        # the region also holds the init draw's int8 slices before the final W
+        # (int8 Gram plans), so it may be longer than rows x K
+        return self.region(_lib.R_WOUT)[: self.rows * self.K].view(self.rows, self.K)
 
     @property
     def mu(self):

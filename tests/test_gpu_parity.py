@@ -706,3 +706,32 @@ def test_transform_reference_cases(srm):
     x = rng.standard_normal(m.W[0].shape[0])
     once = srm.map_between(m, 0, 0, x)
     assert np.max(np.abs(srm.map_between(m, 0, 0, once) - once)) <= 1e-10
+
+
+@pytest.mark.parametrize("dtype,K", [("f64", 50), ("f32", 100), ("f32", 20)])
+def test_int8_init_term_matches_dmma(srm, dtype, K):
+    """The initial E-step term W_0^T Xhat = M_0^T (G^T Xhat) with G^T Xhat from
+    the int8 slices of the draw and of X-hat (int8 Gram plans) against the
+    fp64 DMMA contraction (fp64 Gram plans), per subject; the int8 plan is
+    initialised before any srm_prepare_gram call (it slices X-hat itself)."""
+    import torch
+
+    from paper_1608_04647_b200.data import recipe_numpy
+    from paper_1608_04647_b200.engine import SrmEngine
+
+    xs, _, _ = recipe_numpy(3, 2000, 300, K, seed=41, dtype=dtype)
+    xs[1] = xs[1][:1531]  # ragged V: a partial 32-voxel block
+    terms = []
+    for i8 in (True, False):
+        eng = SrmEngine([x.shape[0] for x in xs], 300, K, 2, storage=dtype, gram=True, gram_i8=i8)
+        assert eng.gram_i8 == i8
+        eng.load(xs)
+        eng.init_mapping(7, 0)
+        torch.cuda.synchronize()
+        eng.raise_status()
+        t = eng.terms[:, : eng.kp * eng.ldx].view(-1, eng.kp, eng.ldx)[:, :K, :300].cpu().numpy()
+        terms.append(t)
+        eng.close()
+    tol = 1e-13 if dtype == "f64" else 1e-7  # four fp32 slices: 2^-27 of the column maxima
+    for j in range(3):
+        assert nrel(terms[0][j], terms[1][j]) <= tol, (j, nrel(terms[0][j], terms[1][j]))
