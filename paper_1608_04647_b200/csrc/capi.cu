@@ -137,7 +137,10 @@ struct srm_plan {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   TmaMap tm_x_a, tm_s, tm_a, tm_x_b;  // tensor-core path TMA maps (bound at srm_plan_bind)
-  std::vector<OzItem> items_oz;       // int8-sliced Gram tiles (SRM_FLAG_GRAM_I8)
+  std::vector<OzItem> items_oz;       // int8-sliced Gram tiles (SRM_FLAG_GRAM_I8): single CTAs, or
+                                      // with gram_pairs (subject, 256-row pair, n0) for CTA pairs
+  bool gram_pairs = false;            // the int8 Gram on CTA pairs (k_oz_gram2)
+  TmaMap tm_qb;                       // the X-hat records with a 64-row box (the pairs' B halves)
   int64_t oz_lq = 0, max_v = 0;       // bytes per sliced TR row; largest local V
   int oz_nsl = 7;                     // int8 slices per X-hat value: 7 (fp64), 4 (fp32)
   TmaMap tm_q;
@@ -385,11 +388,27 @@ void build_work(srm_plan* p) {
                                (int32_t)std::min<int64_t>(128, p->V[i] - v0)});
     p->ow_first.push_back((int)p->items_ow.size());
   }
+  {
+    // SRM_B200_GRAM_PAIRS=1: the CTA-pair kernel (bit-identical; measured no
+    // faster at T = 1000 -- 12.9 vs 12.5 ms on cfg 2 -- the pairs' extra
+    // below-diagonal blocks (40 vs 36 tiles) cost what the halved B staging saves)
+    const char* env = getenv("SRM_B200_GRAM_PAIRS");
+    p->gram_pairs = env && env[0] == '1';
+  }
   if (p->flags & SRM_FLAG_GRAM_I8) {
-    for (int i = 0; i < p->n_local; ++i)
-      for (int64_t m0 = 0; m0 < p->ldx; m0 += 128)
-        for (int64_t n0 = m0; n0 < p->ldx; n0 += 128)
-          p->items_oz.push_back({i, (int32_t)m0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32)});
+    for (int i = 0; i < p->n_local; ++i) {
+      if (p->gram_pairs) {
+        // column block n, row blocks (2j, 2j + 1) for 2j <= n: the upper tiles
+        // plus, when n is even, the block below the diagonal (discarded)
+        for (int64_t n0 = 0; n0 < p->ldx; n0 += 128)
+          for (int64_t m0 = 0; m0 <= n0; m0 += 256)
+            p->items_oz.push_back({i, (int32_t)m0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32)});
+      } else {
+        for (int64_t m0 = 0; m0 < p->ldx; m0 += 128)
+          for (int64_t n0 = m0; n0 < p->ldx; n0 += 128)
+            p->items_oz.push_back({i, (int32_t)m0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32)});
+      }
+    }
   }
   // the init E-step term B_0 = G^T Xhat from int8 slices too (with the int8 B = S G)
   p->items_tn.clear();
@@ -810,6 +829,10 @@ std::vector<Stage> gram_stages(srm_plan* p, int first, int count) {
                                             p->oz_lq, region<int32_t>(p, I_OZEXP), p->max_v, st);
                  }});
     v.push_back({"oz_gram", [p, d, first, count, per](cudaStream_t st) {
+                   if (p->gram_pairs)
+                     return launch_oz_gram2(p->tm_q, p->tm_qb, region<int32_t>(p, I_OZEXP), d.gram, p->ldx,
+                                            region<OzItem>(p, I_ITEMS_OZ) + (int64_t)first * per, count * per,
+                                            p->oz_nsl, st);
                    return launch_oz_gram(p->tm_q, region<int32_t>(p, I_OZEXP), d.gram, p->ldx,
                                          region<OzItem>(p, I_ITEMS_OZ) + (int64_t)first * per, count * per,
                                          p->oz_nsl, st);
@@ -1081,7 +1104,10 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     e = launch_gram_tiles(p->dtype, d.xhat, p->ldx, d.gram, p->ldx, nullptr, 0, 0);
   if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM_I8)) {
     e = make_map_q(&p->tm_q, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, 128);
+    if (e == cudaSuccess) e = make_map_q(&p->tm_qb, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, 64);
     if (e == cudaSuccess) e = launch_oz_gram(p->tm_q, nullptr, nullptr, p->ldx, nullptr, 0, p->oz_nsl, 0);
+    if (e == cudaSuccess)
+      e = launch_oz_gram2(p->tm_q, p->tm_qb, nullptr, nullptr, p->ldx, nullptr, 0, p->oz_nsl, 0);
     if (e == cudaSuccess && p->oz_sg) {
       // tiled G slices: rows of 128 B, oz_tiled_bytes / 128 rows per subject
       e = make_map_q(&p->tm_g, region<int8_t>(p, I_OZG), 128, (int64_t)oz_tiled_bytes(p->ldx, p->ldx) / 128,
@@ -1286,7 +1312,8 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
   // slicing of every batch on the side stream (17 KB CTAs that fit beside the
   // Gram's) and each batch's Gram, mirror and G slices on `st` after its slices
   const int per = p->ldx / 128 > 0 ? (int)(p->items_oz.size() / std::max(p->n_local, 1)) : 1;
-  const int batch = std::max(1, 148 / std::max(per, 1));
+  const int ctas = per * (p->gram_pairs ? 2 : 1);  // CTAs per subject
+  const int batch = std::max(1, 148 / std::max(ctas, 1));
   if ((p->flags & SRM_FLAG_GRAM_I8) && count > batch) {
     const Lanes* ln = nullptr;
     int rc = plan_lanes(p, &ln);

@@ -503,6 +503,256 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
 }
 
 // ---------------------------------------------------------------------------
+// gram tiles on CTA pairs: tcgen05.mma.cta_group::2, M = 256 (two 128-row
+// blocks of the Gram, one per CTA) x N = 128.  Each CTA stages its own 128 A
+// rows and half of the B rows (64), so a CTA's shared-memory operand reads per
+// MMA drop from 8 KB to 6 KB and its TMA writes by a quarter -- the
+// single-CTA kernel is bound by the tensor core's shared-memory port (ncu:
+// sm__mem_tensor_cycles_active 85%).  Both producers signal the leader's full
+// barrier (cta_group::2 TMA), the leader issues every MMA and multicasts its
+// commits to both CTAs' empty / accumulator barriers, and every epilogue warp
+// of the pair arrives on the leader's accumulator-free barrier.  Pairs cover
+// the upper 128-tiles of a column block two row blocks at a time; a tile below
+// the diagonal is computed and discarded (mirror_gram fills the lower half).
+// ---------------------------------------------------------------------------
+constexpr int kOz2Stages = 4;
+constexpr int kOzBoxB = 8192;  // 64 rows x 128 bytes
+constexpr int kOz2StageBytes = 2 * kOzBox + 2 * kOzBoxB;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_s8_pair(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, int acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
+               :: "r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"((uint16_t)3));
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+// slice s of an operand staged as [lo box][hi box] of `box` bytes each
+__host__ __device__ constexpr uint64_t oz_slice_off_box(int s, int box) {
+  return (uint64_t)((s >> 2) * (box >> 4) + 2 * (s & 3));
+}
+
+template <int NSL, int P>
+__device__ __forceinline__ void oz_issue_pass_pair(uint32_t tmem, uint64_t da0, uint64_t db0, uint32_t idesc,
+                                                   uint32_t keep) {
+  constexpr int dlo = P ? 4 : 0, dhi = P ? kOzSlices - 1 : 3;
+#pragma unroll
+  for (int d = dlo; d <= dhi; ++d) {
+    const uint32_t acc = tmem + 128u * (uint32_t)(d - dlo);
+    const int s0 = d - (NSL - 1) > 0 ? d - (NSL - 1) : 0, s1 = d < NSL - 1 ? d : NSL - 1;
+#pragma unroll
+    for (int s = s0; s <= s1; ++s)
+      mma_s8_pair(acc, da0 + oz_slice_off_box(s, kOzBox), db0 + oz_slice_off_box(d - s, kOzBoxB), idesc,
+                  s == s0 ? keep : 1u);
+  }
+}
+
+template <int NSL>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
+    k_oz_gram2(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmqb,
+               const int32_t* __restrict__ expo, double* __restrict__ G, int64_t ldx,
+               const OzItem* __restrict__ items) {
+  constexpr int nsl = NSL;
+  constexpr int kPasses = 2;
+  extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[kOz2Stages], empty[kOz2Stages], accfull, accfree;
+  __shared__ uint32_t tmem_base;
+  const uint32_t rank = cluster_rank();
+  const OzItem it = items[blockIdx.x >> 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nvb = it.nvb;
+  const int nchunks = (nvb + kOzChunkBlocks - 1) / kOzChunkBlocks;
+  const int arow = it.m0 + 128 * (int)rank, brow = it.n0 + 64 * (int)rank;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < kOz2Stages; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      mbar_init(&accfull, 1);
+      mbar_init(&accfree, 2 * (kOzThreads - 64) / 32);  // every epilogue warp of the pair
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+  } else if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    // ---------------- TMA producers (both CTAs), the leader's full barriers ----------------
+    if (lane == 0) {
+      int k = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
+        for (int pass = 0; pass < kPasses; ++pass) {
+          const bool hi = pass && nsl > 4;
+          const int step = hi ? 1 : 2;
+          for (int vb = b0; vb < b1; vb += step, ++k) {
+            const int slot = k % kOz2Stages;
+            if (k >= kOz2Stages) mbar_wait(&empty[slot], ((k / kOz2Stages) - 1) & 1);
+            const int nj = min(step, b1 - vb);
+            if (rank == 0)  // both CTAs' bytes land on the leader's barrier
+              mbar_expect_tx(&full[slot], (uint32_t)(2 * (hi ? 2 * (kOzBox + kOzBoxB) : nj * (kOzBox + kOzBoxB))));
+            const uint32_t fb = leader_addr(&full[slot]);
+            unsigned char* st = smem + slot * kOz2StageBytes;
+            unsigned char* sb = st + 2 * kOzBox;
+            if (hi) {  // [A lo][A hi][B lo][B hi]
+              const int x = vb * oz_record_bytes(nsl);
+              tma_load_3d_pair(st, &tmq, x, arow, it.subj, fb);
+              tma_load_3d_pair(st + kOzBox, &tmq, x + 128, arow, it.subj, fb);
+              tma_load_3d_pair(sb, &tmqb, x, brow, it.subj, fb);
+              tma_load_3d_pair(sb + kOzBoxB, &tmqb, x + 128, brow, it.subj, fb);
+            } else {   // [A lo vb][A lo vb + 1][B lo vb][B lo vb + 1]
+              for (int j = 0; j < nj; ++j) {
+                const int xj = (vb + j) * oz_record_bytes(nsl);
+                tma_load_3d_pair(st + j * kOzBox, &tmq, xj, arow, it.subj, fb);
+                tma_load_3d_pair(sb + j * kOzBoxB, &tmqb, xj, brow, it.subj, fb);
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader only) ----------------
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_s8(256, 128);
+      int k = 0, npass = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
+        for (int pass = 0; pass < kPasses; ++pass, ++npass) {
+          if (npass > 0) mbar_wait(&accfree, (npass - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const bool hi = pass && nsl > 4;
+          const int step = hi ? 1 : 2;
+          for (int vb = b0; vb < b1; vb += step, ++k) {
+            const int slot = k % kOz2Stages;
+            mbar_wait(&full[slot], (k / kOz2Stages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t sa = smem_u32(smem + slot * kOz2StageBytes);
+            const uint64_t da0 = umma_desc_sw128(sa), db0 = umma_desc_sw128(sa + 2 * kOzBox);
+            const uint32_t keep = vb == b0 ? 0u : 1u;
+            if (hi) {
+              oz_issue_pass_pair<nsl, 1>(tmem, da0, db0, idesc, keep);
+            } else {
+              const uint64_t boxa = (uint64_t)(kOzBox >> 4), boxb = (uint64_t)(kOzBoxB >> 4);
+              const int nj = min(step, b1 - vb);
+              if (pass == 0) {
+                oz_issue_pass_pair<nsl, 0>(tmem, da0, db0, idesc, keep);
+                if (nj > 1) oz_issue_pass_pair<nsl, 0>(tmem, da0 + boxa, db0 + boxb, idesc, 1u);
+              } else {
+                oz_issue_pass_pair<nsl, 1>(tmem, da0, db0, idesc, keep);
+                if (nj > 1) oz_issue_pass_pair<nsl, 1>(tmem, da0 + boxa, db0 + boxb, idesc, 1u);
+              }
+            }
+            mma_commit_pair(&empty[slot]);
+          }
+          mma_commit_pair(&accfull);
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2-9 of each CTA, its own 128 rows ----------------
+    const int quarter = warp & 3;
+    const int cbase = ((warp - 2) >> 2) * 64;
+    const int r = quarter * 32 + lane;
+    const int64_t ta = arow + r;
+    const bool below = (arow / 128) > (it.n0 / 128);  // a tile below the diagonal: discarded
+    const bool rin = ta < ldx && !below;
+    const int32_t* ex = expo + (int64_t)it.subj * ldx;
+    const int ea = rin ? ex[ta] : 0;
+    double* grow = G + (int64_t)it.subj * ldx * ldx + ta * ldx + it.n0;
+    const uint32_t freebar = leader_addr(&accfree);
+    int npass = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      for (int pass = 0; pass < kPasses; ++pass, ++npass) {
+        mbar_wait(&accfull, npass & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int dlo = pass ? 4 : 0, dhi = pass ? kOzSlices - 1 : 3;
+        if (!below) {
+          for (int c0 = cbase; c0 < cbase + 64; c0 += 16) {
+            double prev[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              prev[j] = (npass > 0 && rin && it.n0 + c0 + j < ldx) ? grow[c0 + j] : 0.0;
+            uint32_t raw[4][16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (dlo + q <= dhi) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 128u * (uint32_t)q + c0, raw[q]);
+            tmem_wait_ld();
+            double val[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              long long h = 0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (dlo + q <= dhi) h = h * 128 + (long long)(int32_t)raw[q][j];
+              val[j] = (double)h * (pass ? 0x1p-54 : 0x1p-33);
+            }
+            if (rin) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const int64_t tb = it.n0 + c0 + j;
+                if (tb < ldx) {
+                  const double g = val[j] * pow2(ea + ex[tb]);
+                  grow[c0 + j] = (npass == 0) ? g : prev[j] + g;
+                }
+              }
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(freebar);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// ---------------------------------------------------------------------------
 // B_i = G_i^T Xhat_i on the int8 tensor cores (the E-step term of the initial
 // mapping, srm.py:101-118: W_0 = G M_0, so W_0^T Xhat = M_0^T (G^T Xhat)).
 // The same machinery as k_oz_gram with two record tensors: A = the seven
@@ -1522,6 +1772,29 @@ cudaError_t launch_oz_tn(const TmaMap& tma, const TmaMap& tmb, const int32_t* ae
     k_oz_tn<7><<<n_items, kOzThreads, bytes, st>>>(*a, *b, g, items);
   else
     k_oz_tn<4><<<n_items, kOzThreads, bytes, st>>>(*a, *b, g, items);
+  return cudaGetLastError();
+}
+
+size_t oz_gram2_smem_bytes() { return (size_t)kOz2Stages * kOz2StageBytes + 1024; }
+
+cudaError_t launch_oz_gram2(const TmaMap& tmq, const TmaMap& tmqb, const int32_t* expo, double* G, int64_t ldx,
+                            const OzItem* items, int n_items, int nsl, cudaStream_t st) {
+  const size_t bytes = oz_gram2_smem_bytes();
+  static bool configured[2] = {false, false};
+  if (nsl != 7 && nsl != 4) return cudaErrorInvalidValue;
+  const void* fn = nsl == 7 ? (const void*)k_oz_gram2<7> : (const void*)k_oz_gram2<4>;
+  if (!configured[nsl == 7]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    configured[nsl == 7] = true;
+  }
+  if (n_items == 0) return cudaSuccess;
+  const CUtensorMap* a = reinterpret_cast<const CUtensorMap*>(tmq.opaque);
+  const CUtensorMap* b = reinterpret_cast<const CUtensorMap*>(tmqb.opaque);
+  if (nsl == 7)
+    k_oz_gram2<7><<<2 * n_items, kOzThreads, bytes, st>>>(*a, *b, expo, G, ldx, items);
+  else
+    k_oz_gram2<4><<<2 * n_items, kOzThreads, bytes, st>>>(*a, *b, expo, G, ldx, items);
   return cudaGetLastError();
 }
 

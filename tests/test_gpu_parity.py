@@ -735,3 +735,33 @@ def test_int8_init_term_matches_dmma(srm, dtype, K):
     tol = 1e-13 if dtype == "f64" else 1e-7  # four fp32 slices: 2^-27 of the column maxima
     for j in range(3):
         assert nrel(terms[0][j], terms[1][j]) <= tol, (j, nrel(terms[0][j], terms[1][j]))
+
+
+@pytest.mark.parametrize("dtype,T", [("f64", 1000), ("f32", 300), ("f64", 130)])
+def test_int8_gram_cta_pairs_bit_identical(srm, monkeypatch, dtype, T):
+    """X^T X from the CTA-pair kernel (tcgen05 cta_group::2, M = 256) equals the
+    single-CTA kernel's bit for bit: same slice products, same exact int32 /
+    int64 sums, same epilogue; odd and even tile counts, partial tiles."""
+    import torch
+
+    from paper_1608_04647_b200 import _lib
+    from paper_1608_04647_b200.data import recipe_numpy
+    from paper_1608_04647_b200.engine import SrmEngine
+
+    xs, _, _ = recipe_numpy(3, 1500, T, 10, seed=43, dtype=dtype)
+    xs[2] = xs[2][:977]
+    out = []
+    for pairs in ("1", "0"):  # the pair kernel is opt-in (no faster at T = 1000)
+        monkeypatch.setenv("SRM_B200_GRAM_PAIRS", pairs)
+        eng = SrmEngine([x.shape[0] for x in xs], T, 10, 1, storage=dtype, gram=True, gram_i8=True)
+        eng.load(xs)
+        eng.prepare_gram()
+        torch.cuda.synchronize()
+        eng.raise_status()
+        g = eng.region(_lib.R_GRAM, torch.float64).view(3, eng.ldx, eng.ldx)[:, :T, :T].cpu().numpy()
+        out.append(g)
+        eng.close()
+    assert np.array_equal(out[0], out[1])
+    xh = [x.astype(np.float64) - x.astype(np.float64).mean(axis=1, keepdims=True) for x in xs]
+    for i in range(3):
+        assert nrel(out[0][i], xh[i].T @ xh[i]) <= (1e-13 if dtype == "f64" else 1e-6)
