@@ -244,12 +244,19 @@ cudaError_t run_ns(const DevPlan& p, int init, cudaStream_t s) {
 // fp64 throughout, so the transform is as accurate as the kp <= 80 kernel's
 // (an fp32 iteration carried ~4e-7 into S per iteration).
 // ---------------------------------------------------------------------------
-constexpr int kSlab = 32;
-constexpr int kSlabLd = kSlab + 4;  // == 4 mod 16 doubles
+// k-slab of the staged operands: the whole matrix while two fit in shared
+// memory (kp <= 112: one round of loads, all in flight), else 64 wide
+template <int KP>
+struct NsgSlab {
+  static constexpr int W = KP <= 112 ? KP : 64;
+  static constexpr int LDA = ns_ld(W);  // == 4 mod 16 doubles: conflict-free fragments
+};
 
 template <int KP, typename Epi>
 __device__ __forceinline__ void gmm_sym(const double* A, const double* B, double* As, double* Bs, Epi epi) {
   constexpr int LDB = ns_ld(KP);
+  constexpr int kSlab = NsgSlab<KP>::W;
+  constexpr int kSlabLd = NsgSlab<KP>::LDA;
   using TL = SymTiles<KP>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int tm[TL::PER], tn[TL::PER];
@@ -281,7 +288,7 @@ __device__ __forceinline__ void gmm_sym(const double* A, const double* B, double
     }
     __syncthreads();
 #pragma unroll 2
-    for (int kk = 0; kk < kSlab; kk += 4) {
+    for (int kk = 0; kk < kw; kk += 4) {
 #pragma unroll
       for (int q = 0; q < TL::PER; ++q) {
         if (on[q]) {
@@ -305,8 +312,8 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar_g(DevPlan p, int init) 
   extern __shared__ __align__(16) double gsm[];
   __shared__ double red[32];
   __shared__ double s_scale;
-  double* As = gsm;                 // [KP][kSlabLd]
-  double* Bs = gsm + KP * kSlabLd;  // [kSlab][LDB]
+  double* As = gsm;                              // [KP][slab pitch]
+  double* Bs = gsm + KP * NsgSlab<KP>::LDA;      // [slab][LDB]
   const int i = p.sub0 + blockIdx.x;
   const int n = (int)p.K;
   const int tid = threadIdx.x;
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar_g(DevPlan p, int init) 
 
 template <int KP>
 cudaError_t run_ns_g(const DevPlan& p, int init, cudaStream_t s) {
-  constexpr int bytes = (KP * kSlabLd + kSlab * ns_ld(KP)) * (int)sizeof(double);
+  constexpr int bytes = (KP * NsgSlab<KP>::LDA + NsgSlab<KP>::W * ns_ld(KP)) * (int)sizeof(double);
   if (!p.nsg) return cudaErrorInvalidValue;
   static bool configured = false;
   if (!configured) {
