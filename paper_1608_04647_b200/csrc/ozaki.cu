@@ -35,6 +35,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -200,7 +201,8 @@ __global__ void __launch_bounds__(256) k_oz_split_f32(DevPlan p, const float* __
                                                       const unsigned long long* __restrict__ cmax,
                                                       int8_t* __restrict__ q, int64_t lq, int32_t* __restrict__ expo) {
   constexpr int rec = 128;
-  __shared__ __align__(16) uint32_t buf[kSplitCols * kSplitLdw];
+  constexpr int LDW = NB * rec / 4 + 4;  // words per column row: NB records + 16 B (16-byte aligned)
+  __shared__ __align__(16) uint32_t buf[kSplitCols * LDW];
   const int i = blockIdx.z;
   const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
   const int64_t row0 = sj[SC_ROW_OFF], V = sj[SC_V];
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(256) k_oz_split_f32(DevPlan p, const float* __
 #pragma unroll
       for (int u = 0; u < 8; ++u) nv[j][u] = __double2int_rn((double)xv[j][u] * sd);
   }
-  uint2* row = reinterpret_cast<uint2*>(buf + tl * kSplitLdw);
+  uint2* row = reinterpret_cast<uint2*>(buf + tl * LDW);
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     int dg[4][8];  // [slice][voxel]
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(256) k_oz_split_f32(DevPlan p, const float* __
     const int64_t tt = t0 + r;
     if (tt < ldx) {
       uint4* dst = reinterpret_cast<uint4*>(q + ((int64_t)i * ldx + tt) * lq + vb0 * rec);
-      dst[k] = reinterpret_cast<const uint4*>(buf + r * kSplitLdw)[k];
+      dst[k] = reinterpret_cast<const uint4*>(buf + r * LDW)[k];
     }
   }
 }
@@ -1705,9 +1707,20 @@ cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first,
   if (x_dtype == SRM_F64)
     k_oz_split<double, 7, 1><<<dim3((unsigned)((max_v + 31) / 32), gy, (unsigned)count), 256, 0, st>>>(
         sub, static_cast<const double*>(p.xhat), p.ldx, p.ldx, cm, qs, lq, ex);
-  else  // two 128-byte records per column per CTA: 256-byte runs
-    k_oz_split_f32<2><<<dim3((unsigned)((max_v + 63) / 64), gy, (unsigned)count), 256, 0, st>>>(
-        sub, static_cast<const float*>(p.xhat), cm, qs, lq, ex);
+  else {
+    // four 128-byte records per column per CTA (512-byte runs, 32 loads in
+    // flight per thread): 9% faster than two on cfg 4 (SRM_B200_SPLIT_NB=2 keeps two)
+    static const int nb = [] {
+      const char* e = getenv("SRM_B200_SPLIT_NB");
+      return e && e[0] == '2' ? 2 : 4;
+    }();
+    if (nb == 4)
+      k_oz_split_f32<4><<<dim3((unsigned)((max_v + 127) / 128), gy, (unsigned)count), 256, 0, st>>>(
+          sub, static_cast<const float*>(p.xhat), cm, qs, lq, ex);
+    else  // two 128-byte records per column per CTA: 256-byte runs
+      k_oz_split_f32<2><<<dim3((unsigned)((max_v + 63) / 64), gy, (unsigned)count), 256, 0, st>>>(
+          sub, static_cast<const float*>(p.xhat), cm, qs, lq, ex);
+  }
   return cudaGetLastError();
 }
 
