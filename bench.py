@@ -398,10 +398,18 @@ def run_ours(args):
     from paper_1608_04647_b200.engine import SrmEngine
 
     rank, world, local = env_rank()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # SRM_BENCH_BACKEND=gloo with SRM_BENCH_ONE_GPU=1 runs every rank on GPU 0
+    # with the exchange through host memory: a check of the multi-rank flow on a
+    # one-GPU box (no kernel waits on another rank's), not a scaling measurement
+    backend = os.environ.get("SRM_BENCH_BACKEND", "nccl")
+    gpu = 0 if os.environ.get("SRM_BENCH_ONE_GPU") == "1" else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     comm = TorchCommunicator() if world > 1 else None
     cfg = workload(args)
     iters = cfg["iterations"]
@@ -465,7 +473,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(gpu)
     sampler.start()
     time.sleep(0.2)
     e0 = torch.cuda.Event(enable_timing=True)
