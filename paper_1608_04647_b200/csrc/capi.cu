@@ -151,7 +151,7 @@ struct srm_plan {
   std::vector<OzItem> items_ow;       // 128-voxel tiles of the final int8 W = Xhat R
   std::vector<OzItem> items_tn;       // (subject, 128-TR tile) of the int8 init term B_0 = G^T Xhat
   int64_t oz_lqg_init = 0;            // bytes per sliced row (feature) of the init draw G (records in WOUT)
-  TmaMap tm_gi;
+  TmaMap tm_gi, tm_gi64;
   std::vector<char> sliced;           // srm_prepare_gram_range has been enqueued for the subject
   std::vector<int> ow_first;          // [n_local + 1]: first items_ow entry of each subject
   TmaMap tm_q32, tm_r;
@@ -1122,7 +1122,12 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     if (e == cudaSuccess && p->oz_lqg_init) {
       e = make_map_q(&p->tm_gi, region<int8_t>(p, SRM_R_WOUT), p->oz_lqg_init, p->K, p->n_local, 128);
       if (e == cudaSuccess)
+        e = make_map_q(&p->tm_gi64, region<int8_t>(p, SRM_R_WOUT), p->oz_lqg_init, p->K, p->n_local, 64);
+      if (e == cudaSuccess)
         e = launch_oz_tn(p->tm_gi, p->tm_q, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, p->K, nullptr, 0,
+                         p->oz_nsl, 0);
+      if (e == cudaSuccess)
+        e = launch_oz_nt(p->tm_q, p->tm_gi64, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, p->K, nullptr, 0,
                          p->oz_nsl, 0);
     }
     if (e == cudaSuccess && p->oz_w) {
@@ -1191,7 +1196,16 @@ int srm_init_mapping_range(srm_plan* p, int first, int count, void* stream) {
     e = launch_oz_init_slices(d, first, count, region<int8_t>(p, SRM_R_WOUT), p->oz_lqg_init,
                               region<int32_t>(p, I_OZGIEXP), region<unsigned long long>(p, I_OZGICMAX), maxv, st);
     const int per = (int)((p->ldx + 127) / 128);
-    if (e == cudaSuccess)
+    // kp <= 64: the transposed one-pass kernel (N = 64 features); else M = 128 features
+    static const bool nt_off = [] {
+      const char* v = getenv("SRM_B200_INIT_NT");
+      return v && v[0] == '0';
+    }();
+    if (e == cudaSuccess && p->kp <= 64 && !nt_off)
+      e = launch_oz_nt(p->tm_q, p->tm_gi64, region<int32_t>(p, I_OZGIEXP), region<int32_t>(p, I_OZEXP), d.bred,
+                       p->ldx, p->kp, p->ldo, p->K, region<OzItem>(p, I_ITEMS_TN) + (int64_t)first * per, count * per,
+                       p->oz_nsl, st);
+    else if (e == cudaSuccess)
       e = launch_oz_tn(p->tm_gi, p->tm_q, region<int32_t>(p, I_OZGIEXP), region<int32_t>(p, I_OZEXP), d.bred, p->ldx,
                        p->kp, p->ldo, p->K, region<OzItem>(p, I_ITEMS_TN) + (int64_t)first * per, count * per,
                        p->oz_nsl, st);

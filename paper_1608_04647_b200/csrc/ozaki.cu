@@ -938,6 +938,139 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_tn(const __grid_constant__
   if (warp == 1) tmem_free(tmem, 512);
 }
 
+// The same B_i = G_i^T Xhat_i for kp <= 64, transposed: M = 128 TRs (the
+// X-hat records) x N = 64 features (the draw's records), so a K = 50 tile
+// wastes 14 of 64 columns instead of 78 of 128 rows, and all seven 64-column
+// d-groups fit the 512 TMEM columns at once -- one pass over the slices, the
+// exact int64 combination of both d-group halves in one epilogue.
+template <int NSX>
+__global__ void __launch_bounds__(kOzThreads, 1) k_oz_nt(const __grid_constant__ CUtensorMap tmx,
+                                                         const __grid_constant__ CUtensorMap tmg, OzTnArgs g,
+                                                         const OzItem* __restrict__ items) {
+  constexpr int NSG = kOzSlices;
+  constexpr int recx = NSX <= 4 ? 128 : 256;
+  constexpr int kBoxG = 8192;                          // 64 rows x 128 B
+  constexpr int kStage = (NSX > 4 ? 2 : 1) * kOzBox + 2 * kBoxG;
+  constexpr int kSt = 4;
+  extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[kSt], empty[kSt], accfull, accfree;
+  __shared__ uint32_t tmem_base;
+  const OzItem it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nvb = it.nvb;
+  const int nchunks = (nvb + kOzChunkBlocks - 1) / kOzChunkBlocks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < kSt; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      mbar_init(&accfull, 1);
+      mbar_init(&accfree, kOzThreads - 64);
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+  } else if (warp == 1) {
+    tmem_alloc(&tmem_base, 512);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer: [X lo][X hi][G lo][G hi] per 32-voxel block
+      int k = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
+        for (int vb = b0; vb < b1; ++vb, ++k) {
+          const int slot = k % kSt;
+          if (k >= kSt) mbar_wait(&empty[slot], ((k / kSt) - 1) & 1);
+          mbar_expect_tx(&full[slot], (uint32_t)kStage);
+          unsigned char* st = smem + slot * kStage;
+          tma_load_3d(st, &tmx, vb * recx, it.n0, it.subj, &full[slot]);
+          if (NSX > 4) tma_load_3d(st + kOzBox, &tmx, vb * recx + 128, it.n0, it.subj, &full[slot]);
+          unsigned char* sg = st + (NSX > 4 ? 2 : 1) * kOzBox;
+          tma_load_3d(sg, &tmg, vb * 256, 0, it.subj, &full[slot]);
+          tma_load_3d(sg + kBoxG, &tmg, vb * 256 + 128, 0, it.subj, &full[slot]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer: seven 64-column d-groups, one pass
+      constexpr uint32_t idesc = idesc_s8(128, 64);
+      int k = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        if (c > 0) mbar_wait(&accfree, (c - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
+        for (int vb = b0; vb < b1; ++vb, ++k) {
+          const int slot = k % kSt;
+          mbar_wait(&full[slot], (k / kSt) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t sa = smem_u32(smem + slot * kStage);
+          const uint64_t da0 = umma_desc_sw128(sa);
+          const uint64_t db0 = umma_desc_sw128(sa + (NSX > 4 ? 2 : 1) * kOzBox);
+          const uint32_t keep = vb == b0 ? 0u : 1u;
+#pragma unroll
+          for (int d = 0; d < kOzSlices; ++d) {
+            const int s0 = d - (NSG - 1) > 0 ? d - (NSG - 1) : 0, s1 = d < NSX - 1 ? d : NSX - 1;
+#pragma unroll
+            for (int sx = s0; sx <= s1; ++sx)
+              mma_s8(tmem + 64u * (uint32_t)d, da0 + oz_slice_off_box(sx, kOzBox),
+                     db0 + oz_slice_off_box(d - sx, kBoxG), idesc, sx == s0 ? keep : 1u);
+          }
+          mma_commit(&empty[slot]);
+        }
+        mma_commit(&accfull);
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2-9; TMEM lane = TR, 32-feature halves ----------------
+    const int quarter = warp & 3;
+    const int kbase = ((warp - 2) >> 2) * 32;
+    const int r = quarter * 32 + lane;
+    const int64_t t = it.n0 + r;
+    const bool tin = t < g.ldx;
+    const int et = tin ? g.bexp[(int64_t)it.subj * g.ldx + t] : 0;
+    const int32_t* ek = g.aexp + (int64_t)it.subj * g.K;
+    double* ocol = g.out + (int64_t)it.subj * g.kp * g.ldo + t;  // out[k][t] = ocol[k * ldo]
+    for (int c = 0; c < nchunks; ++c) {
+      mbar_wait(&accfull, c & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      for (int k0 = kbase; k0 < kbase + 32; k0 += 16) {
+        uint32_t raw[kOzSlices][16];
+#pragma unroll
+        for (int d = 0; d < kOzSlices; ++d)
+          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 64u * (uint32_t)d + k0, raw[d]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int kk = k0 + j;
+          if (!tin || kk >= g.kp) continue;
+          long long h = 0, l = 0;
+#pragma unroll
+          for (int d = 0; d < 4; ++d) h = h * 128 + (long long)(int32_t)raw[d][j];
+#pragma unroll
+          for (int d = 4; d < kOzSlices; ++d) l = l * 128 + (long long)(int32_t)raw[d][j];
+          // the two-pass kernel's arithmetic: (double) H 2^-33, then + (double) L 2^-54
+          const double sc = pow2(et + (kk < g.K ? ek[kk] : 0));
+          const double v0 = (double)h * 0x1p-33 * sc;
+          const double v1 = (double)l * 0x1p-54 * sc;
+          double* o = ocol + (int64_t)kk * g.ldo;
+          *o = (c == 0) ? v0 + v1 : (*o + v0) + v1;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&accfree);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) tmem_free(tmem, 512);
+}
+
 // column maxima |a[:, c]| of each subject's rows (c < ncols), as IEEE bits: one
 // CTA per 256 rows, eight row groups reduced in shared memory, one atomic per
 // column per CTA
@@ -1761,6 +1894,31 @@ cudaError_t launch_oz_init_slices(const DevPlan& p, int first, int count, int8_t
                                   (unsigned)count), 256, 0, st>>>(sub2, p.amat, p.kp, K, cmaxg + (int64_t)first * K,
                                                                   qg + (int64_t)first * K * lqg, lqg,
                                                                   expog + (int64_t)first * K);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_oz_nt(const TmaMap& tmx, const TmaMap& tmg64, const int32_t* aexp, const int32_t* bexp,
+                         double* bred, int64_t ldx, int64_t kp, int64_t ldo, int64_t K, const OzItem* items, int n_items,
+                         int nslx, cudaStream_t st) {
+  if (nslx != 7 && nslx != 4) return cudaErrorInvalidValue;
+  const int stage = (nslx > 4 ? 2 : 1) * kOzBox + 2 * 8192;
+  const size_t bytes = (size_t)4 * stage + 1024;
+  static bool configured[2] = {false, false};
+  const void* fn = nslx == 7 ? (const void*)k_oz_nt<7> : (const void*)k_oz_nt<4>;
+  if (!configured[nslx == 7]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    configured[nslx == 7] = true;
+  }
+  if (n_items == 0) return cudaSuccess;
+  if (kp > 64) return cudaErrorInvalidValue;
+  OzTnArgs g{aexp, bexp, bred, ldx, kp, ldo, K};
+  const CUtensorMap* x = reinterpret_cast<const CUtensorMap*>(tmx.opaque);
+  const CUtensorMap* gm = reinterpret_cast<const CUtensorMap*>(tmg64.opaque);
+  if (nslx == 7)
+    k_oz_nt<7><<<n_items, kOzThreads, bytes, st>>>(*x, *gm, g, items);
+  else
+    k_oz_nt<4><<<n_items, kOzThreads, bytes, st>>>(*x, *gm, g, items);
   return cudaGetLastError();
 }
 

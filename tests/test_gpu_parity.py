@@ -765,3 +765,28 @@ def test_int8_gram_cta_pairs_bit_identical(srm, monkeypatch, dtype, T):
     xh = [x.astype(np.float64) - x.astype(np.float64).mean(axis=1, keepdims=True) for x in xs]
     for i in range(3):
         assert nrel(out[0][i], xh[i].T @ xh[i]) <= (1e-13 if dtype == "f64" else 1e-6)
+
+
+@pytest.mark.parametrize("dtype,K", [("f64", 50), ("f32", 64), ("f32", 9)])
+def test_int8_init_transposed_bit_identical(srm, monkeypatch, dtype, K):
+    """kp <= 64: the transposed one-pass init GEMM (M = 128 TRs x N = 64
+    features) gives the same G^T Xhat, bit for bit, as the M = 128 feature
+    kernel (same exact d-group sums, same epilogue arithmetic)."""
+    import torch
+
+    from paper_1608_04647_b200.data import recipe_numpy
+    from paper_1608_04647_b200.engine import SrmEngine
+
+    xs, _, _ = recipe_numpy(3, 1700, 260, K, seed=47, dtype=dtype)
+    xs[0] = xs[0][:1333]
+    out = []
+    for nt in ("1", "0"):
+        monkeypatch.setenv("SRM_B200_INIT_NT", nt)
+        eng = SrmEngine([x.shape[0] for x in xs], 260, K, 2, storage=dtype, gram=True, gram_i8=True)
+        eng.load(xs, gram=True)
+        eng.init_mapping(3, 0)
+        torch.cuda.synchronize()
+        eng.raise_status()
+        out.append(eng.terms[:, : eng.kp * eng.ldx].cpu().numpy())
+        eng.close()
+    assert np.array_equal(out[0], out[1])
