@@ -43,7 +43,7 @@ enum srm_status {
   SRM_ERR_DEFINITENESS = 4,  /* DefinitenessError(pivot) */
   SRM_ERR_RANK = 5,          /* RankError              */
   SRM_ERR_CUDA = 6,          /* CUDA runtime failure   */
-  SRM_ERR_UNSUPPORTED = 7,   /* outside this build's limits (e.g. k > 112) */
+  SRM_ERR_UNSUPPORTED = 7,   /* outside this build's limits (k > 128) */
   SRM_ERR_FORMAT = 8,        /* malformed SFAB container (srm_sfab_last_error) */
   SRM_ERR_IO = 9             /* file system error (srm_sfab_last_error) */
 };

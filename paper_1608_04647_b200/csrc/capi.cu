@@ -167,7 +167,7 @@ int64_t esize(int dtype) { return dtype == SRM_F64 ? 8 : 4; }
 void layout(srm_plan* p) {
   const int64_t kp2 = p->kp * p->kp;
   const int ntile_tail = (int)((p->ldx + 31) / 32);
-  const int ntile_apply = (int)((p->ldx + kApplyCols - 1) / kApplyCols);
+  const int ntile_apply = (int)((p->ldx + apply_cols_for(p->kp) - 1) / apply_cols_for(p->kp));
   const int64_t term_stride = p->kp * p->ldx + kRecScalars;
   const int64_t red_stride = p->kp * p->ldx + kRedScalars;
   const int64_t hist_stride = SRM_H_RHO2 + std::max(p->n_local, 1);
@@ -261,6 +261,7 @@ void layout(srm_plan* p) {
   d.kp = p->kp;
   d.ldo = p->ldo;
   d.ntile_apply = ntile_apply;
+  d.apply_cols = apply_cols_for(p->kp);
   d.ntile_tail = ntile_tail;
   d.gfb_chunks = gfb_chunks;
   d.term_stride = term_stride;
@@ -1064,7 +1065,8 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     std::vector<SvdJob> sv;
     for (int i = 0; i < p->n_local; ++i)
       sv.push_back({rfin[i], region<double>(p, SRM_R_MMAT) + (int64_t)i * p->kp * p->kp, p->kp, (int32_t)p->kp,
-                    (int32_t)(p->global0 + i)});
+                    (int32_t)(p->global0 + i),
+                    svd_needs_global_v((int)p->K) ? region<double>(p, I_QSCR) + (int64_t)i * p->kp * p->kp : nullptr});
     e = cudaMemcpy(region<QrJob>(p, I_QRJOBS), flat.data(), flat.size() * sizeof(QrJob), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
       e = cudaMemcpy(region<SvdJob>(p, I_SVDJOBS), sv.data(), sv.size() * sizeof(SvdJob), cudaMemcpyHostToDevice);

@@ -29,6 +29,10 @@ constexpr int kSmemBudget = 104 * 1024;
 
 __host__ __device__ constexpr int pad4mod16(int n) { return n + ((4 - n) % 16 + 16) % 16; }
 
+// apply_rows: rows of A staged per round (128, or 64 above kp = 112 where M
+// and 128 rows of fp64 A would exceed shared memory)
+__host__ __device__ constexpr int apply_rows_tile(int kp) { return kp > 112 ? 64 : 128; }
+
 template <typename T>
 __host__ __device__ constexpr int e_r_stride() { return sizeof(T) == 8 ? kTileN + 4 : kTileN + 8; }
 
@@ -426,6 +430,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_rows(const TA* __restrict__ 
   constexpr int SA = pad4mod16(KP) + (sizeof(TA) == 4 ? 4 : 0);  // floats: == 8 mod 32 words
   constexpr int SM = pad4mod16(KP);
   constexpr int NT = KP / 8;
+  constexpr int RT = apply_rows_tile(KP);  // rows staged per round: M and the row tile fit in shared memory
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Ms = reinterpret_cast<double*>(smem_raw);
   TA* As = reinterpret_cast<TA*>(smem_raw + KP * SM * 8);
@@ -434,15 +439,16 @@ __global__ void __launch_bounds__(kThreads) k_apply_rows(const TA* __restrict__ 
   const int64_t row0 = it.o_off / lda;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int e = tid; e < KP * KP; e += kThreads) Ms[(e / KP) * SM + e % KP] = Mg[e];
-  for (int half = 0; half * 128 < it.rows; ++half) {
-    const int r0 = half * 128;
-    const int nr = min(128, it.rows - r0);
+  for (int half = 0; half * RT < it.rows; ++half) {
+    const int r0 = half * RT;
+    const int nr = min(RT, it.rows - r0);
     __syncthreads();
-    for (int e = tid; e < 128 * KP; e += kThreads) {
+    for (int e = tid; e < RT * KP; e += kThreads) {
       const int r = e / KP, c = e - r * KP;
       As[r * SA + c] = r < nr ? A[(row0 + r0 + r) * lda + c] : TA(0);
     }
     __syncthreads();
+    if (warp * 16 >= RT) continue;  // RT = 64: warps 4-7 only stage
     double acc[2][NT][2];
 #pragma unroll
     for (int m = 0; m < 2; ++m)
@@ -481,7 +487,7 @@ template <int KP, typename TA>
 cudaError_t run_apply(const TA* A, int64_t lda, const double* M, int64_t mstride, double* W, int K,
                       const ItemA* items, int n_items, cudaStream_t st) {
   constexpr int SA = pad4mod16(KP) + (sizeof(TA) == 4 ? 4 : 0);
-  constexpr int bytes = KP * pad4mod16(KP) * 8 + 128 * SA * (int)sizeof(TA);
+  constexpr int bytes = KP * pad4mod16(KP) * 8 + apply_rows_tile(KP) * SA * (int)sizeof(TA);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k_apply_rows<KP, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);

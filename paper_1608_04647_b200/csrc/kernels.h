@@ -139,6 +139,7 @@ struct SvdJob {
   int64_t ldm;
   int32_t mp;
   int32_t subject;  // reported with RankError
+  double* vg;       // K x K global scratch for V when svd_needs_global_v(K), else null
 };
 struct TsqrSchedule {
   struct Job {
@@ -150,6 +151,7 @@ struct TsqrSchedule {
   int64_t buf_doubles = 0;               // per ping-pong buffer
 };
 bool qr_polar_supported(int K);
+bool svd_needs_global_v(int K);
 int tsqr_block_rows(int K);
 TsqrSchedule tsqr_schedule(const std::vector<int64_t>& rows, int K, int target_ctas);
 std::vector<std::vector<QrJob>> tsqr_jobs(const TsqrSchedule& s, const std::vector<const double*>& a,

@@ -27,8 +27,9 @@ enum RedCol { RD_RHO0 = 0, RD_VLOGRHO = 1, RD_SQRHO = 2, RD_VSUM = 3, kRedScalar
 // tail scratch scalars
 enum TailCol { TS_LOGDET_SIGMA = 0, TS_LOGDET_PREC = 1, TS_TRACE = 2, kTailScalars = 8 };
 
-// column tile width of apply_m (W^T Xhat = M^T B)
-constexpr int kApplyCols = 128;
+// column tile width of apply_m (W^T Xhat = M^T B): 128, or 64 for kp > 112
+// (DevPlan::apply_cols, ntile_apply = ceil(ldx / apply_cols))
+inline int apply_cols_for(int64_t kp) { return kp > 112 ? 64 : 128; }
 // TR chunk of gram_from_b (A^T A = B S^T / 2)
 constexpr int kGfbCols = 128;
 
@@ -38,7 +39,8 @@ struct DevPlan {
   int flags;
   int xf32;  // X-hat stored in fp32 (per-iteration polar may run in fp32; the final one is exact)
   int64_t T, K, ldx, kp, ldo;
-  int ntile_apply;  // kApplyCols-column tiles of ldx
+  int ntile_apply;  // apply_cols-column tiles of ldx
+  int apply_cols;   // apply_m column tile (apply_cols_for(kp))
   int ntile_tail;   // 32-column tiles of ldx
   int64_t term_stride, red_stride, hist_stride;
   // regions

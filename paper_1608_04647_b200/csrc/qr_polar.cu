@@ -110,13 +110,18 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_polar(const SvdJob* __restr
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int NW = kSvdThreads / 32;
   const int LD = K + 1;
-  double* U = vsm;          // R, rotated in place: columns become U_R sigma
-  double* V = U + K * LD;   // accumulated rotations
-  double* sig = V + K * LD; // column norms
+  // U (R, rotated in place: its columns become U_R sigma) in shared memory; the
+  // accumulated rotations V too while both fit (K <= 112), else in the job's
+  // global scratch (L2-resident), pitch K
+  const bool vsmem = jb.vg == nullptr;
+  double* U = vsm;
+  double* sig = U + K * LD;                   // column norms
+  double* V = vsmem ? sig + K : jb.vg;
+  const int LV = vsmem ? LD : K;
   for (int e = tid; e < K * K; e += kSvdThreads) {
     const int r = e / K, col = e - r * K;
     U[r * LD + col] = jb.r[e];
-    V[r * LD + col] = r == col ? 1.0 : 0.0;
+    V[r * LV + col] = r == col ? 1.0 : 0.0;
   }
   __syncthreads();
   const int np2 = (K + 1) & ~1;
@@ -146,9 +151,9 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_polar(const SvdJob* __restr
           const double up = U[r * LD + p], uq = U[r * LD + q];
           U[r * LD + p] = cs * up - sn * uq;
           U[r * LD + q] = sn * up + cs * uq;
-          const double vp = V[r * LD + p], vq = V[r * LD + q];
-          V[r * LD + p] = cs * vp - sn * vq;
-          V[r * LD + q] = sn * vp + cs * vq;
+          const double vp = V[r * LV + p], vq = V[r * LV + q];
+          V[r * LV + p] = cs * vp - sn * vq;
+          V[r * LV + q] = sn * vp + cs * vq;
         }
         rot = 1;
       }
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_polar(const SvdJob* __restr
     const int a = e / jb.mp, b = e - a * jb.mp;
     double m = 0.0;
     if (a < K && b < K)
-      for (int j = 0; j < K; ++j) m = fma(V[a * LD + j] * V[b * LD + j], sig[j], m);
+      for (int j = 0; j < K; ++j) m = fma(V[a * LV + j] * V[b * LV + j], sig[j], m);
     jb.m[(int64_t)a * jb.ldm + b] = m;
   }
 }
@@ -204,9 +209,10 @@ int tsqr_block_rows(int K) {
 }
 
 bool qr_polar_supported(int K) {
-  return K >= 1 && (size_t)(K + tsqr_block_rows(K)) * (K + 1) * 8 <= 227 * 1024 &&
-         (size_t)(2 * K * (K + 1) + K) * 8 <= 227 * 1024;
+  return K >= 1 && K <= 128 && (size_t)(K + tsqr_block_rows(K)) * (K + 1) * 8 <= 227 * 1024;
 }
+
+bool svd_needs_global_v(int K) { return (size_t)(2 * K * (K + 1) + K) * 8 > 227 * 1024; }
 
 TsqrSchedule tsqr_schedule(const std::vector<int64_t>& rows, int K, int target_ctas) {
   TsqrSchedule s;
@@ -296,7 +302,7 @@ cudaError_t launch_tsqr(const QrJob* jobs_dev, int n_jobs, int max_ctas, int K, 
 cudaError_t launch_svd_polar(const SvdJob* jobs_dev, int n_jobs, int K, int32_t* status, const int32_t* iter,
                              cudaStream_t st) {
   static size_t cache = 0;
-  const size_t bytes = (size_t)(2 * K * (K + 1) + K) * sizeof(double);
+  const size_t bytes = (size_t)((svd_needs_global_v(K) ? 1 : 2) * K * (K + 1) + K) * sizeof(double);
   cudaError_t e = smem_attr((const void*)k_svd_polar, bytes, &cache);
   if (e != cudaSuccess || n_jobs == 0) return e;
   k_svd_polar<<<(unsigned)n_jobs, kSvdThreads, bytes, st>>>(jobs_dev, K, status, iter);

@@ -27,7 +27,7 @@ namespace srm {
 namespace {
 
 constexpr int kSmallThreads = 256;
-constexpr int kMaxK = 112;
+constexpr int kMaxK = 128;
 
 __device__ __forceinline__ double* rec_ptr(const DevPlan& p, int slot) {
   return p.terms + (int64_t)slot * p.term_stride;
@@ -377,12 +377,13 @@ __device__ __forceinline__ void stage_rows(double* dst, int ldd, const double* _
 // 128-column tile; M^T (A operand) and B are staged in shared memory with row
 // pitches = 4 mod 16 doubles (conflict-free fragments), the contraction over
 // c < K rounded up to 4 with zero rows.
-constexpr int kApplyLd = kApplyCols + 4;
 
-template <int NF>
+template <int NF, int COLS>
 __global__ void __launch_bounds__(kSmallThreads) k_apply_m(DevPlan p, int with_cross) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double scratch[32];
+  constexpr int kApplyCols = COLS;
+  constexpr int kApplyLd = COLS + 4;
   constexpr int kp = 8 * NF;
   constexpr int LDM = kp + ((4 - kp) % 16 + 16) % 16;  // = 4 mod 16
   constexpr int MS = (NF + 7) / 8;                      // strips per warp
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_reduce_terms(DevPlan p, doubl
     }
   }
 }
-// In-place inverse of an SPD n x n matrix (n <= 112) by the symmetric sweep
+// In-place inverse of an SPD n x n matrix (n <= 128) by the symmetric sweep
 // (Gauss-Jordan without pivoting), register-resident: a 16 x 16 thread grid
 // owns the cyclic R x R blocks a[i][k] = A[ty + 16 i][tx + 16 k]
 // (R = ceil(n / 16)), and each pivot step broadcasts only the pivot row
@@ -781,7 +782,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_inv(DevPlan p) {
     case 4: tail_inv_body<4>(p, sh); break;
     case 5: tail_inv_body<5>(p, sh); break;
     case 6: tail_inv_body<6>(p, sh); break;
-    default: tail_inv_body<7>(p, sh); break;
+    case 7: tail_inv_body<7>(p, sh); break;
+    default: tail_inv_body<8>(p, sh); break;
   }
 }
 
@@ -833,8 +835,12 @@ __device__ __forceinline__ void tail_kk_body(const DevPlan& p, int iteration, Sw
     return;
   }
   const double logdet_prec = sum_log(dbuf, n, sh.scratch);
-  double* Vs = sm;           // var_s  [n][ld]
-  double* Ss = sm + n * ld;  // Sigma_s [n][ld]
+  // var_s [n][ld] in shared memory; Sigma_s too while both fit (n <= 112),
+  // else read from global (L2-resident) in the product below
+  const bool sig_smem = n <= 112;
+  double* Vs = sm;
+  double* Ss = sig_smem ? sm + n * ld : p.sigma;
+  const int lds = sig_smem ? ld : kp;
 #pragma unroll
   for (int i = 0; i < R; ++i)
 #pragma unroll
@@ -843,7 +849,7 @@ __device__ __forceinline__ void tail_kk_body(const DevPlan& p, int iteration, Sw
       if (r < n && c < n) {
         Vs[r * ld + c] = -a[i][k];
         p.var[r * kp + c] = -a[i][k];
-        Ss[r * ld + c] = p.sigma[r * kp + c];
+        if (sig_smem) Ss[r * ld + c] = p.sigma[r * kp + c];
       }
     }
   for (int e = tid; e < kp * kp; e += blockDim.x) {
@@ -864,7 +870,7 @@ __device__ __forceinline__ void tail_kk_body(const DevPlan& p, int iteration, Sw
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int r = ty + 16 * i;
-      sr[i] = (r < n) ? Ss[m * ld + r] : 0.0;
+      sr[i] = (r < n) ? Ss[m * lds + r] : 0.0;
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -897,7 +903,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_kk(DevPlan p) {
     case 4: tail_kk_body<4>(p, iteration, sh); break;
     case 5: tail_kk_body<5>(p, iteration, sh); break;
     case 6: tail_kk_body<6>(p, iteration, sh); break;
-    default: tail_kk_body<7>(p, iteration, sh); break;
+    case 7: tail_kk_body<7>(p, iteration, sh); break;
+    default: tail_kk_body<8>(p, iteration, sh); break;
   }
 }
 
@@ -1155,7 +1162,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_spd_inverse(double* a, int n,
     case 4: spd_inverse_body<4>(a, n, status, sh); break;
     case 5: spd_inverse_body<5>(a, n, status, sh); break;
     case 6: spd_inverse_body<6>(a, n, status, sh); break;
-    default: spd_inverse_body<7>(a, n, status, sh); break;
+    case 7: spd_inverse_body<7>(a, n, status, sh); break;
+    default: spd_inverse_body<8>(a, n, status, sh); break;
   }
 }
 
@@ -1300,20 +1308,24 @@ cudaError_t launch_final_polar(const DevPlan& p, cudaStream_t s) { return launch
 cudaError_t launch_apply_m(const DevPlan& p, int with_cross, cudaStream_t s) {
   const int64_t K4 = (p.K + 3) & ~3;
   const int64_t ldm = p.kp + ((4 - p.kp) % 16 + 16) % 16;
-  const size_t bytes = (size_t)(K4 * ldm + K4 * kApplyLd) * sizeof(double);
+  const size_t bytes = (size_t)(K4 * ldm + K4 * (p.apply_cols + 4)) * sizeof(double);
   const void* fn = nullptr;
   switch (p.kp / 8) {
 #define SRM_APPLY_M_CASE(n) \
   case n:                   \
-    fn = (const void*)k_apply_m<n>; \
+    fn = (const void*)k_apply_m<n, 128>; \
     break;
     SRM_APPLY_M_CASE(1) SRM_APPLY_M_CASE(2) SRM_APPLY_M_CASE(3) SRM_APPLY_M_CASE(4) SRM_APPLY_M_CASE(5)
     SRM_APPLY_M_CASE(6) SRM_APPLY_M_CASE(7) SRM_APPLY_M_CASE(8) SRM_APPLY_M_CASE(9) SRM_APPLY_M_CASE(10)
     SRM_APPLY_M_CASE(11) SRM_APPLY_M_CASE(12) SRM_APPLY_M_CASE(13) SRM_APPLY_M_CASE(14)
 #undef SRM_APPLY_M_CASE
+    // kp > 112: 64-column tiles (M and the B tile in shared memory: 205 KB at kp = 128)
+    case 15: fn = (const void*)k_apply_m<15, 64>; break;
+    case 16: fn = (const void*)k_apply_m<16, 64>; break;
     default:
       return cudaErrorInvalidValue;
   }
+  if ((p.kp > 112) != (p.apply_cols == 64)) return cudaErrorInvalidValue;
   cudaError_t e = set_smem(fn, bytes);
   if (e != cudaSuccess) return e;
   const dim3 grid((unsigned)p.ntile_apply, (unsigned)p.nsub);
@@ -1334,7 +1346,7 @@ cudaError_t launch_gram_from_b(const DevPlan& p, cudaStream_t s) {
     break;
     SRM_GFB_CASE(1) SRM_GFB_CASE(2) SRM_GFB_CASE(3) SRM_GFB_CASE(4) SRM_GFB_CASE(5) SRM_GFB_CASE(6)
     SRM_GFB_CASE(7) SRM_GFB_CASE(8) SRM_GFB_CASE(9) SRM_GFB_CASE(10) SRM_GFB_CASE(11) SRM_GFB_CASE(12)
-    SRM_GFB_CASE(13) SRM_GFB_CASE(14)
+    SRM_GFB_CASE(13) SRM_GFB_CASE(14) SRM_GFB_CASE(15) SRM_GFB_CASE(16)
 #undef SRM_GFB_CASE
     default:
       return cudaErrorInvalidValue;
@@ -1383,7 +1395,7 @@ cudaError_t launch_tail_inv(const DevPlan& p, cudaStream_t s) {
 
 cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s) {
   const int K = (int)p.K;
-  const size_t b1 = (size_t)2 * K * (K + 1) * sizeof(double);
+  const size_t b1 = (size_t)(K <= 112 ? 2 : 1) * K * (K + 1) * sizeof(double);
   cudaError_t e = set_smem((const void*)k_tail_kk, b1);
   if (e != cudaSuccess) return e;
   k_tail_kk<<<1, kSmallThreads, b1, s>>>(p);

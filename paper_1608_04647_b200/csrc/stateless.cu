@@ -73,6 +73,21 @@ __global__ void __launch_bounds__(kSqThreads) k_sum_final(const double* __restri
   if (threadIdx.x == 0) *out = s;
 }
 
+// M = (3 I - G) / 2 for a symmetric G (the Newton-Schulz polar step), symmetrised
+__global__ void k_ns_step_matrix(const double* __restrict__ g, int64_t ldg, int n, double* __restrict__ m,
+                                 int64_t ldm) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * n) return;
+  const int r = e / n, c = e - r * n;
+  const double gs = 0.5 * (g[(int64_t)r * ldg + c] + g[(int64_t)c * ldg + r]);
+  m[(int64_t)r * ldm + c] = 0.5 * ((r == c ? 3.0 : 0.0) - gs);
+}
+
+cudaError_t launch_ns_step_matrix(const double* g, int64_t ldg, int n, double* m, int64_t ldm, cudaStream_t st) {
+  k_ns_step_matrix<<<(n * n + 255) / 256, 256, 0, st>>>(g, ldg, n, m, ldm);
+  return cudaGetLastError();
+}
+
 __global__ void k_add_diag(const double* __restrict__ a, int64_t lda, int64_t n, double c, double* __restrict__ out,
                            int64_t ldo) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -125,7 +140,7 @@ int64_t polar_workspace_bytes(int64_t v, int64_t k) {
   int64_t b = 0;
   b += 2 * rup(v * kp * 8, 256);                              // A copy, W = A M
   b += 2 * rup(sch.buf_doubles * 8, 256);                     // TSQR factors (ping-pong)
-  b += rup(nch * kp * kp * 8, 256) + 3 * rup(kp * kp * 8, 256);  // W^T W partials, G, M, M2
+  b += rup(nch * kp * kp * 8, 256) + 4 * rup(kp * kp * 8, 256);  // W^T W partials, G, M, M2, SVD V
   b += rup((int64_t)sch.levels.size() * sizeof(QrJob), 256) + rup(sizeof(SvdJob), 256);
   b += rup(nch * (int64_t)sizeof(ItemE), 256);
   return b;
@@ -259,7 +274,8 @@ int srm_tail_step(const double* reduced, int64_t ldr, const double* sigma, int64
   d.kp = kp;
   d.ldo = ldx + kp;
   d.ntile_tail = ntail;
-  d.ntile_apply = (int)((ldx + kApplyCols - 1) / kApplyCols);
+  d.apply_cols = apply_cols_for(kp);
+  d.ntile_apply = (int)((ldx + d.apply_cols - 1) / d.apply_cols);
   d.red_stride = kp * ldx + kRedScalars;
   d.hist_stride = 8;
   d.n_hist = 1;
@@ -333,6 +349,7 @@ int srm_polar(const double* a, int64_t lda, int64_t v, int64_t k, double* w, int
   double* G = c.take<double>(kp * kp);
   double* M = c.take<double>(kp * kp);
   double* M2 = c.take<double>(kp * kp);
+  double* Vg = c.take<double>(kp * kp);
   QrJob* qj = c.take<QrJob>((int64_t)sch.levels.size());
   SvdJob* sj = c.take<SvdJob>(1);
   ItemE* items = c.take<ItemE>(nch);
@@ -354,14 +371,23 @@ int srm_polar(const double* a, int64_t lda, int64_t v, int64_t k, double* w, int
     where = "polar: tsqr";
     e = launch_tsqr(qj + L, 1, tsqr_max_ctas(sch.levels[L]), (int)k, st);
   }
-  SvdJob sv{rfin[0], M, kp, (int32_t)kp, 0};
+  SvdJob sv{rfin[0], M, kp, (int32_t)kp, 0, svd_needs_global_v((int)k) ? Vg : nullptr};
   if (e == cudaSuccess) { where = "polar: svd"; e = cudaMemcpyAsync(sj, &sv, sizeof(SvdJob), cudaMemcpyHostToDevice, st); }
   if (e == cudaSuccess) e = launch_svd_polar(sj, 1, (int)k, status4, nullptr, st);
   if (e == cudaSuccess) { where = "polar: A M"; e = cudaMemsetAsync(Wt, 0, v * kp * 8, st); }
   if (e == cudaSuccess) e = launch_apply_right(Ap, kp, v, (int)k, M, kp, Wt, kp, st);
-  if (e == cudaSuccess) { where = "polar: W^T W"; e = split_v(Wt, kp, Wt, SRM_F64, kp, kp, v, 1.0, part, G, items, st); }
-  if (e == cudaSuccess) { where = "polar: refine"; e = launch_polar_small(G, kp, (int)k, M2, kp, status4, st); }
-  if (e == cudaSuccess) e = launch_apply_right(Wt, kp, v, (int)k, M2, kp, w, ldw, st);
+  // (4) W <- W (3 I - W^T W) / 2 twice: W^T W is within eps cond(A) of I, and
+  // each Newton-Schulz step squares that distance (cond 1e11: 2e-5 -> 6e-10 -> 1e-18)
+  for (int step = 0; step < 2 && e == cudaSuccess; ++step) {
+    double* src = step == 0 ? Wt : Ap;  // Ap (A) is no longer needed after W = A M
+    double* dst = step == 0 ? Ap : w;
+    const int64_t ldd = step == 0 ? kp : ldw;
+    where = "polar: W^T W";
+    e = split_v(src, kp, src, SRM_F64, kp, kp, v, 1.0, part, G, items, st);
+    if (e == cudaSuccess) { where = "polar: refine"; e = launch_ns_step_matrix(G, kp, (int)k, M2, kp, st); }
+    if (e == cudaSuccess && step == 0) e = cudaMemsetAsync(Ap, 0, v * kp * 8, st);
+    if (e == cudaSuccess) e = launch_apply_right(src, kp, v, (int)k, M2, kp, dst, ldd, st);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the job tables were staged from the host stack
   return ret(e, where);
 }

@@ -83,7 +83,8 @@ def test_plan_ordered_slots_for_ranks():
     ([10], 8, 0, 3, _lib.load().srm_abi_version() and 1),   # k < 1 -> ConfigError
     ([10], 8, 3, 0, 1),                                      # iterations < 1
     ([2], 8, 3, 3, 2),                                       # V < k -> ShapeError
-    ([500], 8, 200, 3, 7),                                   # k > 112 -> unsupported
+    ([500], 8, 200, 3, 7),                                   # k > 128 -> unsupported
+    ([500], 8, 129, 3, 7),
 ])
 def test_plan_errors(v, t, k, iters, code):
     rc, _ = _plan(v, t, k, iters)

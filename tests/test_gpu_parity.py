@@ -790,3 +790,49 @@ def test_int8_init_transposed_bit_identical(srm, monkeypatch, dtype, K):
         out.append(eng.terms[:, : eng.kp * eng.ldx].cpu().numpy())
         eng.close()
     assert np.array_equal(out[0], out[1])
+
+
+# --------------------------------------------------------------------------
+# K up to 128 (kp 120 / 128: 8 x 8 register sweeps, 64-column apply tiles,
+# the L2 Newton-Schulz, the SVD's V in global memory on the exact route)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("K,dtype,algorithm", [(128, "f64", "gram"), (128, "f64", "stream"), (120, "f32", "gram"),
+                                              (128, "f32", "stream")])
+def test_wide_k_fit_vs_oracle(srm, K, dtype, algorithm):
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(3, 1400, 400, K, seed=53, dtype=dtype)
+    xs[1] = xs[1][:1201]
+    ref = orc.run_em(xs, K, 3, seed=5)
+    tol = TOL64 if dtype == "f64" else TOL32
+    for n in (1, 3):
+        eng = []
+        m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=K, iterations=n, seed=5), algorithm=algorithm,
+                    engine_out=eng)
+        assert not eng[-1].exact_polar
+        r = ref["iters"][n - 1]
+        _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], tol, f"K={K} {dtype} {algorithm} it{n - 1}")
+        for j in range(n):
+            assert abs(m.log_likelihood[j] - ref["iters"][j]["ll"]) <= tol * abs(ref["iters"][j]["ll"])
+        for w in m.W:
+            assert np.max(np.abs(w.T @ w - np.eye(K))) <= 1e-10
+
+
+def test_wide_k_exact_polar_and_kernels(srm):
+    from paper_1608_04647_b200 import kernels
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(2, 900, 300, 128, seed=59)
+    ref = orc.run_em(xs, 128, 2, seed=1)
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=128, iterations=2, seed=1), exact_polar=True)
+    r = ref["iters"][-1]
+    _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL64, "K=128 exact")
+    rng = np.random.default_rng(61)
+    a = rng.standard_normal((3000, 128))
+    u, _, vt = np.linalg.svd(a, full_matrices=False)
+    assert nrel(kernels.polar_orthogonal(a), u @ vt) <= 1e-12
+    c = rng.standard_normal((128, 128))
+    spd = c.T @ c + 128 * np.eye(128)
+    inv = kernels.spd_inverse(spd)
+    assert np.max(np.abs(spd @ inv - np.eye(128))) <= 1e-10 and np.array_equal(inv, inv.T)
