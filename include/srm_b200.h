@@ -265,6 +265,14 @@ int srm_unproject(const double* w, int64_t ldw, const double* z, int64_t ldz, co
  * InvalidInputError through status4 (kernels.py:45-46).  workspace >= 8 KB. */
 int srm_trace_ata(const double* a, int64_t lda, int64_t rows, int64_t cols, double* out,
                   int32_t* status4, void* workspace, int64_t ws_bytes, void* stream);
+/* *out = sum_{r,c} a[r][c] b[r][c] over [rows x cols] f64 blocks, fixed order
+ * (srm.py:151 cross term einsum("kt,kt->", W^T Xhat, S)); workspace >= 8 KB */
+int srm_dot(const double* a, int64_t lda, const double* b, int64_t ldb, int64_t rows, int64_t cols,
+            double* out, void* workspace, int64_t ws_bytes, void* stream);
+/* srm.py:140-142 `update_sigma_s` after var_s: out = sym(var_s + ss / t) with
+ * ss = S S^T [k x k], and *trace_out = tr(out) (device pointers) */
+int srm_sigma_update(const double* var, int64_t ldv, const double* ss, int64_t ldss, int64_t k, int64_t t,
+                     double* out, int64_t ldo, double* trace_out, void* stream);
 /* out = A + c I for a [n x n] f64 matrix (kernels.py:158-165); off-diagonal
  * entries are copied bit for bit. */
 int srm_add_diag(const double* a, int64_t lda, int64_t n, double c, double* out, int64_t ldo,

@@ -63,6 +63,8 @@ SIGNATURES = [
     ("srm_unproject", c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp]),
     ("srm_trace_ata", c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     ("srm_add_diag", c_int, [c_vp, c_i64, c_i64, c_dbl, c_vp, c_i64, c_vp]),
+    ("srm_dot", c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp]),
+    ("srm_sigma_update", c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
     ("srm_spd_inverse", c_int, [c_vp, c_i64, c_vp, c_vp]),
     ("srm_polar", c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     ("srm_stateless_workspace_bytes", c_i64, [c_i64, c_i64, c_i64]),

@@ -88,6 +88,41 @@ cudaError_t launch_ns_step_matrix(const double* g, int64_t ldg, int n, double* m
   return cudaGetLastError();
 }
 
+// sum_{r,c} a[r][c] b[r][c] in a fixed order (per-CTA partials, then one CTA)
+__global__ void __launch_bounds__(kSqThreads) k_dot_part(const double* __restrict__ a, int64_t lda,
+                                                        const double* __restrict__ b, int64_t ldb, int64_t rows,
+                                                        int64_t cols, int64_t per, double* __restrict__ part) {
+  __shared__ double scratch[32];
+  const int64_t n = rows * cols;
+  const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min(n, e0 + per);
+  double s = 0.0;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += kSqThreads) {
+    const int64_t r = e / cols, c = e - r * cols;
+    s = fma(a[r * lda + c], b[r * ldb + c], s);
+  }
+  s = block_sum<kSqThreads>(s, scratch);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// srm.py:140-142: Sigma_new = sym(var_s + S S^T / T), trace(Sigma_new) (ss = S S^T)
+__global__ void __launch_bounds__(kSqThreads) k_sigma_update(const double* __restrict__ var, int64_t ldv,
+                                                            const double* __restrict__ ss, int64_t ldss, int n,
+                                                            double inv_t, double* __restrict__ out, int64_t ldo,
+                                                            double* __restrict__ trace) {
+  __shared__ double scratch[32];
+  double tr = 0.0;
+  for (int e = threadIdx.x; e < n * n; e += kSqThreads) {
+    const int r = e / n, c = e - r * n;
+    const double nrc = var[(int64_t)r * ldv + c] + ss[(int64_t)r * ldss + c] * inv_t;
+    const double ncr = var[(int64_t)c * ldv + r] + ss[(int64_t)c * ldss + r] * inv_t;
+    const double v = 0.5 * (nrc + ncr);
+    out[(int64_t)r * ldo + c] = v;
+    if (r == c) tr += v;
+  }
+  tr = block_sum<kSqThreads>(tr, scratch);
+  if (threadIdx.x == 0) *trace = tr;
+}
+
 __global__ void k_add_diag(const double* __restrict__ a, int64_t lda, int64_t n, double c, double* __restrict__ out,
                            int64_t ldo) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -317,6 +352,28 @@ int srm_trace_ata(const double* a, int64_t lda, int64_t rows, int64_t cols, doub
   k_sumsq_part<<<nct, kSqThreads, 0, st>>>(a, lda, rows, cols, per, part, status4);
   k_sum_final<<<1, kSqThreads, 0, st>>>(part, nct, out);
   return ret(cudaGetLastError(), "trace_ata");
+}
+
+int srm_dot(const double* a, int64_t lda, const double* b, int64_t ldb, int64_t rows, int64_t cols, double* out,
+            void* workspace, int64_t ws_bytes, void* stream) {
+  if (rows < 1 || cols < 1 || lda < cols || ldb < cols) return SRM_ERR_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n = rows * cols;
+  const int nct = (int)std::min<int64_t>(1024, (n + 4095) / 4096);
+  const int64_t per = (n + nct - 1) / nct;
+  if (ws_bytes < nct * 8) return SRM_ERR_CONFIG;
+  double* part = static_cast<double*>(workspace);
+  k_dot_part<<<nct, kSqThreads, 0, st>>>(a, lda, b, ldb, rows, cols, per, part);
+  k_sum_final<<<1, kSqThreads, 0, st>>>(part, nct, out);
+  return ret(cudaGetLastError(), "dot");
+}
+
+int srm_sigma_update(const double* var, int64_t ldv, const double* ss, int64_t ldss, int64_t k, int64_t t,
+                     double* out, int64_t ldo, double* trace_out, void* stream) {
+  if (k < 1 || t < 1) return SRM_ERR_SHAPE;
+  k_sigma_update<<<1, kSqThreads, 0, static_cast<cudaStream_t>(stream)>>>(var, ldv, ss, ldss, (int)k, 1.0 / (double)t,
+                                                                         out, ldo, trace_out);
+  return ret(cudaGetLastError(), "sigma_update");
 }
 
 int srm_add_diag(const double* a, int64_t lda, int64_t n, double c, double* out, int64_t ldo, void* stream) {

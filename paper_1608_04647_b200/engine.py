@@ -526,6 +526,24 @@ class SrmEngine:
         if code:
             raise from_status(code, arg=arg)
 
+    def poll(self, it):
+        """(code, arg, warnings, |S - S_prev|, |S_prev|) after iteration ``it``:
+        the status word and the tolerance statistics in one asynchronous copy
+        to pinned memory and one stream synchronisation (the tolerance stop,
+        srm.py:275-287)."""
+        torch = _torch()
+        if getattr(self, "_poll_buf", None) is None:
+            self._poll_buf = torch.empty(32, dtype=torch.uint8, pin_memory=True)
+        buf = self._poll_buf
+        status = self.region(_lib.R_STATUS, torch.uint8)[:16]
+        row = self.hist[it % self.iterations][_lib.H_SDIFF: _lib.H_SPREV + 1].contiguous().view(torch.uint8)
+        buf[:16].copy_(status, non_blocking=True)
+        buf[16:].copy_(row, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        st = buf[:16].view(torch.int32).tolist()
+        sdiff, sprev = buf[16:].view(torch.float64).tolist()
+        return st[0], st[1], st[3], sdiff, sprev
+
     @property
     def warnings(self):
         """SRM_WARN_* bits raised so far (synchronises)."""

@@ -169,8 +169,18 @@ def _stream():
 
 
 def _finite(t, name):
+    """kernels.py:45-46 on the device: the sum-of-squares kernel flags
+    non-finite entries (InvalidInputError)."""
     torch = _torch()
-    if not bool(torch.isfinite(t).all()):
+    lib = _lib.load()
+    d = t if t.dtype == torch.float64 else t.to(torch.float64)
+    d = d.reshape(d.shape[0], -1) if d.dim() != 2 else d
+    out = torch.empty(1, dtype=torch.float64, device=d.device)
+    ws = torch.empty(1024, dtype=torch.float64, device=d.device)
+    st = _status_tensor()
+    _lib.check(lib.srm_trace_ata(_ptr(d), _ld(d), d.shape[0], d.shape[1], _ptr(out), _ptr(st), _ptr(ws), 8192,
+                                 _stream()), "finite check")
+    if int(st[0].item()):
         from .errors import InvalidInputError
 
         raise InvalidInputError(f"{name} contains non-finite entries")
@@ -289,28 +299,42 @@ def update_sigma_s(sigma_s, rho0, S):
     output is discarded.
     """
     torch = _torch()
+    lib = _lib.load()
     s_dev = _dev(_as_matrix(S, "S"), torch.float64)
     k, t = s_dev.shape
     _, var, _, _ = _tail(torch.zeros((k, t), dtype=torch.float64, device="cuda"), sigma_s, rho0)
-    ss = _gemm_tn(s_dev.t().contiguous(), s_dev.t().contiguous())  # S S^T via the V-contraction
-    new = var + ss / t
-    new = 0.5 * (new + new.t())
-    return new.cpu().numpy(), float(torch.diagonal(new).sum().item())
+    st = s_dev.t().contiguous()
+    ss = _gemm_tn(st, st)  # S S^T via the V-contraction
+    new = torch.empty((k, k), dtype=torch.float64, device="cuda")
+    trace = torch.empty(1, dtype=torch.float64, device="cuda")
+    _lib.check(lib.srm_sigma_update(_ptr(var), k, _ptr(ss), k, k, t, _ptr(new), k, _ptr(trace), _stream()),
+               "sigma_update")
+    return new.cpu().numpy(), float(trace.item())
 
 
 def m_step_subject(Xhat_i, S, trace_sigma_s_new):
     """Per-subject mapping and noise update (srm.py:145-155)."""
     torch = _torch()
-    x = _dev(_as_matrix(Xhat_i, "Xhat"))
+    lib = _lib.load()
+    x = _dev(_as_matrix(Xhat_i, "Xhat"), torch.float64)
     s = _dev(_as_matrix(S, "S"), torch.float64)
-    _finite(x, "A")
     a = _gemm_nt(x, s, 0.5)
+    _finite(a, "A")  # kernels.py:201 via _as_matrix: non-finite A is InvalidInputError
     w = _polar(a, s.shape[0])
     n_trs = s.shape[1]
     n_voxels = x.shape[0]
-    cross = float((_gemm_tn(w, x) * s).sum().item())
-    xd = x.to(torch.float64)
-    sq = float((xd * xd).sum().item())
+    wtx = _gemm_tn(w, x)
+    scal = torch.empty(2, dtype=torch.float64, device="cuda")
+    ws = torch.empty(1024, dtype=torch.float64, device="cuda")
+    st = _status_tensor()
+    # cross = <W^T Xhat, S> (srm.py:151) and trace_ata(Xhat) (srm.py:152, with
+    # the kernels.py:45 finite check) on the device, fixed summation order
+    _lib.check(lib.srm_dot(_ptr(wtx), n_trs, _ptr(s), _ld(s), s.shape[0], n_trs, _ptr(scal), _ptr(ws), 8192,
+                           _stream()), "dot")
+    _lib.check(lib.srm_trace_ata(_ptr(x), _ld(x), n_voxels, x.shape[1], ctypes.c_void_p(scal.data_ptr() + 8),
+                                 _ptr(st), _ptr(ws), 8192, _stream()), "trace_ata")
+    _raise_status(st)
+    cross, sq = (float(v) for v in scal.cpu().numpy())
     rho2 = (sq + n_trs * trace_sigma_s_new - 2.0 * cross) / (n_trs * n_voxels)
     return w.cpu().numpy(), max(rho2, RHO_FLOOR)
 
@@ -593,18 +617,15 @@ def _fit_pass(subjects, config, comm, *, exact, storage, ordered, graphs, keep_o
         if on_iteration is not None:
             on_iteration(_snapshot(eng, it))
         if config.tolerance is not None:
-            code, arg, _, warn = eng.status()
+            # one copy + one stream synchronisation per iteration: status and |dS|, |S_prev|
+            code, arg, warn, sdiff, sprev = eng.poll(it)
             if not exact and any_rank(comm, warn != 0):
                 eng.close()
                 return None
             if code:
                 raise from_status(code, arg=arg)
-            row = eng.hist[it]
-            if it >= 1:
-                sdiff = float(row[_lib.H_SDIFF].item())
-                sprev = float(row[_lib.H_SPREV].item())
-                if sdiff / max(sprev, 1e-300) < config.tolerance:
-                    break
+            if it >= 1 and sdiff / max(sprev, 1e-300) < config.tolerance:
+                break
     clock.tick("em")
     if keep_on_device:
         eng.finalize()

@@ -836,3 +836,27 @@ def test_wide_k_exact_polar_and_kernels(srm):
     spd = c.T @ c + 128 * np.eye(128)
     inv = kernels.spd_inverse(spd)
     assert np.max(np.abs(spd @ inv - np.eye(128))) <= 1e-10 and np.array_equal(inv, inv.T)
+
+
+def test_step_api_native_pieces(srm):
+    """update_sigma_s / m_step_subject compute the symmetrised Sigma, its trace,
+    the cross term and trace_ata on the device (srm_sigma_update, srm_dot,
+    srm_trace_ata); vs the oracle steps and the non-finite error path."""
+    from paper_1608_04647_b200.errors import InvalidInputError
+
+    rng = np.random.default_rng(71)
+    k, t, v = 7, 40, 300
+    sig = np.cov(rng.standard_normal((k, 3 * k))) + np.eye(k)
+    s = rng.standard_normal((k, t))
+    ref_sig, ref_tr = orc.shared_covariance(sig, 3.5, s)
+    new, tr = srm.update_sigma_s(sig, 3.5, s)
+    assert nrel(new, ref_sig) <= 1e-14 and abs(tr - ref_tr) <= 1e-14 * abs(ref_tr) and np.array_equal(new, new.T)
+    xh = rng.standard_normal((v, t))
+    xh -= xh.mean(axis=1, keepdims=True)
+    w_ref, r_ref = orc.subject_update(xh, s, ref_tr)
+    w, r = srm.m_step_subject(xh, s, ref_tr)
+    assert nrel(w, w_ref) <= 1e-13 and abs(r - r_ref) <= 1e-13 * r_ref
+    bad = xh.copy()
+    bad[5, 7] = np.inf
+    with pytest.raises(InvalidInputError):
+        srm.m_step_subject(bad, s, ref_tr)
