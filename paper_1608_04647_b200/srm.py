@@ -476,7 +476,8 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
     per-iteration trace of the reference's loop (srm.py:254-287), for
     checking a long fit against an oracle without refitting.  Forming W_i
     reads the EM state only, so the fit is bit-identical with or without it
-    (tested); it synchronises once per iteration.
+    (tested); it synchronises once per iteration.  A fit redone on the exact
+    polar route reports its iterations again from 0.
     """
     config.validate()
     if not subjects:
@@ -515,9 +516,6 @@ class IterationState:
 
 def _snapshot(eng, it):
     eng.finalize()  # W_i = A_i M_i of this M-step; writes only W (and finalize scratch)
-    code, arg, _, _ = eng.status()
-    if code:
-        raise from_status(code, arg=arg)
     w = hostio.to_host(eng.wout)
     return IterationState(
         iteration=it, S=eng.S.cpu().numpy(), sigma_s=eng.sigma.cpu().numpy(),
@@ -614,17 +612,22 @@ def _fit_pass(subjects, config, comm, *, exact, storage, ordered, graphs, keep_o
         else:
             eng.step(comm)
         n_done = it + 1
-        if on_iteration is not None:
-            on_iteration(_snapshot(eng, it))
-        if config.tolerance is not None:
-            # one copy + one stream synchronisation per iteration: status and |dS|, |S_prev|
+        if config.tolerance is not None or on_iteration is not None:
+            # one copy + one stream synchronisation per iteration: status and |dS|, |S_prev|;
+            # a polar-conditioning warning first (the pass is redone), then errors
             code, arg, warn, sdiff, sprev = eng.poll(it)
             if not exact and any_rank(comm, warn != 0):
                 eng.close()
                 return None
             if code:
                 raise from_status(code, arg=arg)
-            if it >= 1 and sdiff / max(sprev, 1e-300) < config.tolerance:
+            if on_iteration is not None:
+                state = _snapshot(eng, it)
+                if not exact and any_rank(comm, eng.status()[3] != 0):  # the snapshot's final transform
+                    eng.close()
+                    return None
+                on_iteration(state)
+            if config.tolerance is not None and it >= 1 and sdiff / max(sprev, 1e-300) < config.tolerance:
                 break
     clock.tick("em")
     if keep_on_device:

@@ -860,3 +860,60 @@ def test_step_api_native_pieces(srm):
     bad[5, 7] = np.inf
     with pytest.raises(InvalidInputError):
         srm.m_step_subject(bad, s, ref_tr)
+
+
+# --------------------------------------------------------------------------
+# seeded random shapes: every path against the oracle at edge sizes
+# (K = 1, T = 2, V = K, one subject, T / V / K off every tile multiple)
+# --------------------------------------------------------------------------
+
+_EDGE_CASES = [
+    # (subjects, V, T, K, dtype, algorithm)
+    (1, 40, 2, 1, "f64", "stream"),
+    (1, 9, 12, 9, "f64", "gram"),       # V = K: a square polar
+    (2, 33, 5, 3, "f64", "gram"),
+    (3, 130, 131, 17, "f64", "gram"),   # T = 131: a partial 128-TR tile, K off a multiple of 8
+    (3, 257, 33, 12, "f64", "stream"),
+    (2, 1001, 257, 65, "f32", "gram"),  # kp = 72 > 64: two 64-feature halves
+    (4, 77, 300, 30, "f32", "stream"),
+    (2, 500, 97, 31, "f64", "exact"),
+    (5, 60, 45, 8, "f32", "gram"),
+]
+
+
+@pytest.mark.parametrize("n,v,t,k,dtype,algorithm", _EDGE_CASES)
+def test_edge_shapes_vs_oracle(srm, n, v, t, k, dtype, algorithm):
+    rng = np.random.default_rng(1000 + 7 * v + t)
+    np_dt = np.float64 if dtype == "f64" else np.float32
+    xs = [(rng.standard_normal((v - 3 * j if v - 3 * j >= k else v, t)) * (1 + j)).astype(np_dt) for j in range(n)]
+    iters = 4
+    ref = orc.run_em(xs, k, iters, seed=3)
+    kw = {"exact_polar": True} if algorithm == "exact" else {"algorithm": algorithm}
+    tol = TOL64 if dtype == "f64" else TOL32
+    states = []
+    m = srm.fit(_subjects(srm, xs), srm.SrmConfig(k=k, iterations=iters, seed=3), on_iteration=states.append, **kw)
+    states = states[-iters:]  # a fit redone on the exact polar route reports its iterations again
+    assert [s.iteration for s in states] == list(range(iters))
+    for st, r in zip(states, ref["iters"]):
+        what = f"{(n, v, t, k, dtype, algorithm)} it{st.iteration}"
+        assert nrel(st.S, r["S"]) <= tol, (what, "S", nrel(st.S, r["S"]))
+        assert nrel(st.sigma_s, r["sigma_s"]) <= tol, (what, "sigma")
+        assert nrel(st.rho2, r["rho2"]) <= tol, (what, "rho2")
+        for w, rw in zip(st.W, r["W"]):
+            assert nrel(w, rw) <= tol, (what, "W", nrel(w, rw))
+        assert abs(st.log_likelihood - r["ll"]) <= tol * abs(r["ll"]), (what, "ll")
+    assert nrel(m.S, ref["S"]) <= tol
+
+
+@pytest.mark.parametrize("algorithm", ["gram", "stream"])
+def test_fewer_trs_than_features_raises_like_reference(srm, algorithm):
+    """T < K: S has rank <= T, so A = Xhat S^T / 2 is rank deficient; the
+    reference's polar raises RankError in the first M-step (srm.py:148)."""
+    from paper_1608_04647_b200.errors import RankError
+
+    rng = np.random.default_rng(77)
+    xs = [rng.standard_normal((20, 7))]
+    with pytest.raises(orc.OracleError, match="RankError"):
+        orc.run_em(xs, 9, 3, seed=3)
+    with pytest.raises(RankError):
+        srm.fit(_subjects(srm, xs), srm.SrmConfig(k=9, iterations=3, seed=3), algorithm=algorithm)
