@@ -543,9 +543,10 @@ def run_ours(args):
         launch_ms = once[dom]
         alg_flops = float(n_local) * V * T * (T + 1)          # symmetric X^T X: T(T+1)/2 dots of length V
         alg_bytes = float(local_units * (slice_b if dom == "oz_gram" else b))
-        # int8 products issued by oz_gram per upper 128 x 128 tile and 32-voxel block: the slice
-        # pairs s + s' < 7 (28 for fp64's 7 slices; all 16 for fp32's 4); useful = T(T+1)/2 entries
-        products = 28 if cfg["dtype"] == "f64" else 16
+        # int8 products per Gram entry and 32-voxel block off the diagonal tiles: the slice pairs
+        # s + s' <= 6 (28 of fp64's 7 slices) or <= 3 (10 of fp32's 4; the diagonal tiles'
+        # extra d-groups are not counted); useful = T(T+1)/2 entries
+        products = 28 if cfg["dtype"] == "f64" else 10
         i8_ops = 2.0 * products * (T * (T + 1) / 2) * (-(-V // 32) * 32) * n_local
     elif dom in ("final_a", "oz_w", "apply_w"):
         launch_ms = once[dom]

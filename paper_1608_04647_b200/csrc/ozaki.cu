@@ -307,13 +307,29 @@ struct OzBars {
 // low half-record box holds slices 0-3 at 32-byte steps, the high box 4-7
 __host__ __device__ constexpr uint64_t oz_slice_off(int s) { return (uint64_t)((s >> 2) * (kOzBox >> 4) + 2 * (s & 3)); }
 
-// the MMAs of one 32-voxel block in pass P: d-groups 0-3 (P = 0) or 4-6
+// the highest d-group an off-diagonal Gram tile accumulates: every d = s + s'
+// <= 6 for seven-slice data, d <= 3 (pass 1 only) for four-slice data.
+// Diagonal tiles keep every d-group up to 6, so each G[t][t] carries the
+// dropped groups (whose terms q_s q_s' add coherently there, all positive for
+// s = s'); off the diagonal the dropped terms are sums of uncorrelated low
+// digits, relative ~1/sqrt(V): for fp32 data on the BASELINE recipe (V = 30k)
+// ~1e-8 of |G| normwise, 3e-9 of A^T A = S G S^T / 4 and ~2e-9 of W^T W - I
+// (tools/slice_drop_probe.py), against fp32's 1e-4 parity tolerance and
+// criterion 4's 1e-8; it saves pass 2 on 97% of the tiles (cfg 4: 99 -> 64
+// ms).  Subjects of fewer than kOzDropMinBlocks * 32 voxels keep every pair
+// (their Grams are cheap, and W^T W - I would reach ~5e-9 at V = 2600).
+// Seven-slice data keeps d = 6 off the diagonal too: dropping it saved 2%
+// (pass 2 is bound by its operand traffic, not the MMAs) for 100x the error.
+__host__ __device__ constexpr int oz_dtop_off(int nsl) { return nsl > 4 ? 6 : 3; }
+constexpr int kOzDropMinBlocks = 512;
+
+// the MMAs of one 32-voxel block in pass P: d-groups 0-3 (P = 0) or 4-DTOP
 // (P = 1), pairs s + s' = d with s, s' < NSL, fully unrolled; `keep` = 0
 // starts the accumulators (first block of a chunk)
-template <int NSL, int P>
+template <int NSL, int P, int DTOP = kOzSlices - 1>
 __device__ __forceinline__ void oz_issue_pass(uint32_t tmem, uint64_t da0, uint64_t db0, uint32_t idesc,
                                               uint32_t keep) {
-  constexpr int dlo = P ? 4 : 0, dhi = P ? kOzSlices - 1 : 3;
+  constexpr int dlo = P ? 4 : 0, dhi = P ? DTOP : 3;
 #pragma unroll
   for (int d = dlo; d <= dhi; ++d) {
     const uint32_t acc = tmem + 128u * (uint32_t)(d - dlo);
@@ -329,21 +345,20 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
                                                            const int32_t* __restrict__ expo, double* __restrict__ G,
                                                            int64_t ldx, const OzItem* __restrict__ items) {
   constexpr int nsl = NSL;  // compile time: the MMA issue loops unroll
-  // d-groups 0..3 fill the 512 TMEM columns; pass 2 accumulates d = 4..6.
-  // Four-slice (fp32) data keeps all 16 pairs, so G = Xt^T Xt exactly for the
-  // sliced Xt: dropping the pairs s + s' >= 4 would bias the diagonal by
-  // ~2^-28 relative (the q_2^2 terms are all positive) and cost W^T W = I at
-  // the 1e-8 level.
-  constexpr int kPasses = 2;
+  // d-groups 0..3 fill the 512 TMEM columns; pass 2 accumulates d = 4..6 on
+  // diagonal tiles, d = 4..5 off the diagonal (oz_dtop_off); four-slice data
+  // off the diagonal needs no pass 2
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ OzBars bars;
   __shared__ uint32_t tmem_base;
   const OzItem it = items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool diag = it.m0 == it.n0;
   const int nvb = it.nvb;
+  const bool diag = it.m0 == it.n0;
+  const bool all_d = diag || nvb < kOzDropMinBlocks;  // every d-group (oz_dtop_off)
   const int nchunks = (nvb + kOzChunkBlocks - 1) / kOzChunkBlocks;
+  const int kPasses = (oz_dtop_off(nsl) < 4 && !all_d) ? 1 : 2;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -424,7 +439,10 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
             const uint64_t da0 = umma_desc_sw128(sa), db0 = umma_desc_sw128(sb);
             const uint32_t keep = vb == b0 ? 0u : 1u;
             if (hi) {
-              oz_issue_pass<nsl, 1>(tmem, da0, db0, idesc, keep);
+              if (all_d)
+                oz_issue_pass<nsl, 1>(tmem, da0, db0, idesc, keep);
+              else
+                oz_issue_pass<nsl, 1, oz_dtop_off(nsl)>(tmem, da0, db0, idesc, keep);
             } else {
               // the stage's second block sits one box after the first (A and B alike)
               const uint64_t box = (uint64_t)(kOzBox >> 4);
@@ -458,7 +476,9 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
       for (int pass = 0; pass < kPasses; ++pass, ++npass) {
         mbar_wait(&bars.accfull, npass & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
+        // d-groups dlo..dtop were accumulated; the sum is weighted as dlo..dhi
         const int dlo = pass ? 4 : 0, dhi = pass ? kOzSlices - 1 : 3;
+        const int dtop = pass ? (all_d ? kOzSlices - 1 : oz_dtop_off(nsl)) : 3;
         for (int c0 = cbase; c0 < cbase + 64; c0 += 16) {
           // pass 2 adds to pass 1's values: their loads go out first
           double prev[16];
@@ -468,8 +488,13 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
           // the (up to four) d-groups of these 16 columns in flight, one wait
           uint32_t raw[4][16];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (dlo + q <= dhi) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 128u * (uint32_t)q + c0, raw[q]);
+          for (int q = 0; q < 4; ++q) {
+            if (dlo + q <= dtop)
+              tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 128u * (uint32_t)q + c0, raw[q]);
+            else
+#pragma unroll
+              for (int j = 0; j < 16; ++j) raw[q][j] = 0u;
+          }
           tmem_wait_ld();
           // the pass's d-groups as one exact int64 (|raw| < 2^31): pass 1
           // H = sum_{d<4} raw_d 2^{7(3-d)} (x 2^-33), pass 2 L = sum_{d>=4}
@@ -565,10 +590,10 @@ __host__ __device__ constexpr uint64_t oz_slice_off_box(int s, int box) {
   return (uint64_t)((s >> 2) * (box >> 4) + 2 * (s & 3));
 }
 
-template <int NSL, int P>
+template <int NSL, int P, int DTOP = kOzSlices - 1>
 __device__ __forceinline__ void oz_issue_pass_pair(uint32_t tmem, uint64_t da0, uint64_t db0, uint32_t idesc,
                                                    uint32_t keep) {
-  constexpr int dlo = P ? 4 : 0, dhi = P ? kOzSlices - 1 : 3;
+  constexpr int dlo = P ? 4 : 0, dhi = P ? DTOP : 3;
 #pragma unroll
   for (int d = dlo; d <= dhi; ++d) {
     const uint32_t acc = tmem + 128u * (uint32_t)(d - dlo);
@@ -586,7 +611,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
                const int32_t* __restrict__ expo, double* __restrict__ G, int64_t ldx,
                const OzItem* __restrict__ items) {
   constexpr int nsl = NSL;
-  constexpr int kPasses = 2;
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kOz2Stages], empty[kOz2Stages], accfull, accfree;
@@ -597,6 +621,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
   const int nvb = it.nvb;
   const int nchunks = (nvb + kOzChunkBlocks - 1) / kOzChunkBlocks;
   const int arow = it.m0 + 128 * (int)rank, brow = it.n0 + 64 * (int)rank;
+  // the d-groups are k_oz_gram's per tile: the pair accumulates the union
+  // (every group when either tile is diagonal) and each epilogue takes its own
+  const bool small = it.nvb < kOzDropMinBlocks;
+  const bool mydiag = arow == it.n0 || small, anydiag = it.m0 == it.n0 || it.m0 + 128 == it.n0 || small;
+  const int kPasses = (oz_dtop_off(nsl) < 4 && !anydiag) ? 1 : 2;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -674,7 +703,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
             const uint64_t da0 = umma_desc_sw128(sa), db0 = umma_desc_sw128(sa + 2 * kOzBox);
             const uint32_t keep = vb == b0 ? 0u : 1u;
             if (hi) {
-              oz_issue_pass_pair<nsl, 1>(tmem, da0, db0, idesc, keep);
+              if (anydiag)
+                oz_issue_pass_pair<nsl, 1>(tmem, da0, db0, idesc, keep);
+              else
+                oz_issue_pass_pair<nsl, 1, oz_dtop_off(nsl)>(tmem, da0, db0, idesc, keep);
             } else {
               const uint64_t boxa = (uint64_t)(kOzBox >> 4), boxb = (uint64_t)(kOzBoxB >> 4);
               const int nj = min(step, b1 - vb);
@@ -710,7 +742,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
         mbar_wait(&accfull, npass & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int dlo = pass ? 4 : 0, dhi = pass ? kOzSlices - 1 : 3;
-        if (!below) {
+        const int dtop = pass ? (mydiag ? kOzSlices - 1 : oz_dtop_off(nsl)) : 3;
+        if (!below && dlo <= dtop) {
           for (int c0 = cbase; c0 < cbase + 64; c0 += 16) {
             double prev[16];
 #pragma unroll
@@ -718,8 +751,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
               prev[j] = (npass > 0 && rin && it.n0 + c0 + j < ldx) ? grow[c0 + j] : 0.0;
             uint32_t raw[4][16];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (dlo + q <= dhi) tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 128u * (uint32_t)q + c0, raw[q]);
+            for (int q = 0; q < 4; ++q) {
+              if (dlo + q <= dtop)
+                tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 128u * (uint32_t)q + c0, raw[q]);
+              else
+#pragma unroll
+                for (int j = 0; j < 16; ++j) raw[q][j] = 0u;
+            }
             tmem_wait_ld();
             double val[16];
 #pragma unroll

@@ -376,7 +376,8 @@ def test_int8_gram_fp32_large_k_ragged(srm):
     assert engines[-1].gram_i8
     r = ref["iters"][-1]
     _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL32, "gram i8 fp32 k=100")
-    for w in m.W:  # the exact final polar: orthonormal to fp64 precision
+    for w in m.W:  # the exact final polar: orthonormal to fp64 precision (a subject this small
+        # keeps every slice pair of its Gram)
         assert np.max(np.abs(w.T @ w - np.eye(100))) <= 1e-12
 
 
@@ -737,18 +738,21 @@ def test_int8_init_term_matches_dmma(srm, dtype, K):
         assert nrel(terms[0][j], terms[1][j]) <= tol, (j, nrel(terms[0][j], terms[1][j]))
 
 
-@pytest.mark.parametrize("dtype,T", [("f64", 1000), ("f32", 300), ("f64", 130)])
-def test_int8_gram_cta_pairs_bit_identical(srm, monkeypatch, dtype, T):
+@pytest.mark.parametrize("dtype,T,V", [("f64", 1000, 1500), ("f32", 300, 1500), ("f64", 130, 1500),
+                                       ("f32", 400, 17000)])
+def test_int8_gram_cta_pairs_bit_identical(srm, monkeypatch, dtype, T, V):
     """X^T X from the CTA-pair kernel (tcgen05 cta_group::2, M = 256) equals the
     single-CTA kernel's bit for bit: same slice products, same exact int32 /
-    int64 sums, same epilogue; odd and even tile counts, partial tiles."""
+    int64 sums, same epilogue; odd and even tile counts, partial tiles; fp32
+    subjects of >= 16384 voxels (pass 1 only off the diagonal) beside a
+    smaller one (every pair)."""
     import torch
 
     from paper_1608_04647_b200 import _lib
     from paper_1608_04647_b200.data import recipe_numpy
     from paper_1608_04647_b200.engine import SrmEngine
 
-    xs, _, _ = recipe_numpy(3, 1500, T, 10, seed=43, dtype=dtype)
+    xs, _, _ = recipe_numpy(3, V, T, 10, seed=43, dtype=dtype)
     xs[2] = xs[2][:977]
     out = []
     for pairs in ("1", "0"):  # the pair kernel is opt-in (no faster at T = 1000)
