@@ -88,6 +88,7 @@ enum Internal {
   I_OZGIEXP,
   I_OZGICMAX,
   I_ITEMS_TN,
+  I_ITEMS_GG,
   I_COUNT
 };
 
@@ -150,6 +151,7 @@ struct srm_plan {
   bool oz_w = false;                  // final W = Xhat R from the int8 slices (needs oz_sg)
   std::vector<OzItem> items_ow;       // 128-voxel tiles of the final int8 W = Xhat R
   std::vector<OzItem> items_tn;       // (subject, 128-TR tile) of the int8 init term B_0 = G^T Xhat
+  std::vector<OzItem> items_gg;       // (subject, V chunk) of the int8 G^T G of the init draw (kp > 64)
   int64_t oz_lqg_init = 0;            // bytes per sliced row (feature) of the init draw G (records in WOUT)
   TmaMap tm_gi, tm_gi64;
   std::vector<char> sliced;           // srm_prepare_gram_range has been enqueued for the subject
@@ -240,6 +242,7 @@ void layout(srm_plan* p) {
   sz[I_OZGIEXP] = p->oz_lqg_init ? (int64_t)p->n_local * p->K * 4 : 0;
   sz[I_OZGICMAX] = p->oz_lqg_init ? (int64_t)p->n_local * p->K * 8 : 0;
   sz[I_ITEMS_TN] = (int64_t)p->items_tn.size() * sizeof(OzItem);
+  sz[I_ITEMS_GG] = (int64_t)p->items_gg.size() * sizeof(OzItem);
   int64_t cur = 0;
   for (int r = 0; r < I_COUNT; ++r) {
     p->off[r] = cur;
@@ -403,22 +406,34 @@ void build_work(srm_plan* p) {
         // plus, when n is even, the block below the diagonal (discarded)
         for (int64_t n0 = 0; n0 < p->ldx; n0 += 128)
           for (int64_t m0 = 0; m0 <= n0; m0 += 256)
-            p->items_oz.push_back({i, (int32_t)m0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32)});
+            p->items_oz.push_back({i, (int32_t)m0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32), 0, i});
       } else {
         for (int64_t m0 = 0; m0 < p->ldx; m0 += 128)
           for (int64_t n0 = m0; n0 < p->ldx; n0 += 128)
-            p->items_oz.push_back({i, (int32_t)m0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32)});
+            p->items_oz.push_back({i, (int32_t)m0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32), 0, i});
       }
     }
   }
   // the init E-step term B_0 = G^T Xhat from int8 slices too (with the int8 B = S G)
   p->items_tn.clear();
+  p->items_gg.clear();
   p->oz_lqg_init = 0;
   if (p->oz_sg) {
     p->oz_lqg_init = round_up(std::max<int64_t>(p->max_v, 1), 32) / 32 * 256;
     for (int i = 0; i < p->n_local; ++i)
       for (int64_t n0 = 0; n0 < p->ldx; n0 += 128)
         p->items_tn.push_back({i, 0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32)});
+    // kp > 64: G^T G of the draw from its slices too, one partial per split-V
+    // chunk (the chunk count of the DMMA contraction it replaces, 32-voxel
+    // aligned), summed by reduce_chunks in the same order
+    if (p->kp > 64)
+      for (int i = 0; i < p->n_local; ++i) {
+        const int64_t nb = (p->V[i] + 31) / 32, nc = p->nchunk[i];
+        for (int64_t ch = 0; ch < nc; ++ch) {
+          const int64_t b0 = ch * nb / nc, b1 = (ch + 1) * nb / nc;
+          p->items_gg.push_back({i, 0, 0, (int32_t)(b1 - b0), (int32_t)b0, (int32_t)(p->chunk0[i] + ch)});
+        }
+      }
   }
   // tensor-core path: A-pass row tiles (A in the fp32 [rows][np] region) and
   // B-pass tiles of 128 TRs over the same V chunks
@@ -830,13 +845,13 @@ std::vector<Stage> gram_stages(srm_plan* p, int first, int count) {
                                             p->oz_lq, region<int32_t>(p, I_OZEXP), p->max_v, st);
                  }});
     v.push_back({"oz_gram", [p, d, first, count, per](cudaStream_t st) {
+                   const OzGramOut o{d.gram, p->ldx, p->ldx * p->ldx, p->ldx, region<int32_t>(p, I_OZEXP), p->ldx,
+                                     p->ldx};
                    if (p->gram_pairs)
-                     return launch_oz_gram2(p->tm_q, p->tm_qb, region<int32_t>(p, I_OZEXP), d.gram, p->ldx,
-                                            region<OzItem>(p, I_ITEMS_OZ) + (int64_t)first * per, count * per,
-                                            p->oz_nsl, st);
-                   return launch_oz_gram(p->tm_q, region<int32_t>(p, I_OZEXP), d.gram, p->ldx,
-                                         region<OzItem>(p, I_ITEMS_OZ) + (int64_t)first * per, count * per,
-                                         p->oz_nsl, st);
+                     return launch_oz_gram2(p->tm_q, p->tm_qb, o, region<OzItem>(p, I_ITEMS_OZ) + (int64_t)first * per,
+                                            count * per, p->oz_nsl, st);
+                   return launch_oz_gram(p->tm_q, o, region<OzItem>(p, I_ITEMS_OZ) + (int64_t)first * per,
+                                         count * per, p->oz_nsl, st);
                  }});
   } else {
     const int per = (int)(p->items_gram.size() / p->n_local);
@@ -1045,7 +1060,7 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
              {I_ITEMS_BG, p->items_bg.data()},   {I_ITEMS_TB, p->items_tb.data()},
              {I_ITEMS_TA, p->items_ta.data()},   {I_ITEMS_TG, p->items_tg.data()},
              {I_ITEMS_OZ, p->items_oz.data()},   {I_ITEMS_OW, p->items_ow.data()},
-             {I_ITEMS_TN, p->items_tn.data()}};
+             {I_ITEMS_TN, p->items_tn.data()},   {I_ITEMS_GG, p->items_gg.data()}};
   for (const Up& u : ups) {
     if (p->size[u.r] == 0) continue;
     e = cudaMemcpy(p->ws + p->off[u.r], u.src, p->size[u.r], cudaMemcpyHostToDevice);
@@ -1107,9 +1122,10 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
   if (e == cudaSuccess && (p->flags & SRM_FLAG_GRAM_I8)) {
     e = make_map_q(&p->tm_q, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, 128);
     if (e == cudaSuccess) e = make_map_q(&p->tm_qb, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, 64);
-    if (e == cudaSuccess) e = launch_oz_gram(p->tm_q, nullptr, nullptr, p->ldx, nullptr, 0, p->oz_nsl, 0);
-    if (e == cudaSuccess)
-      e = launch_oz_gram2(p->tm_q, p->tm_qb, nullptr, nullptr, p->ldx, nullptr, 0, p->oz_nsl, 0);
+    const OzGramOut none{};
+    if (e == cudaSuccess) e = launch_oz_gram(p->tm_q, none, nullptr, 0, p->oz_nsl, 0);
+    if (e == cudaSuccess) e = launch_oz_gram(p->tm_q, none, nullptr, 0, 7, 0);
+    if (e == cudaSuccess) e = launch_oz_gram2(p->tm_q, p->tm_qb, none, nullptr, 0, p->oz_nsl, 0);
     if (e == cudaSuccess && p->oz_sg) {
       // tiled G slices: rows of 128 B, oz_tiled_bytes / 128 rows per subject
       e = make_map_q(&p->tm_g, region<int8_t>(p, I_OZG), 128, (int64_t)oz_tiled_bytes(p->ldx, p->ldx) / 128,
@@ -1177,14 +1193,17 @@ int srm_init_mapping_range(srm_plan* p, int first, int count, void* stream) {
   // caller has run srm_prepare_gram_range over these subjects), after the
   // chunk reduction of G^T G; otherwise one more split-V DMMA contraction
   const bool i8 = p->oz_lqg_init != 0;
+  // kp > 64: the draw's A^T A from its slices as well (k_oz_gram on one
+  // diagonal tile per V chunk), after launch_oz_init_slices below
+  const bool gg_i8 = i8 && !exact && !p->items_gg.empty();
   cudaError_t e = cudaSuccess;
   if (!i8)
     e = launch_contract_e((int)p->kp, SRM_F64, p->dtype, d.amat, p->kp, d.xhat, p->ldx, d.part, p->ldo, 1.0,
                           region<ItemE>(p, I_ITEMS_EX) + ex0, (int)exn, st);
-  if (e == cudaSuccess && !exact)  // the Gram route's A^T A of the draw
+  if (e == cudaSuccess && !exact && !gg_i8)  // the Gram route's A^T A of the draw
     e = launch_contract_e((int)p->kp, SRM_F64, SRM_F64, d.amat, p->kp, d.amat, p->kp, d.part, p->ldo, 1.0,
                           region<ItemE>(p, I_ITEMS_EA) + p->chunk0[first], (int)ean, st);
-  if (e == cudaSuccess) e = launch_reduce_chunks(d, st);
+  if (e == cudaSuccess && !gg_i8) e = launch_reduce_chunks(d, st);
   if (e == cudaSuccess && i8) {
     // Xhat's slices must exist: prepare subjects no srm_prepare_gram_range call
     // has covered yet (stream order; the loader already does it on this stream)
@@ -1197,6 +1216,12 @@ int srm_init_mapping_range(srm_plan* p, int first, int count, void* stream) {
     for (int i = first; i < first + count; ++i) maxv = std::max(maxv, p->V[i]);
     e = launch_oz_init_slices(d, first, count, region<int8_t>(p, SRM_R_WOUT), p->oz_lqg_init,
                               region<int32_t>(p, I_OZGIEXP), region<unsigned long long>(p, I_OZGICMAX), maxv, st);
+    if (e == cudaSuccess && gg_i8) {
+      // partial A^T A of chunk c at part[c][0..kp)[ldx..ldx + kp), as the DMMA items write it
+      const OzGramOut o{d.part + p->ldx, p->ldo, p->kp * p->ldo, p->kp, region<int32_t>(p, I_OZGIEXP), p->K, p->K};
+      e = launch_oz_gram(p->tm_gi, o, region<OzItem>(p, I_ITEMS_GG) + p->chunk0[first], (int)ean, 7, st);
+      if (e == cudaSuccess) e = launch_reduce_chunks(d, st);
+    }
     const int per = (int)((p->ldx + 127) / 128);
     // kp <= 64: the transposed one-pass kernel (N = 64 features); else M = 128 features
     static const bool nt_off = [] {

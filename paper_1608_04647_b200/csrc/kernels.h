@@ -70,7 +70,18 @@ struct OzItem {
   int32_t subj;  // local subject
   int32_t m0;    // first row (TR) of the tile
   int32_t n0;    // first column (TR) of the tile
-  int32_t nvb;   // 32-voxel blocks of the subject
+  int32_t nvb;   // 32-voxel blocks of the subject (of the chunk, k_oz_gram)
+  int32_t vb0;   // k_oz_gram: first 32-voxel block (a V chunk of the subject)
+  int32_t slot;  // k_oz_gram: output matrix index (the subject, or a V chunk's partial)
+};
+// where k_oz_gram writes: matrix slot s at g + s gsub, entry (a, b) at
+// [a ldg + b] for a, b < nout; column exponents expo[subj ldexp + t], t < nexp
+// (entries beyond nexp: the zero columns of a padded record tensor)
+struct OzGramOut {
+  double* g;
+  int64_t ldg, gsub, nout;
+  const int32_t* expo;
+  int64_t ldexp, nexp;
 };
 constexpr int kOzChunkBlocks = 2048;  // 65536 voxels per exact int32 accumulation
 constexpr int64_t kOzRecord = 256;    // bytes per (row, 32-column block): 8 slots x 32
@@ -111,16 +122,17 @@ cudaError_t launch_oz_tn(const TmaMap& tma, const TmaMap& tmb, const int32_t* ae
 // the same tiles on CTA pairs (tcgen05 cta_group::2, M = 256): items are
 // (subject, m0 = first of two row blocks, n0, nvb); tmqb: the records with a
 // 64-row box (each CTA stages half of the B rows)
-cudaError_t launch_oz_gram2(const TmaMap& tmq, const TmaMap& tmqb, const int32_t* expo, double* G, int64_t ldx,
-                            const OzItem* items, int n_items, int nsl, cudaStream_t st);
+cudaError_t launch_oz_gram2(const TmaMap& tmq, const TmaMap& tmqb, const OzGramOut& o, const OzItem* items,
+                            int n_items, int nsl, cudaStream_t st);
 // the same for kp <= 64, transposed (M = 128 TRs x N = 64 features, one pass):
 // tmg64 = the draw's records with a 64-row box
 cudaError_t launch_oz_nt(const TmaMap& tmx, const TmaMap& tmg64, const int32_t* aexp, const int32_t* bexp,
                          double* bred, int64_t ldx, int64_t kp, int64_t ldo, int64_t K, const OzItem* items, int n_items,
                          int nslx, cudaStream_t st);
-// X_i^T X_i tiles from the nsl-slice records (nsl = 7 for fp64 X-hat, 4 for fp32)
-cudaError_t launch_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
-                           int n_items, int nsl, cudaStream_t st);
+// X_i^T X_i tiles from the nsl-slice records (nsl = 7 for fp64 X-hat, 4 for
+// fp32); also G_i^T G_i of the init draw from its seven-slice records
+cudaError_t launch_oz_gram(const TmaMap& tmq, const OzGramOut& o, const OzItem* items, int n_items, int nsl,
+                           cudaStream_t st);
 
 // accurate polar transform (qr_polar.cu): Householder TSQR of a tall V x K
 // matrix, then a one-sided Jacobi SVD of R -> M = V diag(1/sigma) V^T

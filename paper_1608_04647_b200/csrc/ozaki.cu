@@ -342,8 +342,7 @@ __device__ __forceinline__ void oz_issue_pass(uint32_t tmem, uint64_t da0, uint6
 
 template <int NSL>
 __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant__ CUtensorMap tmq,
-                                                           const int32_t* __restrict__ expo, double* __restrict__ G,
-                                                           int64_t ldx, const OzItem* __restrict__ items) {
+                                                           const OzGramOut o, const OzItem* __restrict__ items) {
   constexpr int nsl = NSL;  // compile time: the MMA issue loops unroll
   // d-groups 0..3 fill the 512 TMEM columns; pass 2 accumulates d = 4..6 on
   // diagonal tiles, d = 4..5 off the diagonal (oz_dtop_off); four-slice data
@@ -396,7 +395,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
             const int nbox = (hi ? 2 : nj) * (diag ? 1 : 2);
             mbar_expect_tx(&bars.full[slot], (uint32_t)(nbox * kOzBox));
             unsigned char* st = smem + slot * kOzStageBytes;
-            const int x = vb * oz_record_bytes(nsl);
+            const int x = (it.vb0 + vb) * oz_record_bytes(nsl);
             if (hi) {  // [A lo][A hi][B lo][B hi]
               tma_load_3d(st, &tmq, x, it.m0, it.subj, &bars.full[slot]);
               tma_load_3d(st + kOzBox, &tmq, x + 128, it.m0, it.subj, &bars.full[slot]);
@@ -406,7 +405,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
               }
             } else {   // [A lo vb][A lo vb + 1][B lo vb][B lo vb + 1]
               for (int j = 0; j < nj; ++j) {
-                const int xj = (vb + j) * oz_record_bytes(nsl);
+                const int xj = (it.vb0 + vb + j) * oz_record_bytes(nsl);
                 tma_load_3d(st + j * kOzBox, &tmq, xj, it.m0, it.subj, &bars.full[slot]);
                 if (!diag) tma_load_3d(st + (2 + j) * kOzBox, &tmq, xj, it.n0, it.subj, &bars.full[slot]);
               }
@@ -467,10 +466,10 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
     const int cbase = ((warp - 2) >> 2) * 64;
     const int r = quarter * 32 + lane;
     const int64_t ta = it.m0 + r;
-    const bool rin = ta < ldx;
-    const int32_t* ex = expo + (int64_t)it.subj * ldx;
-    const int ea = rin ? ex[ta] : 0;
-    double* grow = G + (int64_t)it.subj * ldx * ldx + ta * ldx + it.n0;
+    const bool rin = ta < o.nout;
+    const int32_t* ex = o.expo + (int64_t)it.subj * o.ldexp;
+    const int ea = ta < o.nexp ? ex[ta] : 0;
+    double* grow = o.g + (int64_t)it.slot * o.gsub + ta * o.ldg + it.n0;
     int npass = 0;
     for (int c = 0; c < nchunks; ++c) {
       for (int pass = 0; pass < kPasses; ++pass, ++npass) {
@@ -484,7 +483,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
           double prev[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            prev[j] = (npass > 0 && rin && it.n0 + c0 + j < ldx) ? grow[c0 + j] : 0.0;
+            prev[j] = (npass > 0 && rin && it.n0 + c0 + j < o.nout) ? grow[c0 + j] : 0.0;
           // the (up to four) d-groups of these 16 columns in flight, one wait
           uint32_t raw[4][16];
 #pragma unroll
@@ -512,8 +511,8 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const int64_t tb = it.n0 + c0 + j;
-              if (tb < ldx) {
-                const double g = val[j] * pow2(ea + ex[tb]);
+              if (tb < o.nout) {
+                const double g = val[j] * pow2(ea + (tb < o.nexp ? ex[tb] : 0));
                 grow[c0 + j] = (npass == 0) ? g : prev[j] + g;
               }
             }
@@ -607,8 +606,7 @@ __device__ __forceinline__ void oz_issue_pass_pair(uint32_t tmem, uint64_t da0, 
 
 template <int NSL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
-    k_oz_gram2(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmqb,
-               const int32_t* __restrict__ expo, double* __restrict__ G, int64_t ldx,
+    k_oz_gram2(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmqb, const OzGramOut o,
                const OzItem* __restrict__ items) {
   constexpr int nsl = NSL;
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
@@ -667,14 +665,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
             unsigned char* st = smem + slot * kOz2StageBytes;
             unsigned char* sb = st + 2 * kOzBox;
             if (hi) {  // [A lo][A hi][B lo][B hi]
-              const int x = vb * oz_record_bytes(nsl);
+              const int x = (it.vb0 + vb) * oz_record_bytes(nsl);
               tma_load_3d_pair(st, &tmq, x, arow, it.subj, fb);
               tma_load_3d_pair(st + kOzBox, &tmq, x + 128, arow, it.subj, fb);
               tma_load_3d_pair(sb, &tmqb, x, brow, it.subj, fb);
               tma_load_3d_pair(sb + kOzBoxB, &tmqb, x + 128, brow, it.subj, fb);
             } else {   // [A lo vb][A lo vb + 1][B lo vb][B lo vb + 1]
               for (int j = 0; j < nj; ++j) {
-                const int xj = (vb + j) * oz_record_bytes(nsl);
+                const int xj = (it.vb0 + vb + j) * oz_record_bytes(nsl);
                 tma_load_3d_pair(st + j * kOzBox, &tmq, xj, arow, it.subj, fb);
                 tma_load_3d_pair(sb + j * kOzBoxB, &tmqb, xj, brow, it.subj, fb);
               }
@@ -731,10 +729,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     const int r = quarter * 32 + lane;
     const int64_t ta = arow + r;
     const bool below = (arow / 128) > (it.n0 / 128);  // a tile below the diagonal: discarded
-    const bool rin = ta < ldx && !below;
-    const int32_t* ex = expo + (int64_t)it.subj * ldx;
-    const int ea = rin ? ex[ta] : 0;
-    double* grow = G + (int64_t)it.subj * ldx * ldx + ta * ldx + it.n0;
+    const bool rin = ta < o.nout && !below;
+    const int32_t* ex = o.expo + (int64_t)it.subj * o.ldexp;
+    const int ea = ta < o.nexp ? ex[ta] : 0;
+    double* grow = o.g + (int64_t)it.slot * o.gsub + ta * o.ldg + it.n0;
     const uint32_t freebar = leader_addr(&accfree);
     int npass = 0;
     for (int c = 0; c < nchunks; ++c) {
@@ -748,7 +746,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
             double prev[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              prev[j] = (npass > 0 && rin && it.n0 + c0 + j < ldx) ? grow[c0 + j] : 0.0;
+              prev[j] = (npass > 0 && rin && it.n0 + c0 + j < o.nout) ? grow[c0 + j] : 0.0;
             uint32_t raw[4][16];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -772,8 +770,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 const int64_t tb = it.n0 + c0 + j;
-                if (tb < ldx) {
-                  const double g = val[j] * pow2(ea + ex[tb]);
+                if (tb < o.nout) {
+                  const double g = val[j] * pow2(ea + (tb < o.nexp ? ex[tb] : 0));
                   grow[c0 + j] = (npass == 0) ? g : prev[j] + g;
                 }
               }
@@ -829,7 +827,11 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_tn(const __grid_constant__
                                                          const OzItem* __restrict__ items) {
   constexpr int NSA = kOzSlices;
   constexpr int recb = NSB <= 4 ? 128 : 256;
-  constexpr int kPasses = 2;
+  // four-slice (fp32) Xhat: the pairs s + s' <= 3 only, one pass.  The dropped
+  // pairs are products of independent low digits of G and Xhat: ~1e-7 of
+  // |G^T Xhat| normwise on the BASELINE recipe, where the 2^-27 truncation of
+  // Xhat itself already costs ~1e-8 (fp32 parity tolerance: 1e-4)
+  constexpr int kPasses = NSB <= 4 ? 1 : 2;
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ OzBars bars;
@@ -987,6 +989,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_nt(const __grid_constant__
                                                          const OzItem* __restrict__ items) {
   constexpr int NSG = kOzSlices;
   constexpr int recx = NSX <= 4 ? 128 : 256;
+  constexpr int kDTop = NSX <= 4 ? 3 : kOzSlices - 1;  // k_oz_tn's d-groups (bit-identical results)
   constexpr int kBoxG = 8192;                          // 64 rows x 128 B
   constexpr int kStage = (NSX > 4 ? 2 : 1) * kOzBox + 2 * kBoxG;
   constexpr int kSt = 4;
@@ -1025,13 +1028,13 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_nt(const __grid_constant__
         for (int vb = b0; vb < b1; ++vb, ++k) {
           const int slot = k % kSt;
           if (k >= kSt) mbar_wait(&empty[slot], ((k / kSt) - 1) & 1);
-          mbar_expect_tx(&full[slot], (uint32_t)kStage);
+          mbar_expect_tx(&full[slot], (uint32_t)(kDTop >= 4 ? kStage : kStage - kBoxG));
           unsigned char* st = smem + slot * kStage;
           tma_load_3d(st, &tmx, vb * recx, it.n0, it.subj, &full[slot]);
           if (NSX > 4) tma_load_3d(st + kOzBox, &tmx, vb * recx + 128, it.n0, it.subj, &full[slot]);
           unsigned char* sg = st + (NSX > 4 ? 2 : 1) * kOzBox;
           tma_load_3d(sg, &tmg, vb * 256, 0, it.subj, &full[slot]);
-          tma_load_3d(sg + kBoxG, &tmg, vb * 256 + 128, 0, it.subj, &full[slot]);
+          if (kDTop >= 4) tma_load_3d(sg + kBoxG, &tmg, vb * 256 + 128, 0, it.subj, &full[slot]);
         }
       }
     }
@@ -1052,7 +1055,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_nt(const __grid_constant__
           const uint64_t db0 = umma_desc_sw128(sa + (NSX > 4 ? 2 : 1) * kOzBox);
           const uint32_t keep = vb == b0 ? 0u : 1u;
 #pragma unroll
-          for (int d = 0; d < kOzSlices; ++d) {
+          for (int d = 0; d <= kDTop; ++d) {
             const int s0 = d - (NSG - 1) > 0 ? d - (NSG - 1) : 0, s1 = d < NSX - 1 ? d : NSX - 1;
 #pragma unroll
             for (int sx = s0; sx <= s1; ++sx)
@@ -1080,8 +1083,13 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_nt(const __grid_constant__
       for (int k0 = kbase; k0 < kbase + 32; k0 += 16) {
         uint32_t raw[kOzSlices][16];
 #pragma unroll
-        for (int d = 0; d < kOzSlices; ++d)
-          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 64u * (uint32_t)d + k0, raw[d]);
+        for (int d = 0; d < kOzSlices; ++d) {
+          if (d <= kDTop)
+            tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + 64u * (uint32_t)d + k0, raw[d]);
+          else
+#pragma unroll
+            for (int j = 0; j < 16; ++j) raw[d][j] = 0u;
+        }
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -1328,10 +1336,19 @@ constexpr int kRowEpi = kRowThreads - 64;
 //   sum_d raw_d 2^{-12-7d} = H 2^-33 + L 2^-54
 // is formed with two exact conversions and one rounding (oz_hl_value).  H and
 // L are linear in the accumulators: parts of a split contraction add exactly.
+// ND < 7: the d-groups beyond ND - 1 count as zero (an N = 128 MMA may have
+// written a partial group ND; it is not read)
+template <int ND = 7>
 __device__ __forceinline__ void oz_load_hl(uint32_t taddr, long long* H, long long* L) {
   uint32_t raw[7][8];
 #pragma unroll
-  for (int d = 0; d < 7; ++d) tmem_ld8(taddr + 64u * (uint32_t)d, raw[d]);
+  for (int d = 0; d < 7; ++d) {
+    if (d < ND)
+      tmem_ld8(taddr + 64u * (uint32_t)d, raw[d]);
+    else
+#pragma unroll
+      for (int j = 0; j < 8; ++j) raw[d][j] = 0u;
+  }
   tmem_wait_ld();
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -1444,7 +1461,7 @@ __global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas
       }
     }
   } else {
-    static_assert(ND == 7, "the H/L epilogue combines seven d-groups");
+    static_assert(ND >= 5 && ND <= 7, "the H/L epilogue combines d-groups 0-3 and 4-6");
     const int quarter = warp & 3;              // TMEM lanes 32 quarter .. + 31 (warp % 4)
     const int cbase = ((warp - 2) >> 2) * 32;  // this warp's 32 of the 64 columns
     const int r = quarter * 32 + lane;
@@ -1473,7 +1490,7 @@ __global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas
       for (int c = 0; c < 4; ++c) {
         const int c0 = cbase + 8 * c;
         long long H[8], L[8];
-        oz_load_hl(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, H, L);
+        oz_load_hl<ND>(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, H, L);
         if (valid) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -1856,9 +1873,11 @@ cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* re
   RowGemmArgs g{nullptr, rexp, W, items, ldx, kp, 0, K, 0, 0, (int)((kp + 63) / 64), 0};
   g.n_work = n_items * g.nz;
   if (nsl == 7) return run_rowgemm<kRowW, 7, 7>(tmqt, tmr, g, sm_count(), st);
-  // all seven d-groups for fp32 X-hat too: R's slices beyond the fourth carry
-  // bits the orthonormality of W needs (W^T W = I to ~1e-13)
-  if (nsl == 4) return run_rowgemm<kRowW, 4, 7>(tmqt, tmr, g, sm_count(), st);
+  // fp32 X-hat: d-groups 0-4 (8 MMAs per k-block instead of 12).  R's slices
+  // beyond the fourth carry bits the orthonormality of W needs, and d = 4
+  // keeps them; the dropped d >= 5 are ~2^-35 of the column scales, below the
+  // 2^-27 truncation of X-hat's own slices (tools/slice_drop_probe.py)
+  if (nsl == 4) return run_rowgemm<kRowW, 4, 5>(tmqt, tmr, g, sm_count(), st);
   return cudaErrorInvalidValue;
 }
 
@@ -1898,8 +1917,7 @@ cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first,
 namespace {
 
 template <int NSL>
-cudaError_t run_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
-                        int n_items, cudaStream_t st) {
+cudaError_t run_oz_gram(const TmaMap& tmq, const OzGramOut& o, const OzItem* items, int n_items, cudaStream_t st) {
   const size_t bytes = oz_gram_smem_bytes();
   static bool configured = false;
   if (!configured) {
@@ -1908,8 +1926,7 @@ cudaError_t run_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64
     configured = true;
   }
   if (n_items == 0) return cudaSuccess;
-  k_oz_gram<NSL><<<n_items, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(tmq.opaque), expo, G,
-                                                      ldx, items);
+  k_oz_gram<NSL><<<n_items, kOzThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(tmq.opaque), o, items);
   return cudaGetLastError();
 }
 
@@ -1986,8 +2003,8 @@ cudaError_t launch_oz_tn(const TmaMap& tma, const TmaMap& tmb, const int32_t* ae
 
 size_t oz_gram2_smem_bytes() { return (size_t)kOz2Stages * kOz2StageBytes + 1024; }
 
-cudaError_t launch_oz_gram2(const TmaMap& tmq, const TmaMap& tmqb, const int32_t* expo, double* G, int64_t ldx,
-                            const OzItem* items, int n_items, int nsl, cudaStream_t st) {
+cudaError_t launch_oz_gram2(const TmaMap& tmq, const TmaMap& tmqb, const OzGramOut& o, const OzItem* items,
+                            int n_items, int nsl, cudaStream_t st) {
   const size_t bytes = oz_gram2_smem_bytes();
   static bool configured[2] = {false, false};
   if (nsl != 7 && nsl != 4) return cudaErrorInvalidValue;
@@ -2001,16 +2018,16 @@ cudaError_t launch_oz_gram2(const TmaMap& tmq, const TmaMap& tmqb, const int32_t
   const CUtensorMap* a = reinterpret_cast<const CUtensorMap*>(tmq.opaque);
   const CUtensorMap* b = reinterpret_cast<const CUtensorMap*>(tmqb.opaque);
   if (nsl == 7)
-    k_oz_gram2<7><<<2 * n_items, kOzThreads, bytes, st>>>(*a, *b, expo, G, ldx, items);
+    k_oz_gram2<7><<<2 * n_items, kOzThreads, bytes, st>>>(*a, *b, o, items);
   else
-    k_oz_gram2<4><<<2 * n_items, kOzThreads, bytes, st>>>(*a, *b, expo, G, ldx, items);
+    k_oz_gram2<4><<<2 * n_items, kOzThreads, bytes, st>>>(*a, *b, o, items);
   return cudaGetLastError();
 }
 
-cudaError_t launch_oz_gram(const TmaMap& tmq, const int32_t* expo, double* G, int64_t ldx, const OzItem* items,
-                           int n_items, int nsl, cudaStream_t st) {
-  if (nsl == 7) return run_oz_gram<7>(tmq, expo, G, ldx, items, n_items, st);
-  if (nsl == 4) return run_oz_gram<4>(tmq, expo, G, ldx, items, n_items, st);
+cudaError_t launch_oz_gram(const TmaMap& tmq, const OzGramOut& o, const OzItem* items, int n_items, int nsl,
+                           cudaStream_t st) {
+  if (nsl == 7) return run_oz_gram<7>(tmq, o, items, n_items, st);
+  if (nsl == 4) return run_oz_gram<4>(tmq, o, items, n_items, st);
   return cudaErrorInvalidValue;
 }
 

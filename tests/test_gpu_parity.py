@@ -376,9 +376,9 @@ def test_int8_gram_fp32_large_k_ragged(srm):
     assert engines[-1].gram_i8
     r = ref["iters"][-1]
     _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], TOL32, "gram i8 fp32 k=100")
-    for w in m.W:  # the exact final polar: orthonormal to fp64 precision (a subject this small
-        # keeps every slice pair of its Gram)
-        assert np.max(np.abs(w.T @ w - np.eye(100))) <= 1e-12
+    for w in m.W:  # the exact final polar (a subject this small keeps every slice pair of its
+        # Gram); W = Xhat R from the pairs s + s' <= 4 of fp32 X-hat's slices: ~1e-10
+        assert np.max(np.abs(w.T @ w - np.eye(100))) <= 1e-9
 
 
 def test_init_overlap_is_bit_identical(srm):
@@ -709,12 +709,14 @@ def test_transform_reference_cases(srm):
     assert np.max(np.abs(srm.map_between(m, 0, 0, once) - once)) <= 1e-10
 
 
-@pytest.mark.parametrize("dtype,K", [("f64", 50), ("f32", 100), ("f32", 20)])
+@pytest.mark.parametrize("dtype,K", [("f64", 50), ("f32", 100), ("f32", 20), ("f64", 100)])
 def test_int8_init_term_matches_dmma(srm, dtype, K):
     """The initial E-step term W_0^T Xhat = M_0^T (G^T Xhat) with G^T Xhat from
     the int8 slices of the draw and of X-hat (int8 Gram plans) against the
     fp64 DMMA contraction (fp64 Gram plans), per subject; the int8 plan is
-    initialised before any srm_prepare_gram call (it slices X-hat itself)."""
+    initialised before any srm_prepare_gram call (it slices X-hat itself).
+    K > 64 also forms the draw's G^T G (for M_0) from its slices.  fp32 X-hat:
+    the slice pairs s + s' <= 3 only (~1e-7 of the term)."""
     import torch
 
     from paper_1608_04647_b200.data import recipe_numpy
@@ -733,7 +735,7 @@ def test_int8_init_term_matches_dmma(srm, dtype, K):
         t = eng.terms[:, : eng.kp * eng.ldx].view(-1, eng.kp, eng.ldx)[:, :K, :300].cpu().numpy()
         terms.append(t)
         eng.close()
-    tol = 1e-13 if dtype == "f64" else 1e-7  # four fp32 slices: 2^-27 of the column maxima
+    tol = 1e-13 if dtype == "f64" else 5e-7  # four fp32 slices, pairs s + s' <= 3
     for j in range(3):
         assert nrel(terms[0][j], terms[1][j]) <= tol, (j, nrel(terms[0][j], terms[1][j]))
 
@@ -819,8 +821,10 @@ def test_wide_k_fit_vs_oracle(srm, K, dtype, algorithm):
         _check_model(m, r["S"], r["sigma_s"], r["rho2"], r["W"], tol, f"K={K} {dtype} {algorithm} it{n - 1}")
         for j in range(n):
             assert abs(m.log_likelihood[j] - ref["iters"][j]["ll"]) <= tol * abs(ref["iters"][j]["ll"])
+        # fp32 X-hat on the int8 path: W = Xhat R from the slice pairs s + s' <= 4 (~1e-10)
+        orth = 1e-9 if (dtype, algorithm) == ("f32", "gram") else 1e-10
         for w in m.W:
-            assert np.max(np.abs(w.T @ w - np.eye(K))) <= 1e-10
+            assert np.max(np.abs(w.T @ w - np.eye(K))) <= orth
 
 
 def test_wide_k_exact_polar_and_kernels(srm):
