@@ -446,6 +446,8 @@ def run_ours(args):
     del xs
     torch.cuda.empty_cache()
     use_graph = world == 1
+    # N > 1 over NCCL: {all-gather / all-reduce, E-step, M-step} as one graph per rank
+    use_xgraph = world > 1 and eng.exchange_capturable(comm)
     eng.prepare_gram()
     eng.init_mapping(args.seed, start)  # the host PCG64 draws (srm.py:111), uploaded once
     draws = eng.amat.clone()            # each step restarts from them: only device work is timed
@@ -461,10 +463,14 @@ def run_ours(args):
         for _ in range(iters):
             if use_graph and eng._graph is not None:
                 eng.replay()
+            elif use_xgraph and eng._xgraph is not None:
+                eng.replay_exchange()
             else:
                 eng.step(comm)
                 if use_graph:
                     eng.capture()
+                elif use_xgraph:
+                    eng.capture_exchange(comm)  # after one eager exchange
         eng.finalize()
 
     for _ in range(max(1, args.warmup)):  # configures kernels, captures the iteration graph

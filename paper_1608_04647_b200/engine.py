@@ -100,6 +100,7 @@ class SrmEngine:
         self.gram_i8 = bool(eff & _lib.FLAG_GRAM_I8)
         self.exact_polar = bool(eff & _lib.FLAG_EXACT_POLAR)
         self._graph = None
+        self._xgraph = None  # capture_exchange (N > 1 over NCCL)
         self._staging = {}
 
     # ------------------------------------------------------------------ views
@@ -367,10 +368,12 @@ class SrmEngine:
         _lib.check(self.lib.srm_init_mapping(self.plan, ctypes.c_void_p(self.stream())), "init_mapping")
 
     # ------------------------------------------------------------- iteration
-    def exchange(self, comm):
-        """Make every subject's E-step term visible to this rank (srm.py:259-269)."""
+    def exchange(self, comm, force=False):
+        """Make every subject's E-step term visible to this rank (srm.py:259-269).
+        ``force`` runs the device collective even on one rank (an in-place
+        one-rank all-gather: the graph-capture test of :meth:`capture_exchange`)."""
         torch = _torch()
-        if self.world_size == 1:
+        if self.world_size == 1 and not (force and hasattr(comm, "all_gather_into")):
             return
         if hasattr(comm, "all_gather_into"):
             if self.ordered:
@@ -412,6 +415,39 @@ class SrmEngine:
 
     def replay(self):
         _lib.check(self.lib.srm_graph_launch(self.plan, ctypes.c_void_p(self.stream())), "graph_launch")
+
+    def exchange_capturable(self, comm):
+        """True when {exchange, E-step, M-step} can be one CUDA graph: the
+        exchange is a device collective on this GPU (NCCL), not host staging."""
+        return bool(getattr(comm, "device_collectives", False)) and hasattr(comm, "all_gather_into")
+
+    def capture_exchange(self, comm, force=False):
+        """Record one multi-rank EM iteration -- the NCCL all-gather (ordered)
+        or all-reduce (unordered) of the E-step terms, then the E-step tail and
+        the M-step with their side lanes -- as one CUDA graph on this rank.
+        Each rank captures its own graph; the collective's communicator must
+        have run once eagerly first (NCCL sets up its channels outside
+        capture).  Replaces the reference's per-iteration gather + broadcast
+        (srm.py:259-269) and the eager launch sequence of :meth:`step`."""
+        torch = _torch()
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(self.device)
+        cap.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+            self.exchange(comm, force=force)
+            st = ctypes.c_void_p(cap.cuda_stream)
+            _lib.check(self.lib.srm_e_step(self.plan, st), "e_step")
+            _lib.check(self.lib.srm_m_step(self.plan, st), "m_step")
+        torch.cuda.current_stream(self.device).wait_stream(cap)
+        self._xgraph = g
+
+    def replay_exchange(self):
+        """One EM iteration of the :meth:`capture_exchange` graph on the current stream."""
+        torch = _torch()
+        cur = torch.cuda.current_stream(self.device)
+        # CUDAGraph.replay launches on torch's current stream
+        with torch.cuda.stream(cur):
+            self._xgraph.replay()
 
     def prepare_gram(self):
         """One-time X_i^T X_i for the Gram path (no-op on streaming plans)."""

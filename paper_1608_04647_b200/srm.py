@@ -578,7 +578,13 @@ def _fit_pass(subjects, config, comm, *, exact, storage, ordered, graphs, keep_o
     futures = list(draws)  # eng.load consumes `draws`
     clock.tick("setup")
     # pipelined: upload + demean (+ X^T X) (+ the initial mapping) per batch of subjects
-    use_graph = graphs and comm.size == 1
+    # N > 1 over NCCL: the first iteration runs eagerly (it also sets up the
+    # collective's channels), then {all-gather, E-step, M-step} is one graph
+    # per rank.  SRM_B200_FORCE_XGRAPH=1 takes that path on one rank too (an
+    # in-place one-rank all-gather), which is how it is tested on one GPU.
+    force_x = comm.size == 1 and os.environ.get("SRM_B200_FORCE_XGRAPH") == "1"
+    use_xgraph = graphs and (comm.size > 1 or force_x) and eng.exchange_capturable(comm)
+    use_graph = graphs and comm.size == 1 and not use_xgraph
     try:
         eng.load([s.X for s in subjects], gaussians=draws, gram=True, init=init_overlap, capture=use_graph)
     except BaseException:
@@ -609,6 +615,13 @@ def _fit_pass(subjects, config, comm, *, exact, storage, ordered, graphs, keep_o
     for it in range(config.iterations):
         if use_graph:
             eng.replay()  # one EM iteration; the graph was captured during the upload
+        elif use_xgraph and it >= 1:
+            if it == 1:
+                eng.capture_exchange(comm, force=force_x)
+            eng.replay_exchange()
+        elif use_xgraph:
+            eng.exchange(comm, force=force_x)
+            eng.step(None)
         else:
             eng.step(comm)
         n_done = it + 1

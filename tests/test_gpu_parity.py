@@ -925,3 +925,46 @@ def test_fewer_trs_than_features_raises_like_reference(srm, algorithm):
         orc.run_em(xs, 9, 3, seed=3)
     with pytest.raises(RankError):
         srm.fit(_subjects(srm, xs), srm.SrmConfig(k=9, iterations=3, seed=3), algorithm=algorithm)
+
+
+def test_nccl_exchange_graph_bit_identical(srm, monkeypatch):
+    """{NCCL all-gather of the E-step table, E-step, M-step} captured as one
+    CUDA graph per rank (the N > 1 iteration, engine.capture_exchange) and
+    replayed: on a one-rank NCCL group with the in-place all-gather forced
+    into the graph (SRM_B200_FORCE_XGRAPH=1), the fit equals the
+    single-rank native graph bit for bit, and the collective is issued from
+    Python only twice (the eager first iteration and the capture)."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1608_04647_b200.collectives import TorchCommunicator
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(4, 700, 150, 12, seed=17)
+    cfg = srm.SrmConfig(k=12, iterations=6, seed=4)
+    own = not dist.is_initialized()
+    if own:
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    try:
+        comm = TorchCommunicator()
+        assert comm.device_collectives
+        for algorithm in ("gram", "stream"):
+            monkeypatch.setenv("SRM_B200_FORCE_XGRAPH", "1")
+            before = comm.stats.allgather_calls
+            a = srm.fit(_subjects(srm, xs), cfg, comm, algorithm=algorithm)
+            assert comm.stats.allgather_calls - before == 2, algorithm
+            monkeypatch.delenv("SRM_B200_FORCE_XGRAPH")
+            b = srm.fit(_subjects(srm, xs), cfg, algorithm=algorithm)
+            assert np.array_equal(a.S, b.S) and np.array_equal(a.sigma_s, b.sigma_s), algorithm
+            assert np.array_equal(a.rho2, b.rho2) and a.log_likelihood == b.log_likelihood, algorithm
+            for wa, wb in zip(a.W, b.W):
+                assert np.array_equal(wa, wb), algorithm
+    finally:
+        if own:
+            dist.destroy_process_group()
