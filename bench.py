@@ -21,7 +21,9 @@ voxels x 1,000 TRs, k=50, fp64, 20 iterations); subjects are sharded across
 ranks (strong scaling, cli.py:82-85 contiguous shards).
 
 Under torchrun (N > 1) every rank drives one GPU over NCCL; the per-iteration
-exchange is one all-gather of the ordered E-step table.
+exchange is the ordered column-block exchange (an all-to-all of the E-step
+terms in N TR blocks, ordered block sums, an all-gather of K x T / N),
+captured with the iteration in one CUDA graph per rank.
 """
 
 import argparse
@@ -103,7 +105,8 @@ def config_json(cfg, name, world):
         "n_subjects": cfg["n_subjects"], "n_voxels": cfg["n_voxels"], "n_trs": cfg["n_trs"], "k": cfg["k"],
         "fit_iterations": cfg["iterations"], "x_bytes": xbytes,
         "l2_policy": f"inputs larger than L2 ({xbytes / 1e9:.1f} GB of X-hat streamed per pass vs 126 MB L2)",
-        "parallelism": f"subject shards x {world} ranks (contiguous, cli.py:82-85); ordered all-gather per iteration",
+        "parallelism": (f"subject shards x {world} ranks (contiguous, cli.py:82-85); ordered column-block "
+                        "exchange per iteration (all-to-all + all-gather of K x T / N)"),
     }
 
 
@@ -432,7 +435,8 @@ def run_ours(args):
                                     torch.cuda.mem_get_info(dev)[0] * world, storage=cfg["dtype"],
                                     gram_int8=use_i8)
     eng = SrmEngine([V] * n_local, T, K, iters, storage=cfg["dtype"], world_size=world, rank=rank,
-                    counts=counts, ordered=True, gram=(algo == "gram"), tc=(cfg["dtype"] == "f32"),
+                    counts=counts, ordered=True, colblock=world > 1 and hasattr(comm, "all_to_all_into"),
+                    gram=(algo == "gram"), tc=(cfg["dtype"] == "f32"),
                     gram_i8=(algo == "gram" and use_i8), device=dev)
     use_i8 = eng.gram_i8
     eng.load(xs)
@@ -518,6 +522,8 @@ def run_ours(args):
             for name, t_ms in eng.profile_gram():
                 prof_g.setdefault(name, []).append(t_ms)
         once.update({k_: float(np.mean(v_)) for k_, v_ in prof_g.items()})
+        if "oz_gram_pairs" in once:  # SRM_B200_GRAM_PAIRS=1: the CTA-pair tiles are part of the Gram
+            once["oz_gram"] = once.get("oz_gram", 0.0) + once.pop("oz_gram_pairs")
     prof_f = {}
     for _ in range(3):
         for name, t_ms in eng.profile_finalize():

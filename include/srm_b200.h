@@ -74,10 +74,19 @@ enum srm_flags {
                              exact int8 slices per value (power-of-two column
                              scales) on the tcgen05 int8 tensor cores, ~2^-48
                              relative to the column maxima; otherwise fp64 DMMA */
-  SRM_FLAG_EXACT_POLAR = 32 /* every polar transform (init and M-step) from A itself:
+  SRM_FLAG_EXACT_POLAR = 32, /* every polar transform (init and M-step) from A itself:
                              Householder TSQR + one-sided Jacobi SVD of R, never
                              A^T A; implies the fp64 streaming path (A_i = X_i S^T / 2
                              formed each iteration; clears GRAM, GRAM_I8, TC) */
+  SRM_FLAG_COLBLOCK = 64  /* world_size > 1: the ordered accumulation of srm.py:193-213
+                             by TR column blocks -- each rank's terms cut into
+                             world_size column blocks and exchanged all-to-all
+                             (SRM_R_XSEND -> SRM_R_XRECV), every rank sums its block
+                             over all subjects in ascending global order
+                             (srm_xchg_reduce), the K x T / world_size results are
+                             all-gathered (SRM_R_XRED) and unpacked into SRM_R_RED.
+                             Bit-identical to one rank, with 1 / world_size of the
+                             all-gather's traffic; overrides SRM_FLAG_ORDERED */
 };
 
 /* workspace regions (srm_plan_region) */
@@ -97,7 +106,10 @@ enum srm_region {
   SRM_R_SCAL = 12,    /* [n_local x 8] f64: per-subject scalars                        */
   SRM_R_GRAM = 13,    /* [n_local x ldx x ldx] f64/f32: X_i^T X_i (SRM_FLAG_GRAM only) */
   SRM_R_VAR = 14,     /* [kp x kp] f64: posterior covariance var_s                     */
-  SRM_R_COUNT = 15
+  SRM_R_XSEND = 15,   /* SRM_FLAG_COLBLOCK: [world x max_local x xrec] f64 column blocks  */
+  SRM_R_XRECV = 16,   /*   ... received: [world (source rank) x max_local x xrec]          */
+  SRM_R_XRED = 17,    /*   [world x xred] f64: the reduced blocks (this rank's at `rank`) */
+  SRM_R_COUNT = 18
 };
 
 /* plan dimensions (srm_plan_dim) */
@@ -114,7 +126,9 @@ enum srm_dim {
   SRM_D_ITEMS_A = 9,      /* work items of the T-contraction kernel     */
   SRM_D_CHUNK_ROWS = 10,  /* rows per V chunk                           */
   SRM_D_LAUNCHES = 11,    /* kernel launches per EM iteration (e+m step) */
-  SRM_D_FLAGS = 12        /* effective plan flags                        */
+  SRM_D_FLAGS = 12,       /* effective plan flags                        */
+  SRM_D_XREC = 13,        /* SRM_FLAG_COLBLOCK: doubles per block record */
+  SRM_D_XRED = 14         /*   doubles per reduced block                  */
 };
 
 /* per-iteration history columns (SRM_R_HIST, hist_stride doubles per row) */
@@ -209,6 +223,18 @@ int srm_reset(srm_plan* plan, void* stream);
  */
 int srm_set_iteration(srm_plan* plan, int iteration, void* stream);
 int srm_reduce_local(srm_plan* plan, void* stream);
+/* SRM_FLAG_COLBLOCK exchange, around an all-to-all of SRM_R_XSEND into
+ * SRM_R_XRECV (equal splits of max_local * xrec doubles) and an all-gather of
+ * this rank's block of SRM_R_XRED:
+ *   srm_xchg_pack: this rank's E-step terms (and record scalars) cut into
+ *     world column blocks of ceil(ldx / world) TRs -> SRM_R_XSEND;
+ *   srm_xchg_reduce: its own block summed over every subject of every rank in
+ *     ascending global order (srm.py:193-213, the same left fold as one rank),
+ *     plus the scalar sums -> SRM_R_XRED[rank];
+ *   srm_xchg_unpack: the gathered blocks -> SRM_R_RED. */
+int srm_xchg_pack(srm_plan* plan, void* stream);
+int srm_xchg_reduce(srm_plan* plan, void* stream);
+int srm_xchg_unpack(srm_plan* plan, void* stream);
 int srm_e_step(srm_plan* plan, void* stream);
 int srm_m_step(srm_plan* plan, void* stream);
 int srm_finalize(srm_plan* plan, void* stream);

@@ -40,6 +40,9 @@ SIGNATURES = [
     ("srm_reset", c_int, [c_vp, c_vp]),
     ("srm_set_iteration", c_int, [c_vp, c_int, c_vp]),
     ("srm_reduce_local", c_int, [c_vp, c_vp]),
+    ("srm_xchg_pack", c_int, [c_vp, c_vp]),
+    ("srm_xchg_reduce", c_int, [c_vp, c_vp]),
+    ("srm_xchg_unpack", c_int, [c_vp, c_vp]),
     ("srm_e_step", c_int, [c_vp, c_vp]),
     ("srm_m_step", c_int, [c_vp, c_vp]),
     ("srm_finalize", c_int, [c_vp, c_vp]),
@@ -76,12 +79,12 @@ SIGNATURES = [
 
 # include/srm_b200.h enums
 SRM_F64, SRM_F32 = 0, 1
-FLAG_ORDERED, FLAG_TOLERANCE, FLAG_GRAM, FLAG_TC, FLAG_GRAM_I8, FLAG_EXACT_POLAR = 1, 2, 4, 8, 16, 32
+FLAG_ORDERED, FLAG_TOLERANCE, FLAG_GRAM, FLAG_TC, FLAG_GRAM_I8, FLAG_EXACT_POLAR, FLAG_COLBLOCK = 1, 2, 4, 8, 16, 32, 64
 WARN_POLAR_CONDITION = 1
 (R_XHAT, R_AMAT, R_WOUT, R_MU, R_TERMS, R_RED, R_REDLOCAL, R_S, R_SIGMA, R_HIST, R_STATUS,
- R_MMAT, R_SCAL, R_GRAM, R_VAR) = range(15)
+ R_MMAT, R_SCAL, R_GRAM, R_VAR, R_XSEND, R_XRECV, R_XRED) = range(18)
 (D_LDX, D_KP, D_ROWS, D_TERM_STRIDE, D_RED_STRIDE, D_HIST_STRIDE, D_N_SLOTS, D_SLOT_OFFSET,
- D_ITEMS_E, D_ITEMS_A, D_CHUNK_ROWS, D_LAUNCHES, D_FLAGS) = range(13)
+ D_ITEMS_E, D_ITEMS_A, D_CHUNK_ROWS, D_LAUNCHES, D_FLAGS, D_XREC, D_XRED) = range(15)
 H_LL, H_TRACE, H_RHO0, H_SDIFF, H_SPREV, H_RHO2 = 0, 1, 2, 3, 4, 8
 REC_RHO2, REC_V, REC_SQNORM, REC_SCALARS = 0, 1, 2, 8
 RED_RHO0, RED_VLOGRHO, RED_SQRHO, RED_VSUM = 0, 1, 2, 3

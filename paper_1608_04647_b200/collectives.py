@@ -58,6 +58,8 @@ class CollectiveStats:
     allgather_bytes: int = 0
     allreduce_calls: int = 0
     allreduce_bytes: int = 0
+    alltoall_calls: int = 0
+    alltoall_bytes: int = 0
     seconds: float = field(default=0.0)
 
 
@@ -134,6 +136,17 @@ class Communicator:
         self.stats.allgather_calls += 1
         self.stats.allgather_bytes += mine.numel() * mine.element_size()
 
+    def all_to_all_into(self, out, inp):
+        """``out`` chunk r <- rank r's ``inp`` chunk for this rank (equal
+        chunks of ``inp.numel() / size`` elements)."""
+        t0 = time.perf_counter()
+        try:
+            self._all_to_all_into(out, inp)
+        finally:
+            self.stats.seconds += time.perf_counter() - t0
+        self.stats.alltoall_calls += 1
+        self.stats.alltoall_bytes += inp.numel() * inp.element_size()
+
     def all_reduce_sum(self, buf):
         t0 = time.perf_counter()
         try:
@@ -182,6 +195,10 @@ class SerialCommunicator(Communicator):
 
     def _all_reduce_sum(self, buf):
         pass
+
+    def _all_to_all_into(self, out, inp):
+        if out.data_ptr() != inp.data_ptr():
+            out.copy_(inp.reshape(out.shape))
 
 
 class TorchCommunicator(Communicator):
@@ -264,6 +281,17 @@ class TorchCommunicator(Communicator):
         parts = [torch.empty_like(host) for _ in range(self.size)]
         self._dist.all_gather(parts, host, group=self._group)
         out.view(-1).copy_(torch.cat(parts).to(out.device))
+
+    def _all_to_all_into(self, out, inp):
+        if self.device_collectives and out.is_cuda:
+            self._dist.all_to_all_single(out.view(-1), inp.reshape(-1), group=self._group)
+            return
+        import torch
+
+        host_in = inp.detach().reshape(-1).cpu()
+        host_out = torch.empty_like(host_in)
+        self._dist.all_to_all_single(host_out, host_in, group=self._group)
+        out.view(-1).copy_(host_out.to(out.device))
 
     def _all_reduce_sum(self, buf):
         if self.device_collectives and buf.is_cuda:

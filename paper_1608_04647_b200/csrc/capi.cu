@@ -89,6 +89,8 @@ enum Internal {
   I_OZGICMAX,
   I_ITEMS_TN,
   I_ITEMS_GG,
+  I_ITEMS_OZ2,
+  I_XCOUNTS,
   I_COUNT
 };
 
@@ -135,12 +137,17 @@ struct srm_plan {
   bool lanes_ready = false;
   std::vector<cudaEvent_t> gram_events;  // per-batch "slices ready" of the pipelined Gram
   cudaStream_t hi_stream = nullptr;      // high-priority stream of the pipelined Gram
+  cudaStream_t hi_stream2 = nullptr;     // ... and of its CTA-pair tiles
+  std::vector<cudaEvent_t> pair_events;  // per-batch "pair tiles done"
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   TmaMap tm_x_a, tm_s, tm_a, tm_x_b;  // tensor-core path TMA maps (bound at srm_plan_bind)
-  std::vector<OzItem> items_oz;       // int8-sliced Gram tiles (SRM_FLAG_GRAM_I8): single CTAs, or
-                                      // with gram_pairs (subject, 256-row pair, n0) for CTA pairs
-  bool gram_pairs = false;            // the int8 Gram on CTA pairs (k_oz_gram2)
+  std::vector<OzItem> items_oz;       // int8-sliced Gram tiles (SRM_FLAG_GRAM_I8) on single CTAs
+  std::vector<OzItem> items_oz2;      // with gram_pairs: (subject, 256-row pair, n0) tiles on CTA pairs
+  bool gram_pairs = false;            // off-diagonal tile pairs on CTA pairs (k_oz_gram2)
+  // one rank, polar_cross: the next E-step's K x K tail (k_tail_kk, needs only
+  // Sigma_s^{-1} and rho0) runs at the end of the M-step beside apply_m
+  bool early_kk = false;
   TmaMap tm_qb;                       // the X-hat records with a 64-row box (the pairs' B halves)
   int64_t oz_lq = 0, max_v = 0;       // bytes per sliced TR row; largest local V
   int oz_nsl = 7;                     // int8 slices per X-hat value: 7 (fp64), 4 (fp32)
@@ -190,6 +197,14 @@ void layout(srm_plan* p) {
   sz[SRM_R_SCAL] = (int64_t)p->n_local * 8 * 8;
   sz[SRM_R_GRAM] = (p->flags & SRM_FLAG_GRAM) ? (int64_t)p->n_local * p->ldx * p->ldx * 8 : 0;
   sz[SRM_R_VAR] = kp2 * 8;
+  // SRM_FLAG_COLBLOCK exchange buffers
+  const bool cb = (p->flags & SRM_FLAG_COLBLOCK) != 0;
+  const int64_t xw = (p->ldx + p->world - 1) / p->world;
+  const int64_t xrec = p->kp * xw + kRecScalars, xred = p->kp * xw + kRedScalars;
+  sz[SRM_R_XSEND] = cb ? (int64_t)p->world * p->max_local * xrec * 8 : 0;
+  sz[SRM_R_XRECV] = sz[SRM_R_XSEND];
+  sz[SRM_R_XRED] = cb ? (int64_t)p->world * xred * 8 : 0;
+  sz[I_XCOUNTS] = cb ? (int64_t)p->world * 4 : 0;
   sz[I_ROWSQ] = p->rows_total * 8;
   sz[I_CMAT] = kp2 * 8;
   sz[I_TAILSCR] = kTailScalars * 8;
@@ -221,6 +236,7 @@ void layout(srm_plan* p) {
   sz[I_OZCMAX] = i8 ? (int64_t)p->n_local * p->ldx * 8 : 0;
   sz[I_OZEXP] = i8 ? (int64_t)p->n_local * p->ldx * 4 : 0;
   sz[I_ITEMS_OZ] = (int64_t)p->items_oz.size() * sizeof(OzItem);
+  sz[I_ITEMS_OZ2] = (int64_t)p->items_oz2.size() * sizeof(OzItem);
   const int gfb_chunks = (int)((p->ldx + kGfbCols - 1) / kGfbCols);
   sz[I_GFBPART] = (int64_t)p->n_local * gfb_chunks * kp2 * 8;
   sz[I_GFBCOUNT] = (int64_t)p->n_local * 4;
@@ -258,6 +274,12 @@ void layout(srm_plan* p) {
   d.n_order = (int)p->order.size();
   d.flags = p->flags;
   d.xf32 = p->dtype == SRM_F32 ? 1 : 0;
+  // the M-step polar is one of the Newton-Schulz kernels (launch_eig_polar's
+  // dispatch), which then also form the cross term; not on the exact route
+  d.polar_cross = !(p->flags & SRM_FLAG_EXACT_POLAR) &&
+                  (ns_polar_supported((int)p->kp) || ns_polar_g_supported((int)p->kp)) &&
+                  !getenv("SRM_B200_APPLY_CROSS");
+  p->early_kk = d.polar_cross && p->world == 1;
   d.T = p->T;
   d.K = p->K;
   d.ldx = p->ldx;
@@ -364,6 +386,7 @@ void build_work(srm_plan* p) {
   }
   // int8-sliced Gram: the same upper tiles, slices [n_local][ldx][oz_lq]
   p->items_oz.clear();
+  p->items_oz2.clear();
   p->max_v = 0;
   for (int i = 0; i < p->n_local; ++i) p->max_v = std::max(p->max_v, p->V[i]);
   p->oz_nsl = p->dtype == SRM_F64 ? 7 : 4;
@@ -393,24 +416,37 @@ void build_work(srm_plan* p) {
     p->ow_first.push_back((int)p->items_ow.size());
   }
   {
-    // SRM_B200_GRAM_PAIRS=1: the CTA-pair kernel (bit-identical; measured no
-    // faster at T = 1000 -- 12.9 vs 12.5 ms on cfg 2 -- the pairs' extra
-    // below-diagonal blocks (40 vs 36 tiles) cost what the halved B staging saves)
+    // SRM_B200_GRAM_PAIRS=1: the off-diagonal tiles of each column block two
+    // row blocks at a time on CTA pairs (k_oz_gram2, cta_group::2, M = 256:
+    // each CTA stages half of the shared B rows, a quarter less operand
+    // traffic through the tensor core's shared-memory port), the diagonal
+    // tiles and the odd leftover on single CTAs -- the same 36 tiles at T =
+    // 1000, none below the diagonal.  Bit-identical to the single-CTA grid.
+    // Opt-in: the pair and single tiles run concurrently in each batch of the
+    // pipelined Gram, and the Gram stage alone is 10% faster on four-slice
+    // records (cfg 5: 61 vs 69 ms), but the whole fit is not (166 vs 164 ms at
+    // the power-capped clock); on seven-slice records the pairs are slower
     const char* env = getenv("SRM_B200_GRAM_PAIRS");
     p->gram_pairs = env && env[0] == '1';
   }
   if (p->flags & SRM_FLAG_GRAM_I8) {
     for (int i = 0; i < p->n_local; ++i) {
-      if (p->gram_pairs) {
-        // column block n, row blocks (2j, 2j + 1) for 2j <= n: the upper tiles
-        // plus, when n is even, the block below the diagonal (discarded)
-        for (int64_t n0 = 0; n0 < p->ldx; n0 += 128)
-          for (int64_t m0 = 0; m0 <= n0; m0 += 256)
-            p->items_oz.push_back({i, (int32_t)m0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32), 0, i});
-      } else {
-        for (int64_t m0 = 0; m0 < p->ldx; m0 += 128)
-          for (int64_t n0 = m0; n0 < p->ldx; n0 += 128)
-            p->items_oz.push_back({i, (int32_t)m0, (int32_t)n0, (int32_t)((p->V[i] + 31) / 32), 0, i});
+      const OzItem base{i, 0, 0, (int32_t)((p->V[i] + 31) / 32), 0, i};
+      for (int64_t n0 = 0; n0 < p->ldx; n0 += 128) {
+        int64_t m0 = 0;
+        if (p->gram_pairs)
+          for (; m0 + 128 < n0; m0 += 256) {
+            OzItem it = base;
+            it.m0 = (int32_t)m0;
+            it.n0 = (int32_t)n0;
+            p->items_oz2.push_back(it);
+          }
+        for (; m0 <= n0; m0 += 128) {
+          OzItem it = base;
+          it.m0 = (int32_t)m0;
+          it.n0 = (int32_t)n0;
+          p->items_oz.push_back(it);
+        }
       }
     }
   }
@@ -551,6 +587,17 @@ void set_pointers(srm_plan* p) {
   d.n_hist = std::max(p->iterations, 1);
   d.subj = region<int64_t>(p, I_SUBJ);
   d.order = region<int32_t>(p, I_ORDER);
+  d.world = p->world;
+  d.rank = p->rank;
+  d.max_local = p->max_local;
+  d.xw = (int)((p->ldx + p->world - 1) / p->world);
+  d.xrec = p->kp * d.xw + kRecScalars;
+  d.xred = p->kp * d.xw + kRedScalars;
+  const bool cbx = (p->flags & SRM_FLAG_COLBLOCK) != 0;
+  d.xsend = cbx ? region<double>(p, SRM_R_XSEND) : nullptr;
+  d.xrecv = cbx ? region<double>(p, SRM_R_XRECV) : nullptr;
+  d.xredbuf = cbx ? region<double>(p, SRM_R_XRED) : nullptr;
+  d.xcounts = cbx ? region<int32_t>(p, I_XCOUNTS) : nullptr;
 }
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
@@ -581,8 +628,9 @@ void contraction_stages(srm_plan* p, std::vector<Stage>& out) {
 std::vector<Stage> e_stages(srm_plan* p) {
   const DevPlan& d = p->dp;
   std::vector<Stage> v;
-  // var_s and C (needs only Sigma_s^{-1} and rho0) beside the ordered sum
-  v.push_back({"tail_kk", [d](cudaStream_t st) { return launch_tail_kk(d, st); }, 1});
+  // var_s and C (needs only Sigma_s^{-1} and rho0) beside the ordered sum --
+  // or already done by the previous M-step (early_kk)
+  if (!p->early_kk) v.push_back({"tail_kk", [d](cudaStream_t st) { return launch_tail_kk(d, st); }, 1});
   if (p->flags & SRM_FLAG_ORDERED) {
     const int n = (int)p->order.size();
     bool ident = true;
@@ -608,6 +656,22 @@ void push_finalize_rho(const DevPlan& d, std::vector<Stage>& v) {
     v.push_back({"finalize_rho", [d](cudaStream_t st) { return launch_finalize_rho(d, 0, st); }, 0, true});
     v.push_back({"advance_iteration", [d](cudaStream_t st) { return launch_set_iteration(d, 0, 1, st); }});
   }
+}
+
+// after the polar of the M-step: P = M^T B (apply_m), rho_i^2 and the counter
+// (finalize_rho).  With the cross term from the polar (polar_cross) rho_i^2 no
+// longer waits for apply_m; on one rank the next E-step's tail_kk then runs on
+// the side lane beside apply_m (early_kk).
+void push_polar_tail(srm_plan* p, std::vector<Stage>& v) {
+  const DevPlan& d = p->dp;
+  if (!d.polar_cross) {
+    v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 1, st); }});
+    push_finalize_rho(d, v);
+    return;
+  }
+  push_finalize_rho(d, v);
+  if (p->early_kk) v.push_back({"tail_kk", [d](cudaStream_t st) { return launch_tail_kk(d, st); }, 1});
+  v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 0, st); }});
 }
 
 // SRM_FLAG_EXACT_POLAR: M_i of local subjects [first, first + count) from A_i
@@ -674,8 +738,7 @@ std::vector<Stage> m_stages(srm_plan* p) {
     }
     v.push_back({"gram_from_b", [d](cudaStream_t st) { return launch_gram_from_b(d, st); }});
     v.push_back({"eig_polar", [d](cudaStream_t st) { return launch_eig_polar(d, 0, st); }});
-    v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 1, st); }});
-    push_finalize_rho(d, v);
+    push_polar_tail(p, v);
     return v;
   }
   if (p->flags & SRM_FLAG_TC) {
@@ -701,8 +764,7 @@ std::vector<Stage> m_stages(srm_plan* p) {
   v.push_back({"reduce_chunks", [d](cudaStream_t st) { return launch_reduce_chunks(d, st); }});
   v.push_back({"gram_from_b", [d](cudaStream_t st) { return launch_gram_from_b(d, st); }});
   v.push_back({"eig_polar", [d](cudaStream_t st) { return launch_eig_polar(d, 0, st); }});
-  v.push_back({"apply_m", [d](cudaStream_t st) { return launch_apply_m(d, 1, st); }});
-  push_finalize_rho(d, v);
+  push_polar_tail(p, v);
   return v;
 }
 
@@ -844,12 +906,16 @@ std::vector<Stage> gram_stages(srm_plan* p, int first, int count) {
                                             region<unsigned long long>(p, I_OZCMAX), region<int8_t>(p, I_OZQ),
                                             p->oz_lq, region<int32_t>(p, I_OZEXP), p->max_v, st);
                  }});
-    v.push_back({"oz_gram", [p, d, first, count, per](cudaStream_t st) {
-                   const OzGramOut o{d.gram, p->ldx, p->ldx * p->ldx, p->ldx, region<int32_t>(p, I_OZEXP), p->ldx,
-                                     p->ldx};
-                   if (p->gram_pairs)
-                     return launch_oz_gram2(p->tm_q, p->tm_qb, o, region<OzItem>(p, I_ITEMS_OZ) + (int64_t)first * per,
-                                            count * per, p->oz_nsl, st);
+    const OzGramOut o{d.gram, p->ldx, p->ldx * p->ldx, p->ldx, region<int32_t>(p, I_OZEXP), p->ldx, p->ldx};
+    if (!p->items_oz2.empty()) {
+      // the CTA-pair tiles (the batched prepare runs them beside the single tiles)
+      const int per2 = (int)(p->items_oz2.size() / p->n_local);
+      v.push_back({"oz_gram_pairs", [p, o, first, count, per2](cudaStream_t st) {
+                     return launch_oz_gram2(p->tm_q, p->tm_qb, o, region<OzItem>(p, I_ITEMS_OZ2) + (int64_t)first * per2,
+                                            count * per2, p->oz_nsl, st);
+                   }});
+    }
+    v.push_back({"oz_gram", [p, o, first, count, per](cudaStream_t st) {
                    return launch_oz_gram(p->tm_q, o, region<OzItem>(p, I_ITEMS_OZ) + (int64_t)first * per,
                                          count * per, p->oz_nsl, st);
                  }});
@@ -946,6 +1012,8 @@ int srm_plan_create(srm_plan** out, int dtype, int n_local, const int64_t* n_vox
   p->counts.assign(counts_per_rank, counts_per_rank + world_size);
   p->flags = flags;
   if (world_size == 1) p->flags |= SRM_FLAG_ORDERED;
+  // column-block exchange: multi-rank only; it replaces the gathered table
+  if (p->flags & SRM_FLAG_COLBLOCK) p->flags &= world_size > 1 ? ~SRM_FLAG_ORDERED : ~SRM_FLAG_COLBLOCK;
   if ((p->flags & SRM_FLAG_TC) && (dtype != SRM_F32 || !tc_supported((int)k))) p->flags &= ~SRM_FLAG_TC;
   if ((p->flags & SRM_FLAG_TC) && (p->flags & SRM_FLAG_GRAM)) p->flags &= ~SRM_FLAG_TC;
   if ((p->flags & SRM_FLAG_GRAM_I8) && !(p->flags & SRM_FLAG_GRAM)) p->flags &= ~SRM_FLAG_GRAM_I8;
@@ -1000,6 +1068,8 @@ int srm_plan_destroy(srm_plan* plan) {
       }
     for (cudaEvent_t ev : plan->gram_events) cudaEventDestroy(ev);
     if (plan->hi_stream) cudaStreamDestroy(plan->hi_stream);
+    if (plan->hi_stream2) cudaStreamDestroy(plan->hi_stream2);
+    for (cudaEvent_t ev : plan->pair_events) cudaEventDestroy(ev);
   }
   delete plan;
   return SRM_OK;
@@ -1022,6 +1092,8 @@ int64_t srm_plan_dim(const srm_plan* p, int which) {
     case SRM_D_ITEMS_A: return (int64_t)p->items_a.size();
     case SRM_D_CHUNK_ROWS: return p->chunk_rows;
     case SRM_D_FLAGS: return p->flags;
+    case SRM_D_XREC: return p->kp * ((p->ldx + p->world - 1) / p->world) + kRecScalars;
+    case SRM_D_XRED: return p->kp * ((p->ldx + p->world - 1) / p->world) + kRedScalars;
     case SRM_D_LAUNCHES: return (int64_t)(e_stages(const_cast<srm_plan*>(p)).size() + m_stages(const_cast<srm_plan*>(p)).size());
     default: return -1;
   }
@@ -1060,7 +1132,8 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
              {I_ITEMS_BG, p->items_bg.data()},   {I_ITEMS_TB, p->items_tb.data()},
              {I_ITEMS_TA, p->items_ta.data()},   {I_ITEMS_TG, p->items_tg.data()},
              {I_ITEMS_OZ, p->items_oz.data()},   {I_ITEMS_OW, p->items_ow.data()},
-             {I_ITEMS_TN, p->items_tn.data()},   {I_ITEMS_GG, p->items_gg.data()}};
+             {I_ITEMS_TN, p->items_tn.data()},   {I_ITEMS_GG, p->items_gg.data()},
+             {I_ITEMS_OZ2, p->items_oz2.data()},  {I_XCOUNTS, p->counts.data()}};
   for (const Up& u : ups) {
     if (p->size[u.r] == 0) continue;
     e = cudaMemcpy(p->ws + p->off[u.r], u.src, p->size[u.r], cudaMemcpyHostToDevice);
@@ -1240,6 +1313,8 @@ int srm_init_mapping_range(srm_plan* p, int first, int count, void* stream) {
   if (e == cudaSuccess) e = exact ? launch_exact_polar(p, first, count, true, st) : launch_eig_polar(d, 1, st);
   if (e == cudaSuccess) e = launch_apply_m(d, 0, st);
   if (e == cudaSuccess) e = launch_finalize_rho(d, 1, st);
+  // early_kk: the first E-step's K x K tail once every rho_i^2 = 1 is in place
+  if (e == cudaSuccess && p->early_kk && first + count == p->n_local) e = launch_tail_kk(p->dp, st);
   return check(e, "init_mapping");
 }
 
@@ -1248,6 +1323,21 @@ int srm_init_mapping(srm_plan* p, void* stream) {
   const int rc = srm_init_mapping_range(p, 0, p->n_local, stream);
   if (rc) return rc;
   return check(launch_set_iteration(p->dp, 0, 0, as_stream(stream)), "init_mapping");
+}
+
+int srm_xchg_pack(srm_plan* p, void* stream) {
+  if (!p || !p->ws || !(p->flags & SRM_FLAG_COLBLOCK)) return fail(SRM_ERR_CONFIG, "not a column-block plan");
+  return check(launch_xchg_pack(p->dp, as_stream(stream)), "xchg_pack");
+}
+
+int srm_xchg_reduce(srm_plan* p, void* stream) {
+  if (!p || !p->ws || !(p->flags & SRM_FLAG_COLBLOCK)) return fail(SRM_ERR_CONFIG, "not a column-block plan");
+  return check(launch_xchg_reduce(p->dp, as_stream(stream)), "xchg_reduce");
+}
+
+int srm_xchg_unpack(srm_plan* p, void* stream) {
+  if (!p || !p->ws || !(p->flags & SRM_FLAG_COLBLOCK)) return fail(SRM_ERR_CONFIG, "not a column-block plan");
+  return check(launch_xchg_unpack(p->dp, as_stream(stream)), "xchg_unpack");
 }
 
 int srm_reduce_local(srm_plan* p, void* stream) {
@@ -1276,6 +1366,26 @@ int srm_m_step(srm_plan* p, void* stream) {
   return run_stages(m_stages(p), as_stream(stream));
 }
 
+// The stages of one captured EM iteration.  With early_kk the M-step ends
+// with {tail_kk (side lane) || apply_m} after finalize_rho, and a graph replay
+// joins every lane at its end -- so the captured iteration is rotated to
+// [tail_kk || apply_m] [E-step] [M-step up to finalize_rho]: the next E-step's
+// reduce_terms then follows apply_m inside the same graph while tail_kk runs,
+// and the lanes meet at finalize_rho (which waits for tail_sigma anyway).
+// Replays compose to the eager order E M E M ...; the first replay repeats the
+// init's own apply_m and tail_kk (the same inputs, so the same values).
+std::vector<Stage> iteration_stages(srm_plan* p) {
+  std::vector<Stage> e = e_stages(p), m = m_stages(p);
+  size_t cut = m.size();
+  if (p->early_kk)
+    for (size_t k = 0; k < m.size(); ++k)
+      if (!strcmp(m[k].name, "finalize_rho") || !strcmp(m[k].name, "advance_iteration")) cut = k + 1;
+  std::vector<Stage> v(m.begin() + cut, m.end());
+  v.insert(v.end(), e.begin(), e.end());
+  v.insert(v.end(), m.begin(), m.begin() + cut);
+  return v;
+}
+
 int srm_graph_capture(srm_plan* p) {
   if (!p || !p->ws) return fail(SRM_ERR_CONFIG, "plan not bound");
   if (p->graph_exec) return SRM_OK;
@@ -1285,9 +1395,7 @@ int srm_graph_capture(srm_plan* p) {
   e = cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return cuda_fail(e, "begin capture");
   // one list: the side-stream stages of the E-step overlap the M-step
-  std::vector<Stage> stages = e_stages(p);
-  std::vector<Stage> m = m_stages(p);
-  stages.insert(stages.end(), m.begin(), m.end());
+  std::vector<Stage> stages = iteration_stages(p);
   const Lanes* ln = nullptr;
   int rc = plan_lanes(p, &ln);
   if (rc == SRM_OK) rc = run_stages(stages, p->cap_stream, ln);
@@ -1353,7 +1461,7 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
   // slicing of every batch on the side stream (17 KB CTAs that fit beside the
   // Gram's) and each batch's Gram, mirror and G slices on `st` after its slices
   const int per = p->ldx / 128 > 0 ? (int)(p->items_oz.size() / std::max(p->n_local, 1)) : 1;
-  const int ctas = per * (p->gram_pairs ? 2 : 1);  // CTAs per subject
+  const int ctas = per + 2 * (int)(p->items_oz2.size() / std::max(p->n_local, 1));  // CTAs per subject
   const int batch = std::max(1, 148 / std::max(ctas, 1));
   if ((p->flags & SRM_FLAG_GRAM_I8) && count > batch) {
     const Lanes* ln = nullptr;
@@ -1366,12 +1474,19 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
       if (e != cudaSuccess) return cuda_fail(e, "gram events");
       p->gram_events.push_back(ev);
     }
+    while (!p->items_oz2.empty() && (int)p->pair_events.size() < nb) {
+      cudaEvent_t ev;
+      const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "gram events");
+      p->pair_events.push_back(ev);
+    }
     // the Gram batches run on a high-priority stream, so their CTAs are
     // dispatched ahead of pending slicing CTAs as SMs free up
     if (!p->hi_stream) {
       int lo = 0, hi = 0;
       cudaError_t e0 = cudaDeviceGetStreamPriorityRange(&lo, &hi);
       if (e0 == cudaSuccess) e0 = cudaStreamCreateWithPriority(&p->hi_stream, cudaStreamNonBlocking, hi);
+      if (e0 == cudaSuccess) e0 = cudaStreamCreateWithPriority(&p->hi_stream2, cudaStreamNonBlocking, hi);
       if (e0 != cudaSuccess) return cuda_fail(e0, "gram stream");
     }
     cudaStream_t gs = p->hi_stream;
@@ -1387,7 +1502,19 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
       const int f = first + b * batch, n = std::min(batch, first + count - f);
       e = cudaStreamWaitEvent(gs, p->gram_events[b], 0);
       const std::vector<Stage> v = gram_stages(p, f, n);
-      for (size_t k = 1; k < v.size() && e == cudaSuccess; ++k) e = v[k].fn(gs);
+      for (size_t k = 1; k < v.size() && e == cudaSuccess; ++k) {
+        if (!strcmp(v[k].name, "oz_gram_pairs")) {
+          // the pairs on a second high-priority stream, beside the batch's
+          // single tiles: together one wave, as the single-CTA batch is
+          e = cudaStreamWaitEvent(p->hi_stream2, p->gram_events[b], 0);
+          if (e == cudaSuccess) e = v[k].fn(p->hi_stream2);
+          if (e == cudaSuccess) e = cudaEventRecord(p->pair_events[b], p->hi_stream2);
+          continue;
+        }
+        e = v[k].fn(gs);
+        if (e == cudaSuccess && !strcmp(v[k].name, "oz_gram") && !p->items_oz2.empty())
+          e = cudaStreamWaitEvent(gs, p->pair_events[b], 0);
+      }
     }
     if (e == cudaSuccess) e = cudaEventRecord(ln->join[1], gs);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ln->join[1], 0);

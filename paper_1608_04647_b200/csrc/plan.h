@@ -42,6 +42,7 @@ struct DevPlan {
   int ntile_apply;  // apply_cols-column tiles of ldx
   int apply_cols;   // apply_m column tile (apply_cols_for(kp))
   int ntile_tail;   // 32-column tiles of ldx
+  int polar_cross;  // the M-step polar (k_ns_polar / k_ns_polar_g) writes the cross term into crossp
   int64_t term_stride, red_stride, hist_stride;
   // regions
   void* xhat;
@@ -83,6 +84,14 @@ struct DevPlan {
   int n_hist;             // history rows
   const int64_t* subj;   // [n_local][kSubjCols]
   const int32_t* order;  // [n_order] record slots, ascending global subject index
+  // SRM_FLAG_COLBLOCK exchange: world column blocks of xw TRs; block records
+  // of xrec = kp * xw + kRecScalars doubles, reduced blocks of xred
+  int world, rank, max_local, xw;
+  int64_t xrec, xred;
+  double* xsend;            // [world][max_local][xrec]
+  double* xrecv;            // [world][max_local][xrec]
+  double* xredbuf;          // [world][xred]
+  const int32_t* xcounts;   // [world] subjects per rank
 };
 
 cudaError_t launch_prep(const DevPlan& p, int local, int64_t V, const void* x, int x_dtype,
@@ -103,6 +112,10 @@ cudaError_t launch_set_iteration(const DevPlan& p, int iteration, int advance, c
 cudaError_t launch_reduce_terms(const DevPlan& p, double* dst, const int32_t* order, int count,
                                 cudaStream_t s, bool ident = false);
 cudaError_t launch_tail(const DevPlan& p, cudaStream_t s);
+// SRM_FLAG_COLBLOCK exchange kernels (smallmat.cu)
+cudaError_t launch_xchg_pack(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_xchg_reduce(const DevPlan& p, cudaStream_t s);
+cudaError_t launch_xchg_unpack(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_inv(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s);
 cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s);

@@ -24,6 +24,18 @@ namespace {
 
 constexpr int kNsThreads = 512;
 
+// The M-step's cross term <W^T Xhat, S> (srm.py:151) from the polar itself:
+// with P = M^T B and B S^T = 2 C (C = A^T A as gram_from_b stores it, before
+// symmetrisation), <P, S> = tr(M^T B S^T) = 2 sum_{c,f} M[c][f] C[c][f] -- a
+// K x K dot product here instead of a reduction over apply_m's K x T tiles, so
+// rho_i^2 (finalize_rho) no longer waits for apply_m (DevPlan::polar_cross).
+// `cr` is this thread's part of sum M C; every thread of the block calls this.
+__device__ __forceinline__ void polar_cross_out(const DevPlan& p, int i, double cr, double* red) {
+  cr = block_sum<kNsThreads>(cr, red);
+  for (int t = threadIdx.x; t < p.ntile_apply; t += blockDim.x)
+    p.crossp[(int64_t)i * p.ntile_apply + t] = t == 0 ? 2.0 * cr : 0.0;
+}
+
 __host__ __device__ constexpr int ns_ld(int kp) { return kp + ((4 - kp) % 16 + 16) % 16; }
 
 // D = A * B for symmetric products (A, B commuting polynomials in C): only
@@ -209,14 +221,17 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar(DevPlan p, int init) {
   double* Mg = p.mmat + (int64_t)i * kp * kp;
   const double* Z = buf[z];
   const double s = degenerate ? 0.0 : 1.0 / sqrt(c);
-  double zz = 0.0;
+  double zz = 0.0, cr = 0.0;
+  const bool want_cross = p.polar_cross && !init;
   for (int e = tid; e < kp * kp; e += blockDim.x) {
     const int a = e / kp, b = e - a * kp;
     const double v = (a < n && b < n) ? 0.5 * (Z[a * LD + b] + Z[b * LD + a]) : 0.0;
     zz = fma(v, v, zz);
     Mg[e] = v * s;
+    if (want_cross && a < n && b < n) cr = fma(v * s, Cg[(int64_t)a * p.ldo + b], cr);
   }
   zz = block_sum<kNsThreads>(zz, red);
+  if (want_cross) polar_cross_out(p, i, cr, red);
   if (tid == 0) {
     p.scal[(int64_t)i * 8 + 0] = (double)it;
     if (degenerate || !converged || !(zz <= kGramCondLimit)) raise_warning(p.status, SRM_WARN_POLAR_CONDITION);
@@ -412,14 +427,18 @@ __global__ void __launch_bounds__(kNsThreads) k_ns_polar_g(DevPlan p, int init) 
   double* Mg = p.mmat + (int64_t)i * kp * kp;
   const double* Z = buf[z];
   const double sc = degenerate ? 0.0 : 1.0 / sqrt(c);
-  double zz = 0.0;
+  double zz = 0.0, cr = 0.0;
+  const bool want_cross = p.polar_cross && !init;
+  const double* Cx = p.bred + (int64_t)i * p.kp * p.ldo + p.ldx;
   for (int e = tid; e < kp * kp; e += kNsThreads) {
     const int a = e / kp, b = e - a * kp;
     const double v = (a < n && b < n) ? 0.5 * (Z[a * KP + b] + Z[b * KP + a]) : 0.0;
     zz = fma(v, v, zz);
     Mg[e] = v * sc;
+    if (want_cross && a < n && b < n) cr = fma(v * sc, Cx[(int64_t)a * p.ldo + b], cr);
   }
   zz = block_sum<kNsThreads>(zz, red);
+  if (want_cross) polar_cross_out(p, i, cr, red);
   if (tid == 0) {
     p.scal[(int64_t)i * 8 + 0] = (double)it;
     if (degenerate || !converged || !(zz <= kGramCondLimit)) raise_warning(p.status, SRM_WARN_POLAR_CONDITION);

@@ -548,6 +548,100 @@ __global__ void __launch_bounds__(kSmallThreads, KP <= 64 ? 3 : 1) k_gram_from_b
   if (tid == 0) p.gfb_count[i] = 0;
 }
 
+// ---------------------------------------------------------------------------
+// SRM_FLAG_COLBLOCK: the ordered accumulation of srm.py:193-213 by TR column
+// blocks.  pack: local record j's columns [q xw, (q + 1) xw) (and its scalars)
+// -> xsend[q][j]; after the all-to-all, xrecv[r][j] holds rank r's subject j
+// for this rank's block.  reduce: the same left fold as k_reduce_terms over
+// (r, j) = ascending global subject order (ranks own contiguous shards,
+// cli.py:82-85), so the block equals one rank's sum bit for bit.  unpack: the
+// all-gathered blocks -> red.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSmallThreads) k_xchg_pack(DevPlan p) {
+  const int j = blockIdx.y, q = blockIdx.z;
+  const int64_t e = (int64_t)blockIdx.x * kSmallThreads + threadIdx.x;
+  if (e >= p.xrec) return;
+  const int64_t* sj = p.subj + (int64_t)j * kSubjCols;
+  const double* rec = rec_ptr(p, (int)sj[SC_SLOT]);
+  const int64_t kx = p.kp * p.xw;
+  double v;
+  if (e < kx) {
+    const int64_t f = e / p.xw, col = (int64_t)q * p.xw + (e - f * p.xw);
+    v = col < p.ldx ? rec[f * p.ldx + col] : 0.0;
+  } else {
+    v = rec[p.kp * p.ldx + (e - kx)];
+  }
+  p.xsend[((int64_t)q * p.max_local + j) * p.xrec + e] = v;
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_xchg_reduce(DevPlan p) {
+  const int64_t kx = p.kp * p.xw;
+  const int64_t e = (int64_t)blockIdx.x * kSmallThreads + threadIdx.x;
+  double* out = p.xredbuf + (int64_t)p.rank * p.xred;
+  if (e < kx) {
+    double acc = 0.0;
+    bool first = true;
+    for (int r = 0; r < p.world; ++r) {
+      const double* base = p.xrecv + (int64_t)r * p.max_local * p.xrec;
+      const int cnt = p.xcounts[r];
+      int j = 0;
+      for (; j + 8 <= cnt; j += 8) {  // eight loads in flight, summed in order
+        double x[8], rr[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          x[u] = base[(int64_t)(j + u) * p.xrec + e];
+          rr[u] = base[(int64_t)(j + u) * p.xrec + kx + RC_RHO2];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc = first ? x[u] / rr[u] : acc + x[u] / rr[u];
+          first = false;
+        }
+      }
+      for (; j < cnt; ++j) {
+        const double v = base[(int64_t)j * p.xrec + e] / base[(int64_t)j * p.xrec + kx + RC_RHO2];
+        acc = first ? v : acc + v;
+        first = false;
+      }
+    }
+    out[e] = acc;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // the scalar sums of k_reduce_terms, same order
+    double rho0 = 0.0, vlog = 0.0, sq = 0.0, vsum = 0.0;
+    bool first = true;
+    for (int r = 0; r < p.world; ++r) {
+      const double* base = p.xrecv + (int64_t)r * p.max_local * p.xrec + kx;
+      for (int j = 0; j < p.xcounts[r]; ++j) {
+        const double* sc = base + (int64_t)j * p.xrec;
+        const double rr = sc[RC_RHO2];
+        rho0 = first ? 1.0 / rr : rho0 + 1.0 / rr;
+        first = false;
+        vlog += sc[RC_V] * log(rr);
+        sq += sc[RC_SQNORM] / rr;
+        vsum += sc[RC_V];
+      }
+    }
+    out[kx + RD_RHO0] = rho0;
+    out[kx + RD_VLOGRHO] = vlog;
+    out[kx + RD_SQRHO] = sq;
+    out[kx + RD_VSUM] = vsum;
+  }
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_xchg_unpack(DevPlan p) {
+  const int q = blockIdx.y;
+  const int64_t kx = p.kp * p.xw;
+  const int64_t e = (int64_t)blockIdx.x * kSmallThreads + threadIdx.x;
+  const double* src = p.xredbuf + (int64_t)q * p.xred;
+  if (e < kx) {
+    const int64_t f = e / p.xw, col = (int64_t)q * p.xw + (e - f * p.xw);
+    if (col < p.ldx) p.red[f * p.ldx + col] = src[e];
+  } else if (q == p.rank && e < kx + kRedScalars) {
+    p.red[p.kp * p.ldx + (e - kx)] = src[e];
+  }
+}
+
 __device__ __forceinline__ int64_t hist_row(const DevPlan& p, int it) { return (int64_t)(it % p.n_hist) * p.hist_stride; }
 
 __global__ void k_set_iteration(DevPlan p, int iteration, int advance) {
@@ -789,16 +883,15 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_inv(DevPlan p) {
 
 // ---------------------------------------------------------------------------
 // tail, stage 1 (one CTA): var_s = (rho0 I + Sigma_s^{-1})^{-1} and
-// C = Sigma_s^T (I - rho0 var_s) (srm.py:127-128).  rho0 = sum 1 / rho_j^2 in
+// C = Sigma_s^T (I - rho0 var_s) = var_s (srm.py:127-128).  rho0 = sum 1 / rho_j^2 in
 // ascending order straight from the term table (ordered plans: the same sum
 // k_reduce_terms forms, so this stage runs beside it), else from `red`.
 // ---------------------------------------------------------------------------
 template <int R>
 __device__ __forceinline__ void tail_kk_body(const DevPlan& p, int iteration, SweepShared& sh) {
-  extern __shared__ __align__(16) double sm[];
   double* pbuf = sh.pbuf;
   double* dbuf = sh.dbuf;
-  const int n = (int)p.K, ld = n + 1, kp = (int)p.kp;
+  const int n = (int)p.K, kp = (int)p.kp;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   __shared__ double s_rho0;
   double a[R][R];
@@ -835,59 +928,23 @@ __device__ __forceinline__ void tail_kk_body(const DevPlan& p, int iteration, Sw
     return;
   }
   const double logdet_prec = sum_log(dbuf, n, sh.scratch);
-  // var_s [n][ld] in shared memory; Sigma_s too while both fit (n <= 112),
-  // else read from global (L2-resident) in the product below
-  const bool sig_smem = n <= 112;
-  double* Vs = sm;
-  double* Ss = sig_smem ? sm + n * ld : p.sigma;
-  const int lds = sig_smem ? ld : kp;
+  // C = Sigma_s^T (I - rho0 var_s) (srm.py:128) is var_s itself: Sigma_s and
+  // var_s = (Sigma_s^{-1} + rho0 I)^{-1} = Sigma_s (I + rho0 Sigma_s)^{-1}
+  // commute, and var_s (Sigma_s^{-1} + rho0 I) = I gives var_s = Sigma_s -
+  // rho0 Sigma_s var_s = Sigma_s (I - rho0 var_s).  Taking var_s also skips
+  // the cancellation in I - rho0 var_s (~1 / (1 + rho0 lambda)) and the K^3
+  // product on the critical path; the two differ by rounding only (~eps
+  // cond(Sigma_s^{-1} + rho0 I)).
 #pragma unroll
   for (int i = 0; i < R; ++i)
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const int r = ty + 16 * i, c = tx + 16 * k;
-      if (r < n && c < n) {
-        Vs[r * ld + c] = -a[i][k];
-        p.var[r * kp + c] = -a[i][k];
-        if (sig_smem) Ss[r * ld + c] = p.sigma[r * kp + c];
+      if (r < kp && c < kp) {
+        const double v = (r < n && c < n) ? -a[i][k] : 0.0;
+        p.var[r * kp + c] = v;
+        p.cmat[r * kp + c] = v;
       }
-    }
-  for (int e = tid; e < kp * kp; e += blockDim.x) {
-    const int r = e / kp, c = e - r * kp;
-    if (r >= n || c >= n) {
-      p.var[e] = 0.0;
-      p.cmat[e] = 0.0;
-    }
-  }
-  __syncthreads();
-  // C[r][c] = sum_m Sigma[m][r] (delta_mc - rho0 var[m][c])
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-#pragma unroll
-    for (int k = 0; k < R; ++k) a[i][k] = 0.0;
-  for (int m = 0; m < n; ++m) {
-    double sr[R], vc[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int r = ty + 16 * i;
-      sr[i] = (r < n) ? Ss[m * lds + r] : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const int c = tx + 16 * k;
-      vc[k] = (c < n) ? (m == c ? 1.0 : 0.0) - rho0 * Vs[m * ld + c] : 0.0;
-    }
-#pragma unroll
-    for (int i = 0; i < R; ++i)
-#pragma unroll
-      for (int k = 0; k < R; ++k) a[i][k] = fma(sr[i], vc[k], a[i][k]);
-  }
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const int r = ty + 16 * i, c = tx + 16 * k;
-      if (r < n && c < n) p.cmat[r * kp + c] = a[i][k];
     }
   if (tid == 0) p.tailscr[TS_LOGDET_PREC] = logdet_prec;
 }
@@ -1388,17 +1445,32 @@ cudaError_t launch_reduce_terms(const DevPlan& p, double* dst, const int32_t* or
   return cudaGetLastError();
 }
 
+cudaError_t launch_xchg_pack(const DevPlan& p, cudaStream_t s) {
+  if (p.n_local == 0) return cudaSuccess;
+  const dim3 grid((unsigned)((p.xrec + kSmallThreads - 1) / kSmallThreads), (unsigned)p.n_local, (unsigned)p.world);
+  k_xchg_pack<<<grid, kSmallThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xchg_reduce(const DevPlan& p, cudaStream_t s) {
+  const int64_t kx = p.kp * p.xw;
+  k_xchg_reduce<<<(unsigned)((kx + kSmallThreads - 1) / kSmallThreads), kSmallThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xchg_unpack(const DevPlan& p, cudaStream_t s) {
+  const dim3 grid((unsigned)((p.xred + kSmallThreads - 1) / kSmallThreads), (unsigned)p.world);
+  k_xchg_unpack<<<grid, kSmallThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tail_inv(const DevPlan& p, cudaStream_t s) {
   k_tail_inv<<<1, kSmallThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s) {
-  const int K = (int)p.K;
-  const size_t b1 = (size_t)(K <= 112 ? 2 : 1) * K * (K + 1) * sizeof(double);
-  cudaError_t e = set_smem((const void*)k_tail_kk, b1);
-  if (e != cudaSuccess) return e;
-  k_tail_kk<<<1, kSmallThreads, b1, s>>>(p);
+  k_tail_kk<<<1, kSmallThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -40,7 +40,7 @@ class SrmEngine:
 
     def __init__(self, n_voxels, n_trs, k, iterations, *, storage="f64", world_size=1,
                  rank=0, counts=None, ordered=True, tolerance=False, gram=False, tc=False, gram_i8=False,
-                 exact_polar=False, device=None):
+                 exact_polar=False, colblock=False, device=None):
         torch = _torch()
         self.lib = _lib.load()
         if not torch.cuda.is_available():
@@ -72,6 +72,8 @@ class SrmEngine:
             flags |= _lib.FLAG_GRAM_I8
         if exact_polar:
             flags |= _lib.FLAG_EXACT_POLAR
+        if colblock and ordered:
+            flags |= _lib.FLAG_COLBLOCK
         self.ordered = bool(ordered) or self.world_size == 1
         plan = ctypes.c_void_p()
         varr = (ctypes.c_int64 * self.n_local)(*self.n_voxels)
@@ -99,6 +101,11 @@ class SrmEngine:
         self.tc = bool(eff & _lib.FLAG_TC)
         self.gram_i8 = bool(eff & _lib.FLAG_GRAM_I8)
         self.exact_polar = bool(eff & _lib.FLAG_EXACT_POLAR)
+        # ordered accumulation by column blocks (all-to-all + all-gather of K x T / N)
+        self.colblock = bool(eff & _lib.FLAG_COLBLOCK)
+        if self.colblock:
+            self.xrec = d(_lib.D_XREC)
+            self.xred = d(_lib.D_XRED)
         self._graph = None
         self._xgraph = None  # capture_exchange (N > 1 over NCCL)
         self._staging = {}
@@ -375,6 +382,17 @@ class SrmEngine:
         torch = _torch()
         if self.world_size == 1 and not (force and hasattr(comm, "all_gather_into")):
             return
+        if self.colblock:
+            # srm.py:193-213 by column blocks: pack -> all-to-all -> ordered
+            # block sums -> all-gather of the K x T / N blocks -> unpack
+            st = ctypes.c_void_p(self.stream())
+            _lib.check(self.lib.srm_xchg_pack(self.plan, st), "xchg_pack")
+            comm.all_to_all_into(self.region(_lib.R_XRECV), self.region(_lib.R_XSEND))
+            _lib.check(self.lib.srm_xchg_reduce(self.plan, st), "xchg_reduce")
+            blocks = self.region(_lib.R_XRED)
+            comm.all_gather_into(blocks, blocks[self.rank * self.xred: (self.rank + 1) * self.xred])
+            _lib.check(self.lib.srm_xchg_unpack(self.plan, st), "xchg_unpack")
+            return
         if hasattr(comm, "all_gather_into"):
             if self.ordered:
                 m = self.n_slots // self.world_size
@@ -419,7 +437,8 @@ class SrmEngine:
     def exchange_capturable(self, comm):
         """True when {exchange, E-step, M-step} can be one CUDA graph: the
         exchange is a device collective on this GPU (NCCL), not host staging."""
-        return bool(getattr(comm, "device_collectives", False)) and hasattr(comm, "all_gather_into")
+        return (bool(getattr(comm, "device_collectives", False)) and hasattr(comm, "all_gather_into")
+                and (not self.colblock or hasattr(comm, "all_to_all_into")))
 
     def capture_exchange(self, comm, force=False):
         """Record one multi-rank EM iteration -- the NCCL all-gather (ordered)

@@ -444,9 +444,13 @@ def fit(subjects, config, comm=None, *, storage="auto", ordered=None, graphs=Tru
 
     ``storage`` picks the HBM dtype of X-hat: ``"auto"`` keeps fp32 inputs
     fp32 (half the bytes; arithmetic stays fp64), else fp64.
-    ``ordered`` (default: when the gathered E-step table is <= 64 MiB) sums
-    subject terms in ascending global order on every rank -- bit-identical
-    results for any shard layout; otherwise per-rank sums are all-reduced.
+    ``ordered`` (default ``True``) sums subject terms in ascending global order
+    on every rank -- bit-identical results for any shard layout (srm.py:193-213):
+    on N > 1 ranks by TR column blocks (each rank sums every subject's block
+    of T / N columns, then the K x T / N results are all-gathered) when the
+    communicator has an all-to-all, else from the gathered term table.
+    ``ordered=False`` all-reduces per-rank partial sums instead (opt-in: the
+    rounding then depends on the sharding).
     ``timings`` (a dict) receives per-phase wall seconds (synchronising).
     ``algorithm``: ``"stream"`` (two passes over X-hat per iteration),
     ``"gram"`` (one-time X^T X, then T x T algebra per iteration) or
@@ -534,10 +538,13 @@ def _fit_pass(subjects, config, comm, *, exact, storage, ordered, graphs, keep_o
     offset = int(sum(counts[: comm.rank]))
     n_subjects = int(sum(counts))
     if ordered is None:
-        kp = -(-k // 8) * 8
-        ldx = -(-n_trs // 32) * 32
-        table = comm.size * max(counts) * (kp * ldx + 8) * 8
-        ordered = comm.size == 1 or table <= (64 << 20) or not hasattr(comm, "all_reduce_sum")
+        ordered = True
+    # ordered multi-rank exchange: by column blocks (all-to-all of the K x T
+    # terms in N blocks, ordered block sums, all-gather of K x T / N) where the
+    # communicator has an all-to-all, else the gathered table;
+    # SRM_B200_EXCHANGE=gather forces the gathered table
+    colblock = (bool(ordered) and comm.size > 1 and hasattr(comm, "all_to_all_into")
+                and os.environ.get("SRM_B200_EXCHANGE") != "gather")
 
     n_vox = [int(s.X.shape[0]) for s in subjects]
     store = _storage_for(subjects, storage)
@@ -557,7 +564,7 @@ def _fit_pass(subjects, config, comm, *, exact, storage, ordered, graphs, keep_o
         raise ConfigError("algorithm must be 'auto', 'stream' or 'gram'")
     eng = SrmEngine(n_vox, n_trs, k, config.iterations,
                     storage=store, world_size=comm.size, rank=comm.rank,
-                    counts=counts, ordered=ordered, tolerance=config.tolerance is not None,
+                    counts=counts, ordered=ordered, colblock=colblock, tolerance=config.tolerance is not None,
                     gram=algorithm == "gram", tc=bool(tensor_cores) and store == "f32" and not exact,
                     gram_i8=algorithm == "gram" and use_i8, exact_polar=exact, device=device)
     if engine_out is not None:

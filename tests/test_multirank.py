@@ -115,8 +115,97 @@ def _dataset(name):
     return golden_subjects(g), int(g["k"]), int(g["iterations"]), int(g["seed"])
 
 
-def _fit_worker(rank, world, port, out, algorithm, data="em_ragged", ordered=None):
+def _colblock_worker(rank, world, port, out):
+    """The SRM_FLAG_COLBLOCK exchange restated on host tensors with the plan's
+    own dimensions (srm_plan_dim D_XREC / D_XRED, the k_xchg_* index maps):
+    pack each local record's TR block q for rank q, all-to-all, sum this
+    rank's block over (rank, local j) = ascending global order as the left
+    fold of k_reduce_terms (acc = t_0 / r_0, acc += t_j / r_j), all-gather,
+    unpack -- equal to one rank's fold bit for bit."""
+    import torch
     import torch.distributed as dist
+
+    from paper_1608_04647_b200 import _lib
+    from paper_1608_04647_b200.collectives import TorchCommunicator, rank_counts, shard_bounds
+
+    _init(rank, world, port)
+    comm = TorchCommunicator()
+    n_total, K, T = 5, 3, 70
+    a, b = shard_bounds(n_total, world, rank)
+    counts = rank_counts(comm, b - a)
+    lib = _lib.load()
+    p = ctypes.c_void_p()
+    v = (ctypes.c_int64 * (b - a))(*([40] * (b - a)))
+    rc = lib.srm_plan_create(ctypes.byref(p), 0, b - a, v, T, K, 2, world, rank,
+                             (ctypes.c_int32 * world)(*counts), _lib.FLAG_ORDERED | _lib.FLAG_COLBLOCK)
+    assert rc == 0
+    flags = lib.srm_plan_dim(p, _lib.D_FLAGS)
+    kp, ldx = lib.srm_plan_dim(p, _lib.D_KP), lib.srm_plan_dim(p, _lib.D_LDX)
+    xrec, xred = lib.srm_plan_dim(p, _lib.D_XREC), lib.srm_plan_dim(p, _lib.D_XRED)
+    lib.srm_plan_destroy(p)
+    assert flags & _lib.FLAG_COLBLOCK and not flags & _lib.FLAG_ORDERED
+    m, xw = max(counts), (ldx + world - 1) // world
+    assert xrec == kp * xw + 8 and xred == kp * xw + 8
+    rng = np.random.default_rng(5)
+    terms = rng.standard_normal((n_total, kp, ldx))
+    rho2 = rng.uniform(0.5, 1.5, n_total)
+    send = torch.zeros((world, m, xrec), dtype=torch.float64)
+    for q in range(world):
+        for j in range(b - a):
+            for f in range(kp):
+                cols = [q * xw + c for c in range(xw)]
+                send[q, j, f * xw: (f + 1) * xw] = torch.tensor(
+                    [terms[a + j, f, c] if c < ldx else 0.0 for c in cols])
+            send[q, j, kp * xw] = rho2[a + j]
+    recv = torch.empty_like(send)
+    comm.all_to_all_into(recv, send)
+    mine = None
+    for r in range(world):
+        for j in range(counts[r]):
+            x = recv[r, j, : kp * xw] / recv[r, j, kp * xw]
+            mine = x.clone() if mine is None else mine + x
+    blocks = torch.zeros((world, xred), dtype=torch.float64)
+    blocks[rank, : kp * xw] = mine
+    comm.all_gather_into(blocks.view(-1), blocks[rank].clone())
+    red = np.zeros((kp, ldx))
+    for q in range(world):
+        for f in range(kp):
+            for c in range(xw):
+                if q * xw + c < ldx:
+                    red[f, q * xw + c] = blocks[q, f * xw + c].item()
+    serial = terms[0] / rho2[0]
+    for i in range(1, n_total):
+        serial = serial + terms[i] / rho2[i]
+    out.put((rank, np.array_equal(red, serial), comm.stats.alltoall_calls))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_column_block_exchange():
+    """Uneven shards [3, 2] of 5 subjects, T = 70 in two TR blocks: the
+    column-block exchange equals the serial ascending sum bit for bit on both
+    ranks (the all-to-all path of TorchCommunicator over gloo)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_colblock_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, calls in res:
+        assert ok, rank
+        assert calls == 1
+
+
+def _fit_worker(rank, world, port, out, algorithm, data="em_ragged", ordered=None, exchange=None):
+    import os
+
+    import torch.distributed as dist
+
+    if exchange == "gather":
+        os.environ["SRM_B200_EXCHANGE"] = "gather"
 
     from paper_1608_04647_b200 import srm
     from paper_1608_04647_b200.collectives import TorchCommunicator, shard_bounds
@@ -128,15 +217,17 @@ def _fit_worker(rank, world, port, out, algorithm, data="em_ragged", ordered=Non
     m = srm.fit([srm.SubjectData(f"s{i}", xs[i]) for i in range(a, b)],
                 srm.SrmConfig(k=k, iterations=iters, seed=seed),
                 TorchCommunicator(), algorithm=algorithm, ordered=ordered, engine_out=engines)
-    out.put((rank, m.S, m.W, m.rho2, m.rho0, m.sigma_s, m.rho2_all, m.subject_indices, engines[-1].ordered))
+    out.put((rank, m.S, m.W, m.rho2, m.rho0, m.sigma_s, m.rho2_all, m.subject_indices, engines[-1].ordered,
+             engines[-1].colblock))
     dist.destroy_process_group()
 
 
-def _two_ranks(algorithm, data="em_ragged", ordered=None):
+def _two_ranks(algorithm, data="em_ragged", ordered=None, exchange=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_fit_worker, args=(r, 2, port, q, algorithm, data, ordered)) for r in range(2)]
+    procs = [ctx.Process(target=_fit_worker, args=(r, 2, port, q, algorithm, data, ordered, exchange))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = {}
@@ -158,18 +249,22 @@ def _serial(data, algorithm):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("exchange", ["colblock", "gather"])
 @pytest.mark.parametrize("algorithm", ["stream", "gram"])
 @pytest.mark.parametrize("data", ["em_ragged", "recipe5"])
-def test_two_rank_fit_bit_identical_to_serial(algorithm, data):
-    """Ordered exchange (the all-gathered term table summed in ascending
-    global subject order on every rank, srm.py:193-213): equal shards [2, 2]
-    take the identity-order reduction, uneven shards [3, 2] the order table
-    of k_reduce_terms; both bit-identical to the serial fit."""
+def test_two_rank_fit_bit_identical_to_serial(algorithm, data, exchange):
+    """Ordered exchange (srm.py:193-213), both forms bit-identical to the
+    serial fit: the column-block exchange (default: all-to-all of each rank's
+    terms in two TR blocks, each rank's block summed over every subject in
+    ascending global order, all-gather of the K x T / 2 results) and the
+    all-gathered term table (equal shards [2, 2] take the identity-order
+    reduction, uneven shards [3, 2] the order table of k_reduce_terms)."""
     serial = _serial(data, algorithm)
-    res = _two_ranks(algorithm, data)
-    _, S0, W0, r0, rho0_0, sig0, all0, idx0, ord0 = res[0]
-    _, S1, W1, r1, rho0_1, sig1, all1, idx1, ord1 = res[1]
+    res = _two_ranks(algorithm, data, exchange=exchange)
+    _, S0, W0, r0, rho0_0, sig0, all0, idx0, ord0, cb0 = res[0]
+    _, S1, W1, r1, rho0_1, sig1, all1, idx1, ord1, cb1 = res[1]
     assert ord0 and ord1
+    assert cb0 == cb1 == (exchange == "colblock")
     n0 = 2 if data == "em_ragged" else 3
     assert idx0 == list(range(n0)) and idx1 == list(range(n0, n0 + len(W1)))
     assert np.array_equal(S0, serial.S) and np.array_equal(S1, serial.S)
@@ -192,8 +287,8 @@ def test_two_rank_unordered_exchange_matches_serial(algorithm):
 
     serial = _serial("recipe5", algorithm)
     res = _two_ranks(algorithm, "recipe5", ordered=False)
-    _, S0, W0, r0, rho0_0, sig0, all0, _, ord0 = res[0]
-    _, S1, W1, r1, rho0_1, _, _, _, ord1 = res[1]
+    _, S0, W0, r0, rho0_0, sig0, all0, _, ord0, _ = res[0]
+    _, S1, W1, r1, rho0_1, _, _, _, ord1, _ = res[1]
     assert not ord0 and not ord1
     assert np.array_equal(S0, S1) and rho0_0 == rho0_1
     assert nrel(S0, serial.S) <= 1e-12 and nrel(sig0, serial.sigma_s) <= 1e-12
