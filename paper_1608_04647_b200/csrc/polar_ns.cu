@@ -293,14 +293,21 @@ __device__ __forceinline__ void gmm_sym(const double* A, const double* B, double
   for (int q = 0; q < TL::PER; ++q) acc[q][0] = acc[q][1] = 0.0;
   for (int k0 = 0; k0 < KP; k0 += kSlab) {
     const int kw = min(kSlab, KP - k0);
-    for (int e = threadIdx.x; e < KP * kSlab; e += kNsThreads) {
-      const int r = e / kSlab, kk = e - r * kSlab;
-      As[r * kSlabLd + kk] = kk < kw ? A[r * KP + k0 + kk] : 0.0;
+    // 16-byte cp.async (LDGSTS) copies from L2, ~20 per thread in flight at
+    // kp = 104 (scalar loads held one or two: the staging was 60% of the kernel)
+    constexpr int ca = kSlab / 2, cb = KP / 2;
+    for (int e = threadIdx.x; e < KP * ca; e += kNsThreads) {
+      const int r = e / ca, kk = 2 * (e - r * ca);
+      const bool ok = kk < kw;
+      cp_async16(As + r * kSlabLd + kk, A + r * KP + k0 + (ok ? kk : 0), ok);
     }
-    for (int e = threadIdx.x; e < kSlab * KP; e += kNsThreads) {
-      const int kk = e / KP, c = e - kk * KP;
-      Bs[kk * LDB + c] = kk < kw ? B[(k0 + kk) * KP + c] : 0.0;
+    for (int e = threadIdx.x; e < kSlab * cb; e += kNsThreads) {
+      const int kk = e / cb, c = 2 * (e - kk * cb);
+      const bool ok = kk < kw;
+      cp_async16(Bs + kk * LDB + c, B + (ok ? (k0 + kk) * KP + c : 0), ok);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
 #pragma unroll 2
     for (int kk = 0; kk < kw; kk += 4) {

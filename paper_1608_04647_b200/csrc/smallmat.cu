@@ -780,6 +780,31 @@ __device__ __forceinline__ void reg_load(double (&a)[R][R], const double* src, i
     }
 }
 
+// Row / column s = j / 16 of the thread's register block by a compile-time
+// index (a runtime index would put a[][] in local memory): the switch on s is
+// warp-uniform, and inside it the owners of row j / column j / the pivot take
+// their new values by selects -- 3R selects per thread and pivot where a
+// select per element cost R^2, and no divergent branch.
+template <int R, int S>
+__device__ __forceinline__ void sweep_fix(double (&a)[R][R], const double* pr, const double* pc, double inv,
+                                          bool row_owner, bool col_owner) {
+  if constexpr (S < R) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) a[S][k] = row_owner ? pc[k] * inv : a[S][k];
+#pragma unroll
+    for (int i = 0; i < R; ++i) a[i][S] = col_owner ? pr[i] : a[i][S];
+    a[S][S] = (row_owner && col_owner) ? -inv : a[S][S];
+  }
+}
+template <int R, int S>
+__device__ __forceinline__ void sweep_put_row(const double (&a)[R][R], double* nx, int tx, int n) {
+  if constexpr (S < R) {
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (tx + 16 * k < n) nx[tx + 16 * k] = a[S][k];
+  }
+}
+
 template <int R>
 __device__ __forceinline__ int reg_sweep(double (&a)[R][R], int n, double* pbuf, double* dbuf) {
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -805,27 +830,38 @@ __device__ __forceinline__ int reg_sweep(double (&a)[R][R], int n, double* pbuf,
       const int c = tx + 16 * k;
       pc[k] = (c < n) ? pv[c] : 0.0;
     }
+    // every element as if off the pivot row and column (one FMA each), then
+    // row j (pv[c] / d), column j (pv[r] / d) and the pivot (-1 / d) written
+    // over it by their owners -- the values of the per-element select form
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int r = ty + 16 * i;
+    for (int i = 0; i < R; ++i)
 #pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const int c = tx + 16 * k;
-        const double v = fma(-pr[i], pc[k], a[i][k]);
-        a[i][k] = (r == j) ? ((c == j) ? -inv : pc[k] * inv) : ((c == j) ? pr[i] : v);
-      }
+      for (int k = 0; k < R; ++k) a[i][k] = fma(-pr[i], pc[k], a[i][k]);
+    const int jr = j & 15;
+    const bool row_owner = ty == jr, col_owner = tx == jr;
+    switch (j >> 4) {
+      case 0: sweep_fix<R, 0>(a, pr, pc, inv, row_owner, col_owner); break;
+      case 1: sweep_fix<R, 1>(a, pr, pc, inv, row_owner, col_owner); break;
+      case 2: sweep_fix<R, 2>(a, pr, pc, inv, row_owner, col_owner); break;
+      case 3: sweep_fix<R, 3>(a, pr, pc, inv, row_owner, col_owner); break;
+      case 4: sweep_fix<R, 4>(a, pr, pc, inv, row_owner, col_owner); break;
+      case 5: sweep_fix<R, 5>(a, pr, pc, inv, row_owner, col_owner); break;
+      case 6: sweep_fix<R, 6>(a, pr, pc, inv, row_owner, col_owner); break;
+      default: sweep_fix<R, 7>(a, pr, pc, inv, row_owner, col_owner); break;
     }
     if (threadIdx.x == 0) dbuf[j] = d;
     const int jn = j + 1;
     if (jn < n && ty == (jn & 15)) {
       double* nx = pbuf + (jn & 1) * kSweepLd;
-      const int isel = jn >> 4;
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        double v = a[0][k];  // select chain: keeps a[][] in registers
-#pragma unroll
-        for (int i = 1; i < R; ++i) v = (isel == i) ? a[i][k] : v;
-        if (tx + 16 * k < n) nx[tx + 16 * k] = v;
+      switch (jn >> 4) {
+        case 0: sweep_put_row<R, 0>(a, nx, tx, n); break;
+        case 1: sweep_put_row<R, 1>(a, nx, tx, n); break;
+        case 2: sweep_put_row<R, 2>(a, nx, tx, n); break;
+        case 3: sweep_put_row<R, 3>(a, nx, tx, n); break;
+        case 4: sweep_put_row<R, 4>(a, nx, tx, n); break;
+        case 5: sweep_put_row<R, 5>(a, nx, tx, n); break;
+        case 6: sweep_put_row<R, 6>(a, nx, tx, n); break;
+        default: sweep_put_row<R, 7>(a, nx, tx, n); break;
       }
     }
     __syncthreads();
@@ -866,19 +902,11 @@ __device__ __forceinline__ void tail_inv_body(const DevPlan& p, SweepShared& sh)
   if (tid == 0) p.tailscr[TS_LOGDET_SIGMA] = logdet_sigma;
 }
 
+template <int R>
 __global__ void __launch_bounds__(kSmallThreads) k_tail_inv(DevPlan p) {
   __shared__ SweepShared sh;
   if (failed(p)) return;
-  switch ((p.K + 15) / 16) {
-    case 1: tail_inv_body<1>(p, sh); break;
-    case 2: tail_inv_body<2>(p, sh); break;
-    case 3: tail_inv_body<3>(p, sh); break;
-    case 4: tail_inv_body<4>(p, sh); break;
-    case 5: tail_inv_body<5>(p, sh); break;
-    case 6: tail_inv_body<6>(p, sh); break;
-    case 7: tail_inv_body<7>(p, sh); break;
-    default: tail_inv_body<8>(p, sh); break;
-  }
+  tail_inv_body<R>(p, sh);
 }
 
 // ---------------------------------------------------------------------------
@@ -949,25 +977,20 @@ __device__ __forceinline__ void tail_kk_body(const DevPlan& p, int iteration, Sw
   if (tid == 0) p.tailscr[TS_LOGDET_PREC] = logdet_prec;
 }
 
+template <int R>
 __global__ void __launch_bounds__(kSmallThreads) k_tail_kk(DevPlan p) {
   __shared__ SweepShared sh;
   const int iteration = *p.iter;
   if (failed(p)) return;
-  switch ((p.K + 15) / 16) {
-    case 1: tail_kk_body<1>(p, iteration, sh); break;
-    case 2: tail_kk_body<2>(p, iteration, sh); break;
-    case 3: tail_kk_body<3>(p, iteration, sh); break;
-    case 4: tail_kk_body<4>(p, iteration, sh); break;
-    case 5: tail_kk_body<5>(p, iteration, sh); break;
-    case 6: tail_kk_body<6>(p, iteration, sh); break;
-    case 7: tail_kk_body<7>(p, iteration, sh); break;
-    default: tail_kk_body<8>(p, iteration, sh); break;
-  }
+  tail_kk_body<R>(p, iteration, sh);
 }
 
 // tail, stage 2 (32-column tiles): S = C red, quad = <red, var red>, S S^T
 // partials and the tolerance statistics.
-__global__ void __launch_bounds__(kSmallThreads) k_tail_s(DevPlan p) {
+// sixteen warps: each row chain (a K-long dependent FMA sequence per
+// accumulator) is short of issue slots at two warps per scheduler
+constexpr int kTailSThreads = 512;
+__global__ void __launch_bounds__(kTailSThreads) k_tail_s(DevPlan p) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double scratch[32];
   if (failed(p)) return;
@@ -994,13 +1017,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_s(DevPlan p) {
     cm[q] = (c < K && rg < K) ? p.cmat[rg * kp + c] : 0.0;
     vr[q] = (c < K && rg < K) ? p.var[rg * kp + c] : 0.0;
   }
-  for (int f = rg; f < K; f += 8) {
+  for (int f = rg; f < K; f += kTailSThreads / 32) {
     double cmn[4], vrn[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int c = q * 32 + col;
-      cmn[q] = (c < K && f + 8 < K) ? p.cmat[(f + 8) * kp + c] : 0.0;
-      vrn[q] = (c < K && f + 8 < K) ? p.var[(f + 8) * kp + c] : 0.0;
+      cmn[q] = (c < K && f + kTailSThreads / 32 < K) ? p.cmat[(f + kTailSThreads / 32) * kp + c] : 0.0;
+      vrn[q] = (c < K && f + kTailSThreads / 32 < K) ? p.var[(f + kTailSThreads / 32) * kp + c] : 0.0;
     }
     double s = 0.0, y = 0.0;
 #pragma unroll
@@ -1046,9 +1069,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_tail_s(DevPlan p) {
     ssp[a * kp + b] = v;
     ssp[b * kp + a] = v;
   }
-  quad = block_sum<kSmallThreads>(quad, scratch);
-  dsq = block_sum<kSmallThreads>(dsq, scratch);
-  osq = block_sum<kSmallThreads>(osq, scratch);
+  quad = block_sum<kTailSThreads>(quad, scratch);
+  dsq = block_sum<kTailSThreads>(dsq, scratch);
+  osq = block_sum<kTailSThreads>(osq, scratch);
   if (tid == 0) {
     p.tailpart[tile * 4 + 0] = quad;
     p.tailpart[tile * 4 + 1] = dsq;
@@ -1210,18 +1233,10 @@ __device__ __forceinline__ void spd_inverse_body(double* g, int n, int32_t* stat
     }
 }
 
+template <int R>
 __global__ void __launch_bounds__(kSmallThreads) k_spd_inverse(double* a, int n, int32_t* status) {
   __shared__ SweepShared sh;
-  switch ((n + 15) / 16) {
-    case 1: spd_inverse_body<1>(a, n, status, sh); break;
-    case 2: spd_inverse_body<2>(a, n, status, sh); break;
-    case 3: spd_inverse_body<3>(a, n, status, sh); break;
-    case 4: spd_inverse_body<4>(a, n, status, sh); break;
-    case 5: spd_inverse_body<5>(a, n, status, sh); break;
-    case 6: spd_inverse_body<6>(a, n, status, sh); break;
-    case 7: spd_inverse_body<7>(a, n, status, sh); break;
-    default: spd_inverse_body<8>(a, n, status, sh); break;
-  }
+  spd_inverse_body<R>(a, n, status, sh);
 }
 
 // stateless polar transform from a Gram matrix: M = G^{-1/2}
@@ -1465,12 +1480,30 @@ cudaError_t launch_xchg_unpack(const DevPlan& p, cudaStream_t s) {
 }
 
 cudaError_t launch_tail_inv(const DevPlan& p, cudaStream_t s) {
-  k_tail_inv<<<1, kSmallThreads, 0, s>>>(p);
+  switch ((p.K + 15) / 16) {
+#define SRM_SWEEP_CASE(r) \
+  case r:                 \
+    k_tail_inv<r><<<1, kSmallThreads, 0, s>>>(p); \
+    break;
+    SRM_SWEEP_CASE(1) SRM_SWEEP_CASE(2) SRM_SWEEP_CASE(3) SRM_SWEEP_CASE(4)
+    SRM_SWEEP_CASE(5) SRM_SWEEP_CASE(6) SRM_SWEEP_CASE(7)
+    default: k_tail_inv<8><<<1, kSmallThreads, 0, s>>>(p); break;
+#undef SRM_SWEEP_CASE
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_tail_kk(const DevPlan& p, cudaStream_t s) {
-  k_tail_kk<<<1, kSmallThreads, 0, s>>>(p);
+  switch ((p.K + 15) / 16) {
+#define SRM_SWEEP_CASE(r) \
+  case r:                 \
+    k_tail_kk<r><<<1, kSmallThreads, 0, s>>>(p); \
+    break;
+    SRM_SWEEP_CASE(1) SRM_SWEEP_CASE(2) SRM_SWEEP_CASE(3) SRM_SWEEP_CASE(4)
+    SRM_SWEEP_CASE(5) SRM_SWEEP_CASE(6) SRM_SWEEP_CASE(7)
+    default: k_tail_kk<8><<<1, kSmallThreads, 0, s>>>(p); break;
+#undef SRM_SWEEP_CASE
+  }
   return cudaGetLastError();
 }
 
@@ -1478,7 +1511,7 @@ cudaError_t launch_tail_s(const DevPlan& p, cudaStream_t s) {
   const size_t b2 = (size_t)3 * p.K * 33 * sizeof(double);
   cudaError_t e = set_smem((const void*)k_tail_s, b2);
   if (e != cudaSuccess) return e;
-  k_tail_s<<<p.ntile_tail, kSmallThreads, b2, s>>>(p);
+  k_tail_s<<<p.ntile_tail, kTailSThreads, b2, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -1528,7 +1561,18 @@ cudaError_t launch_apply_w_f32(const DevPlan& p, const void* items_a, int n_item
 }
 
 cudaError_t launch_spd_inverse(double* a, int n, int32_t* status, cudaStream_t s) {
-  k_spd_inverse<<<1, kSmallThreads, 0, s>>>(a, n, status);
+  // one instantiation per register block (R = ceil(n / 16)): each gets its
+  // own register allocation
+  switch ((n + 15) / 16) {
+#define SRM_SWEEP_CASE(r) \
+  case r:                 \
+    k_spd_inverse<r><<<1, kSmallThreads, 0, s>>>(a, n, status); \
+    break;
+    SRM_SWEEP_CASE(1) SRM_SWEEP_CASE(2) SRM_SWEEP_CASE(3) SRM_SWEEP_CASE(4)
+    SRM_SWEEP_CASE(5) SRM_SWEEP_CASE(6) SRM_SWEEP_CASE(7)
+    default: k_spd_inverse<8><<<1, kSmallThreads, 0, s>>>(a, n, status); break;
+#undef SRM_SWEEP_CASE
+  }
   return cudaGetLastError();
 }
 
