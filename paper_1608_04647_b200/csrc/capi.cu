@@ -882,9 +882,14 @@ std::vector<Stage> finalize_stages(srm_plan* p, int first, int count) {
                                             1.0, region<ItemE>(p, I_ITEMS_TG), (int)p->items_tg.size(), st);
                  }});
     v.push_back({"final_reduce", [d](cudaStream_t st) { return launch_reduce_chunks(d, st); }});
-    v.push_back({"final_polar", [d](cudaStream_t st) { return launch_final_polar(d, st); }});
-    v.push_back({"apply_w", [p, d](cudaStream_t st) {
-                   return launch_apply_rows((int)p->kp, SRM_F32, d.af, p->np, d.mmat, p->kp * p->kp, d.wout,
+    // the final transform goes to its own buffer (QSCR): MMAT still holds the
+    // iteration's M, which the next iteration's apply_m reads when a caller
+    // forms W mid-fit (on_iteration snapshots, rotated iteration graph)
+    DevPlan fd = d;
+    fd.mmat = region<double>(p, I_QSCR);
+    v.push_back({"final_polar", [fd](cudaStream_t st) { return launch_final_polar(fd, st); }});
+    v.push_back({"apply_w", [p, fd](cudaStream_t st) {
+                   return launch_apply_rows((int)p->kp, SRM_F32, fd.af, p->np, fd.mmat, p->kp * p->kp, fd.wout,
                                             (int)p->K, region<ItemA>(p, I_ITEMS_TA), (int)p->items_ta.size(), st);
                  }});
     return v;
@@ -906,7 +911,7 @@ std::vector<Stage> gram_stages(srm_plan* p, int first, int count) {
                                             region<unsigned long long>(p, I_OZCMAX), region<int8_t>(p, I_OZQ),
                                             p->oz_lq, region<int32_t>(p, I_OZEXP), p->max_v, st);
                  }});
-    const OzGramOut o{d.gram, p->ldx, p->ldx * p->ldx, p->ldx, region<int32_t>(p, I_OZEXP), p->ldx, p->ldx};
+    const OzGramOut o{d.gram, p->ldx, p->ldx * p->ldx, p->ldx, region<int32_t>(p, I_OZEXP), p->ldx, p->ldx, p->T};
     if (!p->items_oz2.empty()) {
       // the CTA-pair tiles (the batched prepare runs them beside the single tiles)
       const int per2 = (int)(p->items_oz2.size() / p->n_local);
@@ -1223,7 +1228,9 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     }
     if (e == cudaSuccess && p->oz_w) {
       e = make_map_q5(&p->tm_q32, region<int8_t>(p, I_OZQ), p->oz_lq, p->ldx, p->n_local, p->oz_nsl);
-      if (e == cudaSuccess) e = make_map_q8(&p->tm_r, region<int8_t>(p, I_OZR), p->oz_lqg, p->kp, p->n_local);
+      // four-slice X-hat: the final W keeps d-groups 0-4, which read R's slots 0-5 only
+      if (e == cudaSuccess)
+        e = make_map_q8(&p->tm_r, region<int8_t>(p, I_OZR), p->oz_lqg, p->kp, p->n_local, p->oz_nsl == 4 ? 6 : 8);
       if (e == cudaSuccess)
         e = launch_oz_w(p->tm_q32, p->tm_r, nullptr, nullptr, nullptr, 0, p->ldx, p->kp, p->K, p->oz_nsl, 0);
     }
@@ -1291,7 +1298,8 @@ int srm_init_mapping_range(srm_plan* p, int first, int count, void* stream) {
                               region<int32_t>(p, I_OZGIEXP), region<unsigned long long>(p, I_OZGICMAX), maxv, st);
     if (e == cudaSuccess && gg_i8) {
       // partial A^T A of chunk c at part[c][0..kp)[ldx..ldx + kp), as the DMMA items write it
-      const OzGramOut o{d.part + p->ldx, p->ldo, p->kp * p->ldo, p->kp, region<int32_t>(p, I_OZGIEXP), p->K, p->K};
+      const OzGramOut o{d.part + p->ldx, p->ldo, p->kp * p->ldo, p->kp, region<int32_t>(p, I_OZGIEXP), p->K, p->K,
+                        p->K};
       e = launch_oz_gram(p->tm_gi, o, region<OzItem>(p, I_ITEMS_GG) + p->chunk0[first], (int)ean, 7, st);
       if (e == cudaSuccess) e = launch_reduce_chunks(d, st);
     }

@@ -82,6 +82,10 @@ struct OzGramOut {
   int64_t ldg, gsub, nout;
   const int32_t* expo;
   int64_t ldexp, nexp;
+  // columns the MMAs must cover (T): a tile's N is trimmed to the 16-column
+  // multiple that reaches it, and its columns beyond are written as the zeros
+  // they are (0 = all of nout)
+  int64_t nmma = 0;
 };
 constexpr int kOzChunkBlocks = 2048;  // 65536 voxels per exact int32 accumulation
 constexpr int64_t kOzRecord = 256;    // bytes per (row, 32-column block): 8 slots x 32
@@ -90,7 +94,8 @@ constexpr int64_t kOzRecord = 256;    // bytes per (row, 32-column block): 8 slo
 inline __host__ __device__ int oz_record_bytes(int nsl) { return nsl <= 4 ? 128 : 256; }
 cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n, int box_rows);
 cudaError_t make_map_q5(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, int64_t n, int nsl);
-cudaError_t make_map_q8(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n);
+// box {32 B, 64 rows, `slots` 32-byte slots of a record, 1}: the leading slots of each record
+cudaError_t make_map_q8(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n, int slots = 8);
 // int8 slices of the rows of a row-major fp64 matrix (ozaki.cu): 2^e[r] >= max|M[r][:]|
 // tile_rows > 0: the tiled layout of the G_i slices (rows per G_i; oz_tiled_bytes per G_i)
 cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int64_t ncols, int8_t* q, int64_t lq,

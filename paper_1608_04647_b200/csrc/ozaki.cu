@@ -340,6 +340,15 @@ __device__ __forceinline__ void oz_issue_pass(uint32_t tmem, uint64_t da0, uint6
   }
 }
 
+// N of a Gram tile's MMAs: the 16-column multiple covering the columns
+// below o.nmma (T), at most 128 -- the last column block of T = 1000 (ldx
+// 1024) needs 112, so its eight tiles issue 12.5% fewer MACs
+__device__ __forceinline__ int oz_tile_n(const OzGramOut& o, int n0) {
+  const int64_t lim = o.nmma > 0 ? o.nmma : o.nout;
+  const int64_t c = lim - n0;
+  return c >= 128 ? 128 : (c <= 16 ? 16 : (int)((c + 15) & ~15));
+}
+
 template <int NSL>
 __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant__ CUtensorMap tmq,
                                                            const OzGramOut o, const OzItem* __restrict__ items) {
@@ -417,7 +426,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_s8(128, 128);
+      const uint32_t idesc = idesc_s8(128, oz_tile_n(o, it.n0));
       int k = 0, npass = 0;
       for (int c = 0; c < nchunks; ++c) {
         const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
@@ -470,6 +479,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
     const int32_t* ex = o.expo + (int64_t)it.subj * o.ldexp;
     const int ea = ta < o.nexp ? ex[ta] : 0;
     double* grow = o.g + (int64_t)it.slot * o.gsub + ta * o.ldg + it.n0;
+    const int tn = oz_tile_n(o, it.n0);
     int npass = 0;
     for (int c = 0; c < nchunks; ++c) {
       for (int pass = 0; pass < kPasses; ++pass, ++npass) {
@@ -512,7 +522,8 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_gram(const __grid_constant
             for (int j = 0; j < 16; ++j) {
               const int64_t tb = it.n0 + c0 + j;
               if (tb < o.nout) {
-                const double g = val[j] * pow2(ea + (tb < o.nexp ? ex[tb] : 0));
+                // columns past the trimmed N are the zeros of X-hat's padded TRs
+                const double g = c0 + j < tn ? val[j] * pow2(ea + (tb < o.nexp ? ex[tb] : 0)) : 0.0;
                 grow[c0 + j] = (npass == 0) ? g : prev[j] + g;
               }
             }
@@ -618,7 +629,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nvb = it.nvb;
   const int nchunks = (nvb + kOzChunkBlocks - 1) / kOzChunkBlocks;
-  const int arow = it.m0 + 128 * (int)rank, brow = it.n0 + 64 * (int)rank;
+  // B's N columns split between the pair at N / 2 (N = 128, or trimmed to T
+  // on the last column block): CTA r stages rows n0 + r N / 2 ..
+  const int arow = it.m0 + 128 * (int)rank, brow = it.n0 + (oz_tile_n(o, it.n0) / 2) * (int)rank;
   // the d-groups are k_oz_gram's per tile: the pair accumulates the union
   // (every group when either tile is diagonal) and each epilogue takes its own
   const bool small = it.nvb < kOzDropMinBlocks;
@@ -684,7 +697,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only) ----------------
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = idesc_s8(256, 128);
+      const uint32_t idesc = idesc_s8(256, oz_tile_n(o, it.n0));
       int k = 0, npass = 0;
       for (int c = 0; c < nchunks; ++c) {
         const int b0 = c * kOzChunkBlocks, b1 = min(nvb, b0 + kOzChunkBlocks);
@@ -733,6 +746,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     const int32_t* ex = o.expo + (int64_t)it.subj * o.ldexp;
     const int ea = ta < o.nexp ? ex[ta] : 0;
     double* grow = o.g + (int64_t)it.slot * o.gsub + ta * o.ldg + it.n0;
+    const int tn = oz_tile_n(o, it.n0);
     const uint32_t freebar = leader_addr(&accfree);
     int npass = 0;
     for (int c = 0; c < nchunks; ++c) {
@@ -771,7 +785,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
               for (int j = 0; j < 16; ++j) {
                 const int64_t tb = it.n0 + c0 + j;
                 if (tb < o.nout) {
-                  const double g = val[j] * pow2(ea + (tb < o.nexp ? ex[tb] : 0));
+                  const double g = c0 + j < tn ? val[j] * pow2(ea + (tb < o.nexp ? ex[tb] : 0)) : 0.0;
                   grow[c0 + j] = (npass == 0) ? g : prev[j] + g;
                 }
               }
@@ -1274,8 +1288,11 @@ template <int MODE, int NSA, int ND>
 struct RowGemmShape {
   static constexpr int halves = ND > 4 ? 2 : 1;
   static constexpr int a_bytes = MODE == kRowSG ? halves * kOzBox : NSA * 4096;
-  // B: the eight slots of 64 rows x 32 B (k-block of 32 TRs), slot-major
-  static constexpr int b_bytes = 8 * 64 * 32;
+  // B: the slots of 64 rows x 32 B (k-block of 32 TRs), slot-major -- all
+  // eight, or for kRowW with ND <= 6 the six its slot pairs (s2, s2 + 1),
+  // s2 <= ND - 2, read (the map's box must match: make_map_q8 slots)
+  static constexpr int b_slots = (MODE == kRowW && ND <= 6) ? 6 : 8;
+  static constexpr int b_bytes = b_slots * 64 * 32;
   static constexpr int stage_bytes = a_bytes + b_bytes;
   // kRowW keeps a W staging tile (128 rows x 64 features, pitch 65) beside the
   // ring: three stages of seven-slice operands fit with it, four otherwise

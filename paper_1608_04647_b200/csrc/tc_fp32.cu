@@ -488,12 +488,12 @@ cudaError_t make_map_q(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, 
 // (non-monotonic strides) and box {32, 64, 8, 1}, SWIZZLE_32B: one load lands
 // as [slot][row][32 B], so slots j and j + 1 of 64 rows form one 128-row
 // K-major SW32 operand (the N = 128 slice pairs of the int8 row GEMMs)
-cudaError_t make_map_q8(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n) {
+cudaError_t make_map_q8(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n, int slots) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
   cuuint64_t dims[4] = {32, (cuuint64_t)rows, (cuuint64_t)(lq / 32), (cuuint64_t)n};
   cuuint64_t strides[3] = {(cuuint64_t)lq, 32, (cuuint64_t)(lq * rows)};
-  cuuint32_t box[4] = {32, 64, 8, 1};
+  cuuint32_t box[4] = {32, 64, (cuuint32_t)slots, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(reinterpret_cast<CUtensorMap*>(m->opaque), CU_TENSOR_MAP_DATA_TYPE_UINT8, 4,
                   const_cast<int8_t*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -244,8 +244,10 @@ def _gram_pair(xs):
         eng.prepare_gram()
         torch.cuda.synchronize()
         eng.raise_status()
-        g = eng.region(_lib.R_GRAM, torch.float64).view(len(xs), eng.ldx, eng.ldx)[:, :T, :T]
-        out.append(g.cpu().numpy())
+        full = eng.region(_lib.R_GRAM, torch.float64).view(len(xs), eng.ldx, eng.ldx)
+        if i8:  # the padded TRs (T..ldx): zeros, also where a tile's N was trimmed to T
+            assert torch.count_nonzero(full[:, T:, :]) == 0 and torch.count_nonzero(full[:, :, T:]) == 0
+        out.append(full[:, :T, :T].cpu().numpy())
         eng.close()
     return out
 
