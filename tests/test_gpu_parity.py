@@ -970,3 +970,30 @@ def test_nccl_exchange_graph_bit_identical(srm, monkeypatch):
     finally:
         if own:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("k", [10, 64, 100])
+def test_fp32_final_w_in_kernel_slicing_bit_identical(srm, monkeypatch, k):
+    """fp32 X-hat: the final W_i = Xhat_i R_i with the A operand sliced from
+    X-hat inside the kernel (kRowWX: fp32 tiles by TMA, int8 digits by slicer
+    warps) equals the W formed from the stored int8 records (SRM_B200_OZW=
+    records) bit for bit: same digits, same MMAs, same epilogue. Ragged V (a
+    partial 128-voxel tile), one or two 64-feature halves, T = 260 (partial
+    32-TR k-block)."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(4, 1500, 260, k, seed=37)
+    xs = [x.astype(np.float32) for x in xs]
+    xs[1] = xs[1][:1157]
+    cfg = srm.SrmConfig(k=k, iterations=2, seed=3)
+    out = []
+    for mode in (None, "records"):
+        if mode:
+            monkeypatch.setenv("SRM_B200_OZW", mode)
+        else:
+            monkeypatch.delenv("SRM_B200_OZW", raising=False)
+        eng = []
+        out.append(srm.fit(_subjects(srm, xs), cfg, algorithm="gram", engine_out=eng))
+        assert eng[0].gram_i8
+    for wa, wb in zip(out[0].W, out[1].W):
+        assert np.array_equal(wa, wb)
