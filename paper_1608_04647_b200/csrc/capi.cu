@@ -164,6 +164,8 @@ struct srm_plan {
   std::vector<char> sliced;           // srm_prepare_gram_range has been enqueued for the subject
   std::vector<int> ow_first;          // [n_local + 1]: first items_ow entry of each subject
   TmaMap tm_q32, tm_r;
+  TmaMap tm_xw;     // fp32 X-hat, box {32 TRs, 128 voxels}, SWIZZLE_128B (the final W's in-kernel slicing)
+  bool ozw_x = false;  // fp32 X-hat: oz_w slices X-hat in the kernel (opt-in, SRM_B200_OZW=x)
   bool sk_off = false;                // SRM_B200_SG_PER_TILE=1: per-tile B = S G / 2 (test knob)
   int sk_ctas = 0;                    // stream-K B = S G / 2: persistent CTAs (SMs less two for the side lane)
   TsqrSchedule qr;                    // SRM_FLAG_EXACT_POLAR: TSQR levels over the local A_i (job table: level-major)
@@ -394,6 +396,12 @@ void build_work(srm_plan* p) {
   p->oz_sg = (p->flags & SRM_FLAG_GRAM_I8) && p->kp <= 128;
   p->oz_lqg = p->ldx / 32 * kOzRecord;
   p->oz_w = p->oz_sg;
+  {
+    // opt-in (SRM_B200_OZW=x): bit-identical, but measured 3-4x slower than the
+    // records path so far (cfg 5: 139 vs 37 ms)
+    const char* env = getenv("SRM_B200_OZW");
+    p->ozw_x = p->oz_w && p->dtype == SRM_F32 && env && !strcmp(env, "x");
+  }
   {
     int dev = 0, sms = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
@@ -836,16 +844,22 @@ std::vector<std::string> g_profile_names;
 // local subjects [first, first + count).  The shared prelude runs with the
 // range that starts at subject 0; only the int8 W = Xhat R is split by
 // subject (the other variants form every W_i in that first range).
+// W = Xhat R over the final-W items [i0, i1): from the int8 records, or for fp32
+// X-hat with the A operand sliced from X-hat in the kernel (ozw_x)
+cudaError_t run_oz_w(srm_plan* p, const DevPlan& d, int i0, int i1, cudaStream_t st) {
+  if (p->ozw_x)
+    return launch_oz_wx(p->tm_xw, p->tm_r, region<int32_t>(p, I_OZEXP), region<int32_t>(p, I_OZREXP), d.wout,
+                        region<OzItem>(p, I_ITEMS_OW) + i0, i1 - i0, p->ldx, p->kp, p->K, st);
+  return launch_oz_w(p->tm_q32, p->tm_r, region<int32_t>(p, I_OZREXP), d.wout, region<OzItem>(p, I_ITEMS_OW) + i0,
+                     i1 - i0, p->ldx, p->kp, p->K, p->oz_nsl, st);
+}
+
 std::vector<Stage> finalize_stages(srm_plan* p, int first, int count) {
   const DevPlan& d = p->dp;
   std::vector<Stage> v;
   if (p->oz_w && first > 0) {
     const int i0 = p->ow_first[first], i1 = p->ow_first[first + count];
-    v.push_back({"oz_w", [p, d, i0, i1](cudaStream_t st) {
-                   return launch_oz_w(p->tm_q32, p->tm_r, region<int32_t>(p, I_OZREXP), d.wout,
-                                      region<OzItem>(p, I_ITEMS_OW) + i0, i1 - i0, p->ldx, p->kp, p->K,
-                                      p->oz_nsl, st);
-                 }});
+    v.push_back({"oz_w", [p, d, i0, i1](cudaStream_t st) { return run_oz_w(p, d, i0, i1, st); }});
     return v;
   }
   if (first > 0) return v;
@@ -861,10 +875,7 @@ std::vector<Stage> finalize_stages(srm_plan* p, int first, int count) {
                                                region<int8_t>(p, I_OZR), p->oz_lqg, region<int32_t>(p, I_OZREXP), st);
                  }});
     const int i1 = p->ow_first[count];
-    v.push_back({"oz_w", [p, d, i1](cudaStream_t st) {
-                   return launch_oz_w(p->tm_q32, p->tm_r, region<int32_t>(p, I_OZREXP), d.wout,
-                                      region<OzItem>(p, I_ITEMS_OW), i1, p->ldx, p->kp, p->K, p->oz_nsl, st);
-                 }});
+    v.push_back({"oz_w", [p, d, i1](cudaStream_t st) { return run_oz_w(p, d, 0, i1, st); }});
     return v;
   }
   if (p->flags & SRM_FLAG_GRAM) {  // A_i = Xhat_i S^T / 2 is not kept per iteration on the Gram path
@@ -1233,6 +1244,11 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
         e = make_map_q8(&p->tm_r, region<int8_t>(p, I_OZR), p->oz_lqg, p->kp, p->n_local, p->oz_nsl == 4 ? 6 : 8);
       if (e == cudaSuccess)
         e = launch_oz_w(p->tm_q32, p->tm_r, nullptr, nullptr, nullptr, 0, p->ldx, p->kp, p->K, p->oz_nsl, 0);
+      if (e == cudaSuccess && p->ozw_x) {
+        e = make_map_f32(&p->tm_xw, static_cast<const float*>(d.xhat), p->ldx, p->rows_total, p->ldx, 32, 128, true);
+        if (e == cudaSuccess)
+          e = launch_oz_wx(p->tm_xw, p->tm_r, nullptr, nullptr, nullptr, nullptr, 0, p->ldx, p->kp, p->K, 0);
+      }
     }
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");

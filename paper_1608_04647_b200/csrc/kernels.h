@@ -117,6 +117,11 @@ cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* exp
 // W rows = Qt (voxel-major X-hat slices) x the row slices of R'^T (kp <= 64)
 cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* rexp, double* W, const OzItem* items,
                         int n_items, int64_t ldx, int64_t kp, int64_t K, int nsl, cudaStream_t st);
+// fp32 X-hat: the same W with the A operand sliced in the kernel from X-hat
+// (tmx: fp32 [rows_total][ldx], box {32, 128}, SWIZZLE_128B; xexp: the column
+// exponents k_oz_split_f32 used), bit-identical to launch_oz_w's
+cudaError_t launch_oz_wx(const TmaMap& tmx, const TmaMap& tmr, const int32_t* xexp, const int32_t* rexp, double* W,
+                         const OzItem* items, int n_items, int64_t ldx, int64_t kp, int64_t K, cudaStream_t st);
 size_t oz_gram_smem_bytes();
 // init E-step on the int8 tensor cores: B_i = G_i^T Xhat_i (G = the N(0,1) draw
 // in AMAT) into bred, from G's seven-slice records [i][k][vb] (qg, pitch lqg)

@@ -1277,7 +1277,14 @@ __global__ void __launch_bounds__(256) k_oz_slice_rows_wide(const double* __rest
 // folded into R), so W[v][f] = 2^{r_f} sum_d 2^{-12-7d} (...)[v][f].
 // ---------------------------------------------------------------------------
 constexpr int kSgStages = 4;
-enum RowGemmMode { kRowSG = 0, kRowW = 1 };
+// kRowWX: the final W of four-slice (fp32) X-hat with the A operand sliced in
+// the kernel from X-hat itself: TMA brings 128 voxels x 32 TRs of fp32 as
+// 128-byte rows (the records' 32-byte voxel runs bound kRowW by TMA row issue,
+// ~0.3 of HBM), four slicer warps cut them into the same int8 digits the
+// records hold (k_oz_split_f32's N = rint(x 2^(27 - e_t)), balanced base-128)
+// and write them K-major (SWIZZLE_32B, the layout TMA gives the B operand), so
+// the MMAs and the result are kRowW's bit for bit
+enum RowGemmMode { kRowSG = 0, kRowW = 1, kRowWX = 2 };
 
 // Per-stage shared memory of k_oz_rowgemm<MODE, NSA, ND>: the A boxes (kRowSG:
 // the G record halves holding the slices used; kRowW: NSA MN-major slices of
@@ -1288,17 +1295,21 @@ template <int MODE, int NSA, int ND>
 struct RowGemmShape {
   static constexpr int halves = ND > 4 ? 2 : 1;
   static constexpr int a_bytes = MODE == kRowSG ? halves * kOzBox : NSA * 4096;
+  // kRowWX: the fp32 X-hat tile ahead of the slices (128 rows x 128 B, SWIZZLE_128B)
+  static constexpr int x_bytes = MODE == kRowWX ? 128 * 32 * 4 : 0;
   // B: the slots of 64 rows x 32 B (k-block of 32 TRs), slot-major -- all
   // eight, or for kRowW with ND <= 6 the six its slot pairs (s2, s2 + 1),
   // s2 <= ND - 2, read (the map's box must match: make_map_q8 slots)
-  static constexpr int b_slots = (MODE == kRowW && ND <= 6) ? 6 : 8;
+  static constexpr int b_slots = (MODE != kRowSG && ND <= 6) ? 6 : 8;
   static constexpr int b_bytes = b_slots * 64 * 32;
-  static constexpr int stage_bytes = a_bytes + b_bytes;
+  static constexpr int stage_bytes = x_bytes + a_bytes + b_bytes;
   // kRowW keeps a W staging tile (128 rows x 64 features, pitch 65) beside the
   // ring: three stages of seven-slice operands fit with it, four otherwise
-  static constexpr int stages = (MODE == kRowW && NSA > 4) ? 3 : kSgStages;
+  static constexpr int stages = ((MODE == kRowW && NSA > 4) || MODE == kRowWX) ? 3 : kSgStages;
   static constexpr int wst_pitch = 65;
-  static constexpr int wst_bytes = MODE == kRowW ? 128 * wst_pitch * 8 : 0;
+  static constexpr int wst_bytes = MODE != kRowSG ? 128 * wst_pitch * 8 : 0;
+  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue; kRowWX: warps 10-13 slice
+  static constexpr int threads = MODE == kRowWX ? 448 : 320;
   static constexpr uint32_t tmem_cols = 512;  // eight 64-column d-groups (d = 7 unused)
   static constexpr int ctas_per_sm = 1;
   static constexpr size_t smem_bytes = (size_t)stages * stage_bytes + wst_bytes + 1024;
@@ -1386,14 +1397,14 @@ __device__ __forceinline__ double oz_hl_value(long long H, long long L) {
 // k-blocks while the epilogue drains the last, and the MMA warp waits only
 // for the accumulators to be drained (accempty).
 template <int MODE, int NSA, int ND>
-__global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas_per_sm)
+__global__ void __launch_bounds__(RowGemmShape<MODE, NSA, ND>::threads, RowGemmShape<MODE, NSA, ND>::ctas_per_sm)
     k_oz_rowgemm(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, RowGemmArgs g) {
   using Shape = RowGemmShape<MODE, NSA, ND>;
   constexpr int kStage = Shape::stage_bytes;
   constexpr int kSt = Shape::stages;
   extern __shared__ __align__(1024) unsigned char oz_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t full[kSt], empty[kSt], accfull, accempty;
+  __shared__ uint64_t full[kSt], empty[kSt], sliced[kSt], accfull, accempty;
   __shared__ uint32_t tmem_base;
   const int64_t ldx = g.ldx, kp = g.kp, ldo = g.ldo;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1403,6 +1414,7 @@ __global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas
       for (int s = 0; s < kSt; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], 1);
+        mbar_init(&sliced[s], 4);  // kRowWX: one arrival per slicer warp
       }
       mbar_init(&accfull, 1);
       mbar_init(&accempty, kRowEpi / 32);
@@ -1424,8 +1436,11 @@ __global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas
           const int slot = kk % kSt;
           if (kk >= kSt) mbar_wait(&empty[slot], ((kk / kSt) - 1) & 1);
           unsigned char* st = smem + slot * kStage;
-          mbar_expect_tx(&full[slot], (uint32_t)kStage);
-          if (MODE == kRowSG) {
+          mbar_expect_tx(&full[slot], (uint32_t)(MODE == kRowWX ? kStage - Shape::a_bytes : kStage));
+          if (MODE == kRowWX) {
+            // fp32 X-hat rows v0 .. v0 + 127 (global), TRs 32 k .. 32 k + 31
+            tma_load_2d(st, &tma, k * 32, tl.n0, &full[slot]);
+          } else if (MODE == kRowSG) {
             // tiled G slices: (128-row block, k-block, record half) rows of 128 B
             const int grow = ((tl.arow / 128) * nub + k) * 256;
             tma_load_3d(st, &tma, 0, grow, tl.i, &full[slot]);
@@ -1434,7 +1449,8 @@ __global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas
             // Q records of 32 TRs x 4 voxel blocks x nsa slots -> [slot][vb][t][32 B]
             tma_load_5d(st, &tma, 0, k * 32, tl.arow / 32, 0, tl.i, &full[slot]);
           }
-          tma_load_4d(st + Shape::a_bytes, &tmb, 0, tl.z * 64, k * 8, MODE == kRowSG ? 0 : tl.i, &full[slot]);
+          tma_load_4d(st + Shape::x_bytes + Shape::a_bytes, &tmb, 0, tl.z * 64, k * 8, MODE == kRowSG ? 0 : tl.i,
+                      &full[slot]);
         }
       }
     }
@@ -1444,20 +1460,22 @@ __global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas
       // N = 128: B is the slot pair (s2, s2 + 1) of 64 features each, so one MMA
       // feeds d-groups s + s2 and s + s2 + 1 (adjacent 64-column accumulators);
       // an N = 64 MMA costs the same tensor-pipe time as N = 128 (tools/i8_peak.cu)
-      constexpr uint32_t idesc = idesc_s8(128, 128) | (MODE == kRowW ? (1u << 15) : 0u);
+      constexpr uint32_t idesc = idesc_s8(128, 128) | (MODE == kRowW ? (1u << 15) : 0u);  // kRowWX: A K-major
       int kk = 0, li = 0;
       for (int w = blockIdx.x; w < g.n_work; w += gridDim.x, ++li) {
         if (li > 0) mbar_wait(&accempty, (li - 1) & 1);  // the last tile's accumulators drained
         asm volatile("tcgen05.fence::after_thread_sync;");
         for (int k = 0; k < nub; ++k, ++kk) {
           const int slot = kk % kSt;
-          mbar_wait(&full[slot], (kk / kSt) & 1);
+          mbar_wait(MODE == kRowWX ? &sliced[slot] : &full[slot], (kk / kSt) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t sa = smem_u32(smem + slot * kStage);
+          const uint32_t sa = smem_u32(smem + slot * kStage + Shape::x_bytes);
           const uint32_t sb = sa + Shape::a_bytes;
           // one descriptor per operand and stage; a slice is a constant offset of
           // the 16-byte address field (no carry: smem addresses < 2^18)
-          const uint64_t da0 = MODE == kRowSG ? umma_desc_sw128(sa) : umma_desc_sw32_mn(sa, 1024, 256);
+          const uint64_t da0 = MODE == kRowSG   ? umma_desc_sw128(sa)
+                               : MODE == kRowW  ? umma_desc_sw32_mn(sa, 1024, 256)
+                                                : umma_desc_sw32_mn(sa, 16, 256);  // kRowWX: K-major, as B
           // K-major SWIZZLE_32B: 8-row atoms of 256 B (SBO); slot j starts at 2 KB j
           const uint64_t db0 = umma_desc_sw32_mn(sb, 16, 256);
           const uint32_t keep = k == 0 ? 0u : 1u;
@@ -1475,6 +1493,64 @@ __global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas
           mma_commit(&empty[slot]);
         }
         mma_commit(&accfull);
+      }
+    }
+  } else if (MODE == kRowWX && warp >= 10) {
+    // ---------------- slicers (kRowWX): thread r cuts voxel row r of the tile ----------------
+    const int r = (int)threadIdx.x - 320;
+    int kk = 0;
+    for (int w = blockIdx.x; w < g.n_work; w += gridDim.x) {
+      const RowTile tl = row_tile<MODE>(g, w);
+      const int32_t* ex = g.aexp + (int64_t)tl.i * ldx;  // X-hat column exponents e_t (k_oz_split_f32's)
+      for (int k = 0; k < nub; ++k, ++kk) {
+        const int slot = kk % kSt;
+        int e[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) e[j] = __ldg(ex + k * 32 + j);
+        mbar_wait(&full[slot], (kk / kSt) & 1);
+        const unsigned char* xs = smem + slot * kStage;  // [128 rows][128 B], SWIZZLE_128B
+        unsigned char* as = smem + slot * kStage + Shape::x_bytes;
+        uint32_t wd[4][8];  // [slice][four TRs per word]
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          // 16-byte chunk c of row r sits at chunk c ^ (r & 7)
+          const float4 q = *reinterpret_cast<const float4*>(xs + r * 128 + ((c ^ (r & 7)) << 4));
+          const float xv[4] = {q.x, q.y, q.z, q.w};
+          int dg[4][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ej = e[4 * c + u];
+            int n;
+            if (ej >= -100 && ej <= 153)
+              n = __float2int_rn(xv[u] * __int_as_float((127 + 27 - ej) << 23));
+            else
+              n = __double2int_rn((double)xv[u] * ldexp(1.0, 27 - ej));
+#pragma unroll
+            for (int sl = 3; sl >= 1; --sl) {
+              const int n1 = (n + 64) >> 7;
+              dg[sl][u] = n - (n1 << 7);
+              n = n1;
+            }
+            dg[0][u] = n;
+          }
+#pragma unroll
+          for (int sl = 0; sl < 4; ++sl) {
+            const uint32_t lo = __byte_perm((uint32_t)dg[sl][0], (uint32_t)dg[sl][1], 0x0040);
+            const uint32_t hi = __byte_perm((uint32_t)dg[sl][2], (uint32_t)dg[sl][3], 0x0040);
+            wd[sl][c] = __byte_perm(lo, hi, 0x5410);
+          }
+        }
+        // slice sl, row r: 32 bytes (TRs 0-31) as two 16-byte chunks, chunk h at h ^ ((r >> 2) & 1)
+        // (TMA SWIZZLE_32B's layout of 32-byte rows)
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            *reinterpret_cast<uint4*>(as + sl * 4096 + r * 32 + ((h ^ ((r >> 2) & 1)) << 4)) =
+                make_uint4(wd[sl][4 * h], wd[sl][4 * h + 1], wd[sl][4 * h + 2], wd[sl][4 * h + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tcgen05 reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sliced[slot]);
       }
     }
   } else {
@@ -1521,7 +1597,7 @@ __global__ void __launch_bounds__(kRowThreads, RowGemmShape<MODE, NSA, ND>::ctas
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(&accempty);
-      if (MODE == kRowW) {
+      if (MODE != kRowSG) {
         asm volatile("bar.sync 1, %0;" ::"r"(kRowEpi) : "memory");  // the staged tile is complete
         const int K = (int)g.K;
         const int nc = min(64, K - f0);  // this tile's columns f0 .. f0 + nc - 1 of W
@@ -1811,7 +1887,7 @@ cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, RowGemmArgs g, int m
   if (g.n_work <= 0) return cudaSuccess;
   if (g.kp > 128 || g.ldx % 32 != 0) return cudaErrorInvalidValue;
   const int grid = max_ctas > 0 ? std::min(g.n_work, max_ctas) : g.n_work;
-  k_oz_rowgemm<MODE, NSA, ND><<<grid, kRowThreads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(ta.opaque),
+  k_oz_rowgemm<MODE, NSA, ND><<<grid, RowGemmShape<MODE, NSA, ND>::threads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(ta.opaque),
                                                                *reinterpret_cast<const CUtensorMap*>(tb.opaque), g);
   return cudaGetLastError();
 }
@@ -1896,6 +1972,13 @@ cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* re
   // 2^-27 truncation of X-hat's own slices (tools/slice_drop_probe.py)
   if (nsl == 4) return run_rowgemm<kRowW, 4, 5>(tmqt, tmr, g, sm_count(), st);
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_oz_wx(const TmaMap& tmx, const TmaMap& tmr, const int32_t* xexp, const int32_t* rexp, double* W,
+                         const OzItem* items, int n_items, int64_t ldx, int64_t kp, int64_t K, cudaStream_t st) {
+  RowGemmArgs g{xexp, rexp, W, items, ldx, kp, 0, K, 0, 0, (int)((kp + 63) / 64), 0};
+  g.n_work = n_items * g.nz;
+  return run_rowgemm<kRowWX, 4, 5>(tmx, tmr, g, sm_count(), st);
 }
 
 cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first, int count,
