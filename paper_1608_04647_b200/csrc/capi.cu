@@ -246,7 +246,7 @@ void layout(srm_plan* p) {
   sz[I_OZGEXP] = p->oz_sg ? (int64_t)p->n_local * p->ldx * 4 : 0;
   sz[I_OZS] = p->oz_sg ? p->kp * p->oz_lqg : 0;
   sz[I_OZSEXP] = p->oz_sg ? p->kp * 4 : 0;
-  sz[I_OZR] = p->oz_w ? (int64_t)p->n_local * p->kp * p->oz_lqg : 0;
+  sz[I_OZR] = p->oz_w ? (int64_t)p->n_local * oz_rtiled_bytes(p->kp, p->ldx) : 0;  // zeroed at bind: rows past kp
   sz[I_OZREXP] = p->oz_w ? (int64_t)p->n_local * p->kp * 4 : 0;
   sz[I_ITEMS_OW] = (int64_t)p->items_ow.size() * sizeof(OzItem);
   sz[I_OZSKPART] = p->oz_sg ? (int64_t)p->sk_ctas * oz_sk_park_bytes() : 0;
@@ -848,10 +848,11 @@ std::vector<std::string> g_profile_names;
 // X-hat with the A operand sliced from X-hat in the kernel (ozw_x)
 cudaError_t run_oz_w(srm_plan* p, const DevPlan& d, int i0, int i1, cudaStream_t st) {
   if (p->ozw_x)
-    return launch_oz_wx(p->tm_xw, p->tm_r, region<int32_t>(p, I_OZEXP), region<int32_t>(p, I_OZREXP), d.wout,
-                        region<OzItem>(p, I_ITEMS_OW) + i0, i1 - i0, p->ldx, p->kp, p->K, st);
-  return launch_oz_w(p->tm_q32, p->tm_r, region<int32_t>(p, I_OZREXP), d.wout, region<OzItem>(p, I_ITEMS_OW) + i0,
-                     i1 - i0, p->ldx, p->kp, p->K, p->oz_nsl, st);
+    return launch_oz_wx(p->tm_xw, p->tm_r, region<int8_t>(p, I_OZR), region<int32_t>(p, I_OZEXP),
+                        region<int32_t>(p, I_OZREXP), d.wout, region<OzItem>(p, I_ITEMS_OW) + i0, i1 - i0, p->ldx,
+                        p->kp, p->K, st);
+  return launch_oz_w(p->tm_q32, p->tm_r, region<int8_t>(p, I_OZR), region<int32_t>(p, I_OZREXP), d.wout,
+                     region<OzItem>(p, I_ITEMS_OW) + i0, i1 - i0, p->ldx, p->kp, p->K, p->oz_nsl, st);
 }
 
 std::vector<Stage> finalize_stages(srm_plan* p, int first, int count) {
@@ -872,7 +873,8 @@ std::vector<Stage> finalize_stages(srm_plan* p, int first, int count) {
                  }});
     v.push_back({"oz_slice_r", [p, d](cudaStream_t st) {
                    return launch_oz_slice_rows(d.part, p->ldx, (int64_t)p->n_local * p->kp, p->ldx,
-                                               region<int8_t>(p, I_OZR), p->oz_lqg, region<int32_t>(p, I_OZREXP), st);
+                                               region<int8_t>(p, I_OZR), p->oz_lqg, region<int32_t>(p, I_OZREXP), st,
+                                               -p->kp);
                  }});
     const int i1 = p->ow_first[count];
     v.push_back({"oz_w", [p, d, i1](cudaStream_t st) { return run_oz_w(p, d, 0, i1, st); }});
@@ -1243,11 +1245,11 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
       if (e == cudaSuccess)
         e = make_map_q8(&p->tm_r, region<int8_t>(p, I_OZR), p->oz_lqg, p->kp, p->n_local, p->oz_nsl == 4 ? 6 : 8);
       if (e == cudaSuccess)
-        e = launch_oz_w(p->tm_q32, p->tm_r, nullptr, nullptr, nullptr, 0, p->ldx, p->kp, p->K, p->oz_nsl, 0);
+        e = launch_oz_w(p->tm_q32, p->tm_r, nullptr, nullptr, nullptr, nullptr, 0, p->ldx, p->kp, p->K, p->oz_nsl, 0);
       if (e == cudaSuccess && p->ozw_x) {
         e = make_map_f32(&p->tm_xw, static_cast<const float*>(d.xhat), p->ldx, p->rows_total, p->ldx, 32, 128, true);
         if (e == cudaSuccess)
-          e = launch_oz_wx(p->tm_xw, p->tm_r, nullptr, nullptr, nullptr, nullptr, 0, p->ldx, p->kp, p->K, 0);
+          e = launch_oz_wx(p->tm_xw, p->tm_r, nullptr, nullptr, nullptr, nullptr, nullptr, 0, p->ldx, p->kp, p->K, 0);
       }
     }
   }

@@ -98,6 +98,11 @@ cudaError_t make_map_q5(TmaMap* m, const int8_t* base, int64_t lq, int64_t ldx, 
 cudaError_t make_map_q8(TmaMap* m, const int8_t* base, int64_t lq, int64_t rows, int64_t n, int slots = 8);
 // int8 slices of the rows of a row-major fp64 matrix (ozaki.cu): 2^e[r] >= max|M[r][:]|
 // tile_rows > 0: the tiled layout of the G_i slices (rows per G_i; oz_tiled_bytes per G_i)
+// tile_rows < 0: the tiled layout of R'^T for the final W (-tile_rows = kp rows per
+// subject): [subject][32-column block][64-row half][8 slots][64 rows][32 B] in the
+// SWIZZLE_32B chunk order, kOzRTile bytes per (block, half); rows past kp stay as zeroed
+constexpr int64_t kOzRTile = 8 * 64 * 32;
+inline int64_t oz_rtiled_bytes(int64_t kp, int64_t ncols) { return (kp + 63) / 64 * (ncols / 32) * kOzRTile; }
 cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int64_t ncols, int8_t* q, int64_t lq,
                                  int32_t* expo, cudaStream_t st, int64_t tile_rows = 0);
 size_t oz_tiled_bytes(int64_t rows, int64_t ncols);
@@ -115,13 +120,15 @@ cudaError_t launch_oz_sg_sk(const TmaMap& tmg, const TmaMap& tms, const int32_t*
 cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* expo, double* rt, int64_t ldx,
                          int64_t kp, int64_t K, int n_local, cudaStream_t st);
 // W rows = Qt (voxel-major X-hat slices) x the row slices of R'^T (kp <= 64)
-cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* rexp, double* W, const OzItem* items,
-                        int n_items, int64_t ldx, int64_t kp, int64_t K, int nsl, cudaStream_t st);
+// (rt: the tiled slices of R'^T, launch_oz_slice_rows with tile_rows = -kp)
+cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int8_t* rt, const int32_t* rexp, double* W,
+                        const OzItem* items, int n_items, int64_t ldx, int64_t kp, int64_t K, int nsl, cudaStream_t st);
 // fp32 X-hat: the same W with the A operand sliced in the kernel from X-hat
 // (tmx: fp32 [rows_total][ldx], box {32, 128}, SWIZZLE_128B; xexp: the column
 // exponents k_oz_split_f32 used), bit-identical to launch_oz_w's
-cudaError_t launch_oz_wx(const TmaMap& tmx, const TmaMap& tmr, const int32_t* xexp, const int32_t* rexp, double* W,
-                         const OzItem* items, int n_items, int64_t ldx, int64_t kp, int64_t K, cudaStream_t st);
+cudaError_t launch_oz_wx(const TmaMap& tmx, const TmaMap& tmr, const int8_t* rt, const int32_t* xexp,
+                         const int32_t* rexp, double* W, const OzItem* items, int n_items, int64_t ldx, int64_t kp,
+                         int64_t K, cudaStream_t st);
 size_t oz_gram_smem_bytes();
 // init E-step on the int8 tensor cores: B_i = G_i^T Xhat_i (G = the N(0,1) draw
 // in AMAT) into bred, from G's seven-slice records [i][k][vb] (qg, pitch lqg)

@@ -1210,6 +1210,15 @@ __global__ void __launch_bounds__(256) k_oz_slice_rows(const double* __restrict_
       int8_t* dst;
       if (tile_rows == 0) {
         dst = q + r * lq + b * kOzRecord + lane * 16;
+      } else if (tile_rows < 0) {
+        // tiled (R'^T of the final W, -tile_rows = kp rows per subject): per
+        // (subject, k-block, 64-row half) the eight slots of 64 rows x 32 B, contiguous
+        // and already in TMA SWIZZLE_32B order (16-byte chunk h of row r at h ^ ((r >> 2) & 1)),
+        // so the B operand of a k-block is one bulk copy instead of 64 x slots 32-byte rows
+        const int64_t kpr = -tile_rows, i = r / kpr, f = r - i * kpr;
+        const int64_t nz = (kpr + 63) / 64, nub = ncols / 32, rr = f & 63;
+        dst = q + ((i * nub + b) * nz + (f >> 6)) * kOzRTile + (lane >> 1) * 2048 + rr * 32 +
+              (((lane & 1) ^ ((rr >> 2) & 1)) << 4);
       } else {
         // tiled (G_i): record halves of 128 rows x one k-block contiguous
         const int64_t i = r / tile_rows, t = r - i * tile_rows;
@@ -1320,6 +1329,7 @@ struct RowGemmArgs {
   const int32_t* bexp;   // kRowSG: S row exponents [kp]; kRowW: R'^T row exponents [n_local][kp]
   double* out;           // kRowSG: bred; kRowW: W [rows_total][K]
   const OzItem* items;   // kRowW: {subject, local voxel v0, global row of v0, valid rows}
+  const int8_t* bt;      // kRowW / kRowWX: the tiled R'^T slices (k_oz_slice_rows, tile_rows < 0)
   int64_t ldx, kp, ldo, K;
   int first;             // kRowSG: subject of the first tile
   int n_work;            // tiles: kRowSG (subject, 128-TR block, feature half); kRowW (item, feature half)
@@ -1449,8 +1459,11 @@ __global__ void __launch_bounds__(RowGemmShape<MODE, NSA, ND>::threads, RowGemmS
             // Q records of 32 TRs x 4 voxel blocks x nsa slots -> [slot][vb][t][32 B]
             tma_load_5d(st, &tma, 0, k * 32, tl.arow / 32, 0, tl.i, &full[slot]);
           }
-          tma_load_4d(st + Shape::x_bytes + Shape::a_bytes, &tmb, 0, tl.z * 64, k * 8, MODE == kRowSG ? 0 : tl.i,
-                      &full[slot]);
+          if (MODE == kRowSG)
+            tma_load_4d(st + Shape::x_bytes + Shape::a_bytes, &tmb, 0, tl.z * 64, k * 8, 0, &full[slot]);
+          else  // one contiguous run of the slots read, already in the SWIZZLE_32B order
+            bulk_load(st + Shape::x_bytes + Shape::a_bytes,
+                      g.bt + (((int64_t)tl.i * nub + k) * g.nz + tl.z) * kOzRTile, (uint32_t)Shape::b_bytes, &full[slot]);
         }
       }
     }
@@ -1851,7 +1864,7 @@ cudaError_t launch_oz_slice_rows(const double* M, int64_t ldm, int64_t rows, int
                                  int32_t* expo, cudaStream_t st, int64_t tile_rows) {
   if (rows <= 0) return cudaSuccess;
   if (ncols % 32 != 0) return cudaErrorInvalidValue;
-  if (tile_rows == 0 && rows <= 1024)
+  if (tile_rows == 0 && rows <= 1024)  // (the tiled layouts go through k_oz_slice_rows)
     k_oz_slice_rows_wide<<<(unsigned)rows, 256, 0, st>>>(M, ldm, ncols, q, lq, expo);
   else
     k_oz_slice_rows<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(M, ldm, rows, ncols, q, lq, expo, tile_rows);
@@ -1896,7 +1909,7 @@ cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, RowGemmArgs g, int m
 
 cudaError_t launch_oz_sg(const TmaMap& tmg, const TmaMap& tms, const int32_t* gexp, const int32_t* sexp,
                          double* bred, int64_t ldx, int64_t kp, int64_t ldo, int first, int count, cudaStream_t st) {
-  RowGemmArgs g{gexp, sexp, bred, nullptr, ldx, kp, ldo, 0, first, 0, (int)((kp + 63) / 64), (int)((ldx + 127) / 128)};
+  RowGemmArgs g{gexp, sexp, bred, nullptr, nullptr, ldx, kp, ldo, 0, first, 0, (int)((kp + 63) / 64), (int)((ldx + 127) / 128)};
   g.n_work = count * g.nz * g.ntb;
   return run_rowgemm<kRowSG, kOzSlices, 7>(tmg, tms, g, 0, st);
 }
@@ -1961,9 +1974,9 @@ cudaError_t launch_oz_rt(const double* mmat, const double* S, const int32_t* exp
   return cudaGetLastError();
 }
 
-cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* rexp, double* W, const OzItem* items,
-                        int n_items, int64_t ldx, int64_t kp, int64_t K, int nsl, cudaStream_t st) {
-  RowGemmArgs g{nullptr, rexp, W, items, ldx, kp, 0, K, 0, 0, (int)((kp + 63) / 64), 0};
+cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int8_t* rt, const int32_t* rexp, double* W,
+                        const OzItem* items, int n_items, int64_t ldx, int64_t kp, int64_t K, int nsl, cudaStream_t st) {
+  RowGemmArgs g{nullptr, rexp, W, items, rt, ldx, kp, 0, K, 0, 0, (int)((kp + 63) / 64), 0};
   g.n_work = n_items * g.nz;
   if (nsl == 7) return run_rowgemm<kRowW, 7, 7>(tmqt, tmr, g, sm_count(), st);
   // fp32 X-hat: d-groups 0-4 (8 MMAs per k-block instead of 12).  R's slices
@@ -1974,9 +1987,10 @@ cudaError_t launch_oz_w(const TmaMap& tmqt, const TmaMap& tmr, const int32_t* re
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_oz_wx(const TmaMap& tmx, const TmaMap& tmr, const int32_t* xexp, const int32_t* rexp, double* W,
-                         const OzItem* items, int n_items, int64_t ldx, int64_t kp, int64_t K, cudaStream_t st) {
-  RowGemmArgs g{xexp, rexp, W, items, ldx, kp, 0, K, 0, 0, (int)((kp + 63) / 64), 0};
+cudaError_t launch_oz_wx(const TmaMap& tmx, const TmaMap& tmr, const int8_t* rt, const int32_t* xexp,
+                         const int32_t* rexp, double* W, const OzItem* items, int n_items, int64_t ldx, int64_t kp,
+                         int64_t K, cudaStream_t st) {
+  RowGemmArgs g{xexp, rexp, W, items, rt, ldx, kp, 0, K, 0, 0, (int)((kp + 63) / 64), 0};
   g.n_work = n_items * g.nz;
   return run_rowgemm<kRowWX, 4, 5>(tmx, tmr, g, sm_count(), st);
 }
