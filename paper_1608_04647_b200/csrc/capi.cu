@@ -161,6 +161,7 @@ struct srm_plan {
   std::vector<OzItem> items_gg;       // (subject, V chunk) of the int8 G^T G of the init draw (kp > 64)
   int64_t oz_lqg_init = 0;            // bytes per sliced row (feature) of the init draw G (records in WOUT)
   TmaMap tm_gi, tm_gi64;
+  std::vector<cudaEvent_t> post_events;  // batched int8 Gram: batch b's Gram done (mirror / G slices follow on hi_stream2)
   std::vector<char> sliced;           // srm_prepare_gram_range has been enqueued for the subject
   std::vector<int> ow_first;          // [n_local + 1]: first items_ow entry of each subject
   TmaMap tm_q32, tm_r;
@@ -1085,6 +1086,7 @@ int srm_plan_destroy(srm_plan* plan) {
         cudaEventDestroy(plan->lanes.join[l]);
       }
     for (cudaEvent_t ev : plan->gram_events) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : plan->post_events) cudaEventDestroy(ev);
     if (plan->hi_stream) cudaStreamDestroy(plan->hi_stream);
     if (plan->hi_stream2) cudaStreamDestroy(plan->hi_stream2);
     for (cudaEvent_t ev : plan->pair_events) cudaEventDestroy(ev);
@@ -1515,7 +1517,15 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
       if (e0 == cudaSuccess) e0 = cudaStreamCreateWithPriority(&p->hi_stream2, cudaStreamNonBlocking, hi);
       if (e0 != cudaSuccess) return cuda_fail(e0, "gram stream");
     }
-    cudaStream_t gs = p->hi_stream;
+    // a batch's mirror and G row slices run on the second high-priority stream
+    // behind the batch's Gram, so the next batch's Gram starts at once
+    while ((int)p->post_events.size() < nb) {
+      cudaEvent_t ev;
+      const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "gram events");
+      p->post_events.push_back(ev);
+    }
+    cudaStream_t gs = p->hi_stream, ps = p->hi_stream2;
     cudaError_t e = cudaEventRecord(ln->fork[1], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ln->side[1], ln->fork[1], 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(gs, ln->fork[1], 0);
@@ -1537,13 +1547,20 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
           if (e == cudaSuccess) e = cudaEventRecord(p->pair_events[b], p->hi_stream2);
           continue;
         }
-        e = v[k].fn(gs);
-        if (e == cudaSuccess && !strcmp(v[k].name, "oz_gram") && !p->items_oz2.empty())
-          e = cudaStreamWaitEvent(gs, p->pair_events[b], 0);
+        if (!strcmp(v[k].name, "oz_gram")) {
+          e = v[k].fn(gs);
+          if (e == cudaSuccess && !p->items_oz2.empty()) e = cudaStreamWaitEvent(gs, p->pair_events[b], 0);
+          if (e == cudaSuccess) e = cudaEventRecord(p->post_events[b], gs);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(ps, p->post_events[b], 0);
+          continue;
+        }
+        e = v[k].fn(ps);  // mirror_gram, oz_slice_g
       }
     }
     if (e == cudaSuccess) e = cudaEventRecord(ln->join[1], gs);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ln->join[1], 0);
+    if (e == cudaSuccess) e = cudaEventRecord(ln->join[2], ps);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ln->join[2], 0);
     return check(e, "prepare_gram");
   }
   for (const Stage& s : gram_stages(p, first, count)) {
