@@ -68,11 +68,16 @@ __device__ __forceinline__ int frexp_exp(double m) {
 
 // ---------------------------------------------------------------------------
 // split: grid (32-voxel blocks, 64-column tiles, subjects); thread (t, quarter)
-// handles 8 voxels of one column, 4 voxels per packed 32-bit word.  17 KB of
-// shared memory per CTA, so split CTAs fit beside a resident k_oz_gram CTA
-// (193 KB) and the slicing of later subjects overlaps the Gram of earlier ones.
+// handles 8 voxels of one column, 4 voxels per packed 32-bit word.  The
+// slicing of later subjects is enqueued beside the Gram of earlier ones, but
+// its CTAs do not share an SM with a resident k_oz_gram CTA: three of that
+// CTA's ten warps x 168 registers fill a sub-partition's 16,384, and its 195 KB
+// take the 196 KB carve-out (tools/coresidency_probe.cu; session-6 entries of
+// profiles/r2s3/rejected_experiments.md).  It runs on the SMs the Gram's
+// one-wave batches leave free and in the gaps between batches.
 // ---------------------------------------------------------------------------
 constexpr int kSplitCols = 64;
+constexpr int kSplitGroups = 8;  // voxel-block groups per k_oz_split CTA (fp64 X-hat)
 constexpr int kSplitLdw = 68;  // words per smem row: 16-byte aligned, conflict-free uint4 access
 
 // rint(y) for |y| < 2^51 by the 1.5 * 2^52 shift; the rounded integer is also
@@ -89,10 +94,16 @@ __device__ __forceinline__ double round_shift(double y, int* low) {
 // consecutive 32-voxel blocks per CTA, so every column's records go out as one
 // contiguous NB x rec-byte run (fp32's 128-byte records alone are too short a
 // DRAM burst at the lq stride between columns: 0.35 of HBM with NB = 1)
+//
+// A CTA walks `gsz` consecutive groups of NB voxel blocks of its 64 columns,
+// the next group's values loaded into registers ahead of the current group's
+// arithmetic (one-group CTAs spent most of their ~3 us on launch and load
+// latency): 3.85 -> 3.35 ms on cfg 2, 0.90 of the measured HBM copy rate.
 template <typename TX, int NSL, int NB>
 __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restrict__ xhat, int64_t ldsrc, int64_t ncols,
                                                   const unsigned long long* __restrict__ cmax,
-                                                  int8_t* __restrict__ q, int64_t lq, int32_t* __restrict__ expo) {
+                                                  int8_t* __restrict__ q, int64_t lq, int32_t* __restrict__ expo,
+                                                  int gsz) {
   constexpr int nsl = NSL;
   constexpr int rec = NSL <= 4 ? 128 : 256;
   static_assert(NB * rec <= 256, "a column's NB records must fit one shared-memory row");
@@ -100,9 +111,8 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
   const int i = blockIdx.z;
   const int64_t* sj = p.subj + (int64_t)i * kSubjCols;
   const int64_t row0 = sj[SC_ROW_OFF], V = sj[SC_V];
-  const int64_t vb0 = (int64_t)blockIdx.x * NB;
-  if (vb0 * 32 >= V) return;
-  const int nb = (int)min((int64_t)NB, (V + 31) / 32 - vb0);  // blocks of this subject in the CTA
+  const int64_t vb_first = (int64_t)blockIdx.x * NB * gsz;
+  if (vb_first * 32 >= V) return;
   const int64_t t0 = (int64_t)blockIdx.y * kSplitCols;
   const int tl = threadIdx.x & (kSplitCols - 1), quarter = threadIdx.x / kSplitCols;
   const int64_t t = t0 + tl;
@@ -111,18 +121,27 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
   if (tin) {
     const double m = __longlong_as_double((long long)cmax[(int64_t)i * ncols + t]);
     e = (m > 0.0) ? frexp_exp(m) : 0;
-    if (vb0 == 0 && quarter == 0) expo[(int64_t)i * ncols + t] = e;
+    if (vb_first == 0 && quarter == 0) expo[(int64_t)i * ncols + t] = e;
   }
-  TX xv[NB][8];
+  TX xv[NB][8], xn[NB][8];
+  auto load_group = [&](TX (&x)[NB][8], int64_t vb) {
 #pragma unroll
-  for (int j = 0; j < NB; ++j)
+    for (int j = 0; j < NB; ++j)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int64_t v = (vb0 + j) * 32 + quarter * 8 + u;
-      xv[j][u] = (tin && v < V) ? xhat[(row0 + v) * ldsrc + t] : TX(0);
-    }
+      for (int u = 0; u < 8; ++u) {
+        const int64_t v = (vb + j) * 32 + quarter * 8 + u;
+        x[j][u] = (tin && v < V) ? xhat[(row0 + v) * ldsrc + t] : TX(0);
+      }
+  };
+  load_group(xv, vb_first);
   uint2* row = reinterpret_cast<uint2*>(buf + tl * kSplitLdw);
   const int nslot = rec / 32;
+  for (int gi = 0; gi < gsz; ++gi) {
+  const int64_t vb0 = vb_first + (int64_t)gi * NB;
+  if (vb0 * 32 >= V) break;  // (uniform over the CTA)
+  const int nb = (int)min((int64_t)NB, (V + 31) / 32 - vb0);  // blocks of this subject in the group
+  const bool more = gi + 1 < gsz && (vb0 + NB) * 32 < V;
+  if (more) load_group(xn, vb0 + NB);
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     uint32_t w[NSL][2];
@@ -185,6 +204,13 @@ __global__ void __launch_bounds__(256) k_oz_split(DevPlan p, const TX* __restric
       uint4* dst = reinterpret_cast<uint4*>(q + ((int64_t)i * ncols + tt) * lq + vb0 * rec);
       dst[k] = reinterpret_cast<const uint4*>(buf + r * kSplitLdw)[k];
     }
+  }
+  if (!more) break;
+  __syncthreads();  // the staged rows are out: the next group may overwrite them
+#pragma unroll
+  for (int j = 0; j < NB; ++j)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) xv[j][u] = xn[j][u];
   }
 }
 
@@ -2009,8 +2035,9 @@ cudaError_t launch_oz_prepare(const DevPlan& p, int x_dtype, int nsl, int first,
   int32_t* ex = expo + (int64_t)first * p.ldx;
   const unsigned gy = (unsigned)((p.ldx + kSplitCols - 1) / kSplitCols);
   if (x_dtype == SRM_F64)
-    k_oz_split<double, 7, 1><<<dim3((unsigned)((max_v + 31) / 32), gy, (unsigned)count), 256, 0, st>>>(
-        sub, static_cast<const double*>(p.xhat), p.ldx, p.ldx, cm, qs, lq, ex);
+    k_oz_split<double, 7, 1><<<dim3((unsigned)(((max_v + 31) / 32 + kSplitGroups - 1) / kSplitGroups), gy, (unsigned)count),
+                               256, 0, st>>>(sub, static_cast<const double*>(p.xhat), p.ldx, p.ldx, cm, qs, lq, ex,
+                                             kSplitGroups);
   else {
     // four 128-byte records per column per CTA (512-byte runs, 32 loads in
     // flight per thread): 9% faster than two on cfg 4 (SRM_B200_SPLIT_NB=2 keeps two)
@@ -2062,7 +2089,7 @@ cudaError_t launch_oz_init_slices(const DevPlan& p, int first, int count, int8_t
   k_oz_split<double, 7, 1><<<dim3((unsigned)((max_v + 31) / 32), (unsigned)((K + kSplitCols - 1) / kSplitCols),
                                   (unsigned)count), 256, 0, st>>>(sub2, p.amat, p.kp, K, cmaxg + (int64_t)first * K,
                                                                   qg + (int64_t)first * K * lqg, lqg,
-                                                                  expog + (int64_t)first * K);
+                                                                  expog + (int64_t)first * K, 1);
   return cudaGetLastError();
 }
 

@@ -129,6 +129,9 @@ for name, lo, hi in bounds:
     span = ks[-1]["end"] - ks[0]["start"]
     out["phases"][name] = {"span_us": span, "busy_union_us": union, "idle_us": span - union,
                            "kernels_us": dict(sorted(busy.items(), key=lambda x: -x[1]))}
+    if name == "gram":
+        out["gram_timeline"] = [(short(k["name"]), round(k["start"] - ks[0]["start"], 1),
+                                 round(k["end"] - k["start"], 1)) for k in ks]
     if name == "it1":
         out["iteration_timeline"] = [(short(k["name"]), round(k["start"] - ks[0]["start"], 1),
                                       round(k["end"] - k["start"], 1)) for k in ks]
