@@ -1233,7 +1233,10 @@ int srm_plan_bind(srm_plan* p, void* workspace, int64_t bytes) {
     if (e == cudaSuccess && p->oz_lqg_init) {
       e = make_map_q(&p->tm_gi, region<int8_t>(p, SRM_R_WOUT), p->oz_lqg_init, p->K, p->n_local, 128);
       if (e == cudaSuccess)
-        e = make_map_q(&p->tm_gi64, region<int8_t>(p, SRM_R_WOUT), p->oz_lqg_init, p->K, p->n_local, 64);
+        // (k_oz_nt: the draw's slots of a voxel block slot-major, eight or -- four-slice X-hat,
+        // d-groups 0-3 -- the four it reads)
+        e = make_map_q8(&p->tm_gi64, region<int8_t>(p, SRM_R_WOUT), p->oz_lqg_init, p->K, p->n_local,
+                        p->oz_nsl == 4 ? 4 : 8);
       if (e == cudaSuccess)
         e = launch_oz_tn(p->tm_gi, p->tm_q, nullptr, nullptr, nullptr, p->ldx, p->kp, p->ldo, p->K, nullptr, 0,
                          p->oz_nsl, 0);
@@ -1491,7 +1494,11 @@ int srm_prepare_gram_range(srm_plan* p, int first, int count, void* stream) {
   const int per = p->ldx / 128 > 0 ? (int)(p->items_oz.size() / std::max(p->n_local, 1)) : 1;
   const int ctas = per + 2 * (int)(p->items_oz2.size() / std::max(p->n_local, 1));  // CTAs per subject
   const int batch = std::max(1, 148 / std::max(ctas, 1));
-  if ((p->flags & SRM_FLAG_GRAM_I8) && count > batch) {
+  static const bool batched = [] {  // SRM_B200_GRAM_BATCH=0: slice everything, then one Gram launch (test knob)
+    const char* e = getenv("SRM_B200_GRAM_BATCH");
+    return !(e && e[0] == '0');
+  }();
+  if ((p->flags & SRM_FLAG_GRAM_I8) && count > batch && batched) {
     const Lanes* ln = nullptr;
     int rc = plan_lanes(p, &ln);
     if (rc) return rc;

@@ -141,9 +141,10 @@ cudaError_t launch_oz_tn(const TmaMap& tma, const TmaMap& tmb, const int32_t* ae
 // 64-row box (each CTA stages half of the B rows)
 cudaError_t launch_oz_gram2(const TmaMap& tmq, const TmaMap& tmqb, const OzGramOut& o, const OzItem* items,
                             int n_items, int nsl, cudaStream_t st);
-// the same for kp <= 64, transposed (M = 128 TRs x N = 64 features, one pass):
-// tmg64 = the draw's records with a 64-row box
-cudaError_t launch_oz_nt(const TmaMap& tmx, const TmaMap& tmg64, const int32_t* aexp, const int32_t* bexp,
+// the same for kp <= 64, transposed (M = 128 TRs x N = two slots of 64 features, one
+// pass): tmg8 = the draw's records through make_map_q8 (slot-major boxes of 64 rows;
+// eight slots, or the first four for four-slice X-hat)
+cudaError_t launch_oz_nt(const TmaMap& tmx, const TmaMap& tmg8, const int32_t* aexp, const int32_t* bexp,
                          double* bred, int64_t ldx, int64_t kp, int64_t ldo, int64_t K, const OzItem* items, int n_items,
                          int nslx, cudaStream_t st);
 // X_i^T X_i tiles from the nsl-slice records (nsl = 7 for fp64 X-hat, 4 for

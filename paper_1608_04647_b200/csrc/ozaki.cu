@@ -1072,15 +1072,21 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_nt(const __grid_constant__
           unsigned char* st = smem + slot * kStage;
           tma_load_3d(st, &tmx, vb * recx, it.n0, it.subj, &full[slot]);
           if (NSX > 4) tma_load_3d(st + kOzBox, &tmx, vb * recx + 128, it.n0, it.subj, &full[slot]);
+          // the draw's slots of this voxel block as [slot][64 features][32 B] (SWIZZLE_32B):
+          // slots j, j + 1 form one 128-row K-major operand
           unsigned char* sg = st + (NSX > 4 ? 2 : 1) * kOzBox;
-          tma_load_3d(sg, &tmg, vb * 256, 0, it.subj, &full[slot]);
-          if (kDTop >= 4) tma_load_3d(sg + kBoxG, &tmg, vb * 256 + 128, 0, it.subj, &full[slot]);
+          tma_load_4d(sg, &tmg, 0, 0, vb * 8, it.subj, &full[slot]);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer: seven 64-column d-groups, one pass
-      constexpr uint32_t idesc = idesc_s8(128, 64);
+      // N = 128: B is the slot pair (s2, s2 + 1) of the draw, 64 features each, so one MMA
+      // feeds d-groups sx + s2 and sx + s2 + 1 (adjacent accumulators) -- 16 MMAs per voxel
+      // block instead of 28 at N = 64, which cost the same tensor-pipe time each
+      // (tools/i8_peak.cu); the same integer sums per d-group, so the result is unchanged.
+      // A partial group past kDTop is written and never read.
+      constexpr uint32_t idesc = idesc_s8(128, 128);
       int k = 0;
       for (int c = 0; c < nchunks; ++c) {
         if (c > 0) mbar_wait(&accfree, (c - 1) & 1);
@@ -1092,16 +1098,15 @@ __global__ void __launch_bounds__(kOzThreads, 1) k_oz_nt(const __grid_constant__
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t sa = smem_u32(smem + slot * kStage);
           const uint64_t da0 = umma_desc_sw128(sa);
-          const uint64_t db0 = umma_desc_sw128(sa + (NSX > 4 ? 2 : 1) * kOzBox);
+          const uint64_t db0 = umma_desc_sw32_mn(sa + (NSX > 4 ? 2 : 1) * kOzBox, 16, 256);
           const uint32_t keep = vb == b0 ? 0u : 1u;
+          // sx = 0 first: its pairs touch every d-group read, so they alone start a chunk's sums
 #pragma unroll
-          for (int d = 0; d <= kDTop; ++d) {
-            const int s0 = d - (NSG - 1) > 0 ? d - (NSG - 1) : 0, s1 = d < NSX - 1 ? d : NSX - 1;
+          for (int sx = 0; sx < NSX; ++sx)
 #pragma unroll
-            for (int sx = s0; sx <= s1; ++sx)
-              mma_s8(tmem + 64u * (uint32_t)d, da0 + oz_slice_off_box(sx, kOzBox),
-                     db0 + oz_slice_off_box(d - sx, kBoxG), idesc, sx == s0 ? keep : 1u);
-          }
+            for (int s2 = 0; sx + s2 <= kDTop; s2 += 2)
+              mma_s8(tmem + 64u * (uint32_t)(sx + s2), da0 + oz_slice_off_box(sx, kOzBox),
+                     db0 + (uint64_t)(s2 * (2048 >> 4)), idesc, sx == 0 ? keep : 1u);
           mma_commit(&empty[slot]);
         }
         mma_commit(&accfull);
@@ -2093,7 +2098,7 @@ cudaError_t launch_oz_init_slices(const DevPlan& p, int first, int count, int8_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_oz_nt(const TmaMap& tmx, const TmaMap& tmg64, const int32_t* aexp, const int32_t* bexp,
+cudaError_t launch_oz_nt(const TmaMap& tmx, const TmaMap& tmg8, const int32_t* aexp, const int32_t* bexp,
                          double* bred, int64_t ldx, int64_t kp, int64_t ldo, int64_t K, const OzItem* items, int n_items,
                          int nslx, cudaStream_t st) {
   if (nslx != 7 && nslx != 4) return cudaErrorInvalidValue;
@@ -2110,7 +2115,7 @@ cudaError_t launch_oz_nt(const TmaMap& tmx, const TmaMap& tmg64, const int32_t* 
   if (kp > 64) return cudaErrorInvalidValue;
   OzTnArgs g{aexp, bexp, bred, ldx, kp, ldo, K};
   const CUtensorMap* x = reinterpret_cast<const CUtensorMap*>(tmx.opaque);
-  const CUtensorMap* gm = reinterpret_cast<const CUtensorMap*>(tmg64.opaque);
+  const CUtensorMap* gm = reinterpret_cast<const CUtensorMap*>(tmg8.opaque);
   if (nslx == 7)
     k_oz_nt<7><<<n_items, kOzThreads, bytes, st>>>(*x, *gm, g, items);
   else
