@@ -2,7 +2,7 @@
 # the reference arm, the ncu launch list of the default command, one full capture of the
 # dominant kernel (oz_gram, cfg2 shape), CUPTI timelines, then the GPU test suite and smoke()
 set -x
-O=gpurun_out/final3
+O=gpurun_out/final6
 mkdir -p $O
 for c in cfg2 cfg1 cfg3 cfg4 cfg5; do
   timeout 900 python bench.py --config $c --steps 5 --warmup 3 > $O/bench_$c.json 2> $O/bench_$c.err
