@@ -1365,6 +1365,7 @@ struct RowGemmArgs {
   int first;             // kRowSG: subject of the first tile
   int n_work;            // tiles: kRowSG (subject, 128-TR block, feature half); kRowW (item, feature half)
   int nz, ntb;           // feature halves; kRowSG: 128-TR blocks per subject
+  int zseq;              // kRowW / kRowWX: a CTA takes every feature half of its items, one after the other
 };
 
 // the operands of work tile w: subject, first A row, feature half
@@ -1391,6 +1392,16 @@ __device__ __forceinline__ RowTile row_tile(const RowGemmArgs& g, int w) {
     r.n0 = it.n0;
   }
   return r;
+}
+
+// The j-th work tile of this CTA (>= n_work: none left; increasing in j).
+// zseq: items c, c + grid, ... with their nz feature halves back to back on
+// the same CTA, so the second half's A operand is an L2 hit on this SM's own
+// L2 partition (halves on neighbouring CTAs land on either die: ncu showed
+// 1.7x the A bytes from DRAM at kp = 128)
+__device__ __forceinline__ int row_work(const RowGemmArgs& g, int j) {
+  if (!g.zseq) return (int)blockIdx.x + j * (int)gridDim.x;
+  return ((j / g.nz) * (int)gridDim.x + (int)blockIdx.x) * g.nz + j % g.nz;
 }
 
 // Row GEMM CTAs: warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue
@@ -1471,7 +1482,7 @@ __global__ void __launch_bounds__(RowGemmShape<MODE, NSA, ND>::threads, RowGemmS
   if (warp == 0) {
     if (lane == 0) {
       int kk = 0;
-      for (int w = blockIdx.x; w < g.n_work; w += gridDim.x) {
+      for (int j = 0, w = row_work(g, 0); w < g.n_work; w = row_work(g, ++j)) {
         const RowTile tl = row_tile<MODE>(g, w);
         for (int k = 0; k < nub; ++k, ++kk) {
           const int slot = kk % kSt;
@@ -1506,7 +1517,7 @@ __global__ void __launch_bounds__(RowGemmShape<MODE, NSA, ND>::threads, RowGemmS
       // an N = 64 MMA costs the same tensor-pipe time as N = 128 (tools/i8_peak.cu)
       constexpr uint32_t idesc = idesc_s8(128, 128) | (MODE == kRowW ? (1u << 15) : 0u);  // kRowWX: A K-major
       int kk = 0, li = 0;
-      for (int w = blockIdx.x; w < g.n_work; w += gridDim.x, ++li) {
+      for (int w = row_work(g, 0); w < g.n_work; w = row_work(g, ++li)) {
         if (li > 0) mbar_wait(&accempty, (li - 1) & 1);  // the last tile's accumulators drained
         asm volatile("tcgen05.fence::after_thread_sync;");
         for (int k = 0; k < nub; ++k, ++kk) {
@@ -1543,7 +1554,7 @@ __global__ void __launch_bounds__(RowGemmShape<MODE, NSA, ND>::threads, RowGemmS
     // ---------------- slicers (kRowWX): thread r cuts voxel row r of the tile ----------------
     const int r = (int)threadIdx.x - 320;
     int kk = 0;
-    for (int w = blockIdx.x; w < g.n_work; w += gridDim.x) {
+    for (int j = 0, w = row_work(g, 0); w < g.n_work; w = row_work(g, ++j)) {
       const RowTile tl = row_tile<MODE>(g, w);
       const int32_t* ex = g.aexp + (int64_t)tl.i * ldx;  // X-hat column exponents e_t (k_oz_split_f32's)
       for (int k = 0; k < nub; ++k, ++kk) {
@@ -1607,7 +1618,7 @@ __global__ void __launch_bounds__(RowGemmShape<MODE, NSA, ND>::threads, RowGemmS
     const int fmax_ = MODE == kRowSG ? (int)kp : (int)g.K;
     const int half = MODE == kRowSG ? -1 : 0;  // the 1/2 of B = S G / 2 (R already holds its 1/2)
     int li = 0;
-    for (int w = blockIdx.x; w < g.n_work; w += gridDim.x, ++li) {
+    for (int w = row_work(g, 0); w < g.n_work; w = row_work(g, ++li)) {
       const RowTile tl = row_tile<MODE>(g, w);
       const int f0 = tl.z * 64;
       // kRowSG: B[f][t] of subject i; kRowW: W[row][f]
@@ -1930,7 +1941,13 @@ cudaError_t run_rowgemm(const TmaMap& ta, const TmaMap& tb, RowGemmArgs g, int m
   }
   if (g.n_work <= 0) return cudaSuccess;
   if (g.kp > 128 || g.ldx % 32 != 0) return cudaErrorInvalidValue;
-  const int grid = max_ctas > 0 ? std::min(g.n_work, max_ctas) : g.n_work;
+  // persistent kRowW / kRowWX grids with two feature halves: both halves of an item on one CTA
+  // (SRM_B200_OZW_ZSEQ=0 restores halves on neighbouring CTAs; same tiles, bit-identical W)
+  const char* zenv = getenv("SRM_B200_OZW_ZSEQ");  // (read per launch: the tests toggle it)
+  const bool zseq_on = !(zenv && zenv[0] == '0');
+  g.zseq = (MODE != kRowSG && g.nz > 1 && max_ctas > 0 && zseq_on) ? 1 : 0;
+  const int units = g.zseq ? g.n_work / g.nz : g.n_work;
+  const int grid = max_ctas > 0 ? std::min(units, max_ctas) : g.n_work;
   k_oz_rowgemm<MODE, NSA, ND><<<grid, RowGemmShape<MODE, NSA, ND>::threads, bytes, st>>>(*reinterpret_cast<const CUtensorMap*>(ta.opaque),
                                                                *reinterpret_cast<const CUtensorMap*>(tb.opaque), g);
   return cudaGetLastError();

@@ -994,3 +994,26 @@ def test_fp32_final_w_in_kernel_slicing_bit_identical(srm, monkeypatch, k):
         assert eng[0].gram_i8
     for wa, wb in zip(out[0].W, out[1].W):
         assert np.array_equal(wa, wb)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_final_w_feature_halves_on_one_cta_bit_identical(srm, monkeypatch, dtype):
+    """K = 100 (two 64-feature halves): the final W with both halves of a
+    128-voxel item on one persistent CTA (default; the second half's A operand
+    is an L2 hit) equals the W with the halves on neighbouring CTAs
+    (SRM_B200_OZW_ZSEQ=0) bit for bit -- the same tiles, a different CTA
+    assignment. More items than CTAs (so CTAs loop), ragged V, partial k-block."""
+    from paper_1608_04647_b200.data import recipe_numpy
+
+    xs, _, _ = recipe_numpy(4, 6000, 260, 100, seed=41)
+    xs = [x.astype(dtype) for x in xs]
+    xs[2] = xs[2][:5157]
+    cfg = srm.SrmConfig(k=100, iterations=2, seed=5)
+    out = []
+    for mode in ("1", "0"):
+        monkeypatch.setenv("SRM_B200_OZW_ZSEQ", mode)
+        eng = []
+        out.append(srm.fit(_subjects(srm, xs), cfg, algorithm="gram", engine_out=eng))
+        assert eng[0].gram_i8
+    for wa, wb in zip(out[0].W, out[1].W):
+        assert np.array_equal(wa, wb)
