@@ -19,7 +19,7 @@ the per-iteration error table of each config there as JSON.
 Time guard: the oracle's CPU work dominates (cfg 3 / 4 / 5: ~130 / 220 / 230 s
 on the pool's 16 host cores; the whole ``-m gpu`` suite ~12.5 min against the
 driver's 20-minute limit).  On a box whose host runs slower, a heavy config
-that would not end inside ``SRM_GPU_SUITE_BUDGET_S`` (default 880 s since the
+that would not end inside ``SRM_GPU_SUITE_BUDGET_S`` (default 840 s since the
 process started) runs on its first n subjects instead of failing the whole
 suite by timeout -- every iteration, full V x T, n stated in a warning and in
 the report.  ``SRM_PARITY_FULL=1`` disables the guard.
@@ -56,7 +56,7 @@ def _subject_count(name, n_full):
     """All n_full subjects unless the box is too slow for the suite's time budget (module docstring)."""
     if os.environ.get("SRM_PARITY_FULL") == "1":
         return n_full
-    left = float(os.environ.get("SRM_GPU_SUITE_BUDGET_S", "880")) - _process_seconds()
+    left = float(os.environ.get("SRM_GPU_SUITE_BUDGET_S", "840")) - _process_seconds()
     need = _FULL_SECONDS[name] * _rate[0]
     if need <= left:
         return n_full
